@@ -1,0 +1,397 @@
+#!/usr/bin/env python
+"""Benchmark: DQN learner updates/sec (batch 32) of the B200-native Gorila learner update.
+
+Workload (BASELINE.json configs[1]): one learner per GPU, |A| = 18, batch 32, a 1M-frame
+device replay (synthetic Atari-shaped frames, synth/), RMSProp parameter server sharded over
+the ranks, target sync every 100 PS updates. A step = learner_step + ps_apply_shard +
+sync_target (the whole hot path: sample -> 2 forwards -> TD -> backward -> [reduce-scatter]
+-> RMSProp -> [all-gather] -> replica -> target sync).
+
+python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+Under torchrun (N > 1) every rank runs one learner; rank 0 prints ONE JSON line.
+"""
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "DQN learner updates/sec (batch 32)"
+UNIT = "updates/s"
+
+# algorithmic work per learner update, per sample
+MAC = {"conv1": 3_276_800, "conv2": 2_654_208, "conv3": 1_806_336, "fc4": 1_605_632}
+
+
+def fc5_mac(nA):
+    return 512 * nA
+
+
+def phase_work(phase, B, nA, P, esz):
+    """(bound, algorithmic amount per launch-group, unit) of a profiled phase."""
+    fl = lambda mac: 2.0 * mac * B  # noqa: E731
+    table = {
+        "conv1_fwd": ("tensor", 2 * fl(MAC["conv1"])), "conv2_fwd": ("tensor", 2 * fl(MAC["conv2"])),
+        "conv3_fwd": ("tensor", 2 * fl(MAC["conv3"])), "fc4_fwd": ("tensor", 2 * fl(MAC["fc4"])),
+        "fc4_dgrad": ("tensor", fl(MAC["fc4"])), "fc4_wgrad": ("tensor", fl(MAC["fc4"])),
+        "conv3_dgrad": ("tensor", fl(MAC["conv3"])), "conv3_wgrad": ("tensor", fl(MAC["conv3"])),
+        "conv2_dgrad": ("tensor", fl(MAC["conv2"])), "conv2_wgrad": ("tensor", fl(MAC["conv2"])),
+        "conv1_wgrad": ("tensor", fl(MAC["conv1"])),
+        # sampler: reads 5 frames + meta per sample, writes s and s' (NHWC, esz bytes/element)
+        "sample": ("hbm", B * (5 * 7056 + 6 + 2 * 4 * 7056 * esz)),
+        # centered RMSProp: read theta, m, v, g (16 B) + write theta, m, v (12 B) per parameter
+        "apply": ("hbm", 28.0 * P),
+        # replica: read fp32 theta, write fwd copy + transposed dgrad copies of W2/W3/W4 + fp32 area
+        "pack": ("hbm", 4.0 * P + esz * (P + 32768 + 36864 + 1605632)),
+    }
+    return table.get(phase)
+
+
+def read_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            pk = json.load(f)
+        return {"hbm": float(pk["hbm_gbs"]), "tensor": float(pk["bf16_tflops_sustained"]),
+                "tensor_burst": float(pk["bf16_tflops"]), "src": "measured (MEASURED_PEAKS.json)"}
+    except Exception:
+        return {"hbm": 6650.0, "tensor": 1400.0, "tensor_burst": 1590.0, "src": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.idx = gpu_index
+        self.proc = None
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                         stderr=subprocess.DEVNULL)
+        except FileNotFoundError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc:
+            self.proc.terminate()
+            self.proc.wait()
+
+    def summary(self):
+        self.f.flush()
+        self.f.seek(0)
+        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 5 + i and "Active" in r[5 + i]})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(rows)}
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    return ws, int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0"))
+
+
+def max_over_ranks(x, world):
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([x], dtype=torch.float64, device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(world):
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+
+
+def fill_replay(g, learner, capacity, n_actions, seed, learner_gid, chunk=131072):
+    import torch
+    import synth
+    fr = torch.empty((chunk, 84, 84), dtype=torch.uint8, device="cuda")
+    a = torch.empty(chunk, dtype=torch.uint8, device="cuda")
+    r = torch.empty(chunk, dtype=torch.float32, device="cuda")
+    d = torch.empty(chunk, dtype=torch.uint8, device="cuda")
+    st = torch.cuda.current_stream().cuda_stream
+    t = 0
+    while t < capacity:
+        n = min(chunk, capacity - t)
+        synth.fill_frames_dev(seed, learner_gid, t, n, fr.data_ptr(), st)
+        synth.fill_meta_dev(seed, learner_gid, t, n, n_actions, 0.0, a.data_ptr(), r.data_ptr(), d.data_ptr(), st)
+        g.replay_insert(learner, fr[:n], a[:n], r[:n], d[:n])
+        t += n
+    torch.cuda.synchronize()
+
+
+def cpu_baseline(args, budget_s):
+    """The oracle (as it stands) on the host cores: a bounded sample of the same workload."""
+    import oracle as O
+    import synth
+    nA, B = args.n_actions, args.batch
+    cap = 20_000
+    cfg = O.Config(n_actions=nA, batch=B, capacity=cap, mode="exact", target_period=args.target_period)
+    orc = O.GorilaOracle(cfg, synth.theta0(nA))
+    f = synth.frames(synth.SEED_DATA, 0, 0, cap)
+    a, r, d = synth.meta(synth.SEED_DATA, 0, 0, cap, nA)
+    orc.insert(0, f, a, r, d)
+    orc.round(0)  # warm-up (page-in, OpenMP pool)
+    t0 = time.perf_counter()
+    k = 1
+    while True:
+        orc.round(k)
+        k += 1
+        el = time.perf_counter() - t0
+        if el >= budget_s or k > 200:
+            break
+    n = k - 1
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    return {"value": n / el, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "sample": f"{n} oracle learner updates (nA={nA}, B={B}, fp64, {cores} OpenMP threads) on a "
+                      f"{cap}-frame replay (per-update work does not depend on replay size), {el:.1f} s"}
+
+
+def run_reference(args):
+    world, rank, _ = dist_env()
+    if rank != 0:
+        return
+    import oracle as O
+    import synth
+    nA, B = args.n_actions, args.batch
+    cap = 20_000
+    cfg = O.Config(n_actions=nA, batch=B, capacity=cap, mode="exact", target_period=args.target_period)
+    orc = O.GorilaOracle(cfg, synth.theta0(nA))
+    f = synth.frames(synth.SEED_DATA, 0, 0, cap)
+    a, r, d = synth.meta(synth.SEED_DATA, 0, 0, cap, nA)
+    orc.insert(0, f, a, r, d)
+    t1 = time.perf_counter()
+    orc.round(0)
+    one = time.perf_counter() - t1
+    warm = min(args.warmup, 3)
+    for k in range(1, warm):
+        orc.round(k)
+    budget = 150.0
+    steps = int(max(3, min(args.steps, budget // max(one, 1e-3))))
+    t0 = time.perf_counter()
+    for k in range(steps):
+        orc.round(warm + k)
+    el = time.perf_counter() - t0
+    val = steps / el
+    cores = int(os.environ.get("OMP_NUM_THREADS", os.cpu_count() or 1))
+    sample = (f"{steps} oracle learner updates (of --steps {args.steps}; bounded to ~{int(budget)} s) nA={nA} "
+              f"B={B} fp64 on a {cap}-frame replay")
+    print(json.dumps({"impl": "reference", "metric": METRIC, "value": val, "unit": UNIT, "n_gpus": args.gpus,
+                      "steps": steps, "warmup": warm, "ms_per_step": 1000 * el / steps, "higher_is_better": True,
+                      "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+                      "config": config_dict(args, world),
+                      "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
+                      "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+
+
+def config_dict(args, world):
+    return {"workload": "configs[1]: 1 learner/GPU, |A|=18, batch 32, 1M-frame device replay, target sync every 100",
+            "n_actions": args.n_actions, "batch_per_learner": args.batch, "global_batch": args.batch * world,
+            "replay_frames_per_learner": args.capacity, "target_period": args.target_period,
+            "ps_shards": world, "parallelism": f"dp{world} learners + {world}-way sharded PS (NCCL RS/AG)",
+            "math": args.math, "l2": "inputs larger than L2: 7.06 GB replay per GPU (126 MB L2); the 27 MB "
+                                     "parameter/optimizer state stays L2-resident across steps as in training"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--warmup", type=int, default=10)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--math", default="bf16", choices=["bf16", "fp32"])
+    ap.add_argument("--batch", type=int, default=32)
+    ap.add_argument("--n-actions", type=int, default=18)
+    ap.add_argument("--capacity", type=int, default=1_000_000)
+    ap.add_argument("--target-period", type=int, default=100)
+    ap.add_argument("--cpu-seconds", type=float, default=15.0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--e2e-steps", type=int, default=200)
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+
+    if args.impl == "reference":
+        return run_reference(args)
+
+    import torch
+    world, rank, local_rank = dist_env()
+    torch.cuda.set_device(local_rank)
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    import synth
+    from paper_1507_04296_b200 import Gorila, nccl_unique_id
+    synth.build()
+    uid = None
+    if world > 1:
+        import torch.distributed as dist
+        obj = [nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    stream = torch.cuda.Stream()
+    torch.cuda.set_stream(stream)
+    g = Gorila(n_actions=args.n_actions, batch=args.batch, replay_capacity=args.capacity, n_learners_local=1,
+               learner_id_base=rank, rank=rank, world=world, nccl_unique_id=uid, stream=stream,
+               theta0=synth.theta0(args.n_actions), math=args.math, target_period=args.target_period, history=2)
+    fill_replay(g, 0, args.capacity, args.n_actions, synth.SEED_DATA, rank)
+    ids = np.array([0], np.int32)
+
+    def step(k):
+        g.learner_step_async(ids, k)
+        g.ps_apply_shard(k, want_info=False)
+        g.sync_target(ids, want_info=False)
+
+    k = 0
+    for _ in range(args.warmup):
+        step(k)
+        k += 1
+    stream.synchronize()
+    barrier(world)
+
+    # ---------------- timed region (device time, CUDA events on the launching stream)
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    launches0 = g.kernel_launches()
+    with ClockSampler(local_rank) as clk:
+        stream.synchronize()
+        barrier(world)
+        ev0.record(stream)
+        for _ in range(args.steps):
+            step(k)
+            k += 1
+        ev1.record(stream)
+        stream.synchronize()
+    barrier(world)
+    launches = g.kernel_launches() - launches0
+    ms_local = ev0.elapsed_time(ev1)
+    ms = max_over_ranks(ms_local, world)
+    value = world * args.steps / (ms / 1000.0)
+
+    # ---------------- end to end through the public API with host buffers
+    f1 = torch.empty((1, 84, 84), dtype=torch.uint8).pin_memory()
+    a1 = torch.zeros(1, dtype=torch.uint8).pin_memory()
+    r1 = torch.zeros(1, dtype=torch.float32).pin_memory()
+    d1 = torch.zeros(1, dtype=torch.uint8).pin_memory()
+    hf = synth.frames(synth.SEED_DATA, rank, args.capacity, args.e2e_steps)
+    ha, hr, hd = synth.meta(synth.SEED_DATA, rank, args.capacity, args.e2e_steps, args.n_actions)
+    barrier(world)
+    stream.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    for i in range(args.e2e_steps):
+        f1.numpy()[0] = hf[i]
+        a1.numpy()[0], r1.numpy()[0], d1.numpy()[0] = ha[i], hr[i], hd[i]
+        g.replay_insert(0, f1, a1, r1, d1)           # this step's new experience, pinned host -> device
+        info = g.learner_step([0], k)                 # result (loss, decisions) device -> host
+        g.ps_apply_shard(k, want_info=True)
+        g.sync_target([0], want_info=True)
+        k += 1
+    e1.record(stream)
+    stream.synchronize()
+    e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
+    e2e_value = world * args.e2e_steps / (e2e_ms / 1000.0)
+    _ = info
+
+    # ---------------- per-phase device timing (roofline of the dominant kernel)
+    g.profile_enable(True)
+    prof_steps = min(args.steps, 300)
+    stream.synchronize()
+    for _ in range(prof_steps):
+        step(k)
+        k += 1
+    phases, n_prof = g.profile_read()
+    g.profile_enable(False)
+
+    peaks = read_peaks()
+    P = g.P
+    esz = 2 if args.math == "bf16" else 4
+    total_prof = sum(phases.values())
+    dom = max(phases, key=lambda p: phases[p])
+    per_launch_ms = {p: v / max(n_prof, 1) for p, v in phases.items()}
+
+    def roof(p):
+        w = phase_work(p, args.batch, args.n_actions, P, esz)
+        if w is None:
+            return None
+        bound, amount = w
+        t = per_launch_ms[p] / 1000.0
+        if bound == "tensor":
+            ach = amount / t / 1e12
+            peak = peaks["tensor"] if args.math == "bf16" else peaks["tensor"] / 16  # fp32 SIMT: not tensor
+            unit = "TFLOP/s"
+        else:
+            ach = amount / t / 1e9
+            peak = peaks["hbm"]
+            unit = "GB/s"
+        return {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
+                "algorithmic_per_launch": amount, "ms_per_launch": per_launch_ms[p]}
+
+    dom_roof = roof(dom)
+    if dom_roof is None:  # dominant phase without an algorithmic model: report the biggest modelled one
+        modelled = [p for p in phases if phase_work(p, args.batch, args.n_actions, P, esz)]
+        dom = max(modelled, key=lambda p: phases[p])
+        dom_roof = roof(dom)
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(args.math, {}).get(dom)
+        except Exception:
+            traffic = None
+
+    if rank == 0:
+        clocks = clk.summary()
+        out = {
+            "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "bf16" if args.math == "bf16" else "f32", "data": "synthetic",
+            "frames_per_s": value * args.batch,
+            "config": config_dict(args, world),
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 7056 + 1 + 4 + 1,
+                    "d2h_bytes_per_step": 48 + 24 + 1,
+                    "note": "per step: replay_insert of 1 new transition from pinned host memory, learner_step "
+                            "with its learner info read back, ps_apply_shard with round info, sync_target flag"},
+            "roofline": {"kernel": dom, "bound": dom_roof["bound"], "achieved": dom_roof["achieved"],
+                         "peak": dom_roof["peak"], "unit": dom_roof["unit"], "frac": dom_roof["frac"],
+                         "traffic": traffic, "peak_src": peaks["src"],
+                         "share_of_step": phases[dom] / total_prof if total_prof else None,
+                         "ms_per_launch": dom_roof["ms_per_launch"],
+                         "algorithmic_per_launch": dom_roof["algorithmic_per_launch"]},
+            "phases_ms_per_step": {p: v for p, v in per_launch_ms.items() if v > 0},
+            "phase_rooflines": {p: roof(p) for p in phases if roof(p) is not None},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(args, args.cpu_seconds)
+        print(json.dumps(out))
+    g.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

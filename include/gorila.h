@@ -1,0 +1,223 @@
+/* gorila.h — C-ABI of the B200-native Gorila DQN learner update.
+ *
+ * Paper: Nair et al. 2015, "Massively Parallel Methods for Deep Reinforcement
+ * Learning" (arXiv:1507.04296), /root/reference/PAPER.md. Citations are
+ * PAPER.md line numbers (P:L) with the section / equation / algorithm.
+ *
+ * The library implements Algorithm 1's learner half and the
+ * sharded parameter server for the Nature-DQN Q-network
+ * (§5.1), one process per GPU. All compute runs in the library's own
+ * sm_100a kernels; NCCL (the copy torch loads) carries the gradient
+ * reduce-scatter and the parameter all-gather when world > 1.
+ *
+ * Conventions (all entry points):
+ *  - Ownership: the caller owns the workspace (device memory, e.g. a torch
+ *    tensor of gorila_workspace_bytes()), the stream and every host buffer.
+ *    The context owns sub-allocations of the workspace and its NCCL
+ *    communicator (destroyed by gorila_destroy). No pointer argument is retained
+ *    after a call returns, except config.workspace and config.stream.
+ *  - Asynchrony: every call enqueues work on config.stream and returns without
+ *    synchronising, unless stated. *_info / *_out host buffers are written by
+ *    cudaMemcpyAsync on that stream: valid after the stream synchronises
+ *    (pass pinned memory for a fully asynchronous copy).
+ *  - Collectives: gorila_init (world > 1) and ps_apply_shard are collective —
+ *    every rank calls them in the same order with the same arguments.
+ *  - Errors: every call returns a gorila_status; no C++ exception crosses the
+ *    ABI; gorila_last_error() returns a thread-local message. After
+ *    GORILA_E_CUDA / GORILA_E_NCCL the context is poisoned: only
+ *    gorila_destroy is legal. Outcomes (outlier-rejected, stale, not ready)
+ *    are NOT errors; they are reported in gorila_learner_info.
+ *  - Parameter layout at the boundary ("canonical"): flat float32 vector
+ *    [W1,b1,W2,b2,W3,b3,W4,b4,W5,b5]; conv weights OIHW, FC weights
+ *    [out][in]; fc4's input index = c*49 + y*7 + x (CHW flatten, reading R18).
+ *    P = 1,684,128 + 513*nA (1,693,362 for nA = 18). Internal layouts are private.
+ */
+#ifndef GORILA_H
+#define GORILA_H
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define GORILA_API __attribute__((visibility("default")))
+#else
+#define GORILA_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct gorila_ctx gorila_ctx; /* opaque; one per rank */
+
+typedef enum {
+    GORILA_OK = 0,
+    GORILA_E_INVALID = 1,   /* invalid config or argument */
+    GORILA_E_SHAPE = 2,     /* wrong buffer size / count */
+    GORILA_E_RANGE = 3,     /* learner id or action out of range */
+    GORILA_E_NOT_READY = 4, /* replay below the warm-up size (replay_sample only) */
+    GORILA_E_CUDA = 5,
+    GORILA_E_NCCL = 6,
+    GORILA_E_OOM = 7        /* workspace too small */
+} gorila_status;
+
+typedef enum {
+    GORILA_MATH_FP32 = 0, /* fp32 SIMT check mode: parity 1e-5 vs the exact oracle */
+    GORILA_MATH_BF16 = 2  /* bf16 operands on tcgen05 tensor cores, fp32 accumulate (reading R16) */
+} gorila_math;
+
+typedef enum {
+    GORILA_OPT_RMSPROP = 0, /* centered RMSProp (BASELINE north_star; reading R2) */
+    GORILA_OPT_ADAGRAD = 1  /* the paper's rule, "we used the AdaGrad update rule" */
+} gorila_optimizer;
+
+typedef struct {
+    int32_t n_actions;         /* nA in [1, 32]: "a single output unit for each valid action" */
+    int32_t batch;             /* B in [1, 4096], minibatch per learner (Alg.1) */
+    float gamma;               /* discount, Alg.1 target P:125 */
+    int64_t replay_capacity;   /* C frames per learner ("1 million frames"); >= 2 */
+    int32_t n_learners_local;  /* learners (bundles) hosted by this rank, >= 1 */
+    int32_t learner_id_base;   /* global id of local learner 0 (ids feed the sampler's Philox counter) */
+    int32_t rank, world;       /* this rank; number of ranks = parameter-server shards */
+    const void* nccl_unique_id;/* 128-byte ncclUniqueId broadcast by the caller; NULL iff world == 1 */
+    void* stream;              /* cudaStream_t every call enqueues on (0 = legacy default stream) */
+    void* workspace;           /* device memory, >= gorila_workspace_bytes(cfg), 256-B aligned */
+    uint64_t workspace_bytes;
+    int32_t optimizer;         /* gorila_optimizer */
+    float lr;                  /* learning rate eta (2.5e-4, reading R2) */
+    float rms_rho;             /* RMSProp decay of both averages (0.95) */
+    float rms_eps;             /* RMSProp epsilon inside the sqrt (0.01) */
+    float ada_eps;             /* AdaGrad epsilon outside the sqrt (1e-8) */
+    int64_t target_period;     /* N: theta^- <- theta^+ once V >= last + N (Alg.1) */
+    int64_t max_staleness;     /* discard iff V0 - base > max_staleness; < 0 disables */
+    int32_t outlier_enabled;   /* discard batches with |loss| > mu + k*sigma */
+    int32_t outlier_warmup;    /* batches observed before the filter may reject */
+    float outlier_k;           /* "several standard deviations": k */
+    double outlier_beta;       /* EMA decay of the running mean / variance */
+    int64_t min_replay;        /* learner waits until size-1 >= max(1, min_replay) */
+    uint64_t seed;             /* Philox key of the minibatch sampler */
+    int32_t math;              /* gorila_math */
+    int32_t history;           /* parameter-replica history depth H >= 1: learner_step accepts
+                                  scheduled staleness s < H (deterministic fixed-staleness mode) */
+    const float* theta0;       /* host, canonical layout, P floats: theta^+ = theta = theta^- at init (Alg.1) */
+} gorila_config;
+
+/* Per-learner outcome of one learner_step (Alg.1). */
+typedef struct {
+    float loss;               /* mean delta^2 over the batch (Eq.1; reading R6) */
+    float abs_loss;           /* mean |delta| — the outlier statistic (reading R7) */
+    double mu, var;           /* running stats AFTER this batch (reading R8) */
+    double threshold;         /* mu + k*sigma BEFORE this batch (the decision threshold) */
+    uint64_t base_version;    /* V of the replica the gradient was computed on */
+    uint32_t stats_count;     /* batches observed before this one */
+    uint8_t not_ready;        /* replay below warm-up: no batch, no gradient */
+    uint8_t rejected_outlier; /* discarded by the loss filter (learner side) */
+    uint8_t stale;            /* discarded by the staleness rule (PS side) */
+    uint8_t accepted;         /* contributed to this round's update */
+} gorila_learner_info;
+
+/* Outcome of one ps_apply_shard. */
+typedef struct {
+    uint32_t n_accepted;      /* |Acc|: learner gradients applied this round (all ranks) */
+    uint32_t pad_;
+    uint64_t version_before;  /* V0 */
+    uint64_t version_after;   /* V0 + |Acc| (reading R12) */
+} gorila_round_info;
+
+/* P for nA actions (closed form from P:182). */
+GORILA_API int64_t gorila_param_count(int32_t n_actions);
+/* Device workspace bytes cfg needs (all learners' replay included). */
+GORILA_API uint64_t gorila_workspace_bytes(const gorila_config* cfg);
+/* Validate cfg, carve the workspace, set theta^+ = theta = theta^- = theta0,
+ * m = v = 0, V = 0, last_sync = 0, empty loss stats, empty replays; create the
+ * NCCL communicator when world > 1 (collective). Synchronises the stream. */
+GORILA_API gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out);
+GORILA_API void gorila_destroy(gorila_ctx* ctx);
+GORILA_API const char* gorila_last_error(void);
+
+/* Store steps (o_t, a_t, r_t, d_t) for t = n .. n+count-1 into local learner
+ * `learner`'s frame ring (slot t mod C; Alg.1 P:119 "Store ... in D"; P:140
+ * local replay; reading R14). frames: count*84*84 u8 (row-major 84x84 each,
+ * "84x84" preprocessed luminance); actions u8 (< nA, else E_RANGE is
+ * NOT checked on device data), rewards f32, terminals u8 (d_t = 1 iff s_{t+1}
+ * is terminal, Alg.1). src_on_device != 0: all four are device pointers.
+ * Host pointers are copied before the call returns. */
+GORILA_API gorila_status replay_insert(gorila_ctx* ctx, int32_t learner, int64_t count, const uint8_t* frames,
+                            const uint8_t* actions, const float* rewards, const uint8_t* terminals,
+                            int32_t src_on_device);
+
+/* Draw and gather learner `learner`'s minibatch for `round` exactly as
+ * learner_step does ("sampled uniformly from the replay memory D", §3.3;
+ * Alg.1): tau_i uniform over [n-size, n-2] from Philox4x32-10, then
+ * s_i = stack(tau_i), s'_i = stack(tau_i + 1) (4 frames, oldest first, P:181,
+ * zero-padded across episode ends and evicted slots, reading R15). Outputs
+ * (host pointers, each may be NULL): idx_out int64[B] (absolute step tau_i),
+ * s_out / s2_out u8 [B][4][84][84], a_out u8[B], r_out f32[B], d_out u8[B].
+ * Returns E_NOT_READY (no side effects) if size-1 < max(1, min_replay).
+ * Synchronises the stream (parity / debugging entry point). */
+GORILA_API gorila_status replay_sample(gorila_ctx* ctx, int32_t learner, uint64_t round, int64_t* idx_out,
+                            uint8_t* s_out, uint8_t* s2_out, uint8_t* a_out, float* r_out,
+                            uint8_t* d_out);
+
+/* One learner update for each listed local learner (Alg.1):
+ * theta <- replica of round max(round - s_j, 0) (fixed-staleness schedule
+ * s_j = staleness[j] or 0 if staleness == NULL, s_j < history), sample, online
+ * forward Q(s;theta), target forward Q(s';theta^-_j), y = r or r + gamma max Q(s')
+ * (P:122-126), delta = y - Q(s,a), loss, outlier decision + EMA update,
+ * stale decision V0 - base > max_staleness, backward of Eq.2
+ * with delta clipped to [-1,1] (BASELINE north_star; reading R3) unless discarded,
+ * and accumulation into this rank's gradient buffer. learners: local ids
+ * (ascending, each at most once); n >= 1. info_out: n entries or NULL.
+ * Rounds must be issued in increasing order; one learner_step per round. */
+GORILA_API gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
+                           const int32_t* staleness, gorila_learner_info* info_out);
+
+/* Parameter-server step for `round` ("split disjointly across N_param
+ * machines", "applies the updates that are accumulated from many
+ * learners"; reading R12): reduce-scatter of the gradient buffers onto the
+ * owning shard (NCCL when world > 1), one optimizer step on this rank's shard
+ * with the mean of the accepted gradients (skipped if none), V += |Acc|,
+ * all-gather of the updated theta^+ (Alg.1 P:116/"Update theta from
+ * theta^+"), and the next replica. COLLECTIVE. info_out may be NULL. */
+GORILA_API gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info* info_out);
+
+/* Target sync (Alg.1 P:130 "Every global N steps sync theta^- with theta^+";
+ * P:158-160 N counts PS updates; reading R13): for each listed local learner,
+ * if force or V >= last_j + N then theta^-_j <- theta^+ and last_j <- V. The
+ * predicate is evaluated on the device (no host sync). synced_out: n bytes or NULL. */
+GORILA_API gorila_status sync_target(gorila_ctx* ctx, const int32_t* learners, int32_t n, int32_t force,
+                          uint8_t* synced_out);
+
+/* State access for checkpointing and teacher-forced parity (canonical layout,
+ * host buffers, any may be NULL; synchronises the stream). m / v are the full
+ * optimizer state vectors (world == 1), or zeros outside this rank's shard.
+ * stats: per local learner {mu, var, count(as double), last_sync(as double)}. */
+GORILA_API gorila_status gorila_get_state(gorila_ctx* ctx, float* theta, float* m, float* v, uint64_t* version);
+GORILA_API gorila_status gorila_set_state(gorila_ctx* ctx, const float* theta, const float* m, const float* v,
+                               uint64_t version);
+GORILA_API gorila_status gorila_get_learner_state(gorila_ctx* ctx, int32_t learner, float* theta_minus,
+                                       double* stats4);
+GORILA_API gorila_status gorila_set_learner_state(gorila_ctx* ctx, int32_t learner, const float* theta_minus,
+                                       const double* stats4);
+/* The gradient buffer G (canonical layout, sum over this rank's accepted
+ * learners of the last learner_step, before the reduce-scatter). */
+GORILA_API gorila_status gorila_get_grad(gorila_ctx* ctx, float* g);
+/* Q and Q-hat [B][nA] of the last learner_step of local learner `learner`. */
+GORILA_API gorila_status gorila_get_q(gorila_ctx* ctx, int32_t learner, float* q, float* qhat);
+/* Per-phase device timing (diagnostics for the roofline report). When enabled,
+ * learner_step / ps_apply_shard / sync_target record a CUDA event after each
+ * phase on the stream; gorila_profile_read synchronises, returns the summed
+ * milliseconds per phase (n entries, phase names from gorila_profile_phase_name)
+ * and the number of learner steps covered, and resets the accumulators. */
+GORILA_API gorila_status gorila_profile_enable(gorila_ctx* ctx, int32_t enable);
+GORILA_API gorila_status gorila_profile_read(gorila_ctx* ctx, double* ms, int32_t n, uint64_t* n_steps);
+GORILA_API int32_t gorila_profile_phase_count(void);
+GORILA_API const char* gorila_profile_phase_name(int32_t i);
+/* Writes a fresh 128-byte ncclUniqueId (rank 0 calls it and broadcasts the bytes). */
+GORILA_API gorila_status gorila_nccl_unique_id(void* out128);
+/* Number of kernels this library launched so far (evidence counter). */
+GORILA_API uint64_t gorila_kernel_launches(gorila_ctx* ctx);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

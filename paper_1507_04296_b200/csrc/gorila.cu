@@ -1,0 +1,989 @@
+// gorila.cu — context, workspace, orchestration and the C-ABI (include/gorila.h).
+//
+// One learner update (Alg.1) for local learner j at round k, all on `stream`:
+//   K1 sample -> conv1..fc4 fwd (online + target batched per launch) -> fc5 fwd -> K7 TD +
+//   decisions -> fc5 bwd -> fc4 dgrad/wgrad -> conv3/conv2 dgrad + wgrad -> conv1 wgrad ->
+//   bias grads -> K10 wgrad reduce into G.
+// ps_apply_shard: [NCCL reduce-scatter] -> K11 apply -> [NCCL all-gather] -> replica pack.
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "../../include/gorila.h"
+#include "common.cuh"
+#include "gemm.cuh"
+#include "kernels.cuh"
+#include "layout.cuh"
+
+using namespace gorila;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+gorila_status fail(gorila_status st, const std::string& msg) {
+    g_last_error = msg;
+    return st;
+}
+
+#define CU(expr)                                                                                     \
+    do {                                                                                             \
+        cudaError_t _e = (expr);                                                                     \
+        if (_e != cudaSuccess) {                                                                     \
+            ctx->poisoned = true;                                                                    \
+            return fail(GORILA_E_CUDA, std::string(#expr) + ": " + cudaGetErrorString(_e));          \
+        }                                                                                            \
+    } while (0)
+
+#define NC(expr)                                                                                     \
+    do {                                                                                             \
+        ncclResult_t _r = (expr);                                                                    \
+        if (_r != ncclSuccess) {                                                                     \
+            ctx->poisoned = true;                                                                    \
+            return fail(GORILA_E_NCCL, std::string(#expr) + ": " + ncclGetErrorString(_r));          \
+        }                                                                                            \
+    } while (0)
+
+#define LAUNCHED() (ctx->launches++)
+
+int64_t round_up(int64_t x, int64_t m) { return (x + m - 1) / m * m; }
+
+struct Learner {
+    uint8_t* frames;
+    uint8_t* a;
+    float* r;
+    uint8_t* d;
+    uint64_t* n_dev;
+    int64_t n_host = 0;
+    void* tminus_t;   // target replica (fwd only), element type T
+    float* tminus_f;  // fp32 area
+    LearnerStats* stats;
+    DevLearnerInfo* info;
+    float* Q;
+    float* Qhat;
+    uint8_t* sync_flag;
+};
+
+// carve helper over the caller's workspace (256-B aligned bump allocator; nullptr base = dry run)
+struct Carver {
+    uint8_t* base;
+    uint64_t off = 0;
+    template <typename X>
+    X* take(int64_t count) {
+        off = (uint64_t)round_up((int64_t)off, 256);
+        X* p = base ? reinterpret_cast<X*>(base + off) : nullptr;
+        off += (uint64_t)count * sizeof(X);
+        return p;
+    }
+};
+
+}  // namespace
+
+struct gorila_ctx {
+    gorila_config cfg;
+    cudaStream_t stream;
+    bool poisoned = false;
+    uint64_t launches = 0;
+    int nA, B, L, W, rank;
+    int64_t P, q, per;  // params, real elements per slice, slice stride
+    size_t esz;         // sizeof(T)
+    ReplicaLayout rl_full, rl_fwd;
+    // PS state
+    float* theta;   // [W*per] full theta^+ (sliced)
+    float* m;       // [per] own slice
+    float* v;
+    float* G;       // [W*per] gradient (sliced)
+    uint64_t* V;
+    uint64_t* round_info;  // [3]
+    uint32_t* n_acc_local;
+    // history of replicas (H slots)
+    int H;
+    std::vector<void*> rep_t;
+    std::vector<float*> rep_f;
+    uint64_t* Vhist;
+    // learners
+    std::vector<Learner> learners;
+    // per-step scratch (shared by the local learners)
+    void *s, *s2, *a1, *a2, *a3, *a4, *t1, *t2, *t3, *t4, *g1, *g2, *g3, *g4;
+    uint8_t *sa, *sd;
+    float* sr;
+    int64_t* sidx;
+    float* dQ;
+    float* part_fc4;   // [2][splits][512][B]
+    float* part_w[3];  // conv wgrad partials
+    int split_w[3];
+    int split_fc4;
+    float* tmp_canon;  // [P]
+    float* tmp_int;    // [W*per]
+    ncclComm_t comm = nullptr;
+    // per-phase profiling (gorila_profile_*)
+    bool prof = false;
+    std::vector<cudaEvent_t> ev_pool;
+    size_t ev_used = 0;
+    std::vector<std::pair<int, size_t>> marks;
+    double prof_ms[32] = {};
+    uint64_t prof_steps = 0;
+};
+
+namespace {
+
+enum Phase {
+    PH_SAMPLE, PH_CONV1F, PH_CONV2F, PH_CONV3F, PH_FC4F, PH_FC5F, PH_TD, PH_FC5B, PH_FC4DG, PH_FC4WG,
+    PH_CONV3DG, PH_CONV3WG, PH_CONV2DG, PH_CONV2WG, PH_CONV1WG, PH_BIASG, PH_WGRED, PH_STEP_MISC,
+    PH_RS, PH_APPLY, PH_AG, PH_PACK, PH_SYNC, PH_COUNT
+};
+const char* kPhaseNames[PH_COUNT] = {
+    "sample", "conv1_fwd", "conv2_fwd", "conv3_fwd", "fc4_fwd", "fc5_fwd", "td", "fc5_bwd", "fc4_dgrad",
+    "fc4_wgrad", "conv3_dgrad", "conv3_wgrad", "conv2_dgrad", "conv2_wgrad", "conv1_wgrad", "bias_grad",
+    "wgrad_reduce", "step_misc", "reduce_scatter", "apply", "all_gather", "pack", "target_sync"};
+
+// record "phase ph ends here" (ph < 0: a boundary that starts the next phase)
+void mark(gorila_ctx* ctx, int ph) {
+    if (!ctx->prof) return;
+    if (ctx->ev_used == ctx->ev_pool.size()) {
+        cudaEvent_t e;
+        cudaEventCreate(&e);
+        ctx->ev_pool.push_back(e);
+    }
+    cudaEventRecord(ctx->ev_pool[ctx->ev_used], ctx->stream);
+    ctx->marks.push_back({ph, ctx->ev_used});
+    ctx->ev_used++;
+}
+
+int pick_splits(int64_t chunks_total, int64_t base_ctas, int target_ctas, int max_splits) {
+    int64_t s = std::max<int64_t>(1, std::min<int64_t>(max_splits, (target_ctas + base_ctas - 1) / base_ctas));
+    s = std::min<int64_t>(s, chunks_total);
+    return (int)s;
+}
+
+// ------------------------------------------------------------------ GEMM dispatch
+template <int BN, typename LA, typename LB, typename EP>
+void launch_tc(GemmBatch<LA, LB, EP> gb, int nprob, cudaStream_t st) {
+    const int smem = tc_smem_bytes(BN);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(gemm_tc<BN, LA, LB, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        attr_set = true;
+    }
+    dim3 grid((gb.M + TC_BM - 1) / TC_BM, (gb.N + BN - 1) / BN, nprob * gb.splits);
+    gemm_tc<BN, LA, LB, EP><<<grid, TC_THREADS, smem, st>>>(gb);
+}
+
+template <typename LA, typename LB, typename EP>
+void launch_simt(GemmBatch<LA, LB, EP> gb, int nprob, cudaStream_t st) {
+    dim3 grid((gb.M + SM_BI - 1) / SM_BI, (gb.N + SM_BJ - 1) / SM_BJ, nprob * gb.splits);
+    gemm_simt<LA, LB, EP><<<grid, 256, 0, st>>>(gb);
+}
+
+// C[M][N] = sum_r A(i,r) B(j,r): bf16 -> tcgen05 engine (BN = N tile), fp32 -> SIMT engine.
+// `splits` requested split of the reduction (rounded to whole chunks).
+template <typename T, int BN, typename LA, typename LB, typename EP>
+void gemm(gorila_ctx* ctx, const GemmProb<LA, LB, EP>* probs, int nprob, int M, int N, int R, int splits) {
+    GemmBatch<LA, LB, EP> gb{};
+    for (int i = 0; i < nprob; ++i) gb.prob[i] = probs[i];
+    if (nprob == 1) gb.prob[1] = probs[0];
+    gb.M = M;
+    gb.N = N;
+    gb.R = R;
+    const int chunk = std::is_same<T, float>::value ? SM_BR : TC_BK;
+    const int chunks = std::max(1, (R + chunk - 1) / chunk);
+    splits = std::max(1, std::min(splits, chunks));
+    gb.chunks_per_split = (chunks + splits - 1) / splits;
+    gb.splits = (chunks + gb.chunks_per_split - 1) / gb.chunks_per_split;
+    if constexpr (std::is_same<T, float>::value) {
+        launch_simt(gb, nprob, ctx->stream);
+    } else {
+        launch_tc<BN>(gb, nprob, ctx->stream);
+    }
+    LAUNCHED();
+}
+
+template <typename T>
+T* P_(void* p) {
+    return reinterpret_cast<T*>(p);
+}
+
+// number of effective splits the gemm() call will use (so partial buffers are consistent)
+int eff_splits(bool fp32, int R, int splits) {
+    const int chunk = fp32 ? SM_BR : TC_BK;
+    const int chunks = std::max(1, (R + chunk - 1) / chunk);
+    splits = std::max(1, std::min(splits, chunks));
+    const int cps = (chunks + splits - 1) / splits;
+    return (chunks + cps - 1) / cps;
+}
+
+// the fc4 forward / dgrad N tile (= batch columns)
+#define DISPATCH_BN_BATCH(B, CALL) \
+    do {                           \
+        if ((B) <= 32) { CALL(32); } else if ((B) <= 64) { CALL(64); } else if ((B) <= 128) { CALL(128); } else { CALL(256); } \
+    } while (0)
+
+// ------------------------------------------------------------------ one learner update
+template <typename T>
+gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
+    const gorila_config& cfg = ctx->cfg;
+    Learner& Lr = ctx->learners[j];
+    const int B = ctx->B, nA = ctx->nA;
+    const bool fp32 = std::is_same<T, float>::value;
+    cudaStream_t st = ctx->stream;
+    const uint64_t k_src = round >= (uint64_t)s_j ? round - (uint64_t)s_j : 0;
+    const int slot = (int)(k_src % (uint64_t)ctx->H);
+    const T* rt = P_<T>(ctx->rep_t[slot]);
+    const float* rf = ctx->rep_f[slot];
+    const T* tt = P_<T>(Lr.tminus_t);
+    const float* tf = Lr.tminus_f;
+    const ReplicaLayout& RL = ctx->rl_full;
+    const ReplicaLayout& RT = ctx->rl_fwd;
+
+    T *s = P_<T>(ctx->s), *s2 = P_<T>(ctx->s2);
+    T *a1 = P_<T>(ctx->a1), *a2 = P_<T>(ctx->a2), *a3 = P_<T>(ctx->a3), *a4 = P_<T>(ctx->a4);
+    T *t1 = P_<T>(ctx->t1), *t2 = P_<T>(ctx->t2), *t3 = P_<T>(ctx->t3), *t4 = P_<T>(ctx->t4);
+    T *g1 = P_<T>(ctx->g1), *g2 = P_<T>(ctx->g2), *g3 = P_<T>(ctx->g3), *g4 = P_<T>(ctx->g4);
+
+    // K1: sample + gather + stack (Alg.1)
+    {
+        dim3 grid((FRAME_BYTES / 16 + 255) / 256, B);
+        uint2 key = make_uint2((uint32_t)cfg.seed, (uint32_t)(cfg.seed >> 32));
+        k_sample<T><<<grid, 256, 0, st>>>(Lr.frames, Lr.a, Lr.r, Lr.d, cfg.replay_capacity, Lr.n_dev, key,
+                                          (uint32_t)(cfg.learner_id_base + j), round, B, s, s2, ctx->sa, ctx->sr,
+                                          ctx->sd, ctx->sidx);
+        LAUNCHED();
+    }
+    mark(ctx, PH_SAMPLE);
+    const float in_scale = 1.0f / 255.0f;  // reading R17 (fp32 constant, folded into conv1's epilogue)
+    // conv1 fwd (online on s with theta, target on s' with theta^-)
+    {
+        using LA = LdConvIn<T>; using LB = LdRows<T>; using EP = EpAct<T>;
+        const int M = B * H1 * H1;
+        GemmProb<LA, LB, EP> pr[2] = {
+            {{s, IMG, IMG, NSTACK, C1_K, C1_S, H1, H1, M, K1}, {rt + RL.w1, K1, C1_OUT, K1},
+             {a1, C1_OUT, rf + RL.b1, in_scale, M, C1_OUT, 1}},
+            {{s2, IMG, IMG, NSTACK, C1_K, C1_S, H1, H1, M, K1}, {tt + RT.w1, K1, C1_OUT, K1},
+             {t1, C1_OUT, tf + RT.b1, in_scale, M, C1_OUT, 1}}};
+        gemm<T, 32>(ctx, pr, 2, M, C1_OUT, K1, 1);
+    }
+    mark(ctx, PH_CONV1F);
+    // conv2 fwd
+    {
+        using LA = LdConvIn<T>; using LB = LdRows<T>; using EP = EpAct<T>;
+        const int M = B * H2 * H2;
+        GemmProb<LA, LB, EP> pr[2] = {
+            {{a1, H1, H1, C1_OUT, C2_K, C2_S, H2, H2, M, K2}, {rt + RL.w2, K2, C2_OUT, K2},
+             {a2, C2_OUT, rf + RL.b2, 1.f, M, C2_OUT, 1}},
+            {{t1, H1, H1, C1_OUT, C2_K, C2_S, H2, H2, M, K2}, {tt + RT.w2, K2, C2_OUT, K2},
+             {t2, C2_OUT, tf + RT.b2, 1.f, M, C2_OUT, 1}}};
+        gemm<T, 64>(ctx, pr, 2, M, C2_OUT, K2, 1);
+    }
+    mark(ctx, PH_CONV2F);
+    // conv3 fwd
+    {
+        using LA = LdConvIn<T>; using LB = LdRows<T>; using EP = EpAct<T>;
+        const int M = B * H3 * H3;
+        GemmProb<LA, LB, EP> pr[2] = {
+            {{a2, H2, H2, C2_OUT, C3_K, C3_S, H3, H3, M, K3}, {rt + RL.w3, K3, C3_OUT, K3},
+             {a3, C3_OUT, rf + RL.b3, 1.f, M, C3_OUT, 1}},
+            {{t2, H2, H2, C2_OUT, C3_K, C3_S, H3, H3, M, K3}, {tt + RT.w3, K3, C3_OUT, K3},
+             {t3, C3_OUT, tf + RT.b3, 1.f, M, C3_OUT, 1}}};
+        gemm<T, 64>(ctx, pr, 2, M, C3_OUT, K3, 1);
+    }
+    mark(ctx, PH_CONV3F);
+    // fc4 fwd, swap-AB + split-K: partial[z][s][n][b] = sum_k W4[n][k] a3[b][k]; finalize bias + ReLU
+    {
+        using LA = LdRows<T>; using LB = LdRows<T>; using EP = EpStore;
+        const int S = ctx->split_fc4;
+        const int64_t pstride = (int64_t)S * FC4_OUT * B;
+        GemmProb<LA, LB, EP> pr[2] = {
+            {{rt + RL.w4, FC4_IN, FC4_OUT, FC4_IN}, {a3, FC4_IN, B, FC4_IN},
+             {ctx->part_fc4, B, (int64_t)FC4_OUT * B, FC4_OUT, B}},
+            {{tt + RT.w4, FC4_IN, FC4_OUT, FC4_IN}, {t3, FC4_IN, B, FC4_IN},
+             {ctx->part_fc4 + pstride, B, (int64_t)FC4_OUT * B, FC4_OUT, B}}};
+#define FC4F(BN_) gemm<T, BN_>(ctx, pr, 2, FC4_OUT, B, FC4_IN, S)
+        DISPATCH_BN_BATCH(B, FC4F);
+#undef FC4F
+        dim3 grid((B * FC4_OUT + 255) / 256, 2);
+        k_fc4_finalize<T><<<grid, 256, 0, st>>>(ctx->part_fc4, S, pstride, B, rf + RL.b4, tf + RT.b4, a4, t4);
+        LAUNCHED();
+    }
+    mark(ctx, PH_FC4F);
+    // fc5 fwd (both nets)
+    k_fc5_fwd<T><<<dim3(B, 2), 256, 0, st>>>(a4, t4, rf + RL.w5, tf + RT.w5, rf + RL.b5, tf + RT.b5, Lr.Q, Lr.Qhat, nA);
+    LAUNCHED();
+    mark(ctx, PH_FC5F);
+    // K7: TD target, clipped error, loss, outlier + stale decisions
+    {
+        TdParams p{};
+        p.Q = Lr.Q; p.Qhat = Lr.Qhat; p.a = ctx->sa; p.r = ctx->sr; p.d = ctx->sd; p.dQ = ctx->dQ;
+        p.B = B; p.nA = nA; p.gamma = cfg.gamma; p.stats = Lr.stats; p.info = Lr.info; p.V = ctx->V;
+        p.base_V = ctx->Vhist + slot; p.n_acc_local = ctx->n_acc_local; p.max_staleness = cfg.max_staleness;
+        p.outlier_enabled = cfg.outlier_enabled; p.outlier_warmup = cfg.outlier_warmup;
+        p.outlier_k = cfg.outlier_k; p.outlier_beta = cfg.outlier_beta;
+        k_td<<<1, 256, 0, st>>>(p);
+        LAUNCHED();
+    }
+    mark(ctx, PH_TD);
+    // fc5 bwd: dW5, db5 into G; g4 = mask(dQ W5)
+    k_fc5_bwd<T><<<148, 256, 0, st>>>(ctx->dQ, a4, rf + RL.w5, B, nA, ctx->G, ctx->q, ctx->per, g4);
+    LAUNCHED();
+    mark(ctx, PH_FC5B);
+    // fc4 dgrad (i = k, j = b, red = n): g3[b][k] = mask(sum_n W4[n][k] g4[b][n])
+    {
+        using LA = LdRows<T>; using LB = LdRows<T>; using EP = EpMaskT<T>;
+        GemmProb<LA, LB, EP> pr[1] = {{{rt + RL.w4t, FC4_OUT, FC4_IN, FC4_OUT}, {g4, FC4_OUT, B, FC4_OUT},
+                                       {g3, a3, FC4_IN, FC4_IN, B}}};
+#define FC4D(BN_) gemm<T, BN_>(ctx, pr, 1, FC4_IN, B, FC4_OUT, 1)
+        DISPATCH_BN_BATCH(B, FC4D);
+#undef FC4D
+    }
+    mark(ctx, PH_FC4DG);
+    // fc4 wgrad (i = k, j = n, red = b): G[W4][n][k] += sum_b a3[b][k] g4[b][n]
+    {
+        using LA = LdRowsT<T>; using LB = LdRowsT<T>; using EP = EpAddW4;
+        GemmProb<LA, LB, EP> pr[1] = {{{a3, FC4_IN, FC4_IN, B}, {g4, FC4_OUT, FC4_OUT, B},
+                                       {ctx->G, ctx->q, ctx->per, FC4_IN, FC4_OUT}}};
+        gemm<T, 256>(ctx, pr, 1, FC4_IN, FC4_OUT, B, 1);
+    }
+    mark(ctx, PH_FC4WG);
+    // conv3 dgrad: g2 = mask(conv3^T(g3))
+    {
+        using LA = LdDgrad<T>; using LB = LdRows<T>; using EP = EpMask<T>;
+        const int M = B * H2 * H2;
+        GemmProb<LA, LB, EP> pr[1] = {{{g3, H2, H2, C3_OUT, C3_K, C3_S, H3, H3, M, K3},
+                                       {rt + RL.w3d, K3, C2_OUT, K3}, {g2, a2, C2_OUT, M, C2_OUT}}};
+        gemm<T, 64>(ctx, pr, 1, M, C2_OUT, K3, 1);
+    }
+    mark(ctx, PH_CONV3DG);
+    // conv3 wgrad (i = r, j = o, red = m): partial[s][o][r]
+    {
+        using LA = LdConvInT<T>; using LB = LdRowsT<T>; using EP = EpStoreT;
+        const int Mred = B * H3 * H3;
+        GemmProb<LA, LB, EP> pr[1] = {{{{a2, H2, H2, C2_OUT, C3_K, C3_S, H3, H3, Mred, K3}},
+                                       {g3, C3_OUT, C3_OUT, Mred},
+                                       {ctx->part_w[2], K3, (int64_t)C3_OUT * K3, 1.f, K3, C3_OUT}}};
+        gemm<T, 64>(ctx, pr, 1, K3, C3_OUT, Mred, ctx->split_w[2]);
+    }
+    mark(ctx, PH_CONV3WG);
+    // conv2 dgrad: g1 = mask(conv2^T(g2))
+    {
+        using LA = LdDgrad<T>; using LB = LdRows<T>; using EP = EpMask<T>;
+        const int M = B * H1 * H1;
+        GemmProb<LA, LB, EP> pr[1] = {{{g2, H1, H1, C2_OUT, C2_K, C2_S, H2, H2, M, C2_K * C2_K * C2_OUT},
+                                       {rt + RL.w2d, K2 * 2, C1_OUT, K2 * 2}, {g1, a1, C1_OUT, M, C1_OUT}}};
+        gemm<T, 32>(ctx, pr, 1, M, C1_OUT, C2_K * C2_K * C2_OUT, 1);
+    }
+    mark(ctx, PH_CONV2DG);
+    // conv2 wgrad
+    {
+        using LA = LdConvInT<T>; using LB = LdRowsT<T>; using EP = EpStoreT;
+        const int Mred = B * H2 * H2;
+        GemmProb<LA, LB, EP> pr[1] = {{{{a1, H1, H1, C1_OUT, C2_K, C2_S, H2, H2, Mred, K2}},
+                                       {g2, C2_OUT, C2_OUT, Mred},
+                                       {ctx->part_w[1], K2, (int64_t)C2_OUT * K2, 1.f, K2, C2_OUT}}};
+        gemm<T, 64>(ctx, pr, 1, K2, C2_OUT, Mred, ctx->split_w[1]);
+    }
+    mark(ctx, PH_CONV2WG);
+    // conv1 wgrad (input scale 1/255 folded into the store)
+    {
+        using LA = LdConvInT<T>; using LB = LdRowsT<T>; using EP = EpStoreT;
+        const int Mred = B * H1 * H1;
+        GemmProb<LA, LB, EP> pr[1] = {{{{s, IMG, IMG, NSTACK, C1_K, C1_S, H1, H1, Mred, K1}},
+                                       {g1, C1_OUT, C1_OUT, Mred},
+                                       {ctx->part_w[0], K1, (int64_t)C1_OUT * K1, in_scale, K1, C1_OUT}}};
+        gemm<T, 32>(ctx, pr, 1, K1, C1_OUT, Mred, ctx->split_w[0]);
+    }
+    mark(ctx, PH_CONV1WG);
+    // bias gradients b1..b4
+    k_bias_grad<T><<<C1_OUT + C2_OUT + C3_OUT + FC4_OUT, 256, 0, st>>>(g1, g2, g3, g4, B, ctx->G, ctx->q, ctx->per);
+    LAUNCHED();
+    mark(ctx, PH_BIASG);
+    // K10: fixed-order reduction of the conv wgrad partials into G
+    {
+        WgradReduceParams p{};
+        p.part[0] = ctx->part_w[0]; p.part[1] = ctx->part_w[1]; p.part[2] = ctx->part_w[2];
+        p.splits[0] = eff_splits(fp32, B * H1 * H1, ctx->split_w[0]);
+        p.splits[1] = eff_splits(fp32, B * H2 * H2, ctx->split_w[1]);
+        p.splits[2] = eff_splits(fp32, B * H3 * H3, ctx->split_w[2]);
+        p.count[0] = (int64_t)C1_OUT * K1; p.count[1] = (int64_t)C2_OUT * K2; p.count[2] = (int64_t)C3_OUT * K3;
+        p.off[0] = OFF_W1; p.off[1] = OFF_W2; p.off[2] = OFF_W3;
+        k_wgrad_reduce<<<148 * 2, 256, 0, st>>>(p, ctx->G, ctx->q, ctx->per);
+        LAUNCHED();
+    }
+    mark(ctx, PH_WGRED);
+    CU(cudaGetLastError());
+    return GORILA_OK;
+}
+
+template <typename T>
+gorila_status pack_replica(gorila_ctx* ctx, const float* theta_sliced, void* rt, float* rf, bool with_dgrad,
+                           const uint8_t* pred, uint64_t* vhist_dst) {
+    k_pack<T><<<148 * 4, 256, 0, ctx->stream>>>(theta_sliced, ctx->q, ctx->per, ctx->nA, P_<T>(rt), rf,
+                                                with_dgrad ? 1 : 0, pred, vhist_dst, ctx->V);
+    ctx->launches++;
+    CU(cudaGetLastError());
+    return GORILA_OK;
+}
+
+gorila_status pack_any(gorila_ctx* ctx, const float* theta_sliced, void* rt, float* rf, bool with_dgrad,
+                       const uint8_t* pred, uint64_t* vhist_dst) {
+    if (ctx->cfg.math == GORILA_MATH_FP32) return pack_replica<float>(ctx, theta_sliced, rt, rf, with_dgrad, pred, vhist_dst);
+    return pack_replica<__nv_bfloat16>(ctx, theta_sliced, rt, rf, with_dgrad, pred, vhist_dst);
+}
+
+uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) {
+    // computes the carve; if ctx != nullptr and base != nullptr fills the pointers
+    const int nA = cfg->n_actions, B = cfg->batch, L = cfg->n_learners_local, W = cfg->world;
+    const int64_t P = param_count(nA);
+    const int64_t q = round_up((P + W - 1) / W, 64), per = q + 64;
+    const size_t esz = cfg->math == GORILA_MATH_FP32 ? 4 : 2;
+    const ReplicaLayout rl_full = replica_layout(nA, true), rl_fwd = replica_layout(nA, false);
+    const int H = std::max(1, cfg->history);
+    const bool fp32 = cfg->math == GORILA_MATH_FP32;
+    Carver c{base};
+    float* theta = c.take<float>(W * per);
+    float* m = c.take<float>(per);
+    float* v = c.take<float>(per);
+    float* G = c.take<float>(W * per);
+    uint64_t* V = c.take<uint64_t>(4);
+    uint64_t* rinfo = c.take<uint64_t>(4);
+    uint32_t* nacc = c.take<uint32_t>(4);
+    uint64_t* Vhist = c.take<uint64_t>(H);
+    std::vector<void*> rep_t(H);
+    std::vector<float*> rep_f(H);
+    for (int h = 0; h < H; ++h) {
+        rep_t[h] = c.take<uint8_t>(rl_full.n_t * esz);
+        rep_f[h] = c.take<float>(rl_full.n_f);
+    }
+    std::vector<Learner> lrs(L);
+    for (int j = 0; j < L; ++j) {
+        Learner& l = lrs[j];
+        l.frames = c.take<uint8_t>(cfg->replay_capacity * FRAME_BYTES);
+        l.a = c.take<uint8_t>(cfg->replay_capacity);
+        l.r = c.take<float>(cfg->replay_capacity);
+        l.d = c.take<uint8_t>(cfg->replay_capacity);
+        l.n_dev = c.take<uint64_t>(1);
+        l.tminus_t = c.take<uint8_t>(rl_fwd.n_t * esz);
+        l.tminus_f = c.take<float>(rl_fwd.n_f);
+        l.stats = c.take<LearnerStats>(1);
+        l.info = c.take<DevLearnerInfo>(1);
+        l.Q = c.take<float>((int64_t)B * nA);
+        l.Qhat = c.take<float>((int64_t)B * nA);
+        l.sync_flag = c.take<uint8_t>(1);
+    }
+    const int64_t Bs = B;
+    void* s = c.take<uint8_t>(Bs * FRAME_BYTES * NSTACK * esz);
+    void* s2 = c.take<uint8_t>(Bs * FRAME_BYTES * NSTACK * esz);
+    void* a1 = c.take<uint8_t>(Bs * A1 * esz);
+    void* a2 = c.take<uint8_t>(Bs * A2 * esz);
+    void* a3 = c.take<uint8_t>(Bs * A3 * esz);
+    void* a4 = c.take<uint8_t>(Bs * A4 * esz);
+    void* t1 = c.take<uint8_t>(Bs * A1 * esz);
+    void* t2 = c.take<uint8_t>(Bs * A2 * esz);
+    void* t3 = c.take<uint8_t>(Bs * A3 * esz);
+    void* t4 = c.take<uint8_t>(Bs * A4 * esz);
+    void* g1 = c.take<uint8_t>(Bs * A1 * esz);
+    void* g2 = c.take<uint8_t>(Bs * A2 * esz);
+    void* g3 = c.take<uint8_t>(Bs * A3 * esz);
+    void* g4 = c.take<uint8_t>(Bs * A4 * esz);
+    uint8_t* sa = c.take<uint8_t>(Bs);
+    uint8_t* sd = c.take<uint8_t>(Bs);
+    float* sr = c.take<float>(Bs);
+    int64_t* sidx = c.take<int64_t>(Bs);
+    float* dQ = c.take<float>(Bs * nA);
+    // split choices (reduction chunks of 64 for tc, 16 for simt)
+    const int chunk = fp32 ? SM_BR : TC_BK;
+    const int split_fc4 =
+        fp32 ? 1 : eff_splits(false, FC4_IN, pick_splits((FC4_IN + chunk - 1) / chunk, 4 * ((B + 255) / 256), 64, 16));
+    float* part_fc4 = c.take<float>((int64_t)2 * split_fc4 * FC4_OUT * B);
+    int split_w[3];
+    const int Mred[3] = {B * H1 * H1, B * H2 * H2, B * H3 * H3};
+    const int64_t wcount[3] = {(int64_t)C1_OUT * K1, (int64_t)C2_OUT * K2, (int64_t)C3_OUT * K3};
+    const int tiles[3] = {fp32 ? 4 * 1 : 2, fp32 ? 8 : 4, fp32 ? 9 : 5};
+    float* part_w[3];
+    for (int l = 0; l < 3; ++l) {
+        int want = pick_splits((Mred[l] + chunk - 1) / chunk, tiles[l], 148, 128);
+        split_w[l] = eff_splits(fp32, Mred[l], want);
+        part_w[l] = c.take<float>((int64_t)split_w[l] * wcount[l]);
+    }
+    float* tmp_canon = c.take<float>(P);
+    float* tmp_int = c.take<float>(W * per);
+    if (ctx) {
+        ctx->nA = nA; ctx->B = B; ctx->L = L; ctx->W = W; ctx->P = P; ctx->q = q; ctx->per = per; ctx->esz = esz;
+        ctx->rl_full = rl_full; ctx->rl_fwd = rl_fwd; ctx->H = H;
+        ctx->theta = theta; ctx->m = m; ctx->v = v; ctx->G = G; ctx->V = V; ctx->round_info = rinfo;
+        ctx->n_acc_local = nacc; ctx->Vhist = Vhist; ctx->rep_t = rep_t; ctx->rep_f = rep_f; ctx->learners = lrs;
+        ctx->s = s; ctx->s2 = s2; ctx->a1 = a1; ctx->a2 = a2; ctx->a3 = a3; ctx->a4 = a4;
+        ctx->t1 = t1; ctx->t2 = t2; ctx->t3 = t3; ctx->t4 = t4;
+        ctx->g1 = g1; ctx->g2 = g2; ctx->g3 = g3; ctx->g4 = g4;
+        ctx->sa = sa; ctx->sd = sd; ctx->sr = sr; ctx->sidx = sidx; ctx->dQ = dQ;
+        ctx->part_fc4 = part_fc4; ctx->split_fc4 = split_fc4;
+        for (int l = 0; l < 3; ++l) { ctx->part_w[l] = part_w[l]; ctx->split_w[l] = split_w[l]; }
+        ctx->tmp_canon = tmp_canon; ctx->tmp_int = tmp_int;
+    }
+    return c.off + 256;
+}
+
+gorila_status check_learner(gorila_ctx* ctx, int32_t j) {
+    if (!ctx) return fail(GORILA_E_INVALID, "null context");
+    if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned by an earlier CUDA/NCCL error");
+    if (j < 0 || j >= ctx->L) return fail(GORILA_E_RANGE, "learner id out of range");
+    return GORILA_OK;
+}
+
+}  // namespace
+
+// ==================================================================== C-ABI
+extern "C" {
+
+int64_t gorila_param_count(int32_t n_actions) { return param_count(n_actions); }
+
+const char* gorila_last_error(void) { return g_last_error.c_str(); }
+
+uint64_t gorila_workspace_bytes(const gorila_config* cfg) {
+    if (!cfg) return 0;
+    return layout_bytes(cfg, nullptr, nullptr);
+}
+
+uint64_t gorila_kernel_launches(gorila_ctx* ctx) { return ctx ? ctx->launches : 0; }
+
+int32_t gorila_profile_phase_count(void) { return PH_COUNT; }
+
+const char* gorila_profile_phase_name(int32_t i) { return (i >= 0 && i < PH_COUNT) ? kPhaseNames[i] : ""; }
+
+gorila_status gorila_profile_enable(gorila_ctx* ctx, int32_t enable) {
+    if (!ctx) return fail(GORILA_E_INVALID, "null context");
+    ctx->prof = enable != 0;
+    return GORILA_OK;
+}
+
+gorila_status gorila_profile_read(gorila_ctx* ctx, double* ms, int32_t n, uint64_t* n_steps) {
+    if (!ctx) return fail(GORILA_E_INVALID, "null context");
+    CU(cudaStreamSynchronize(ctx->stream));
+    for (size_t i = 1; i < ctx->marks.size(); ++i) {
+        const int ph = ctx->marks[i].first;
+        if (ph < 0) continue;
+        float t = 0.f;
+        CU(cudaEventElapsedTime(&t, ctx->ev_pool[ctx->marks[i - 1].second], ctx->ev_pool[ctx->marks[i].second]));
+        ctx->prof_ms[ph] += t;
+    }
+    ctx->marks.clear();
+    ctx->ev_used = 0;
+    for (int i = 0; i < n && i < PH_COUNT; ++i) ms[i] = ctx->prof_ms[i];
+    if (n_steps) *n_steps = ctx->prof_steps;
+    for (double& x : ctx->prof_ms) x = 0.0;
+    ctx->prof_steps = 0;
+    return GORILA_OK;
+}
+
+gorila_status gorila_nccl_unique_id(void* out128) {
+    if (!out128) return fail(GORILA_E_INVALID, "null argument");
+    ncclUniqueId id;
+    ncclResult_t r = ncclGetUniqueId(&id);
+    if (r != ncclSuccess) return fail(GORILA_E_NCCL, ncclGetErrorString(r));
+    memcpy(out128, &id, sizeof(id));
+    return GORILA_OK;
+}
+
+gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
+    if (!cfg || !out) return fail(GORILA_E_INVALID, "null argument");
+    *out = nullptr;
+    if (cfg->n_actions < 1 || cfg->n_actions > 32) return fail(GORILA_E_INVALID, "n_actions must be in [1, 32]");
+    if (cfg->batch < 1 || cfg->batch > 4096) return fail(GORILA_E_INVALID, "batch must be in [1, 4096]");
+    if (cfg->replay_capacity < 2) return fail(GORILA_E_INVALID, "replay_capacity must be >= 2");
+    if (cfg->n_learners_local < 1) return fail(GORILA_E_INVALID, "n_learners_local must be >= 1");
+    if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return fail(GORILA_E_INVALID, "bad rank/world");
+    if (cfg->world > 1 && !cfg->nccl_unique_id) return fail(GORILA_E_INVALID, "world > 1 needs nccl_unique_id");
+    if (cfg->math != GORILA_MATH_FP32 && cfg->math != GORILA_MATH_BF16) return fail(GORILA_E_INVALID, "bad math");
+    if (cfg->optimizer != GORILA_OPT_RMSPROP && cfg->optimizer != GORILA_OPT_ADAGRAD)
+        return fail(GORILA_E_INVALID, "bad optimizer");
+    if (cfg->history < 1 || cfg->history > 64) return fail(GORILA_E_INVALID, "history must be in [1, 64]");
+    if (cfg->target_period < 1) return fail(GORILA_E_INVALID, "target_period must be >= 1");
+    if (!cfg->theta0) return fail(GORILA_E_INVALID, "theta0 is required");
+    if (!cfg->workspace) return fail(GORILA_E_INVALID, "workspace is required");
+    if (((uintptr_t)cfg->workspace) % 256) return fail(GORILA_E_INVALID, "workspace must be 256-byte aligned");
+    const uint64_t need = layout_bytes(cfg, nullptr, nullptr);
+    if (cfg->workspace_bytes < need) return fail(GORILA_E_OOM, "workspace too small: need " + std::to_string(need));
+
+    gorila_ctx* ctx = new gorila_ctx();
+    ctx->cfg = *cfg;
+    ctx->cfg.theta0 = nullptr;
+    ctx->cfg.nccl_unique_id = nullptr;
+    ctx->stream = (cudaStream_t)cfg->stream;
+    ctx->rank = cfg->rank;
+    layout_bytes(cfg, ctx, (uint8_t*)cfg->workspace);
+    cudaStream_t st = ctx->stream;
+    // zero the PS state, gradient buffer, counters, learner state
+    CU(cudaMemsetAsync(ctx->theta, 0, sizeof(float) * ctx->W * ctx->per, st));
+    CU(cudaMemsetAsync(ctx->m, 0, sizeof(float) * ctx->per, st));
+    CU(cudaMemsetAsync(ctx->v, 0, sizeof(float) * ctx->per, st));
+    CU(cudaMemsetAsync(ctx->G, 0, sizeof(float) * ctx->W * ctx->per, st));
+    CU(cudaMemsetAsync(ctx->V, 0, sizeof(uint64_t) * 4, st));
+    CU(cudaMemsetAsync(ctx->n_acc_local, 0, sizeof(uint32_t) * 4, st));
+    CU(cudaMemsetAsync(ctx->Vhist, 0, sizeof(uint64_t) * ctx->H, st));
+    for (auto& l : ctx->learners) {
+        CU(cudaMemsetAsync(l.n_dev, 0, sizeof(uint64_t), st));
+        CU(cudaMemsetAsync(l.stats, 0, sizeof(LearnerStats), st));
+        CU(cudaMemsetAsync(l.info, 0, sizeof(DevLearnerInfo), st));
+        CU(cudaMemsetAsync(l.d, 0, cfg->replay_capacity, st));
+    }
+    // theta^+ = theta0 (canonical -> internal sliced)
+    CU(cudaMemcpyAsync(ctx->tmp_canon, cfg->theta0, sizeof(float) * ctx->P, cudaMemcpyHostToDevice, st));
+    k_convert<<<148 * 4, 256, 0, st>>>(ctx->tmp_canon, ctx->theta, ctx->P, ctx->q, ctx->per, 0);
+    ctx->launches++;
+    // replica slot 0 and every learner's theta^- (Alg.1 P:113 theta^- = theta)
+    gorila_status s;
+    if ((s = pack_any(ctx, ctx->theta, ctx->rep_t[0], ctx->rep_f[0], true, nullptr, ctx->Vhist)) != GORILA_OK) return s;
+    for (auto& l : ctx->learners)
+        if ((s = pack_any(ctx, ctx->theta, l.tminus_t, l.tminus_f, false, nullptr, nullptr)) != GORILA_OK) return s;
+    if (cfg->world > 1) {
+        ncclUniqueId id;
+        memcpy(&id, cfg->nccl_unique_id, sizeof(id));
+        NC(ncclCommInitRank(&ctx->comm, cfg->world, id, cfg->rank));
+    }
+    CU(cudaStreamSynchronize(st));
+    *out = ctx;
+    return GORILA_OK;
+}
+
+void gorila_destroy(gorila_ctx* ctx) {
+    if (!ctx) return;
+    if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+    for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->comm) {
+        if (ctx->poisoned) ncclCommAbort(ctx->comm);
+        else ncclCommDestroy(ctx->comm);
+    }
+    delete ctx;
+}
+
+gorila_status replay_insert(gorila_ctx* ctx, int32_t learner, int64_t count, const uint8_t* frames,
+                            const uint8_t* actions, const float* rewards, const uint8_t* terminals,
+                            int32_t src_on_device) {
+    gorila_status s = check_learner(ctx, learner);
+    if (s != GORILA_OK) return s;
+    if (count < 0) return fail(GORILA_E_SHAPE, "negative count");
+    if (count == 0) return GORILA_OK;
+    if (!frames || !actions || !rewards || !terminals) return fail(GORILA_E_INVALID, "null buffer");
+    Learner& l = ctx->learners[learner];
+    const int64_t C = ctx->cfg.replay_capacity;
+    const cudaMemcpyKind kind = src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    cudaStream_t st = ctx->stream;
+    // only the last min(count, C) steps survive; copy them in at most two contiguous segments
+    int64_t skip = count > C ? count - C : 0;
+    int64_t t = l.n_host + skip, left = count - skip, src = skip;
+    while (left > 0) {
+        const int64_t slot = t % C, seg = std::min(left, C - slot);
+        CU(cudaMemcpyAsync(l.frames + slot * FRAME_BYTES, frames + src * FRAME_BYTES, seg * FRAME_BYTES, kind, st));
+        CU(cudaMemcpyAsync(l.a + slot, actions + src, seg, kind, st));
+        CU(cudaMemcpyAsync(l.r + slot, rewards + src, seg * sizeof(float), kind, st));
+        CU(cudaMemcpyAsync(l.d + slot, terminals + src, seg, kind, st));
+        t += seg; src += seg; left -= seg;
+    }
+    if (!src_on_device) CU(cudaStreamSynchronize(st));  // host buffers may be reused on return
+    l.n_host += count;
+    k_set_u64<<<1, 1, 0, st>>>(l.n_dev, (uint64_t)l.n_host);
+    ctx->launches++;
+    CU(cudaGetLastError());
+    return GORILA_OK;
+}
+
+gorila_status replay_sample(gorila_ctx* ctx, int32_t learner, uint64_t round, int64_t* idx_out, uint8_t* s_out,
+                            uint8_t* s2_out, uint8_t* a_out, float* r_out, uint8_t* d_out) {
+    gorila_status s = check_learner(ctx, learner);
+    if (s != GORILA_OK) return s;
+    Learner& l = ctx->learners[learner];
+    const int64_t size = std::min<int64_t>(l.n_host, ctx->cfg.replay_capacity);
+    if (size - 1 < std::max<int64_t>(1, ctx->cfg.min_replay)) return fail(GORILA_E_NOT_READY, "replay not ready");
+    const int B = ctx->B;
+    cudaStream_t st = ctx->stream;
+    const gorila_config& cfg = ctx->cfg;
+    // sample into u8-valued T buffers of the scratch (same kernel as learner_step)
+    dim3 grid((FRAME_BYTES / 16 + 255) / 256, B);
+    uint2 key = make_uint2((uint32_t)cfg.seed, (uint32_t)(cfg.seed >> 32));
+    if (cfg.math == GORILA_MATH_FP32)
+        k_sample<float><<<grid, 256, 0, st>>>(l.frames, l.a, l.r, l.d, cfg.replay_capacity, l.n_dev, key,
+                                              (uint32_t)(cfg.learner_id_base + learner), round, B, (float*)ctx->s,
+                                              (float*)ctx->s2, ctx->sa, ctx->sr, ctx->sd, ctx->sidx);
+    else
+        k_sample<__nv_bfloat16><<<grid, 256, 0, st>>>(l.frames, l.a, l.r, l.d, cfg.replay_capacity, l.n_dev, key,
+                                                      (uint32_t)(cfg.learner_id_base + learner), round, B,
+                                                      (__nv_bfloat16*)ctx->s, (__nv_bfloat16*)ctx->s2, ctx->sa,
+                                                      ctx->sr, ctx->sd, ctx->sidx);
+    ctx->launches++;
+    CU(cudaGetLastError());
+    CU(cudaStreamSynchronize(st));
+    if (idx_out) CU(cudaMemcpy(idx_out, ctx->sidx, sizeof(int64_t) * B, cudaMemcpyDeviceToHost));
+    if (a_out) CU(cudaMemcpy(a_out, ctx->sa, B, cudaMemcpyDeviceToHost));
+    if (r_out) CU(cudaMemcpy(r_out, ctx->sr, sizeof(float) * B, cudaMemcpyDeviceToHost));
+    if (d_out) CU(cudaMemcpy(d_out, ctx->sd, B, cudaMemcpyDeviceToHost));
+    // NHWC T -> NCHW u8 on the host side of the boundary (debug / parity entry point)
+    const int64_t n_el = (int64_t)B * FRAME_BYTES * NSTACK;
+    std::vector<uint8_t> raw(n_el * ctx->esz);
+    for (int which = 0; which < 2; ++which) {
+        uint8_t* dst = which ? s2_out : s_out;
+        if (!dst) continue;
+        CU(cudaMemcpy(raw.data(), which ? ctx->s2 : ctx->s, raw.size(), cudaMemcpyDeviceToHost));
+        for (int64_t b = 0; b < B; ++b)
+            for (int64_t p = 0; p < FRAME_BYTES; ++p)
+                for (int c = 0; c < NSTACK; ++c) {
+                    const int64_t src = (b * FRAME_BYTES + p) * NSTACK + c;
+                    float val;
+                    if (ctx->esz == 4) {
+                        memcpy(&val, raw.data() + src * 4, 4);
+                    } else {
+                        uint16_t h;
+                        memcpy(&h, raw.data() + src * 2, 2);
+                        uint32_t bits = (uint32_t)h << 16;
+                        memcpy(&val, &bits, 4);
+                    }
+                    dst[(b * NSTACK + c) * FRAME_BYTES + p] = (uint8_t)val;
+                }
+    }
+    return GORILA_OK;
+}
+
+gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
+                           const int32_t* staleness, gorila_learner_info* info_out) {
+    if (!ctx) return fail(GORILA_E_INVALID, "null context");
+    if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned");
+    if (!learners || n < 1 || n > ctx->L) return fail(GORILA_E_SHAPE, "bad learner list");
+    for (int i = 0; i < n; ++i) {
+        if (learners[i] < 0 || learners[i] >= ctx->L) return fail(GORILA_E_RANGE, "learner id out of range");
+        if (i && learners[i] <= learners[i - 1]) return fail(GORILA_E_INVALID, "learners must be ascending");
+        if (staleness && (staleness[i] < 0 || staleness[i] >= ctx->H))
+            return fail(GORILA_E_RANGE, "staleness must be in [0, history)");
+    }
+    cudaStream_t st = ctx->stream;
+    mark(ctx, -1);
+    ctx->prof_steps += ctx->prof ? 1 : 0;
+    CU(cudaMemsetAsync(ctx->G, 0, sizeof(float) * ctx->W * ctx->per, st));
+    CU(cudaMemsetAsync(ctx->n_acc_local, 0, sizeof(uint32_t), st));
+    mark(ctx, PH_STEP_MISC);
+    for (int i = 0; i < n; ++i) {
+        const int j = learners[i];
+        Learner& l = ctx->learners[j];
+        const int64_t size = std::min<int64_t>(l.n_host, ctx->cfg.replay_capacity);
+        if (size - 1 < std::max<int64_t>(1, ctx->cfg.min_replay)) {
+            k_mark_not_ready<<<1, 1, 0, st>>>(l.info, l.stats);
+            ctx->launches++;
+            continue;
+        }
+        const int s_j = staleness ? staleness[i] : 0;
+        gorila_status s = ctx->cfg.math == GORILA_MATH_FP32 ? run_learner<float>(ctx, j, round, s_j)
+                                                             : run_learner<__nv_bfloat16>(ctx, j, round, s_j);
+        if (s != GORILA_OK) return s;
+    }
+    k_write_counts<<<1, 64, 0, st>>>(ctx->G, ctx->q, ctx->per, ctx->W, ctx->n_acc_local);
+    ctx->launches++;
+    mark(ctx, PH_STEP_MISC);
+    if (info_out)
+        for (int i = 0; i < n; ++i)
+            CU(cudaMemcpyAsync(&info_out[i], ctx->learners[learners[i]].info, sizeof(gorila_learner_info),
+                               cudaMemcpyDeviceToHost, st));
+    CU(cudaGetLastError());
+    return GORILA_OK;
+}
+
+gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info* info_out) {
+    if (!ctx) return fail(GORILA_E_INVALID, "null context");
+    if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned");
+    cudaStream_t st = ctx->stream;
+    const int W = ctx->W, r = ctx->rank;
+    float* gsl = ctx->G + (int64_t)r * ctx->per;
+    mark(ctx, -1);
+    if (W > 1) NC(ncclReduceScatter(ctx->G, gsl, ctx->per, ncclFloat, ncclSum, ctx->comm, st));
+    mark(ctx, PH_RS);
+    ApplyParams p{};
+    p.theta = ctx->theta + (int64_t)r * ctx->per;
+    p.m = ctx->m;
+    p.v = ctx->v;
+    p.g = gsl;
+    p.n_real = std::max<int64_t>(0, std::min<int64_t>(ctx->q, ctx->P - (int64_t)r * ctx->q));
+    p.q = ctx->q;
+    p.optimizer = ctx->cfg.optimizer;
+    p.lr = ctx->cfg.lr; p.rho = ctx->cfg.rms_rho; p.eps = ctx->cfg.rms_eps; p.ada_eps = ctx->cfg.ada_eps;
+    p.V = ctx->V;
+    p.round_info = ctx->round_info;
+    k_apply<<<148 * 4, 256, 0, st>>>(p);
+    ctx->launches++;
+    mark(ctx, PH_APPLY);
+    if (W > 1) NC(ncclAllGather(p.theta, ctx->theta, ctx->per, ncclFloat, ctx->comm, st));
+    mark(ctx, PH_AG);
+    const int slot = (int)((round + 1) % (uint64_t)ctx->H);
+    gorila_status s = pack_any(ctx, ctx->theta, ctx->rep_t[slot], ctx->rep_f[slot], true, nullptr, ctx->Vhist + slot);
+    if (s != GORILA_OK) return s;
+    mark(ctx, PH_PACK);
+    if (info_out) {
+        uint64_t tmp[3];
+        CU(cudaMemcpyAsync(tmp, ctx->round_info, sizeof(tmp), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        info_out->n_accepted = (uint32_t)tmp[0];
+        info_out->pad_ = 0;
+        info_out->version_before = tmp[1];
+        info_out->version_after = tmp[2];
+    }
+    CU(cudaGetLastError());
+    return GORILA_OK;
+}
+
+gorila_status sync_target(gorila_ctx* ctx, const int32_t* learners, int32_t n, int32_t force, uint8_t* synced_out) {
+    if (!ctx) return fail(GORILA_E_INVALID, "null context");
+    if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned");
+    if (!learners || n < 1) return fail(GORILA_E_SHAPE, "bad learner list");
+    cudaStream_t st = ctx->stream;
+    mark(ctx, -1);
+    for (int i = 0; i < n; ++i) {
+        gorila_status s = check_learner(ctx, learners[i]);
+        if (s != GORILA_OK) return s;
+        Learner& l = ctx->learners[learners[i]];
+        k_sync_decide<<<1, 1, 0, st>>>(l.stats, ctx->V, ctx->cfg.target_period, force, l.sync_flag);
+        ctx->launches++;
+        if ((s = pack_any(ctx, ctx->theta, l.tminus_t, l.tminus_f, false, l.sync_flag, nullptr)) != GORILA_OK) return s;
+        if (synced_out) CU(cudaMemcpyAsync(&synced_out[i], l.sync_flag, 1, cudaMemcpyDeviceToHost, st));
+    }
+    mark(ctx, PH_SYNC);
+    CU(cudaGetLastError());
+    return GORILA_OK;
+}
+
+gorila_status gorila_get_state(gorila_ctx* ctx, float* theta, float* m, float* v, uint64_t* version) {
+    if (!ctx) return fail(GORILA_E_INVALID, "null context");
+    cudaStream_t st = ctx->stream;
+    const int64_t P = ctx->P;
+    struct Item { const float* src_slice; float* dst; bool full; } items[3] = {
+        {ctx->theta, theta, true}, {ctx->m, m, false}, {ctx->v, v, false}};
+    for (auto& it : items) {
+        if (!it.dst) continue;
+        if (it.full) {
+            CU(cudaMemcpyAsync(ctx->tmp_int, it.src_slice, sizeof(float) * ctx->W * ctx->per, cudaMemcpyDeviceToDevice, st));
+        } else {  // own slice only; other slices zero
+            CU(cudaMemsetAsync(ctx->tmp_int, 0, sizeof(float) * ctx->W * ctx->per, st));
+            CU(cudaMemcpyAsync(ctx->tmp_int + (int64_t)ctx->rank * ctx->per, it.src_slice, sizeof(float) * ctx->per,
+                               cudaMemcpyDeviceToDevice, st));
+        }
+        k_convert<<<148 * 4, 256, 0, st>>>(ctx->tmp_int, ctx->tmp_canon, P, ctx->q, ctx->per, 1);
+        ctx->launches++;
+        CU(cudaMemcpyAsync(it.dst, ctx->tmp_canon, sizeof(float) * P, cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    if (version) CU(cudaMemcpy(version, ctx->V, sizeof(uint64_t), cudaMemcpyDeviceToHost));
+    return GORILA_OK;
+}
+
+gorila_status gorila_set_state(gorila_ctx* ctx, const float* theta, const float* m, const float* v, uint64_t version) {
+    if (!ctx) return fail(GORILA_E_INVALID, "null context");
+    cudaStream_t st = ctx->stream;
+    const int64_t P = ctx->P;
+    struct Item { const float* src; float* dst_slice; bool full; } items[3] = {
+        {theta, ctx->theta, true}, {m, ctx->m, false}, {v, ctx->v, false}};
+    for (auto& it : items) {
+        if (!it.src) continue;
+        CU(cudaMemcpyAsync(ctx->tmp_canon, it.src, sizeof(float) * P, cudaMemcpyHostToDevice, st));
+        CU(cudaMemsetAsync(ctx->tmp_int, 0, sizeof(float) * ctx->W * ctx->per, st));
+        k_convert<<<148 * 4, 256, 0, st>>>(ctx->tmp_canon, ctx->tmp_int, P, ctx->q, ctx->per, 0);
+        ctx->launches++;
+        if (it.full)
+            CU(cudaMemcpyAsync(it.dst_slice, ctx->tmp_int, sizeof(float) * ctx->W * ctx->per, cudaMemcpyDeviceToDevice, st));
+        else
+            CU(cudaMemcpyAsync(it.dst_slice, ctx->tmp_int + (int64_t)ctx->rank * ctx->per, sizeof(float) * ctx->per,
+                               cudaMemcpyDeviceToDevice, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    k_set_u64<<<1, 1, 0, st>>>(ctx->V, version);
+    ctx->launches++;
+    // every replica slot = the new theta (teacher forcing restarts the history)
+    for (int h = 0; h < ctx->H; ++h) {
+        gorila_status s = pack_any(ctx, ctx->theta, ctx->rep_t[h], ctx->rep_f[h], true, nullptr, ctx->Vhist + h);
+        if (s != GORILA_OK) return s;
+    }
+    CU(cudaStreamSynchronize(st));
+    return GORILA_OK;
+}
+
+gorila_status gorila_get_learner_state(gorila_ctx* ctx, int32_t learner, float* theta_minus, double* stats4) {
+    gorila_status s = check_learner(ctx, learner);
+    if (s != GORILA_OK) return s;
+    cudaStream_t st = ctx->stream;
+    Learner& l = ctx->learners[learner];
+    CU(cudaStreamSynchronize(st));
+    if (stats4) {
+        LearnerStats h;
+        CU(cudaMemcpy(&h, l.stats, sizeof(h), cudaMemcpyDeviceToHost));
+        stats4[0] = h.mu; stats4[1] = h.var; stats4[2] = (double)h.count; stats4[3] = (double)h.last_sync;
+    }
+    if (theta_minus) {
+        // unpack the fwd replica (T) + fp32 area back to canonical fp32 on the host
+        const ReplicaLayout& R = ctx->rl_fwd;
+        std::vector<uint8_t> t(R.n_t * ctx->esz);
+        std::vector<float> f(R.n_f);
+        CU(cudaMemcpy(t.data(), l.tminus_t, t.size(), cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(f.data(), l.tminus_f, f.size() * sizeof(float), cudaMemcpyDeviceToHost));
+        auto tval = [&](int64_t e) -> float {
+            if (ctx->esz == 4) { float x; memcpy(&x, t.data() + e * 4, 4); return x; }
+            uint16_t h; memcpy(&h, t.data() + e * 2, 2); uint32_t bits = (uint32_t)h << 16; float x; memcpy(&x, &bits, 4); return x;
+        };
+        for (int64_t i = 0; i < ctx->P; ++i) {
+            float w;
+            if (i < OFF_B1) w = tval(R.w1 + i);
+            else if (i < OFF_W2) w = f[R.b1 + i - OFF_B1];
+            else if (i < OFF_B2) w = tval(R.w2 + i - OFF_W2);
+            else if (i < OFF_W3) w = f[R.b2 + i - OFF_B2];
+            else if (i < OFF_B3) w = tval(R.w3 + i - OFF_W3);
+            else if (i < OFF_W4) w = f[R.b3 + i - OFF_B3];
+            else if (i < OFF_B4) w = tval(R.w4 + i - OFF_W4);
+            else if (i < OFF_W5) w = f[R.b4 + i - OFF_B4];
+            else w = f[R.w5 + i - OFF_W5];
+            theta_minus[canon_of_internal(i)] = w;
+        }
+    }
+    return GORILA_OK;
+}
+
+gorila_status gorila_set_learner_state(gorila_ctx* ctx, int32_t learner, const float* theta_minus,
+                                       const double* stats4) {
+    gorila_status s = check_learner(ctx, learner);
+    if (s != GORILA_OK) return s;
+    cudaStream_t st = ctx->stream;
+    Learner& l = ctx->learners[learner];
+    if (stats4) {
+        LearnerStats h{};
+        h.mu = stats4[0]; h.var = stats4[1]; h.count = (uint32_t)stats4[2]; h.last_sync = (uint64_t)stats4[3];
+        CU(cudaMemcpyAsync(l.stats, &h, sizeof(h), cudaMemcpyHostToDevice, st));
+        CU(cudaStreamSynchronize(st));
+    }
+    if (theta_minus) {
+        CU(cudaMemcpyAsync(ctx->tmp_canon, theta_minus, sizeof(float) * ctx->P, cudaMemcpyHostToDevice, st));
+        CU(cudaMemsetAsync(ctx->tmp_int, 0, sizeof(float) * ctx->W * ctx->per, st));
+        k_convert<<<148 * 4, 256, 0, st>>>(ctx->tmp_canon, ctx->tmp_int, ctx->P, ctx->q, ctx->per, 0);
+        ctx->launches++;
+        if ((s = pack_any(ctx, ctx->tmp_int, l.tminus_t, l.tminus_f, false, nullptr, nullptr)) != GORILA_OK) return s;
+        CU(cudaStreamSynchronize(st));
+    }
+    return GORILA_OK;
+}
+
+gorila_status gorila_get_grad(gorila_ctx* ctx, float* g) {
+    if (!ctx || !g) return fail(GORILA_E_INVALID, "null argument");
+    cudaStream_t st = ctx->stream;
+    k_convert<<<148 * 4, 256, 0, st>>>(ctx->G, ctx->tmp_canon, ctx->P, ctx->q, ctx->per, 1);
+    ctx->launches++;
+    CU(cudaMemcpyAsync(g, ctx->tmp_canon, sizeof(float) * ctx->P, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    return GORILA_OK;
+}
+
+gorila_status gorila_get_q(gorila_ctx* ctx, int32_t learner, float* q, float* qhat) {
+    gorila_status s = check_learner(ctx, learner);
+    if (s != GORILA_OK) return s;
+    Learner& l = ctx->learners[learner];
+    CU(cudaStreamSynchronize(ctx->stream));
+    if (q) CU(cudaMemcpy(q, l.Q, sizeof(float) * ctx->B * ctx->nA, cudaMemcpyDeviceToHost));
+    if (qhat) CU(cudaMemcpy(qhat, l.Qhat, sizeof(float) * ctx->B * ctx->nA, cudaMemcpyDeviceToHost));
+    return GORILA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,473 @@
+// kernels.cuh — the non-GEMM kernels of the learner update (SIMT, HBM / latency bound).
+#pragma once
+#include "common.cuh"
+#include "layout.cuh"
+
+namespace gorila {
+
+constexpr uint32_t TAG_SAMPLE = 3u;
+
+// position of internal element i in the sliced storage (q real elements per shard slice,
+// slice stride per = q + 64; element q of every slice is the accepted-gradient count slot)
+GORILA_DEV int64_t gslot(int64_t i, int64_t q, int64_t per) { return (i / q) * per + (i % q); }
+
+// ------------------------------------------------------------------------- K1 sampler
+// Alg.1 P:121 "Sample random mini-batch from D"; "(s,a,r,s') ~ U(D)"; P:181 4-frame stack.
+// Block (cx, b): tau_b from Philox4x32-10 (counter {b/2, learner, round lo, round hi | TAG}),
+// tau = (n - size) + floor(u * (size-1) / 2^64); thread = one 16-pixel chunk of the 84x84
+// frame: reads the 5 frames o_{tau-3} .. o_{tau+1} (16 B each, coalesced), applies the
+// episode / eviction zero mask and writes s, s' as NHWC [B][84][84][4] in T.
+template <typename T>
+__global__ void __launch_bounds__(256) k_sample(const uint8_t* __restrict__ frames, const uint8_t* __restrict__ ring_a,
+                                                const float* __restrict__ ring_r, const uint8_t* __restrict__ ring_d,
+                                                int64_t C, const uint64_t* __restrict__ ring_n, uint2 key,
+                                                uint32_t learner_gid, uint64_t round, int B, T* __restrict__ s_out,
+                                                T* __restrict__ s2_out, uint8_t* __restrict__ a_out,
+                                                float* __restrict__ r_out, uint8_t* __restrict__ d_out,
+                                                int64_t* __restrict__ idx_out) {
+    const int b = blockIdx.y;
+    const int64_t n = (int64_t)*ring_n;
+    const int64_t size = n < C ? n : C;
+    const uint64_t M = (uint64_t)(size - 1);
+    const uint4 x = philox4x32_10(make_uint4((uint32_t)(b >> 1), learner_gid, (uint32_t)round,
+                                             (uint32_t)((round >> 32) & 0xffffffu) | (TAG_SAMPLE << 24)),
+                                  key);
+    const uint64_t u = (b & 1) ? ((uint64_t)x.z | ((uint64_t)x.w << 32)) : ((uint64_t)x.x | ((uint64_t)x.y << 32));
+    const int64_t tau = (n - size) + (int64_t)__umul64hi(u, M);
+    const int64_t oldest = n - size;
+
+    // keep[f] for frames tau-3+f, f = 0..4 (s uses f = 0..3, s' uses f = 1..4)
+    bool keep_s[4], keep_s2[4];
+    {
+        bool dflag[4];  // d_{tau-3+t}, t = 0..3 (only read when the frame is retained)
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            int64_t st = tau - 3 + t;
+            dflag[t] = (st >= oldest) ? (ring_d[st % C] != 0) : true;
+        }
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            // s channel c = frame tau-3+c: zero if evicted or an episode ended at t' in [tau-3+c, tau-1]
+            bool k = (tau - 3 + c) >= oldest;
+            for (int t = c; t < 3; ++t) k = k && !dflag[t];
+            keep_s[c] = k;
+            // s' channel c = frame tau-2+c: zero if evicted or an episode ended at t' in [tau-2+c, tau]
+            bool k2 = (tau - 2 + c) >= oldest;
+            for (int t = c + 1; t < 4; ++t) k2 = k2 && !dflag[t];
+            keep_s2[c] = k2;
+        }
+    }
+    const int chunk = blockIdx.x * blockDim.x + threadIdx.x;
+    if (chunk < FRAME_BYTES / 16) {
+        uint4 f[5];
+#pragma unroll
+        for (int t = 0; t < 5; ++t) {
+            int64_t st = tau - 3 + t;
+            bool need = (t < 4 && keep_s[t]) || (t >= 1 && keep_s2[t - 1]);
+            f[t] = need ? *reinterpret_cast<const uint4*>(frames + (st % C) * FRAME_BYTES + chunk * 16)
+                        : make_uint4(0, 0, 0, 0);
+        }
+        const uint8_t* fb[5];
+#pragma unroll
+        for (int t = 0; t < 5; ++t) fb[t] = reinterpret_cast<const uint8_t*>(&f[t]);
+        T* so = s_out + ((int64_t)b * FRAME_BYTES + chunk * 16) * NSTACK;
+        T* so2 = s2_out + ((int64_t)b * FRAME_BYTES + chunk * 16) * NSTACK;
+#pragma unroll
+        for (int px = 0; px < 16; ++px) {
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                so[px * 4 + c] = fromf<T>(keep_s[c] ? (float)fb[c][px] : 0.f);
+                so2[px * 4 + c] = fromf<T>(keep_s2[c] ? (float)fb[c + 1][px] : 0.f);
+            }
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        a_out[b] = ring_a[tau % C];
+        r_out[b] = ring_r[tau % C];
+        d_out[b] = ring_d[tau % C];
+        idx_out[b] = tau;
+    }
+}
+
+// ------------------------------------------------------------------------- fc4 split-K finalize
+// a4[b][n] = round_T(ReLU(sum_s partial[s][n][b] + b4[n])), both nets (z = problem)
+template <typename T>
+__global__ void k_fc4_finalize(const float* __restrict__ partial, int splits, int64_t prob_stride, int B,
+                               const float* __restrict__ bias0, const float* __restrict__ bias1, T* out0, T* out1) {
+    const int z = blockIdx.y;
+    const float* P = partial + z * prob_stride;
+    const float* bias = z ? bias1 : bias0;
+    T* out = z ? out1 : out0;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < B * FC4_OUT; e += gridDim.x * blockDim.x) {
+        int b = e / FC4_OUT, n = e - b * FC4_OUT;
+        float acc = 0.f;
+        for (int s = 0; s < splits; ++s) acc += P[(int64_t)s * FC4_OUT * B + (int64_t)n * B + b];
+        out[e] = fromf<T>(fmaxf(acc + bias[n], 0.f));
+    }
+}
+
+// ------------------------------------------------------------------------- fc5 forward
+// Q[b][a] = sum_n a4[b][n] * W5[a][n] + b5[a]  (fp32 weights, fp32 result; z = online / target)
+template <typename T>
+__global__ void __launch_bounds__(256) k_fc5_fwd(const T* __restrict__ a4_0, const T* __restrict__ a4_1,
+                                                 const float* __restrict__ w5_0, const float* __restrict__ w5_1,
+                                                 const float* __restrict__ b5_0, const float* __restrict__ b5_1,
+                                                 float* __restrict__ q0, float* __restrict__ q1, int nA) {
+    const int b = blockIdx.x, z = blockIdx.y;
+    const T* a4 = (z ? a4_1 : a4_0) + (int64_t)b * FC4_OUT;
+    const float* w5 = z ? w5_1 : w5_0;
+    const float* b5 = z ? b5_1 : b5_0;
+    float* q = z ? q1 : q0;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int a = warp; a < nA; a += 8) {
+        float acc = 0.f;
+        for (int n = lane; n < FC4_OUT; n += 32) acc = fmaf(tof(a4[n]), w5[a * FC4_OUT + n], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) q[b * nA + a] = acc + b5[a];
+    }
+}
+
+// ------------------------------------------------------------------------- K7 TD + decisions
+struct LearnerStats {  // device-resident per learner (reading R8)
+    double mu, var;
+    uint32_t count, pad_;
+    uint64_t last_sync;
+};
+
+struct DevLearnerInfo {  // mirrors gorila_learner_info
+    float loss, abs_loss;
+    double mu, var, threshold;
+    uint64_t base_version;
+    uint32_t stats_count;
+    uint8_t not_ready, rejected_outlier, stale, accepted;
+};
+
+struct TdParams {
+    const float* Q;
+    const float* Qhat;
+    const uint8_t* a;
+    const float* r;
+    const uint8_t* d;
+    float* dQ;
+    int B, nA;
+    float gamma;
+    LearnerStats* stats;
+    DevLearnerInfo* info;
+    const uint64_t* V;        // V0 (PS version before this round's apply)
+    const uint64_t* base_V;   // version of the replica used (history)
+    uint32_t* n_acc_local;
+    int64_t max_staleness;
+    int outlier_enabled, outlier_warmup;
+    float outlier_k;
+    double outlier_beta;
+};
+
+// One block, 8 warps; warp w handles samples w, w+8, ... (fixed order):
+// y = r if terminal else r + gamma * max_a Qhat (Alg.1), delta = y - Q[a]
+// (Eq.1/Eq.2), dQ[a] = -clip(delta, -1, 1) / B (reading R3/R4); loss = mean delta^2,
+// l = mean |delta|; outlier + stale decisions; rejected or stale => dQ = 0.
+__global__ void __launch_bounds__(256) k_td(TdParams p) {
+    __shared__ float s_sq[8], s_ab[8];
+    __shared__ int s_keep;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    float sq = 0.f, ab = 0.f;
+    for (int i = warp; i < p.B; i += 8) {
+        const float qh = lane < p.nA ? p.Qhat[i * p.nA + lane] : -INFINITY;
+        const float mx = warp_max(qh);
+        const int ai = p.a[i];
+        const float y = p.d[i] ? p.r[i] : p.r[i] + p.gamma * mx;
+        const float qa = p.Q[i * p.nA + ai];
+        const float delta = y - qa;
+        if (lane < p.nA) {
+            const float cl = fminf(fmaxf(delta, -1.f), 1.f);
+            p.dQ[i * p.nA + lane] = (lane == ai) ? -cl / (float)p.B : 0.f;
+        }
+        sq += delta * delta;
+        ab += fabsf(delta);
+    }
+    if (lane == 0) {
+        s_sq[warp] = sq;
+        s_ab[warp] = ab;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        float tsq = 0.f, tab = 0.f;
+        for (int w = 0; w < 8; ++w) {
+            tsq += s_sq[w];
+            tab += s_ab[w];
+        }
+        const float loss = tsq / (float)p.B, ell = tab / (float)p.B;
+        LearnerStats st = *p.stats;
+        const double thr = st.mu + (double)p.outlier_k * sqrt(st.var);
+        const bool rejected = p.outlier_enabled && st.count >= (uint32_t)p.outlier_warmup && (double)ell > thr;
+        DevLearnerInfo inf{};
+        inf.stats_count = st.count;
+        // EMA update with every batch (reading R8)
+        if (st.count == 0) {
+            st.mu = ell;
+            st.var = 0.0;
+        } else {
+            const double e = (double)ell - st.mu;
+            st.mu = st.mu + (1.0 - p.outlier_beta) * e;
+            st.var = p.outlier_beta * (st.var + (1.0 - p.outlier_beta) * e * e);
+        }
+        st.count += 1;
+        *p.stats = st;
+        const uint64_t V0 = *p.V, base = *p.base_V;
+        const bool stale = p.max_staleness >= 0 && (int64_t)(V0 - base) > p.max_staleness;
+        const bool accepted = !rejected && !stale;
+        inf.loss = loss;
+        inf.abs_loss = ell;
+        inf.mu = st.mu;
+        inf.var = st.var;
+        inf.threshold = thr;
+        inf.base_version = base;
+        inf.rejected_outlier = rejected;
+        inf.stale = stale;
+        inf.accepted = accepted;
+        *p.info = inf;
+        if (accepted) *p.n_acc_local += 1;
+        s_keep = accepted;
+    }
+    __syncthreads();
+    if (!s_keep)
+        for (int e = threadIdx.x; e < p.B * p.nA; e += blockDim.x) p.dQ[e] = 0.f;
+}
+
+__global__ void k_mark_not_ready(DevLearnerInfo* info, const LearnerStats* st) {
+    DevLearnerInfo inf{};
+    inf.not_ready = 1;
+    inf.mu = st->mu;
+    inf.var = st->var;
+    inf.stats_count = st->count;
+    *info = inf;
+}
+
+// ------------------------------------------------------------------------- fc5 backward
+// dW5[a][n] += sum_b dQ[b][a] a4[b][n]; db5[a] += sum_b dQ[b][a];
+// g4[b][n] = round_T((sum_a dQ[b][a] W5[a][n]) * 1[a4[b][n] > 0])
+template <typename T>
+__global__ void k_fc5_bwd(const float* __restrict__ dQ, const T* __restrict__ a4, const float* __restrict__ w5, int B,
+                          int nA, float* __restrict__ G, int64_t q, int64_t per, T* __restrict__ g4) {
+    const int n_w = nA * FC4_OUT, n_b = nA, n_g = B * FC4_OUT;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_w + n_b + n_g; e += gridDim.x * blockDim.x) {
+        if (e < n_w) {
+            int a = e / FC4_OUT, n = e - a * FC4_OUT;
+            float acc = 0.f;
+            for (int b = 0; b < B; ++b) acc = fmaf(dQ[b * nA + a], tof(a4[(int64_t)b * FC4_OUT + n]), acc);
+            G[gslot(OFF_W5 + e, q, per)] += acc;
+        } else if (e < n_w + n_b) {
+            int a = e - n_w;
+            float acc = 0.f;
+            for (int b = 0; b < B; ++b) acc += dQ[b * nA + a];
+            G[gslot(off_b5(nA) + a, q, per)] += acc;
+        } else {
+            int f = e - n_w - n_b, b = f / FC4_OUT, n = f - b * FC4_OUT;
+            float acc = 0.f;
+            for (int a = 0; a < nA; ++a) acc = fmaf(dQ[b * nA + a], w5[a * FC4_OUT + n], acc);
+            g4[f] = fromf<T>(tof(a4[f]) > 0.f ? acc : 0.f);
+        }
+    }
+}
+
+// ------------------------------------------------------------------------- bias gradients
+// db_l[o] += sum_m g_l[m][o] for layers 1..4 (block = one output channel, fixed-order reduction)
+template <typename T>
+__global__ void __launch_bounds__(256) k_bias_grad(const T* __restrict__ g1, const T* __restrict__ g2,
+                                                   const T* __restrict__ g3, const T* __restrict__ g4, int B,
+                                                   float* __restrict__ G, int64_t q, int64_t per) {
+    __shared__ float red[256];
+    int o = blockIdx.x;
+    const T* g;
+    int C, rows;
+    int64_t off;
+    if (o < C1_OUT) { g = g1; C = C1_OUT; rows = B * H1 * H1; off = OFF_B1; }
+    else if ((o -= C1_OUT) < C2_OUT) { g = g2; C = C2_OUT; rows = B * H2 * H2; off = OFF_B2; }
+    else if ((o -= C2_OUT) < C3_OUT) { g = g3; C = C3_OUT; rows = B * H3 * H3; off = OFF_B3; }
+    else { o -= C3_OUT; g = g4; C = FC4_OUT; rows = B; off = OFF_B4; }
+    float acc = 0.f;
+    for (int m = threadIdx.x; m < rows; m += blockDim.x) acc += tof(g[(int64_t)m * C + o]);
+    red[threadIdx.x] = acc;
+    __syncthreads();
+    for (int w = 128; w > 0; w >>= 1) {
+        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) G[gslot(off + o, q, per)] += red[0];
+}
+
+// ------------------------------------------------------------------------- K10 wgrad reduce
+// G[W_l] += sum_s partial_l[s][.] in split order, for the three conv layers
+struct WgradReduceParams {
+    const float* part[3];
+    int splits[3];
+    int64_t count[3];
+    int64_t off[3];
+};
+__global__ void k_wgrad_reduce(WgradReduceParams p, float* __restrict__ G, int64_t q, int64_t per) {
+    const int64_t total = p.count[0] + p.count[1] + p.count[2];
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        int l = 0;
+        int64_t f = e;
+        if (f >= p.count[0]) { f -= p.count[0]; l = 1; if (f >= p.count[1]) { f -= p.count[1]; l = 2; } }
+        float acc = 0.f;
+        for (int s = 0; s < p.splits[l]; ++s) acc += p.part[l][(int64_t)s * p.count[l] + f];
+        G[gslot(p.off[l] + f, q, per)] += acc;
+    }
+}
+
+// fc4 weight gradient epilogue: G[W4][n][k] += v  with i = k, j = n
+struct EpAddW4 {
+    float* G;
+    int64_t q, per;
+    int M, N;
+    GORILA_DEV void apply(int i, int j, float v, int) const {
+        if (i >= M || j >= N) return;
+        G[gslot(OFF_W4 + (int64_t)j * FC4_IN + i, q, per)] += v;
+    }
+};
+
+// ------------------------------------------------------------------------- PS apply (K11)
+struct ApplyParams {
+    float* theta;  // this rank's slice of theta^+ (sliced storage)
+    float* m;
+    float* v;
+    const float* g;  // this rank's reduced slice; g[q] = accepted count
+    int64_t n_real;  // real elements in this slice
+    int64_t q;
+    int optimizer;
+    float lr, rho, eps, ada_eps;
+    uint64_t* V;
+    uint64_t* round_info;  // [n_acc, V_before, V_after]
+};
+// Centered RMSProp (reading R2) / AdaGrad on the mean of the accepted gradients
+// (reading R12, R25); V += |Acc|. float4-vectorised, grid-stride.
+__global__ void __launch_bounds__(256) k_apply(ApplyParams p) {
+    const float cnt = p.g[p.q];
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const uint64_t v0 = *p.V;
+        const uint64_t n_acc = (uint64_t)(cnt + 0.5f);
+        p.round_info[0] = n_acc;
+        p.round_info[1] = v0;
+        p.round_info[2] = v0 + n_acc;
+        *p.V = v0 + n_acc;
+    }
+    if (!(cnt > 0.5f)) return;
+    const float inv = 1.0f / cnt;
+    const int64_t n4 = p.n_real / 4;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n4; e += (int64_t)gridDim.x * blockDim.x) {
+        float4 g = reinterpret_cast<const float4*>(p.g)[e];
+        float4 th = reinterpret_cast<float4*>(p.theta)[e];
+        float4 m = reinterpret_cast<float4*>(p.m)[e];
+        float4 v = reinterpret_cast<float4*>(p.v)[e];
+        float gv[4] = {g.x * inv, g.y * inv, g.z * inv, g.w * inv};
+        float tv[4] = {th.x, th.y, th.z, th.w}, mv[4] = {m.x, m.y, m.z, m.w}, vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+            if (p.optimizer == 0) {
+                mv[c] = p.rho * mv[c] + (1.f - p.rho) * gv[c];
+                vv[c] = p.rho * vv[c] + (1.f - p.rho) * gv[c] * gv[c];
+                tv[c] -= p.lr * gv[c] / sqrtf(vv[c] - mv[c] * mv[c] + p.eps);
+            } else {
+                vv[c] += gv[c] * gv[c];
+                tv[c] -= p.lr * gv[c] / (sqrtf(vv[c]) + p.ada_eps);
+            }
+        }
+        reinterpret_cast<float4*>(p.theta)[e] = make_float4(tv[0], tv[1], tv[2], tv[3]);
+        reinterpret_cast<float4*>(p.m)[e] = make_float4(mv[0], mv[1], mv[2], mv[3]);
+        reinterpret_cast<float4*>(p.v)[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+    }
+    // tail (n_real % 4)
+    for (int64_t e = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p.n_real;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        float gv = p.g[e] * inv;
+        if (p.optimizer == 0) {
+            p.m[e] = p.rho * p.m[e] + (1.f - p.rho) * gv;
+            p.v[e] = p.rho * p.v[e] + (1.f - p.rho) * gv * gv;
+            p.theta[e] -= p.lr * gv / sqrtf(p.v[e] - p.m[e] * p.m[e] + p.eps);
+        } else {
+            p.v[e] += gv * gv;
+            p.theta[e] -= p.lr * gv / (sqrtf(p.v[e]) + p.ada_eps);
+        }
+    }
+}
+
+// write this rank's accepted count into the count slot of every slice of G
+__global__ void k_write_counts(float* G, int64_t q, int64_t per, int W, const uint32_t* n_acc_local) {
+    int s = threadIdx.x;
+    if (s < W) G[s * per + q] = (float)*n_acc_local;
+}
+
+// ------------------------------------------------------------------------- replica pack
+// theta^+ (sliced, internal order, fp32) -> packed replica in T (+ fp32 area).
+// with_dgrad also writes the transposed dgrad copies. pred (nullable): skip unless *pred.
+template <typename T>
+__global__ void k_pack(const float* __restrict__ theta, int64_t q, int64_t per, int nA, T* __restrict__ rt,
+                       float* __restrict__ rf, int with_dgrad, const uint8_t* __restrict__ pred,
+                       uint64_t* __restrict__ vhist_dst, const uint64_t* __restrict__ V) {
+    if (pred && !*pred) return;
+    const ReplicaLayout L = replica_layout(nA, with_dgrad != 0);
+    const int64_t P = param_count(nA);
+    if (vhist_dst && blockIdx.x == 0 && threadIdx.x == 0) *vhist_dst = *V;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+        const float w = theta[gslot(i, q, per)];
+        if (i < OFF_B1) {
+            rt[L.w1 + i] = fromf<T>(w);
+        } else if (i < OFF_W2) {
+            rf[L.b1 + (i - OFF_B1)] = w;
+        } else if (i < OFF_B2) {
+            int64_t j = i - OFF_W2;
+            rt[L.w2 + j] = fromf<T>(w);
+            if (with_dgrad) {  // (o, ky, kx, c) -> (c, ky, kx, o)
+                int o = (int)(j / K2), r = (int)(j % K2), t = r / C1_OUT, c = r % C1_OUT;
+                rt[L.w2d + (int64_t)c * (C2_K * C2_K * C2_OUT) + t * C2_OUT + o] = fromf<T>(w);
+            }
+        } else if (i < OFF_W3) {
+            rf[L.b2 + (i - OFF_B2)] = w;
+        } else if (i < OFF_B3) {
+            int64_t j = i - OFF_W3;
+            rt[L.w3 + j] = fromf<T>(w);
+            if (with_dgrad) {
+                int o = (int)(j / K3), r = (int)(j % K3), t = r / C2_OUT, c = r % C2_OUT;
+                rt[L.w3d + (int64_t)c * K3 + t * C3_OUT + o] = fromf<T>(w);
+            }
+        } else if (i < OFF_W4) {
+            rf[L.b3 + (i - OFF_B3)] = w;
+        } else if (i < OFF_B4) {
+            int64_t j = i - OFF_W4;
+            rt[L.w4 + j] = fromf<T>(w);
+            if (with_dgrad) {
+                int64_t n = j / FC4_IN, k = j % FC4_IN;
+                rt[L.w4t + k * FC4_OUT + n] = fromf<T>(w);
+            }
+        } else if (i < OFF_W5) {
+            rf[L.b4 + (i - OFF_B4)] = w;
+        } else {
+            rf[L.w5 + (i - OFF_W5)] = w;  // W5 then b5 are contiguous in both layouts
+        }
+    }
+}
+
+// ------------------------------------------------------------------------- target sync decision
+// Alg.1; R13: sync iff force or V >= last + N; then last = V.
+__global__ void k_sync_decide(LearnerStats* st, const uint64_t* V, int64_t period, int force, uint8_t* flag) {
+    const uint64_t v = *V;
+    const bool doit = force || v >= st->last_sync + (uint64_t)period;
+    if (doit) st->last_sync = v;
+    *flag = doit;
+}
+
+// ------------------------------------------------------------------------- layout conversion
+// dir 0: canonical -> internal sliced ; dir 1: internal sliced -> canonical
+__global__ void k_convert(const float* __restrict__ src, float* __restrict__ dst, int64_t P, int64_t q, int64_t per,
+                          int dir) {
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = canon_of_internal(i), s = gslot(i, q, per);
+        if (dir == 0) dst[s] = src[c];
+        else dst[c] = src[s];
+    }
+}
+
+__global__ void k_set_u64(uint64_t* dst, uint64_t v) { *dst = v; }
+
+}  // namespace gorila

@@ -1,0 +1,88 @@
+"""Shared helpers of the -m gpu parity tests: build a GPU context and an oracle on the
+same seeded inputs, teacher-force the oracle from the GPU state, and compare."""
+import numpy as np
+
+import oracle as O
+import synth
+
+TOL = {"fp32": {"q": 1e-5, "g": 1e-5, "dtheta": 1e-5, "loss": 1e-5},
+       "bf16": {"q": 1e-3, "g": 5e-3, "dtheta": 5e-3, "loss": 1e-3}}
+
+
+def make_pair(nA=4, B=32, C=2000, n_insert=2000, math="fp32", L=1, history=2, p_poison=0.0, terminals=None, **kw):
+    from paper_1507_04296_b200 import Gorila
+    theta0 = kw.pop("theta0", None)
+    if theta0 is None:
+        theta0 = synth.theta0(nA)
+    g = Gorila(n_actions=nA, batch=B, replay_capacity=C, n_learners_local=L, theta0=theta0, math=math,
+               history=history, **kw)
+    ocfg = O.Config(n_actions=nA, batch=B, capacity=C, learners=tuple(range(L)),
+                    mode="bf16" if math == "bf16" else "exact", gamma=kw.get("gamma", 0.99),
+                    lr=kw.get("lr", 2.5e-4), rms_rho=kw.get("rms_rho", 0.95), rms_eps=kw.get("rms_eps", 0.01),
+                    optimizer=kw.get("optimizer", "rmsprop"), ada_eps=kw.get("ada_eps", 1e-8),
+                    target_period=kw.get("target_period", 100), max_staleness=kw.get("max_staleness", -1),
+                    outlier_enabled=bool(kw.get("outlier_enabled", True)), outlier_warmup=kw.get("outlier_warmup", 100),
+                    outlier_k=kw.get("outlier_k", 3.0), outlier_beta=kw.get("outlier_beta", 0.999),
+                    min_replay=kw.get("min_replay", 1), seed_sample=kw.get("seed", 1507))
+    orc = O.GorilaOracle(ocfg, theta0)
+    for j in range(L):
+        f = synth.frames(synth.SEED_DATA, j, 0, n_insert)
+        a, r, d = synth.meta(synth.SEED_DATA, j, 0, n_insert, nA, p_poison)
+        if terminals is not None:
+            d = terminals(j, d)
+        g.replay_insert(j, f, a, r, d)
+        orc.insert(j, f, a, r, d)
+    return g, orc
+
+
+def teacher_force(g, orc):
+    """Copy the GPU's PS and learner state into the oracle (one-step parity)."""
+    th, m, v, V = g.get_state()
+    orc.theta = th.astype(np.float64)
+    orc.m = m.astype(np.float64)
+    orc.v = v.astype(np.float64)
+    orc.V = int(V)
+    for j, L in orc.learners.items():
+        tm, st = g.get_learner_state(j)
+        L.theta_minus = tm.astype(np.float64)
+        L.stats = O.LossStats(mu=st["mu"], var=st["var"], count=st["count"])
+        L.last_sync = st["last_sync"]
+    orc.history = {}
+
+
+def rel_inf(x, ref):
+    ref = np.asarray(ref, np.float64)
+    return float(np.max(np.abs(np.asarray(x, np.float64) - ref)) / max(np.max(np.abs(ref)), 1e-30))
+
+
+def rel_l2(x, ref):
+    ref = np.asarray(ref, np.float64)
+    nr = np.linalg.norm(ref)
+    if nr == 0:
+        return 0.0 if np.linalg.norm(x) == 0 else np.inf
+    return float(np.linalg.norm(np.asarray(x, np.float64) - ref) / nr)
+
+
+def per_tensor_rel_l2(x, ref, nA):
+    out, off = {}, 0
+    for name, shp in O.param_shapes(nA):
+        n = int(np.prod(shp))
+        out[name] = rel_l2(x[off:off + n], ref[off:off + n])
+        off += n
+    return out
+
+
+def run_round_both(g, orc, k, learners, staleness=None):
+    """One round on both sides. Returns (gpu dict, oracle dict)."""
+    stal = None if staleness is None else [staleness.get(j, 0) for j in learners]
+    th0 = g.get_state()[0]
+    info = g.learner_step(learners, k, staleness=stal)
+    G = g.get_grad()
+    qs = {j: g.get_q(j) for j in learners}
+    ri = g.ps_apply_shard(k)
+    synced = g.sync_target(learners)
+    th1, m1, v1, V1 = g.get_state()
+    gpu = {"info": dict(zip(learners, info)), "G": G, "q": qs, "round": ri, "synced": dict(zip(learners, synced)),
+           "theta0": th0, "theta1": th1, "V": V1}
+    res = orc.round(k, staleness=staleness)
+    return gpu, res

@@ -1,0 +1,188 @@
+"""GPU parity: the CUDA path (through the C-ABI) against the CPU oracle, element by element.
+
+Bit-exact: sampled indices, gathered / stacked frames, a/r/d, discard decisions,
+accepted counts, versions, sync events. Floating point (BASELINE.json north_star):
+Q, Q-hat, loss within 1e-3 relative (bf16 tensor-core mode vs the bf16-emulating
+oracle) / 1e-5 (fp32 check mode vs the exact oracle); gradients and parameter
+updates within 5e-3 / 1e-5 normalised L2, on the whole vector and per tensor.
+"""
+import numpy as np
+import pytest
+
+import oracle as O
+import synth
+from gpu_util import TOL, make_pair, per_tensor_rel_l2, rel_inf, rel_l2, run_round_both, teacher_force
+
+pytestmark = pytest.mark.gpu
+
+
+def test_device_synth_matches_host():
+    import torch
+    from synth import fill_frames_dev, fill_meta_dev
+    n, t0, nA = 300, 123_456, 18
+    fr = torch.empty((n, 84, 84), dtype=torch.uint8, device="cuda")
+    a = torch.empty(n, dtype=torch.uint8, device="cuda")
+    r = torch.empty(n, dtype=torch.float32, device="cuda")
+    d = torch.empty(n, dtype=torch.uint8, device="cuda")
+    fill_frames_dev(synth.SEED_DATA, 3, t0, n, fr.data_ptr())
+    fill_meta_dev(synth.SEED_DATA, 3, t0, n, nA, 1e-3, a.data_ptr(), r.data_ptr(), d.data_ptr())
+    torch.cuda.synchronize()
+    hf = synth.frames(synth.SEED_DATA, 3, t0, n)
+    ha, hr, hd = synth.meta(synth.SEED_DATA, 3, t0, n, nA, 1e-3)
+    assert (fr.cpu().numpy() == hf).all()
+    assert (a.cpu().numpy() == ha).all() and (r.cpu().numpy() == hr).all() and (d.cpu().numpy() == hd).all()
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
+def test_replay_sample_bitexact_with_wraparound_and_terminals(math):
+    # C = 500 ring after 1337 inserts (wrapped twice), dense terminals -> many zero-padded stacks
+    def dense_terms(j, d):
+        d = d.copy()
+        d[::5] = 1
+        return d
+
+    g, orc = make_pair(nA=6, B=64, C=500, n_insert=1337, math=math, terminals=dense_terms)
+    ring = orc.learners[0].ring
+    for k in (0, 1, 7, 2 ** 33 + 5):
+        out = g.replay_sample(0, k)
+        tau = O.sample_indices(ring.n, ring.size, 64, 1507, 0, k)
+        assert (out["tau"] == tau).all()
+        s, s2, a, r, d = ring.gather(tau)
+        assert (out["s"] == s).all() and (out["s2"] == s2).all()
+        assert (out["a"] == a).all() and (out["r"] == r).all() and (out["d"] == d).all()
+    assert g.kernel_launches() > 0
+
+
+def test_replay_not_ready():
+    from paper_1507_04296_b200 import GorilaError
+    g, orc = make_pair(nA=4, B=8, C=100, n_insert=1, math="fp32")
+    with pytest.raises(GorilaError):
+        g.replay_sample(0, 0)
+    info = g.learner_step([0], 0)
+    assert info[0]["not_ready"] == 1 and info[0]["accepted"] == 0
+    ri = g.ps_apply_shard(0)
+    assert ri["n_accepted"] == 0 and ri["version_after"] == 0
+
+
+def _check_round(gpu, res, math, nA, learners):
+    tol = TOL[math]
+    G_ref = np.zeros_like(gpu["G"], dtype=np.float64)
+    for j in learners:
+        gi, oi = gpu["info"][j], res["learners"][j]
+        q, qh = gpu["q"][j]
+        assert rel_inf(q, oi["Q"]) <= tol["q"], ("Q", rel_inf(q, oi["Q"]))
+        assert rel_inf(qh, oi["Qhat"]) <= tol["q"], ("Qhat", rel_inf(qh, oi["Qhat"]))
+        assert abs(gi["loss"] - oi["loss"]) <= tol["loss"] * max(abs(oi["loss"]), 1e-12)
+        assert abs(gi["abs_loss"] - oi["abs_loss"]) <= tol["loss"] * max(abs(oi["abs_loss"]), 1e-12)
+        # decisions: stale is integer-exact; outlier is exact outside the R9 margin
+        assert bool(gi["stale"]) == bool(oi["stale"])
+        thr = oi["threshold"]
+        if oi["stats_count_before"] < 1 or abs(oi["abs_loss"] - thr) > 1e-2 * abs(thr):
+            assert bool(gi["rejected_outlier"]) == bool(oi["rejected_outlier"])
+        assert bool(gi["accepted"]) == bool(oi["accepted"])
+        assert gi["base_version"] == oi["base_version"]
+        if oi["accepted"]:
+            G_ref += oi["G"]
+    if np.any(G_ref):
+        assert rel_l2(gpu["G"], G_ref) <= tol["g"], ("G", rel_l2(gpu["G"], G_ref))
+        for name, e in per_tensor_rel_l2(gpu["G"], G_ref, nA).items():
+            assert e <= tol["g"], ("G", name, e)
+    else:
+        assert not np.any(gpu["G"])
+    assert gpu["round"]["n_accepted"] == res["n_accepted"]
+    assert gpu["round"]["version_after"] == res["version_after"] == gpu["V"]
+    assert all(bool(gpu["synced"][j]) == bool(res["synced"][j]) for j in learners)
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
+def test_learner_update_parity_c1_teacher_forced(math):
+    """C1 (BASELINE configs[0]): nA=4, B=32, 10k transitions, 1 shard, 10 RMSProp rounds, gamma=0.99."""
+    nA = 4
+    g, orc = make_pair(nA=nA, B=32, C=10_000, n_insert=10_000, math=math, target_period=5, outlier_warmup=2)
+    tol = TOL[math]
+    for k in range(10):
+        teacher_force(g, orc)
+        th_before = orc.theta.copy()
+        gpu, res = run_round_both(g, orc, k, [0])
+        _check_round(gpu, res, math, nA, [0])
+        d_gpu = gpu["theta1"].astype(np.float64) - gpu["theta0"]
+        d_ref = orc.theta - th_before
+        if np.any(d_ref):
+            assert rel_l2(d_gpu, d_ref) <= tol["dtheta"], ("dtheta", k, rel_l2(d_gpu, d_ref))
+            for name, e in per_tensor_rel_l2(d_gpu, d_ref, nA).items():
+                assert e <= tol["dtheta"], ("dtheta", k, name, e)
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
+@pytest.mark.parametrize("nA,B", [(18, 33), (1, 7), (32, 130)])
+def test_learner_update_parity_ragged_shapes(math, nA, B):
+    """Ragged batch (not a multiple of any tile), degenerate nA = 1 and the maximum nA = 32."""
+    g, orc = make_pair(nA=nA, B=B, C=3000, n_insert=3000, math=math, outlier_enabled=False)
+    teacher_force(g, orc)
+    gpu, res = run_round_both(g, orc, 0, [0])
+    _check_round(gpu, res, math, nA, [0])
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
+def test_multi_learner_staleness_outlier_and_sync(math):
+    """3 learners on one rank, fixed-staleness schedule (history 3), poison rewards, target sync."""
+    nA = 6
+
+    def terms(j, d):
+        return d
+
+    g, orc = make_pair(nA=nA, B=16, C=1500, n_insert=1500, math=math, L=3, history=3, max_staleness=4,
+                       target_period=5, outlier_warmup=3, p_poison=0.0, terminals=terms)
+    for k in range(6):
+        stal = {0: 0, 1: 2 if k == 4 else 0, 2: 1 if k % 2 else 0}
+        if k == 3:  # poison learner 2's replay: rewards 1e6 -> outlier
+            ring = orc.learners[2].ring
+            f = ring.frames.copy()
+            a, d = ring.a.copy(), ring.d.copy()
+            r = np.full_like(ring.r, 1e6)
+            g.replay_insert(2, f, a, r, d)
+            orc.insert(2, f, a, r, d)
+        gpu, res = run_round_both(g, orc, k, [0, 1, 2], staleness=stal)
+        _check_round(gpu, res, math, nA, [0, 1, 2])
+        if k == 3:
+            assert gpu["info"][2]["rejected_outlier"] == 1
+        # free-running after the common start (history of replicas must match the schedule)
+
+
+def test_no_update_invariant_gpu():
+    # zero weights, fc5 bias 1, gamma 0.75, r = 0.25 / terminal r = 1 -> delta == 0 -> theta bitwise unchanged
+    nA = 4
+    theta0 = np.zeros(O.param_count(nA), np.float32)
+    theta0[-nA:] = 1.0
+    for math in ("fp32", "bf16"):
+        from paper_1507_04296_b200 import Gorila
+        g = Gorila(n_actions=nA, batch=16, replay_capacity=300, theta0=theta0, math=math, gamma=0.75,
+                   outlier_enabled=False)
+        f = synth.frames(synth.SEED_DATA, 0, 0, 300)
+        a, _, d = synth.meta(synth.SEED_DATA, 0, 0, 300, nA)
+        d = d.copy()
+        d[::7] = 1
+        r = np.where(d == 1, 1.0, 0.25).astype(np.float32)
+        g.replay_insert(0, f, a, r, d)
+        for k in range(3):
+            info = g.learner_step([0], k)
+            assert info[0]["loss"] == 0.0 and info[0]["accepted"] == 1
+            assert not np.any(g.get_grad())
+            g.ps_apply_shard(k)
+        th, _, _, V = g.get_state()
+        assert (th == theta0).all() and V == 3
+
+
+def test_target_net_immutable_between_syncs():
+    g, orc = make_pair(nA=4, B=16, C=800, n_insert=800, math="bf16", target_period=3, outlier_enabled=False)
+    tm_prev = g.get_learner_state(0)[0]
+    for k in range(7):
+        g.learner_step([0], k)
+        g.ps_apply_shard(k)
+        synced = g.sync_target([0])[0]
+        tm = g.get_learner_state(0)[0]
+        if synced:
+            assert k in (2, 5)
+        else:
+            assert (tm == tm_prev).all()
+        tm_prev = tm
