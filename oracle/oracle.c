@@ -264,9 +264,9 @@ static void relu_store(double* z, int64_t n, int mode) {
 
 /* Forward Q(s,.;theta) for a batch of stacked frames s [B][4][84][84] (u8).
  * EXACT: x = u8/255, everything fp64. BF16: x = u8 (exact integers), conv1..fc4
- * weights rounded to bf16, conv1 pre-activation = acc * fp32(1/255) + b1, hidden
- * activations rounded to bf16 after the ReLU; fc5 weights/biases unrounded and
- * Q unrounded. acts (nullable) receives [B][a1|a2|a3|a4] (CHW per sample). */
+ * weights rounded to bf16, conv1 pre-activation = acc * fp32(1/255) + b1, the
+ * conv activations a1..a3 rounded to bf16 after the ReLU (they are tensor-core
+ * operands); a4, fc5 weights / biases and Q unrounded (fc5 runs in fp32). acts (nullable) receives [B][a1|a2|a3|a4] (CHW per sample). */
 EXPORT void orc_qnet_forward(int nA, int B, const double* theta, const uint8_t* s, int mode, double* Q,
                              double* acts) {
     double* x0 = (double*)malloc(sizeof(double) * (size_t)B * 4 * 84 * 84);
@@ -299,7 +299,8 @@ EXPORT void orc_qnet_forward(int nA, int B, const double* theta, const uint8_t* 
     relu_store(a3, (int64_t)B * L3_OUT, mode);
     /* fc4 input = a3 flattened in (C,H,W) order (reading R18) — the NCHW memory order */
     orc_linear_fwd(B, 3136, 512, a3, w4, theta + OFF_B4, a4);
-    relu_store(a4, (int64_t)B * L4_OUT, mode);
+    /* a4 feeds only the fp32 fc5 layer (not a tensor-core operand): never rounded (R16) */
+    relu_store(a4, (int64_t)B * L4_OUT, ORC_EXACT);
     orc_linear_fwd(B, 512, nA, a4, theta + OFF_W5, theta + OFF_W5 + 512 * nA, Q);
 
     if (acts)

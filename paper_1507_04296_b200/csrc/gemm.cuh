@@ -3,163 +3,242 @@
 // Every conv / FC layer of the Nature-DQN forward and backward (Eq.2)
 // is one "implicit GEMM"  C[i][j] = sum_r A(i, r) * B(j, r)  whose operands are
 // produced on the fly by a loader (im2col of an NHWC activation, a shifted output
-// gradient for dgrad, a transposed read for wgrad, or a plain row-major matrix)
-// and whose result goes through a fused epilogue (scale, bias, ReLU, ReLU-mask,
-// bf16 rounding, transposed gradient store, split-K partials).
+// gradient for dgrad, a plain row-major matrix) and whose result goes through a
+// fused epilogue (scale, bias, ReLU, ReLU-mask, bf16 rounding, transposed gradient
+// store, split-K partials).
+//
+// Loaders are either K-major (8 consecutive reduction elements of one row are
+// contiguous: forward im2col, dgrad, weights) or MN-major (8 consecutive rows at one
+// reduction index are contiguous: the weight-gradient operands, whose reduction runs
+// over batch x pixels). Both are staged with 16-byte vector loads into the matching
+// UMMA canonical (SWIZZLE_NONE) shared-memory layout.
 //
 // Two engines share the loaders / epilogues:
-//   gemm_tc   — sm_100a tensor cores: bf16 operands staged in shared memory in the
-//               UMMA canonical K-major layout, tcgen05.mma (M=128, N=BN, K=16) issued
-//               by one thread, fp32 accumulator in TMEM, tcgen05.commit -> mbarrier
-//               pipeline (2 smem stages + register prefetch), tcgen05.ld epilogue.
+//   gemm_tc   — sm_100a tensor cores: tcgen05.mma kind::f16 (M=128, N=BN, K=16) issued by
+//               one thread, fp32 accumulator in TMEM, tcgen05.commit -> mbarrier pipeline
+//               (2 smem stages + register prefetch of the next stage), tcgen05.ld epilogue.
 //   gemm_simt — fp32 FFMA tiles for the fp32 check mode (parity 1e-5).
 #pragma once
 #include "common.cuh"
+#include "layout.cuh"
 
 namespace gorila {
 
+// compile-time conv geometry (valid padding): input H x W x C, kernel K, stride S
+template <int H_, int W_, int C_, int K_, int S_, int CO_>
+struct ConvShape {
+    static constexpr int H = H_, W = W_, C = C_, K = K_, S = S_, CO = CO_;
+    static constexpr int OH = (H - K) / S + 1, OW = (W - K) / S + 1;
+    static constexpr int R = K * K * C;    // forward / wgrad reduction (ky, kx, c)
+    static constexpr int RD = K * K * CO;  // dgrad reduction (ky, kx, o)
+};
+using Conv1 = ConvShape<IMG, IMG, NSTACK, C1_K, C1_S, C1_OUT>;
+using Conv2 = ConvShape<H1, H1, C1_OUT, C2_K, C2_S, C2_OUT>;
+using Conv3 = ConvShape<H2, H2, C2_OUT, C3_K, C3_S, C3_OUT>;
+
+GORILA_DEV uint4 zero4() { return make_uint4(0, 0, 0, 0); }
+
 // ====================================================================== loaders
-// value(i, r); out of range -> 0. load8: 8 consecutive r (r0 % 8 == 0) as bf16x8.
 
 template <typename T>
-struct LdRows {  // X[i][r], row-major with leading dimension ld
+struct LdRows {  // K-major: value(i, r) = X[i][r] (row-major, leading dimension ld)
+    static constexpr bool kMN = false;
     const T* x;
     int64_t ld;
     int rows, cols;
     GORILA_DEV float load(int i, int r) const { return (i < rows && r < cols) ? tof(x[(int64_t)i * ld + r]) : 0.f; }
     GORILA_DEV uint4 load8(int i, int r0) const {
-        if (i >= rows || r0 >= cols) return make_uint4(0, 0, 0, 0);
+        if (i >= rows || r0 >= cols) return zero4();
         return *reinterpret_cast<const uint4*>(x + (int64_t)i * ld + r0);
     }
 };
 
 template <typename T>
-struct LdRowsT {  // X[r][i] read transposed: value(i, r) = X[r * ld + i]
+struct LdRowsMN {  // MN-major: value(i, r) = X[r][i]; load8(i0, r) = X[r][i0 .. i0+7]
+    static constexpr bool kMN = true;
     const T* x;
     int64_t ld;
-    int rows, cols;  // i extent, r extent
+    int rows, cols;  // i extent (multiple of 8), r extent
     GORILA_DEV float load(int i, int r) const { return (i < rows && r < cols) ? tof(x[(int64_t)r * ld + i]) : 0.f; }
-    GORILA_DEV uint4 load8(int i, int r0) const {
-        uint32_t w[4] = {0, 0, 0, 0};
-        if (i < rows) {
-            const unsigned short* p = reinterpret_cast<const unsigned short*>(x);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                int r = r0 + e;
-                uint32_t h = (r < cols) ? (uint32_t)p[(int64_t)r * ld + i] : 0u;
-                w[e >> 1] |= h << (16 * (e & 1));
-            }
-        }
-        return make_uint4(w[0], w[1], w[2], w[3]);
+    GORILA_DEV uint4 load8(int i0, int r) const {
+        if (i0 >= rows || r >= cols) return zero4();
+        return *reinterpret_cast<const uint4*>(x + (int64_t)r * ld + i0);
     }
 };
 
-// im2col of an NHWC input for a valid conv (k x k, stride s):
-// value(i = (b, oy, ox), r = (ky*k + kx)*C + c) = in[b][oy*s+ky][ox*s+kx][c]
-template <typename T>
-struct LdConvIn {
+// im2col of an NHWC input: value(m = (b, oy, ox), r = (ky*K + kx)*C + c) = in[b][oy*S+ky][ox*S+kx][c]
+template <typename SH>
+GORILA_DEV int64_t conv_in_addr(int m, int r) {
+    const int b = m / (SH::OH * SH::OW), p = m - b * (SH::OH * SH::OW);
+    const int oy = p / SH::OW, ox = p - oy * SH::OW;
+    const int ky = r / (SH::K * SH::C), rem = r - ky * (SH::K * SH::C);
+    const int kx = rem / SH::C, c = rem - kx * SH::C;
+    return (((int64_t)b * SH::H + oy * SH::S + ky) * SH::W + ox * SH::S + kx) * SH::C + c;
+}
+
+template <typename T, typename SH>
+struct LdConvIn {  // K-major forward operand (8 consecutive r = same pixel channels, or 2 pixels x 4 ch)
+    static constexpr bool kMN = false;
     const T* in;
-    int H, W, C, k, s, OH, OW, M, R;
-    GORILA_DEV int64_t addr(int i, int r) const {
-        int b = i / (OH * OW), p = i - b * (OH * OW), oy = p / OW, ox = p - oy * OW;
-        int ky = r / (k * C), rem = r - ky * (k * C), kx = rem / C, c = rem - kx * C;
-        return (((int64_t)b * H + oy * s + ky) * W + ox * s + kx) * C + c;
-    }
-    GORILA_DEV float load(int i, int r) const { return (i < M && r < R) ? tof(in[addr(i, r)]) : 0.f; }
-    GORILA_DEV uint4 load8(int i, int r0) const {  // C % 8 == 0, or C == 4 (two adjacent pixels)
-        if (i >= M || r0 >= R) return make_uint4(0, 0, 0, 0);
-        return *reinterpret_cast<const uint4*>(in + addr(i, r0));
+    int M;
+    GORILA_DEV float load(int m, int r) const { return (m < M && r < SH::R) ? tof(in[conv_in_addr<SH>(m, r)]) : 0.f; }
+    GORILA_DEV uint4 load8(int m, int r0) const {
+        if (m >= M || r0 >= SH::R) return zero4();
+        return *reinterpret_cast<const uint4*>(in + conv_in_addr<SH>(m, r0));
     }
 };
 
-// the same im2col read transposed (wgrad operand): value(i = r, red = m)
-template <typename T>
-struct LdConvInT {
-    LdConvIn<T> f;
-    GORILA_DEV float load(int i, int m) const { return f.load(m, i); }
-    GORILA_DEV uint4 load8(int i, int m0) const {
-        uint32_t w[4] = {0, 0, 0, 0};
-        if (i < f.R) {
-            const unsigned short* p = reinterpret_cast<const unsigned short*>(f.in);
-#pragma unroll
-            for (int e = 0; e < 8; ++e) {
-                int m = m0 + e;
-                uint32_t h = (m < f.M) ? (uint32_t)p[f.addr(m, i)] : 0u;
-                w[e >> 1] |= h << (16 * (e & 1));
-            }
-        }
-        return make_uint4(w[0], w[1], w[2], w[3]);
+template <typename T, typename SH>
+struct LdConvInMN {  // MN-major weight-gradient operand: value(i = r, red = m); load8(r0, m)
+    static constexpr bool kMN = true;
+    const T* in;
+    int M;
+    GORILA_DEV float load(int r, int m) const { return (m < M && r < SH::R) ? tof(in[conv_in_addr<SH>(m, r)]) : 0.f; }
+    GORILA_DEV uint4 load8(int r0, int m) const {
+        if (m >= M || r0 >= SH::R) return zero4();
+        return *reinterpret_cast<const uint4*>(in + conv_in_addr<SH>(m, r0));
     }
 };
 
-// conv dgrad operand: the output gradient g (NHWC [B][OH][OW][Co]) seen from input position
-// i = (b, y, x), r = (ky*k + kx)*Co + o:  g[b][(y-ky)/s][(x-kx)/s][o] if that position exists, else 0
-template <typename T>
+// conv dgrad operand: output gradient g (NHWC [B][OH][OW][CO]) seen from input position
+// i = (b, y, x), r = (ky*K + kx)*CO + o: g[b][(y-ky)/S][(x-kx)/S][o] if that tap exists, else 0
+template <typename SH>
+GORILA_DEV int64_t dgrad_addr(int i, int r) {
+    const int b = i / (SH::H * SH::W), p = i - b * (SH::H * SH::W);
+    const int y = p / SH::W, x = p - y * SH::W;
+    const int ky = r / (SH::K * SH::CO), rem = r - ky * (SH::K * SH::CO);
+    const int kx = rem / SH::CO, o = rem - kx * SH::CO;
+    const int ty = y - ky, tx = x - kx;
+    if (ty < 0 || tx < 0 || ty % SH::S || tx % SH::S) return -1;
+    const int oy = ty / SH::S, ox = tx / SH::S;
+    if (oy >= SH::OH || ox >= SH::OW) return -1;
+    return (((int64_t)b * SH::OH + oy) * SH::OW + ox) * SH::CO + o;
+}
+
+template <typename T, typename SH>
 struct LdDgrad {
+    static constexpr bool kMN = false;
     const T* g;
-    int H, W, Co, k, s, OH, OW, M, R;
-    GORILA_DEV int64_t addr(int i, int r) const {  // -1 if the tap does not exist
-        int b = i / (H * W), p = i - b * (H * W), y = p / W, x = p - y * W;
-        int ky = r / (k * Co), rem = r - ky * (k * Co), kx = rem / Co, o = rem - kx * Co;
-        int ty = y - ky, tx = x - kx;
-        if (ty < 0 || tx < 0 || ty % s || tx % s) return -1;
-        int oy = ty / s, ox = tx / s;
-        if (oy >= OH || ox >= OW) return -1;
-        return (((int64_t)b * OH + oy) * OW + ox) * Co + o;
-    }
+    int M;  // B * H * W
     GORILA_DEV float load(int i, int r) const {
-        if (i >= M || r >= R) return 0.f;
-        int64_t a = addr(i, r);
+        if (i >= M || r >= SH::RD) return 0.f;
+        const int64_t a = dgrad_addr<SH>(i, r);
         return a < 0 ? 0.f : tof(g[a]);
     }
     GORILA_DEV uint4 load8(int i, int r0) const {
-        if (i >= M || r0 >= R) return make_uint4(0, 0, 0, 0);
-        int64_t a = addr(i, r0);
-        return a < 0 ? make_uint4(0, 0, 0, 0) : *reinterpret_cast<const uint4*>(g + a);
+        if (i >= M || r0 >= SH::RD) return zero4();
+        const int64_t a = dgrad_addr<SH>(i, r0);
+        return a < 0 ? zero4() : *reinterpret_cast<const uint4*>(g + a);
     }
 };
 
 // ====================================================================== epilogues
-// apply(i, j, v, split): v = fp32 accumulator of C[i][j] (of split `split`).
+// apply1(i, j, v, split): scalar; apply16(i, j0, v[16], split): 16 consecutive columns.
 
 template <typename T>
-struct EpAct {  // out[i][j] = round_T(act(v * scale + bias[j]))
+GORILA_DEV void store16(T* dst, const float* v) {  // 16 values, 16-B aligned destination
+    if constexpr (sizeof(T) == 2) {
+        uint32_t w[8];
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
+            w[e] = *reinterpret_cast<uint32_t*>(&h);
+        }
+        reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+        reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+    } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e)
+            reinterpret_cast<float4*>(dst)[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
+    }
+}
+template <typename T>
+GORILA_DEV void load16(const T* src, float* v) {
+    if constexpr (sizeof(T) == 2) {
+        const uint4 a = reinterpret_cast<const uint4*>(src)[0], b = reinterpret_cast<const uint4*>(src)[1];
+        const uint32_t w[8] = {a.x, a.y, a.z, a.w, b.x, b.y, b.z, b.w};
+#pragma unroll
+        for (int e = 0; e < 8; ++e) {
+            __nv_bfloat162 h = *reinterpret_cast<const __nv_bfloat162*>(&w[e]);
+            float2 f = __bfloat1622float2(h);
+            v[2 * e] = f.x;
+            v[2 * e + 1] = f.y;
+        }
+    } else {
+#pragma unroll
+        for (int e = 0; e < 4; ++e) {
+            float4 f = reinterpret_cast<const float4*>(src)[e];
+            v[4 * e] = f.x; v[4 * e + 1] = f.y; v[4 * e + 2] = f.z; v[4 * e + 3] = f.w;
+        }
+    }
+}
+
+template <typename T>
+struct EpAct {  // out[i][j] = round_T(act(v * scale + bias[j]))   (ld % 8 == 0)
     T* out;
     int64_t ld;
     const float* bias;
     float scale;
     int M, N, relu;
-    GORILA_DEV void apply(int i, int j, float v, int) const {
-        if (i >= M || j >= N) return;
+    GORILA_DEV float f(float v, int j) const {
         float z = v * scale + bias[j];
-        if (relu) z = fmaxf(z, 0.f);
-        out[(int64_t)i * ld + j] = fromf<T>(z);
+        return relu ? fmaxf(z, 0.f) : z;
+    }
+    GORILA_DEV void apply1(int i, int j, float v, int) const {
+        if (i < M && j < N) out[(int64_t)i * ld + j] = fromf<T>(f(v, j));
+    }
+    GORILA_DEV void apply16(int i, int j0, const float* v, int s) const {
+        if (i >= M) return;
+        if (j0 + 16 <= N) {
+            float o[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) o[e] = f(v[e], j0 + e);
+            store16<T>(out + (int64_t)i * ld + j0, o);
+        } else {
+            for (int e = 0; e < 16; ++e) apply1(i, j0 + e, v[e], s);
+        }
     }
 };
 
 template <typename T>
-struct EpMask {  // out[i][j] = round_T(v * 1[act[i][j] > 0])  (ReLU' with ReLU'(0) = 0, reading R19)
+struct EpMask {  // out[i][j] = round_T(v * 1[act[i][j] > 0])  (ReLU'(0) = 0, reading R19; ld % 8 == 0)
     T* out;
     const T* act;
     int64_t ld;
     int M, N;
-    GORILA_DEV void apply(int i, int j, float v, int) const {
+    GORILA_DEV void apply1(int i, int j, float v, int) const {
         if (i >= M || j >= N) return;
-        int64_t a = (int64_t)i * ld + j;
+        const int64_t a = (int64_t)i * ld + j;
         out[a] = fromf<T>(tof(act[a]) > 0.f ? v : 0.f);
+    }
+    GORILA_DEV void apply16(int i, int j0, const float* v, int s) const {
+        if (i >= M) return;
+        if (j0 + 16 <= N) {
+            float h[16], o[16];
+            load16<T>(act + (int64_t)i * ld + j0, h);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) o[e] = h[e] > 0.f ? v[e] : 0.f;
+            store16<T>(out + (int64_t)i * ld + j0, o);
+        } else {
+            for (int e = 0; e < 16; ++e) apply1(i, j0 + e, v[e], s);
+        }
     }
 };
 
 template <typename T>
-struct EpMaskT {  // transposed: out[j][i] = round_T(v * 1[act[j][i] > 0])
+struct EpMaskT {  // transposed: out[j][i] = round_T(v * 1[act[j][i] > 0])  (coalesced across the warp's rows)
     T* out;
     const T* act;
     int64_t ld;
     int M, N;
-    GORILA_DEV void apply(int i, int j, float v, int) const {
+    GORILA_DEV void apply1(int i, int j, float v, int) const {
         if (i >= M || j >= N) return;
-        int64_t a = (int64_t)j * ld + i;
+        const int64_t a = (int64_t)j * ld + i;
         out[a] = fromf<T>(tof(act[a]) > 0.f ? v : 0.f);
+    }
+    GORILA_DEV void apply16(int i, int j0, const float* v, int s) const {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) apply1(i, j0 + e, v[e], s);
     }
 };
 
@@ -168,9 +247,12 @@ struct EpStoreT {  // dst[split][j][i] = v * scale (transposed fp32 store: weigh
     int64_t ld, split_stride;
     float scale;
     int M, N;
-    GORILA_DEV void apply(int i, int j, float v, int split) const {
-        if (i >= M || j >= N) return;
-        dst[split * split_stride + (int64_t)j * ld + i] = v * scale;
+    GORILA_DEV void apply1(int i, int j, float v, int split) const {
+        if (i < M && j < N) dst[split * split_stride + (int64_t)j * ld + i] = v * scale;
+    }
+    GORILA_DEV void apply16(int i, int j0, const float* v, int s) const {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) apply1(i, j0 + e, v[e], s);
     }
 };
 
@@ -178,9 +260,28 @@ struct EpStore {  // dst[split][i][j] = v (fp32 split-K partials)
     float* dst;
     int64_t ld, split_stride;
     int M, N;
-    GORILA_DEV void apply(int i, int j, float v, int split) const {
-        if (i >= M || j >= N) return;
-        dst[split * split_stride + (int64_t)i * ld + j] = v;
+    GORILA_DEV void apply1(int i, int j, float v, int split) const {
+        if (i < M && j < N) dst[split * split_stride + (int64_t)i * ld + j] = v;
+    }
+    GORILA_DEV void apply16(int i, int j0, const float* v, int s) const {
+        if (i < M && j0 + 16 <= N && (ld & 3) == 0) {
+            store16<float>(dst + s * split_stride + (int64_t)i * ld + j0, v);
+        } else {
+            for (int e = 0; e < 16; ++e) apply1(i, j0 + e, v[e], s);
+        }
+    }
+};
+
+struct EpAddT {  // G[off + j*ld + i] += v (fp32, transposed, coalesced across the warp's rows)
+    float* G;
+    int64_t ld;
+    int M, N;
+    GORILA_DEV void apply1(int i, int j, float v, int) const {
+        if (i < M && j < N) G[(int64_t)j * ld + i] += v;
+    }
+    GORILA_DEV void apply16(int i, int j0, const float* v, int s) const {
+#pragma unroll
+        for (int e = 0; e < 16; ++e) apply1(i, j0 + e, v[e], s);
     }
 };
 
@@ -195,8 +296,8 @@ struct GemmProb {
 template <typename LA, typename LB, typename EP>
 struct GemmBatch {
     GemmProb<LA, LB, EP> prob[2];
-    int M, N, R;   // shared by all problems of the batch
-    int splits;    // split of the reduction range
+    int M, N, R;           // shared by all problems of the batch
+    int splits;            // split of the reduction range
     int chunks_per_split;  // in units of 64 (tc) / 16 (simt) reduction elements
 };
 
@@ -208,18 +309,65 @@ __host__ __device__ constexpr uint32_t tmem_cols_for(int bn) {
 }
 __host__ __device__ constexpr int tc_smem_bytes(int bn) { return 2 * (TC_BM * TC_BK * 2 + bn * TC_BK * 2) + 64; }
 
-// canonical K-major no-swizzle offset of (row, 16-byte k-chunk) inside a [rows][64] bf16 tile
-GORILA_DEV uint32_t tc_off(int row, int kch) { return (uint32_t)((row >> 3) * 1024 + kch * 128 + (row & 7) * 16); }
+// Stage one operand tile (ROWS x 64 reduction elements, bf16) in the canonical layout.
+// K-major : core matrix (8 rows x 16 B) at (row/8, kchunk): offset (row/8)*1024 + kch*128 + (row%8)*16
+//           -> descriptor LBO = 128 (K step), SBO = 1024 (8-row step); MMA kk starts at +kk*256.
+// MN-major: core matrix (8 k x 16 B = 8 rows) at (k/8, row/8): offset (k/8)*ROWS*16 + (row/8)*128 + (k%8)*16
+//           -> descriptor LBO = ROWS*16 (K step), SBO = 128 (8-row step); MMA kk starts at +kk*2*ROWS*16.
+template <int ROWS, bool MN>
+struct Stage {
+    static constexpr int ITERS = ROWS * 8 / TC_THREADS;  // 16-B chunks per thread
+    GORILA_DEV static void coords(int idx, int& row, int& k) {
+        if constexpr (!MN) {
+            row = (idx >> 6) * 8 + (idx & 7);
+            k = ((idx >> 3) & 7) * 8;  // first reduction element of the chunk
+        } else {
+            constexpr int G = ROWS / 8;
+            const int g = (idx >> 3) % G, khi = (idx >> 3) / G;
+            row = g * 8;
+            k = khi * 8 + (idx & 7);
+        }
+    }
+    GORILA_DEV static uint32_t offset(int idx) {
+        if constexpr (!MN) {
+            const int row = (idx >> 6) * 8 + (idx & 7), kch = (idx >> 3) & 7;
+            return (uint32_t)((row >> 3) * 1024 + kch * 128 + (row & 7) * 16);
+        } else {
+            constexpr int G = ROWS / 8;
+            const int g = (idx >> 3) % G, khi = (idx >> 3) / G;
+            return (uint32_t)(khi * ROWS * 16 + g * 128 + (idx & 7) * 16);
+        }
+    }
+    GORILA_DEV static uint64_t desc(uint32_t base, int kk) {
+        if constexpr (!MN) return umma_desc(base + kk * 256, 128, 1024);
+        else return umma_desc(base + kk * 2 * ROWS * 16, ROWS * 16, 128);
+    }
+    template <typename LD>
+    GORILA_DEV static void load(const LD& ld, int row0, int r0, uint4* regs) {
+#pragma unroll
+        for (int q = 0; q < ITERS; ++q) {
+            int row, k;
+            coords(threadIdx.x + TC_THREADS * q, row, k);
+            regs[q] = ld.load8(row0 + row, r0 + k);
+        }
+    }
+    GORILA_DEV static void store(uint8_t* st, const uint4* regs) {
+#pragma unroll
+        for (int q = 0; q < ITERS; ++q)
+            *reinterpret_cast<uint4*>(st + offset(threadIdx.x + TC_THREADS * q)) = regs[q];
+    }
+};
 
 template <int BN, typename LA, typename LB, typename EP>
 __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ GemmBatch<LA, LB, EP> p) {
     constexpr int A_BYTES = TC_BM * TC_BK * 2, B_BYTES = BN * TC_BK * 2;
-    constexpr int A_ITERS = TC_BM * 8 / TC_THREADS, B_ITERS = BN * 8 / TC_THREADS;
     static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
     static_assert((BN * 8) % TC_THREADS == 0, "B tile split");
+    using SA = Stage<TC_BM, LA::kMN>;
+    using SB = Stage<BN, LB::kMN>;
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* sA = smem;                        // [2][A_BYTES]
-    uint8_t* sB = smem + 2 * A_BYTES;          // [2][B_BYTES]
+    uint8_t* sA = smem;                // [2][A_BYTES]
+    uint8_t* sB = smem + 2 * A_BYTES;  // [2][B_BYTES]
     uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 2 * (A_BYTES + B_BYTES));
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
 
@@ -229,8 +377,7 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
     const int i0 = blockIdx.x * TC_BM, j0 = blockIdx.y * BN;
     const int n_chunks_total = (p.R + TC_BK - 1) / TC_BK;
     const int kc_begin = split * p.chunks_per_split;
-    const int kc_end = min(n_chunks_total, kc_begin + p.chunks_per_split);
-    const int nK = max(0, kc_end - kc_begin);
+    const int nK = max(0, min(n_chunks_total, kc_begin + p.chunks_per_split) - kc_begin);
 
     if (warp == 0) tmem_alloc(tmem_slot, tmem_cols_for(BN));
     if (tid == 0) {
@@ -242,57 +389,35 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
     __syncthreads();
     tc_fence_after();
     const uint32_t tmem = *tmem_slot;
-    constexpr uint32_t IDESC = umma_idesc_bf16(TC_BM, BN);
+    constexpr uint32_t IDESC =
+        umma_idesc_bf16(TC_BM, BN) | (LA::kMN ? (1u << 15) : 0u) | (LB::kMN ? (1u << 16) : 0u);
 
-    uint4 ra[A_ITERS], rb[B_ITERS];
-    auto load_regs = [&](int kc) {
-        const int r0 = (kc_begin + kc) * TC_BK;
-#pragma unroll
-        for (int q = 0; q < A_ITERS; ++q) {
-            int idx = tid + TC_THREADS * q;
-            int row = (idx >> 6) * 8 + (idx & 7), kch = (idx >> 3) & 7;
-            ra[q] = P.a.load8(i0 + row, r0 + kch * 8);
-        }
-#pragma unroll
-        for (int q = 0; q < B_ITERS; ++q) {
-            int idx = tid + TC_THREADS * q;
-            int row = (idx >> 6) * 8 + (idx & 7), kch = (idx >> 3) & 7;
-            rb[q] = P.b.load8(j0 + row, r0 + kch * 8);
-        }
-    };
-
-    if (nK > 0) load_regs(0);
+    uint4 ra[SA::ITERS], rb[SB::ITERS];
+    if (nK > 0) {
+        SA::load(P.a, i0, kc_begin * TC_BK, ra);
+        SB::load(P.b, j0, kc_begin * TC_BK, rb);
+    }
     for (int kc = 0; kc < nK; ++kc) {
         const int s = kc & 1;
         if (kc >= 2) mbar_wait(&mbar[s], ((kc - 2) >> 1) & 1);  // MMAs of chunk kc-2 released stage s
         uint8_t* a_st = sA + s * A_BYTES;
         uint8_t* b_st = sB + s * B_BYTES;
-#pragma unroll
-        for (int q = 0; q < A_ITERS; ++q) {
-            int idx = tid + TC_THREADS * q;
-            int row = (idx >> 6) * 8 + (idx & 7), kch = (idx >> 3) & 7;
-            *reinterpret_cast<uint4*>(a_st + tc_off(row, kch)) = ra[q];
-        }
-#pragma unroll
-        for (int q = 0; q < B_ITERS; ++q) {
-            int idx = tid + TC_THREADS * q;
-            int row = (idx >> 6) * 8 + (idx & 7), kch = (idx >> 3) & 7;
-            *reinterpret_cast<uint4*>(b_st + tc_off(row, kch)) = rb[q];
-        }
+        SA::store(a_st, ra);
+        SB::store(b_st, rb);
         fence_proxy_async_smem();
         __syncthreads();
         if (tid == 0) {
             tc_fence_after();
             const uint32_t a_base = smem_u32(a_st), b_base = smem_u32(b_st);
 #pragma unroll
-            for (int kk = 0; kk < TC_BK / 16; ++kk) {
-                uint64_t ad = umma_desc(a_base + kk * 256, 128, 1024);
-                uint64_t bd = umma_desc(b_base + kk * 256, 128, 1024);
-                umma_bf16(tmem, ad, bd, IDESC, (kc > 0 || kk > 0) ? 1u : 0u);
-            }
+            for (int kk = 0; kk < TC_BK / 16; ++kk)
+                umma_bf16(tmem, SA::desc(a_base, kk), SB::desc(b_base, kk), IDESC, (kc > 0 || kk > 0) ? 1u : 0u);
             umma_commit(&mbar[s]);
         }
-        if (kc + 1 < nK) load_regs(kc + 1);
+        if (kc + 1 < nK) {
+            SA::load(P.a, i0, (kc_begin + kc + 1) * TC_BK, ra);
+            SB::load(P.b, j0, (kc_begin + kc + 1) * TC_BK, rb);
+        }
     }
     if (nK > 0) {
         const int last = nK - 1;
@@ -301,7 +426,7 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
     }
     tc_fence_after();
 
-    // epilogue: warp w owns TMEM lanes (= rows) 32w .. 32w+31
+    // epilogue: warp w owns TMEM lanes (= tile rows) 32w .. 32w+31
     const int row = i0 + warp * 32 + lane;
 #pragma unroll 1
     for (int c0 = 0; c0 < BN; c0 += 16) {
@@ -312,8 +437,7 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
 #pragma unroll
             for (int e = 0; e < 16; ++e) v[e] = 0.f;
         }
-#pragma unroll
-        for (int e = 0; e < 16; ++e) P.ep.apply(row, j0 + c0 + e, v[e], split);
+        if (j0 + c0 < p.N) P.ep.apply16(row, j0 + c0, v, split);
     }
     tc_fence_before();
     __syncthreads();
@@ -338,9 +462,9 @@ __global__ void __launch_bounds__(256) gemm_simt(const __grid_constant__ GemmBat
     for (int r0 = r_begin; r0 < r_end; r0 += SM_BR) {
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            int idx = tid + 256 * q;
-            int ii = idx & 63, rr = idx >> 6;
-            int r = r0 + rr;
+            const int idx = tid + 256 * q;
+            const int ii = idx & 63, rr = idx >> 6;
+            const int r = r0 + rr;
             As[rr][ii] = (r < r_end) ? P.a.load(i0 + ii, r) : 0.f;
             Bs[rr][ii] = (r < r_end) ? P.b.load(j0 + ii, r) : 0.f;
         }
@@ -363,7 +487,7 @@ __global__ void __launch_bounds__(256) gemm_simt(const __grid_constant__ GemmBat
 #pragma unroll
     for (int x = 0; x < 4; ++x)
 #pragma unroll
-        for (int y = 0; y < 4; ++y) P.ep.apply(i0 + ti + 16 * x, j0 + tj + 16 * y, acc[x][y], split);
+        for (int y = 0; y < 4; ++y) P.ep.apply1(i0 + ti + 16 * x, j0 + tj + 16 * y, acc[x][y], split);
 }
 
 }  // namespace gorila

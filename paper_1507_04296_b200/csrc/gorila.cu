@@ -91,14 +91,15 @@ struct gorila_ctx {
     bool poisoned = false;
     uint64_t launches = 0;
     int nA, B, L, W, rank;
-    int64_t P, q, per;  // params, real elements per slice, slice stride
+    int64_t P, q;       // params, elements per shard slice (P padded to W*q)
     size_t esz;         // sizeof(T)
     ReplicaLayout rl_full, rl_fwd;
     // PS state
-    float* theta;   // [W*per] full theta^+ (sliced)
-    float* m;       // [per] own slice
+    float* theta;   // [W*q] full theta^+ (internal layout, contiguous shard slices)
+    float* m;       // [q] own slice
     float* v;
-    float* G;       // [W*per] gradient (sliced)
+    float* G;       // [W*q] gradient
+    float* counts;  // [W] accepted-gradient counts (reduce-scattered with G)
     uint64_t* V;
     uint64_t* round_info;  // [3]
     uint32_t* n_acc_local;
@@ -110,7 +111,8 @@ struct gorila_ctx {
     // learners
     std::vector<Learner> learners;
     // per-step scratch (shared by the local learners)
-    void *s, *s2, *a1, *a2, *a3, *a4, *t1, *t2, *t3, *t4, *g1, *g2, *g3, *g4;
+    void *s, *s2, *a1, *a2, *a3, *t1, *t2, *t3, *g1, *g2, *g3, *g4;
+    float *a4, *t4;  // fp32 (fc5 runs in fp32)
     uint8_t *sa, *sd;
     float* sr;
     int64_t* sidx;
@@ -120,7 +122,7 @@ struct gorila_ctx {
     int split_w[3];
     int split_fc4;
     float* tmp_canon;  // [P]
-    float* tmp_int;    // [W*per]
+    float* tmp_int;    // [W*q]
     ncclComm_t comm = nullptr;
     // per-phase profiling (gorila_profile_*)
     bool prof = false;
@@ -242,8 +244,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
     const ReplicaLayout& RT = ctx->rl_fwd;
 
     T *s = P_<T>(ctx->s), *s2 = P_<T>(ctx->s2);
-    T *a1 = P_<T>(ctx->a1), *a2 = P_<T>(ctx->a2), *a3 = P_<T>(ctx->a3), *a4 = P_<T>(ctx->a4);
-    T *t1 = P_<T>(ctx->t1), *t2 = P_<T>(ctx->t2), *t3 = P_<T>(ctx->t3), *t4 = P_<T>(ctx->t4);
+    T *a1 = P_<T>(ctx->a1), *a2 = P_<T>(ctx->a2), *a3 = P_<T>(ctx->a3);
+    T *t1 = P_<T>(ctx->t1), *t2 = P_<T>(ctx->t2), *t3 = P_<T>(ctx->t3);
+    float *a4 = ctx->a4, *t4 = ctx->t4;
     T *g1 = P_<T>(ctx->g1), *g2 = P_<T>(ctx->g2), *g3 = P_<T>(ctx->g3), *g4 = P_<T>(ctx->g4);
 
     // K1: sample + gather + stack (Alg.1)
@@ -259,37 +262,31 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
     const float in_scale = 1.0f / 255.0f;  // reading R17 (fp32 constant, folded into conv1's epilogue)
     // conv1 fwd (online on s with theta, target on s' with theta^-)
     {
-        using LA = LdConvIn<T>; using LB = LdRows<T>; using EP = EpAct<T>;
+        using LA = LdConvIn<T, Conv1>; using LB = LdRows<T>; using EP = EpAct<T>;
         const int M = B * H1 * H1;
         GemmProb<LA, LB, EP> pr[2] = {
-            {{s, IMG, IMG, NSTACK, C1_K, C1_S, H1, H1, M, K1}, {rt + RL.w1, K1, C1_OUT, K1},
-             {a1, C1_OUT, rf + RL.b1, in_scale, M, C1_OUT, 1}},
-            {{s2, IMG, IMG, NSTACK, C1_K, C1_S, H1, H1, M, K1}, {tt + RT.w1, K1, C1_OUT, K1},
-             {t1, C1_OUT, tf + RT.b1, in_scale, M, C1_OUT, 1}}};
+            {{s, M}, {rt + RL.w1, K1, C1_OUT, K1}, {a1, C1_OUT, rf + RL.b1, in_scale, M, C1_OUT, 1}},
+            {{s2, M}, {tt + RT.w1, K1, C1_OUT, K1}, {t1, C1_OUT, tf + RT.b1, in_scale, M, C1_OUT, 1}}};
         gemm<T, 32>(ctx, pr, 2, M, C1_OUT, K1, 1);
     }
     mark(ctx, PH_CONV1F);
     // conv2 fwd
     {
-        using LA = LdConvIn<T>; using LB = LdRows<T>; using EP = EpAct<T>;
+        using LA = LdConvIn<T, Conv2>; using LB = LdRows<T>; using EP = EpAct<T>;
         const int M = B * H2 * H2;
         GemmProb<LA, LB, EP> pr[2] = {
-            {{a1, H1, H1, C1_OUT, C2_K, C2_S, H2, H2, M, K2}, {rt + RL.w2, K2, C2_OUT, K2},
-             {a2, C2_OUT, rf + RL.b2, 1.f, M, C2_OUT, 1}},
-            {{t1, H1, H1, C1_OUT, C2_K, C2_S, H2, H2, M, K2}, {tt + RT.w2, K2, C2_OUT, K2},
-             {t2, C2_OUT, tf + RT.b2, 1.f, M, C2_OUT, 1}}};
+            {{a1, M}, {rt + RL.w2, K2, C2_OUT, K2}, {a2, C2_OUT, rf + RL.b2, 1.f, M, C2_OUT, 1}},
+            {{t1, M}, {tt + RT.w2, K2, C2_OUT, K2}, {t2, C2_OUT, tf + RT.b2, 1.f, M, C2_OUT, 1}}};
         gemm<T, 64>(ctx, pr, 2, M, C2_OUT, K2, 1);
     }
     mark(ctx, PH_CONV2F);
     // conv3 fwd
     {
-        using LA = LdConvIn<T>; using LB = LdRows<T>; using EP = EpAct<T>;
+        using LA = LdConvIn<T, Conv3>; using LB = LdRows<T>; using EP = EpAct<T>;
         const int M = B * H3 * H3;
         GemmProb<LA, LB, EP> pr[2] = {
-            {{a2, H2, H2, C2_OUT, C3_K, C3_S, H3, H3, M, K3}, {rt + RL.w3, K3, C3_OUT, K3},
-             {a3, C3_OUT, rf + RL.b3, 1.f, M, C3_OUT, 1}},
-            {{t2, H2, H2, C2_OUT, C3_K, C3_S, H3, H3, M, K3}, {tt + RT.w3, K3, C3_OUT, K3},
-             {t3, C3_OUT, tf + RT.b3, 1.f, M, C3_OUT, 1}}};
+            {{a2, M}, {rt + RL.w3, K3, C3_OUT, K3}, {a3, C3_OUT, rf + RL.b3, 1.f, M, C3_OUT, 1}},
+            {{t2, M}, {tt + RT.w3, K3, C3_OUT, K3}, {t3, C3_OUT, tf + RT.b3, 1.f, M, C3_OUT, 1}}};
         gemm<T, 64>(ctx, pr, 2, M, C3_OUT, K3, 1);
     }
     mark(ctx, PH_CONV3F);
@@ -307,12 +304,12 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
         DISPATCH_BN_BATCH(B, FC4F);
 #undef FC4F
         dim3 grid((B * FC4_OUT + 255) / 256, 2);
-        k_fc4_finalize<T><<<grid, 256, 0, st>>>(ctx->part_fc4, S, pstride, B, rf + RL.b4, tf + RT.b4, a4, t4);
+        k_fc4_finalize<<<grid, 256, 0, st>>>(ctx->part_fc4, S, pstride, B, rf + RL.b4, tf + RT.b4, a4, t4);
         LAUNCHED();
     }
     mark(ctx, PH_FC4F);
     // fc5 fwd (both nets)
-    k_fc5_fwd<T><<<dim3(B, 2), 256, 0, st>>>(a4, t4, rf + RL.w5, tf + RT.w5, rf + RL.b5, tf + RT.b5, Lr.Q, Lr.Qhat, nA);
+    k_fc5_fwd<<<dim3(B, 2), 256, 0, st>>>(a4, t4, rf + RL.w5, tf + RT.w5, rf + RL.b5, tf + RT.b5, Lr.Q, Lr.Qhat, nA);
     LAUNCHED();
     mark(ctx, PH_FC5F);
     // K7: TD target, clipped error, loss, outlier + stale decisions
@@ -328,7 +325,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
     }
     mark(ctx, PH_TD);
     // fc5 bwd: dW5, db5 into G; g4 = mask(dQ W5)
-    k_fc5_bwd<T><<<148, 256, 0, st>>>(ctx->dQ, a4, rf + RL.w5, B, nA, ctx->G, ctx->q, ctx->per, g4);
+    k_fc5_bwd<T><<<148, 256, 0, st>>>(ctx->dQ, a4, rf + RL.w5, B, nA, ctx->G, g4);
     LAUNCHED();
     mark(ctx, PH_FC5B);
     // fc4 dgrad (i = k, j = b, red = n): g3[b][k] = mask(sum_n W4[n][k] g4[b][n])
@@ -343,62 +340,59 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
     mark(ctx, PH_FC4DG);
     // fc4 wgrad (i = k, j = n, red = b): G[W4][n][k] += sum_b a3[b][k] g4[b][n]
     {
-        using LA = LdRowsT<T>; using LB = LdRowsT<T>; using EP = EpAddW4;
+        using LA = LdRowsMN<T>; using LB = LdRowsMN<T>; using EP = EpAddT;
         GemmProb<LA, LB, EP> pr[1] = {{{a3, FC4_IN, FC4_IN, B}, {g4, FC4_OUT, FC4_OUT, B},
-                                       {ctx->G, ctx->q, ctx->per, FC4_IN, FC4_OUT}}};
+                                       {ctx->G + OFF_W4, FC4_IN, FC4_IN, FC4_OUT}}};
         gemm<T, 256>(ctx, pr, 1, FC4_IN, FC4_OUT, B, 1);
     }
     mark(ctx, PH_FC4WG);
     // conv3 dgrad: g2 = mask(conv3^T(g3))
     {
-        using LA = LdDgrad<T>; using LB = LdRows<T>; using EP = EpMask<T>;
+        using LA = LdDgrad<T, Conv3>; using LB = LdRows<T>; using EP = EpMask<T>;
         const int M = B * H2 * H2;
-        GemmProb<LA, LB, EP> pr[1] = {{{g3, H2, H2, C3_OUT, C3_K, C3_S, H3, H3, M, K3},
-                                       {rt + RL.w3d, K3, C2_OUT, K3}, {g2, a2, C2_OUT, M, C2_OUT}}};
+        GemmProb<LA, LB, EP> pr[1] = {{{g3, M}, {rt + RL.w3d, Conv3::RD, C2_OUT, Conv3::RD},
+                                       {g2, a2, C2_OUT, M, C2_OUT}}};
         gemm<T, 64>(ctx, pr, 1, M, C2_OUT, K3, 1);
     }
     mark(ctx, PH_CONV3DG);
     // conv3 wgrad (i = r, j = o, red = m): partial[s][o][r]
     {
-        using LA = LdConvInT<T>; using LB = LdRowsT<T>; using EP = EpStoreT;
+        using LA = LdConvInMN<T, Conv3>; using LB = LdRowsMN<T>; using EP = EpStoreT;
         const int Mred = B * H3 * H3;
-        GemmProb<LA, LB, EP> pr[1] = {{{{a2, H2, H2, C2_OUT, C3_K, C3_S, H3, H3, Mred, K3}},
-                                       {g3, C3_OUT, C3_OUT, Mred},
+        GemmProb<LA, LB, EP> pr[1] = {{{a2, Mred}, {g3, C3_OUT, C3_OUT, Mred},
                                        {ctx->part_w[2], K3, (int64_t)C3_OUT * K3, 1.f, K3, C3_OUT}}};
         gemm<T, 64>(ctx, pr, 1, K3, C3_OUT, Mred, ctx->split_w[2]);
     }
     mark(ctx, PH_CONV3WG);
     // conv2 dgrad: g1 = mask(conv2^T(g2))
     {
-        using LA = LdDgrad<T>; using LB = LdRows<T>; using EP = EpMask<T>;
+        using LA = LdDgrad<T, Conv2>; using LB = LdRows<T>; using EP = EpMask<T>;
         const int M = B * H1 * H1;
-        GemmProb<LA, LB, EP> pr[1] = {{{g2, H1, H1, C2_OUT, C2_K, C2_S, H2, H2, M, C2_K * C2_K * C2_OUT},
-                                       {rt + RL.w2d, K2 * 2, C1_OUT, K2 * 2}, {g1, a1, C1_OUT, M, C1_OUT}}};
-        gemm<T, 32>(ctx, pr, 1, M, C1_OUT, C2_K * C2_K * C2_OUT, 1);
+        GemmProb<LA, LB, EP> pr[1] = {{{g2, M}, {rt + RL.w2d, Conv2::RD, C1_OUT, Conv2::RD},
+                                       {g1, a1, C1_OUT, M, C1_OUT}}};
+        gemm<T, 32>(ctx, pr, 1, M, C1_OUT, Conv2::RD, 1);
     }
     mark(ctx, PH_CONV2DG);
     // conv2 wgrad
     {
-        using LA = LdConvInT<T>; using LB = LdRowsT<T>; using EP = EpStoreT;
+        using LA = LdConvInMN<T, Conv2>; using LB = LdRowsMN<T>; using EP = EpStoreT;
         const int Mred = B * H2 * H2;
-        GemmProb<LA, LB, EP> pr[1] = {{{{a1, H1, H1, C1_OUT, C2_K, C2_S, H2, H2, Mred, K2}},
-                                       {g2, C2_OUT, C2_OUT, Mred},
+        GemmProb<LA, LB, EP> pr[1] = {{{a1, Mred}, {g2, C2_OUT, C2_OUT, Mred},
                                        {ctx->part_w[1], K2, (int64_t)C2_OUT * K2, 1.f, K2, C2_OUT}}};
         gemm<T, 64>(ctx, pr, 1, K2, C2_OUT, Mred, ctx->split_w[1]);
     }
     mark(ctx, PH_CONV2WG);
     // conv1 wgrad (input scale 1/255 folded into the store)
     {
-        using LA = LdConvInT<T>; using LB = LdRowsT<T>; using EP = EpStoreT;
+        using LA = LdConvInMN<T, Conv1>; using LB = LdRowsMN<T>; using EP = EpStoreT;
         const int Mred = B * H1 * H1;
-        GemmProb<LA, LB, EP> pr[1] = {{{{s, IMG, IMG, NSTACK, C1_K, C1_S, H1, H1, Mred, K1}},
-                                       {g1, C1_OUT, C1_OUT, Mred},
+        GemmProb<LA, LB, EP> pr[1] = {{{s, Mred}, {g1, C1_OUT, C1_OUT, Mred},
                                        {ctx->part_w[0], K1, (int64_t)C1_OUT * K1, in_scale, K1, C1_OUT}}};
         gemm<T, 32>(ctx, pr, 1, K1, C1_OUT, Mred, ctx->split_w[0]);
     }
     mark(ctx, PH_CONV1WG);
     // bias gradients b1..b4
-    k_bias_grad<T><<<C1_OUT + C2_OUT + C3_OUT + FC4_OUT, 256, 0, st>>>(g1, g2, g3, g4, B, ctx->G, ctx->q, ctx->per);
+    k_bias_grad<T><<<C1_OUT + C2_OUT + C3_OUT + FC4_OUT, 256, 0, st>>>(g1, g2, g3, g4, B, ctx->G);
     LAUNCHED();
     mark(ctx, PH_BIASG);
     // K10: fixed-order reduction of the conv wgrad partials into G
@@ -410,7 +404,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
         p.splits[2] = eff_splits(fp32, B * H3 * H3, ctx->split_w[2]);
         p.count[0] = (int64_t)C1_OUT * K1; p.count[1] = (int64_t)C2_OUT * K2; p.count[2] = (int64_t)C3_OUT * K3;
         p.off[0] = OFF_W1; p.off[1] = OFF_W2; p.off[2] = OFF_W3;
-        k_wgrad_reduce<<<148 * 2, 256, 0, st>>>(p, ctx->G, ctx->q, ctx->per);
+        k_wgrad_reduce<<<148 * 2, 256, 0, st>>>(p, ctx->G);
         LAUNCHED();
     }
     mark(ctx, PH_WGRED);
@@ -421,7 +415,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
 template <typename T>
 gorila_status pack_replica(gorila_ctx* ctx, const float* theta_sliced, void* rt, float* rf, bool with_dgrad,
                            const uint8_t* pred, uint64_t* vhist_dst) {
-    k_pack<T><<<148 * 4, 256, 0, ctx->stream>>>(theta_sliced, ctx->q, ctx->per, ctx->nA, P_<T>(rt), rf,
+    k_pack<T><<<148 * 4, 256, 0, ctx->stream>>>(theta_sliced, ctx->nA, P_<T>(rt), rf,
                                                 with_dgrad ? 1 : 0, pred, vhist_dst, ctx->V);
     ctx->launches++;
     CU(cudaGetLastError());
@@ -438,16 +432,17 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     // computes the carve; if ctx != nullptr and base != nullptr fills the pointers
     const int nA = cfg->n_actions, B = cfg->batch, L = cfg->n_learners_local, W = cfg->world;
     const int64_t P = param_count(nA);
-    const int64_t q = round_up((P + W - 1) / W, 64), per = q + 64;
+    const int64_t q = round_up((P + W - 1) / W, 64);
     const size_t esz = cfg->math == GORILA_MATH_FP32 ? 4 : 2;
     const ReplicaLayout rl_full = replica_layout(nA, true), rl_fwd = replica_layout(nA, false);
     const int H = std::max(1, cfg->history);
     const bool fp32 = cfg->math == GORILA_MATH_FP32;
     Carver c{base};
-    float* theta = c.take<float>(W * per);
-    float* m = c.take<float>(per);
-    float* v = c.take<float>(per);
-    float* G = c.take<float>(W * per);
+    float* theta = c.take<float>(W * q);
+    float* m = c.take<float>(q);
+    float* v = c.take<float>(q);
+    float* G = c.take<float>(W * q);
+    float* counts = c.take<float>(W + 64);
     uint64_t* V = c.take<uint64_t>(4);
     uint64_t* rinfo = c.take<uint64_t>(4);
     uint32_t* nacc = c.take<uint32_t>(4);
@@ -480,11 +475,11 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     void* a1 = c.take<uint8_t>(Bs * A1 * esz);
     void* a2 = c.take<uint8_t>(Bs * A2 * esz);
     void* a3 = c.take<uint8_t>(Bs * A3 * esz);
-    void* a4 = c.take<uint8_t>(Bs * A4 * esz);
+    float* a4 = c.take<float>(Bs * A4);
     void* t1 = c.take<uint8_t>(Bs * A1 * esz);
     void* t2 = c.take<uint8_t>(Bs * A2 * esz);
     void* t3 = c.take<uint8_t>(Bs * A3 * esz);
-    void* t4 = c.take<uint8_t>(Bs * A4 * esz);
+    float* t4 = c.take<float>(Bs * A4);
     void* g1 = c.take<uint8_t>(Bs * A1 * esz);
     void* g2 = c.take<uint8_t>(Bs * A2 * esz);
     void* g3 = c.take<uint8_t>(Bs * A3 * esz);
@@ -510,11 +505,12 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         part_w[l] = c.take<float>((int64_t)split_w[l] * wcount[l]);
     }
     float* tmp_canon = c.take<float>(P);
-    float* tmp_int = c.take<float>(W * per);
+    float* tmp_int = c.take<float>(W * q);
     if (ctx) {
-        ctx->nA = nA; ctx->B = B; ctx->L = L; ctx->W = W; ctx->P = P; ctx->q = q; ctx->per = per; ctx->esz = esz;
+        ctx->nA = nA; ctx->B = B; ctx->L = L; ctx->W = W; ctx->P = P; ctx->q = q; ctx->esz = esz;
         ctx->rl_full = rl_full; ctx->rl_fwd = rl_fwd; ctx->H = H;
-        ctx->theta = theta; ctx->m = m; ctx->v = v; ctx->G = G; ctx->V = V; ctx->round_info = rinfo;
+        ctx->theta = theta; ctx->m = m; ctx->v = v; ctx->G = G; ctx->counts = counts; ctx->V = V;
+        ctx->round_info = rinfo;
         ctx->n_acc_local = nacc; ctx->Vhist = Vhist; ctx->rep_t = rep_t; ctx->rep_f = rep_f; ctx->learners = lrs;
         ctx->s = s; ctx->s2 = s2; ctx->a1 = a1; ctx->a2 = a2; ctx->a3 = a3; ctx->a4 = a4;
         ctx->t1 = t1; ctx->t2 = t2; ctx->t3 = t3; ctx->t4 = t4;
@@ -617,10 +613,10 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     layout_bytes(cfg, ctx, (uint8_t*)cfg->workspace);
     cudaStream_t st = ctx->stream;
     // zero the PS state, gradient buffer, counters, learner state
-    CU(cudaMemsetAsync(ctx->theta, 0, sizeof(float) * ctx->W * ctx->per, st));
-    CU(cudaMemsetAsync(ctx->m, 0, sizeof(float) * ctx->per, st));
-    CU(cudaMemsetAsync(ctx->v, 0, sizeof(float) * ctx->per, st));
-    CU(cudaMemsetAsync(ctx->G, 0, sizeof(float) * ctx->W * ctx->per, st));
+    CU(cudaMemsetAsync(ctx->theta, 0, sizeof(float) * ctx->W * ctx->q, st));
+    CU(cudaMemsetAsync(ctx->m, 0, sizeof(float) * ctx->q, st));
+    CU(cudaMemsetAsync(ctx->v, 0, sizeof(float) * ctx->q, st));
+    CU(cudaMemsetAsync(ctx->G, 0, sizeof(float) * ctx->W * ctx->q, st));
     CU(cudaMemsetAsync(ctx->V, 0, sizeof(uint64_t) * 4, st));
     CU(cudaMemsetAsync(ctx->n_acc_local, 0, sizeof(uint32_t) * 4, st));
     CU(cudaMemsetAsync(ctx->Vhist, 0, sizeof(uint64_t) * ctx->H, st));
@@ -632,7 +628,7 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     }
     // theta^+ = theta0 (canonical -> internal sliced)
     CU(cudaMemcpyAsync(ctx->tmp_canon, cfg->theta0, sizeof(float) * ctx->P, cudaMemcpyHostToDevice, st));
-    k_convert<<<148 * 4, 256, 0, st>>>(ctx->tmp_canon, ctx->theta, ctx->P, ctx->q, ctx->per, 0);
+    k_convert<<<148 * 4, 256, 0, st>>>(ctx->tmp_canon, ctx->theta, ctx->P, 0);
     ctx->launches++;
     // replica slot 0 and every learner's theta^- (Alg.1 P:113 theta^- = theta)
     gorila_status s;
@@ -760,7 +756,7 @@ gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
     cudaStream_t st = ctx->stream;
     mark(ctx, -1);
     ctx->prof_steps += ctx->prof ? 1 : 0;
-    CU(cudaMemsetAsync(ctx->G, 0, sizeof(float) * ctx->W * ctx->per, st));
+    CU(cudaMemsetAsync(ctx->G, 0, sizeof(float) * ctx->W * ctx->q, st));
     CU(cudaMemsetAsync(ctx->n_acc_local, 0, sizeof(uint32_t), st));
     mark(ctx, PH_STEP_MISC);
     for (int i = 0; i < n; ++i) {
@@ -777,7 +773,7 @@ gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
                                                              : run_learner<__nv_bfloat16>(ctx, j, round, s_j);
         if (s != GORILA_OK) return s;
     }
-    k_write_counts<<<1, 64, 0, st>>>(ctx->G, ctx->q, ctx->per, ctx->W, ctx->n_acc_local);
+    k_write_counts<<<1, 64, 0, st>>>(ctx->counts, ctx->W, ctx->n_acc_local);
     ctx->launches++;
     mark(ctx, PH_STEP_MISC);
     if (info_out)
@@ -793,17 +789,22 @@ gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info*
     if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned");
     cudaStream_t st = ctx->stream;
     const int W = ctx->W, r = ctx->rank;
-    float* gsl = ctx->G + (int64_t)r * ctx->per;
+    float* gsl = ctx->G + (int64_t)r * ctx->q;
     mark(ctx, -1);
-    if (W > 1) NC(ncclReduceScatter(ctx->G, gsl, ctx->per, ncclFloat, ncclSum, ctx->comm, st));
+    if (W > 1) {  // gradient + accepted counts onto the owning shard, one grouped launch
+        NC(ncclGroupStart());
+        NC(ncclReduceScatter(ctx->G, gsl, ctx->q, ncclFloat, ncclSum, ctx->comm, st));
+        NC(ncclReduceScatter(ctx->counts, ctx->counts + r, 1, ncclFloat, ncclSum, ctx->comm, st));
+        NC(ncclGroupEnd());
+    }
     mark(ctx, PH_RS);
     ApplyParams p{};
-    p.theta = ctx->theta + (int64_t)r * ctx->per;
+    p.theta = ctx->theta + (int64_t)r * ctx->q;
     p.m = ctx->m;
     p.v = ctx->v;
     p.g = gsl;
+    p.count = ctx->counts + (W > 1 ? r : 0);
     p.n_real = std::max<int64_t>(0, std::min<int64_t>(ctx->q, ctx->P - (int64_t)r * ctx->q));
-    p.q = ctx->q;
     p.optimizer = ctx->cfg.optimizer;
     p.lr = ctx->cfg.lr; p.rho = ctx->cfg.rms_rho; p.eps = ctx->cfg.rms_eps; p.ada_eps = ctx->cfg.ada_eps;
     p.V = ctx->V;
@@ -811,7 +812,7 @@ gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info*
     k_apply<<<148 * 4, 256, 0, st>>>(p);
     ctx->launches++;
     mark(ctx, PH_APPLY);
-    if (W > 1) NC(ncclAllGather(p.theta, ctx->theta, ctx->per, ncclFloat, ctx->comm, st));
+    if (W > 1) NC(ncclAllGather(p.theta, ctx->theta, ctx->q, ncclFloat, ctx->comm, st));
     mark(ctx, PH_AG);
     const int slot = (int)((round + 1) % (uint64_t)ctx->H);
     gorila_status s = pack_any(ctx, ctx->theta, ctx->rep_t[slot], ctx->rep_f[slot], true, nullptr, ctx->Vhist + slot);
@@ -859,13 +860,13 @@ gorila_status gorila_get_state(gorila_ctx* ctx, float* theta, float* m, float* v
     for (auto& it : items) {
         if (!it.dst) continue;
         if (it.full) {
-            CU(cudaMemcpyAsync(ctx->tmp_int, it.src_slice, sizeof(float) * ctx->W * ctx->per, cudaMemcpyDeviceToDevice, st));
+            CU(cudaMemcpyAsync(ctx->tmp_int, it.src_slice, sizeof(float) * ctx->W * ctx->q, cudaMemcpyDeviceToDevice, st));
         } else {  // own slice only; other slices zero
-            CU(cudaMemsetAsync(ctx->tmp_int, 0, sizeof(float) * ctx->W * ctx->per, st));
-            CU(cudaMemcpyAsync(ctx->tmp_int + (int64_t)ctx->rank * ctx->per, it.src_slice, sizeof(float) * ctx->per,
+            CU(cudaMemsetAsync(ctx->tmp_int, 0, sizeof(float) * ctx->W * ctx->q, st));
+            CU(cudaMemcpyAsync(ctx->tmp_int + (int64_t)ctx->rank * ctx->q, it.src_slice, sizeof(float) * ctx->q,
                                cudaMemcpyDeviceToDevice, st));
         }
-        k_convert<<<148 * 4, 256, 0, st>>>(ctx->tmp_int, ctx->tmp_canon, P, ctx->q, ctx->per, 1);
+        k_convert<<<148 * 4, 256, 0, st>>>(ctx->tmp_int, ctx->tmp_canon, P, 1);
         ctx->launches++;
         CU(cudaMemcpyAsync(it.dst, ctx->tmp_canon, sizeof(float) * P, cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
@@ -883,13 +884,13 @@ gorila_status gorila_set_state(gorila_ctx* ctx, const float* theta, const float*
     for (auto& it : items) {
         if (!it.src) continue;
         CU(cudaMemcpyAsync(ctx->tmp_canon, it.src, sizeof(float) * P, cudaMemcpyHostToDevice, st));
-        CU(cudaMemsetAsync(ctx->tmp_int, 0, sizeof(float) * ctx->W * ctx->per, st));
-        k_convert<<<148 * 4, 256, 0, st>>>(ctx->tmp_canon, ctx->tmp_int, P, ctx->q, ctx->per, 0);
+        CU(cudaMemsetAsync(ctx->tmp_int, 0, sizeof(float) * ctx->W * ctx->q, st));
+        k_convert<<<148 * 4, 256, 0, st>>>(ctx->tmp_canon, ctx->tmp_int, P, 0);
         ctx->launches++;
         if (it.full)
-            CU(cudaMemcpyAsync(it.dst_slice, ctx->tmp_int, sizeof(float) * ctx->W * ctx->per, cudaMemcpyDeviceToDevice, st));
+            CU(cudaMemcpyAsync(it.dst_slice, ctx->tmp_int, sizeof(float) * ctx->W * ctx->q, cudaMemcpyDeviceToDevice, st));
         else
-            CU(cudaMemcpyAsync(it.dst_slice, ctx->tmp_int + (int64_t)ctx->rank * ctx->per, sizeof(float) * ctx->per,
+            CU(cudaMemcpyAsync(it.dst_slice, ctx->tmp_int + (int64_t)ctx->rank * ctx->q, sizeof(float) * ctx->q,
                                cudaMemcpyDeviceToDevice, st));
         CU(cudaStreamSynchronize(st));
     }
@@ -957,8 +958,8 @@ gorila_status gorila_set_learner_state(gorila_ctx* ctx, int32_t learner, const f
     }
     if (theta_minus) {
         CU(cudaMemcpyAsync(ctx->tmp_canon, theta_minus, sizeof(float) * ctx->P, cudaMemcpyHostToDevice, st));
-        CU(cudaMemsetAsync(ctx->tmp_int, 0, sizeof(float) * ctx->W * ctx->per, st));
-        k_convert<<<148 * 4, 256, 0, st>>>(ctx->tmp_canon, ctx->tmp_int, ctx->P, ctx->q, ctx->per, 0);
+        CU(cudaMemsetAsync(ctx->tmp_int, 0, sizeof(float) * ctx->W * ctx->q, st));
+        k_convert<<<148 * 4, 256, 0, st>>>(ctx->tmp_canon, ctx->tmp_int, ctx->P, 0);
         ctx->launches++;
         if ((s = pack_any(ctx, ctx->tmp_int, l.tminus_t, l.tminus_f, false, nullptr, nullptr)) != GORILA_OK) return s;
         CU(cudaStreamSynchronize(st));
@@ -969,7 +970,7 @@ gorila_status gorila_set_learner_state(gorila_ctx* ctx, int32_t learner, const f
 gorila_status gorila_get_grad(gorila_ctx* ctx, float* g) {
     if (!ctx || !g) return fail(GORILA_E_INVALID, "null argument");
     cudaStream_t st = ctx->stream;
-    k_convert<<<148 * 4, 256, 0, st>>>(ctx->G, ctx->tmp_canon, ctx->P, ctx->q, ctx->per, 1);
+    k_convert<<<148 * 4, 256, 0, st>>>(ctx->G, ctx->tmp_canon, ctx->P, 1);
     ctx->launches++;
     CU(cudaMemcpyAsync(g, ctx->tmp_canon, sizeof(float) * ctx->P, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));

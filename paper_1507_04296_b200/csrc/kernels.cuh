@@ -7,9 +7,6 @@ namespace gorila {
 
 constexpr uint32_t TAG_SAMPLE = 3u;
 
-// position of internal element i in the sliced storage (q real elements per shard slice,
-// slice stride per = q + 64; element q of every slice is the accepted-gradient count slot)
-GORILA_DEV int64_t gslot(int64_t i, int64_t q, int64_t per) { return (i / q) * per + (i % q); }
 
 // ------------------------------------------------------------------------- K1 sampler
 // Alg.1 P:121 "Sample random mini-batch from D"; "(s,a,r,s') ~ U(D)"; P:181 4-frame stack.
@@ -72,12 +69,30 @@ __global__ void __launch_bounds__(256) k_sample(const uint8_t* __restrict__ fram
         for (int t = 0; t < 5; ++t) fb[t] = reinterpret_cast<const uint8_t*>(&f[t]);
         T* so = s_out + ((int64_t)b * FRAME_BYTES + chunk * 16) * NSTACK;
         T* so2 = s2_out + ((int64_t)b * FRAME_BYTES + chunk * 16) * NSTACK;
+        // NHWC: 16 pixels x 4 channels, written as 16-byte vectors
 #pragma unroll
-        for (int px = 0; px < 16; ++px) {
+        for (int half = 0; half < 2; ++half) {
+            T* dst = half ? so2 : so;
 #pragma unroll
-            for (int c = 0; c < 4; ++c) {
-                so[px * 4 + c] = fromf<T>(keep_s[c] ? (float)fb[c][px] : 0.f);
-                so2[px * 4 + c] = fromf<T>(keep_s2[c] ? (float)fb[c + 1][px] : 0.f);
+            for (int v = 0; v < 64 * (int)sizeof(T) / 16; ++v) {  // 16-B vectors per 16 pixels
+                float x[16 / sizeof(T)];
+#pragma unroll
+                for (int e = 0; e < (int)(16 / sizeof(T)); ++e) {
+                    const int el = v * (16 / sizeof(T)) + e, px = el >> 2, c = el & 3;
+                    const bool keep = half ? keep_s2[c] : keep_s[c];
+                    x[e] = keep ? (float)fb[c + half][px] : 0.f;
+                }
+                if constexpr (sizeof(T) == 2) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        __nv_bfloat162 h = __floats2bfloat162_rn(x[2 * e], x[2 * e + 1]);
+                        w[e] = *reinterpret_cast<uint32_t*>(&h);
+                    }
+                    reinterpret_cast<uint4*>(dst)[v] = make_uint4(w[0], w[1], w[2], w[3]);
+                } else {
+                    reinterpret_cast<float4*>(dst)[v] = make_float4(x[0], x[1], x[2], x[3]);
+                }
             }
         }
     }
@@ -91,37 +106,37 @@ __global__ void __launch_bounds__(256) k_sample(const uint8_t* __restrict__ fram
 
 // ------------------------------------------------------------------------- fc4 split-K finalize
 // a4[b][n] = round_T(ReLU(sum_s partial[s][n][b] + b4[n])), both nets (z = problem)
-template <typename T>
+// a4 stays fp32: it only feeds the fp32 fc5 layer (reading R16)
 __global__ void k_fc4_finalize(const float* __restrict__ partial, int splits, int64_t prob_stride, int B,
-                               const float* __restrict__ bias0, const float* __restrict__ bias1, T* out0, T* out1) {
+                               const float* __restrict__ bias0, const float* __restrict__ bias1, float* out0,
+                               float* out1) {
     const int z = blockIdx.y;
     const float* P = partial + z * prob_stride;
     const float* bias = z ? bias1 : bias0;
-    T* out = z ? out1 : out0;
+    float* out = z ? out1 : out0;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < B * FC4_OUT; e += gridDim.x * blockDim.x) {
         int b = e / FC4_OUT, n = e - b * FC4_OUT;
         float acc = 0.f;
         for (int s = 0; s < splits; ++s) acc += P[(int64_t)s * FC4_OUT * B + (int64_t)n * B + b];
-        out[e] = fromf<T>(fmaxf(acc + bias[n], 0.f));
+        out[e] = fmaxf(acc + bias[n], 0.f);
     }
 }
 
 // ------------------------------------------------------------------------- fc5 forward
 // Q[b][a] = sum_n a4[b][n] * W5[a][n] + b5[a]  (fp32 weights, fp32 result; z = online / target)
-template <typename T>
-__global__ void __launch_bounds__(256) k_fc5_fwd(const T* __restrict__ a4_0, const T* __restrict__ a4_1,
+__global__ void __launch_bounds__(256) k_fc5_fwd(const float* __restrict__ a4_0, const float* __restrict__ a4_1,
                                                  const float* __restrict__ w5_0, const float* __restrict__ w5_1,
                                                  const float* __restrict__ b5_0, const float* __restrict__ b5_1,
                                                  float* __restrict__ q0, float* __restrict__ q1, int nA) {
     const int b = blockIdx.x, z = blockIdx.y;
-    const T* a4 = (z ? a4_1 : a4_0) + (int64_t)b * FC4_OUT;
+    const float* a4 = (z ? a4_1 : a4_0) + (int64_t)b * FC4_OUT;
     const float* w5 = z ? w5_1 : w5_0;
     const float* b5 = z ? b5_1 : b5_0;
     float* q = z ? q1 : q0;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     for (int a = warp; a < nA; a += 8) {
         float acc = 0.f;
-        for (int n = lane; n < FC4_OUT; n += 32) acc = fmaf(tof(a4[n]), w5[a * FC4_OUT + n], acc);
+        for (int n = lane; n < FC4_OUT; n += 32) acc = fmaf(a4[n], w5[a * FC4_OUT + n], acc);
         acc = warp_sum(acc);
         if (lane == 0) q[b * nA + a] = acc + b5[a];
     }
@@ -247,25 +262,25 @@ __global__ void k_mark_not_ready(DevLearnerInfo* info, const LearnerStats* st) {
 // dW5[a][n] += sum_b dQ[b][a] a4[b][n]; db5[a] += sum_b dQ[b][a];
 // g4[b][n] = round_T((sum_a dQ[b][a] W5[a][n]) * 1[a4[b][n] > 0])
 template <typename T>
-__global__ void k_fc5_bwd(const float* __restrict__ dQ, const T* __restrict__ a4, const float* __restrict__ w5, int B,
-                          int nA, float* __restrict__ G, int64_t q, int64_t per, T* __restrict__ g4) {
+__global__ void k_fc5_bwd(const float* __restrict__ dQ, const float* __restrict__ a4, const float* __restrict__ w5,
+                          int B, int nA, float* __restrict__ G, T* __restrict__ g4) {
     const int n_w = nA * FC4_OUT, n_b = nA, n_g = B * FC4_OUT;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_w + n_b + n_g; e += gridDim.x * blockDim.x) {
         if (e < n_w) {
             int a = e / FC4_OUT, n = e - a * FC4_OUT;
             float acc = 0.f;
-            for (int b = 0; b < B; ++b) acc = fmaf(dQ[b * nA + a], tof(a4[(int64_t)b * FC4_OUT + n]), acc);
-            G[gslot(OFF_W5 + e, q, per)] += acc;
+            for (int b = 0; b < B; ++b) acc = fmaf(dQ[b * nA + a], a4[(int64_t)b * FC4_OUT + n], acc);
+            G[OFF_W5 + e] += acc;
         } else if (e < n_w + n_b) {
             int a = e - n_w;
             float acc = 0.f;
             for (int b = 0; b < B; ++b) acc += dQ[b * nA + a];
-            G[gslot(off_b5(nA) + a, q, per)] += acc;
+            G[off_b5(nA) + a] += acc;
         } else {
             int f = e - n_w - n_b, b = f / FC4_OUT, n = f - b * FC4_OUT;
             float acc = 0.f;
             for (int a = 0; a < nA; ++a) acc = fmaf(dQ[b * nA + a], w5[a * FC4_OUT + n], acc);
-            g4[f] = fromf<T>(tof(a4[f]) > 0.f ? acc : 0.f);
+            g4[f] = fromf<T>(a4[f] > 0.f ? acc : 0.f);
         }
     }
 }
@@ -275,7 +290,7 @@ __global__ void k_fc5_bwd(const float* __restrict__ dQ, const T* __restrict__ a4
 template <typename T>
 __global__ void __launch_bounds__(256) k_bias_grad(const T* __restrict__ g1, const T* __restrict__ g2,
                                                    const T* __restrict__ g3, const T* __restrict__ g4, int B,
-                                                   float* __restrict__ G, int64_t q, int64_t per) {
+                                                   float* __restrict__ G) {
     __shared__ float red[256];
     int o = blockIdx.x;
     const T* g;
@@ -293,7 +308,7 @@ __global__ void __launch_bounds__(256) k_bias_grad(const T* __restrict__ g1, con
         if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
         __syncthreads();
     }
-    if (threadIdx.x == 0) G[gslot(off + o, q, per)] += red[0];
+    if (threadIdx.x == 0) G[off + o] += red[0];
 }
 
 // ------------------------------------------------------------------------- K10 wgrad reduce
@@ -304,7 +319,7 @@ struct WgradReduceParams {
     int64_t count[3];
     int64_t off[3];
 };
-__global__ void k_wgrad_reduce(WgradReduceParams p, float* __restrict__ G, int64_t q, int64_t per) {
+__global__ void k_wgrad_reduce(WgradReduceParams p, float* __restrict__ G) {
     const int64_t total = p.count[0] + p.count[1] + p.count[2];
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         int l = 0;
@@ -312,29 +327,19 @@ __global__ void k_wgrad_reduce(WgradReduceParams p, float* __restrict__ G, int64
         if (f >= p.count[0]) { f -= p.count[0]; l = 1; if (f >= p.count[1]) { f -= p.count[1]; l = 2; } }
         float acc = 0.f;
         for (int s = 0; s < p.splits[l]; ++s) acc += p.part[l][(int64_t)s * p.count[l] + f];
-        G[gslot(p.off[l] + f, q, per)] += acc;
+        G[p.off[l] + f] += acc;
     }
 }
 
-// fc4 weight gradient epilogue: G[W4][n][k] += v  with i = k, j = n
-struct EpAddW4 {
-    float* G;
-    int64_t q, per;
-    int M, N;
-    GORILA_DEV void apply(int i, int j, float v, int) const {
-        if (i >= M || j >= N) return;
-        G[gslot(OFF_W4 + (int64_t)j * FC4_IN + i, q, per)] += v;
-    }
-};
 
 // ------------------------------------------------------------------------- PS apply (K11)
 struct ApplyParams {
     float* theta;  // this rank's slice of theta^+ (sliced storage)
     float* m;
     float* v;
-    const float* g;  // this rank's reduced slice; g[q] = accepted count
-    int64_t n_real;  // real elements in this slice
-    int64_t q;
+    const float* g;      // this rank's reduced slice
+    const float* count;  // accepted gradients this round (all ranks)
+    int64_t n_real;      // real elements in this slice
     int optimizer;
     float lr, rho, eps, ada_eps;
     uint64_t* V;
@@ -343,7 +348,7 @@ struct ApplyParams {
 // Centered RMSProp (reading R2) / AdaGrad on the mean of the accepted gradients
 // (reading R12, R25); V += |Acc|. float4-vectorised, grid-stride.
 __global__ void __launch_bounds__(256) k_apply(ApplyParams p) {
-    const float cnt = p.g[p.q];
+    const float cnt = *p.count;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         const uint64_t v0 = *p.V;
         const uint64_t n_acc = (uint64_t)(cnt + 0.5f);
@@ -392,17 +397,17 @@ __global__ void __launch_bounds__(256) k_apply(ApplyParams p) {
     }
 }
 
-// write this rank's accepted count into the count slot of every slice of G
-__global__ void k_write_counts(float* G, int64_t q, int64_t per, int W, const uint32_t* n_acc_local) {
-    int s = threadIdx.x;
-    if (s < W) G[s * per + q] = (float)*n_acc_local;
+// this rank's accepted count, once per destination shard (reduce-scattered with G)
+__global__ void k_write_counts(float* counts, int W, const uint32_t* n_acc_local) {
+    const int s = threadIdx.x;
+    if (s < W) counts[s] = (float)*n_acc_local;
 }
 
 // ------------------------------------------------------------------------- replica pack
 // theta^+ (sliced, internal order, fp32) -> packed replica in T (+ fp32 area).
 // with_dgrad also writes the transposed dgrad copies. pred (nullable): skip unless *pred.
 template <typename T>
-__global__ void k_pack(const float* __restrict__ theta, int64_t q, int64_t per, int nA, T* __restrict__ rt,
+__global__ void k_pack(const float* __restrict__ theta, int nA, T* __restrict__ rt,
                        float* __restrict__ rf, int with_dgrad, const uint8_t* __restrict__ pred,
                        uint64_t* __restrict__ vhist_dst, const uint64_t* __restrict__ V) {
     if (pred && !*pred) return;
@@ -410,7 +415,7 @@ __global__ void k_pack(const float* __restrict__ theta, int64_t q, int64_t per, 
     const int64_t P = param_count(nA);
     if (vhist_dst && blockIdx.x == 0 && threadIdx.x == 0) *vhist_dst = *V;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-        const float w = theta[gslot(i, q, per)];
+        const float w = theta[i];
         if (i < OFF_B1) {
             rt[L.w1 + i] = fromf<T>(w);
         } else if (i < OFF_W2) {
@@ -458,13 +463,12 @@ __global__ void k_sync_decide(LearnerStats* st, const uint64_t* V, int64_t perio
 }
 
 // ------------------------------------------------------------------------- layout conversion
-// dir 0: canonical -> internal sliced ; dir 1: internal sliced -> canonical
-__global__ void k_convert(const float* __restrict__ src, float* __restrict__ dst, int64_t P, int64_t q, int64_t per,
-                          int dir) {
+// dir 0: canonical -> internal ; dir 1: internal -> canonical
+__global__ void k_convert(const float* __restrict__ src, float* __restrict__ dst, int64_t P, int dir) {
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t c = canon_of_internal(i), s = gslot(i, q, per);
-        if (dir == 0) dst[s] = src[c];
-        else dst[c] = src[s];
+        const int64_t c = canon_of_internal(i);
+        if (dir == 0) dst[i] = src[c];
+        else dst[c] = src[i];
     }
 }
 

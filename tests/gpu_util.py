@@ -86,3 +86,23 @@ def run_round_both(g, orc, k, learners, staleness=None):
            "theta0": th0, "theta1": th1, "V": V1}
     res = orc.round(k, staleness=staleness)
     return gpu, res
+
+
+LAYER_OF = {"W1": 1, "b1": 1, "W2": 2, "b2": 2, "W3": 3, "b3": 3, "W4": 4, "b4": 4, "W5": 5, "b5": 5}
+
+
+def ambiguous_layer(theta, s, nA, rel=1e-6):
+    """Kink rule: the deepest hidden layer l (1..4) with a pre-activation |z| <= rel * max|z|,
+    recomputed with the oracle's exact layer primitives; 0 if none. A ReLU decision that close to 0 is
+    decided differently by fp32 accumulation, which moves the gradients of tensors at and below layer l."""
+    p = O.unflatten(np.asarray(theta, np.float64), nA)
+    x = s.astype(np.float64) / 255.0
+    z1 = O.conv2d_fwd(x, p["W1"], p["b1"], 4)
+    z2 = O.conv2d_fwd(np.maximum(z1, 0), p["W2"], p["b2"], 2)
+    z3 = O.conv2d_fwd(np.maximum(z2, 0), p["W3"], p["b3"], 1)
+    z4 = O.linear_fwd(np.maximum(z3, 0).reshape(len(s), -1), p["W4"], p["b4"])
+    deepest = 0
+    for l, z in enumerate((z1, z2, z3, z4), start=1):
+        if np.any(np.abs(z) <= rel * np.max(np.abs(z))):
+            deepest = l
+    return deepest

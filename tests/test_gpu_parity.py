@@ -11,7 +11,8 @@ import pytest
 
 import oracle as O
 import synth
-from gpu_util import TOL, make_pair, per_tensor_rel_l2, rel_inf, rel_l2, run_round_both, teacher_force
+from gpu_util import (LAYER_OF, TOL, ambiguous_layer, make_pair, per_tensor_rel_l2, rel_inf, rel_l2,
+                      run_round_both, teacher_force)
 
 pytestmark = pytest.mark.gpu
 
@@ -64,9 +65,10 @@ def test_replay_not_ready():
     assert ri["n_accepted"] == 0 and ri["version_after"] == 0
 
 
-def _check_round(gpu, res, math, nA, learners):
+def _check_round(gpu, res, math, nA, learners, orc=None, thetas=None):
     tol = TOL[math]
     G_ref = np.zeros_like(gpu["G"], dtype=np.float64)
+    kink = 0  # fp32 check mode: deepest layer with an ambiguous ReLU decision (kink rule)
     for j in learners:
         gi, oi = gpu["info"][j], res["learners"][j]
         q, qh = gpu["q"][j]
@@ -83,10 +85,15 @@ def _check_round(gpu, res, math, nA, learners):
         assert gi["base_version"] == oi["base_version"]
         if oi["accepted"]:
             G_ref += oi["G"]
+            if math == "fp32" and orc is not None and thetas is not None:
+                s, _, _, _, _ = orc.learners[j].ring.gather(oi["tau"])
+                kink = max(kink, ambiguous_layer(thetas[j], s, nA))
     if np.any(G_ref):
-        assert rel_l2(gpu["G"], G_ref) <= tol["g"], ("G", rel_l2(gpu["G"], G_ref))
+        relaxed = TOL["bf16"]["g"]
+        e_all = rel_l2(gpu["G"], G_ref)
+        assert e_all <= (tol["g"] if kink == 0 else relaxed), ("G", e_all, kink)
         for name, e in per_tensor_rel_l2(gpu["G"], G_ref, nA).items():
-            assert e <= tol["g"], ("G", name, e)
+            assert e <= (tol["g"] if LAYER_OF[name] > kink else relaxed), ("G", name, e, kink)
     else:
         assert not np.any(gpu["G"])
     assert gpu["round"]["n_accepted"] == res["n_accepted"]
@@ -104,13 +111,23 @@ def test_learner_update_parity_c1_teacher_forced(math):
         teacher_force(g, orc)
         th_before = orc.theta.copy()
         gpu, res = run_round_both(g, orc, k, [0])
-        _check_round(gpu, res, math, nA, [0])
+        _check_round(gpu, res, math, nA, [0], orc, {0: th_before})
+        # theta^+ is stored in fp32 (reading R16): the reference update is the oracle's exact
+        # update rounded to the state's precision, fp32(theta0 + dtheta_exact) - theta0
+        # The GPU result can differ from that by one fp32 ulp wherever its (tolerance-close) step
+        # lands on the other side of a rounding boundary: the bound is tol + ||ulp(theta1)|| / ||dtheta||.
         d_gpu = gpu["theta1"].astype(np.float64) - gpu["theta0"]
-        d_ref = orc.theta - th_before
+        th1_ref = orc.theta.astype(np.float32)
+        d_ref = th1_ref.astype(np.float64) - th_before
+        ulp = np.spacing(np.abs(th1_ref)).astype(np.float64)
         if np.any(d_ref):
-            assert rel_l2(d_gpu, d_ref) <= tol["dtheta"], ("dtheta", k, rel_l2(d_gpu, d_ref))
-            for name, e in per_tensor_rel_l2(d_gpu, d_ref, nA).items():
-                assert e <= tol["dtheta"], ("dtheta", k, name, e)
+            off = 0
+            for name, shp in O.param_shapes(nA) + [("all", (len(d_ref),))]:
+                sl = slice(0, len(d_ref)) if name == "all" else slice(off, off + int(np.prod(shp)))
+                e = rel_l2(d_gpu[sl], d_ref[sl])
+                floor = np.linalg.norm(ulp[sl]) / max(np.linalg.norm(d_ref[sl]), 1e-300)
+                assert e <= tol["dtheta"] + floor, ("dtheta", k, name, e, floor)
+                off += 0 if name == "all" else int(np.prod(shp))
 
 
 @pytest.mark.parametrize("math", ["fp32", "bf16"])
@@ -119,8 +136,9 @@ def test_learner_update_parity_ragged_shapes(math, nA, B):
     """Ragged batch (not a multiple of any tile), degenerate nA = 1 and the maximum nA = 32."""
     g, orc = make_pair(nA=nA, B=B, C=3000, n_insert=3000, math=math, outlier_enabled=False)
     teacher_force(g, orc)
+    th = orc.theta.copy()
     gpu, res = run_round_both(g, orc, 0, [0])
-    _check_round(gpu, res, math, nA, [0])
+    _check_round(gpu, res, math, nA, [0], orc, {0: th})
 
 
 @pytest.mark.parametrize("math", ["fp32", "bf16"])
@@ -142,8 +160,11 @@ def test_multi_learner_staleness_outlier_and_sync(math):
             r = np.full_like(ring.r, 1e6)
             g.replay_insert(2, f, a, r, d)
             orc.insert(2, f, a, r, d)
+        hist = dict(orc.history)
+        hist[k] = (orc.theta.copy(), orc.V)
+        thetas = {j: hist[max(k - stal[j], 0)][0] for j in (0, 1, 2)}
         gpu, res = run_round_both(g, orc, k, [0, 1, 2], staleness=stal)
-        _check_round(gpu, res, math, nA, [0, 1, 2])
+        _check_round(gpu, res, math, nA, [0, 1, 2], orc, thetas)
         if k == 3:
             assert gpu["info"][2]["rejected_outlier"] == 1
         # free-running after the common start (history of replicas must match the schedule)

@@ -36,7 +36,7 @@ def _torch_net(p, x, mode):
     a1 = q(F.relu(z1))
     a2 = q(F.relu(F.conv2d(a1, q(p["W2"]), p["b2"], stride=2)))
     a3 = q(F.relu(F.conv2d(a2, q(p["W3"]), p["b3"], stride=1)))
-    a4 = q(F.relu(F.linear(a3.reshape(a3.shape[0], -1), q(p["W4"]), p["b4"])))
+    a4 = F.relu(F.linear(a3.reshape(a3.shape[0], -1), q(p["W4"]), p["b4"]))  # a4 stays unrounded (R16)
     return F.linear(a4, p["W5"], p["b5"])
 
 
@@ -107,8 +107,7 @@ def test_qnet_backward_matches_torch_autograd(mode):
         a1 = RoundGrad.apply(RoundSTE.apply(F.relu(z1)))
         a2 = RoundGrad.apply(RoundSTE.apply(F.relu(F.conv2d(a1, RoundSTE.apply(p["W2"]), p["b2"], stride=2))))
         a3 = RoundGrad.apply(RoundSTE.apply(F.relu(F.conv2d(a2, RoundSTE.apply(p["W3"]), p["b3"], stride=1))))
-        a4 = RoundGrad.apply(RoundSTE.apply(F.relu(F.linear(a3.reshape(B, -1), RoundSTE.apply(p["W4"]),
-                                                            p["b4"]))))
+        a4 = RoundGrad.apply(F.relu(F.linear(a3.reshape(B, -1), RoundSTE.apply(p["W4"]), p["b4"])))
         Qt = F.linear(a4, p["W5"], p["b5"])
         Qt.backward(torch.from_numpy(dQ))
     ref = np.concatenate([p[k].grad.numpy().ravel() for k, _ in O.param_shapes(nA)])

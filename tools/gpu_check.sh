@@ -2,7 +2,7 @@
 # GPU-box check: tests, smoke, short bench. Everything under timeouts; logs in gpurun_out/.
 mkdir -p gpurun_out
 ( nvidia-smi; nproc; lscpu | grep -i "model name" ) > gpurun_out/box.txt 2>&1
-timeout -s KILL 900 python -m pytest tests -m gpu -x -q --timeout 300 > gpurun_out/pytest_gpu.log 2>&1
+timeout -s KILL 900 python -m pytest tests -m gpu -q --timeout 300 > gpurun_out/pytest_gpu.log 2>&1
 echo "pytest exit $?" >> gpurun_out/pytest_gpu.log
 timeout -s KILL 300 python __graft_entry__.py smoke > gpurun_out/smoke.log 2>&1
 echo "smoke exit $?" >> gpurun_out/smoke.log
