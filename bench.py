@@ -46,10 +46,11 @@ def phase_work(phase, B, nA, P, esz):
         "conv1_wgrad": ("tensor", fl(MAC["conv1"])),
         # sampler: reads 5 frames + meta per sample, writes s and s' (NHWC, esz bytes/element)
         "sample": ("hbm", B * (5 * 7056 + 6 + 2 * 4 * 7056 * esz)),
-        # centered RMSProp: read theta, m, v, g (16 B) + write theta, m, v (12 B) per parameter
-        "apply": ("hbm", 28.0 * P),
-        # replica: read fp32 theta, write fwd copy + transposed dgrad copies of W2/W3/W4 + fp32 area
-        "pack": ("hbm", 4.0 * P + esz * (P + 32768 + 36864 + 1605632)),
+        # centered RMSProp: read theta, m, v, g (16 B) + write theta, m, v (12 B) per parameter, plus the
+        # fused emission of the next replica (esz bytes per parameter)
+        "apply": ("hbm", (28.0 + esz) * P),
+        # replica pack (world > 1, after the all-gather): read fp32 theta, write the replica
+        "pack": ("hbm", (4.0 + esz) * P),
     }
     return table.get(phase)
 
@@ -260,6 +261,9 @@ def main():
     ids = np.array([0], np.int32)
 
     def step(k):
+        g.round(ids, k)  # learner_step + ps_apply_shard + sync_target, replayed as one CUDA graph
+
+    def step_eager(k):
         g.learner_step_async(ids, k)
         g.ps_apply_shard(k, want_info=False)
         g.sync_target(ids, want_info=False)
@@ -304,9 +308,7 @@ def main():
         f1.numpy()[0] = hf[i]
         a1.numpy()[0], r1.numpy()[0], d1.numpy()[0] = ha[i], hr[i], hd[i]
         g.replay_insert(0, f1, a1, r1, d1)           # this step's new experience, pinned host -> device
-        info = g.learner_step([0], k)                 # result (loss, decisions) device -> host
-        g.ps_apply_shard(k, want_info=True)
-        g.sync_target([0], want_info=True)
+        info = g.round(ids, k, want_info=True)        # the round; its result (loss, decisions) device -> host
         k += 1
     e1.record(stream)
     stream.synchronize()
@@ -319,7 +321,7 @@ def main():
     prof_steps = min(args.steps, 300)
     stream.synchronize()
     for _ in range(prof_steps):
-        step(k)
+        step_eager(k)  # per-phase events need the eager (non-graph) path
         k += 1
     phases, n_prof = g.profile_read()
     g.profile_enable(False)

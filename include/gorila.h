@@ -187,6 +187,17 @@ GORILA_API gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_
 GORILA_API gorila_status sync_target(gorila_ctx* ctx, const int32_t* learners, int32_t n, int32_t force,
                           uint8_t* synced_out);
 
+/* One whole round = learner_step + ps_apply_shard + sync_target(force = 0) for
+ * the listed learners, replayed from a CUDA graph captured on first reuse (key:
+ * learner list, staleness schedule, replica slot round mod history). Semantics
+ * are exactly those of the three calls in sequence; rounds with a not-ready
+ * learner (or round < max staleness) run them eagerly instead. Outputs (each may
+ * be NULL) are copied after the round: info n entries, round_info, synced n
+ * bytes; any non-NULL output synchronises the stream. COLLECTIVE. */
+GORILA_API gorila_status gorila_round(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
+                                      const int32_t* staleness, gorila_learner_info* info_out,
+                                      gorila_round_info* round_info_out, uint8_t* synced_out);
+
 /* State access for checkpointing and teacher-forced parity (canonical layout,
  * host buffers, any may be NULL; synchronises the stream). m / v are the full
  * optimizer state vectors (world == 1), or zeros outside this rank's shard.

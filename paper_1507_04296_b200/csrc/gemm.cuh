@@ -132,6 +132,23 @@ struct LdDgrad {
     }
 };
 
+// conv dgrad weight operand read straight from the forward (KRSC) weight, MN-major over c:
+// value(i = c, r = (ky*K + kx)*CO + o) = W[o][ky][kx][c]
+template <typename T, typename SH>
+struct LdWdgradMN {
+    static constexpr bool kMN = true;
+    const T* w;
+    GORILA_DEV int64_t addr(int c, int r) const {
+        const int t = r / SH::CO, o = r - t * SH::CO;
+        return (int64_t)o * SH::R + t * SH::C + c;
+    }
+    GORILA_DEV float load(int c, int r) const { return (c < SH::C && r < SH::RD) ? tof(w[addr(c, r)]) : 0.f; }
+    GORILA_DEV uint4 load8(int c0, int r) const {
+        if (c0 >= SH::C || r >= SH::RD) return zero4();
+        return *reinterpret_cast<const uint4*>(w + addr(c0, r));
+    }
+};
+
 // ====================================================================== epilogues
 // apply1(i, j, v, split): scalar; apply16(i, j0, v[16], split): 16 consecutive columns.
 
@@ -236,9 +253,14 @@ struct EpMaskT {  // transposed: out[j][i] = round_T(v * 1[act[j][i] > 0])  (coa
         const int64_t a = (int64_t)j * ld + i;
         out[a] = fromf<T>(tof(act[a]) > 0.f ? v : 0.f);
     }
-    GORILA_DEV void apply16(int i, int j0, const float* v, int s) const {
+    GORILA_DEV void apply16(int i, int j0, const float* v, int) const {
+        if (i >= M) return;
+        float h[16];  // all loads before any store (no load/store aliasing chain)
 #pragma unroll
-        for (int e = 0; e < 16; ++e) apply1(i, j0 + e, v[e], s);
+        for (int e = 0; e < 16; ++e) h[e] = (j0 + e < N) ? tof(act[(int64_t)(j0 + e) * ld + i]) : 0.f;
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+            if (j0 + e < N) out[(int64_t)(j0 + e) * ld + i] = fromf<T>(h[e] > 0.f ? v[e] : 0.f);
     }
 };
 
@@ -272,16 +294,21 @@ struct EpStore {  // dst[split][i][j] = v (fp32 split-K partials)
     }
 };
 
-struct EpAddT {  // G[off + j*ld + i] += v (fp32, transposed, coalesced across the warp's rows)
+struct EpAddT {  // G[j*ld + i] (+)= v (fp32, transposed, coalesced across the warp's rows)
     float* G;
     int64_t ld;
-    int M, N;
+    int M, N, accumulate;
     GORILA_DEV void apply1(int i, int j, float v, int) const {
-        if (i < M && j < N) G[(int64_t)j * ld + i] += v;
+        if (i < M && j < N) G[(int64_t)j * ld + i] = accumulate ? G[(int64_t)j * ld + i] + v : v;
     }
-    GORILA_DEV void apply16(int i, int j0, const float* v, int s) const {
+    GORILA_DEV void apply16(int i, int j0, const float* v, int) const {
+        if (i >= M) return;
+        float o[16];  // all loads before any store
 #pragma unroll
-        for (int e = 0; e < 16; ++e) apply1(i, j0 + e, v[e], s);
+        for (int e = 0; e < 16; ++e) o[e] = (accumulate && j0 + e < N) ? G[(int64_t)(j0 + e) * ld + i] : 0.f;
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+            if (j0 + e < N) G[(int64_t)(j0 + e) * ld + i] = o[e] + v[e];
     }
 };
 

@@ -9,6 +9,7 @@
 #include <nccl.h>
 
 #include <algorithm>
+#include <map>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -93,7 +94,7 @@ struct gorila_ctx {
     int nA, B, L, W, rank;
     int64_t P, q;       // params, elements per shard slice (P padded to W*q)
     size_t esz;         // sizeof(T)
-    ReplicaLayout rl_full, rl_fwd;
+    ReplicaLayout rl;
     // PS state
     float* theta;   // [W*q] full theta^+ (internal layout, contiguous shard slices)
     float* m;       // [q] own slice
@@ -119,6 +120,7 @@ struct gorila_ctx {
     float* dQ;
     float* part_fc4;   // [2][splits][512][B]
     float* part_w[3];  // conv wgrad partials
+    float* part_b;     // bias-gradient partials [4 layers][BIAS_CHUNKS][C]
     int split_w[3];
     int split_fc4;
     float* tmp_canon;  // [P]
@@ -131,6 +133,12 @@ struct gorila_ctx {
     std::vector<std::pair<int, size_t>> marks;
     double prof_ms[32] = {};
     uint64_t prof_steps = 0;
+    // CUDA-graph cache of whole rounds (gorila_round)
+    uint64_t* dev_round = nullptr;  // round counter the sampler reads
+    bool capturing = false;
+    std::map<std::vector<int64_t>, cudaGraphExec_t> graphs;
+    std::map<std::vector<int64_t>, uint64_t> graph_kernels;
+    std::map<std::vector<int64_t>, int> graph_seen;
 };
 
 namespace {
@@ -228,7 +236,7 @@ int eff_splits(bool fp32, int R, int splits) {
 
 // ------------------------------------------------------------------ one learner update
 template <typename T>
-gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
+gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int accumulate) {
     const gorila_config& cfg = ctx->cfg;
     Learner& Lr = ctx->learners[j];
     const int B = ctx->B, nA = ctx->nA;
@@ -240,8 +248,8 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
     const float* rf = ctx->rep_f[slot];
     const T* tt = P_<T>(Lr.tminus_t);
     const float* tf = Lr.tminus_f;
-    const ReplicaLayout& RL = ctx->rl_full;
-    const ReplicaLayout& RT = ctx->rl_fwd;
+    const ReplicaLayout& RL = ctx->rl;
+    const ReplicaLayout& RT = ctx->rl;
 
     T *s = P_<T>(ctx->s), *s2 = P_<T>(ctx->s2);
     T *a1 = P_<T>(ctx->a1), *a2 = P_<T>(ctx->a2), *a3 = P_<T>(ctx->a3);
@@ -254,8 +262,8 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
         dim3 grid((FRAME_BYTES / 16 + 255) / 256, B);
         uint2 key = make_uint2((uint32_t)cfg.seed, (uint32_t)(cfg.seed >> 32));
         k_sample<T><<<grid, 256, 0, st>>>(Lr.frames, Lr.a, Lr.r, Lr.d, cfg.replay_capacity, Lr.n_dev, key,
-                                          (uint32_t)(cfg.learner_id_base + j), round, B, s, s2, ctx->sa, ctx->sr,
-                                          ctx->sd, ctx->sidx);
+                                          (uint32_t)(cfg.learner_id_base + j), ctx->dev_round, B, s, s2, ctx->sa,
+                                          ctx->sr, ctx->sd, ctx->sidx);
         LAUNCHED();
     }
     mark(ctx, PH_SAMPLE);
@@ -325,13 +333,13 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
     }
     mark(ctx, PH_TD);
     // fc5 bwd: dW5, db5 into G; g4 = mask(dQ W5)
-    k_fc5_bwd<T><<<148, 256, 0, st>>>(ctx->dQ, a4, rf + RL.w5, B, nA, ctx->G, g4);
+    k_fc5_bwd<T><<<148, 256, 0, st>>>(ctx->dQ, a4, rf + RL.w5, B, nA, ctx->G, g4, accumulate);
     LAUNCHED();
     mark(ctx, PH_FC5B);
     // fc4 dgrad (i = k, j = b, red = n): g3[b][k] = mask(sum_n W4[n][k] g4[b][n])
     {
-        using LA = LdRows<T>; using LB = LdRows<T>; using EP = EpMaskT<T>;
-        GemmProb<LA, LB, EP> pr[1] = {{{rt + RL.w4t, FC4_OUT, FC4_IN, FC4_OUT}, {g4, FC4_OUT, B, FC4_OUT},
+        using LA = LdRowsMN<T>; using LB = LdRows<T>; using EP = EpMaskT<T>;
+        GemmProb<LA, LB, EP> pr[1] = {{{rt + RL.w4, FC4_IN, FC4_IN, FC4_OUT}, {g4, FC4_OUT, B, FC4_OUT},
                                        {g3, a3, FC4_IN, FC4_IN, B}}};
 #define FC4D(BN_) gemm<T, BN_>(ctx, pr, 1, FC4_IN, B, FC4_OUT, 1)
         DISPATCH_BN_BATCH(B, FC4D);
@@ -342,15 +350,15 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
     {
         using LA = LdRowsMN<T>; using LB = LdRowsMN<T>; using EP = EpAddT;
         GemmProb<LA, LB, EP> pr[1] = {{{a3, FC4_IN, FC4_IN, B}, {g4, FC4_OUT, FC4_OUT, B},
-                                       {ctx->G + OFF_W4, FC4_IN, FC4_IN, FC4_OUT}}};
+                                       {ctx->G + OFF_W4, FC4_IN, FC4_IN, FC4_OUT, accumulate}}};
         gemm<T, 256>(ctx, pr, 1, FC4_IN, FC4_OUT, B, 1);
     }
     mark(ctx, PH_FC4WG);
     // conv3 dgrad: g2 = mask(conv3^T(g3))
     {
-        using LA = LdDgrad<T, Conv3>; using LB = LdRows<T>; using EP = EpMask<T>;
+        using LA = LdDgrad<T, Conv3>; using LB = LdWdgradMN<T, Conv3>; using EP = EpMask<T>;
         const int M = B * H2 * H2;
-        GemmProb<LA, LB, EP> pr[1] = {{{g3, M}, {rt + RL.w3d, Conv3::RD, C2_OUT, Conv3::RD},
+        GemmProb<LA, LB, EP> pr[1] = {{{g3, M}, {rt + RL.w3},
                                        {g2, a2, C2_OUT, M, C2_OUT}}};
         gemm<T, 64>(ctx, pr, 1, M, C2_OUT, K3, 1);
     }
@@ -366,9 +374,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
     mark(ctx, PH_CONV3WG);
     // conv2 dgrad: g1 = mask(conv2^T(g2))
     {
-        using LA = LdDgrad<T, Conv2>; using LB = LdRows<T>; using EP = EpMask<T>;
+        using LA = LdDgrad<T, Conv2>; using LB = LdWdgradMN<T, Conv2>; using EP = EpMask<T>;
         const int M = B * H1 * H1;
-        GemmProb<LA, LB, EP> pr[1] = {{{g2, M}, {rt + RL.w2d, Conv2::RD, C1_OUT, Conv2::RD},
+        GemmProb<LA, LB, EP> pr[1] = {{{g2, M}, {rt + RL.w2},
                                        {g1, a1, C1_OUT, M, C1_OUT}}};
         gemm<T, 32>(ctx, pr, 1, M, C1_OUT, Conv2::RD, 1);
     }
@@ -391,8 +399,8 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
         gemm<T, 32>(ctx, pr, 1, K1, C1_OUT, Mred, ctx->split_w[0]);
     }
     mark(ctx, PH_CONV1WG);
-    // bias gradients b1..b4
-    k_bias_grad<T><<<C1_OUT + C2_OUT + C3_OUT + FC4_OUT, 256, 0, st>>>(g1, g2, g3, g4, B, ctx->G);
+    // bias gradients b1..b4 (coalesced partials; reduced by K10)
+    k_bias_partial<T><<<dim3(BIAS_CHUNKS, 4), 256, 0, st>>>(g1, g2, g3, g4, B, ctx->part_b);
     LAUNCHED();
     mark(ctx, PH_BIASG);
     // K10: fixed-order reduction of the conv wgrad partials into G
@@ -404,6 +412,15 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
         p.splits[2] = eff_splits(fp32, B * H3 * H3, ctx->split_w[2]);
         p.count[0] = (int64_t)C1_OUT * K1; p.count[1] = (int64_t)C2_OUT * K2; p.count[2] = (int64_t)C3_OUT * K3;
         p.off[0] = OFF_W1; p.off[1] = OFF_W2; p.off[2] = OFF_W3;
+        const int bc[4] = {C1_OUT, C2_OUT, C3_OUT, FC4_OUT};
+        const int64_t boff[4] = {OFF_B1, OFF_B2, OFF_B3, OFF_B4};
+        const float* bp = ctx->part_b;
+        for (int l = 0; l < 4; ++l) {
+            p.part[3 + l] = bp; p.splits[3 + l] = BIAS_CHUNKS; p.count[3 + l] = bc[l]; p.off[3 + l] = boff[l];
+            bp += BIAS_CHUNKS * bc[l];
+        }
+        p.nseg = 7;
+        p.accumulate = accumulate;
         k_wgrad_reduce<<<148 * 2, 256, 0, st>>>(p, ctx->G);
         LAUNCHED();
     }
@@ -413,19 +430,18 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j) {
 }
 
 template <typename T>
-gorila_status pack_replica(gorila_ctx* ctx, const float* theta_sliced, void* rt, float* rf, bool with_dgrad,
-                           const uint8_t* pred, uint64_t* vhist_dst) {
-    k_pack<T><<<148 * 4, 256, 0, ctx->stream>>>(theta_sliced, ctx->nA, P_<T>(rt), rf,
-                                                with_dgrad ? 1 : 0, pred, vhist_dst, ctx->V);
+gorila_status pack_replica(gorila_ctx* ctx, const float* theta, void* rt, float* rf, const uint8_t* pred,
+                           uint64_t* vhist_dst) {
+    k_pack<T><<<148 * 4, 256, 0, ctx->stream>>>(theta, ctx->nA, P_<T>(rt), rf, pred, vhist_dst, ctx->V);
     ctx->launches++;
     CU(cudaGetLastError());
     return GORILA_OK;
 }
 
-gorila_status pack_any(gorila_ctx* ctx, const float* theta_sliced, void* rt, float* rf, bool with_dgrad,
-                       const uint8_t* pred, uint64_t* vhist_dst) {
-    if (ctx->cfg.math == GORILA_MATH_FP32) return pack_replica<float>(ctx, theta_sliced, rt, rf, with_dgrad, pred, vhist_dst);
-    return pack_replica<__nv_bfloat16>(ctx, theta_sliced, rt, rf, with_dgrad, pred, vhist_dst);
+gorila_status pack_any(gorila_ctx* ctx, const float* theta, void* rt, float* rf, const uint8_t* pred,
+                       uint64_t* vhist_dst) {
+    if (ctx->cfg.math == GORILA_MATH_FP32) return pack_replica<float>(ctx, theta, rt, rf, pred, vhist_dst);
+    return pack_replica<__nv_bfloat16>(ctx, theta, rt, rf, pred, vhist_dst);
 }
 
 uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) {
@@ -434,7 +450,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     const int64_t P = param_count(nA);
     const int64_t q = round_up((P + W - 1) / W, 64);
     const size_t esz = cfg->math == GORILA_MATH_FP32 ? 4 : 2;
-    const ReplicaLayout rl_full = replica_layout(nA, true), rl_fwd = replica_layout(nA, false);
+    const ReplicaLayout rl = replica_layout(nA);
     const int H = std::max(1, cfg->history);
     const bool fp32 = cfg->math == GORILA_MATH_FP32;
     Carver c{base};
@@ -447,11 +463,12 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     uint64_t* rinfo = c.take<uint64_t>(4);
     uint32_t* nacc = c.take<uint32_t>(4);
     uint64_t* Vhist = c.take<uint64_t>(H);
+    uint64_t* dev_round = c.take<uint64_t>(1);
     std::vector<void*> rep_t(H);
     std::vector<float*> rep_f(H);
     for (int h = 0; h < H; ++h) {
-        rep_t[h] = c.take<uint8_t>(rl_full.n_t * esz);
-        rep_f[h] = c.take<float>(rl_full.n_f);
+        rep_t[h] = c.take<uint8_t>(rl.n_t * esz);
+        rep_f[h] = c.take<float>(rl.n_f);
     }
     std::vector<Learner> lrs(L);
     for (int j = 0; j < L; ++j) {
@@ -461,8 +478,8 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         l.r = c.take<float>(cfg->replay_capacity);
         l.d = c.take<uint8_t>(cfg->replay_capacity);
         l.n_dev = c.take<uint64_t>(1);
-        l.tminus_t = c.take<uint8_t>(rl_fwd.n_t * esz);
-        l.tminus_f = c.take<float>(rl_fwd.n_f);
+        l.tminus_t = c.take<uint8_t>(rl.n_t * esz);
+        l.tminus_f = c.take<float>(rl.n_f);
         l.stats = c.take<LearnerStats>(1);
         l.info = c.take<DevLearnerInfo>(1);
         l.Q = c.take<float>((int64_t)B * nA);
@@ -504,20 +521,22 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         split_w[l] = eff_splits(fp32, Mred[l], want);
         part_w[l] = c.take<float>((int64_t)split_w[l] * wcount[l]);
     }
+    float* part_b = c.take<float>((int64_t)BIAS_CHUNKS * (C1_OUT + C2_OUT + C3_OUT + FC4_OUT));
     float* tmp_canon = c.take<float>(P);
     float* tmp_int = c.take<float>(W * q);
     if (ctx) {
         ctx->nA = nA; ctx->B = B; ctx->L = L; ctx->W = W; ctx->P = P; ctx->q = q; ctx->esz = esz;
-        ctx->rl_full = rl_full; ctx->rl_fwd = rl_fwd; ctx->H = H;
+        ctx->rl = rl; ctx->H = H;
         ctx->theta = theta; ctx->m = m; ctx->v = v; ctx->G = G; ctx->counts = counts; ctx->V = V;
         ctx->round_info = rinfo;
-        ctx->n_acc_local = nacc; ctx->Vhist = Vhist; ctx->rep_t = rep_t; ctx->rep_f = rep_f; ctx->learners = lrs;
+        ctx->n_acc_local = nacc; ctx->Vhist = Vhist; ctx->dev_round = dev_round; ctx->rep_t = rep_t; ctx->rep_f = rep_f; ctx->learners = lrs;
         ctx->s = s; ctx->s2 = s2; ctx->a1 = a1; ctx->a2 = a2; ctx->a3 = a3; ctx->a4 = a4;
         ctx->t1 = t1; ctx->t2 = t2; ctx->t3 = t3; ctx->t4 = t4;
         ctx->g1 = g1; ctx->g2 = g2; ctx->g3 = g3; ctx->g4 = g4;
         ctx->sa = sa; ctx->sd = sd; ctx->sr = sr; ctx->sidx = sidx; ctx->dQ = dQ;
         ctx->part_fc4 = part_fc4; ctx->split_fc4 = split_fc4;
         for (int l = 0; l < 3; ++l) { ctx->part_w[l] = part_w[l]; ctx->split_w[l] = split_w[l]; }
+        ctx->part_b = part_b;
         ctx->tmp_canon = tmp_canon; ctx->tmp_int = tmp_int;
     }
     return c.off + 256;
@@ -632,9 +651,9 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     ctx->launches++;
     // replica slot 0 and every learner's theta^- (Alg.1 P:113 theta^- = theta)
     gorila_status s;
-    if ((s = pack_any(ctx, ctx->theta, ctx->rep_t[0], ctx->rep_f[0], true, nullptr, ctx->Vhist)) != GORILA_OK) return s;
+    if ((s = pack_any(ctx, ctx->theta, ctx->rep_t[0], ctx->rep_f[0], nullptr, ctx->Vhist)) != GORILA_OK) return s;
     for (auto& l : ctx->learners)
-        if ((s = pack_any(ctx, ctx->theta, l.tminus_t, l.tminus_f, false, nullptr, nullptr)) != GORILA_OK) return s;
+        if ((s = pack_any(ctx, ctx->theta, l.tminus_t, l.tminus_f, nullptr, nullptr)) != GORILA_OK) return s;
     if (cfg->world > 1) {
         ncclUniqueId id;
         memcpy(&id, cfg->nccl_unique_id, sizeof(id));
@@ -649,6 +668,7 @@ void gorila_destroy(gorila_ctx* ctx) {
     if (!ctx) return;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
     if (ctx->comm) {
         if (ctx->poisoned) ncclCommAbort(ctx->comm);
         else ncclCommDestroy(ctx->comm);
@@ -698,16 +718,18 @@ gorila_status replay_sample(gorila_ctx* ctx, int32_t learner, uint64_t round, in
     cudaStream_t st = ctx->stream;
     const gorila_config& cfg = ctx->cfg;
     // sample into u8-valued T buffers of the scratch (same kernel as learner_step)
+    k_set_u64<<<1, 1, 0, st>>>(ctx->dev_round, round);
+    ctx->launches++;
     dim3 grid((FRAME_BYTES / 16 + 255) / 256, B);
     uint2 key = make_uint2((uint32_t)cfg.seed, (uint32_t)(cfg.seed >> 32));
     if (cfg.math == GORILA_MATH_FP32)
         k_sample<float><<<grid, 256, 0, st>>>(l.frames, l.a, l.r, l.d, cfg.replay_capacity, l.n_dev, key,
-                                              (uint32_t)(cfg.learner_id_base + learner), round, B, (float*)ctx->s,
+                                              (uint32_t)(cfg.learner_id_base + learner), ctx->dev_round, B, (float*)ctx->s,
                                               (float*)ctx->s2, ctx->sa, ctx->sr, ctx->sd, ctx->sidx);
     else
         k_sample<__nv_bfloat16><<<grid, 256, 0, st>>>(l.frames, l.a, l.r, l.d, cfg.replay_capacity, l.n_dev, key,
-                                                      (uint32_t)(cfg.learner_id_base + learner), round, B,
-                                                      (__nv_bfloat16*)ctx->s, (__nv_bfloat16*)ctx->s2, ctx->sa,
+                                                      (uint32_t)(cfg.learner_id_base + learner), ctx->dev_round,
+                                                      B, (__nv_bfloat16*)ctx->s, (__nv_bfloat16*)ctx->s2, ctx->sa,
                                                       ctx->sr, ctx->sd, ctx->sidx);
     ctx->launches++;
     CU(cudaGetLastError());
@@ -756,9 +778,13 @@ gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
     cudaStream_t st = ctx->stream;
     mark(ctx, -1);
     ctx->prof_steps += ctx->prof ? 1 : 0;
-    CU(cudaMemsetAsync(ctx->G, 0, sizeof(float) * ctx->W * ctx->q, st));
     CU(cudaMemsetAsync(ctx->n_acc_local, 0, sizeof(uint32_t), st));
+    if (!ctx->capturing) {  // a captured round reads / advances the device counter instead
+        k_set_u64<<<1, 1, 0, st>>>(ctx->dev_round, round);
+        ctx->launches++;
+    }
     mark(ctx, PH_STEP_MISC);
+    int ran = 0;  // the first learner that runs stores G, later ones accumulate (no memset)
     for (int i = 0; i < n; ++i) {
         const int j = learners[i];
         Learner& l = ctx->learners[j];
@@ -769,10 +795,12 @@ gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
             continue;
         }
         const int s_j = staleness ? staleness[i] : 0;
-        gorila_status s = ctx->cfg.math == GORILA_MATH_FP32 ? run_learner<float>(ctx, j, round, s_j)
-                                                             : run_learner<__nv_bfloat16>(ctx, j, round, s_j);
+        gorila_status s = ctx->cfg.math == GORILA_MATH_FP32 ? run_learner<float>(ctx, j, round, s_j, ran > 0)
+                                                             : run_learner<__nv_bfloat16>(ctx, j, round, s_j, ran > 0);
         if (s != GORILA_OK) return s;
+        ++ran;
     }
+    if (ran == 0) CU(cudaMemsetAsync(ctx->G, 0, sizeof(float) * ctx->W * ctx->q, st));
     k_write_counts<<<1, 64, 0, st>>>(ctx->counts, ctx->W, ctx->n_acc_local);
     ctx->launches++;
     mark(ctx, PH_STEP_MISC);
@@ -809,15 +837,25 @@ gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info*
     p.lr = ctx->cfg.lr; p.rho = ctx->cfg.rms_rho; p.eps = ctx->cfg.rms_eps; p.ada_eps = ctx->cfg.ada_eps;
     p.V = ctx->V;
     p.round_info = ctx->round_info;
-    k_apply<<<148 * 4, 256, 0, st>>>(p);
+    const int slot = (int)((round + 1) % (uint64_t)ctx->H);
+    p.nA = ctx->nA;
+    p.base = (int64_t)r * ctx->q;
+    if (W == 1) {  // the optimizer emits the next round's replica directly (no separate pack)
+        p.rep_t = ctx->rep_t[slot];
+        p.rep_f = ctx->rep_f[slot];
+        p.vhist_dst = ctx->Vhist + slot;
+    }
+    if (ctx->cfg.math == GORILA_MATH_FP32) k_apply<float><<<148 * 4, 256, 0, st>>>(p);
+    else k_apply<__nv_bfloat16><<<148 * 4, 256, 0, st>>>(p);
     ctx->launches++;
     mark(ctx, PH_APPLY);
-    if (W > 1) NC(ncclAllGather(p.theta, ctx->theta, ctx->q, ncclFloat, ctx->comm, st));
-    mark(ctx, PH_AG);
-    const int slot = (int)((round + 1) % (uint64_t)ctx->H);
-    gorila_status s = pack_any(ctx, ctx->theta, ctx->rep_t[slot], ctx->rep_f[slot], true, nullptr, ctx->Vhist + slot);
-    if (s != GORILA_OK) return s;
-    mark(ctx, PH_PACK);
+    if (W > 1) {
+        NC(ncclAllGather(p.theta, ctx->theta, ctx->q, ncclFloat, ctx->comm, st));
+        mark(ctx, PH_AG);
+        gorila_status s = pack_any(ctx, ctx->theta, ctx->rep_t[slot], ctx->rep_f[slot], nullptr, ctx->Vhist + slot);
+        if (s != GORILA_OK) return s;
+        mark(ctx, PH_PACK);
+    }
     if (info_out) {
         uint64_t tmp[3];
         CU(cudaMemcpyAsync(tmp, ctx->round_info, sizeof(tmp), cudaMemcpyDeviceToHost, st));
@@ -843,10 +881,89 @@ gorila_status sync_target(gorila_ctx* ctx, const int32_t* learners, int32_t n, i
         Learner& l = ctx->learners[learners[i]];
         k_sync_decide<<<1, 1, 0, st>>>(l.stats, ctx->V, ctx->cfg.target_period, force, l.sync_flag);
         ctx->launches++;
-        if ((s = pack_any(ctx, ctx->theta, l.tminus_t, l.tminus_f, false, l.sync_flag, nullptr)) != GORILA_OK) return s;
+        if ((s = pack_any(ctx, ctx->theta, l.tminus_t, l.tminus_f, l.sync_flag, nullptr)) != GORILA_OK) return s;
         if (synced_out) CU(cudaMemcpyAsync(&synced_out[i], l.sync_flag, 1, cudaMemcpyDeviceToHost, st));
     }
     mark(ctx, PH_SYNC);
+    CU(cudaGetLastError());
+    return GORILA_OK;
+}
+
+gorila_status gorila_round(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
+                           const int32_t* staleness, gorila_learner_info* info_out, gorila_round_info* round_info_out,
+                           uint8_t* synced_out) {
+    if (!ctx) return fail(GORILA_E_INVALID, "null context");
+    if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned");
+    if (!learners || n < 1 || n > ctx->L) return fail(GORILA_E_SHAPE, "bad learner list");
+    cudaStream_t st = ctx->stream;
+    bool graphable = !ctx->prof;
+    std::vector<int64_t> key;
+    for (int i = 0; i < n; ++i) {
+        if (learners[i] < 0 || learners[i] >= ctx->L) return fail(GORILA_E_RANGE, "learner id out of range");
+        const Learner& l = ctx->learners[learners[i]];
+        const int64_t size = std::min<int64_t>(l.n_host, ctx->cfg.replay_capacity);
+        if (size - 1 < std::max<int64_t>(1, ctx->cfg.min_replay)) graphable = false;
+        const int s_i = staleness ? staleness[i] : 0;
+        if ((uint64_t)s_i > round) graphable = false;
+        key.push_back(learners[i]);
+        key.push_back(s_i);
+    }
+    key.push_back((int64_t)(round % (uint64_t)ctx->H));
+    gorila_status s;
+    auto eager = [&]() -> gorila_status {
+        gorila_status r = learner_step(ctx, learners, n, round, staleness, nullptr);
+        if (r != GORILA_OK) return r;
+        if ((r = ps_apply_shard(ctx, round, nullptr)) != GORILA_OK) return r;
+        return sync_target(ctx, learners, n, 0, nullptr);
+    };
+    auto it = graphable ? ctx->graphs.find(key) : ctx->graphs.end();
+    if (it != ctx->graphs.end()) {
+        k_set_u64<<<1, 1, 0, st>>>(ctx->dev_round, round);
+        ctx->launches++;
+        CU(cudaGraphLaunch(it->second, st));
+        ctx->launches += ctx->graph_kernels[key];
+    } else if (!graphable || ctx->graph_seen[key]++ == 0) {
+        if ((s = eager()) != GORILA_OK) return s;  // first use: eager (also sets lazy kernel attributes)
+    } else {
+        // capture the round once; the captured sampler reads ctx->dev_round, set before each replay
+        k_set_u64<<<1, 1, 0, st>>>(ctx->dev_round, round);
+        ctx->launches++;
+        CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+        ctx->capturing = true;
+        const uint64_t launches0 = ctx->launches;
+        s = eager();
+        ctx->capturing = false;
+        cudaGraph_t graph = nullptr;
+        cudaError_t ce = cudaStreamEndCapture(st, &graph);
+        if (s != GORILA_OK) {
+            if (graph) cudaGraphDestroy(graph);
+            return s;
+        }
+        CU(ce);
+        cudaGraphExec_t exec = nullptr;
+        CU(cudaGraphInstantiate(&exec, graph, 0));
+        cudaGraphDestroy(graph);
+        ctx->graphs[key] = exec;
+        ctx->graph_kernels[key] = ctx->launches - launches0;
+        CU(cudaGraphLaunch(exec, st));
+    }
+    if (info_out)
+        for (int i = 0; i < n; ++i)
+            CU(cudaMemcpyAsync(&info_out[i], ctx->learners[learners[i]].info, sizeof(gorila_learner_info),
+                               cudaMemcpyDeviceToHost, st));
+    if (synced_out)
+        for (int i = 0; i < n; ++i)
+            CU(cudaMemcpyAsync(&synced_out[i], ctx->learners[learners[i]].sync_flag, 1, cudaMemcpyDeviceToHost, st));
+    if (round_info_out) {
+        uint64_t tmp[3];
+        CU(cudaMemcpyAsync(tmp, ctx->round_info, sizeof(tmp), cudaMemcpyDeviceToHost, st));
+        CU(cudaStreamSynchronize(st));
+        round_info_out->n_accepted = (uint32_t)tmp[0];
+        round_info_out->pad_ = 0;
+        round_info_out->version_before = tmp[1];
+        round_info_out->version_after = tmp[2];
+    }
+    if (info_out || synced_out) CU(cudaStreamSynchronize(st));
     CU(cudaGetLastError());
     return GORILA_OK;
 }
@@ -898,7 +1015,7 @@ gorila_status gorila_set_state(gorila_ctx* ctx, const float* theta, const float*
     ctx->launches++;
     // every replica slot = the new theta (teacher forcing restarts the history)
     for (int h = 0; h < ctx->H; ++h) {
-        gorila_status s = pack_any(ctx, ctx->theta, ctx->rep_t[h], ctx->rep_f[h], true, nullptr, ctx->Vhist + h);
+        gorila_status s = pack_any(ctx, ctx->theta, ctx->rep_t[h], ctx->rep_f[h], nullptr, ctx->Vhist + h);
         if (s != GORILA_OK) return s;
     }
     CU(cudaStreamSynchronize(st));
@@ -918,7 +1035,7 @@ gorila_status gorila_get_learner_state(gorila_ctx* ctx, int32_t learner, float* 
     }
     if (theta_minus) {
         // unpack the fwd replica (T) + fp32 area back to canonical fp32 on the host
-        const ReplicaLayout& R = ctx->rl_fwd;
+        const ReplicaLayout& R = ctx->rl;
         std::vector<uint8_t> t(R.n_t * ctx->esz);
         std::vector<float> f(R.n_f);
         CU(cudaMemcpy(t.data(), l.tminus_t, t.size(), cudaMemcpyDeviceToHost));
@@ -961,7 +1078,7 @@ gorila_status gorila_set_learner_state(gorila_ctx* ctx, int32_t learner, const f
         CU(cudaMemsetAsync(ctx->tmp_int, 0, sizeof(float) * ctx->W * ctx->q, st));
         k_convert<<<148 * 4, 256, 0, st>>>(ctx->tmp_canon, ctx->tmp_int, ctx->P, 0);
         ctx->launches++;
-        if ((s = pack_any(ctx, ctx->tmp_int, l.tminus_t, l.tminus_f, false, nullptr, nullptr)) != GORILA_OK) return s;
+        if ((s = pack_any(ctx, ctx->tmp_int, l.tminus_t, l.tminus_f, nullptr, nullptr)) != GORILA_OK) return s;
         CU(cudaStreamSynchronize(st));
     }
     return GORILA_OK;

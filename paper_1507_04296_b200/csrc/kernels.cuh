@@ -18,11 +18,13 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_sample(const uint8_t* __restrict__ frames, const uint8_t* __restrict__ ring_a,
                                                 const float* __restrict__ ring_r, const uint8_t* __restrict__ ring_d,
                                                 int64_t C, const uint64_t* __restrict__ ring_n, uint2 key,
-                                                uint32_t learner_gid, uint64_t round, int B, T* __restrict__ s_out,
+                                                uint32_t learner_gid, const uint64_t* __restrict__ round_ptr, int B,
+                                                T* __restrict__ s_out,
                                                 T* __restrict__ s2_out, uint8_t* __restrict__ a_out,
                                                 float* __restrict__ r_out, uint8_t* __restrict__ d_out,
                                                 int64_t* __restrict__ idx_out) {
     const int b = blockIdx.y;
+    const uint64_t round = *round_ptr;  // device-resident round counter (graph replay friendly)
     const int64_t n = (int64_t)*ring_n;
     const int64_t size = n < C ? n : C;
     const uint64_t M = (uint64_t)(size - 1);
@@ -263,19 +265,19 @@ __global__ void k_mark_not_ready(DevLearnerInfo* info, const LearnerStats* st) {
 // g4[b][n] = round_T((sum_a dQ[b][a] W5[a][n]) * 1[a4[b][n] > 0])
 template <typename T>
 __global__ void k_fc5_bwd(const float* __restrict__ dQ, const float* __restrict__ a4, const float* __restrict__ w5,
-                          int B, int nA, float* __restrict__ G, T* __restrict__ g4) {
+                          int B, int nA, float* __restrict__ G, T* __restrict__ g4, int accumulate) {
     const int n_w = nA * FC4_OUT, n_b = nA, n_g = B * FC4_OUT;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_w + n_b + n_g; e += gridDim.x * blockDim.x) {
         if (e < n_w) {
             int a = e / FC4_OUT, n = e - a * FC4_OUT;
             float acc = 0.f;
             for (int b = 0; b < B; ++b) acc = fmaf(dQ[b * nA + a], a4[(int64_t)b * FC4_OUT + n], acc);
-            G[OFF_W5 + e] += acc;
+            G[OFF_W5 + e] = accumulate ? G[OFF_W5 + e] + acc : acc;
         } else if (e < n_w + n_b) {
             int a = e - n_w;
             float acc = 0.f;
             for (int b = 0; b < B; ++b) acc += dQ[b * nA + a];
-            G[off_b5(nA) + a] += acc;
+            G[off_b5(nA) + a] = accumulate ? G[off_b5(nA) + a] + acc : acc;
         } else {
             int f = e - n_w - n_b, b = f / FC4_OUT, n = f - b * FC4_OUT;
             float acc = 0.f;
@@ -286,51 +288,62 @@ __global__ void k_fc5_bwd(const float* __restrict__ dQ, const float* __restrict_
 }
 
 // ------------------------------------------------------------------------- bias gradients
-// db_l[o] += sum_m g_l[m][o] for layers 1..4 (block = one output channel, fixed-order reduction)
+// db_l[o] = sum_m g_l[m][o], layers 1..4: block (chunk, l) sums rows [chunk*rows_per, ...) with
+// coalesced row reads and a fixed-order in-block reduction -> part[l][chunk][o]; K10 sums chunks.
+constexpr int BIAS_CHUNKS = 32;
 template <typename T>
-__global__ void __launch_bounds__(256) k_bias_grad(const T* __restrict__ g1, const T* __restrict__ g2,
-                                                   const T* __restrict__ g3, const T* __restrict__ g4, int B,
-                                                   float* __restrict__ G) {
+__global__ void __launch_bounds__(256) k_bias_partial(const T* __restrict__ g1, const T* __restrict__ g2,
+                                                      const T* __restrict__ g3, const T* __restrict__ g4, int B,
+                                                      float* __restrict__ part) {
     __shared__ float red[256];
-    int o = blockIdx.x;
-    const T* g;
-    int C, rows;
-    int64_t off;
-    if (o < C1_OUT) { g = g1; C = C1_OUT; rows = B * H1 * H1; off = OFF_B1; }
-    else if ((o -= C1_OUT) < C2_OUT) { g = g2; C = C2_OUT; rows = B * H2 * H2; off = OFF_B2; }
-    else if ((o -= C2_OUT) < C3_OUT) { g = g3; C = C3_OUT; rows = B * H3 * H3; off = OFF_B3; }
-    else { o -= C3_OUT; g = g4; C = FC4_OUT; rows = B; off = OFF_B4; }
-    float acc = 0.f;
-    for (int m = threadIdx.x; m < rows; m += blockDim.x) acc += tof(g[(int64_t)m * C + o]);
-    red[threadIdx.x] = acc;
-    __syncthreads();
-    for (int w = 128; w > 0; w >>= 1) {
-        if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    const int l = blockIdx.y, chunk = blockIdx.x;
+    const T* g = l == 0 ? g1 : l == 1 ? g2 : l == 2 ? g3 : g4;
+    const int C = l == 0 ? C1_OUT : l == 3 ? FC4_OUT : C2_OUT;
+    const int rows = B * (l == 0 ? H1 * H1 : l == 1 ? H2 * H2 : l == 2 ? H3 * H3 : 1);
+    float* out = part + (l == 0 ? 0 : l == 1 ? BIAS_CHUNKS * C1_OUT : l == 2 ? BIAS_CHUNKS * (C1_OUT + C2_OUT)
+                                                                             : BIAS_CHUNKS * (C1_OUT + 2 * C2_OUT));
+    const int per = (rows + BIAS_CHUNKS - 1) / BIAS_CHUNKS;
+    const int r0 = chunk * per, r1 = min(rows, r0 + per);
+    for (int c0 = 0; c0 < C; c0 += 256) {
+        const int cw = min(256, C - c0);
+        const int RG = 256 / cw;
+        const int c = c0 + threadIdx.x % cw, rg = threadIdx.x / cw;
+        float acc = 0.f;
+        if (rg < RG)
+            for (int r = r0 + rg; r < r1; r += RG) acc += tof(g[(int64_t)r * C + c]);
+        red[threadIdx.x] = acc;
+        __syncthreads();
+        if (threadIdx.x < cw) {
+            float t = 0.f;
+            for (int q = 0; q < RG; ++q) t += red[threadIdx.x + q * cw];
+            out[chunk * C + c0 + threadIdx.x] = t;
+        }
         __syncthreads();
     }
-    if (threadIdx.x == 0) G[off + o] += red[0];
 }
 
 // ------------------------------------------------------------------------- K10 wgrad reduce
-// G[W_l] += sum_s partial_l[s][.] in split order, for the three conv layers
+// G[seg] (+)= sum_s partial_seg[s][.] in split order, for the conv weights and the four biases
 struct WgradReduceParams {
-    const float* part[3];
-    int splits[3];
-    int64_t count[3];
-    int64_t off[3];
+    const float* part[7];
+    int splits[7];
+    int64_t count[7];
+    int64_t off[7];
+    int nseg, accumulate;
 };
 __global__ void k_wgrad_reduce(WgradReduceParams p, float* __restrict__ G) {
-    const int64_t total = p.count[0] + p.count[1] + p.count[2];
+    int64_t total = 0;
+    for (int l = 0; l < p.nseg; ++l) total += p.count[l];
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         int l = 0;
         int64_t f = e;
-        if (f >= p.count[0]) { f -= p.count[0]; l = 1; if (f >= p.count[1]) { f -= p.count[1]; l = 2; } }
+        while (f >= p.count[l]) f -= p.count[l++];
         float acc = 0.f;
         for (int s = 0; s < p.splits[l]; ++s) acc += p.part[l][(int64_t)s * p.count[l] + f];
-        G[p.off[l] + f] += acc;
+        float* dst = G + p.off[l] + f;
+        *dst = p.accumulate ? *dst + acc : acc;
     }
 }
-
 
 // ------------------------------------------------------------------------- PS apply (K11)
 struct ApplyParams {
@@ -344,9 +357,34 @@ struct ApplyParams {
     float lr, rho, eps, ada_eps;
     uint64_t* V;
     uint64_t* round_info;  // [n_acc, V_before, V_after]
+    // fused replica emission (world == 1): theta -> replica slot for the next round
+    void* rep_t;           // T area (nullptr: no emission)
+    float* rep_f;
+    uint64_t* vhist_dst;
+    int nA;
+    int64_t base;          // internal index of this slice's element 0
 };
 // Centered RMSProp (reading R2) / AdaGrad on the mean of the accepted gradients
 // (reading R12, R25); V += |Acc|. float4-vectorised, grid-stride.
+template <typename T>
+GORILA_DEV void emit4(const ApplyParams& p, int64_t e4, const float* tv) {
+    const ReplicaLayout L = replica_layout(p.nA);
+    const int64_t slot = replica_slot(L, p.base + 4 * e4);
+    if (slot >= 0) {
+        T* dst = reinterpret_cast<T*>(p.rep_t) + slot;
+        if constexpr (sizeof(T) == 2) {
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(tv[0], tv[1]), h1 = __floats2bfloat162_rn(tv[2], tv[3]);
+            *reinterpret_cast<uint2*>(dst) =
+                make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+        } else {
+            *reinterpret_cast<float4*>(dst) = make_float4(tv[0], tv[1], tv[2], tv[3]);
+        }
+    } else {
+        *reinterpret_cast<float4*>(p.rep_f + (-slot - 1)) = make_float4(tv[0], tv[1], tv[2], tv[3]);
+    }
+}
+
+template <typename T>
 __global__ void __launch_bounds__(256) k_apply(ApplyParams p) {
     const float cnt = *p.count;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
@@ -356,13 +394,21 @@ __global__ void __launch_bounds__(256) k_apply(ApplyParams p) {
         p.round_info[1] = v0;
         p.round_info[2] = v0 + n_acc;
         *p.V = v0 + n_acc;
+        if (p.vhist_dst) *p.vhist_dst = v0 + n_acc;
     }
-    if (!(cnt > 0.5f)) return;
-    const float inv = 1.0f / cnt;
-    const int64_t n4 = p.n_real / 4;
+    const bool update = cnt > 0.5f;
+    const float inv = update ? 1.0f / cnt : 0.f;
+    const int64_t n4 = (p.n_real + 3) / 4;  // slices are padded to 64 elements (zeros, never read back)
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n4; e += (int64_t)gridDim.x * blockDim.x) {
-        float4 g = reinterpret_cast<const float4*>(p.g)[e];
         float4 th = reinterpret_cast<float4*>(p.theta)[e];
+        if (!update) {  // nothing accepted: theta, m, v unchanged; still emit the next replica
+            if (p.rep_t) {
+                const float tv[4] = {th.x, th.y, th.z, th.w};
+                emit4<T>(p, e, tv);
+            }
+            continue;
+        }
+        float4 g = reinterpret_cast<const float4*>(p.g)[e];
         float4 m = reinterpret_cast<float4*>(p.m)[e];
         float4 v = reinterpret_cast<float4*>(p.v)[e];
         float gv[4] = {g.x * inv, g.y * inv, g.z * inv, g.w * inv};
@@ -381,19 +427,7 @@ __global__ void __launch_bounds__(256) k_apply(ApplyParams p) {
         reinterpret_cast<float4*>(p.theta)[e] = make_float4(tv[0], tv[1], tv[2], tv[3]);
         reinterpret_cast<float4*>(p.m)[e] = make_float4(mv[0], mv[1], mv[2], mv[3]);
         reinterpret_cast<float4*>(p.v)[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
-    }
-    // tail (n_real % 4)
-    for (int64_t e = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < p.n_real;
-         e += (int64_t)gridDim.x * blockDim.x) {
-        float gv = p.g[e] * inv;
-        if (p.optimizer == 0) {
-            p.m[e] = p.rho * p.m[e] + (1.f - p.rho) * gv;
-            p.v[e] = p.rho * p.v[e] + (1.f - p.rho) * gv * gv;
-            p.theta[e] -= p.lr * gv / sqrtf(p.v[e] - p.m[e] * p.m[e] + p.eps);
-        } else {
-            p.v[e] += gv * gv;
-            p.theta[e] -= p.lr * gv / (sqrtf(p.v[e]) + p.ada_eps);
-        }
+        if (p.rep_t) emit4<T>(p, e, tv);
     }
 }
 
@@ -404,52 +438,19 @@ __global__ void k_write_counts(float* counts, int W, const uint32_t* n_acc_local
 }
 
 // ------------------------------------------------------------------------- replica pack
-// theta^+ (sliced, internal order, fp32) -> packed replica in T (+ fp32 area).
-// with_dgrad also writes the transposed dgrad copies. pred (nullable): skip unless *pred.
+// theta^+ (internal order, fp32) -> replica (T area + fp32 area). pred (nullable): skip unless *pred.
 template <typename T>
-__global__ void k_pack(const float* __restrict__ theta, int nA, T* __restrict__ rt,
-                       float* __restrict__ rf, int with_dgrad, const uint8_t* __restrict__ pred,
-                       uint64_t* __restrict__ vhist_dst, const uint64_t* __restrict__ V) {
+__global__ void k_pack(const float* __restrict__ theta, int nA, T* __restrict__ rt, float* __restrict__ rf,
+                       const uint8_t* __restrict__ pred, uint64_t* __restrict__ vhist_dst,
+                       const uint64_t* __restrict__ V) {
     if (pred && !*pred) return;
-    const ReplicaLayout L = replica_layout(nA, with_dgrad != 0);
+    const ReplicaLayout L = replica_layout(nA);
     const int64_t P = param_count(nA);
     if (vhist_dst && blockIdx.x == 0 && threadIdx.x == 0) *vhist_dst = *V;
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
-        const float w = theta[i];
-        if (i < OFF_B1) {
-            rt[L.w1 + i] = fromf<T>(w);
-        } else if (i < OFF_W2) {
-            rf[L.b1 + (i - OFF_B1)] = w;
-        } else if (i < OFF_B2) {
-            int64_t j = i - OFF_W2;
-            rt[L.w2 + j] = fromf<T>(w);
-            if (with_dgrad) {  // (o, ky, kx, c) -> (c, ky, kx, o)
-                int o = (int)(j / K2), r = (int)(j % K2), t = r / C1_OUT, c = r % C1_OUT;
-                rt[L.w2d + (int64_t)c * (C2_K * C2_K * C2_OUT) + t * C2_OUT + o] = fromf<T>(w);
-            }
-        } else if (i < OFF_W3) {
-            rf[L.b2 + (i - OFF_B2)] = w;
-        } else if (i < OFF_B3) {
-            int64_t j = i - OFF_W3;
-            rt[L.w3 + j] = fromf<T>(w);
-            if (with_dgrad) {
-                int o = (int)(j / K3), r = (int)(j % K3), t = r / C2_OUT, c = r % C2_OUT;
-                rt[L.w3d + (int64_t)c * K3 + t * C3_OUT + o] = fromf<T>(w);
-            }
-        } else if (i < OFF_W4) {
-            rf[L.b3 + (i - OFF_B3)] = w;
-        } else if (i < OFF_B4) {
-            int64_t j = i - OFF_W4;
-            rt[L.w4 + j] = fromf<T>(w);
-            if (with_dgrad) {
-                int64_t n = j / FC4_IN, k = j % FC4_IN;
-                rt[L.w4t + k * FC4_OUT + n] = fromf<T>(w);
-            }
-        } else if (i < OFF_W5) {
-            rf[L.b4 + (i - OFF_B4)] = w;
-        } else {
-            rf[L.w5 + (i - OFF_W5)] = w;  // W5 then b5 are contiguous in both layouts
-        }
+        const int64_t slot = replica_slot(L, i);
+        if (slot >= 0) rt[slot] = fromf<T>(theta[i]);
+        else rf[-slot - 1] = theta[i];
     }
 }
 
@@ -473,5 +474,6 @@ __global__ void k_convert(const float* __restrict__ src, float* __restrict__ dst
 }
 
 __global__ void k_set_u64(uint64_t* dst, uint64_t v) { *dst = v; }
+__global__ void k_inc_u64(uint64_t* dst) { *dst += 1; }
 
 }  // namespace gorila

@@ -64,33 +64,40 @@ __host__ __device__ inline int64_t canon_of_internal(int64_t i) {
 }
 
 // ------------------------------------------------------------ packed replica
-// A replica ("what the kernels read") of theta in element type T, plus an fp32 area.
-//   fwd:   w1 [32][256], w2 [64][512], w3 [64][576], w4 [512][3136]  (internal order)
-//   dgrad: w2d [32][4][4][64] = (c,ky,kx,o), w3d [64][3][3][64] = (c,ky,kx,o), w4t [3136][512]
-//   fp32:  b1 b2 b3 b4 w5 [nA][512] b5
+// A replica ("what the kernels read") of theta: the conv / fc4 weights in element type T
+// (internal KRSC order; the backward reads the same copy through MN-major descriptors),
+// and an fp32 area with the biases and fc5.
+//   T:    w1 [32][256], w2 [64][512], w3 [64][576], w4 [512][3136]
+//   fp32: b1 b2 b3 b4 w5 [nA][512] b5
 struct ReplicaLayout {
-    int64_t w1, w2, w3, w4, w2d, w3d, w4t, n_t;  // element offsets / count in T
-    int64_t b1, b2, b3, b4, w5, b5, n_f;         // element offsets / count in the fp32 area
+    int64_t w1, w2, w3, w4, n_t;     // element offsets / count in T
+    int64_t b1, b2, b3, b4, w5, b5, n_f;  // element offsets / count in the fp32 area
 };
-__host__ __device__ inline ReplicaLayout replica_layout(int nA, bool with_dgrad) {
+__host__ __device__ inline ReplicaLayout replica_layout(int nA) {
     ReplicaLayout L{};
     L.w1 = 0;
     L.w2 = L.w1 + (int64_t)C1_OUT * K1;
     L.w3 = L.w2 + (int64_t)C2_OUT * K2;
     L.w4 = L.w3 + (int64_t)C3_OUT * K3;
-    int64_t e = L.w4 + (int64_t)FC4_OUT * FC4_IN;
-    if (with_dgrad) {
-        L.w2d = e; e += (int64_t)C2_OUT * K2;
-        L.w3d = e; e += (int64_t)C3_OUT * K3;
-        L.w4t = e; e += (int64_t)FC4_OUT * FC4_IN;
-    } else {
-        L.w2d = L.w3d = L.w4t = -1;
-    }
-    L.n_t = (e + 127) / 128 * 128;
+    L.n_t = (L.w4 + (int64_t)FC4_OUT * FC4_IN + 127) / 128 * 128;
     L.b1 = 0; L.b2 = 32; L.b3 = 96; L.b4 = 160; L.w5 = 672;
     L.b5 = L.w5 + (int64_t)nA * FC4_OUT;
-    L.n_f = (L.b5 + nA + 63) / 64 * 64;
+    L.n_f = (L.b5 + nA + 4 + 63) / 64 * 64;  // room for the 4-wide tail of the optimizer's emission
     return L;
+}
+
+// where internal element i lives in the replica: returns the T-area offset (>= 0) or
+// -(fp32-area offset) - 1
+__host__ __device__ inline int64_t replica_slot(const ReplicaLayout& L, int64_t i) {
+    if (i < OFF_B1) return L.w1 + i;
+    if (i < OFF_W2) return -(L.b1 + (i - OFF_B1)) - 1;
+    if (i < OFF_B2) return L.w2 + (i - OFF_W2);
+    if (i < OFF_W3) return -(L.b2 + (i - OFF_B2)) - 1;
+    if (i < OFF_B3) return L.w3 + (i - OFF_W3);
+    if (i < OFF_W4) return -(L.b3 + (i - OFF_B3)) - 1;
+    if (i < OFF_B4) return L.w4 + (i - OFF_W4);
+    if (i < OFF_W5) return -(L.b4 + (i - OFF_B4)) - 1;
+    return -(L.w5 + (i - OFF_W5)) - 1;  // W5 then b5 are contiguous in both layouts
 }
 
 }  // namespace gorila

@@ -61,7 +61,7 @@ EXPORTS = ["gorila_param_count", "gorila_workspace_bytes", "gorila_init", "goril
            "replay_insert", "replay_sample", "learner_step", "ps_apply_shard", "sync_target", "gorila_get_state",
            "gorila_set_state", "gorila_get_learner_state", "gorila_set_learner_state", "gorila_get_grad",
            "gorila_get_q", "gorila_kernel_launches", "gorila_profile_enable", "gorila_profile_read",
-           "gorila_profile_phase_count", "gorila_profile_phase_name", "gorila_nccl_unique_id"]
+           "gorila_profile_phase_count", "gorila_profile_phase_name", "gorila_nccl_unique_id", "gorila_round"]
 
 
 def load(build_if_missing=True):
@@ -101,6 +101,7 @@ def load(build_if_missing=True):
     L.gorila_profile_phase_name.argtypes = [i32]
     L.gorila_profile_phase_name.restype = ctypes.c_char_p
     L.gorila_nccl_unique_id.argtypes = [P]
+    L.gorila_round.argtypes = [P, P, i32, u64, P, P, P, P]
     _lib = L
     return L
 
@@ -225,6 +226,22 @@ class Gorila:
         """No host sync, no info copy (throughput path). learners_arr: int32 numpy array."""
         _check(load().learner_step(self.h, learners_arr.ctypes.data, len(learners_arr), rnd,
                                    None if staleness_arr is None else staleness_arr.ctypes.data, None))
+
+    def round(self, learners_arr, rnd, staleness_arr=None, want_info=False):
+        """learner_step + ps_apply_shard + sync_target as one (graph-replayed) round."""
+        if not want_info:
+            _check(load().gorila_round(self.h, learners_arr.ctypes.data, len(learners_arr), rnd,
+                                       None if staleness_arr is None else staleness_arr.ctypes.data,
+                                       None, None, None))
+            return None
+        ri = RoundInfo()
+        synced = np.zeros(len(learners_arr), np.uint8)
+        _check(load().gorila_round(self.h, learners_arr.ctypes.data, len(learners_arr), rnd,
+                                   None if staleness_arr is None else staleness_arr.ctypes.data,
+                                   ctypes.cast(self._info, ctypes.c_void_p), ctypes.byref(ri), synced.ctypes.data))
+        return ([self._info[i].as_dict() for i in range(len(learners_arr))],
+                {"n_accepted": ri.n_accepted, "version_before": ri.version_before,
+                 "version_after": ri.version_after}, synced.astype(bool))
 
     def ps_apply_shard(self, rnd, want_info=True):
         ri = RoundInfo() if want_info else None

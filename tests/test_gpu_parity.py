@@ -207,3 +207,21 @@ def test_target_net_immutable_between_syncs():
         else:
             assert (tm == tm_prev).all()
         tm_prev = tm
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
+def test_round_graph_matches_eager_bitwise(math):
+    """gorila_round (CUDA-graph replay of learner_step + ps_apply_shard + sync_target) == the eager calls."""
+    ga, _ = make_pair(nA=18, B=32, C=3000, n_insert=3000, math=math, target_period=3, outlier_warmup=2)
+    gb, _ = make_pair(nA=18, B=32, C=3000, n_insert=3000, math=math, target_period=3, outlier_warmup=2)
+    ids = np.array([0], np.int32)
+    for k in range(8):
+        ia = ga.learner_step([0], k)
+        ra = ga.ps_apply_shard(k)
+        sa = ga.sync_target([0])
+        ib, rb, sb = gb.round(ids, k, want_info=True)
+        assert ia == ib and ra == rb and list(sa) == list(sb)
+    ta, ma, va, Va = ga.get_state()
+    tb, mb, vb, Vb = gb.get_state()
+    assert (ta == tb).all() and (ma == mb).all() and (va == vb).all() and Va == Vb
+    assert (ga.get_learner_state(0)[0] == gb.get_learner_state(0)[0]).all()
