@@ -321,7 +321,7 @@ def main():
     prof_steps = min(args.steps, 300)
     stream.synchronize()
     for _ in range(prof_steps):
-        step_eager(k)  # per-phase events need the eager (non-graph) path
+        step(k)  # graph replay with event-record nodes between phases
         k += 1
     phases, n_prof = g.profile_read()
     g.profile_enable(False)
@@ -335,7 +335,7 @@ def main():
 
     def roof(p):
         w = phase_work(p, args.batch, args.n_actions, P, esz)
-        if w is None:
+        if w is None or per_launch_ms.get(p, 0.0) <= 0.0:
             return None
         bound, amount = w
         t = per_launch_ms[p] / 1000.0

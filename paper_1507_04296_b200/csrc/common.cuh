@@ -107,6 +107,32 @@ GORILA_DEV void tmem_ld16(uint32_t taddr, float* v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// ---- programmatic dependent launch: wait for the preceding grid's results / let the next grid launch
+GORILA_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+GORILA_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+// ---- thread-block clusters / distributed shared memory
+GORILA_DEV uint32_t cluster_ctarank() {
+    uint32_t r;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(r));
+    return r;
+}
+GORILA_DEV void cluster_sync() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// address of the same smem location in CTA `rank` of the cluster
+GORILA_DEV uint32_t dsmem_map(uint32_t saddr, uint32_t rank) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(saddr), "r"(rank));
+    return r;
+}
+GORILA_DEV float4 dsmem_ld4(uint32_t caddr) {
+    float4 v;
+    asm volatile("ld.shared::cluster.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(v.x), "=f"(v.y), "=f"(v.z), "=f"(v.w) : "r"(caddr) : "memory");
+    return v;
+}
+
 // UMMA shared-memory descriptor, SWIZZLE_NONE, K-major canonical layout:
 // core matrix = 8 rows x 16 B contiguous; LBO = byte step between K-adjacent core
 // matrices; SBO = byte step between M/N-adjacent 8-row groups; version 1 (sm_100).

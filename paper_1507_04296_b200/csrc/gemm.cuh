@@ -278,6 +278,23 @@ struct EpStoreT {  // dst[split][j][i] = v * scale (transposed fp32 store: weigh
     }
 };
 
+struct EpActT {  // out[j][i] = ReLU(v + bias[i]) in fp32 (fc4 forward computed as W4 . a3^T)
+    float* out;
+    int64_t ld;
+    const float* bias;
+    int M, N;
+    GORILA_DEV void apply1(int i, int j, float v, int) const {
+        if (i < M && j < N) out[(int64_t)j * ld + i] = fmaxf(v + bias[i], 0.f);
+    }
+    GORILA_DEV void apply16(int i, int j0, const float* v, int s) const {
+        if (i >= M) return;
+        const float b = bias[i];
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+            if (j0 + e < N) out[(int64_t)(j0 + e) * ld + i] = fmaxf(v[e] + b, 0.f);
+    }
+};
+
 struct EpStore {  // dst[split][i][j] = v (fp32 split-K partials)
     float* dst;
     int64_t ld, split_stride;
@@ -326,6 +343,7 @@ struct GemmBatch {
     int M, N, R;           // shared by all problems of the batch
     int splits;            // split of the reduction range
     int chunks_per_split;  // in units of 64 (tc) / 16 (simt) reduction elements
+    int cluster;           // > 1: the `splits` CTAs of one tile form a cluster and reduce through DSMEM
 };
 
 // ====================================================================== tcgen05 engine
@@ -334,7 +352,12 @@ constexpr int TC_BM = 128, TC_BK = 64, TC_THREADS = 128;
 __host__ __device__ constexpr uint32_t tmem_cols_for(int bn) {
     return bn <= 32 ? 32u : bn <= 64 ? 64u : bn <= 128 ? 128u : 256u;
 }
-__host__ __device__ constexpr int tc_smem_bytes(int bn) { return 2 * (TC_BM * TC_BK * 2 + bn * TC_BK * 2) + 64; }
+// fp32 partial tile for the cluster reduction: [BN/16][128 rows][20 floats] (80-B row pitch: conflict-free)
+__host__ __device__ constexpr int tc_red_bytes(int bn) { return (bn / 16) * TC_BM * 80; }
+__host__ __device__ constexpr int tc_stage_bytes(int bn) { return 2 * (TC_BM * TC_BK * 2 + bn * TC_BK * 2); }
+__host__ __device__ constexpr int tc_smem_bytes(int bn) {
+    return (tc_stage_bytes(bn) > tc_red_bytes(bn) ? tc_stage_bytes(bn) : tc_red_bytes(bn)) + 64;
+}
 
 // Stage one operand tile (ROWS x 64 reduction elements, bf16) in the canonical layout.
 // K-major : core matrix (8 rows x 16 B) at (row/8, kchunk): offset (row/8)*1024 + kch*128 + (row%8)*16
@@ -395,7 +418,7 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
     extern __shared__ __align__(1024) uint8_t smem[];
     uint8_t* sA = smem;                // [2][A_BYTES]
     uint8_t* sB = smem + 2 * A_BYTES;  // [2][B_BYTES]
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 2 * (A_BYTES + B_BYTES));
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + tc_smem_bytes(BN) - 64);
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -415,6 +438,8 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    pdl_wait();     // operands come from the preceding kernel(s)
+    pdl_trigger();  // the next kernel may start its prologue
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t IDESC =
         umma_idesc_bf16(TC_BM, BN) | (LA::kMN ? (1u << 15) : 0u) | (LB::kMN ? (1u << 16) : 0u);
@@ -454,17 +479,56 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
     tc_fence_after();
 
     // epilogue: warp w owns TMEM lanes (= tile rows) 32w .. 32w+31
-    const int row = i0 + warp * 32 + lane;
+    const int lrow = warp * 32 + lane, row = i0 + lrow;
+    if (p.cluster > 1) {
+        // in-cluster split-K: every CTA parks its fp32 tile in its own smem (the stage buffers are
+        // free now); then CTA q reduces rows [q*128/CL, (q+1)*128/CL) over all CL tiles in rank
+        // order (DSMEM reads) and applies the epilogue to them.
+        float* red = reinterpret_cast<float*>(smem);
+        __syncthreads();
 #pragma unroll 1
-    for (int c0 = 0; c0 < BN; c0 += 16) {
-        float v[16];
-        if (nK > 0) {
-            tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-        } else {
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+            float v[16];
+            if (nK > 0) tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+            else
 #pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = 0.f;
+                for (int e = 0; e < 16; ++e) v[e] = 0.f;
+            float4* dst = reinterpret_cast<float4*>(red + ((c0 / 16) * TC_BM + lrow) * 20);
+#pragma unroll
+            for (int e = 0; e < 4; ++e) dst[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
         }
-        if (j0 + c0 < p.N) P.ep.apply16(row, j0 + c0, v, split);
+        cluster_sync();
+        const int CL = p.cluster, rows_per = TC_BM / CL;
+        const int q = (int)cluster_ctarank();
+        for (int item = tid; item < rows_per * (BN / 16); item += TC_THREADS) {
+            const int r_loc = q * rows_per + item % rows_per, c0 = (item / rows_per) * 16;
+            const uint32_t a = smem_u32(red + ((c0 / 16) * TC_BM + r_loc) * 20);
+            float v[16] = {};
+            for (int pr = 0; pr < CL; ++pr) {
+                const uint32_t pa = dsmem_map(a, (uint32_t)pr);
+                float4 x[4];
+#pragma unroll
+                for (int e = 0; e < 4; ++e) x[e] = dsmem_ld4(pa + 16 * e);
+#pragma unroll
+                for (int e = 0; e < 4; ++e) {
+                    v[4 * e] += x[e].x; v[4 * e + 1] += x[e].y; v[4 * e + 2] += x[e].z; v[4 * e + 3] += x[e].w;
+                }
+            }
+            if (j0 + c0 < p.N) P.ep.apply16(i0 + r_loc, j0 + c0, v, 0);
+        }
+        cluster_sync();  // peers keep their smem alive until everyone has read it
+    } else {
+#pragma unroll 1
+        for (int c0 = 0; c0 < BN; c0 += 16) {
+            float v[16];
+            if (nK > 0) {
+                tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
+            } else {
+#pragma unroll
+                for (int e = 0; e < 16; ++e) v[e] = 0.f;
+            }
+            if (j0 + c0 < p.N) P.ep.apply16(row, j0 + c0, v, split);
+        }
     }
     tc_fence_before();
     __syncthreads();
@@ -478,6 +542,8 @@ template <typename LA, typename LB, typename EP>
 __global__ void __launch_bounds__(256) gemm_simt(const __grid_constant__ GemmBatch<LA, LB, EP> p) {
     __shared__ float As[SM_BR][SM_BI + 4];
     __shared__ float Bs[SM_BR][SM_BJ + 4];
+    pdl_wait();
+    pdl_trigger();
     const int tid = threadIdx.x;
     const int prob = blockIdx.z / p.splits, split = blockIdx.z - prob * p.splits;
     const GemmProb<LA, LB, EP>& P = p.prob[prob];

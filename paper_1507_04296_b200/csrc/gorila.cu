@@ -11,6 +11,7 @@
 #include <algorithm>
 #include <map>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <type_traits>
@@ -118,11 +119,9 @@ struct gorila_ctx {
     float* sr;
     int64_t* sidx;
     float* dQ;
-    float* part_fc4;   // [2][splits][512][B]
     float* part_w[3];  // conv wgrad partials
     float* part_b;     // bias-gradient partials [4 layers][BIAS_CHUNKS][C]
     int split_w[3];
-    int split_fc4;
     float* tmp_canon;  // [P]
     float* tmp_int;    // [W*q]
     ncclComm_t comm = nullptr;
@@ -135,10 +134,17 @@ struct gorila_ctx {
     uint64_t prof_steps = 0;
     // CUDA-graph cache of whole rounds (gorila_round)
     uint64_t* dev_round = nullptr;  // round counter the sampler reads
+    uint64_t dev_round_expect = ~0ull;  // value dev_round will hold when the queued work completes
+    unsigned int* head_counter = nullptr;
+    bool pdl = true;               // programmatic dependent launch between the round's kernels
+    bool fused_sync = false;       // gorila_round: k_apply takes the target-sync decisions
+    int sync_ids[8] = {};
+    int sync_n = 0;
     bool capturing = false;
     std::map<std::vector<int64_t>, cudaGraphExec_t> graphs;
     std::map<std::vector<int64_t>, uint64_t> graph_kernels;
     std::map<std::vector<int64_t>, int> graph_seen;
+    std::map<std::vector<int64_t>, std::vector<std::pair<int, cudaEvent_t>>> graph_marks;  // profiling graphs
 };
 
 namespace {
@@ -161,9 +167,42 @@ void mark(gorila_ctx* ctx, int ph) {
         cudaEventCreate(&e);
         ctx->ev_pool.push_back(e);
     }
-    cudaEventRecord(ctx->ev_pool[ctx->ev_used], ctx->stream);
+    if (ctx->capturing)  // becomes an event-record node of the graph, readable after each replay
+        cudaEventRecordWithFlags(ctx->ev_pool[ctx->ev_used], ctx->stream, cudaEventRecordExternal);
+    else
+        cudaEventRecord(ctx->ev_pool[ctx->ev_used], ctx->stream);
     ctx->marks.push_back({ph, ctx->ev_used});
     ctx->ev_used++;
+}
+
+// fold recorded marks into the per-phase accumulators (events must be complete)
+cudaError_t fold_marks(gorila_ctx* ctx, const std::vector<std::pair<int, cudaEvent_t>>& m) {
+    for (size_t i = 1; i < m.size(); ++i) {
+        if (m[i].first < 0) continue;
+        float t = 0.f;
+        cudaError_t e = cudaEventElapsedTime(&t, m[i - 1].second, m[i].second);
+        if (e != cudaSuccess) return e;
+        ctx->prof_ms[m[i].first] += t;
+    }
+    return cudaSuccess;
+}
+
+// every kernel of the round goes through here: programmatic dependent launch (the next kernel's
+// launch / prologue overlaps this one; kernels griddepcontrol.wait before reading inputs)
+template <typename... KP, typename... A>
+void launch(gorila_ctx* ctx, void (*kern)(KP...), dim3 grid, dim3 block, size_t smem, A&&... args) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = ctx->pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+    ctx->launches++;
 }
 
 int pick_splits(int64_t chunks_total, int64_t base_ctas, int target_ctas, int max_splits) {
@@ -174,27 +213,61 @@ int pick_splits(int64_t chunks_total, int64_t base_ctas, int target_ctas, int ma
 
 // ------------------------------------------------------------------ GEMM dispatch
 template <int BN, typename LA, typename LB, typename EP>
-void launch_tc(GemmBatch<LA, LB, EP> gb, int nprob, cudaStream_t st) {
+void launch_tc(GemmBatch<LA, LB, EP> gb, int nprob, cudaStream_t st, bool pdl) {
     const int smem = tc_smem_bytes(BN);
     static bool attr_set = false;
     if (!attr_set) {
         cudaFuncSetAttribute(gemm_tc<BN, LA, LB, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+        cudaFuncSetAttribute(gemm_tc<BN, LA, LB, EP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         attr_set = true;
     }
     dim3 grid((gb.M + TC_BM - 1) / TC_BM, (gb.N + BN - 1) / BN, nprob * gb.splits);
-    gemm_tc<BN, LA, LB, EP><<<grid, TC_THREADS, smem, st>>>(gb);
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = dim3(TC_THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (gb.cluster > 1) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = 1;
+        at[na].val.clusterDim.y = 1;
+        at[na].val.clusterDim.z = gb.cluster;
+        ++na;
+    }
+    if (pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, gemm_tc<BN, LA, LB, EP>, gb);
 }
 
 template <typename LA, typename LB, typename EP>
-void launch_simt(GemmBatch<LA, LB, EP> gb, int nprob, cudaStream_t st) {
-    dim3 grid((gb.M + SM_BI - 1) / SM_BI, (gb.N + SM_BJ - 1) / SM_BJ, nprob * gb.splits);
-    gemm_simt<LA, LB, EP><<<grid, 256, 0, st>>>(gb);
+void launch_simt(GemmBatch<LA, LB, EP> gb, int nprob, cudaStream_t st, bool pdl) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3((gb.M + SM_BI - 1) / SM_BI, (gb.N + SM_BJ - 1) / SM_BJ, nprob * gb.splits);
+    cfg.blockDim = dim3(256);
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    cudaLaunchKernelEx(&cfg, gemm_simt<LA, LB, EP>, gb);
 }
 
 // C[M][N] = sum_r A(i,r) B(j,r): bf16 -> tcgen05 engine (BN = N tile), fp32 -> SIMT engine.
-// `splits` requested split of the reduction (rounded to whole chunks).
+// `splits` requested split of the reduction (rounded to whole chunks) into partial outputs
+// (epilogue gets the split index). cluster_target > 0 (tc only): instead reduce the split
+// inside a thread-block cluster (size <= 8) so that about cluster_target CTAs run, with the
+// epilogue applied once by the leader — no partial buffers.
 template <typename T, int BN, typename LA, typename LB, typename EP>
-void gemm(gorila_ctx* ctx, const GemmProb<LA, LB, EP>* probs, int nprob, int M, int N, int R, int splits) {
+void gemm(gorila_ctx* ctx, const GemmProb<LA, LB, EP>* probs, int nprob, int M, int N, int R, int splits,
+          int cluster_target = 0) {
     GemmBatch<LA, LB, EP> gb{};
     for (int i = 0; i < nprob; ++i) gb.prob[i] = probs[i];
     if (nprob == 1) gb.prob[1] = probs[0];
@@ -206,10 +279,26 @@ void gemm(gorila_ctx* ctx, const GemmProb<LA, LB, EP>* probs, int nprob, int M, 
     splits = std::max(1, std::min(splits, chunks));
     gb.chunks_per_split = (chunks + splits - 1) / splits;
     gb.splits = (chunks + gb.chunks_per_split - 1) / gb.chunks_per_split;
+    gb.cluster = 1;
+    static const int cluster_env = [] {  // GORILA_CLUSTER=0 disables in-cluster split-K (experiments)
+        const char* e = getenv("GORILA_CLUSTER");
+        return e ? atoi(e) : 1;
+    }();
+    if (!std::is_same<T, float>::value && cluster_target > 0 && cluster_env) {
+        const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN) * nprob;
+        const int want = std::max(1, (cluster_target + tiles - 1) / tiles);
+        int cl = 1;  // a power of two <= 16 (the reduction splits the 128 tile rows evenly)
+        while (cl * 2 <= std::min(16, std::min(want, chunks))) cl *= 2;
+        if (cl > 1) {
+            gb.cluster = cl;
+            gb.splits = cl;
+            gb.chunks_per_split = (chunks + cl - 1) / cl;
+        }
+    }
     if constexpr (std::is_same<T, float>::value) {
-        launch_simt(gb, nprob, ctx->stream);
+        launch_simt(gb, nprob, ctx->stream, ctx->pdl);
     } else {
-        launch_tc<BN>(gb, nprob, ctx->stream);
+        launch_tc<BN>(gb, nprob, ctx->stream, ctx->pdl);
     }
     LAUNCHED();
 }
@@ -241,7 +330,6 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     Learner& Lr = ctx->learners[j];
     const int B = ctx->B, nA = ctx->nA;
     const bool fp32 = std::is_same<T, float>::value;
-    cudaStream_t st = ctx->stream;
     const uint64_t k_src = round >= (uint64_t)s_j ? round - (uint64_t)s_j : 0;
     const int slot = (int)(k_src % (uint64_t)ctx->H);
     const T* rt = P_<T>(ctx->rep_t[slot]);
@@ -261,10 +349,10 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     {
         dim3 grid((FRAME_BYTES / 16 + 255) / 256, B);
         uint2 key = make_uint2((uint32_t)cfg.seed, (uint32_t)(cfg.seed >> 32));
-        k_sample<T><<<grid, 256, 0, st>>>(Lr.frames, Lr.a, Lr.r, Lr.d, cfg.replay_capacity, Lr.n_dev, key,
-                                          (uint32_t)(cfg.learner_id_base + j), ctx->dev_round, B, s, s2, ctx->sa,
-                                          ctx->sr, ctx->sd, ctx->sidx);
-        LAUNCHED();
+        launch(ctx, k_sample<T>, grid, dim3(256), 0, (const uint8_t*)Lr.frames, (const uint8_t*)Lr.a,
+               (const float*)Lr.r, (const uint8_t*)Lr.d, (int64_t)cfg.replay_capacity, (const uint64_t*)Lr.n_dev, key,
+               (uint32_t)(cfg.learner_id_base + j), (const uint64_t*)ctx->dev_round, B, s, s2, ctx->sa, ctx->sr,
+               ctx->sd, ctx->sidx, accumulate ? (uint32_t*)nullptr : ctx->n_acc_local);
     }
     mark(ctx, PH_SAMPLE);
     const float in_scale = 1.0f / 255.0f;  // reading R17 (fp32 constant, folded into conv1's epilogue)
@@ -285,7 +373,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         GemmProb<LA, LB, EP> pr[2] = {
             {{a1, M}, {rt + RL.w2, K2, C2_OUT, K2}, {a2, C2_OUT, rf + RL.b2, 1.f, M, C2_OUT, 1}},
             {{t1, M}, {tt + RT.w2, K2, C2_OUT, K2}, {t2, C2_OUT, tf + RT.b2, 1.f, M, C2_OUT, 1}}};
-        gemm<T, 64>(ctx, pr, 2, M, C2_OUT, K2, 1);
+        gemm<T, 64>(ctx, pr, 2, M, C2_OUT, K2, 1, 148);
     }
     mark(ctx, PH_CONV2F);
     // conv3 fwd
@@ -295,53 +383,46 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         GemmProb<LA, LB, EP> pr[2] = {
             {{a2, M}, {rt + RL.w3, K3, C3_OUT, K3}, {a3, C3_OUT, rf + RL.b3, 1.f, M, C3_OUT, 1}},
             {{t2, M}, {tt + RT.w3, K3, C3_OUT, K3}, {t3, C3_OUT, tf + RT.b3, 1.f, M, C3_OUT, 1}}};
-        gemm<T, 64>(ctx, pr, 2, M, C3_OUT, K3, 1);
+        gemm<T, 64>(ctx, pr, 2, M, C3_OUT, K3, 1, 148);
     }
     mark(ctx, PH_CONV3F);
-    // fc4 fwd, swap-AB + split-K: partial[z][s][n][b] = sum_k W4[n][k] a3[b][k]; finalize bias + ReLU
+    // fc4 fwd, swap-AB (i = n, j = b): a4[b][n] = ReLU(W4[n] . a3[b] + b4[n]) in fp32, the split of
+    // K = 3136 reduced inside the cluster (no partial buffers, no finalize kernel)
     {
-        using LA = LdRows<T>; using LB = LdRows<T>; using EP = EpStore;
-        const int S = ctx->split_fc4;
-        const int64_t pstride = (int64_t)S * FC4_OUT * B;
+        using LA = LdRows<T>; using LB = LdRows<T>; using EP = EpActT;
         GemmProb<LA, LB, EP> pr[2] = {
-            {{rt + RL.w4, FC4_IN, FC4_OUT, FC4_IN}, {a3, FC4_IN, B, FC4_IN},
-             {ctx->part_fc4, B, (int64_t)FC4_OUT * B, FC4_OUT, B}},
-            {{tt + RT.w4, FC4_IN, FC4_OUT, FC4_IN}, {t3, FC4_IN, B, FC4_IN},
-             {ctx->part_fc4 + pstride, B, (int64_t)FC4_OUT * B, FC4_OUT, B}}};
-#define FC4F(BN_) gemm<T, BN_>(ctx, pr, 2, FC4_OUT, B, FC4_IN, S)
+            {{rt + RL.w4, FC4_IN, FC4_OUT, FC4_IN}, {a3, FC4_IN, B, FC4_IN}, {a4, FC4_OUT, rf + RL.b4, FC4_OUT, B}},
+            {{tt + RT.w4, FC4_IN, FC4_OUT, FC4_IN}, {t3, FC4_IN, B, FC4_IN}, {t4, FC4_OUT, tf + RT.b4, FC4_OUT, B}}};
+#define FC4F(BN_) gemm<T, BN_>(ctx, pr, 2, FC4_OUT, B, FC4_IN, 1, 148)
         DISPATCH_BN_BATCH(B, FC4F);
 #undef FC4F
-        dim3 grid((B * FC4_OUT + 255) / 256, 2);
-        k_fc4_finalize<<<grid, 256, 0, st>>>(ctx->part_fc4, S, pstride, B, rf + RL.b4, tf + RT.b4, a4, t4);
-        LAUNCHED();
     }
     mark(ctx, PH_FC4F);
-    // fc5 fwd (both nets)
-    k_fc5_fwd<<<dim3(B, 2), 256, 0, st>>>(a4, t4, rf + RL.w5, tf + RT.w5, rf + RL.b5, tf + RT.b5, Lr.Q, Lr.Qhat, nA);
-    LAUNCHED();
-    mark(ctx, PH_FC5F);
-    // K7: TD target, clipped error, loss, outlier + stale decisions
+    // fc5 forward (both nets) + K7: TD target, clipped error, loss, outlier + stale decisions
     {
-        TdParams p{};
-        p.Q = Lr.Q; p.Qhat = Lr.Qhat; p.a = ctx->sa; p.r = ctx->sr; p.d = ctx->sd; p.dQ = ctx->dQ;
-        p.B = B; p.nA = nA; p.gamma = cfg.gamma; p.stats = Lr.stats; p.info = Lr.info; p.V = ctx->V;
-        p.base_V = ctx->Vhist + slot; p.n_acc_local = ctx->n_acc_local; p.max_staleness = cfg.max_staleness;
-        p.outlier_enabled = cfg.outlier_enabled; p.outlier_warmup = cfg.outlier_warmup;
-        p.outlier_k = cfg.outlier_k; p.outlier_beta = cfg.outlier_beta;
-        k_td<<<1, 256, 0, st>>>(p);
-        LAUNCHED();
+        Fc5TdParams p{};
+        p.a4 = a4; p.t4 = t4; p.w5 = rf + RL.w5; p.b5 = rf + RL.b5; p.w5t = tf + RT.w5; p.b5t = tf + RT.b5;
+        p.counter = ctx->head_counter;
+        TdParams& t = p.td;
+        t.Q = Lr.Q; t.Qhat = Lr.Qhat; t.a = ctx->sa; t.r = ctx->sr; t.d = ctx->sd; t.dQ = ctx->dQ;
+        t.B = B; t.nA = nA; t.gamma = cfg.gamma; t.stats = Lr.stats; t.info = Lr.info; t.V = ctx->V;
+        t.base_V = ctx->Vhist + slot; t.n_acc_local = ctx->n_acc_local; t.max_staleness = cfg.max_staleness;
+        t.outlier_enabled = cfg.outlier_enabled; t.outlier_warmup = cfg.outlier_warmup;
+        t.outlier_k = cfg.outlier_k; t.outlier_beta = cfg.outlier_beta;
+        launch(ctx, k_fc5_td, dim3(B, 2), dim3(256), 0, p);
     }
+    mark(ctx, PH_FC5F);
     mark(ctx, PH_TD);
     // fc5 bwd: dW5, db5 into G; g4 = mask(dQ W5)
-    k_fc5_bwd<T><<<148, 256, 0, st>>>(ctx->dQ, a4, rf + RL.w5, B, nA, ctx->G, g4, accumulate);
-    LAUNCHED();
+    launch(ctx, k_fc5_bwd<T>, dim3(148), dim3(256), 0, (const float*)ctx->dQ, (const float*)a4,
+           (const float*)(rf + RL.w5), B, nA, ctx->G, g4, accumulate);
     mark(ctx, PH_FC5B);
     // fc4 dgrad (i = k, j = b, red = n): g3[b][k] = mask(sum_n W4[n][k] g4[b][n])
     {
         using LA = LdRowsMN<T>; using LB = LdRows<T>; using EP = EpMaskT<T>;
         GemmProb<LA, LB, EP> pr[1] = {{{rt + RL.w4, FC4_IN, FC4_IN, FC4_OUT}, {g4, FC4_OUT, B, FC4_OUT},
                                        {g3, a3, FC4_IN, FC4_IN, B}}};
-#define FC4D(BN_) gemm<T, BN_>(ctx, pr, 1, FC4_IN, B, FC4_OUT, 1)
+#define FC4D(BN_) gemm<T, BN_>(ctx, pr, 1, FC4_IN, B, FC4_OUT, 1, 148)
         DISPATCH_BN_BATCH(B, FC4D);
 #undef FC4D
     }
@@ -351,7 +432,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         using LA = LdRowsMN<T>; using LB = LdRowsMN<T>; using EP = EpAddT;
         GemmProb<LA, LB, EP> pr[1] = {{{a3, FC4_IN, FC4_IN, B}, {g4, FC4_OUT, FC4_OUT, B},
                                        {ctx->G + OFF_W4, FC4_IN, FC4_IN, FC4_OUT, accumulate}}};
-        gemm<T, 256>(ctx, pr, 1, FC4_IN, FC4_OUT, B, 1);
+        gemm<T, 64>(ctx, pr, 1, FC4_IN, FC4_OUT, B, 1);
     }
     mark(ctx, PH_FC4WG);
     // conv3 dgrad: g2 = mask(conv3^T(g3))
@@ -360,7 +441,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         const int M = B * H2 * H2;
         GemmProb<LA, LB, EP> pr[1] = {{{g3, M}, {rt + RL.w3},
                                        {g2, a2, C2_OUT, M, C2_OUT}}};
-        gemm<T, 64>(ctx, pr, 1, M, C2_OUT, K3, 1);
+        gemm<T, 64>(ctx, pr, 1, M, C2_OUT, K3, 1, 148);
     }
     mark(ctx, PH_CONV3DG);
     // conv3 wgrad (i = r, j = o, red = m): partial[s][o][r]
@@ -378,7 +459,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         const int M = B * H1 * H1;
         GemmProb<LA, LB, EP> pr[1] = {{{g2, M}, {rt + RL.w2},
                                        {g1, a1, C1_OUT, M, C1_OUT}}};
-        gemm<T, 32>(ctx, pr, 1, M, C1_OUT, Conv2::RD, 1);
+        gemm<T, 32>(ctx, pr, 1, M, C1_OUT, Conv2::RD, 1, 296);
     }
     mark(ctx, PH_CONV2DG);
     // conv2 wgrad
@@ -400,8 +481,8 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }
     mark(ctx, PH_CONV1WG);
     // bias gradients b1..b4 (coalesced partials; reduced by K10)
-    k_bias_partial<T><<<dim3(BIAS_CHUNKS, 4), 256, 0, st>>>(g1, g2, g3, g4, B, ctx->part_b);
-    LAUNCHED();
+    launch(ctx, k_bias_partial<T>, dim3(BIAS_CHUNKS, 4), dim3(256), 0, (const T*)g1, (const T*)g2, (const T*)g3,
+           (const T*)g4, B, ctx->part_b);
     mark(ctx, PH_BIASG);
     // K10: fixed-order reduction of the conv wgrad partials into G
     {
@@ -421,8 +502,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         }
         p.nseg = 7;
         p.accumulate = accumulate;
-        k_wgrad_reduce<<<148 * 2, 256, 0, st>>>(p, ctx->G);
-        LAUNCHED();
+        launch(ctx, k_wgrad_reduce, dim3(148 * 2), dim3(256), 0, p, ctx->G);
     }
     mark(ctx, PH_WGRED);
     CU(cudaGetLastError());
@@ -432,8 +512,8 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
 template <typename T>
 gorila_status pack_replica(gorila_ctx* ctx, const float* theta, void* rt, float* rf, const uint8_t* pred,
                            uint64_t* vhist_dst) {
-    k_pack<T><<<148 * 4, 256, 0, ctx->stream>>>(theta, ctx->nA, P_<T>(rt), rf, pred, vhist_dst, ctx->V);
-    ctx->launches++;
+    launch(ctx, k_pack<T>, dim3(148 * 4), dim3(256), 0, theta, ctx->nA, P_<T>(rt), rf, pred, vhist_dst,
+           (const uint64_t*)ctx->V);
     CU(cudaGetLastError());
     return GORILA_OK;
 }
@@ -464,6 +544,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     uint32_t* nacc = c.take<uint32_t>(4);
     uint64_t* Vhist = c.take<uint64_t>(H);
     uint64_t* dev_round = c.take<uint64_t>(1);
+    unsigned int* head_counter = c.take<unsigned int>(1);
     std::vector<void*> rep_t(H);
     std::vector<float*> rep_f(H);
     for (int h = 0; h < H; ++h) {
@@ -508,9 +589,6 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     float* dQ = c.take<float>(Bs * nA);
     // split choices (reduction chunks of 64 for tc, 16 for simt)
     const int chunk = fp32 ? SM_BR : TC_BK;
-    const int split_fc4 =
-        fp32 ? 1 : eff_splits(false, FC4_IN, pick_splits((FC4_IN + chunk - 1) / chunk, 4 * ((B + 255) / 256), 64, 16));
-    float* part_fc4 = c.take<float>((int64_t)2 * split_fc4 * FC4_OUT * B);
     int split_w[3];
     const int Mred[3] = {B * H1 * H1, B * H2 * H2, B * H3 * H3};
     const int64_t wcount[3] = {(int64_t)C1_OUT * K1, (int64_t)C2_OUT * K2, (int64_t)C3_OUT * K3};
@@ -529,12 +607,11 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         ctx->rl = rl; ctx->H = H;
         ctx->theta = theta; ctx->m = m; ctx->v = v; ctx->G = G; ctx->counts = counts; ctx->V = V;
         ctx->round_info = rinfo;
-        ctx->n_acc_local = nacc; ctx->Vhist = Vhist; ctx->dev_round = dev_round; ctx->rep_t = rep_t; ctx->rep_f = rep_f; ctx->learners = lrs;
+        ctx->n_acc_local = nacc; ctx->Vhist = Vhist; ctx->dev_round = dev_round; ctx->head_counter = head_counter; ctx->rep_t = rep_t; ctx->rep_f = rep_f; ctx->learners = lrs;
         ctx->s = s; ctx->s2 = s2; ctx->a1 = a1; ctx->a2 = a2; ctx->a3 = a3; ctx->a4 = a4;
         ctx->t1 = t1; ctx->t2 = t2; ctx->t3 = t3; ctx->t4 = t4;
         ctx->g1 = g1; ctx->g2 = g2; ctx->g3 = g3; ctx->g4 = g4;
         ctx->sa = sa; ctx->sd = sd; ctx->sr = sr; ctx->sidx = sidx; ctx->dQ = dQ;
-        ctx->part_fc4 = part_fc4; ctx->split_fc4 = split_fc4;
         for (int l = 0; l < 3; ++l) { ctx->part_w[l] = part_w[l]; ctx->split_w[l] = split_w[l]; }
         ctx->part_b = part_b;
         ctx->tmp_canon = tmp_canon; ctx->tmp_int = tmp_int;
@@ -578,13 +655,9 @@ gorila_status gorila_profile_enable(gorila_ctx* ctx, int32_t enable) {
 gorila_status gorila_profile_read(gorila_ctx* ctx, double* ms, int32_t n, uint64_t* n_steps) {
     if (!ctx) return fail(GORILA_E_INVALID, "null context");
     CU(cudaStreamSynchronize(ctx->stream));
-    for (size_t i = 1; i < ctx->marks.size(); ++i) {
-        const int ph = ctx->marks[i].first;
-        if (ph < 0) continue;
-        float t = 0.f;
-        CU(cudaEventElapsedTime(&t, ctx->ev_pool[ctx->marks[i - 1].second], ctx->ev_pool[ctx->marks[i].second]));
-        ctx->prof_ms[ph] += t;
-    }
+    std::vector<std::pair<int, cudaEvent_t>> m;
+    for (auto& mk : ctx->marks) m.push_back({mk.first, ctx->ev_pool[mk.second]});
+    CU(fold_marks(ctx, m));
     ctx->marks.clear();
     ctx->ev_used = 0;
     for (int i = 0; i < n && i < PH_COUNT; ++i) ms[i] = ctx->prof_ms[i];
@@ -639,6 +712,13 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     CU(cudaMemsetAsync(ctx->V, 0, sizeof(uint64_t) * 4, st));
     CU(cudaMemsetAsync(ctx->n_acc_local, 0, sizeof(uint32_t) * 4, st));
     CU(cudaMemsetAsync(ctx->Vhist, 0, sizeof(uint64_t) * ctx->H, st));
+    CU(cudaMemsetAsync(ctx->head_counter, 0, sizeof(unsigned int), st));
+    CU(cudaMemsetAsync(ctx->dev_round, 0, sizeof(uint64_t), st));
+    ctx->dev_round_expect = 0;
+    {
+        const char* e = getenv("GORILA_PDL");  // GORILA_PDL=0 disables programmatic dependent launch
+        ctx->pdl = !(e && atoi(e) == 0);
+    }
     for (auto& l : ctx->learners) {
         CU(cudaMemsetAsync(l.n_dev, 0, sizeof(uint64_t), st));
         CU(cudaMemsetAsync(l.stats, 0, sizeof(LearnerStats), st));
@@ -669,6 +749,8 @@ void gorila_destroy(gorila_ctx* ctx) {
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
     for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+    for (auto& kv : ctx->graph_marks)
+        for (auto& m : kv.second) cudaEventDestroy(m.second);
     if (ctx->comm) {
         if (ctx->poisoned) ncclCommAbort(ctx->comm);
         else ncclCommDestroy(ctx->comm);
@@ -718,19 +800,19 @@ gorila_status replay_sample(gorila_ctx* ctx, int32_t learner, uint64_t round, in
     cudaStream_t st = ctx->stream;
     const gorila_config& cfg = ctx->cfg;
     // sample into u8-valued T buffers of the scratch (same kernel as learner_step)
-    k_set_u64<<<1, 1, 0, st>>>(ctx->dev_round, round);
-    ctx->launches++;
+    launch(ctx, k_set_u64, dim3(1), dim3(1), 0, ctx->dev_round, (uint64_t)round);
+    ctx->dev_round_expect = round;
     dim3 grid((FRAME_BYTES / 16 + 255) / 256, B);
     uint2 key = make_uint2((uint32_t)cfg.seed, (uint32_t)(cfg.seed >> 32));
     if (cfg.math == GORILA_MATH_FP32)
         k_sample<float><<<grid, 256, 0, st>>>(l.frames, l.a, l.r, l.d, cfg.replay_capacity, l.n_dev, key,
                                               (uint32_t)(cfg.learner_id_base + learner), ctx->dev_round, B, (float*)ctx->s,
-                                              (float*)ctx->s2, ctx->sa, ctx->sr, ctx->sd, ctx->sidx);
+                                              (float*)ctx->s2, ctx->sa, ctx->sr, ctx->sd, ctx->sidx, nullptr);
     else
         k_sample<__nv_bfloat16><<<grid, 256, 0, st>>>(l.frames, l.a, l.r, l.d, cfg.replay_capacity, l.n_dev, key,
                                                       (uint32_t)(cfg.learner_id_base + learner), ctx->dev_round,
                                                       B, (__nv_bfloat16*)ctx->s, (__nv_bfloat16*)ctx->s2, ctx->sa,
-                                                      ctx->sr, ctx->sd, ctx->sidx);
+                                                      ctx->sr, ctx->sd, ctx->sidx, nullptr);
     ctx->launches++;
     CU(cudaGetLastError());
     CU(cudaStreamSynchronize(st));
@@ -778,10 +860,9 @@ gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
     cudaStream_t st = ctx->stream;
     mark(ctx, -1);
     ctx->prof_steps += ctx->prof ? 1 : 0;
-    CU(cudaMemsetAsync(ctx->n_acc_local, 0, sizeof(uint32_t), st));
-    if (!ctx->capturing) {  // a captured round reads / advances the device counter instead
-        k_set_u64<<<1, 1, 0, st>>>(ctx->dev_round, round);
-        ctx->launches++;
+    if (ctx->dev_round_expect != round) {  // the device counter is advanced by k_apply each round
+        launch(ctx, k_set_u64, dim3(1), dim3(1), 0, ctx->dev_round, (uint64_t)round);
+        ctx->dev_round_expect = round;
     }
     mark(ctx, PH_STEP_MISC);
     int ran = 0;  // the first learner that runs stores G, later ones accumulate (no memset)
@@ -790,8 +871,7 @@ gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
         Learner& l = ctx->learners[j];
         const int64_t size = std::min<int64_t>(l.n_host, ctx->cfg.replay_capacity);
         if (size - 1 < std::max<int64_t>(1, ctx->cfg.min_replay)) {
-            k_mark_not_ready<<<1, 1, 0, st>>>(l.info, l.stats);
-            ctx->launches++;
+            launch(ctx, k_mark_not_ready, dim3(1), dim3(1), 0, l.info, (const LearnerStats*)l.stats);
             continue;
         }
         const int s_j = staleness ? staleness[i] : 0;
@@ -800,9 +880,12 @@ gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
         if (s != GORILA_OK) return s;
         ++ran;
     }
-    if (ran == 0) CU(cudaMemsetAsync(ctx->G, 0, sizeof(float) * ctx->W * ctx->q, st));
-    k_write_counts<<<1, 64, 0, st>>>(ctx->counts, ctx->W, ctx->n_acc_local);
-    ctx->launches++;
+    if (ran == 0) {
+        CU(cudaMemsetAsync(ctx->G, 0, sizeof(float) * ctx->W * ctx->q, st));
+        CU(cudaMemsetAsync(ctx->n_acc_local, 0, sizeof(uint32_t), st));
+    }
+    if (ctx->W > 1)
+        launch(ctx, k_write_counts, dim3(1), dim3(64), 0, ctx->counts, ctx->W, (const uint32_t*)ctx->n_acc_local);
     mark(ctx, PH_STEP_MISC);
     if (info_out)
         for (int i = 0; i < n; ++i)
@@ -832,6 +915,16 @@ gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info*
     p.v = ctx->v;
     p.g = gsl;
     p.count = ctx->counts + (W > 1 ? r : 0);
+    p.count_local = W > 1 ? nullptr : ctx->n_acc_local;
+    p.dev_round = ctx->dev_round;
+    p.period = ctx->cfg.target_period;
+    p.n_sync = 0;
+    if (ctx->fused_sync)
+        for (int i = 0; i < ctx->sync_n; ++i) {
+            p.sync_stats[p.n_sync] = ctx->learners[ctx->sync_ids[i]].stats;
+            p.sync_flag[p.n_sync] = ctx->learners[ctx->sync_ids[i]].sync_flag;
+            ++p.n_sync;
+        }
     p.n_real = std::max<int64_t>(0, std::min<int64_t>(ctx->q, ctx->P - (int64_t)r * ctx->q));
     p.optimizer = ctx->cfg.optimizer;
     p.lr = ctx->cfg.lr; p.rho = ctx->cfg.rms_rho; p.eps = ctx->cfg.rms_eps; p.ada_eps = ctx->cfg.ada_eps;
@@ -845,9 +938,9 @@ gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info*
         p.rep_f = ctx->rep_f[slot];
         p.vhist_dst = ctx->Vhist + slot;
     }
-    if (ctx->cfg.math == GORILA_MATH_FP32) k_apply<float><<<148 * 4, 256, 0, st>>>(p);
-    else k_apply<__nv_bfloat16><<<148 * 4, 256, 0, st>>>(p);
-    ctx->launches++;
+    if (ctx->cfg.math == GORILA_MATH_FP32) launch(ctx, k_apply<float>, dim3(148 * 4), dim3(256), 0, p);
+    else launch(ctx, k_apply<__nv_bfloat16>, dim3(148 * 4), dim3(256), 0, p);
+    ctx->dev_round_expect = round + 1;
     mark(ctx, PH_APPLY);
     if (W > 1) {
         NC(ncclAllGather(p.theta, ctx->theta, ctx->q, ncclFloat, ctx->comm, st));
@@ -879,8 +972,9 @@ gorila_status sync_target(gorila_ctx* ctx, const int32_t* learners, int32_t n, i
         gorila_status s = check_learner(ctx, learners[i]);
         if (s != GORILA_OK) return s;
         Learner& l = ctx->learners[learners[i]];
-        k_sync_decide<<<1, 1, 0, st>>>(l.stats, ctx->V, ctx->cfg.target_period, force, l.sync_flag);
-        ctx->launches++;
+        if (!ctx->fused_sync)  // gorila_round: k_apply already took the decision
+            launch(ctx, k_sync_decide, dim3(1), dim3(1), 0, l.stats, (const uint64_t*)ctx->V,
+                   (int64_t)ctx->cfg.target_period, (int)force, l.sync_flag);
         if ((s = pack_any(ctx, ctx->theta, l.tminus_t, l.tminus_f, l.sync_flag, nullptr)) != GORILA_OK) return s;
         if (synced_out) CU(cudaMemcpyAsync(&synced_out[i], l.sync_flag, 1, cudaMemcpyDeviceToHost, st));
     }
@@ -896,7 +990,7 @@ gorila_status gorila_round(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
     if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned");
     if (!learners || n < 1 || n > ctx->L) return fail(GORILA_E_SHAPE, "bad learner list");
     cudaStream_t st = ctx->stream;
-    bool graphable = !ctx->prof;
+    bool graphable = st != nullptr;  // the legacy default stream cannot be captured
     std::vector<int64_t> key;
     for (int i = 0; i < n; ++i) {
         if (learners[i] < 0 || learners[i] >= ctx->L) return fail(GORILA_E_RANGE, "learner id out of range");
@@ -909,30 +1003,56 @@ gorila_status gorila_round(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
         key.push_back(s_i);
     }
     key.push_back((int64_t)(round % (uint64_t)ctx->H));
+    key.push_back(ctx->prof ? 1 : 0);  // profiling graphs carry event-record nodes
     gorila_status s;
     auto eager = [&]() -> gorila_status {
         gorila_status r = learner_step(ctx, learners, n, round, staleness, nullptr);
         if (r != GORILA_OK) return r;
-        if ((r = ps_apply_shard(ctx, round, nullptr)) != GORILA_OK) return r;
-        return sync_target(ctx, learners, n, 0, nullptr);
+        ctx->fused_sync = n <= 8;  // k_apply takes the target-sync decisions (same predicate, R13)
+        ctx->sync_n = n;
+        for (int i = 0; i < n && i < 8; ++i) ctx->sync_ids[i] = learners[i];
+        r = ps_apply_shard(ctx, round, nullptr);
+        if (r == GORILA_OK) r = sync_target(ctx, learners, n, 0, nullptr);
+        ctx->fused_sync = false;
+        return r;
     };
     auto it = graphable ? ctx->graphs.find(key) : ctx->graphs.end();
     if (it != ctx->graphs.end()) {
-        k_set_u64<<<1, 1, 0, st>>>(ctx->dev_round, round);
-        ctx->launches++;
+        if (ctx->dev_round_expect != round)
+            launch(ctx, k_set_u64, dim3(1), dim3(1), 0, ctx->dev_round, (uint64_t)round);
         CU(cudaGraphLaunch(it->second, st));
+        ctx->dev_round_expect = round + 1;
         ctx->launches += ctx->graph_kernels[key];
+        if (ctx->prof) {  // the graph's events are re-recorded by every replay: fold them now
+            CU(cudaStreamSynchronize(st));
+            CU(fold_marks(ctx, ctx->graph_marks[key]));
+            ctx->prof_steps += 1;
+        }
     } else if (!graphable || ctx->graph_seen[key]++ == 0) {
         if ((s = eager()) != GORILA_OK) return s;  // first use: eager (also sets lazy kernel attributes)
     } else {
-        // capture the round once; the captured sampler reads ctx->dev_round, set before each replay
-        k_set_u64<<<1, 1, 0, st>>>(ctx->dev_round, round);
-        ctx->launches++;
+        // capture the round once; the captured sampler reads ctx->dev_round (advanced by k_apply)
+        if (ctx->dev_round_expect != round)
+            launch(ctx, k_set_u64, dim3(1), dim3(1), 0, ctx->dev_round, (uint64_t)round);
+        ctx->dev_round_expect = round;
         CU(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
         ctx->capturing = true;
         const uint64_t launches0 = ctx->launches;
+        const size_t marks0 = ctx->marks.size();
+        const size_t used0 = ctx->ev_used;
         s = eager();
         ctx->capturing = false;
+        if (ctx->prof) {  // these marks belong to the graph, not to the eager accumulator
+            std::vector<std::pair<int, cudaEvent_t>> gm;
+            for (size_t i = marks0; i < ctx->marks.size(); ++i)
+                gm.push_back({ctx->marks[i].first, ctx->ev_pool[ctx->marks[i].second]});
+            ctx->graph_marks[key] = gm;
+            ctx->marks.resize(marks0);
+            // hand the graph's events over (they must not be re-recorded by eager marks)
+            ctx->ev_pool.erase(ctx->ev_pool.begin() + used0, ctx->ev_pool.begin() + ctx->ev_used);
+            ctx->ev_used = used0;
+            ctx->prof_steps -= 1;  // the capture itself executed nothing
+        }
         cudaGraph_t graph = nullptr;
         cudaError_t ce = cudaStreamEndCapture(st, &graph);
         if (s != GORILA_OK) {
@@ -946,6 +1066,12 @@ gorila_status gorila_round(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
         ctx->graphs[key] = exec;
         ctx->graph_kernels[key] = ctx->launches - launches0;
         CU(cudaGraphLaunch(exec, st));
+        ctx->dev_round_expect = round + 1;
+        if (ctx->prof) {
+            CU(cudaStreamSynchronize(st));
+            CU(fold_marks(ctx, ctx->graph_marks[key]));
+            ctx->prof_steps += 1;
+        }
     }
     if (info_out)
         for (int i = 0; i < n; ++i)
@@ -1011,8 +1137,7 @@ gorila_status gorila_set_state(gorila_ctx* ctx, const float* theta, const float*
                                cudaMemcpyDeviceToDevice, st));
         CU(cudaStreamSynchronize(st));
     }
-    k_set_u64<<<1, 1, 0, st>>>(ctx->V, version);
-    ctx->launches++;
+    launch(ctx, k_set_u64, dim3(1), dim3(1), 0, ctx->V, version);
     // every replica slot = the new theta (teacher forcing restarts the history)
     for (int h = 0; h < ctx->H; ++h) {
         gorila_status s = pack_any(ctx, ctx->theta, ctx->rep_t[h], ctx->rep_f[h], nullptr, ctx->Vhist + h);

@@ -22,8 +22,11 @@ __global__ void __launch_bounds__(256) k_sample(const uint8_t* __restrict__ fram
                                                 T* __restrict__ s_out,
                                                 T* __restrict__ s2_out, uint8_t* __restrict__ a_out,
                                                 float* __restrict__ r_out, uint8_t* __restrict__ d_out,
-                                                int64_t* __restrict__ idx_out) {
+                                                int64_t* __restrict__ idx_out, uint32_t* __restrict__ n_acc_reset) {
+    pdl_wait();
+    pdl_trigger();
     const int b = blockIdx.y;
+    if (n_acc_reset && b == 0 && blockIdx.x == 0 && threadIdx.x == 0) *n_acc_reset = 0;  // first learner of a round
     const uint64_t round = *round_ptr;  // device-resident round counter (graph replay friendly)
     const int64_t n = (int64_t)*ring_n;
     const int64_t size = n < C ? n : C;
@@ -106,44 +109,6 @@ __global__ void __launch_bounds__(256) k_sample(const uint8_t* __restrict__ fram
     }
 }
 
-// ------------------------------------------------------------------------- fc4 split-K finalize
-// a4[b][n] = round_T(ReLU(sum_s partial[s][n][b] + b4[n])), both nets (z = problem)
-// a4 stays fp32: it only feeds the fp32 fc5 layer (reading R16)
-__global__ void k_fc4_finalize(const float* __restrict__ partial, int splits, int64_t prob_stride, int B,
-                               const float* __restrict__ bias0, const float* __restrict__ bias1, float* out0,
-                               float* out1) {
-    const int z = blockIdx.y;
-    const float* P = partial + z * prob_stride;
-    const float* bias = z ? bias1 : bias0;
-    float* out = z ? out1 : out0;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < B * FC4_OUT; e += gridDim.x * blockDim.x) {
-        int b = e / FC4_OUT, n = e - b * FC4_OUT;
-        float acc = 0.f;
-        for (int s = 0; s < splits; ++s) acc += P[(int64_t)s * FC4_OUT * B + (int64_t)n * B + b];
-        out[e] = fmaxf(acc + bias[n], 0.f);
-    }
-}
-
-// ------------------------------------------------------------------------- fc5 forward
-// Q[b][a] = sum_n a4[b][n] * W5[a][n] + b5[a]  (fp32 weights, fp32 result; z = online / target)
-__global__ void __launch_bounds__(256) k_fc5_fwd(const float* __restrict__ a4_0, const float* __restrict__ a4_1,
-                                                 const float* __restrict__ w5_0, const float* __restrict__ w5_1,
-                                                 const float* __restrict__ b5_0, const float* __restrict__ b5_1,
-                                                 float* __restrict__ q0, float* __restrict__ q1, int nA) {
-    const int b = blockIdx.x, z = blockIdx.y;
-    const float* a4 = (z ? a4_1 : a4_0) + (int64_t)b * FC4_OUT;
-    const float* w5 = z ? w5_1 : w5_0;
-    const float* b5 = z ? b5_1 : b5_0;
-    float* q = z ? q1 : q0;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    for (int a = warp; a < nA; a += 8) {
-        float acc = 0.f;
-        for (int n = lane; n < FC4_OUT; n += 32) acc = fmaf(a4[n], w5[a * FC4_OUT + n], acc);
-        acc = warp_sum(acc);
-        if (lane == 0) q[b * nA + a] = acc + b5[a];
-    }
-}
-
 // ------------------------------------------------------------------------- K7 TD + decisions
 struct LearnerStats {  // device-resident per learner (reading R8)
     double mu, var;
@@ -179,25 +144,98 @@ struct TdParams {
     double outlier_beta;
 };
 
-// One block, 8 warps; warp w handles samples w, w+8, ... (fixed order):
-// y = r if terminal else r + gamma * max_a Qhat (Alg.1), delta = y - Q[a]
-// (Eq.1/Eq.2), dQ[a] = -clip(delta, -1, 1) / B (reading R3/R4); loss = mean delta^2,
-// l = mean |delta|; outlier + stale decisions; rejected or stale => dQ = 0.
-__global__ void __launch_bounds__(256) k_td(TdParams p) {
+// batch loss, outlier decision (on the pre-update stats) + EMA update (reading R8), stale decision
+// (reading R10), info record and accepted count. One thread. Returns "accepted".
+GORILA_DEV int td_decide(const TdParams& p, const float* s_sq, const float* s_ab, int nwarps) {
+    float tsq = 0.f, tab = 0.f;
+    for (int w = 0; w < nwarps; ++w) {
+        tsq += s_sq[w];
+        tab += s_ab[w];
+    }
+    const float loss = tsq / (float)p.B, ell = tab / (float)p.B;
+    LearnerStats st = *p.stats;
+    const double thr = st.mu + (double)p.outlier_k * sqrt(st.var);
+    const bool rejected = p.outlier_enabled && st.count >= (uint32_t)p.outlier_warmup && (double)ell > thr;
+    DevLearnerInfo inf{};
+    inf.stats_count = st.count;
+    if (st.count == 0) {
+        st.mu = ell;
+        st.var = 0.0;
+    } else {
+        const double e = (double)ell - st.mu;
+        st.mu = st.mu + (1.0 - p.outlier_beta) * e;
+        st.var = p.outlier_beta * (st.var + (1.0 - p.outlier_beta) * e * e);
+    }
+    st.count += 1;
+    *p.stats = st;
+    const uint64_t V0 = *p.V, base = *p.base_V;
+    const bool stale = p.max_staleness >= 0 && (int64_t)(V0 - base) > p.max_staleness;
+    const bool accepted = !rejected && !stale;
+    inf.loss = loss;
+    inf.abs_loss = ell;
+    inf.mu = st.mu;
+    inf.var = st.var;
+    inf.threshold = thr;
+    inf.base_version = base;
+    inf.rejected_outlier = rejected;
+    inf.stale = stale;
+    inf.accepted = accepted;
+    *p.info = inf;
+    if (accepted) *p.n_acc_local += 1;
+    return accepted;
+}
+
+// ------------------------------------------------------------------------- fc5 forward + K7
+// Grid (B, 2): block (b, z) computes Q(s_b, .) (z = 0, online) or Q-hat(s'_b, .) (z = 1, target);
+// the last block to finish (device counter) runs K7 for the whole batch. Replaces the
+// fc5-forward and TD launches.
+struct Fc5TdParams {
+    const float *a4, *t4, *w5, *b5, *w5t, *b5t;
+    unsigned int* counter;  // zero between launches (the last block resets it)
+    TdParams td;
+};
+__global__ void __launch_bounds__(256) k_fc5_td(Fc5TdParams p) {
+    pdl_wait();
+    pdl_trigger();
+    const TdParams& t = p.td;
+    const int b = blockIdx.x, z = blockIdx.y, nA = t.nA;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    {
+        const float* x = (z ? p.t4 : p.a4) + (int64_t)b * FC4_OUT;
+        const float* w5 = z ? p.w5t : p.w5;
+        const float* b5 = z ? p.b5t : p.b5;
+        float* q = const_cast<float*>(z ? t.Qhat : t.Q);
+        float xv[FC4_OUT / 32];
+#pragma unroll
+        for (int k = 0; k < FC4_OUT / 32; ++k) xv[k] = x[lane + 32 * k];
+        for (int a = warp; a < nA; a += 8) {
+            float acc = 0.f;
+#pragma unroll
+            for (int k = 0; k < FC4_OUT / 32; ++k) acc = fmaf(xv[k], w5[a * FC4_OUT + lane + 32 * k], acc);
+            acc = warp_sum(acc);
+            if (lane == 0) q[b * nA + a] = acc + b5[a];
+        }
+    }
+    __shared__ unsigned int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(p.counter, 1u) == gridDim.x * gridDim.y - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    // K7 on the whole batch (this block only)
     __shared__ float s_sq[8], s_ab[8];
     __shared__ int s_keep;
-    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     float sq = 0.f, ab = 0.f;
-    for (int i = warp; i < p.B; i += 8) {
-        const float qh = lane < p.nA ? p.Qhat[i * p.nA + lane] : -INFINITY;
+    for (int i = warp; i < t.B; i += 8) {
+        const float qh = lane < nA ? __ldcg(&t.Qhat[i * nA + lane]) : -INFINITY;
         const float mx = warp_max(qh);
-        const int ai = p.a[i];
-        const float y = p.d[i] ? p.r[i] : p.r[i] + p.gamma * mx;
-        const float qa = p.Q[i * p.nA + ai];
-        const float delta = y - qa;
-        if (lane < p.nA) {
-            const float cl = fminf(fmaxf(delta, -1.f), 1.f);
-            p.dQ[i * p.nA + lane] = (lane == ai) ? -cl / (float)p.B : 0.f;
+        const int ai = t.a[i];
+        const float y = t.d[i] ? t.r[i] : t.r[i] + t.gamma * mx;  // Alg.1
+        const float delta = y - __ldcg(&t.Q[i * nA + ai]);
+        if (lane < nA) {
+            const float cl = fminf(fmaxf(delta, -1.f), 1.f);  // reading R3
+            t.dQ[i * nA + lane] = (lane == ai) ? -cl / (float)t.B : 0.f;
         }
         sq += delta * delta;
         ab += fabsf(delta);
@@ -208,50 +246,17 @@ __global__ void __launch_bounds__(256) k_td(TdParams p) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        float tsq = 0.f, tab = 0.f;
-        for (int w = 0; w < 8; ++w) {
-            tsq += s_sq[w];
-            tab += s_ab[w];
-        }
-        const float loss = tsq / (float)p.B, ell = tab / (float)p.B;
-        LearnerStats st = *p.stats;
-        const double thr = st.mu + (double)p.outlier_k * sqrt(st.var);
-        const bool rejected = p.outlier_enabled && st.count >= (uint32_t)p.outlier_warmup && (double)ell > thr;
-        DevLearnerInfo inf{};
-        inf.stats_count = st.count;
-        // EMA update with every batch (reading R8)
-        if (st.count == 0) {
-            st.mu = ell;
-            st.var = 0.0;
-        } else {
-            const double e = (double)ell - st.mu;
-            st.mu = st.mu + (1.0 - p.outlier_beta) * e;
-            st.var = p.outlier_beta * (st.var + (1.0 - p.outlier_beta) * e * e);
-        }
-        st.count += 1;
-        *p.stats = st;
-        const uint64_t V0 = *p.V, base = *p.base_V;
-        const bool stale = p.max_staleness >= 0 && (int64_t)(V0 - base) > p.max_staleness;
-        const bool accepted = !rejected && !stale;
-        inf.loss = loss;
-        inf.abs_loss = ell;
-        inf.mu = st.mu;
-        inf.var = st.var;
-        inf.threshold = thr;
-        inf.base_version = base;
-        inf.rejected_outlier = rejected;
-        inf.stale = stale;
-        inf.accepted = accepted;
-        *p.info = inf;
-        if (accepted) *p.n_acc_local += 1;
-        s_keep = accepted;
+        s_keep = td_decide(t, s_sq, s_ab, 8);
+        *p.counter = 0;
     }
     __syncthreads();
     if (!s_keep)
-        for (int e = threadIdx.x; e < p.B * p.nA; e += blockDim.x) p.dQ[e] = 0.f;
+        for (int e = threadIdx.x; e < t.B * nA; e += blockDim.x) t.dQ[e] = 0.f;
 }
 
 __global__ void k_mark_not_ready(DevLearnerInfo* info, const LearnerStats* st) {
+    pdl_wait();
+    pdl_trigger();
     DevLearnerInfo inf{};
     inf.not_ready = 1;
     inf.mu = st->mu;
@@ -266,6 +271,8 @@ __global__ void k_mark_not_ready(DevLearnerInfo* info, const LearnerStats* st) {
 template <typename T>
 __global__ void k_fc5_bwd(const float* __restrict__ dQ, const float* __restrict__ a4, const float* __restrict__ w5,
                           int B, int nA, float* __restrict__ G, T* __restrict__ g4, int accumulate) {
+    pdl_wait();
+    pdl_trigger();
     const int n_w = nA * FC4_OUT, n_b = nA, n_g = B * FC4_OUT;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_w + n_b + n_g; e += gridDim.x * blockDim.x) {
         if (e < n_w) {
@@ -290,12 +297,15 @@ __global__ void k_fc5_bwd(const float* __restrict__ dQ, const float* __restrict_
 // ------------------------------------------------------------------------- bias gradients
 // db_l[o] = sum_m g_l[m][o], layers 1..4: block (chunk, l) sums rows [chunk*rows_per, ...) with
 // coalesced row reads and a fixed-order in-block reduction -> part[l][chunk][o]; K10 sums chunks.
-constexpr int BIAS_CHUNKS = 32;
+constexpr int BIAS_CHUNKS = 64;
 template <typename T>
 __global__ void __launch_bounds__(256) k_bias_partial(const T* __restrict__ g1, const T* __restrict__ g2,
                                                       const T* __restrict__ g3, const T* __restrict__ g4, int B,
                                                       float* __restrict__ part) {
-    __shared__ float red[256];
+    pdl_wait();
+    pdl_trigger();
+    // each thread owns 8 consecutive channels (one 16-B vector per row) of rows rg, rg+RG, ...
+    __shared__ float red[256 * 8];
     const int l = blockIdx.y, chunk = blockIdx.x;
     const T* g = l == 0 ? g1 : l == 1 ? g2 : l == 2 ? g3 : g4;
     const int C = l == 0 ? C1_OUT : l == 3 ? FC4_OUT : C2_OUT;
@@ -304,21 +314,28 @@ __global__ void __launch_bounds__(256) k_bias_partial(const T* __restrict__ g1, 
                                                                              : BIAS_CHUNKS * (C1_OUT + 2 * C2_OUT));
     const int per = (rows + BIAS_CHUNKS - 1) / BIAS_CHUNKS;
     const int r0 = chunk * per, r1 = min(rows, r0 + per);
-    for (int c0 = 0; c0 < C; c0 += 256) {
-        const int cw = min(256, C - c0);
-        const int RG = 256 / cw;
-        const int c = c0 + threadIdx.x % cw, rg = threadIdx.x / cw;
-        float acc = 0.f;
-        if (rg < RG)
-            for (int r = r0 + rg; r < r1; r += RG) acc += tof(g[(int64_t)r * C + c]);
-        red[threadIdx.x] = acc;
-        __syncthreads();
-        if (threadIdx.x < cw) {
-            float t = 0.f;
-            for (int q = 0; q < RG; ++q) t += red[threadIdx.x + q * cw];
-            out[chunk * C + c0 + threadIdx.x] = t;
+    const int VPR = C / 8;             // vectors per row
+    const int RG = 256 / VPR;          // rows in flight per block pass
+    const int vc = threadIdx.x % VPR, rg = threadIdx.x / VPR;
+    float acc[8] = {};
+    constexpr int V = 16 / sizeof(T);  // elements per 16-B vector (8 bf16 / 4 fp32)
+    for (int r = r0 + rg; r < r1; r += RG) {
+#pragma unroll
+        for (int h = 0; h < 8 / V; ++h) {
+            const uint4 q = *reinterpret_cast<const uint4*>(g + (int64_t)r * C + vc * 8 + h * V);
+            const T* e = reinterpret_cast<const T*>(&q);
+#pragma unroll
+            for (int k = 0; k < V; ++k) acc[h * V + k] += tof(e[k]);
         }
-        __syncthreads();
+    }
+#pragma unroll
+    for (int k = 0; k < 8; ++k) red[threadIdx.x * 8 + k] = acc[k];
+    __syncthreads();
+    for (int c = threadIdx.x; c < C; c += 256) {  // fixed-order sum over the row groups
+        const int v = c / 8, k = c % 8;
+        float t = 0.f;
+        for (int q = 0; q < RG; ++q) t += red[(q * VPR + v) * 8 + k];
+        out[chunk * C + c] = t;
     }
 }
 
@@ -332,14 +349,26 @@ struct WgradReduceParams {
     int nseg, accumulate;
 };
 __global__ void k_wgrad_reduce(WgradReduceParams p, float* __restrict__ G) {
+    pdl_wait();
+    pdl_trigger();
     int64_t total = 0;
     for (int l = 0; l < p.nseg; ++l) total += p.count[l];
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         int l = 0;
         int64_t f = e;
         while (f >= p.count[l]) f -= p.count[l++];
-        float acc = 0.f;
-        for (int s = 0; s < p.splits[l]; ++s) acc += p.part[l][(int64_t)s * p.count[l] + f];
+        // 8 independent partial sums (all loads in flight), combined in a fixed order
+        const float* src = p.part[l] + f;
+        const int S = p.splits[l];
+        const int64_t st = p.count[l];
+        float a8[8] = {};
+        int s = 0;
+        for (; s + 8 <= S; s += 8) {
+#pragma unroll
+            for (int u = 0; u < 8; ++u) a8[u] += src[(int64_t)(s + u) * st];
+        }
+        for (int u = 0; s < S; ++s, ++u) a8[u] += src[(int64_t)s * st];
+        const float acc = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
         float* dst = G + p.off[l] + f;
         *dst = p.accumulate ? *dst + acc : acc;
     }
@@ -351,7 +380,14 @@ struct ApplyParams {
     float* m;
     float* v;
     const float* g;      // this rank's reduced slice
-    const float* count;  // accepted gradients this round (all ranks)
+    const float* count;  // accepted gradients this round (all ranks), world > 1
+    const uint32_t* count_local;  // world == 1: the learners' own counter
+    uint64_t* dev_round;  // advanced by one (the next round's sampler counter)
+    // fused target-sync decisions (gorila_round): R13, evaluated on the updated V
+    LearnerStats* sync_stats[8];
+    uint8_t* sync_flag[8];
+    int n_sync;
+    int64_t period;
     int64_t n_real;      // real elements in this slice
     int optimizer;
     float lr, rho, eps, ada_eps;
@@ -386,7 +422,9 @@ GORILA_DEV void emit4(const ApplyParams& p, int64_t e4, const float* tv) {
 
 template <typename T>
 __global__ void __launch_bounds__(256) k_apply(ApplyParams p) {
-    const float cnt = *p.count;
+    pdl_wait();
+    pdl_trigger();
+    const float cnt = p.count_local ? (float)*p.count_local : *p.count;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         const uint64_t v0 = *p.V;
         const uint64_t n_acc = (uint64_t)(cnt + 0.5f);
@@ -395,6 +433,13 @@ __global__ void __launch_bounds__(256) k_apply(ApplyParams p) {
         p.round_info[2] = v0 + n_acc;
         *p.V = v0 + n_acc;
         if (p.vhist_dst) *p.vhist_dst = v0 + n_acc;
+        if (p.dev_round) *p.dev_round += 1;
+        for (int i = 0; i < p.n_sync; ++i) {
+            LearnerStats* st = p.sync_stats[i];
+            const bool doit = v0 + n_acc >= st->last_sync + (uint64_t)p.period;
+            if (doit) st->last_sync = v0 + n_acc;
+            *p.sync_flag[i] = doit;
+        }
     }
     const bool update = cnt > 0.5f;
     const float inv = update ? 1.0f / cnt : 0.f;
@@ -433,6 +478,8 @@ __global__ void __launch_bounds__(256) k_apply(ApplyParams p) {
 
 // this rank's accepted count, once per destination shard (reduce-scattered with G)
 __global__ void k_write_counts(float* counts, int W, const uint32_t* n_acc_local) {
+    pdl_wait();
+    pdl_trigger();
     const int s = threadIdx.x;
     if (s < W) counts[s] = (float)*n_acc_local;
 }
@@ -443,6 +490,8 @@ template <typename T>
 __global__ void k_pack(const float* __restrict__ theta, int nA, T* __restrict__ rt, float* __restrict__ rf,
                        const uint8_t* __restrict__ pred, uint64_t* __restrict__ vhist_dst,
                        const uint64_t* __restrict__ V) {
+    pdl_wait();
+    pdl_trigger();
     if (pred && !*pred) return;
     const ReplicaLayout L = replica_layout(nA);
     const int64_t P = param_count(nA);
@@ -457,6 +506,8 @@ __global__ void k_pack(const float* __restrict__ theta, int nA, T* __restrict__ 
 // ------------------------------------------------------------------------- target sync decision
 // Alg.1; R13: sync iff force or V >= last + N; then last = V.
 __global__ void k_sync_decide(LearnerStats* st, const uint64_t* V, int64_t period, int force, uint8_t* flag) {
+    pdl_wait();
+    pdl_trigger();
     const uint64_t v = *V;
     const bool doit = force || v >= st->last_sync + (uint64_t)period;
     if (doit) st->last_sync = v;
@@ -466,6 +517,8 @@ __global__ void k_sync_decide(LearnerStats* st, const uint64_t* V, int64_t perio
 // ------------------------------------------------------------------------- layout conversion
 // dir 0: canonical -> internal ; dir 1: internal -> canonical
 __global__ void k_convert(const float* __restrict__ src, float* __restrict__ dst, int64_t P, int dir) {
+    pdl_wait();
+    pdl_trigger();
     for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < P; i += (int64_t)gridDim.x * blockDim.x) {
         const int64_t c = canon_of_internal(i);
         if (dir == 0) dst[i] = src[c];
@@ -473,7 +526,10 @@ __global__ void k_convert(const float* __restrict__ src, float* __restrict__ dst
     }
 }
 
-__global__ void k_set_u64(uint64_t* dst, uint64_t v) { *dst = v; }
-__global__ void k_inc_u64(uint64_t* dst) { *dst += 1; }
+__global__ void k_set_u64(uint64_t* dst, uint64_t v) {
+    pdl_wait();
+    pdl_trigger();
+    *dst = v;
+}
 
 }  // namespace gorila

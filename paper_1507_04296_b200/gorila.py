@@ -151,7 +151,8 @@ class Gorila:
         L = load()
         self.torch = torch
         self.device = device or torch.device("cuda", torch.cuda.current_device())
-        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        # a dedicated stream by default (the legacy default stream cannot be graph-captured)
+        self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
         self.n_actions, self.batch, self.L = n_actions, batch, n_learners_local
         self.P = param_count(n_actions)
         theta0 = np.ascontiguousarray(theta0, dtype=np.float32)
@@ -193,6 +194,8 @@ class Gorila:
     def replay_insert(self, learner, frames, actions, rewards, terminals):
         count = int(frames.shape[0])
         fp, dev = _ptr(frames)
+        if dev:  # device inputs produced on torch's current stream: order our stream after it
+            self.stream.wait_stream(self.torch.cuda.current_stream(self.device))
         ap, _ = _ptr(actions)
         rp, _ = _ptr(rewards)
         dp, _ = _ptr(terminals)
