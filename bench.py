@@ -325,6 +325,12 @@ def main():
         k += 1
     phases, n_prof = g.profile_read()
     g.profile_enable(False)
+    # per-phase marginal device time, kernels re-launched back to back (warm L2, PDL as in the round)
+    iso = {}
+    for ph in phases:
+        if ph in ("td", "step_misc", "reduce_scatter", "all_gather") or (ph == "pack" and world == 1):
+            continue
+        iso[ph] = g.bench_phase(ph, iters=200)
 
     peaks = read_peaks()
     P = g.P
@@ -384,6 +390,7 @@ def main():
                          "ms_per_launch": dom_roof["ms_per_launch"],
                          "algorithmic_per_launch": dom_roof["algorithmic_per_launch"]},
             "phases_ms_per_step": {p: v for p, v in per_launch_ms.items() if v > 0},
+            "phases_isolated_us": iso,
             "phase_rooflines": {p: roof(p) for p in phases if roof(p) is not None},
         }
         if world == 1 and not args.no_cpu_baseline:

@@ -223,6 +223,14 @@ GORILA_API gorila_status gorila_profile_enable(gorila_ctx* ctx, int32_t enable);
 GORILA_API gorila_status gorila_profile_read(gorila_ctx* ctx, double* ms, int32_t n, uint64_t* n_steps);
 GORILA_API int32_t gorila_profile_phase_count(void);
 GORILA_API const char* gorila_profile_phase_name(int32_t i);
+/* Diagnostics: re-launch the kernels of one phase (index < gorila_profile_phase_count();
+ * learner phases act on local learner `learner`'s buffers from its last learner_step)
+ * `iters` times back-to-back on the stream and return the mean device time per
+ * repetition in microseconds (CUDA events; warm L2; launches overlap through PDL as in a
+ * round). Results written by the repeated kernels are scratch: call it outside the
+ * parity-checked sequence. Synchronises the stream. */
+GORILA_API gorila_status gorila_bench_phase(gorila_ctx* ctx, int32_t learner, int32_t phase, int32_t iters,
+                                            double* us_per_iter);
 /* Writes a fresh 128-byte ncclUniqueId (rank 0 calls it and broadcasts the bytes). */
 GORILA_API gorila_status gorila_nccl_unique_id(void* out128);
 /* Number of kernels this library launched so far (evidence counter). */

@@ -107,6 +107,14 @@ GORILA_DEV void tmem_ld16(uint32_t taddr, float* v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// ---- cp.async (LDGSTS): 16-byte global -> shared copies; src_bytes = 0 zero-fills the destination
+GORILA_DEV void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");
+}
+GORILA_DEV void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+GORILA_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory"); }
+
 // ---- programmatic dependent launch: wait for the preceding grid's results / let the next grid launch
 GORILA_DEV void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 GORILA_DEV void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }

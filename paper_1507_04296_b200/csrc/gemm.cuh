@@ -36,8 +36,6 @@ using Conv1 = ConvShape<IMG, IMG, NSTACK, C1_K, C1_S, C1_OUT>;
 using Conv2 = ConvShape<H1, H1, C1_OUT, C2_K, C2_S, C2_OUT>;
 using Conv3 = ConvShape<H2, H2, C2_OUT, C3_K, C3_S, C3_OUT>;
 
-GORILA_DEV uint4 zero4() { return make_uint4(0, 0, 0, 0); }
-
 // ====================================================================== loaders
 
 template <typename T>
@@ -47,23 +45,23 @@ struct LdRows {  // K-major: value(i, r) = X[i][r] (row-major, leading dimension
     int64_t ld;
     int rows, cols;
     GORILA_DEV float load(int i, int r) const { return (i < rows && r < cols) ? tof(x[(int64_t)i * ld + r]) : 0.f; }
-    GORILA_DEV uint4 load8(int i, int r0) const {
-        if (i >= rows || r0 >= cols) return zero4();
-        return *reinterpret_cast<const uint4*>(x + (int64_t)i * ld + r0);
+    GORILA_DEV const T* src8(int i, int r0) const {
+        return (i >= rows || r0 >= cols) ? nullptr : x + (int64_t)i * ld + r0;
     }
+    GORILA_DEV const void* gptr() const { return x; }  // any valid global address (zero-fill source)
 };
 
 template <typename T>
-struct LdRowsMN {  // MN-major: value(i, r) = X[r][i]; load8(i0, r) = X[r][i0 .. i0+7]
+struct LdRowsMN {  // MN-major: value(i, r) = X[r][i]; src8(i0, r) = &X[r][i0] (8 consecutive i)
     static constexpr bool kMN = true;
     const T* x;
     int64_t ld;
     int rows, cols;  // i extent (multiple of 8), r extent
     GORILA_DEV float load(int i, int r) const { return (i < rows && r < cols) ? tof(x[(int64_t)r * ld + i]) : 0.f; }
-    GORILA_DEV uint4 load8(int i0, int r) const {
-        if (i0 >= rows || r >= cols) return zero4();
-        return *reinterpret_cast<const uint4*>(x + (int64_t)r * ld + i0);
+    GORILA_DEV const T* src8(int i0, int r) const {
+        return (i0 >= rows || r >= cols) ? nullptr : x + (int64_t)r * ld + i0;
     }
+    GORILA_DEV const void* gptr() const { return x; }  // any valid global address (zero-fill source)
 };
 
 // im2col of an NHWC input: value(m = (b, oy, ox), r = (ky*K + kx)*C + c) = in[b][oy*S+ky][ox*S+kx][c]
@@ -82,22 +80,22 @@ struct LdConvIn {  // K-major forward operand (8 consecutive r = same pixel chan
     const T* in;
     int M;
     GORILA_DEV float load(int m, int r) const { return (m < M && r < SH::R) ? tof(in[conv_in_addr<SH>(m, r)]) : 0.f; }
-    GORILA_DEV uint4 load8(int m, int r0) const {
-        if (m >= M || r0 >= SH::R) return zero4();
-        return *reinterpret_cast<const uint4*>(in + conv_in_addr<SH>(m, r0));
+    GORILA_DEV const T* src8(int m, int r0) const {
+        return (m >= M || r0 >= SH::R) ? nullptr : in + conv_in_addr<SH>(m, r0);
     }
+    GORILA_DEV const void* gptr() const { return in; }  // any valid global address (zero-fill source)
 };
 
 template <typename T, typename SH>
-struct LdConvInMN {  // MN-major weight-gradient operand: value(i = r, red = m); load8(r0, m)
+struct LdConvInMN {  // MN-major weight-gradient operand: value(i = r, red = m); src8(r0, m)
     static constexpr bool kMN = true;
     const T* in;
     int M;
     GORILA_DEV float load(int r, int m) const { return (m < M && r < SH::R) ? tof(in[conv_in_addr<SH>(m, r)]) : 0.f; }
-    GORILA_DEV uint4 load8(int r0, int m) const {
-        if (m >= M || r0 >= SH::R) return zero4();
-        return *reinterpret_cast<const uint4*>(in + conv_in_addr<SH>(m, r0));
+    GORILA_DEV const T* src8(int r0, int m) const {
+        return (m >= M || r0 >= SH::R) ? nullptr : in + conv_in_addr<SH>(m, r0);
     }
+    GORILA_DEV const void* gptr() const { return in; }  // any valid global address (zero-fill source)
 };
 
 // conv dgrad operand: output gradient g (NHWC [B][OH][OW][CO]) seen from input position
@@ -125,11 +123,12 @@ struct LdDgrad {
         const int64_t a = dgrad_addr<SH>(i, r);
         return a < 0 ? 0.f : tof(g[a]);
     }
-    GORILA_DEV uint4 load8(int i, int r0) const {
-        if (i >= M || r0 >= SH::RD) return zero4();
+    GORILA_DEV const T* src8(int i, int r0) const {
+        if (i >= M || r0 >= SH::RD) return nullptr;
         const int64_t a = dgrad_addr<SH>(i, r0);
-        return a < 0 ? zero4() : *reinterpret_cast<const uint4*>(g + a);
+        return a < 0 ? nullptr : g + a;
     }
+    GORILA_DEV const void* gptr() const { return g; }  // any valid global address (zero-fill source)
 };
 
 // conv dgrad weight operand read straight from the forward (KRSC) weight, MN-major over c:
@@ -143,10 +142,10 @@ struct LdWdgradMN {
         return (int64_t)o * SH::R + t * SH::C + c;
     }
     GORILA_DEV float load(int c, int r) const { return (c < SH::C && r < SH::RD) ? tof(w[addr(c, r)]) : 0.f; }
-    GORILA_DEV uint4 load8(int c0, int r) const {
-        if (c0 >= SH::C || r >= SH::RD) return zero4();
-        return *reinterpret_cast<const uint4*>(w + addr(c0, r));
+    GORILA_DEV const T* src8(int c0, int r) const {
+        return (c0 >= SH::C || r >= SH::RD) ? nullptr : w + addr(c0, r);
     }
+    GORILA_DEV const void* gptr() const { return w; }  // any valid global address (zero-fill source)
 };
 
 // ====================================================================== epilogues
@@ -354,7 +353,8 @@ __host__ __device__ constexpr uint32_t tmem_cols_for(int bn) {
 }
 // fp32 partial tile for the cluster reduction: [BN/16][128 rows][20 floats] (80-B row pitch: conflict-free)
 __host__ __device__ constexpr int tc_red_bytes(int bn) { return (bn / 16) * TC_BM * 80; }
-__host__ __device__ constexpr int tc_stage_bytes(int bn) { return 2 * (TC_BM * TC_BK * 2 + bn * TC_BK * 2); }
+__host__ __device__ constexpr int tc_stages(int bn) { return bn <= 64 ? 4 : bn <= 128 ? 3 : 2; }
+__host__ __device__ constexpr int tc_stage_bytes(int bn) { return tc_stages(bn) * (TC_BM * TC_BK * 2 + bn * TC_BK * 2); }
 __host__ __device__ constexpr int tc_smem_bytes(int bn) {
     return (tc_stage_bytes(bn) > tc_red_bytes(bn) ? tc_stage_bytes(bn) : tc_red_bytes(bn)) + 64;
 }
@@ -392,34 +392,33 @@ struct Stage {
         if constexpr (!MN) return umma_desc(base + kk * 256, 128, 1024);
         else return umma_desc(base + kk * 2 * ROWS * 16, ROWS * 16, 128);
     }
+    // this thread's 16-B chunks of the tile: cp.async global -> shared, zero-fill where the
+    // loader has no data (out of range rows, missing conv taps)
     template <typename LD>
-    GORILA_DEV static void load(const LD& ld, int row0, int r0, uint4* regs) {
+    GORILA_DEV static void issue(const LD& ld, int row0, int r0, uint32_t st) {
 #pragma unroll
         for (int q = 0; q < ITERS; ++q) {
+            const int idx = threadIdx.x + TC_THREADS * q;
             int row, k;
-            coords(threadIdx.x + TC_THREADS * q, row, k);
-            regs[q] = ld.load8(row0 + row, r0 + k);
+            coords(idx, row, k);
+            const void* src = ld.src8(row0 + row, r0 + k);
+            cp_async16(st + offset(idx), src ? src : ld.gptr(), src ? 16u : 0u);
         }
-    }
-    GORILA_DEV static void store(uint8_t* st, const uint4* regs) {
-#pragma unroll
-        for (int q = 0; q < ITERS; ++q)
-            *reinterpret_cast<uint4*>(st + offset(threadIdx.x + TC_THREADS * q)) = regs[q];
     }
 };
 
 template <int BN, typename LA, typename LB, typename EP>
 __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ GemmBatch<LA, LB, EP> p) {
-    constexpr int A_BYTES = TC_BM * TC_BK * 2, B_BYTES = BN * TC_BK * 2;
+    constexpr int A_BYTES = TC_BM * TC_BK * 2, B_BYTES = BN * TC_BK * 2, STAGES = tc_stages(BN);
     static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
     static_assert((BN * 8) % TC_THREADS == 0, "B tile split");
     using SA = Stage<TC_BM, LA::kMN>;
     using SB = Stage<BN, LB::kMN>;
     extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* sA = smem;                // [2][A_BYTES]
-    uint8_t* sB = smem + 2 * A_BYTES;  // [2][B_BYTES]
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + tc_smem_bytes(BN) - 64);
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + 2);
+    uint8_t* sA = smem;                     // [STAGES][A_BYTES]
+    uint8_t* sB = smem + STAGES * A_BYTES;  // [STAGES][B_BYTES]
+    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + tc_smem_bytes(BN) - 64);  // [STAGES]
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + STAGES);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int prob = blockIdx.z / p.splits, split = blockIdx.z - prob * p.splits;
@@ -431,8 +430,7 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
 
     if (warp == 0) tmem_alloc(tmem_slot, tmem_cols_for(BN));
     if (tid == 0) {
-        mbar_init(&mbar[0], 1);
-        mbar_init(&mbar[1], 1);
+        for (int st = 0; st < STAGES; ++st) mbar_init(&mbar[st], 1);
         fence_mbar_init();
     }
     tc_fence_before();
@@ -443,39 +441,45 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t IDESC =
         umma_idesc_bf16(TC_BM, BN) | (LA::kMN ? (1u << 15) : 0u) | (LB::kMN ? (1u << 16) : 0u);
+    const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
 
-    uint4 ra[SA::ITERS], rb[SB::ITERS];
-    if (nK > 0) {
-        SA::load(P.a, i0, kc_begin * TC_BK, ra);
-        SB::load(P.b, j0, kc_begin * TC_BK, rb);
+    // multi-stage cp.async pipeline: up to STAGES-1 chunks in flight ahead of the MMA
+    auto issue = [&](int kc) {
+        const int st = kc % STAGES;
+        SA::issue(P.a, i0, (kc_begin + kc) * TC_BK, sA0 + st * A_BYTES);
+        SB::issue(P.b, j0, (kc_begin + kc) * TC_BK, sB0 + st * B_BYTES);
+    };
+#pragma unroll 1
+    for (int kc = 0; kc < STAGES - 1; ++kc) {
+        if (kc < nK) issue(kc);
+        cp_async_commit();
     }
+#pragma unroll 1
     for (int kc = 0; kc < nK; ++kc) {
-        const int s = kc & 1;
-        if (kc >= 2) mbar_wait(&mbar[s], ((kc - 2) >> 1) & 1);  // MMAs of chunk kc-2 released stage s
-        uint8_t* a_st = sA + s * A_BYTES;
-        uint8_t* b_st = sB + s * B_BYTES;
-        SA::store(a_st, ra);
-        SB::store(b_st, rb);
-        fence_proxy_async_smem();
+        const int nxt = kc + STAGES - 1;
+        if (nxt < nK) {
+            // stage nxt % STAGES was last read by the MMAs of chunk nxt - STAGES = kc - 1
+            if (nxt >= STAGES) mbar_wait(&mbar[nxt % STAGES], ((nxt - STAGES) / STAGES) & 1);
+            issue(nxt);
+        }
+        cp_async_commit();
+        cp_async_wait<STAGES - 1>();  // this thread's copies of chunk kc have landed
+        fence_proxy_async_smem();     // ... and are visible to the tensor core
         __syncthreads();
         if (tid == 0) {
             tc_fence_after();
-            const uint32_t a_base = smem_u32(a_st), b_base = smem_u32(b_st);
+            const int st = kc % STAGES;
+            const uint32_t a_base = sA0 + st * A_BYTES, b_base = sB0 + st * B_BYTES;
 #pragma unroll
             for (int kk = 0; kk < TC_BK / 16; ++kk)
                 umma_bf16(tmem, SA::desc(a_base, kk), SB::desc(b_base, kk), IDESC, (kc > 0 || kk > 0) ? 1u : 0u);
-            umma_commit(&mbar[s]);
-        }
-        if (kc + 1 < nK) {
-            SA::load(P.a, i0, (kc_begin + kc + 1) * TC_BK, ra);
-            SB::load(P.b, j0, (kc_begin + kc + 1) * TC_BK, rb);
+            umma_commit(&mbar[st]);
         }
     }
-    if (nK > 0) {
-        const int last = nK - 1;
-        mbar_wait(&mbar[last & 1], (last >> 1) & 1);
-        if (last >= 1) mbar_wait(&mbar[(last - 1) & 1], ((last - 1) >> 1) & 1);
-    }
+    cp_async_wait<0>();
+    // the last MMAs are done when the commits of the final chunks arrive (drain the most recent
+    // pending completion of every stage so no arrive is in flight at exit)
+    for (int c = max(0, nK - STAGES); c < nK; ++c) mbar_wait(&mbar[c % STAGES], (c / STAGES) & 1);
     tc_fence_after();
 
     // epilogue: warp w owns TMEM lanes (= tile rows) 32w .. 32w+31

@@ -325,7 +325,9 @@ int eff_splits(bool fp32, int R, int splits) {
 
 // ------------------------------------------------------------------ one learner update
 template <typename T>
-gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int accumulate) {
+gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int accumulate,
+                          uint32_t phases = 0xffffffffu) {
+#define PHASE(ph) if (phases & (1u << (ph)))
     const gorila_config& cfg = ctx->cfg;
     Learner& Lr = ctx->learners[j];
     const int B = ctx->B, nA = ctx->nA;
@@ -345,6 +347,8 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     float *a4 = ctx->a4, *t4 = ctx->t4;
     T *g1 = P_<T>(ctx->g1), *g2 = P_<T>(ctx->g2), *g3 = P_<T>(ctx->g3), *g4 = P_<T>(ctx->g4);
 
+    const float in_scale = 1.0f / 255.0f;  // reading R17 (fp32 constant, folded into conv1's epilogue)
+    PHASE(PH_SAMPLE) {
     // K1: sample + gather + stack (Alg.1)
     {
         dim3 grid((FRAME_BYTES / 16 + 255) / 256, B);
@@ -354,8 +358,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                (uint32_t)(cfg.learner_id_base + j), (const uint64_t*)ctx->dev_round, B, s, s2, ctx->sa, ctx->sr,
                ctx->sd, ctx->sidx, accumulate ? (uint32_t*)nullptr : ctx->n_acc_local);
     }
+    }
     mark(ctx, PH_SAMPLE);
-    const float in_scale = 1.0f / 255.0f;  // reading R17 (fp32 constant, folded into conv1's epilogue)
+    PHASE(PH_CONV1F) {
     // conv1 fwd (online on s with theta, target on s' with theta^-)
     {
         using LA = LdConvIn<T, Conv1>; using LB = LdRows<T>; using EP = EpAct<T>;
@@ -365,7 +370,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             {{s2, M}, {tt + RT.w1, K1, C1_OUT, K1}, {t1, C1_OUT, tf + RT.b1, in_scale, M, C1_OUT, 1}}};
         gemm<T, 32>(ctx, pr, 2, M, C1_OUT, K1, 1);
     }
+    }
     mark(ctx, PH_CONV1F);
+    PHASE(PH_CONV2F) {
     // conv2 fwd
     {
         using LA = LdConvIn<T, Conv2>; using LB = LdRows<T>; using EP = EpAct<T>;
@@ -375,7 +382,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             {{t1, M}, {tt + RT.w2, K2, C2_OUT, K2}, {t2, C2_OUT, tf + RT.b2, 1.f, M, C2_OUT, 1}}};
         gemm<T, 64>(ctx, pr, 2, M, C2_OUT, K2, 1, 148);
     }
+    }
     mark(ctx, PH_CONV2F);
+    PHASE(PH_CONV3F) {
     // conv3 fwd
     {
         using LA = LdConvIn<T, Conv3>; using LB = LdRows<T>; using EP = EpAct<T>;
@@ -385,7 +394,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             {{t2, M}, {tt + RT.w3, K3, C3_OUT, K3}, {t3, C3_OUT, tf + RT.b3, 1.f, M, C3_OUT, 1}}};
         gemm<T, 64>(ctx, pr, 2, M, C3_OUT, K3, 1, 148);
     }
+    }
     mark(ctx, PH_CONV3F);
+    PHASE(PH_FC4F) {
     // fc4 fwd, swap-AB (i = n, j = b): a4[b][n] = ReLU(W4[n] . a3[b] + b4[n]) in fp32, the split of
     // K = 3136 reduced inside the cluster (no partial buffers, no finalize kernel)
     {
@@ -397,7 +408,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         DISPATCH_BN_BATCH(B, FC4F);
 #undef FC4F
     }
+    }
     mark(ctx, PH_FC4F);
+    PHASE(PH_FC5F) {
     // fc5 forward (both nets) + K7: TD target, clipped error, loss, outlier + stale decisions
     {
         Fc5TdParams p{};
@@ -411,12 +424,16 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         t.outlier_k = cfg.outlier_k; t.outlier_beta = cfg.outlier_beta;
         launch(ctx, k_fc5_td, dim3(B, 2), dim3(256), 0, p);
     }
+    }
     mark(ctx, PH_FC5F);
     mark(ctx, PH_TD);
+    PHASE(PH_FC5B) {
     // fc5 bwd: dW5, db5 into G; g4 = mask(dQ W5)
     launch(ctx, k_fc5_bwd<T>, dim3(148), dim3(256), 0, (const float*)ctx->dQ, (const float*)a4,
            (const float*)(rf + RL.w5), B, nA, ctx->G, g4, accumulate);
+    }
     mark(ctx, PH_FC5B);
+    PHASE(PH_FC4DG) {
     // fc4 dgrad (i = k, j = b, red = n): g3[b][k] = mask(sum_n W4[n][k] g4[b][n])
     {
         using LA = LdRowsMN<T>; using LB = LdRows<T>; using EP = EpMaskT<T>;
@@ -426,7 +443,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         DISPATCH_BN_BATCH(B, FC4D);
 #undef FC4D
     }
+    }
     mark(ctx, PH_FC4DG);
+    PHASE(PH_FC4WG) {
     // fc4 wgrad (i = k, j = n, red = b): G[W4][n][k] += sum_b a3[b][k] g4[b][n]
     {
         using LA = LdRowsMN<T>; using LB = LdRowsMN<T>; using EP = EpAddT;
@@ -434,7 +453,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                                        {ctx->G + OFF_W4, FC4_IN, FC4_IN, FC4_OUT, accumulate}}};
         gemm<T, 64>(ctx, pr, 1, FC4_IN, FC4_OUT, B, 1);
     }
+    }
     mark(ctx, PH_FC4WG);
+    PHASE(PH_CONV3DG) {
     // conv3 dgrad: g2 = mask(conv3^T(g3))
     {
         using LA = LdDgrad<T, Conv3>; using LB = LdWdgradMN<T, Conv3>; using EP = EpMask<T>;
@@ -443,7 +464,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                                        {g2, a2, C2_OUT, M, C2_OUT}}};
         gemm<T, 64>(ctx, pr, 1, M, C2_OUT, K3, 1, 148);
     }
+    }
     mark(ctx, PH_CONV3DG);
+    PHASE(PH_CONV3WG) {
     // conv3 wgrad (i = r, j = o, red = m): partial[s][o][r]
     {
         using LA = LdConvInMN<T, Conv3>; using LB = LdRowsMN<T>; using EP = EpStoreT;
@@ -452,7 +475,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                                        {ctx->part_w[2], K3, (int64_t)C3_OUT * K3, 1.f, K3, C3_OUT}}};
         gemm<T, 64>(ctx, pr, 1, K3, C3_OUT, Mred, ctx->split_w[2]);
     }
+    }
     mark(ctx, PH_CONV3WG);
+    PHASE(PH_CONV2DG) {
     // conv2 dgrad: g1 = mask(conv2^T(g2))
     {
         using LA = LdDgrad<T, Conv2>; using LB = LdWdgradMN<T, Conv2>; using EP = EpMask<T>;
@@ -461,7 +486,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                                        {g1, a1, C1_OUT, M, C1_OUT}}};
         gemm<T, 32>(ctx, pr, 1, M, C1_OUT, Conv2::RD, 1, 296);
     }
+    }
     mark(ctx, PH_CONV2DG);
+    PHASE(PH_CONV2WG) {
     // conv2 wgrad
     {
         using LA = LdConvInMN<T, Conv2>; using LB = LdRowsMN<T>; using EP = EpStoreT;
@@ -470,7 +497,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                                        {ctx->part_w[1], K2, (int64_t)C2_OUT * K2, 1.f, K2, C2_OUT}}};
         gemm<T, 64>(ctx, pr, 1, K2, C2_OUT, Mred, ctx->split_w[1]);
     }
+    }
     mark(ctx, PH_CONV2WG);
+    PHASE(PH_CONV1WG) {
     // conv1 wgrad (input scale 1/255 folded into the store)
     {
         using LA = LdConvInMN<T, Conv1>; using LB = LdRowsMN<T>; using EP = EpStoreT;
@@ -479,11 +508,15 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                                        {ctx->part_w[0], K1, (int64_t)C1_OUT * K1, in_scale, K1, C1_OUT}}};
         gemm<T, 32>(ctx, pr, 1, K1, C1_OUT, Mred, ctx->split_w[0]);
     }
+    }
     mark(ctx, PH_CONV1WG);
+    PHASE(PH_BIASG) {
     // bias gradients b1..b4 (coalesced partials; reduced by K10)
     launch(ctx, k_bias_partial<T>, dim3(BIAS_CHUNKS, 4), dim3(256), 0, (const T*)g1, (const T*)g2, (const T*)g3,
            (const T*)g4, B, ctx->part_b);
+    }
     mark(ctx, PH_BIASG);
+    PHASE(PH_WGRED) {
     // K10: fixed-order reduction of the conv wgrad partials into G
     {
         WgradReduceParams p{};
@@ -504,9 +537,11 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         p.accumulate = accumulate;
         launch(ctx, k_wgrad_reduce, dim3(148 * 2), dim3(256), 0, p, ctx->G);
     }
+    }
     mark(ctx, PH_WGRED);
     CU(cudaGetLastError());
     return GORILA_OK;
+#undef PHASE
 }
 
 template <typename T>
@@ -665,6 +700,40 @@ gorila_status gorila_profile_read(gorila_ctx* ctx, double* ms, int32_t n, uint64
     for (double& x : ctx->prof_ms) x = 0.0;
     ctx->prof_steps = 0;
     return GORILA_OK;
+}
+
+gorila_status gorila_bench_phase(gorila_ctx* ctx, int32_t learner, int32_t phase, int32_t iters,
+                                double* us_per_iter) {
+    gorila_status s = check_learner(ctx, learner);
+    if (s != GORILA_OK) return s;
+    if (phase < 0 || phase >= PH_COUNT || iters < 1 || !us_per_iter) return fail(GORILA_E_INVALID, "bad argument");
+    cudaStream_t st = ctx->stream;
+    cudaEvent_t e0, e1;
+    CU(cudaEventCreate(&e0));
+    CU(cudaEventCreate(&e1));
+    const bool prof = ctx->prof;
+    ctx->prof = false;
+    CU(cudaEventRecord(e0, st));
+    for (int it = 0; it < iters && s == GORILA_OK; ++it) {
+        if (phase == PH_APPLY || phase == PH_RS || phase == PH_AG || phase == PH_PACK) {
+            s = ps_apply_shard(ctx, ctx->dev_round_expect - 1, nullptr);
+        } else if (phase == PH_SYNC) {
+            s = sync_target(ctx, &learner, 1, 0, nullptr);
+        } else {
+            s = ctx->cfg.math == GORILA_MATH_FP32
+                    ? run_learner<float>(ctx, learner, 0, 0, 0, 1u << phase)
+                    : run_learner<__nv_bfloat16>(ctx, learner, 0, 0, 0, 1u << phase);
+        }
+    }
+    CU(cudaEventRecord(e1, st));
+    CU(cudaEventSynchronize(e1));
+    ctx->prof = prof;
+    float ms = 0.f;
+    CU(cudaEventElapsedTime(&ms, e0, e1));
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    *us_per_iter = 1000.0 * ms / iters;
+    return s;
 }
 
 gorila_status gorila_nccl_unique_id(void* out128) {

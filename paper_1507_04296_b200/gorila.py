@@ -61,7 +61,8 @@ EXPORTS = ["gorila_param_count", "gorila_workspace_bytes", "gorila_init", "goril
            "replay_insert", "replay_sample", "learner_step", "ps_apply_shard", "sync_target", "gorila_get_state",
            "gorila_set_state", "gorila_get_learner_state", "gorila_set_learner_state", "gorila_get_grad",
            "gorila_get_q", "gorila_kernel_launches", "gorila_profile_enable", "gorila_profile_read",
-           "gorila_profile_phase_count", "gorila_profile_phase_name", "gorila_nccl_unique_id", "gorila_round"]
+           "gorila_profile_phase_count", "gorila_profile_phase_name", "gorila_nccl_unique_id", "gorila_round",
+           "gorila_bench_phase"]
 
 
 def load(build_if_missing=True):
@@ -102,6 +103,7 @@ def load(build_if_missing=True):
     L.gorila_profile_phase_name.restype = ctypes.c_char_p
     L.gorila_nccl_unique_id.argtypes = [P]
     L.gorila_round.argtypes = [P, P, i32, u64, P, P, P, P]
+    L.gorila_bench_phase.argtypes = [P, i32, i32, i32, P]
     _lib = L
     return L
 
@@ -316,3 +318,10 @@ class Gorila:
         n = ctypes.c_uint64()
         _check(load().gorila_profile_read(self.h, ms.ctypes.data, len(names), ctypes.byref(n)))
         return dict(zip(names, ms.tolist())), int(n.value)
+
+    def bench_phase(self, phase_name, learner=0, iters=200):
+        """Mean device microseconds of one phase's kernels, re-launched back to back (diagnostics)."""
+        idx = phase_names().index(phase_name)
+        us = ctypes.c_double()
+        _check(load().gorila_bench_phase(self.h, learner, idx, iters, ctypes.byref(us)))
+        return us.value
