@@ -80,7 +80,7 @@ class ClockSampler:
     def __enter__(self):
         try:
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.Q,
-                                          "--format=csv,noheader,nounits", "-lms", "200"], stdout=self.f,
+                                          "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
                                          stderr=subprocess.DEVNULL)
         except FileNotFoundError:
             self.proc = None
@@ -100,7 +100,7 @@ class ClockSampler:
         sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
         mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 5 + i and "Active" in r[5 + i]})
+        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 5 + i and r[5 + i].strip() == "Active"})
         return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
                 "reasons": reasons, "samples": len(rows)}
 
@@ -220,7 +220,7 @@ def config_dict(args, world):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=1000)
+    ap.add_argument("--steps", type=int, default=3000)
     ap.add_argument("--warmup", type=int, default=10)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--math", default="bf16", choices=["bf16", "fp32"])
@@ -336,15 +336,16 @@ def main():
     P = g.P
     esz = 2 if args.math == "bf16" else 4
     total_prof = sum(phases.values())
-    dom = max(phases, key=lambda p: phases[p])
     per_launch_ms = {p: v / max(n_prof, 1) for p, v in phases.items()}
+    iso_ms = {p: v / 1000.0 for p, v in iso.items()}
+    dom = max(iso_ms, key=lambda p: iso_ms[p])
 
     def roof(p):
         w = phase_work(p, args.batch, args.n_actions, P, esz)
-        if w is None or per_launch_ms.get(p, 0.0) <= 0.0:
+        if w is None or iso_ms.get(p, 0.0) <= 0.0:
             return None
         bound, amount = w
-        t = per_launch_ms[p] / 1000.0
+        t = iso_ms[p] / 1000.0
         if bound == "tensor":
             ach = amount / t / 1e12
             peak = peaks["tensor"] if args.math == "bf16" else peaks["tensor"] / 16  # fp32 SIMT: not tensor
@@ -354,12 +355,12 @@ def main():
             peak = peaks["hbm"]
             unit = "GB/s"
         return {"bound": bound, "achieved": ach, "peak": peak, "unit": unit, "frac": ach / peak,
-                "algorithmic_per_launch": amount, "ms_per_launch": per_launch_ms[p]}
+                "algorithmic_per_launch": amount, "ms_per_launch": iso_ms[p]}
 
     dom_roof = roof(dom)
     if dom_roof is None:  # dominant phase without an algorithmic model: report the biggest modelled one
-        modelled = [p for p in phases if phase_work(p, args.batch, args.n_actions, P, esz)]
-        dom = max(modelled, key=lambda p: phases[p])
+        modelled = [p for p in iso_ms if phase_work(p, args.batch, args.n_actions, P, esz)]
+        dom = max(modelled, key=lambda p: iso_ms[p])
         dom_roof = roof(dom)
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
@@ -386,7 +387,9 @@ def main():
             "roofline": {"kernel": dom, "bound": dom_roof["bound"], "achieved": dom_roof["achieved"],
                          "peak": dom_roof["peak"], "unit": dom_roof["unit"], "frac": dom_roof["frac"],
                          "traffic": traffic, "peak_src": peaks["src"],
-                         "share_of_step": phases[dom] / total_prof if total_prof else None,
+                         "share_of_step": iso_ms[dom] / (ms / args.steps),
+                         "timing": "kernel re-launched back to back on its stream (CUDA events, warm L2, PDL), "
+                                   "gorila_bench_phase; share = that time / device ms per step",
                          "ms_per_launch": dom_roof["ms_per_launch"],
                          "algorithmic_per_launch": dom_roof["algorithmic_per_launch"]},
             "phases_ms_per_step": {p: v for p, v in per_launch_ms.items() if v > 0},
