@@ -171,7 +171,7 @@ def cpu_baseline(args, budget_s):
                       f"{cap}-frame replay (per-update work does not depend on replay size), {el:.1f} s"}
 
 
-def run_reference(args):
+def run_reference(args, json_out):
     world, rank, _ = dist_env()
     if rank != 0:
         return
@@ -205,7 +205,8 @@ def run_reference(args):
                       "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
                       "config": config_dict(args, world),
                       "cpu_baseline": {"value": val, "unit": UNIT, "cores": cores, "kind": "oracle", "sample": sample},
-                      "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}))
+                      "e2e": {"value": val, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}),
+          file=json_out, flush=True)
 
 
 def config_dict(args, world):
@@ -218,6 +219,9 @@ def config_dict(args, world):
 
 
 def main():
+    # the contract's stdout is ONE JSON line: everything else (NCCL banners, warnings) goes to stderr
+    json_out = os.fdopen(os.dup(1), "w")
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=3000)
@@ -235,7 +239,7 @@ def main():
     args.warmup = max(args.warmup, 3)
 
     if args.impl == "reference":
-        return run_reference(args)
+        return run_reference(args, json_out)
 
     import torch
     world, rank, local_rank = dist_env()
@@ -398,7 +402,7 @@ def main():
         }
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(args, args.cpu_seconds)
-        print(json.dumps(out))
+        print(json.dumps(out), file=json_out, flush=True)
     g.close()
     if world > 1:
         import torch.distributed as dist
