@@ -231,6 +231,8 @@ GORILA_API const char* gorila_profile_phase_name(int32_t i);
  * parity-checked sequence. Synchronises the stream. */
 GORILA_API gorila_status gorila_bench_phase(gorila_ctx* ctx, int32_t learner, int32_t phase, int32_t iters,
                                             double* us_per_iter);
+/* Diagnostics build only (-DGORILA_TRACE): clock64 timeline of CTA (0,0,0) of the last GEMM. */
+GORILA_API gorila_status gorila_debug_trace(uint64_t* out64);
 /* Writes a fresh 128-byte ncclUniqueId (rank 0 calls it and broadcasts the bytes). */
 GORILA_API gorila_status gorila_nccl_unique_id(void* out128);
 /* Number of kernels this library launched so far (evidence counter). */

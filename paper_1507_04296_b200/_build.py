@@ -29,19 +29,22 @@ def stale():
     return any(os.path.getmtime(s) > t for s in sources())
 
 
-def build(force=False, verbose=False):
-    if not force and not stale():
+def build(force=False, verbose=False, trace=False):
+    so = SO.replace("libgorila.so", "libgorila_trace.so") if trace else SO
+    if not force and not trace and not stale():
         return SO
     nd = nccl_dir()
     cmd = ["nvcc", "-O3", "-std=c++17", "-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo",
            "-shared", "-Xcompiler", "-fPIC,-fvisibility=hidden", "-I" + os.path.join(nd, "include"),
-           os.path.join(CSRC, "gorila.cu"), "-o", SO + ".tmp",
+           os.path.join(CSRC, "gorila.cu"), "-o", so + ".tmp",
            "-L" + os.path.join(nd, "lib"), "-l:libnccl.so.2", "-Xlinker", "-rpath=" + os.path.join(nd, "lib")]
     if verbose:
         cmd.insert(1, "-Xptxas=-v")
+    if trace:
+        cmd.insert(1, "-DGORILA_TRACE")
     subprocess.check_call(cmd)
-    os.replace(SO + ".tmp", SO)
-    return SO
+    os.replace(so + ".tmp", so)
+    return so
 
 
 if __name__ == "__main__":

@@ -107,6 +107,23 @@ GORILA_DEV void tmem_ld16(uint32_t taddr, float* v) {
     for (int i = 0; i < 16; ++i) v[i] = __uint_as_float(r[i]);
 }
 
+// ---- optional per-CTA timeline instrumentation (diagnostics build only: -DGORILA_TRACE)
+#ifdef GORILA_TRACE
+__device__ unsigned long long gorila_trace_buf[64];
+#define GTRACE(slot)                                                                              \
+    do {                                                                                          \
+        if (blockIdx.x == 0 && blockIdx.y == 0 && blockIdx.z == 0 && threadIdx.x == 0) {         \
+            unsigned long long t_;                                                               \
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_));                                  \
+            gorila_trace_buf[(slot)] = t_;                                                       \
+        }                                                                                         \
+    } while (0)
+#else
+#define GTRACE(slot) \
+    do {             \
+    } while (0)
+#endif
+
 // ---- cp.async (LDGSTS): 16-byte global -> shared copies; src_bytes = 0 zero-fills the destination
 GORILA_DEV void cp_async16(uint32_t dst, const void* src, uint32_t src_bytes) {
     asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(dst), "l"(src), "r"(src_bytes) : "memory");

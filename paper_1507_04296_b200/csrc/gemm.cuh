@@ -355,8 +355,11 @@ __host__ __device__ constexpr uint32_t tmem_cols_for(int bn) {
 __host__ __device__ constexpr int tc_red_bytes(int bn) { return (bn / 16) * TC_BM * 80; }
 __host__ __device__ constexpr int tc_stages(int bn) { return bn <= 64 ? 4 : bn <= 128 ? 3 : 2; }
 __host__ __device__ constexpr int tc_stage_bytes(int bn) { return tc_stages(bn) * (TC_BM * TC_BK * 2 + bn * TC_BK * 2); }
+__host__ __device__ constexpr int tc_slice_bytes(int bn) { return 64 * (bn + 4) * 4; }
 __host__ __device__ constexpr int tc_smem_bytes(int bn) {
-    return (tc_stage_bytes(bn) > tc_red_bytes(bn) ? tc_stage_bytes(bn) : tc_red_bytes(bn)) + 64;
+    return (tc_stage_bytes(bn) > tc_red_bytes(bn) + tc_slice_bytes(bn) ? tc_stage_bytes(bn)
+                                                                        : tc_red_bytes(bn) + tc_slice_bytes(bn)) +
+           64;
 }
 
 // Stage one operand tile (ROWS x 64 reduction elements, bf16) in the canonical layout.
@@ -421,6 +424,7 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + STAGES);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    GTRACE(0);
     const int prob = blockIdx.z / p.splits, split = blockIdx.z - prob * p.splits;
     const GemmProb<LA, LB, EP>& P = p.prob[prob];
     const int i0 = blockIdx.x * TC_BM, j0 = blockIdx.y * BN;
@@ -429,6 +433,7 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
     const int nK = max(0, min(n_chunks_total, kc_begin + p.chunks_per_split) - kc_begin);
 
     if (warp == 0) tmem_alloc(tmem_slot, tmem_cols_for(BN));
+    GTRACE(1);
     if (tid == 0) {
         for (int st = 0; st < STAGES; ++st) mbar_init(&mbar[st], 1);
         fence_mbar_init();
@@ -436,8 +441,10 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    GTRACE(2);
     pdl_wait();     // operands come from the preceding kernel(s)
     pdl_trigger();  // the next kernel may start its prologue
+    GTRACE(3);
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t IDESC =
         umma_idesc_bf16(TC_BM, BN) | (LA::kMN ? (1u << 15) : 0u) | (LB::kMN ? (1u << 16) : 0u);
@@ -454,6 +461,7 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
         if (kc < nK) issue(kc);
         cp_async_commit();
     }
+    GTRACE(4);
 #pragma unroll 1
     for (int kc = 0; kc < nK; ++kc) {
         const int nxt = kc + STAGES - 1;
@@ -464,8 +472,10 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
         }
         cp_async_commit();
         cp_async_wait<STAGES - 1>();  // this thread's copies of chunk kc have landed
+        GTRACE(8 + 2 * (kc & 7));
         fence_proxy_async_smem();     // ... and are visible to the tensor core
         __syncthreads();
+        GTRACE(9 + 2 * (kc & 7));
         if (tid == 0) {
             tc_fence_after();
             const int st = kc % STAGES;
@@ -479,8 +489,10 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
     cp_async_wait<0>();
     // the last MMAs are done when the commits of the final chunks arrive (drain the most recent
     // pending completion of every stage so no arrive is in flight at exit)
+    GTRACE(5);
     for (int c = max(0, nK - STAGES); c < nK; ++c) mbar_wait(&mbar[c % STAGES], (c / STAGES) & 1);
     tc_fence_after();
+    GTRACE(6);
 
     // epilogue: warp w owns TMEM lanes (= tile rows) 32w .. 32w+31
     const int lrow = warp * 32 + lane, row = i0 + lrow;
@@ -502,23 +514,36 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
             for (int e = 0; e < 4; ++e) dst[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
         }
         cluster_sync();
+        // CTA q reduces rows [q*rows_per, (q+1)*rows_per): every thread owns float4 items of that
+        // slice and issues the CL peer reads at once (in flight together), sums them in rank order
+        // and parks the result in a private smem area; then the epilogue runs on the slice.
         const int CL = p.cluster, rows_per = TC_BM / CL;
         const int q = (int)cluster_ctarank();
-        for (int item = tid; item < rows_per * (BN / 16); item += TC_THREADS) {
-            const int r_loc = q * rows_per + item % rows_per, c0 = (item / rows_per) * 16;
-            const uint32_t a = smem_u32(red + ((c0 / 16) * TC_BM + r_loc) * 20);
-            float v[16] = {};
-            for (int pr = 0; pr < CL; ++pr) {
-                const uint32_t pa = dsmem_map(a, (uint32_t)pr);
-                float4 x[4];
+        float* slice = reinterpret_cast<float*>(smem + tc_red_bytes(BN));  // [rows_per][BN + 4]
+        const int n4 = rows_per * BN / 4;
+        for (int it = tid; it < n4; it += TC_THREADS) {
+            const int r_loc = it / (BN / 4), c4 = (it % (BN / 4)) * 4;
+            const int r_glob = q * rows_per + r_loc;
+            const uint32_t a = smem_u32(red + ((c4 / 16) * TC_BM + r_glob) * 20 + (c4 % 16));
+            float4 x[16];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) x[e] = dsmem_ld4(pa + 16 * e);
+            for (int pr = 0; pr < 16; ++pr)
+                if (pr < CL) x[pr] = dsmem_ld4(dsmem_map(a, (uint32_t)pr));
+            float4 acc = x[0];
 #pragma unroll
-                for (int e = 0; e < 4; ++e) {
-                    v[4 * e] += x[e].x; v[4 * e + 1] += x[e].y; v[4 * e + 2] += x[e].z; v[4 * e + 3] += x[e].w;
+            for (int pr = 1; pr < 16; ++pr)
+                if (pr < CL) {
+                    acc.x += x[pr].x; acc.y += x[pr].y; acc.z += x[pr].z; acc.w += x[pr].w;
                 }
-            }
-            if (j0 + c0 < p.N) P.ep.apply16(i0 + r_loc, j0 + c0, v, 0);
+            *reinterpret_cast<float4*>(slice + r_loc * (BN + 4) + c4) = acc;
+        }
+        __syncthreads();
+        for (int item = tid; item < rows_per * (BN / 16); item += TC_THREADS) {
+            const int r_loc = item % rows_per, c0 = (item / rows_per) * 16;
+            float v[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) v[e] = slice[r_loc * (BN + 4) + c0 + e];
+            if (j0 + c0 < p.N) P.ep.apply16(i0 + q * rows_per + r_loc, j0 + c0, v, 0);
         }
         cluster_sync();  // peers keep their smem alive until everyone has read it
     } else {
@@ -534,9 +559,11 @@ __global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ Ge
             if (j0 + c0 < p.N) P.ep.apply16(row, j0 + c0, v, split);
         }
     }
+    GTRACE(7);
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, tmem_cols_for(BN));
+    GTRACE(30);
 }
 
 // ====================================================================== fp32 SIMT engine

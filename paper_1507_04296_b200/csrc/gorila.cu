@@ -736,6 +736,17 @@ gorila_status gorila_bench_phase(gorila_ctx* ctx, int32_t learner, int32_t phase
     return s;
 }
 
+gorila_status gorila_debug_trace(uint64_t* out64) {
+#ifdef GORILA_TRACE
+    cudaMemcpyFromSymbol(out64, gorila_trace_buf, sizeof(unsigned long long) * 64);
+    cudaMemset(nullptr, 0, 0);
+    return GORILA_OK;
+#else
+    (void)out64;
+    return fail(GORILA_E_INVALID, "built without GORILA_TRACE");
+#endif
+}
+
 gorila_status gorila_nccl_unique_id(void* out128) {
     if (!out128) return fail(GORILA_E_INVALID, "null argument");
     ncclUniqueId id;

@@ -62,7 +62,7 @@ EXPORTS = ["gorila_param_count", "gorila_workspace_bytes", "gorila_init", "goril
            "gorila_set_state", "gorila_get_learner_state", "gorila_set_learner_state", "gorila_get_grad",
            "gorila_get_q", "gorila_kernel_launches", "gorila_profile_enable", "gorila_profile_read",
            "gorila_profile_phase_count", "gorila_profile_phase_name", "gorila_nccl_unique_id", "gorila_round",
-           "gorila_bench_phase"]
+           "gorila_bench_phase", "gorila_debug_trace"]
 
 
 def load(build_if_missing=True):
@@ -72,9 +72,10 @@ def load(build_if_missing=True):
         return _lib
     if build_if_missing and _build.stale():
         _build.build()
-    if not os.path.exists(_build.SO):
-        raise RuntimeError(f"libgorila.so missing at {_build.SO}: run __graft_entry__.build()")
-    L = ctypes.CDLL(_build.SO)
+    so = os.environ.get("GORILA_LIB", _build.SO)  # diagnostics builds (e.g. libgorila_trace.so)
+    if not os.path.exists(so):
+        raise RuntimeError(f"libgorila.so missing at {so}: run __graft_entry__.build()")
+    L = ctypes.CDLL(so)
     P, i32, i64, u64 = ctypes.c_void_p, ctypes.c_int32, ctypes.c_int64, ctypes.c_uint64
     L.gorila_param_count.argtypes = [i32]
     L.gorila_param_count.restype = i64
@@ -104,6 +105,7 @@ def load(build_if_missing=True):
     L.gorila_nccl_unique_id.argtypes = [P]
     L.gorila_round.argtypes = [P, P, i32, u64, P, P, P, P]
     L.gorila_bench_phase.argtypes = [P, i32, i32, i32, P]
+    L.gorila_debug_trace.argtypes = [P]
     _lib = L
     return L
 
