@@ -17,11 +17,14 @@
 #include <type_traits>
 #include <vector>
 
+#include <cudaTypedefs.h>
+
 #include "../../include/gorila.h"
 #include "common.cuh"
 #include "gemm.cuh"
 #include "kernels.cuh"
 #include "layout.cuh"
+#include "tma_gemm.cuh"
 
 using namespace gorila;
 
@@ -145,6 +148,8 @@ struct gorila_ctx {
     std::map<std::vector<int64_t>, uint64_t> graph_kernels;
     std::map<std::vector<int64_t>, int> graph_seen;
     std::map<std::vector<int64_t>, std::vector<std::pair<int, cudaEvent_t>>> graph_marks;  // profiling graphs
+    std::map<std::vector<uint64_t>, CUtensorMap> tmaps;  // TMA descriptors, encoded once per (buffer, view)
+    bool tma_failed = false;
 };
 
 namespace {
@@ -202,6 +207,188 @@ void launch(gorila_ctx* ctx, void (*kern)(KP...), dim3 grid, dim3 block, size_t 
     cfg.attrs = at;
     cfg.numAttrs = ctx->pdl ? 1 : 0;
     cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
+    ctx->launches++;
+}
+
+// ---------------------------------------------------------------- TMA descriptors
+PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(f);
+    }();
+    return fn;
+}
+
+// bf16 tensor map over `base` with `rank` dims (dims[0] innermost, = 8 elements = 16 B),
+// byte strides of dims 1.., box and element strides. Cached per argument set.
+CUtensorMap tmap(gorila_ctx* ctx, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
+                 const uint32_t* box, const uint32_t* es = nullptr) {
+    std::vector<uint64_t> key{(uint64_t)(uintptr_t)base, (uint64_t)rank};
+    for (int i = 0; i < rank; ++i) key.push_back(dims[i]);
+    for (int i = 0; i < rank - 1; ++i) key.push_back(strides[i]);
+    for (int i = 0; i < rank; ++i) key.push_back(box[i]);
+    for (int i = 0; i < rank; ++i) key.push_back(es ? es[i] : 1);
+    auto it = ctx->tmaps.find(key);
+    if (it != ctx->tmaps.end()) return it->second;
+    CUtensorMap m;
+    memset(&m, 0, sizeof(m));
+    cuuint64_t d[5], st[4];
+    cuuint32_t b[5], e[5];
+    for (int i = 0; i < rank; ++i) {
+        d[i] = dims[i];
+        b[i] = box[i];
+        e[i] = es ? es[i] : 1;
+    }
+    for (int i = 0; i < rank - 1; ++i) st[i] = strides[i];
+    auto enc = tma_encoder();
+    CUresult r = enc ? enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, st, b, e,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)
+                     : CUDA_ERROR_NOT_INITIALIZED;
+    if (r != CUDA_SUCCESS) {
+        ctx->tma_failed = true;
+        g_last_error = "cuTensorMapEncodeTiled failed (" + std::to_string((int)r) + ")";
+    }
+    ctx->tmaps[key] = m;
+    return m;
+}
+
+// K-major [rows][K] matrix (ld elements per row), tile TR rows
+template <int TR>
+OpMatK<TR> op_matk(gorila_ctx* ctx, const void* x, int rows, int K, int64_t ld) {
+    OpMatK<TR> o;
+    const uint64_t dims[3] = {8, (uint64_t)rows, (uint64_t)K / 8}, str[2] = {(uint64_t)ld * 2, 16};
+    const uint32_t box[3] = {8, TR, 8};
+    o.map = tmap(ctx, x, 3, dims, str, box);
+    o.rows = rows;
+    return o;
+}
+// MN-major [Krows][MN] matrix (ld elements per row), tile TR columns
+template <int TR>
+OpMatMN<TR> op_matmn(gorila_ctx* ctx, const void* x, int krows, int mn, int64_t ld) {
+    OpMatMN<TR> o;
+    const uint64_t dims[3] = {8, (uint64_t)krows, (uint64_t)mn / 8}, str[2] = {(uint64_t)ld * 2, 16};
+    const uint32_t box[3] = {8, 64, TR / 8};
+    o.map = tmap(ctx, x, 3, dims, str, box);
+    o.mn = mn;
+    return o;
+}
+// NHWC view (8, W, H, B, G) of an activation, box (8, bw, bh, bb, bc), element strides (1, s, s, 1, 1).
+// The group dimension has stride 16 B; G may exceed C/8 (groups then run into the next pixels of
+// the row: used to cover several adjacent taps with one copy).
+template <class SH>
+CUtensorMap nhwc_map(gorila_ctx* ctx, const void* x, int B, int bw, int bh, int bb, int bc, int s) {
+    const uint64_t C = SH::C;
+    const uint64_t dims[5] = {8, (uint64_t)SH::W, (uint64_t)SH::H, (uint64_t)B, (uint64_t)bc};
+    const uint64_t str[4] = {C * 2, SH::W * C * 2, (uint64_t)SH::H * SH::W * C * 2, 16};
+    const uint32_t box[5] = {8, (uint32_t)bw, (uint32_t)bh, (uint32_t)bb, (uint32_t)bc};
+    const uint32_t es[5] = {1, (uint32_t)s, (uint32_t)s, 1, 1};
+    return tmap(ctx, x, 5, dims, str, box, es);
+}
+// conv1 pixel-pair view of s [B][84][84][4]: (8, 42 pairs, 84 rows, B, 4 pair offsets)
+CUtensorMap conv1_map(gorila_ctx* ctx, const void* s, int B, int bh_rows, int bb) {
+    const uint64_t dims[5] = {8, 42, 84, (uint64_t)B, 4};
+    const uint64_t str[4] = {16, 84 * 8, 84 * 84 * 8, 16};
+    const uint32_t box[5] = {8, 40, (uint32_t)(bh_rows * 4), (uint32_t)bb, 4};
+    const uint32_t es[5] = {1, 2, 4, 1, 1};
+    return tmap(ctx, s, 5, dims, str, box, es);
+}
+// output-gradient view g [B][OH][OW][CO=64]: (8, OW, OH, B, 8), box (8, bw, bh, NB, 8)
+template <class SH>
+CUtensorMap grad_map(gorila_ctx* ctx, const void* g, int B, int bw, int bh, int bb) {
+    const uint64_t dims[5] = {8, (uint64_t)SH::OW, (uint64_t)SH::OH, (uint64_t)B, SH::CO / 8};
+    const uint64_t str[4] = {SH::CO * 2, (uint64_t)SH::OW * SH::CO * 2, (uint64_t)SH::OH * SH::OW * SH::CO * 2, 16};
+    const uint32_t box[5] = {8, (uint32_t)bw, (uint32_t)bh, (uint32_t)bb, SH::CO / 8};
+    return tmap(ctx, g, 5, dims, str, box);
+}
+// conv weight [CO][K][K][C] seen MN-major over c: (8, CO, C/8, K*K)
+template <class SH>
+CUtensorMap wdgrad_map(gorila_ctx* ctx, const void* w) {
+    const uint64_t dims[4] = {8, SH::CO, SH::C / 8, (uint64_t)SH::K * SH::K};
+    const uint64_t str[3] = {(uint64_t)SH::R * 2, 16, SH::C * 2};
+    const uint32_t box[4] = {8, 64, SH::C / 8, 1};
+    return tmap(ctx, w, 4, dims, str, box);
+}
+
+// weight-gradient output-gradient operand: g [B][npix][CO] per-sample chunks of KC rows (zero tail),
+// or flat chunks of KC rows over B*npix (conv1)
+template <int CO, int KC, bool FLAT>
+OpWgradOut<CO, KC, FLAT> op_wgout(gorila_ctx* ctx, const void* g, int npix, int B) {
+    OpWgradOut<CO, KC, FLAT> o;
+    if (FLAT) {
+        const uint64_t dims[3] = {8, (uint64_t)B * npix, CO / 8}, str[2] = {CO * 2, 16};
+        const uint32_t box[3] = {8, KC, CO / 8};
+        o.map = tmap(ctx, g, 3, dims, str, box);
+    } else {
+        const uint64_t dims[4] = {8, (uint64_t)npix, (uint64_t)B, CO / 8};
+        const uint64_t str[3] = {CO * 2, (uint64_t)npix * CO * 2, 16};
+        const uint32_t box[4] = {8, KC, 1, CO / 8};
+        o.map = tmap(ctx, g, 4, dims, str, box);
+    }
+    return o;
+}
+
+// grid + launch of the TMA engine (cluster split-K when cluster_target > 0)
+template <int BN, int MB, class OA, class OB, class EP>
+void gemm_tma_launch(gorila_ctx* ctx, const TmaProb<OA, OB, EP>* probs, int nprob, int tilesA, int tilesB,
+                     int nchunks, int splits, int cluster_target, int N) {
+    using CFG = TmaCfg<BN, MB, OA, OB>;
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(gemm_tma<BN, MB, OA, OB, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, CFG::SMEM);
+        cudaFuncSetAttribute(gemm_tma<BN, MB, OA, OB, EP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+        attr_set = true;
+    }
+    TmaBatch<OA, OB, EP> gb;
+    memset((void*)&gb, 0, sizeof(gb));
+    for (int i = 0; i < nprob; ++i) gb.prob[i] = probs[i];
+    gb.nchunks = nchunks;
+    gb.N = N;
+    splits = std::max(1, std::min(splits, nchunks));
+    gb.chunks_per_split = (nchunks + splits - 1) / splits;
+    gb.splits = (nchunks + gb.chunks_per_split - 1) / gb.chunks_per_split;
+    gb.cluster = 1;
+    static const int cluster_env = [] {
+        const char* e = getenv("GORILA_CLUSTER");
+        return e ? atoi(e) : 1;
+    }();
+    if (MB == 1 && cluster_target > 0 && cluster_env) {
+        const int tiles = tilesA * tilesB * nprob;
+        const int want = std::max(1, (cluster_target + tiles - 1) / tiles);
+        int cl = 1;
+        while (cl * 2 <= std::min(16, std::min(want, nchunks))) cl *= 2;
+        if (cl > 1) {
+            gb.cluster = cl;
+            gb.splits = cl;
+            gb.chunks_per_split = (nchunks + cl - 1) / cl;
+        }
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(tilesA, tilesB, nprob * gb.splits);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = CFG::SMEM;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[2];
+    int na = 0;
+    if (gb.cluster > 1) {
+        at[na].id = cudaLaunchAttributeClusterDimension;
+        at[na].val.clusterDim.x = 1;
+        at[na].val.clusterDim.y = 1;
+        at[na].val.clusterDim.z = gb.cluster;
+        ++na;
+    }
+    if (ctx->pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, gemm_tma<BN, MB, OA, OB, EP>, gb);
     ctx->launches++;
 }
 
@@ -332,6 +519,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     Learner& Lr = ctx->learners[j];
     const int B = ctx->B, nA = ctx->nA;
     const bool fp32 = std::is_same<T, float>::value;
+    constexpr bool fp32v = std::is_same<T, float>::value;
     const uint64_t k_src = round >= (uint64_t)s_j ? round - (uint64_t)s_j : 0;
     const int slot = (int)(k_src % (uint64_t)ctx->H);
     const T* rt = P_<T>(ctx->rep_t[slot]);
@@ -363,36 +551,75 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     PHASE(PH_CONV1F) {
     // conv1 fwd (online on s with theta, target on s' with theta^-)
     {
-        using LA = LdConvIn<T, Conv1>; using LB = LdRows<T>; using EP = EpAct<T>;
         const int M = B * H1 * H1;
-        GemmProb<LA, LB, EP> pr[2] = {
-            {{s, M}, {rt + RL.w1, K1, C1_OUT, K1}, {a1, C1_OUT, rf + RL.b1, in_scale, M, C1_OUT, 1}},
-            {{s2, M}, {tt + RT.w1, K1, C1_OUT, K1}, {t1, C1_OUT, tf + RT.b1, in_scale, M, C1_OUT, 1}}};
-        gemm<T, 32>(ctx, pr, 2, M, C1_OUT, K1, 1);
+        if constexpr (fp32v) {
+            using LA = LdConvIn<T, Conv1>; using LB = LdRows<T>; using EP = EpAct<T>;
+            GemmProb<LA, LB, EP> pr[2] = {
+                {{s, M}, {rt + RL.w1, K1, C1_OUT, K1}, {a1, C1_OUT, rf + RL.b1, in_scale, M, C1_OUT, 1}},
+                {{s2, M}, {tt + RT.w1, K1, C1_OUT, K1}, {t1, C1_OUT, tf + RT.b1, in_scale, M, C1_OUT, 1}}};
+            gemm<T, 32>(ctx, pr, 2, M, C1_OUT, K1, 1);
+        } else {  // TMA: one sample (400 rows = 4 M-blocks) per tile, pixel-pair im2col boxes
+            using OA = OpConv1Fwd<4>; using OB = OpMatK<32>; using EP = EpAct<T>;
+            TmaProb<OA, OB, EP> pr[2];
+            for (int z = 0; z < 2; ++z) {
+                pr[z].a.map = conv1_map(ctx, z ? (const void*)s2 : (const void*)s, B, H1, 1);
+                pr[z].a.nb = 1;
+                pr[z].a.batch = B;
+                pr[z].b = op_matk<32>(ctx, z ? (const void*)(tt + RT.w1) : (const void*)(rt + RL.w1), C1_OUT, K1, K1);
+                pr[z].ep = {z ? t1 : a1, C1_OUT, z ? tf + RT.b1 : rf + RL.b1, in_scale, M, C1_OUT, 1};
+            }
+            gemm_tma_launch<32, 4>(ctx, pr, 2, B, 1, K1 / 64, 1, 0, C1_OUT);
+        }
     }
     }
     mark(ctx, PH_CONV1F);
     PHASE(PH_CONV2F) {
     // conv2 fwd
     {
-        using LA = LdConvIn<T, Conv2>; using LB = LdRows<T>; using EP = EpAct<T>;
         const int M = B * H2 * H2;
-        GemmProb<LA, LB, EP> pr[2] = {
-            {{a1, M}, {rt + RL.w2, K2, C2_OUT, K2}, {a2, C2_OUT, rf + RL.b2, 1.f, M, C2_OUT, 1}},
-            {{t1, M}, {tt + RT.w2, K2, C2_OUT, K2}, {t2, C2_OUT, tf + RT.b2, 1.f, M, C2_OUT, 1}}};
-        gemm<T, 64>(ctx, pr, 2, M, C2_OUT, K2, 1, 148);
+        if constexpr (fp32v) {
+            using LA = LdConvIn<T, Conv2>; using LB = LdRows<T>; using EP = EpAct<T>;
+            GemmProb<LA, LB, EP> pr[2] = {
+                {{a1, M}, {rt + RL.w2, K2, C2_OUT, K2}, {a2, C2_OUT, rf + RL.b2, 1.f, M, C2_OUT, 1}},
+                {{t1, M}, {tt + RT.w2, K2, C2_OUT, K2}, {t2, C2_OUT, tf + RT.b2, 1.f, M, C2_OUT, 1}}};
+            gemm<T, 64>(ctx, pr, 2, M, C2_OUT, K2, 1, 148);
+        } else {  // TMA: one sample (81 rows) per tile, stride-2 boxes; in-cluster split of K = 512
+            using OA = OpConvFwd<Conv2, 1>; using OB = OpMatK<64>; using EP = EpAct<T>;
+            TmaProb<OA, OB, EP> pr[2];
+            for (int z = 0; z < 2; ++z) {
+                pr[z].a.map = nhwc_map<Conv2>(ctx, z ? (const void*)t1 : (const void*)a1, B, 2 * H2, 2 * H2, 1, 8, 2);
+                pr[z].a.nb = 1;
+                pr[z].a.batch = B;
+                pr[z].b = op_matk<64>(ctx, z ? (const void*)(tt + RT.w2) : (const void*)(rt + RL.w2), C2_OUT, K2, K2);
+                pr[z].ep = {z ? t2 : a2, C2_OUT, z ? tf + RT.b2 : rf + RL.b2, 1.f, M, C2_OUT, 1};
+            }
+            gemm_tma_launch<64, 1>(ctx, pr, 2, B, 1, K2 / 64, 1, 256, C2_OUT);
+        }
     }
     }
     mark(ctx, PH_CONV2F);
     PHASE(PH_CONV3F) {
     // conv3 fwd
     {
-        using LA = LdConvIn<T, Conv3>; using LB = LdRows<T>; using EP = EpAct<T>;
         const int M = B * H3 * H3;
-        GemmProb<LA, LB, EP> pr[2] = {
-            {{a2, M}, {rt + RL.w3, K3, C3_OUT, K3}, {a3, C3_OUT, rf + RL.b3, 1.f, M, C3_OUT, 1}},
-            {{t2, M}, {tt + RT.w3, K3, C3_OUT, K3}, {t3, C3_OUT, tf + RT.b3, 1.f, M, C3_OUT, 1}}};
-        gemm<T, 64>(ctx, pr, 2, M, C3_OUT, K3, 1, 148);
+        if constexpr (fp32v) {
+            using LA = LdConvIn<T, Conv3>; using LB = LdRows<T>; using EP = EpAct<T>;
+            GemmProb<LA, LB, EP> pr[2] = {
+                {{a2, M}, {rt + RL.w3, K3, C3_OUT, K3}, {a3, C3_OUT, rf + RL.b3, 1.f, M, C3_OUT, 1}},
+                {{t2, M}, {tt + RT.w3, K3, C3_OUT, K3}, {t3, C3_OUT, tf + RT.b3, 1.f, M, C3_OUT, 1}}};
+            gemm<T, 64>(ctx, pr, 2, M, C3_OUT, K3, 1, 148);
+        } else {  // TMA: two samples (98 rows) per tile, one tap per K-chunk
+            using OA = OpConvFwd<Conv3, 1>; using OB = OpMatK<64>; using EP = EpAct<T>;
+            TmaProb<OA, OB, EP> pr[2];
+            for (int z = 0; z < 2; ++z) {
+                pr[z].a.map = nhwc_map<Conv3>(ctx, z ? (const void*)t2 : (const void*)a2, B, H3, H3, 2, 8, 1);
+                pr[z].a.nb = 2;
+                pr[z].a.batch = B;
+                pr[z].b = op_matk<64>(ctx, z ? (const void*)(tt + RT.w3) : (const void*)(rt + RL.w3), C3_OUT, K3, K3);
+                pr[z].ep = {z ? t3 : a3, C3_OUT, z ? tf + RT.b3 : rf + RL.b3, 1.f, M, C3_OUT, 1};
+            }
+            gemm_tma_launch<64, 1>(ctx, pr, 2, (B + 1) / 2, 1, K3 / 64, 1, 148, C3_OUT);
+        }
     }
     }
     mark(ctx, PH_CONV3F);
@@ -400,13 +627,28 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     // fc4 fwd, swap-AB (i = n, j = b): a4[b][n] = ReLU(W4[n] . a3[b] + b4[n]) in fp32, the split of
     // K = 3136 reduced inside the cluster (no partial buffers, no finalize kernel)
     {
-        using LA = LdRows<T>; using LB = LdRows<T>; using EP = EpActT;
-        GemmProb<LA, LB, EP> pr[2] = {
-            {{rt + RL.w4, FC4_IN, FC4_OUT, FC4_IN}, {a3, FC4_IN, B, FC4_IN}, {a4, FC4_OUT, rf + RL.b4, FC4_OUT, B}},
-            {{tt + RT.w4, FC4_IN, FC4_OUT, FC4_IN}, {t3, FC4_IN, B, FC4_IN}, {t4, FC4_OUT, tf + RT.b4, FC4_OUT, B}}};
-#define FC4F(BN_) gemm<T, BN_>(ctx, pr, 2, FC4_OUT, B, FC4_IN, 1, 148)
-        DISPATCH_BN_BATCH(B, FC4F);
+        if constexpr (fp32v) {
+            using LA = LdRows<T>; using LB = LdRows<T>; using EP = EpActT;
+            GemmProb<LA, LB, EP> pr[2] = {
+                {{rt + RL.w4, FC4_IN, FC4_OUT, FC4_IN}, {a3, FC4_IN, B, FC4_IN}, {a4, FC4_OUT, rf + RL.b4, FC4_OUT, B}},
+                {{tt + RT.w4, FC4_IN, FC4_OUT, FC4_IN}, {t3, FC4_IN, B, FC4_IN}, {t4, FC4_OUT, tf + RT.b4, FC4_OUT, B}}};
+            gemm<T, 32>(ctx, pr, 2, FC4_OUT, B, FC4_IN, 1, 148);
+        } else {
+#define FC4F(BN_)                                                                                              \
+    {                                                                                                          \
+        using OA = OpMatK<128>; using OB = OpMatK<BN_>; using EP = EpActT;                                     \
+        TmaProb<OA, OB, EP> pr[2];                                                                             \
+        for (int z = 0; z < 2; ++z) {                                                                          \
+            pr[z].a = op_matk<128>(ctx, z ? (const void*)(tt + RT.w4) : (const void*)(rt + RL.w4), FC4_OUT,    \
+                                   FC4_IN, FC4_IN);                                                            \
+            pr[z].b = op_matk<BN_>(ctx, z ? (const void*)t3 : (const void*)a3, B, FC4_IN, FC4_IN);             \
+            pr[z].ep = {z ? t4 : a4, FC4_OUT, z ? tf + RT.b4 : rf + RL.b4, FC4_OUT, B};                        \
+        }                                                                                                      \
+        gemm_tma_launch<BN_, 1>(ctx, pr, 2, FC4_OUT / 128, (B + BN_ - 1) / BN_, FC4_IN / 64, 1, 148, B);      \
+    }
+            DISPATCH_BN_BATCH(B, FC4F);
 #undef FC4F
+        }
     }
     }
     mark(ctx, PH_FC4F);
@@ -436,77 +678,151 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     PHASE(PH_FC4DG) {
     // fc4 dgrad (i = k, j = b, red = n): g3[b][k] = mask(sum_n W4[n][k] g4[b][n])
     {
-        using LA = LdRowsMN<T>; using LB = LdRows<T>; using EP = EpMaskT<T>;
-        GemmProb<LA, LB, EP> pr[1] = {{{rt + RL.w4, FC4_IN, FC4_IN, FC4_OUT}, {g4, FC4_OUT, B, FC4_OUT},
-                                       {g3, a3, FC4_IN, FC4_IN, B}}};
-#define FC4D(BN_) gemm<T, BN_>(ctx, pr, 1, FC4_IN, B, FC4_OUT, 1, 148)
-        DISPATCH_BN_BATCH(B, FC4D);
+        if constexpr (fp32v) {
+            using LA = LdRowsMN<T>; using LB = LdRows<T>; using EP = EpMaskT<T>;
+            GemmProb<LA, LB, EP> pr[1] = {{{rt + RL.w4, FC4_IN, FC4_IN, FC4_OUT}, {g4, FC4_OUT, B, FC4_OUT},
+                                           {g3, a3, FC4_IN, FC4_IN, B}}};
+            gemm<T, 32>(ctx, pr, 1, FC4_IN, B, FC4_OUT, 1, 148);
+        } else {
+#define FC4D(BN_)                                                                                              \
+    {                                                                                                          \
+        using OA = OpMatMN<128>; using OB = OpMatK<BN_>; using EP = EpMaskT<T>;                                \
+        TmaProb<OA, OB, EP> pr[1];                                                                             \
+        pr[0].a = op_matmn<128>(ctx, rt + RL.w4, FC4_OUT, FC4_IN, FC4_IN);                                     \
+        pr[0].b = op_matk<BN_>(ctx, g4, B, FC4_OUT, FC4_OUT);                                                  \
+        pr[0].ep = {g3, a3, FC4_IN, FC4_IN, B};                                                                \
+        gemm_tma_launch<BN_, 1>(ctx, pr, 1, (FC4_IN + 127) / 128, (B + BN_ - 1) / BN_, FC4_OUT / 64, 1, 148, B); \
+    }
+            DISPATCH_BN_BATCH(B, FC4D);
 #undef FC4D
+        }
     }
     }
     mark(ctx, PH_FC4DG);
     PHASE(PH_FC4WG) {
     // fc4 wgrad (i = k, j = n, red = b): G[W4][n][k] += sum_b a3[b][k] g4[b][n]
     {
-        using LA = LdRowsMN<T>; using LB = LdRowsMN<T>; using EP = EpAddT;
-        GemmProb<LA, LB, EP> pr[1] = {{{a3, FC4_IN, FC4_IN, B}, {g4, FC4_OUT, FC4_OUT, B},
-                                       {ctx->G + OFF_W4, FC4_IN, FC4_IN, FC4_OUT, accumulate}}};
-        gemm<T, 64>(ctx, pr, 1, FC4_IN, FC4_OUT, B, 1);
+        if constexpr (fp32v) {
+            using LA = LdRowsMN<T>; using LB = LdRowsMN<T>; using EP = EpAddT;
+            GemmProb<LA, LB, EP> pr[1] = {{{a3, FC4_IN, FC4_IN, B}, {g4, FC4_OUT, FC4_OUT, B},
+                                           {ctx->G + OFF_W4, FC4_IN, FC4_IN, FC4_OUT, accumulate}}};
+            gemm<T, 64>(ctx, pr, 1, FC4_IN, FC4_OUT, B, 1);
+        } else {
+            using OA = OpMatMN<128>; using OB = OpMatMN<64>; using EP = EpAddT;
+            TmaProb<OA, OB, EP> pr[1];
+            pr[0].a = op_matmn<128>(ctx, a3, B, FC4_IN, FC4_IN);
+            pr[0].b = op_matmn<64>(ctx, g4, B, FC4_OUT, FC4_OUT);
+            pr[0].ep = {ctx->G + OFF_W4, FC4_IN, FC4_IN, FC4_OUT, accumulate};
+            gemm_tma_launch<64, 1>(ctx, pr, 1, (FC4_IN + 127) / 128, FC4_OUT / 64, (B + 63) / 64, 1, 0, FC4_OUT);
+        }
     }
     }
     mark(ctx, PH_FC4WG);
     PHASE(PH_CONV3DG) {
     // conv3 dgrad: g2 = mask(conv3^T(g3))
     {
-        using LA = LdDgrad<T, Conv3>; using LB = LdWdgradMN<T, Conv3>; using EP = EpMask<T>;
         const int M = B * H2 * H2;
-        GemmProb<LA, LB, EP> pr[1] = {{{g3, M}, {rt + RL.w3},
-                                       {g2, a2, C2_OUT, M, C2_OUT}}};
-        gemm<T, 64>(ctx, pr, 1, M, C2_OUT, K3, 1, 148);
+        if constexpr (fp32v) {
+            using LA = LdDgrad<T, Conv3>; using LB = LdWdgradMN<T, Conv3>; using EP = EpMask<T>;
+            GemmProb<LA, LB, EP> pr[1] = {{{g3, M}, {rt + RL.w3}, {g2, a2, C2_OUT, M, C2_OUT}}};
+            gemm<T, 64>(ctx, pr, 1, M, C2_OUT, K3, 1, 148);
+        } else {  // TMA: one sample (81 input pixels) per tile, shifted boxes with zero fill
+            using OA = OpDgrad<Conv3, 1>; using OB = OpWdgradMN<Conv3>; using EP = EpMask<T>;
+            TmaProb<OA, OB, EP> pr[1];
+            pr[0].a.map = grad_map<Conv3>(ctx, g3, B, H2, H2, 1);
+            pr[0].a.nb = 1;
+            pr[0].a.batch = B;
+            pr[0].a.phase = -1;
+            pr[0].b.map = wdgrad_map<Conv3>(ctx, rt + RL.w3);
+            pr[0].b.phase = -1;
+            pr[0].ep = {g2, a2, C2_OUT, M, C2_OUT};
+            gemm_tma_launch<64, 1>(ctx, pr, 1, B, 1, C3_K * C3_K, 1, 148, C2_OUT);
+        }
     }
     }
     mark(ctx, PH_CONV3DG);
     PHASE(PH_CONV3WG) {
     // conv3 wgrad (i = r, j = o, red = m): partial[s][o][r]
     {
-        using LA = LdConvInMN<T, Conv3>; using LB = LdRowsMN<T>; using EP = EpStoreT;
         const int Mred = B * H3 * H3;
-        GemmProb<LA, LB, EP> pr[1] = {{{a2, Mred}, {g3, C3_OUT, C3_OUT, Mred},
-                                       {ctx->part_w[2], K3, (int64_t)C3_OUT * K3, 1.f, K3, C3_OUT}}};
-        gemm<T, 64>(ctx, pr, 1, K3, C3_OUT, Mred, ctx->split_w[2]);
+        if constexpr (fp32v) {
+            using LA = LdConvInMN<T, Conv3>; using LB = LdRowsMN<T>; using EP = EpStoreT;
+            GemmProb<LA, LB, EP> pr[1] = {{{a2, Mred}, {g3, C3_OUT, C3_OUT, Mred},
+                                           {ctx->part_w[2], K3, (int64_t)C3_OUT * K3, 1.f, K3, C3_OUT}}};
+            gemm<T, 64>(ctx, pr, 1, K3, C3_OUT, Mred, ctx->split_w[2]);
+        } else {  // TMA: K-chunk = one sample's 49 pixels (64 rows, zero tail in the gradient operand)
+            using OA = OpWgradIn<Conv3, 64>; using OB = OpWgradOut<64, 64, false>; using EP = EpStoreT;
+            TmaProb<OA, OB, EP> pr[1];
+            pr[0].a.map = nhwc_map<Conv3>(ctx, a2, B, H3, H3, 1, 8, 1);
+            pr[0].b = op_wgout<64, 64, false>(ctx, g3, H3 * H3, B);
+            pr[0].ep = {ctx->part_w[2], K3, (int64_t)C3_OUT * K3, 1.f, K3, C3_OUT};
+            gemm_tma_launch<64, 1>(ctx, pr, 1, (K3 + 127) / 128, 1, B, ctx->split_w[2], 0, C3_OUT);
+        }
     }
     }
     mark(ctx, PH_CONV3WG);
     PHASE(PH_CONV2DG) {
     // conv2 dgrad: g1 = mask(conv2^T(g2))
     {
-        using LA = LdDgrad<T, Conv2>; using LB = LdWdgradMN<T, Conv2>; using EP = EpMask<T>;
         const int M = B * H1 * H1;
-        GemmProb<LA, LB, EP> pr[1] = {{{g2, M}, {rt + RL.w2},
-                                       {g1, a1, C1_OUT, M, C1_OUT}}};
-        gemm<T, 32>(ctx, pr, 1, M, C1_OUT, Conv2::RD, 1, 296);
+        if constexpr (fp32v) {
+            using LA = LdDgrad<T, Conv2>; using LB = LdWdgradMN<T, Conv2>; using EP = EpMask<T>;
+            GemmProb<LA, LB, EP> pr[1] = {{{g2, M}, {rt + RL.w2}, {g1, a1, C1_OUT, M, C1_OUT}}};
+            gemm<T, 32>(ctx, pr, 1, M, C1_OUT, Conv2::RD, 1, 296);
+        } else {  // TMA: the stride-2 transpose as 4 phase problems of 2x2 taps (no zero taps)
+            using OA = OpDgrad<Conv2, 1>; using OB = OpWdgradMN<Conv2>; using EP = EpMask<T>;
+            TmaProb<OA, OB, EP> pr[4];
+            for (int ph = 0; ph < 4; ++ph) {
+                pr[ph].a.map = grad_map<Conv2>(ctx, g2, B, 10, 10, 1);
+                pr[ph].a.nb = 1;
+                pr[ph].a.batch = B;
+                pr[ph].a.phase = ph;
+                pr[ph].b.map = wdgrad_map<Conv2>(ctx, rt + RL.w2);
+                pr[ph].b.phase = ph;
+                pr[ph].ep = {g1, a1, C1_OUT, M, C1_OUT};
+            }
+            gemm_tma_launch<32, 1>(ctx, pr, 4, B, 1, 4, 1, 256, C1_OUT);
+        }
     }
     }
     mark(ctx, PH_CONV2DG);
     PHASE(PH_CONV2WG) {
     // conv2 wgrad
     {
-        using LA = LdConvInMN<T, Conv2>; using LB = LdRowsMN<T>; using EP = EpStoreT;
         const int Mred = B * H2 * H2;
-        GemmProb<LA, LB, EP> pr[1] = {{{a1, Mred}, {g2, C2_OUT, C2_OUT, Mred},
-                                       {ctx->part_w[1], K2, (int64_t)C2_OUT * K2, 1.f, K2, C2_OUT}}};
-        gemm<T, 64>(ctx, pr, 1, K2, C2_OUT, Mred, ctx->split_w[1]);
+        if constexpr (fp32v) {
+            using LA = LdConvInMN<T, Conv2>; using LB = LdRowsMN<T>; using EP = EpStoreT;
+            GemmProb<LA, LB, EP> pr[1] = {{{a1, Mred}, {g2, C2_OUT, C2_OUT, Mred},
+                                           {ctx->part_w[1], K2, (int64_t)C2_OUT * K2, 1.f, K2, C2_OUT}}};
+            gemm<T, 64>(ctx, pr, 1, K2, C2_OUT, Mred, ctx->split_w[1]);
+        } else {  // TMA: K-chunk = one sample's 81 pixels (96 rows, zero tail)
+            using OA = OpWgradIn<Conv2, 96>; using OB = OpWgradOut<64, 96, false>; using EP = EpStoreT;
+            TmaProb<OA, OB, EP> pr[1];
+            pr[0].a.map = nhwc_map<Conv2>(ctx, a1, B, 2 * H2, 2 * H2, 1, 16, 2);
+            pr[0].b = op_wgout<64, 96, false>(ctx, g2, H2 * H2, B);
+            pr[0].ep = {ctx->part_w[1], K2, (int64_t)C2_OUT * K2, 1.f, K2, C2_OUT};
+            gemm_tma_launch<64, 1>(ctx, pr, 1, K2 / 128, 1, B, ctx->split_w[1], 0, C2_OUT);
+        }
     }
     }
     mark(ctx, PH_CONV2WG);
     PHASE(PH_CONV1WG) {
     // conv1 wgrad (input scale 1/255 folded into the store)
     {
-        using LA = LdConvInMN<T, Conv1>; using LB = LdRowsMN<T>; using EP = EpStoreT;
         const int Mred = B * H1 * H1;
-        GemmProb<LA, LB, EP> pr[1] = {{{s, Mred}, {g1, C1_OUT, C1_OUT, Mred},
-                                       {ctx->part_w[0], K1, (int64_t)C1_OUT * K1, in_scale, K1, C1_OUT}}};
-        gemm<T, 32>(ctx, pr, 1, K1, C1_OUT, Mred, ctx->split_w[0]);
+        if constexpr (fp32v) {
+            using LA = LdConvInMN<T, Conv1>; using LB = LdRowsMN<T>; using EP = EpStoreT;
+            GemmProb<LA, LB, EP> pr[1] = {{{s, Mred}, {g1, C1_OUT, C1_OUT, Mred},
+                                           {ctx->part_w[0], K1, (int64_t)C1_OUT * K1, in_scale, K1, C1_OUT}}};
+            gemm<T, 32>(ctx, pr, 1, K1, C1_OUT, Mred, ctx->split_w[0]);
+        } else {  // TMA: K-chunk = 4 output rows (80 pixels) of one sample
+            using OA = OpWgradIn1; using OB = OpWgradOut<32, 80, true>; using EP = EpStoreT;
+            TmaProb<OA, OB, EP> pr[1];
+            pr[0].a.map = conv1_map(ctx, s, B, 4, 1);
+            pr[0].b = op_wgout<32, 80, true>(ctx, g1, H1 * H1, B);
+            pr[0].ep = {ctx->part_w[0], K1, (int64_t)C1_OUT * K1, in_scale, K1, C1_OUT};
+            gemm_tma_launch<32, 1>(ctx, pr, 1, K1 / 128, 1, B * 5, ctx->split_w[0], 0, C1_OUT);
+        }
     }
     }
     mark(ctx, PH_CONV1WG);
@@ -521,9 +837,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     {
         WgradReduceParams p{};
         p.part[0] = ctx->part_w[0]; p.part[1] = ctx->part_w[1]; p.part[2] = ctx->part_w[2];
-        p.splits[0] = eff_splits(fp32, B * H1 * H1, ctx->split_w[0]);
-        p.splits[1] = eff_splits(fp32, B * H2 * H2, ctx->split_w[1]);
-        p.splits[2] = eff_splits(fp32, B * H3 * H3, ctx->split_w[2]);
+        p.splits[0] = ctx->split_w[0];
+        p.splits[1] = ctx->split_w[1];
+        p.splits[2] = ctx->split_w[2];
         p.count[0] = (int64_t)C1_OUT * K1; p.count[1] = (int64_t)C2_OUT * K2; p.count[2] = (int64_t)C3_OUT * K3;
         p.off[0] = OFF_W1; p.off[1] = OFF_W2; p.off[2] = OFF_W3;
         const int bc[4] = {C1_OUT, C2_OUT, C3_OUT, FC4_OUT};
@@ -630,8 +946,15 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     const int tiles[3] = {fp32 ? 4 * 1 : 2, fp32 ? 8 : 4, fp32 ? 9 : 5};
     float* part_w[3];
     for (int l = 0; l < 3; ++l) {
-        int want = pick_splits((Mred[l] + chunk - 1) / chunk, tiles[l], 148, 128);
-        split_w[l] = eff_splits(fp32, Mred[l], want);
+        if (fp32) {
+            int want = pick_splits((Mred[l] + chunk - 1) / chunk, tiles[l], 148, 128);
+            split_w[l] = eff_splits(fp32, Mred[l], want);
+        } else {  // TMA engine: chunks are 80-pixel rows (conv1) or whole samples (conv2, conv3)
+            const int nch = l == 0 ? 5 * B : B, ta = l == 0 ? 2 : l == 1 ? 4 : 5;
+            const int want = std::max(1, std::min(nch, (148 + ta - 1) / ta));
+            const int cps = (nch + want - 1) / want;
+            split_w[l] = (nch + cps - 1) / cps;
+        }
         part_w[l] = c.take<float>((int64_t)split_w[l] * wcount[l]);
     }
     float* part_b = c.take<float>((int64_t)BIAS_CHUNKS * (C1_OUT + C2_OUT + C3_OUT + FC4_OUT));
