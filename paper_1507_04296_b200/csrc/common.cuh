@@ -137,6 +137,13 @@ GORILA_DEV void cp_async_wait() { asm volatile("cp.async.wait_group %0;" ::"n"(N
 GORILA_DEV void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
 }
+GORILA_DEV void tma_load(const CUtensorMap* map, uint32_t dst, uint64_t* bar, int c0, int c1) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+            dst),
+        "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+        : "memory");
+}
 GORILA_DEV void tma_load(const CUtensorMap* map, uint32_t dst, uint64_t* bar, int c0, int c1, int c2) {
     asm volatile(
         "cp.async.bulk.tensor.3d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3, %4}], [%5];" ::"r"(
@@ -198,6 +205,19 @@ GORILA_DEV uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     d |= (uint64_t)((sbo >> 4) & 0x3FFF) << 32;
     d |= (uint64_t)1 << 46;  // version
     return d;                // base_offset 0, lbo_mode 0, layout_type 0 (SWIZZLE_NONE)
+}
+// K-major swizzled layouts written by TMA with SWIZZLE_128B / SWIZZLE_64B: rows of 128 / 64 B,
+// 8-row atoms (SBO = 1024 / 512 B), K steps of 16 elements advance the start address by 32 B
+// inside the row; layout_type 2 = SWIZZLE_128B, 4 = SWIZZLE_64B (atoms 1024 / 512-B aligned).
+GORILA_DEV uint64_t umma_desc_sw(uint32_t saddr, uint32_t row_bytes) {
+    const uint64_t layout = row_bytes == 128 ? 2ull : 4ull;
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)1 << 16;                            // LBO (unused for swizzled K-major)
+    d |= (uint64_t)(((8 * row_bytes) >> 4) & 0x3FFF) << 32;  // SBO = one 8-row atom
+    d |= (uint64_t)1 << 46;                            // version
+    d |= layout << 61;
+    return d;
 }
 // instruction descriptor: D f32, A/B bf16, both K-major, M x N
 __host__ __device__ constexpr uint32_t umma_idesc_bf16(int M, int N) {

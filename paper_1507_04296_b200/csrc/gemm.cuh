@@ -272,8 +272,14 @@ struct EpStoreT {  // dst[split][j][i] = v * scale (transposed fp32 store: weigh
         if (i < M && j < N) dst[split * split_stride + (int64_t)j * ld + i] = v * scale;
     }
     GORILA_DEV void apply16(int i, int j0, const float* v, int s) const {
+        if (i < M && j0 + 16 <= N) {  // common case: no per-element bounds branches
+            float* d = dst + s * split_stride + (int64_t)j0 * ld + i;
 #pragma unroll
-        for (int e = 0; e < 16; ++e) apply1(i, j0 + e, v[e], s);
+            for (int e = 0; e < 16; ++e) d[(int64_t)e * ld] = v[e] * scale;
+        } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) apply1(i, j0 + e, v[e], s);
+        }
     }
 };
 
@@ -319,12 +325,18 @@ struct EpAddT {  // G[j*ld + i] (+)= v (fp32, transposed, coalesced across the w
     }
     GORILA_DEV void apply16(int i, int j0, const float* v, int) const {
         if (i >= M) return;
+        float* d = G + (int64_t)j0 * ld + i;
+        if (j0 + 16 <= N && !accumulate) {  // first learner of the round: plain stores
+#pragma unroll
+            for (int e = 0; e < 16; ++e) d[(int64_t)e * ld] = v[e];
+            return;
+        }
         float o[16];  // all loads before any store
 #pragma unroll
-        for (int e = 0; e < 16; ++e) o[e] = (accumulate && j0 + e < N) ? G[(int64_t)(j0 + e) * ld + i] : 0.f;
+        for (int e = 0; e < 16; ++e) o[e] = (accumulate && j0 + e < N) ? d[(int64_t)e * ld] : 0.f;
 #pragma unroll
         for (int e = 0; e < 16; ++e)
-            if (j0 + e < N) G[(int64_t)(j0 + e) * ld + i] = o[e] + v[e];
+            if (j0 + e < N) d[(int64_t)e * ld] = o[e] + v[e];
     }
 };
 

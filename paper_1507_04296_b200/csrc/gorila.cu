@@ -122,6 +122,8 @@ struct gorila_ctx {
     float* sr;
     int64_t* sidx;
     float* dQ;
+    float* td_partial;  // [B][2] per-sample delta^2, |delta|
+    int bias_chunks;
     float* part_w[3];  // conv wgrad partials
     float* part_b;     // bias-gradient partials [4 layers][BIAS_CHUNKS][C]
     int split_w[3];
@@ -150,6 +152,11 @@ struct gorila_ctx {
     std::map<std::vector<int64_t>, std::vector<std::pair<int, cudaEvent_t>>> graph_marks;  // profiling graphs
     std::map<std::vector<uint64_t>, CUtensorMap> tmaps;  // TMA descriptors, encoded once per (buffer, view)
     bool tma_failed = false;
+    // side stream for the weight-gradient GEMMs, which are off the dgrad critical path
+    // (a fork / join of the round; a graph captures it as parallel branches)
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_fork[4] = {}, ev_join = nullptr;
+    bool fork = true;
 };
 
 namespace {
@@ -179,6 +186,26 @@ void mark(gorila_ctx* ctx, int ph) {
     ctx->marks.push_back({ph, ctx->ev_used});
     ctx->ev_used++;
 }
+
+// fork: the side stream waits for everything issued so far on the main stream
+void fork_side(gorila_ctx* ctx, int i) {
+    cudaEventRecord(ctx->ev_fork[i], ctx->stream);
+    cudaStreamWaitEvent(ctx->side, ctx->ev_fork[i], 0);
+}
+// join: the main stream waits for the side stream
+void join_side(gorila_ctx* ctx) {
+    cudaEventRecord(ctx->ev_join, ctx->side);
+    cudaStreamWaitEvent(ctx->stream, ctx->ev_join, 0);
+}
+// launches issued inside this scope go to the side stream (if `on`)
+struct OnSide {
+    gorila_ctx* c;
+    cudaStream_t saved;
+    OnSide(gorila_ctx* c_, bool on) : c(c_), saved(c_->stream) {
+        if (on) c->stream = c->side;
+    }
+    ~OnSide() { c->stream = saved; }
+};
 
 // fold recorded marks into the per-phase accumulators (events must be complete)
 cudaError_t fold_marks(gorila_ctx* ctx, const std::vector<std::pair<int, cudaEvent_t>>& m) {
@@ -226,8 +253,8 @@ PFN_cuTensorMapEncodeTiled_v12000 tma_encoder() {
 // bf16 tensor map over `base` with `rank` dims (dims[0] innermost, = 8 elements = 16 B),
 // byte strides of dims 1.., box and element strides. Cached per argument set.
 CUtensorMap tmap(gorila_ctx* ctx, const void* base, int rank, const uint64_t* dims, const uint64_t* strides,
-                 const uint32_t* box, const uint32_t* es = nullptr) {
-    std::vector<uint64_t> key{(uint64_t)(uintptr_t)base, (uint64_t)rank};
+                 const uint32_t* box, const uint32_t* es = nullptr, int swizzle = 0) {
+    std::vector<uint64_t> key{(uint64_t)(uintptr_t)base, (uint64_t)rank, (uint64_t)swizzle};
     for (int i = 0; i < rank; ++i) key.push_back(dims[i]);
     for (int i = 0; i < rank - 1; ++i) key.push_back(strides[i]);
     for (int i = 0; i < rank; ++i) key.push_back(box[i]);
@@ -246,7 +273,10 @@ CUtensorMap tmap(gorila_ctx* ctx, const void* base, int rank, const uint64_t* di
     for (int i = 0; i < rank - 1; ++i) st[i] = strides[i];
     auto enc = tma_encoder();
     CUresult r = enc ? enc(&m, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, rank, const_cast<void*>(base), d, st, b, e,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           swizzle == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
+                           : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                                           : CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)
                      : CUDA_ERROR_NOT_INITIALIZED;
     if (r != CUDA_SUCCESS) {
@@ -264,6 +294,16 @@ OpMatK<TR> op_matk(gorila_ctx* ctx, const void* x, int rows, int K, int64_t ld) 
     const uint64_t dims[3] = {8, (uint64_t)rows, (uint64_t)K / 8}, str[2] = {(uint64_t)ld * 2, 16};
     const uint32_t box[3] = {8, TR, 8};
     o.map = tmap(ctx, x, 3, dims, str, box);
+    o.rows = rows;
+    return o;
+}
+// the same, SWIZZLE_128B: map (K, rows), box (64, TR)
+template <int TR>
+OpMatKS<TR> op_matks(gorila_ctx* ctx, const void* x, int rows, int K, int64_t ld) {
+    OpMatKS<TR> o;
+    const uint64_t dims[2] = {(uint64_t)K, (uint64_t)rows}, str[1] = {(uint64_t)ld * 2};
+    const uint32_t box[2] = {64, TR};
+    o.map = tmap(ctx, x, 2, dims, str, box, nullptr, 128);
     o.rows = rows;
     return o;
 }
@@ -296,6 +336,34 @@ CUtensorMap conv1_map(gorila_ctx* ctx, const void* s, int B, int bh_rows, int bb
     const uint32_t box[5] = {8, 40, (uint32_t)(bh_rows * 4), (uint32_t)bb, 4};
     const uint32_t es[5] = {1, 2, 4, 1, 1};
     return tmap(ctx, s, 5, dims, str, box, es);
+}
+// swizzled forward im2col views (OpConvFwdS): 128-B rows of 64 K-elements per output pixel.
+// conv3: (64 c, W, H, B); conv2: (64 = 2 pixels x 32 c, W-1 [x stride C*2], H, B), element strides 2
+template <class SH>
+CUtensorMap fwd_map_sw(gorila_ctx* ctx, const void* x, int B, int nb) {
+    constexpr int TPC = 64 / SH::C;
+    const uint64_t dims[4] = {64, (uint64_t)(SH::W - (TPC - 1)), (uint64_t)SH::H, (uint64_t)B};
+    const uint64_t str[3] = {SH::C * 2, SH::W * SH::C * 2, (uint64_t)SH::H * SH::W * SH::C * 2};
+    const uint32_t box[4] = {64, (uint32_t)(SH::OW * SH::S), (uint32_t)(SH::OH * SH::S), (uint32_t)nb};
+    const uint32_t es[4] = {1, (uint32_t)SH::S, (uint32_t)SH::S, 1};
+    return tmap(ctx, x, 4, dims, str, box, es, 128);
+}
+// conv1 (OpConv1FwdS): 64-B rows = 8 pixels x 4 channels at x = 4*ox: (32, 20 ox, 84 y, B)
+CUtensorMap conv1_map_sw(gorila_ctx* ctx, const void* s, int B, int nb) {
+    const uint64_t dims[4] = {32, H1, 84, (uint64_t)B};
+    const uint64_t str[3] = {32, 84 * 8, 84 * 84 * 8};
+    const uint32_t box[4] = {32, H1, 4 * H1, (uint32_t)nb};
+    const uint32_t es[4] = {1, 1, 4, 1};
+    return tmap(ctx, s, 4, dims, str, box, es, 64);
+}
+// swizzled output-gradient view (OpDgradS): (64 co, OW, OH, B), box (64, bw, bh, nb)
+template <class SH>
+CUtensorMap grad_map_sw(gorila_ctx* ctx, const void* g, int B, int bw, int bh, int bb) {
+    static_assert(SH::CO == 64, "one 128-B row per tap");
+    const uint64_t dims[4] = {64, (uint64_t)SH::OW, (uint64_t)SH::OH, (uint64_t)B};
+    const uint64_t str[3] = {128, (uint64_t)SH::OW * 128, (uint64_t)SH::OH * SH::OW * 128};
+    const uint32_t box[4] = {64, (uint32_t)bw, (uint32_t)bh, (uint32_t)bb};
+    return tmap(ctx, g, 4, dims, str, box, nullptr, 128);
 }
 // output-gradient view g [B][OH][OW][CO=64]: (8, OW, OH, B, 8), box (8, bw, bh, NB, 8)
 template <class SH>
@@ -515,6 +583,9 @@ template <typename T>
 gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int accumulate,
                           uint32_t phases = 0xffffffffu) {
 #define PHASE(ph) if (phases & (1u << (ph)))
+    // fork the weight-gradient GEMMs and the bias partials onto the side stream (full rounds only;
+    // phase profiling keeps one stream so that its marks bracket single kernels)
+    const bool fk = ctx->fork && ctx->side && !ctx->prof && phases == ~0u;
     const gorila_config& cfg = ctx->cfg;
     Learner& Lr = ctx->learners[j];
     const int B = ctx->B, nA = ctx->nA;
@@ -559,13 +630,13 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                 {{s2, M}, {tt + RT.w1, K1, C1_OUT, K1}, {t1, C1_OUT, tf + RT.b1, in_scale, M, C1_OUT, 1}}};
             gemm<T, 32>(ctx, pr, 2, M, C1_OUT, K1, 1);
         } else {  // TMA: one sample (400 rows = 4 M-blocks) per tile, pixel-pair im2col boxes
-            using OA = OpConv1Fwd<4>; using OB = OpMatK<32>; using EP = EpAct<T>;
+            using OA = OpConv1FwdS<4>; using OB = OpMatKS<32>; using EP = EpAct<T>;
             TmaProb<OA, OB, EP> pr[2];
             for (int z = 0; z < 2; ++z) {
-                pr[z].a.map = conv1_map(ctx, z ? (const void*)s2 : (const void*)s, B, H1, 1);
+                pr[z].a.map = conv1_map_sw(ctx, z ? (const void*)s2 : (const void*)s, B, 1);
                 pr[z].a.nb = 1;
                 pr[z].a.batch = B;
-                pr[z].b = op_matk<32>(ctx, z ? (const void*)(tt + RT.w1) : (const void*)(rt + RL.w1), C1_OUT, K1, K1);
+                pr[z].b = op_matks<32>(ctx, z ? (const void*)(tt + RT.w1) : (const void*)(rt + RL.w1), C1_OUT, K1, K1);
                 pr[z].ep = {z ? t1 : a1, C1_OUT, z ? tf + RT.b1 : rf + RL.b1, in_scale, M, C1_OUT, 1};
             }
             gemm_tma_launch<32, 4>(ctx, pr, 2, B, 1, K1 / 64, 1, 0, C1_OUT);
@@ -584,16 +655,16 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                 {{t1, M}, {tt + RT.w2, K2, C2_OUT, K2}, {t2, C2_OUT, tf + RT.b2, 1.f, M, C2_OUT, 1}}};
             gemm<T, 64>(ctx, pr, 2, M, C2_OUT, K2, 1, 148);
         } else {  // TMA: one sample (81 rows) per tile, stride-2 boxes; in-cluster split of K = 512
-            using OA = OpConvFwd<Conv2, 1>; using OB = OpMatK<64>; using EP = EpAct<T>;
+            using OA = OpConvFwdS<Conv2, 1>; using OB = OpMatKS<64>; using EP = EpAct<T>;
             TmaProb<OA, OB, EP> pr[2];
             for (int z = 0; z < 2; ++z) {
-                pr[z].a.map = nhwc_map<Conv2>(ctx, z ? (const void*)t1 : (const void*)a1, B, 2 * H2, 2 * H2, 1, 8, 2);
+                pr[z].a.map = fwd_map_sw<Conv2>(ctx, z ? (const void*)t1 : (const void*)a1, B, 1);
                 pr[z].a.nb = 1;
                 pr[z].a.batch = B;
-                pr[z].b = op_matk<64>(ctx, z ? (const void*)(tt + RT.w2) : (const void*)(rt + RL.w2), C2_OUT, K2, K2);
+                pr[z].b = op_matks<64>(ctx, z ? (const void*)(tt + RT.w2) : (const void*)(rt + RL.w2), C2_OUT, K2, K2);
                 pr[z].ep = {z ? t2 : a2, C2_OUT, z ? tf + RT.b2 : rf + RL.b2, 1.f, M, C2_OUT, 1};
             }
-            gemm_tma_launch<64, 1>(ctx, pr, 2, B, 1, K2 / 64, 1, 256, C2_OUT);
+            gemm_tma_launch<64, 1>(ctx, pr, 2, B, 1, K2 / 64, 1, 0, C2_OUT);
         }
     }
     }
@@ -609,16 +680,16 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                 {{t2, M}, {tt + RT.w3, K3, C3_OUT, K3}, {t3, C3_OUT, tf + RT.b3, 1.f, M, C3_OUT, 1}}};
             gemm<T, 64>(ctx, pr, 2, M, C3_OUT, K3, 1, 148);
         } else {  // TMA: two samples (98 rows) per tile, one tap per K-chunk
-            using OA = OpConvFwd<Conv3, 1>; using OB = OpMatK<64>; using EP = EpAct<T>;
+            using OA = OpConvFwdS<Conv3, 1>; using OB = OpMatKS<64>; using EP = EpAct<T>;
             TmaProb<OA, OB, EP> pr[2];
             for (int z = 0; z < 2; ++z) {
-                pr[z].a.map = nhwc_map<Conv3>(ctx, z ? (const void*)t2 : (const void*)a2, B, H3, H3, 2, 8, 1);
+                pr[z].a.map = fwd_map_sw<Conv3>(ctx, z ? (const void*)t2 : (const void*)a2, B, 2);
                 pr[z].a.nb = 2;
                 pr[z].a.batch = B;
-                pr[z].b = op_matk<64>(ctx, z ? (const void*)(tt + RT.w3) : (const void*)(rt + RL.w3), C3_OUT, K3, K3);
+                pr[z].b = op_matks<64>(ctx, z ? (const void*)(tt + RT.w3) : (const void*)(rt + RL.w3), C3_OUT, K3, K3);
                 pr[z].ep = {z ? t3 : a3, C3_OUT, z ? tf + RT.b3 : rf + RL.b3, 1.f, M, C3_OUT, 1};
             }
-            gemm_tma_launch<64, 1>(ctx, pr, 2, (B + 1) / 2, 1, K3 / 64, 1, 148, C3_OUT);
+            gemm_tma_launch<64, 1>(ctx, pr, 2, (B + 1) / 2, 1, K3 / 64, 1, 0, C3_OUT);
         }
     }
     }
@@ -636,12 +707,12 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         } else {
 #define FC4F(BN_)                                                                                              \
     {                                                                                                          \
-        using OA = OpMatK<128>; using OB = OpMatK<BN_>; using EP = EpActT;                                     \
+        using OA = OpMatKS<128>; using OB = OpMatKS<BN_>; using EP = EpActT;                                   \
         TmaProb<OA, OB, EP> pr[2];                                                                             \
         for (int z = 0; z < 2; ++z) {                                                                          \
-            pr[z].a = op_matk<128>(ctx, z ? (const void*)(tt + RT.w4) : (const void*)(rt + RL.w4), FC4_OUT,    \
+            pr[z].a = op_matks<128>(ctx, z ? (const void*)(tt + RT.w4) : (const void*)(rt + RL.w4), FC4_OUT,    \
                                    FC4_IN, FC4_IN);                                                            \
-            pr[z].b = op_matk<BN_>(ctx, z ? (const void*)t3 : (const void*)a3, B, FC4_IN, FC4_IN);             \
+            pr[z].b = op_matks<BN_>(ctx, z ? (const void*)t3 : (const void*)a3, B, FC4_IN, FC4_IN);            \
             pr[z].ep = {z ? t4 : a4, FC4_OUT, z ? tf + RT.b4 : rf + RL.b4, FC4_OUT, B};                        \
         }                                                                                                      \
         gemm_tma_launch<BN_, 1>(ctx, pr, 2, FC4_OUT / 128, (B + BN_ - 1) / BN_, FC4_IN / 64, 1, 148, B);      \
@@ -664,7 +735,8 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         t.base_V = ctx->Vhist + slot; t.n_acc_local = ctx->n_acc_local; t.max_staleness = cfg.max_staleness;
         t.outlier_enabled = cfg.outlier_enabled; t.outlier_warmup = cfg.outlier_warmup;
         t.outlier_k = cfg.outlier_k; t.outlier_beta = cfg.outlier_beta;
-        launch(ctx, k_fc5_td, dim3(B, 2), dim3(256), 0, p);
+        p.per_sample = ctx->td_partial;
+        launch(ctx, k_fc5_td, dim3(B), dim3(256), 0, p);
     }
     }
     mark(ctx, PH_FC5F);
@@ -675,6 +747,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
            (const float*)(rf + RL.w5), B, nA, ctx->G, g4, accumulate);
     }
     mark(ctx, PH_FC5B);
+    if (fk) fork_side(ctx, 0);  // g4 ready: fc4 wgrad may start
     PHASE(PH_FC4DG) {
     // fc4 dgrad (i = k, j = b, red = n): g3[b][k] = mask(sum_n W4[n][k] g4[b][n])
     {
@@ -686,10 +759,10 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         } else {
 #define FC4D(BN_)                                                                                              \
     {                                                                                                          \
-        using OA = OpMatMN<128>; using OB = OpMatK<BN_>; using EP = EpMaskT<T>;                                \
+        using OA = OpMatMN<128>; using OB = OpMatKS<BN_>; using EP = EpMaskT<T>;                               \
         TmaProb<OA, OB, EP> pr[1];                                                                             \
         pr[0].a = op_matmn<128>(ctx, rt + RL.w4, FC4_OUT, FC4_IN, FC4_IN);                                     \
-        pr[0].b = op_matk<BN_>(ctx, g4, B, FC4_OUT, FC4_OUT);                                                  \
+        pr[0].b = op_matks<BN_>(ctx, g4, B, FC4_OUT, FC4_OUT);                                                 \
         pr[0].ep = {g3, a3, FC4_IN, FC4_IN, B};                                                                \
         gemm_tma_launch<BN_, 1>(ctx, pr, 1, (FC4_IN + 127) / 128, (B + BN_ - 1) / BN_, FC4_OUT / 64, 1, 148, B); \
     }
@@ -702,6 +775,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     PHASE(PH_FC4WG) {
     // fc4 wgrad (i = k, j = n, red = b): G[W4][n][k] += sum_b a3[b][k] g4[b][n]
     {
+        OnSide on_side(ctx, fk);
         if constexpr (fp32v) {
             using LA = LdRowsMN<T>; using LB = LdRowsMN<T>; using EP = EpAddT;
             GemmProb<LA, LB, EP> pr[1] = {{{a3, FC4_IN, FC4_IN, B}, {g4, FC4_OUT, FC4_OUT, B},
@@ -718,6 +792,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }
     }
     mark(ctx, PH_FC4WG);
+    if (fk) fork_side(ctx, 1);  // g3 ready (fc4 dgrad is on the main stream before this point)
     PHASE(PH_CONV3DG) {
     // conv3 dgrad: g2 = mask(conv3^T(g3))
     {
@@ -727,16 +802,16 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             GemmProb<LA, LB, EP> pr[1] = {{{g3, M}, {rt + RL.w3}, {g2, a2, C2_OUT, M, C2_OUT}}};
             gemm<T, 64>(ctx, pr, 1, M, C2_OUT, K3, 1, 148);
         } else {  // TMA: one sample (81 input pixels) per tile, shifted boxes with zero fill
-            using OA = OpDgrad<Conv3, 1>; using OB = OpWdgradMN<Conv3>; using EP = EpMask<T>;
+            using OA = OpDgradS<Conv3, 1>; using OB = OpWdgradMN<Conv3>; using EP = EpMask<T>;
             TmaProb<OA, OB, EP> pr[1];
-            pr[0].a.map = grad_map<Conv3>(ctx, g3, B, H2, H2, 1);
+            pr[0].a.map = grad_map_sw<Conv3>(ctx, g3, B, H2, H2, 1);
             pr[0].a.nb = 1;
             pr[0].a.batch = B;
             pr[0].a.phase = -1;
             pr[0].b.map = wdgrad_map<Conv3>(ctx, rt + RL.w3);
             pr[0].b.phase = -1;
             pr[0].ep = {g2, a2, C2_OUT, M, C2_OUT};
-            gemm_tma_launch<64, 1>(ctx, pr, 1, B, 1, C3_K * C3_K, 1, 148, C2_OUT);
+            gemm_tma_launch<64, 1>(ctx, pr, 1, B, 1, C3_K * C3_K, 1, 0, C2_OUT);
         }
     }
     }
@@ -744,6 +819,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     PHASE(PH_CONV3WG) {
     // conv3 wgrad (i = r, j = o, red = m): partial[s][o][r]
     {
+        OnSide on_side(ctx, fk);
         const int Mred = B * H3 * H3;
         if constexpr (fp32v) {
             using LA = LdConvInMN<T, Conv3>; using LB = LdRowsMN<T>; using EP = EpStoreT;
@@ -761,6 +837,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }
     }
     mark(ctx, PH_CONV3WG);
+    if (fk) fork_side(ctx, 2);  // g2 ready
     PHASE(PH_CONV2DG) {
     // conv2 dgrad: g1 = mask(conv2^T(g2))
     {
@@ -770,10 +847,10 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             GemmProb<LA, LB, EP> pr[1] = {{{g2, M}, {rt + RL.w2}, {g1, a1, C1_OUT, M, C1_OUT}}};
             gemm<T, 32>(ctx, pr, 1, M, C1_OUT, Conv2::RD, 1, 296);
         } else {  // TMA: the stride-2 transpose as 4 phase problems of 2x2 taps (no zero taps)
-            using OA = OpDgrad<Conv2, 1>; using OB = OpWdgradMN<Conv2>; using EP = EpMask<T>;
+            using OA = OpDgradS<Conv2, 1>; using OB = OpWdgradMN<Conv2>; using EP = EpMask<T>;
             TmaProb<OA, OB, EP> pr[4];
             for (int ph = 0; ph < 4; ++ph) {
-                pr[ph].a.map = grad_map<Conv2>(ctx, g2, B, 10, 10, 1);
+                pr[ph].a.map = grad_map_sw<Conv2>(ctx, g2, B, 10, 10, 1);
                 pr[ph].a.nb = 1;
                 pr[ph].a.batch = B;
                 pr[ph].a.phase = ph;
@@ -781,7 +858,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                 pr[ph].b.phase = ph;
                 pr[ph].ep = {g1, a1, C1_OUT, M, C1_OUT};
             }
-            gemm_tma_launch<32, 1>(ctx, pr, 4, B, 1, 4, 1, 256, C1_OUT);
+            gemm_tma_launch<32, 1>(ctx, pr, 4, B, 1, 4, 1, 0, C1_OUT);
         }
     }
     }
@@ -789,6 +866,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     PHASE(PH_CONV2WG) {
     // conv2 wgrad
     {
+        OnSide on_side(ctx, fk);
         const int Mred = B * H2 * H2;
         if constexpr (fp32v) {
             using LA = LdConvInMN<T, Conv2>; using LB = LdRowsMN<T>; using EP = EpStoreT;
@@ -806,6 +884,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }
     }
     mark(ctx, PH_CONV2WG);
+    if (fk) fork_side(ctx, 3);  // g1 ready
     PHASE(PH_CONV1WG) {
     // conv1 wgrad (input scale 1/255 folded into the store)
     {
@@ -828,10 +907,12 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     mark(ctx, PH_CONV1WG);
     PHASE(PH_BIASG) {
     // bias gradients b1..b4 (coalesced partials; reduced by K10)
-    launch(ctx, k_bias_partial<T>, dim3(BIAS_CHUNKS, 4), dim3(256), 0, (const T*)g1, (const T*)g2, (const T*)g3,
-           (const T*)g4, B, ctx->part_b);
+    OnSide on_side(ctx, fk);
+    launch(ctx, k_bias_partial<T>, dim3(ctx->bias_chunks, 4), dim3(256), 0, (const T*)g1, (const T*)g2, (const T*)g3,
+           (const T*)g4, B, ctx->part_b, ctx->bias_chunks);
     }
     mark(ctx, PH_BIASG);
+    if (fk) join_side(ctx);
     PHASE(PH_WGRED) {
     // K10: fixed-order reduction of the conv wgrad partials into G
     {
@@ -846,8 +927,8 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         const int64_t boff[4] = {OFF_B1, OFF_B2, OFF_B3, OFF_B4};
         const float* bp = ctx->part_b;
         for (int l = 0; l < 4; ++l) {
-            p.part[3 + l] = bp; p.splits[3 + l] = BIAS_CHUNKS; p.count[3 + l] = bc[l]; p.off[3 + l] = boff[l];
-            bp += BIAS_CHUNKS * bc[l];
+            p.part[3 + l] = bp; p.splits[3 + l] = ctx->bias_chunks; p.count[3 + l] = bc[l]; p.off[3 + l] = boff[l];
+            bp += (int64_t)ctx->bias_chunks * bc[l];
         }
         p.nseg = 7;
         p.accumulate = accumulate;
@@ -938,6 +1019,8 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     float* sr = c.take<float>(Bs);
     int64_t* sidx = c.take<int64_t>(Bs);
     float* dQ = c.take<float>(Bs * nA);
+    float* td_partial = c.take<float>(Bs * 2);
+    const int bias_chunks = std::max(64, std::min(2048, 2 * B));
     // split choices (reduction chunks of 64 for tc, 16 for simt)
     const int chunk = fp32 ? SM_BR : TC_BK;
     int split_w[3];
@@ -957,7 +1040,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         }
         part_w[l] = c.take<float>((int64_t)split_w[l] * wcount[l]);
     }
-    float* part_b = c.take<float>((int64_t)BIAS_CHUNKS * (C1_OUT + C2_OUT + C3_OUT + FC4_OUT));
+    float* part_b = c.take<float>((int64_t)bias_chunks * (C1_OUT + C2_OUT + C3_OUT + FC4_OUT));
     float* tmp_canon = c.take<float>(P);
     float* tmp_int = c.take<float>(W * q);
     if (ctx) {
@@ -970,6 +1053,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         ctx->t1 = t1; ctx->t2 = t2; ctx->t3 = t3; ctx->t4 = t4;
         ctx->g1 = g1; ctx->g2 = g2; ctx->g3 = g3; ctx->g4 = g4;
         ctx->sa = sa; ctx->sd = sd; ctx->sr = sr; ctx->sidx = sidx; ctx->dQ = dQ;
+        ctx->td_partial = td_partial; ctx->bias_chunks = bias_chunks;
         for (int l = 0; l < 3; ++l) { ctx->part_w[l] = part_w[l]; ctx->split_w[l] = split_w[l]; }
         ctx->part_b = part_b;
         ctx->tmp_canon = tmp_canon; ctx->tmp_int = tmp_int;
@@ -1121,7 +1205,12 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     {
         const char* e = getenv("GORILA_PDL");  // GORILA_PDL=0 disables programmatic dependent launch
         ctx->pdl = !(e && atoi(e) == 0);
+        const char* f = getenv("GORILA_FORK");  // GORILA_FORK=0 keeps the round on one stream
+        ctx->fork = !(f && atoi(f) == 0);
     }
+    CU(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    for (auto& e : ctx->ev_fork) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
     for (auto& l : ctx->learners) {
         CU(cudaMemsetAsync(l.n_dev, 0, sizeof(uint64_t), st));
         CU(cudaMemsetAsync(l.stats, 0, sizeof(LearnerStats), st));
@@ -1151,6 +1240,13 @@ void gorila_destroy(gorila_ctx* ctx) {
     if (!ctx) return;
     if (ctx->stream) cudaStreamSynchronize(ctx->stream);
     for (auto e : ctx->ev_pool) cudaEventDestroy(e);
+    if (ctx->side) {
+        cudaStreamSynchronize(ctx->side);
+        cudaStreamDestroy(ctx->side);
+    }
+    for (auto e : ctx->ev_fork)
+        if (e) cudaEventDestroy(e);
+    if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
     for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : ctx->graph_marks)
         for (auto& m : kv.second) cudaEventDestroy(m.second);

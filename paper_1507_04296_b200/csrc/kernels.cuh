@@ -186,25 +186,27 @@ GORILA_DEV int td_decide(const TdParams& p, const float* s_sq, const float* s_ab
 }
 
 // ------------------------------------------------------------------------- fc5 forward + K7
-// Grid (B, 2): block (b, z) computes Q(s_b, .) (z = 0, online) or Q-hat(s'_b, .) (z = 1, target);
-// the last block to finish (device counter) runs K7 for the whole batch. Replaces the
-// fc5-forward and TD launches.
+// Grid (B): block b computes Q(s_b, .) and Q-hat(s'_b, .) (fc5, fp32), the TD target, delta and
+// dQ of sample b (Alg.1; reading R3), and its delta^2 / |delta| into per_sample[b];
+// the last block to finish (device counter) sums the batch in sample order and takes the outlier
+// and stale decisions (td_decide); a rejected batch has its dQ zeroed there.
 struct Fc5TdParams {
     const float *a4, *t4, *w5, *b5, *w5t, *b5t;
     unsigned int* counter;  // zero between launches (the last block resets it)
+    float* per_sample;      // [B][2]
     TdParams td;
 };
 __global__ void __launch_bounds__(256) k_fc5_td(Fc5TdParams p) {
     pdl_wait();
     pdl_trigger();
     const TdParams& t = p.td;
-    const int b = blockIdx.x, z = blockIdx.y, nA = t.nA;
+    const int b = blockIdx.x, nA = t.nA;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    {
+    __shared__ float q[2][32];
+    for (int z = 0; z < 2; ++z) {
         const float* x = (z ? p.t4 : p.a4) + (int64_t)b * FC4_OUT;
         const float* w5 = z ? p.w5t : p.w5;
         const float* b5 = z ? p.b5t : p.b5;
-        float* q = const_cast<float*>(z ? t.Qhat : t.Q);
         float xv[FC4_OUT / 32];
 #pragma unroll
         for (int k = 0; k < FC4_OUT / 32; ++k) xv[k] = x[lane + 32 * k];
@@ -213,36 +215,49 @@ __global__ void __launch_bounds__(256) k_fc5_td(Fc5TdParams p) {
 #pragma unroll
             for (int k = 0; k < FC4_OUT / 32; ++k) acc = fmaf(xv[k], w5[a * FC4_OUT + lane + 32 * k], acc);
             acc = warp_sum(acc);
-            if (lane == 0) q[b * nA + a] = acc + b5[a];
+            if (lane == 0) q[z][a] = acc + b5[a];
+        }
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const float qv = lane < nA ? q[0][lane] : 0.f, qh = lane < nA ? q[1][lane] : -INFINITY;
+        if (lane < nA) {
+            const_cast<float*>(t.Q)[b * nA + lane] = qv;
+            const_cast<float*>(t.Qhat)[b * nA + lane] = q[1][lane];
+        }
+        const float mx = warp_max(qh);
+        const int ab = t.a[b];
+        const float y = t.d[b] ? t.r[b] : t.r[b] + t.gamma * mx;  // Alg.1
+        const float delta = y - q[0][ab];
+        if (lane < nA) {
+            const float cl = fminf(fmaxf(delta, -1.f), 1.f);  // reading R3
+            t.dQ[b * nA + lane] = (lane == ab) ? -cl / (float)t.B : 0.f;
+        }
+        if (lane == 0) {
+            p.per_sample[2 * b] = delta * delta;
+            p.per_sample[2 * b + 1] = fabsf(delta);
         }
     }
     __shared__ unsigned int s_last;
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = (atomicAdd(p.counter, 1u) == gridDim.x * gridDim.y - 1);
+    if (threadIdx.x == 0) s_last = (atomicAdd(p.counter, 1u) == gridDim.x - 1);
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    // K7 on the whole batch (this block only)
+    // last block: fixed-order batch sums (8 interleaved partials, then in order), decisions
     __shared__ float s_sq[8], s_ab[8];
     __shared__ int s_keep;
-    float sq = 0.f, ab = 0.f;
-    for (int i = warp; i < t.B; i += 8) {
-        const float qh = lane < nA ? __ldcg(&t.Qhat[i * nA + lane]) : -INFINITY;
-        const float mx = warp_max(qh);
-        const int ai = t.a[i];
-        const float y = t.d[i] ? t.r[i] : t.r[i] + t.gamma * mx;  // Alg.1
-        const float delta = y - __ldcg(&t.Q[i * nA + ai]);
-        if (lane < nA) {
-            const float cl = fminf(fmaxf(delta, -1.f), 1.f);  // reading R3
-            t.dQ[i * nA + lane] = (lane == ai) ? -cl / (float)t.B : 0.f;
-        }
-        sq += delta * delta;
-        ab += fabsf(delta);
+    float sq = 0.f, sa = 0.f;
+    for (int i = threadIdx.x; i < t.B; i += blockDim.x) {
+        sq += __ldcg(&p.per_sample[2 * i]);
+        sa += __ldcg(&p.per_sample[2 * i + 1]);
     }
+    sq = warp_sum(sq);
+    sa = warp_sum(sa);
     if (lane == 0) {
         s_sq[warp] = sq;
-        s_ab[warp] = ab;
+        s_ab[warp] = sa;
     }
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -297,11 +312,10 @@ __global__ void k_fc5_bwd(const float* __restrict__ dQ, const float* __restrict_
 // ------------------------------------------------------------------------- bias gradients
 // db_l[o] = sum_m g_l[m][o], layers 1..4: block (chunk, l) sums rows [chunk*rows_per, ...) with
 // coalesced row reads and a fixed-order in-block reduction -> part[l][chunk][o]; K10 sums chunks.
-constexpr int BIAS_CHUNKS = 64;
 template <typename T>
 __global__ void __launch_bounds__(256) k_bias_partial(const T* __restrict__ g1, const T* __restrict__ g2,
                                                       const T* __restrict__ g3, const T* __restrict__ g4, int B,
-                                                      float* __restrict__ part) {
+                                                      float* __restrict__ part, int BIAS_CHUNKS) {
     pdl_wait();
     pdl_trigger();
     // each thread owns 8 consecutive channels (one 16-B vector per row) of rows rg, rg+RG, ...

@@ -258,6 +258,108 @@ struct OpWgradOut {
     GORILA_DEV uint64_t desc(uint32_t base, int kk, int) const { return umma_desc(base + kk * 256, 128, KC * 16); }
 };
 
+// ---------------------------------------------------------------- swizzled K-major operands
+// (fewer, larger TMA requests: one 128-B (64-B) row per output row and K-chunk)
+
+// K-major plain matrix X[rows][K]: map dims (K, rows), box (64, TR), SWIZZLE_128B -> [row][128 B]
+template <int TR>
+struct OpMatKS {
+    static constexpr bool kMN = false;
+    static constexpr int KC = 64, STAGE = TR * 128, WRITTEN = STAGE;
+    alignas(64) CUtensorMap map;
+    int rows;
+    GORILA_DEV uint32_t issue(int tile, int kc, uint32_t dst, uint64_t* bar) const {
+        tma_load(&map, dst, bar, kc * 64, tile * TR);
+        return TR * 128;
+    }
+    GORILA_DEV uint64_t desc(uint32_t base, int kk, int mb) const { return umma_desc_sw(base + mb * 16384 + kk * 32, 128); }
+    GORILA_DEV int row(int tile, int r) const {
+        const int i = tile * TR + r;
+        return (r < TR && i < rows) ? i : -1;
+    }
+};
+
+// conv2 / conv3 forward im2col, SWIZZLE_128B: one 128-B row (64 K) per output pixel and chunk.
+// conv3 (C = 64): dims (64, W, H, B), box (64, OW, OH, NB), coords (0, kx, ky, b0).
+// conv2 (C = 32): the chunk = taps (ky, kx0), (ky, kx0+1) = two adjacent pixels = 128 contiguous
+// bytes: dims (64, W-1, H, B) with x stride C*2, box (64, OW*2, OH*2, NB), element strides (1,2,2,1).
+template <class SH, int MB>
+struct OpConvFwdS {
+    static constexpr bool kMN = false;
+    static constexpr int KC = 64, STAGE = MB * 128 * 128, WRITTEN = STAGE, TPC = 64 / SH::C;
+    alignas(64) CUtensorMap map;
+    int nb, batch;
+    GORILA_DEV int rows_tile() const { return nb * SH::OH * SH::OW; }
+    GORILA_DEV uint32_t issue(int tile, int kc, uint32_t dst, uint64_t* bar) const {
+        const int t = kc * TPC, ky = t / SH::K, kx = t - ky * SH::K;
+        tma_load(&map, dst, bar, 0, kx, ky, tile * nb);
+        return rows_tile() * 128;
+    }
+    GORILA_DEV uint64_t desc(uint32_t base, int kk, int mb) const { return umma_desc_sw(base + mb * 16384 + kk * 32, 128); }
+    GORILA_DEV int row(int tile, int r) const {
+        const int b = tile * nb + r / (SH::OH * SH::OW);
+        return (r < rows_tile() && b < batch) ? tile * rows_tile() + r : -1;
+    }
+};
+
+// conv1 forward, SWIZZLE_64B: one 64-B row (the 8 pixels x 4 channels of one kernel row) per
+// output pixel, two kernel rows per chunk. View s as (32, 20 ox [stride 32 B], 84 y, B), box
+// (32, 20, 80, NB), element strides (1, 1, 4, 1): x = 4*ox .. 4*ox+7 at row 4*oy + ky.
+template <int MB>
+struct OpConv1FwdS {
+    static constexpr bool kMN = false;
+    static constexpr int KC = 64, STAGE = 2 * MB * 128 * 64, WRITTEN = STAGE;
+    alignas(64) CUtensorMap map;
+    int nb, batch;
+    GORILA_DEV int rows_tile() const { return nb * H1 * H1; }
+    GORILA_DEV uint32_t issue(int tile, int kc, uint32_t dst, uint64_t* bar) const {
+#pragma unroll
+        for (int u = 0; u < 2; ++u) tma_load(&map, dst + u * MB * 128 * 64, bar, 0, 0, 2 * kc + u, tile * nb);
+        return 2 * rows_tile() * 64;
+    }
+    GORILA_DEV uint64_t desc(uint32_t base, int kk, int mb) const {
+        return umma_desc_sw(base + (kk >> 1) * MB * 128 * 64 + mb * 8192 + (kk & 1) * 32, 64);
+    }
+    GORILA_DEV int row(int tile, int r) const {
+        const int b = tile * nb + r / (H1 * H1);
+        return (r < rows_tile() && b < batch) ? tile * rows_tile() + r : -1;
+    }
+};
+
+// conv dgrad (shifted output gradient, CO = 64 = one 128-B row per tap), SWIZZLE_128B:
+// dims (64, OW, OH, B), box (8.. -> 64, side_x, side_y, NB), coords (0, -dx, -dy, b0)
+template <class SH, int MB>
+struct OpDgradS {
+    static constexpr bool kMN = false;
+    static constexpr int KC = 64, STAGE = MB * 128 * 128, WRITTEN = STAGE;
+    alignas(64) CUtensorMap map;
+    int nb, batch, phase;
+    GORILA_DEV int side_y() const { return phase < 0 ? SH::H : (SH::H + 1) / 2; }
+    GORILA_DEV int side_x() const { return phase < 0 ? SH::W : (SH::W + 1) / 2; }
+    GORILA_DEV int rows_tile() const { return nb * side_y() * side_x(); }
+    GORILA_DEV uint32_t issue(int tile, int kc, uint32_t dst, uint64_t* bar) const {
+        int dy, dx;
+        if (phase < 0) {
+            dy = kc / SH::K;
+            dx = kc - dy * SH::K;
+        } else {
+            dy = kc >> 1;
+            dx = kc & 1;
+        }
+        tma_load(&map, dst, bar, 0, -dx, -dy, tile * nb);
+        return rows_tile() * 128;
+    }
+    GORILA_DEV uint64_t desc(uint32_t base, int kk, int mb) const { return umma_desc_sw(base + mb * 16384 + kk * 32, 128); }
+    GORILA_DEV int row(int tile, int r) const {
+        const int sy = side_y(), sx = side_x(), per = sy * sx;
+        const int bb = r / per, b = tile * nb + bb;
+        if (r >= rows_tile() || b >= batch) return -1;
+        if (phase < 0) return tile * rows_tile() + r;
+        const int rem = r - bb * per, yy = rem / sx, xx = rem - yy * sx;
+        return (b * SH::H + 2 * yy + (phase >> 1)) * SH::W + 2 * xx + (phase & 1);
+    }
+};
+
 // ============================================================ the engine
 template <class OA, class OB, class EP>
 struct TmaProb {
@@ -284,7 +386,7 @@ struct TmaCfg {
     static constexpr int STAGES = (A_ST + B_ST) * 4 <= BUDGET ? 4 : (A_ST + B_ST) * 3 <= BUDGET ? 3 : 2;
     static constexpr int PIPE = STAGES * (A_ST + B_ST);
     static constexpr int RED = MB == 1 ? tc_red_bytes(BN) + tc_slice_bytes(BN) : 0;
-    static constexpr int SMEM = (PIPE > RED ? PIPE : RED) + 128;
+    static constexpr int SMEM = (PIPE > RED ? PIPE : RED) + 128 + 1024;  // + alignment slack
     static constexpr uint32_t TCOLS = tmem_cols_for(MB * BN);
     static_assert(MB * BN <= 256, "TMEM columns");
 };
@@ -294,13 +396,16 @@ __global__ void __launch_bounds__(128) gemm_tma(const __grid_constant__ TmaBatch
     using CFG = TmaCfg<BN, MB, OA, OB>;
     constexpr int STAGES = CFG::STAGES;
     static_assert(OA::KC == OB::KC && OA::KC % 16 == 0, "chunk rows");
-    extern __shared__ __align__(1024) uint8_t smem[];
-    uint64_t* full = reinterpret_cast<uint64_t*>(smem + CFG::SMEM - 128);
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    // swizzle atoms (and so every stage) must sit on 1024-B boundaries of the shared window
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + CFG::SMEM - 128);
     uint64_t* empty = full + STAGES;
     uint64_t* done = empty + STAGES;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    GTRACE(0);
     const int prob = blockIdx.z / p.splits, split = blockIdx.z - prob * p.splits;
     const TmaProb<OA, OB, EP>& P = p.prob[prob];
     const int ta = blockIdx.x, tb = blockIdx.y;
@@ -326,8 +431,10 @@ __global__ void __launch_bounds__(128) gemm_tma(const __grid_constant__ TmaBatch
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
+    GTRACE(1);
     pdl_wait();     // operands are produced by the preceding kernel(s)
     pdl_trigger();  // the next kernel may start its prologue
+    GTRACE(2);
     const uint32_t tmem = *tmem_slot;
     constexpr uint32_t IDESC =
         umma_idesc_bf16(TC_BM, BN) | (OA::kMN ? (1u << 15) : 0u) | (OB::kMN ? (1u << 16) : 0u);
@@ -343,6 +450,7 @@ __global__ void __launch_bounds__(128) gemm_tma(const __grid_constant__ TmaBatch
             uint32_t bytes = P.a.issue(ta, kc0 + kc, a_dst, &full[s]);
             bytes += P.b.issue(tb, kc0 + kc, b_dst, &full[s]);
             mbar_expect_tx(&full[s], bytes);
+            GTRACE(8 + (kc & 7));
         }
     } else if (tid == 32) {  // MMA issuer
         for (int kc = 0; kc < nK; ++kc) {
@@ -362,10 +470,15 @@ __global__ void __launch_bounds__(128) gemm_tma(const __grid_constant__ TmaBatch
         if (nK > 0) umma_commit(done);
     }
     __syncwarp();
+    GTRACE(3);
     if (nK > 0) mbar_wait(done, 0);
     tc_fence_after();
+    GTRACE(4);
 
     // ---------------------------------------------------------------- epilogue
+    // the functor is copied to registers once: indexed by the problem, its fields would otherwise
+    // be re-read from the parameter bank before every store (the compiler cannot rule out aliasing)
+    const EP ep = P.ep;
     if (MB == 1 && p.cluster > 1) {
         float* red = reinterpret_cast<float*>(smem);  // the stage ring is dead now
         const int lrow = warp * 32 + lane;
@@ -385,20 +498,33 @@ __global__ void __launch_bounds__(128) gemm_tma(const __grid_constant__ TmaBatch
         const int q = (int)cluster_ctarank();
         float* slice = reinterpret_cast<float*>(smem + tc_red_bytes(BN));
         const int n4 = rows_per * BN / 4;
-        for (int it = tid; it < n4; it += 128) {
-            const int r_loc = it / (BN / 4), c4 = (it % (BN / 4)) * 4;
-            const uint32_t a = smem_u32(red + ((c4 / 16) * TC_BM + q * rows_per + r_loc) * 20 + (c4 % 16));
-            float4 x[16];
+        // every float4 of this CTA's row slice: all CL peer reads in flight before any add
+        for (int it0 = 0; it0 < n4; it0 += 128 * 2) {
+            float4 x[2][16];
+            uint32_t ad[2];
 #pragma unroll
-            for (int pr = 0; pr < 16; ++pr)
-                if (pr < CL) x[pr] = dsmem_ld4(dsmem_map(a, (uint32_t)pr));
-            float4 acc = x[0];
+            for (int h = 0; h < 2; ++h) {
+                const int it = it0 + h * 128 + tid;
+                const int r_loc = it / (BN / 4), c4 = (it % (BN / 4)) * 4;
+                ad[h] = smem_u32(red + ((c4 / 16) * TC_BM + q * rows_per + r_loc) * 20 + (c4 % 16));
+                if (it < n4)
 #pragma unroll
-            for (int pr = 1; pr < 16; ++pr)
-                if (pr < CL) {
-                    acc.x += x[pr].x; acc.y += x[pr].y; acc.z += x[pr].z; acc.w += x[pr].w;
-                }
-            *reinterpret_cast<float4*>(slice + r_loc * (BN + 4) + c4) = acc;
+                    for (int pr = 0; pr < 16; ++pr)
+                        if (pr < CL) x[h][pr] = dsmem_ld4(dsmem_map(ad[h], (uint32_t)pr));
+            }
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int it = it0 + h * 128 + tid;
+                if (it >= n4) continue;
+                const int r_loc = it / (BN / 4), c4 = (it % (BN / 4)) * 4;
+                float4 acc = x[h][0];
+#pragma unroll
+                for (int pr = 1; pr < 16; ++pr)
+                    if (pr < CL) {
+                        acc.x += x[h][pr].x; acc.y += x[h][pr].y; acc.z += x[h][pr].z; acc.w += x[h][pr].w;
+                    }
+                *reinterpret_cast<float4*>(slice + r_loc * (BN + 4) + c4) = acc;
+            }
         }
         __syncthreads();
         for (int item = tid; item < rows_per * (BN / 16); item += 128) {
@@ -407,13 +533,14 @@ __global__ void __launch_bounds__(128) gemm_tma(const __grid_constant__ TmaBatch
             float v[16];
 #pragma unroll
             for (int e = 0; e < 16; ++e) v[e] = slice[r_loc * (BN + 4) + c0 + e];
-            if (i >= 0 && tb * BN + c0 < p.N) P.ep.apply16(i, tb * BN + c0, v, 0);
+            if (i >= 0 && tb * BN + c0 < p.N) ep.apply16(i, tb * BN + c0, v, 0);
         }
         cluster_sync();
     } else {
 #pragma unroll 1
         for (int mb = 0; mb < MB; ++mb) {
             const int i = P.a.row(ta, mb * 128 + warp * 32 + lane);
+            GTRACE(16);
 #pragma unroll 1
             for (int c0 = 0; c0 < BN; c0 += 16) {
                 float v[16];
@@ -423,13 +550,17 @@ __global__ void __launch_bounds__(128) gemm_tma(const __grid_constant__ TmaBatch
 #pragma unroll
                     for (int e = 0; e < 16; ++e) v[e] = 0.f;
                 }
-                if (i >= 0 && tb * BN + c0 < p.N) P.ep.apply16(i, tb * BN + c0, v, split);
+                if (c0 < 64) GTRACE(17 + 2 * (c0 / 16));
+                if (i >= 0 && tb * BN + c0 < p.N) ep.apply16(i, tb * BN + c0, v, split);
+                if (c0 < 64) GTRACE(18 + 2 * (c0 / 16));
             }
         }
     }
+    GTRACE(5);
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, CFG::TCOLS);
+    GTRACE(6);
 }
 
 }  // namespace gorila

@@ -19,10 +19,11 @@ g.replay_insert(0, f, a, r, d)
 ids = np.array([0], np.int32)
 for k in range(3):
     g.round(ids, k)
-names = {0: "entry", 1: "tmem_alloc", 2: "mbar_init+sync", 3: "pdl_wait", 4: "issue_prologue", 5: "loop_done",
-         6: "mma_done", 7: "epilogue_done", 30: "dealloc"}
-for ph in ["conv1_fwd", "conv2_fwd", "conv3_fwd", "fc4_fwd", "fc4_dgrad", "conv3_dgrad", "conv2_dgrad",
-           "conv3_wgrad", "conv1_wgrad"]:
+names = {0: "entry", 1: "prologue", 2: "pdl_wait", 3: "producer_done", 4: "mma_done", 5: "epilogue_done",
+         6: "dealloc", 16: "epi_row", 17: "ld0", 18: "st0", 19: "ld1", 20: "st1", 21: "ld2", 22: "st2", 23: "ld3",
+         24: "st3"}
+for ph in ["conv1_fwd", "conv2_fwd", "conv3_fwd", "fc4_fwd", "fc4_dgrad", "fc4_wgrad", "conv3_dgrad",
+           "conv2_dgrad", "conv3_wgrad", "conv2_wgrad", "conv1_wgrad"]:
     us = g.bench_phase(ph, iters=50)
     g.bench_phase(ph, iters=1)
     buf = (ctypes.c_uint64 * 64)()
@@ -30,6 +31,7 @@ for ph in ["conv1_fwd", "conv2_fwd", "conv3_fwd", "fc4_fwd", "fc4_dgrad", "conv3
     t = list(buf)
     t0 = t[0]
     ev = sorted([(v - t0, k) for k, v in enumerate(t) if v and v >= t0], key=lambda x: x[0])
-    line = "  ".join(f"{names.get(k, ('wait%d' % ((k - 8) // 2)) if k % 2 == 0 else ('mma%d' % ((k - 9) // 2)))}={v}"
-                     for v, k in ev)
+    line = "  ".join(f"{names.get(k, 'issued%d' % (k - 8))}={v}" for v, k in ev if v < 10**7)
     print(f"{ph:12s} {us:6.2f} us/launch | {line}")
+    if os.environ.get("RAW"):
+        print("   raw:", [(k, v - t0) for k, v in enumerate(t) if v])
