@@ -5,6 +5,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <type_traits>
+
 #define GORILA_DEV __device__ __forceinline__
 
 namespace gorila {
@@ -65,6 +67,9 @@ GORILA_DEV void mbar_wait(uint64_t* bar, uint32_t parity) {
         "@!P1 bra WAIT_%=;\n\t}" ::"r"(a),
         "r"(parity)
         : "memory");
+}
+GORILA_DEV void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
 }
 // make generic-proxy st.shared visible to the tensor core (async proxy)
 GORILA_DEV void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
@@ -216,6 +221,19 @@ GORILA_DEV uint64_t umma_desc_sw(uint32_t saddr, uint32_t row_bytes) {
     d |= (uint64_t)1 << 16;                            // LBO (unused for swizzled K-major)
     d |= (uint64_t)(((8 * row_bytes) >> 4) & 0x3FFF) << 32;  // SBO = one 8-row atom
     d |= (uint64_t)1 << 46;                            // version
+    d |= layout << 61;
+    return d;
+}
+// MN-major swizzled layouts (TMA SWIZZLE_128B / 64B, boxes of 64 / 32 MN elements): K rows of
+// 128 / 64 B, 8-row atoms; LBO = byte stride between MN blocks of 64 / 32 elements, SBO = byte
+// stride between 8-row K groups (the roles are swapped relative to the no-swizzle layout).
+GORILA_DEV uint64_t umma_desc_mn_sw(uint32_t saddr, uint32_t lbo, uint32_t row_bytes) {
+    const uint64_t layout = row_bytes == 128 ? 2ull : 4ull;
+    uint64_t d = 0;
+    d |= (uint64_t)((saddr >> 4) & 0x3FFF);
+    d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;
+    d |= (uint64_t)(((8 * row_bytes) >> 4) & 0x3FFF) << 32;
+    d |= (uint64_t)1 << 46;
     d |= layout << 61;
     return d;
 }

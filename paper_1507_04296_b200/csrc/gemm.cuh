@@ -361,7 +361,7 @@ struct GemmBatch {
 constexpr int TC_BM = 128, TC_BK = 64, TC_THREADS = 128;
 
 __host__ __device__ constexpr uint32_t tmem_cols_for(int bn) {
-    return bn <= 32 ? 32u : bn <= 64 ? 64u : bn <= 128 ? 128u : 256u;
+    return bn <= 32 ? 32u : bn <= 64 ? 64u : bn <= 128 ? 128u : bn <= 256 ? 256u : 512u;
 }
 // fp32 partial tile for the cluster reduction: [BN/16][128 rows][20 floats] (80-B row pitch: conflict-free)
 __host__ __device__ constexpr int tc_red_bytes(int bn) { return (bn / 16) * TC_BM * 80; }

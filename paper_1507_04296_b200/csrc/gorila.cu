@@ -152,6 +152,7 @@ struct gorila_ctx {
     std::map<std::vector<int64_t>, std::vector<std::pair<int, cudaEvent_t>>> graph_marks;  // profiling graphs
     std::map<std::vector<uint64_t>, CUtensorMap> tmaps;  // TMA descriptors, encoded once per (buffer, view)
     bool tma_failed = false;
+    int num_sms = 148;
     // side stream for the weight-gradient GEMMs, which are off the dgrad critical path
     // (a fork / join of the round; a graph captures it as parallel branches)
     cudaStream_t side = nullptr;
@@ -349,10 +350,10 @@ CUtensorMap fwd_map_sw(gorila_ctx* ctx, const void* x, int B, int nb) {
     return tmap(ctx, x, 4, dims, str, box, es, 128);
 }
 // conv1 (OpConv1FwdS): 64-B rows = 8 pixels x 4 channels at x = 4*ox: (32, 20 ox, 84 y, B)
-CUtensorMap conv1_map_sw(gorila_ctx* ctx, const void* s, int B, int nb) {
+CUtensorMap conv1_map_sw(gorila_ctx* ctx, const void* s, int B, int nb, int out_rows = H1) {
     const uint64_t dims[4] = {32, H1, 84, (uint64_t)B};
     const uint64_t str[3] = {32, 84 * 8, 84 * 84 * 8};
-    const uint32_t box[4] = {32, H1, 4 * H1, (uint32_t)nb};
+    const uint32_t box[4] = {32, H1, (uint32_t)(4 * out_rows), (uint32_t)nb};
     const uint32_t es[4] = {1, 1, 4, 1};
     return tmap(ctx, s, 4, dims, str, box, es, 64);
 }
@@ -364,6 +365,39 @@ CUtensorMap grad_map_sw(gorila_ctx* ctx, const void* g, int B, int bw, int bh, i
     const uint64_t str[3] = {128, (uint64_t)SH::OW * 128, (uint64_t)SH::OH * SH::OW * 128};
     const uint32_t box[4] = {64, (uint32_t)bw, (uint32_t)bh, (uint32_t)bb};
     return tmap(ctx, g, 4, dims, str, box, nullptr, 128);
+}
+// MN-major [Krows][MN] matrix, SWIZZLE_128B: map (MN, Krows), box (64, 64)
+template <int TR>
+OpMatMNS<TR> op_matmns(gorila_ctx* ctx, const void* x, int krows, int mn, int64_t ld) {
+    OpMatMNS<TR> o;
+    const uint64_t dims[2] = {(uint64_t)mn, (uint64_t)krows}, str[1] = {(uint64_t)ld * 2};
+    const uint32_t box[2] = {64, 64};
+    o.map = tmap(ctx, x, 2, dims, str, box, nullptr, 128);
+    o.mn = mn;
+    return o;
+}
+// conv weight [CO][K][K][C] as (C, CO, K*K), box (C, 64, 1), swizzle = C*2 bytes
+template <class SH>
+CUtensorMap wdgrad_map_sw(gorila_ctx* ctx, const void* w) {
+    const uint64_t dims[3] = {SH::C, SH::CO, (uint64_t)SH::K * SH::K};
+    const uint64_t str[2] = {(uint64_t)SH::R * 2, SH::C * 2};
+    const uint32_t box[3] = {SH::C, 64, 1};
+    return tmap(ctx, w, 3, dims, str, box, nullptr, SH::C * 2);
+}
+// weight-gradient output-gradient operand, swizzled rows of CO*2 bytes
+template <int CO, int KC, bool FLAT>
+OpWgradOutS<CO, KC, FLAT> op_wgout_s(gorila_ctx* ctx, const void* g, int npix, int B) {
+    OpWgradOutS<CO, KC, FLAT> o;
+    if (FLAT) {
+        const uint64_t dims[2] = {CO, (uint64_t)B * npix}, str[1] = {CO * 2};
+        const uint32_t box[2] = {CO, KC};
+        o.map = tmap(ctx, g, 2, dims, str, box, nullptr, CO * 2);
+    } else {
+        const uint64_t dims[3] = {CO, (uint64_t)npix, (uint64_t)B}, str[2] = {CO * 2, (uint64_t)npix * CO * 2};
+        const uint32_t box[3] = {CO, KC, 1};
+        o.map = tmap(ctx, g, 3, dims, str, box, nullptr, CO * 2);
+    }
+    return o;
 }
 // output-gradient view g [B][OH][OW][CO=64]: (8, OW, OH, B, 8), box (8, bw, bh, NB, 8)
 template <class SH>
@@ -400,6 +434,56 @@ OpWgradOut<CO, KC, FLAT> op_wgout(gorila_ctx* ctx, const void* g, int npix, int 
     return o;
 }
 
+bool cluster_env_on() {
+    static const int v = [] {
+        const char* e = getenv("GORILA_CLUSTER");  // GORILA_CLUSTER=0: no in-cluster split-K
+        return e ? atoi(e) : 1;
+    }();
+    return v != 0;
+}
+
+// persistent launch: grid = min(tiles, SMs x resident CTAs per SM)
+template <int BN, int MB, class OA, class OB, class EP>
+void gemm_tma_p_launch(gorila_ctx* ctx, const TmaProb<OA, OB, EP>* probs, int nprob, int tilesA, int tilesB,
+                       int nchunks, int splits, int N) {
+    using CFG = TmaPCfg<BN, MB, OA, OB>;
+    static int occ = 0;
+    if (!occ) {
+        cudaFuncSetAttribute(gemm_tma_p<BN, MB, OA, OB, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, CFG::SMEM);
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&occ, gemm_tma_p<BN, MB, OA, OB, EP>, CFG::THREADS,
+                                                          CFG::SMEM) != cudaSuccess ||
+            occ < 1)
+            occ = 1;
+        occ = std::min(occ, (int)(512 / CFG::TCOLS));  // TMEM columns per SM
+    }
+    TmaBatch<OA, OB, EP> gb;
+    memset((void*)&gb, 0, sizeof(gb));
+    for (int i = 0; i < nprob; ++i) gb.prob[i] = probs[i];
+    gb.nchunks = nchunks;
+    gb.N = N;
+    splits = std::max(1, std::min(splits, nchunks));
+    gb.chunks_per_split = (nchunks + splits - 1) / splits;
+    gb.splits = (nchunks + gb.chunks_per_split - 1) / gb.chunks_per_split;
+    gb.cluster = 1;
+    const int tiles = tilesA * tilesB * nprob * gb.splits;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(std::min(tiles, ctx->num_sms * occ));
+    cfg.blockDim = dim3(CFG::THREADS);
+    cfg.dynamicSmemBytes = CFG::SMEM;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    int na = 0;
+    if (ctx->pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, gemm_tma_p<BN, MB, OA, OB, EP>, gb, tilesA, tilesB, nprob);
+    ctx->launches++;
+}
+
 // grid + launch of the TMA engine (cluster split-K when cluster_target > 0)
 template <int BN, int MB, class OA, class OB, class EP>
 void gemm_tma_launch(gorila_ctx* ctx, const TmaProb<OA, OB, EP>* probs, int nprob, int tilesA, int tilesB,
@@ -411,6 +495,21 @@ void gemm_tma_launch(gorila_ctx* ctx, const TmaProb<OA, OB, EP>* probs, int npro
         cudaFuncSetAttribute(gemm_tma<BN, MB, OA, OB, EP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
         attr_set = true;
     }
+    static const bool persist_env = [] {
+        const char* e = getenv("GORILA_PERSIST");  // GORILA_PERSIST=0: one CTA per tile (gemm_tma)
+        return !(e && atoi(e) == 0);
+    }();
+    int cl = 1;  // in-cluster split-K size
+    if (MB == 1 && cluster_target > 0 && cluster_env_on()) {
+        const int tiles = tilesA * tilesB * nprob;
+        const int want = std::max(1, (cluster_target + tiles - 1) / tiles);
+        while (cl * 2 <= std::min(16, std::min(want, nchunks))) cl *= 2;
+    }
+    if (persist_env && cl == 1 &&
+        (int64_t)tilesA * tilesB * nprob * std::max(1, std::min(splits, nchunks)) > ctx->num_sms) {
+        gemm_tma_p_launch<BN, MB>(ctx, probs, nprob, tilesA, tilesB, nchunks, splits, N);
+        return;
+    }
     TmaBatch<OA, OB, EP> gb;
     memset((void*)&gb, 0, sizeof(gb));
     for (int i = 0; i < nprob; ++i) gb.prob[i] = probs[i];
@@ -420,20 +519,10 @@ void gemm_tma_launch(gorila_ctx* ctx, const TmaProb<OA, OB, EP>* probs, int npro
     gb.chunks_per_split = (nchunks + splits - 1) / splits;
     gb.splits = (nchunks + gb.chunks_per_split - 1) / gb.chunks_per_split;
     gb.cluster = 1;
-    static const int cluster_env = [] {
-        const char* e = getenv("GORILA_CLUSTER");
-        return e ? atoi(e) : 1;
-    }();
-    if (MB == 1 && cluster_target > 0 && cluster_env) {
-        const int tiles = tilesA * tilesB * nprob;
-        const int want = std::max(1, (cluster_target + tiles - 1) / tiles);
-        int cl = 1;
-        while (cl * 2 <= std::min(16, std::min(want, nchunks))) cl *= 2;
-        if (cl > 1) {
-            gb.cluster = cl;
-            gb.splits = cl;
-            gb.chunks_per_split = (nchunks + cl - 1) / cl;
-        }
+    if (cl > 1) {
+        gb.cluster = cl;
+        gb.splits = cl;
+        gb.chunks_per_split = (nchunks + cl - 1) / cl;
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = dim3(tilesA, tilesB, nprob * gb.splits);
@@ -759,9 +848,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         } else {
 #define FC4D(BN_)                                                                                              \
     {                                                                                                          \
-        using OA = OpMatMN<128>; using OB = OpMatKS<BN_>; using EP = EpMaskT<T>;                               \
+        using OA = OpMatMNS<128>; using OB = OpMatKS<BN_>; using EP = EpMaskT<T>;                              \
         TmaProb<OA, OB, EP> pr[1];                                                                             \
-        pr[0].a = op_matmn<128>(ctx, rt + RL.w4, FC4_OUT, FC4_IN, FC4_IN);                                     \
+        pr[0].a = op_matmns<128>(ctx, rt + RL.w4, FC4_OUT, FC4_IN, FC4_IN);                                    \
         pr[0].b = op_matks<BN_>(ctx, g4, B, FC4_OUT, FC4_OUT);                                                 \
         pr[0].ep = {g3, a3, FC4_IN, FC4_IN, B};                                                                \
         gemm_tma_launch<BN_, 1>(ctx, pr, 1, (FC4_IN + 127) / 128, (B + BN_ - 1) / BN_, FC4_OUT / 64, 1, 148, B); \
@@ -782,10 +871,10 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                                            {ctx->G + OFF_W4, FC4_IN, FC4_IN, FC4_OUT, accumulate}}};
             gemm<T, 64>(ctx, pr, 1, FC4_IN, FC4_OUT, B, 1);
         } else {
-            using OA = OpMatMN<128>; using OB = OpMatMN<64>; using EP = EpAddT;
+            using OA = OpMatMNS<128>; using OB = OpMatMNS<64>; using EP = EpAddT;
             TmaProb<OA, OB, EP> pr[1];
-            pr[0].a = op_matmn<128>(ctx, a3, B, FC4_IN, FC4_IN);
-            pr[0].b = op_matmn<64>(ctx, g4, B, FC4_OUT, FC4_OUT);
+            pr[0].a = op_matmns<128>(ctx, a3, B, FC4_IN, FC4_IN);
+            pr[0].b = op_matmns<64>(ctx, g4, B, FC4_OUT, FC4_OUT);
             pr[0].ep = {ctx->G + OFF_W4, FC4_IN, FC4_IN, FC4_OUT, accumulate};
             gemm_tma_launch<64, 1>(ctx, pr, 1, (FC4_IN + 127) / 128, FC4_OUT / 64, (B + 63) / 64, 1, 0, FC4_OUT);
         }
@@ -802,13 +891,13 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             GemmProb<LA, LB, EP> pr[1] = {{{g3, M}, {rt + RL.w3}, {g2, a2, C2_OUT, M, C2_OUT}}};
             gemm<T, 64>(ctx, pr, 1, M, C2_OUT, K3, 1, 148);
         } else {  // TMA: one sample (81 input pixels) per tile, shifted boxes with zero fill
-            using OA = OpDgradS<Conv3, 1>; using OB = OpWdgradMN<Conv3>; using EP = EpMask<T>;
+            using OA = OpDgradS<Conv3, 1>; using OB = OpWdgradMNS<Conv3>; using EP = EpMask<T>;
             TmaProb<OA, OB, EP> pr[1];
             pr[0].a.map = grad_map_sw<Conv3>(ctx, g3, B, H2, H2, 1);
             pr[0].a.nb = 1;
             pr[0].a.batch = B;
             pr[0].a.phase = -1;
-            pr[0].b.map = wdgrad_map<Conv3>(ctx, rt + RL.w3);
+            pr[0].b.map = wdgrad_map_sw<Conv3>(ctx, rt + RL.w3);
             pr[0].b.phase = -1;
             pr[0].ep = {g2, a2, C2_OUT, M, C2_OUT};
             gemm_tma_launch<64, 1>(ctx, pr, 1, B, 1, C3_K * C3_K, 1, 0, C2_OUT);
@@ -827,10 +916,10 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                                            {ctx->part_w[2], K3, (int64_t)C3_OUT * K3, 1.f, K3, C3_OUT}}};
             gemm<T, 64>(ctx, pr, 1, K3, C3_OUT, Mred, ctx->split_w[2]);
         } else {  // TMA: K-chunk = one sample's 49 pixels (64 rows, zero tail in the gradient operand)
-            using OA = OpWgradIn<Conv3, 64>; using OB = OpWgradOut<64, 64, false>; using EP = EpStoreT;
+            using OA = OpWgradInS<Conv3, 64>; using OB = OpWgradOutS<64, 64, false>; using EP = EpStoreT;
             TmaProb<OA, OB, EP> pr[1];
-            pr[0].a.map = nhwc_map<Conv3>(ctx, a2, B, H3, H3, 1, 8, 1);
-            pr[0].b = op_wgout<64, 64, false>(ctx, g3, H3 * H3, B);
+            pr[0].a.map = fwd_map_sw<Conv3>(ctx, a2, B, 1);
+            pr[0].b = op_wgout_s<64, 64, false>(ctx, g3, H3 * H3, B);
             pr[0].ep = {ctx->part_w[2], K3, (int64_t)C3_OUT * K3, 1.f, K3, C3_OUT};
             gemm_tma_launch<64, 1>(ctx, pr, 1, (K3 + 127) / 128, 1, B, ctx->split_w[2], 0, C3_OUT);
         }
@@ -847,14 +936,14 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             GemmProb<LA, LB, EP> pr[1] = {{{g2, M}, {rt + RL.w2}, {g1, a1, C1_OUT, M, C1_OUT}}};
             gemm<T, 32>(ctx, pr, 1, M, C1_OUT, Conv2::RD, 1, 296);
         } else {  // TMA: the stride-2 transpose as 4 phase problems of 2x2 taps (no zero taps)
-            using OA = OpDgradS<Conv2, 1>; using OB = OpWdgradMN<Conv2>; using EP = EpMask<T>;
+            using OA = OpDgradS<Conv2, 1>; using OB = OpWdgradMNS<Conv2>; using EP = EpMask<T>;
             TmaProb<OA, OB, EP> pr[4];
             for (int ph = 0; ph < 4; ++ph) {
                 pr[ph].a.map = grad_map_sw<Conv2>(ctx, g2, B, 10, 10, 1);
                 pr[ph].a.nb = 1;
                 pr[ph].a.batch = B;
                 pr[ph].a.phase = ph;
-                pr[ph].b.map = wdgrad_map<Conv2>(ctx, rt + RL.w2);
+                pr[ph].b.map = wdgrad_map_sw<Conv2>(ctx, rt + RL.w2);
                 pr[ph].b.phase = ph;
                 pr[ph].ep = {g1, a1, C1_OUT, M, C1_OUT};
             }
@@ -874,10 +963,10 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                                            {ctx->part_w[1], K2, (int64_t)C2_OUT * K2, 1.f, K2, C2_OUT}}};
             gemm<T, 64>(ctx, pr, 1, K2, C2_OUT, Mred, ctx->split_w[1]);
         } else {  // TMA: K-chunk = one sample's 81 pixels (96 rows, zero tail)
-            using OA = OpWgradIn<Conv2, 96>; using OB = OpWgradOut<64, 96, false>; using EP = EpStoreT;
+            using OA = OpWgradInS<Conv2, 96>; using OB = OpWgradOutS<64, 96, false>; using EP = EpStoreT;
             TmaProb<OA, OB, EP> pr[1];
-            pr[0].a.map = nhwc_map<Conv2>(ctx, a1, B, 2 * H2, 2 * H2, 1, 16, 2);
-            pr[0].b = op_wgout<64, 96, false>(ctx, g2, H2 * H2, B);
+            pr[0].a.map = fwd_map_sw<Conv2>(ctx, a1, B, 1);
+            pr[0].b = op_wgout_s<64, 96, false>(ctx, g2, H2 * H2, B);
             pr[0].ep = {ctx->part_w[1], K2, (int64_t)C2_OUT * K2, 1.f, K2, C2_OUT};
             gemm_tma_launch<64, 1>(ctx, pr, 1, K2 / 128, 1, B, ctx->split_w[1], 0, C2_OUT);
         }
@@ -895,10 +984,10 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                                            {ctx->part_w[0], K1, (int64_t)C1_OUT * K1, in_scale, K1, C1_OUT}}};
             gemm<T, 32>(ctx, pr, 1, K1, C1_OUT, Mred, ctx->split_w[0]);
         } else {  // TMA: K-chunk = 4 output rows (80 pixels) of one sample
-            using OA = OpWgradIn1; using OB = OpWgradOut<32, 80, true>; using EP = EpStoreT;
+            using OA = OpWgradIn1S; using OB = OpWgradOutS<32, 80, true>; using EP = EpStoreT;
             TmaProb<OA, OB, EP> pr[1];
-            pr[0].a.map = conv1_map(ctx, s, B, 4, 1);
-            pr[0].b = op_wgout<32, 80, true>(ctx, g1, H1 * H1, B);
+            pr[0].a.map = conv1_map_sw(ctx, s, B, 1, 4);
+            pr[0].b = op_wgout_s<32, 80, true>(ctx, g1, H1 * H1, B);
             pr[0].ep = {ctx->part_w[0], K1, (int64_t)C1_OUT * K1, in_scale, K1, C1_OUT};
             gemm_tma_launch<32, 1>(ctx, pr, 1, K1 / 128, 1, B * 5, ctx->split_w[0], 0, C1_OUT);
         }
@@ -1207,6 +1296,11 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
         ctx->pdl = !(e && atoi(e) == 0);
         const char* f = getenv("GORILA_FORK");  // GORILA_FORK=0 keeps the round on one stream
         ctx->fork = !(f && atoi(f) == 0);
+    }
+    {
+        int dev = 0;
+        CU(cudaGetDevice(&dev));
+        CU(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev));
     }
     CU(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     for (auto& e : ctx->ev_fork) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));

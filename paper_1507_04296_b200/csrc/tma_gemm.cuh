@@ -360,7 +360,116 @@ struct OpDgradS {
     }
 };
 
+// ---------------------------------------------------------------- swizzled MN-major operands
+// smem [MN block][K row][64 (32) elements]: 128-B (64-B) rows, one TMA box per MN block.
+
+// MN-major plain matrix X[Krows][MN]: map dims (MN, Krows), box (64, 64), SWIZZLE_128B;
+// tile = TR columns (TR/64 boxes), chunk = 64 K rows
+template <int TR>
+struct OpMatMNS {
+    static constexpr bool kMN = true, ZERO_ALL = false;
+    static constexpr int KC = 64, STAGE = TR * 128, WRITTEN = STAGE;
+    alignas(64) CUtensorMap map;
+    int mn;
+    GORILA_DEV uint32_t issue(int tile, int kc, uint32_t dst, uint64_t* bar) const {
+#pragma unroll
+        for (int h = 0; h < TR / 64; ++h) tma_load(&map, dst + h * 8192, bar, tile * TR + h * 64, kc * 64);
+        return TR * 128;
+    }
+    GORILA_DEV uint64_t desc(uint32_t base, int kk, int) const { return umma_desc_mn_sw(base + kk * 2048, 8192, 128); }
+    GORILA_DEV int row(int tile, int r) const {
+        const int i = tile * TR + r;
+        return (r < TR && i < mn) ? i : -1;
+    }
+};
+
+// conv dgrad weight operand, MN-major over c (N = C): chunk = one tap x 64 o.
+// map over W [CO][K][K][C]: dims (C, CO, K*K), strides (R*2, C*2), box (C, 64, 1) -> [o][C]
+template <class SH>
+struct OpWdgradMNS {
+    static constexpr bool kMN = true, ZERO_ALL = false;
+    static constexpr int RB = SH::C * 2;  // row bytes (128 or 64)
+    static constexpr int KC = 64, STAGE = 64 * RB, WRITTEN = STAGE;
+    alignas(64) CUtensorMap map;
+    int phase;
+    GORILA_DEV uint32_t issue(int, int kc, uint32_t dst, uint64_t* bar) const {
+        int t;
+        if (phase < 0) t = kc;
+        else t = ((phase >> 1) + 2 * (kc >> 1)) * SH::K + (phase & 1) + 2 * (kc & 1);
+        tma_load(&map, dst, bar, 0, 0, t);
+        return 64 * RB;
+    }
+    GORILA_DEV uint64_t desc(uint32_t base, int kk, int) const { return umma_desc_mn_sw(base + kk * 16 * RB, 0, RB); }
+};
+
+// conv2 / conv3 weight-gradient input operand, MN-major over r = (ky, kx, c), tile = 128 r =
+// two MN blocks of 64 (conv3: one tap each; conv2: two adjacent taps = pixels x, x+1 each);
+// chunk = the output pixels of one sample (KC = 64 / 96 rows; the tail rows stay zero and meet
+// zero rows of the gradient operand). Map as fwd_map_sw with NB = 1.
+template <class SH, int KC_>
+struct OpWgradInS {
+    static constexpr bool kMN = true, ZERO_ALL = true;
+    static constexpr int KC = KC_, NPIX = SH::OH * SH::OW, TPB = 64 / SH::C;  // taps per MN block
+    static constexpr int REG = KC * 128;                                      // bytes of one MN block
+    static constexpr int STAGE = 2 * REG, WRITTEN = STAGE;
+    alignas(64) CUtensorMap map;
+    GORILA_DEV uint32_t issue(int tile, int kc, uint32_t dst, uint64_t* bar) const {
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+            const int t = (tile * 2 + h) * TPB, ky = t / SH::K, kx = t - ky * SH::K;
+            tma_load(&map, dst + h * REG, bar, 0, kx, ky, kc);
+        }
+        return 2 * NPIX * 128;
+    }
+    GORILA_DEV uint64_t desc(uint32_t base, int kk, int) const { return umma_desc_mn_sw(base + kk * 2048, REG, 128); }
+    GORILA_DEV int row(int tile, int r) const {
+        const int i = tile * 128 + r;
+        return i < SH::R ? i : -1;
+    }
+};
+
+// conv1 weight-gradient input operand, MN-major over r = (ky, kx, c): tile = 4 kernel rows = 4
+// MN blocks of 32 (8 pixels x 4 channels, 64-B rows, SWIZZLE_64B); chunk = 4 output rows (80
+// pixels) of one sample. Map as conv1_map_sw with NB = 1 and a box of 4 output rows.
+struct OpWgradIn1S {
+    static constexpr bool kMN = true, ZERO_ALL = false;
+    static constexpr int KC = 80, REG = 80 * 64, STAGE = 4 * REG, WRITTEN = STAGE;
+    alignas(64) CUtensorMap map;
+    GORILA_DEV uint32_t issue(int tile, int kc, uint32_t dst, uint64_t* bar) const {
+        const int b = kc / 5, oy0 = (kc - b * 5) * 4;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) tma_load(&map, dst + u * REG, bar, 0, 0, 4 * oy0 + tile * 4 + u, b);
+        return 4 * REG;
+    }
+    GORILA_DEV uint64_t desc(uint32_t base, int kk, int) const { return umma_desc_mn_sw(base + kk * 1024, REG, 64); }
+    GORILA_DEV int row(int tile, int r) const {
+        const int i = tile * 128 + r;
+        return i < K1 ? i : -1;
+    }
+};
+
+// weight-gradient output-gradient operand g [B][NPIX][CO], MN-major over o (N = CO), rows of
+// CO*2 bytes (SWIZZLE_128B / 64B); per-sample chunks: dims (CO, NPIX, B), box (CO, KC, 1) (rows
+// past the sample zero filled); flat chunks (conv1): dims (CO, B*NPIX), box (CO, KC).
+template <int CO, int KC_, bool FLAT>
+struct OpWgradOutS {
+    static constexpr bool kMN = true, ZERO_ALL = false;
+    static constexpr int RB = CO * 2, KC = KC_, STAGE = KC * RB, WRITTEN = STAGE;
+    alignas(64) CUtensorMap map;
+    GORILA_DEV uint32_t issue(int, int kc, uint32_t dst, uint64_t* bar) const {
+        if (FLAT) tma_load(&map, dst, bar, 0, kc * KC);
+        else tma_load(&map, dst, bar, 0, 0, kc);
+        return KC * RB;
+    }
+    GORILA_DEV uint64_t desc(uint32_t base, int kk, int) const { return umma_desc_mn_sw(base + kk * 16 * RB, 0, RB); }
+};
+
 // ============================================================ the engine
+template <class O, class = void>
+struct zero_all : std::false_type {};
+template <class O>
+struct zero_all<O, std::void_t<decltype(O::ZERO_ALL)>> : std::integral_constant<bool, O::ZERO_ALL> {};
+
 template <class OA, class OB, class EP>
 struct TmaProb {
     OA a;
@@ -413,9 +522,9 @@ __global__ void __launch_bounds__(128) gemm_tma(const __grid_constant__ TmaBatch
     const int nK = max(0, min(p.nchunks, kc0 + p.chunks_per_split) - kc0);
 
     if (warp == 0) tmem_alloc(tmem_slot, CFG::TCOLS);
-    if (OA::WRITTEN < CFG::A_ST)  // zero the never-copied slack of the A stages (finite garbage only)
+    if (OA::WRITTEN < CFG::A_ST || zero_all<OA>::value)  // zero the never-copied rows of the A stages
         for (int s = 0; s < STAGES; ++s)
-            for (int o = OA::WRITTEN + tid * 16; o < CFG::A_ST; o += 128 * 16)
+            for (int o = (zero_all<OA>::value ? 0 : OA::WRITTEN) + tid * 16; o < CFG::A_ST; o += 128 * 16)
                 *reinterpret_cast<uint4*>(smem + s * (CFG::A_ST + CFG::B_ST) + o) = make_uint4(0, 0, 0, 0);
     fence_proxy_async_smem();
     if (tid == 32) {
@@ -561,6 +670,171 @@ __global__ void __launch_bounds__(128) gemm_tma(const __grid_constant__ TmaBatch
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, CFG::TCOLS);
     GTRACE(6);
+}
+
+// ============================================================ persistent engine
+// One CTA per SM slot loops over the tiles (prob, split, tb, ta) of the launch, ta fastest.
+// Warp 0: TMA producer (stage ring continues across tiles). Warp 1: MMA issuer into one of two
+// TMEM accumulators. Warps 2..5: epilogue (warp w reads TMEM lanes 32*(w%4)..): tile t's epilogue
+// overlaps tile t+1's loads and MMAs. No cluster reduction here (launches with cluster > 1 use
+// gemm_tma above).
+template <int BN, int MB, class OA, class OB>
+struct TmaPCfg {
+    static constexpr int A_ST = TmaCfg<BN, MB, OA, OB>::A_ST;
+    static constexpr int B_ST = TmaCfg<BN, MB, OA, OB>::B_ST;
+    static constexpr int BUDGET = 200 * 1024;
+    static constexpr int STAGES = (A_ST + B_ST) * 6 <= BUDGET   ? 6
+                                  : (A_ST + B_ST) * 4 <= BUDGET ? 4
+                                  : (A_ST + B_ST) * 3 <= BUDGET ? 3
+                                                                : 2;
+    static constexpr int SMEM = STAGES * (A_ST + B_ST) + 256 + 1024;
+    static constexpr uint32_t ACC = MB * BN;  // columns of one accumulator
+    static constexpr uint32_t TCOLS = tmem_cols_for(2 * MB * BN);
+    static_assert(2 * MB * BN <= 512, "TMEM columns");
+    static constexpr int THREADS = 192;
+};
+
+template <int BN, int MB, class OA, class OB, class EP>
+__global__ void __launch_bounds__(192) gemm_tma_p(const __grid_constant__ TmaBatch<OA, OB, EP> p, int tilesA,
+                                                  int tilesB, int nprob) {
+    using CFG = TmaPCfg<BN, MB, OA, OB>;
+    constexpr int STAGES = CFG::STAGES;
+    static_assert(OA::KC == OB::KC && OA::KC % 16 == 0, "chunk rows");
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw + CFG::SMEM - 256);
+    uint64_t* empty = full + STAGES;
+    uint64_t* acc_full = empty + STAGES;  // [2] MMA -> epilogue
+    uint64_t* acc_empty = acc_full + 2;   // [2] epilogue -> MMA
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int ntiles = tilesA * tilesB * nprob * p.splits;
+    if (warp == 0) tmem_alloc(tmem_slot, CFG::TCOLS);
+    if (OA::WRITTEN < CFG::A_ST || zero_all<OA>::value)  // zero the never-copied rows of the A stages
+        for (int s = 0; s < STAGES; ++s)
+            for (int o = (zero_all<OA>::value ? 0 : OA::WRITTEN) + tid * 16; o < CFG::A_ST; o += CFG::THREADS * 16)
+                *reinterpret_cast<uint4*>(smem + s * (CFG::A_ST + CFG::B_ST) + o) = make_uint4(0, 0, 0, 0);
+    fence_proxy_async_smem();
+    if (tid == 32) {
+        for (int s = 0; s < STAGES; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], 1);
+        }
+        for (int b = 0; b < 2; ++b) {
+            mbar_init(&acc_full[b], 1);
+            mbar_init(&acc_empty[b], 4);
+        }
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    pdl_wait();
+    pdl_trigger();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t sbase = smem_u32(smem);
+    constexpr uint32_t IDESC =
+        umma_idesc_bf16(TC_BM, BN) | (OA::kMN ? (1u << 15) : 0u) | (OB::kMN ? (1u << 16) : 0u);
+
+    // tile t -> (prob, split, tb, ta)
+    auto decode = [&](int t, int& prob, int& split, int& ta, int& tb) {
+        ta = t % tilesA;
+        t /= tilesA;
+        tb = t % tilesB;
+        t /= tilesB;
+        split = t % p.splits;
+        prob = t / p.splits;
+    };
+    auto chunks = [&](int split, int& kc0) {
+        kc0 = split * p.chunks_per_split;
+        return max(0, min(p.nchunks, kc0 + p.chunks_per_split) - kc0);
+    };
+
+    if (warp == 0) {
+        if (lane == 0) {  // TMA producer
+            uint32_t it = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+                int prob, split, ta, tb, kc0;
+                decode(t, prob, split, ta, tb);
+                const int nK = chunks(split, kc0);
+                const TmaProb<OA, OB, EP>& P = p.prob[prob];
+                for (int kc = 0; kc < nK; ++kc, ++it) {
+                    const int s = it % STAGES;
+                    if (it >= STAGES) mbar_wait(&empty[s], ((it / STAGES) - 1) & 1);
+                    const uint32_t a_dst = sbase + s * (CFG::A_ST + CFG::B_ST), b_dst = a_dst + CFG::A_ST;
+                    uint32_t bytes = P.a.issue(ta, kc0 + kc, a_dst, &full[s]);
+                    bytes += P.b.issue(tb, kc0 + kc, b_dst, &full[s]);
+                    mbar_expect_tx(&full[s], bytes);
+                }
+            }
+        }
+    } else if (warp == 1) {
+        if (lane == 0) {  // MMA issuer
+            uint32_t it = 0, tl = 0;
+            for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+                int prob, split, ta, tb, kc0;
+                decode(t, prob, split, ta, tb);
+                const int nK = chunks(split, kc0);
+                const TmaProb<OA, OB, EP>& P = p.prob[prob];
+                const uint32_t buf = tl & 1;
+                if (tl >= 2) mbar_wait(&acc_empty[buf], ((tl >> 1) - 1) & 1);
+                tc_fence_after();
+                const uint32_t acc = tmem + buf * CFG::ACC;
+                for (int kc = 0; kc < nK; ++kc, ++it) {
+                    const int s = it % STAGES;
+                    mbar_wait(&full[s], (it / STAGES) & 1);
+                    tc_fence_after();
+                    const uint32_t a_base = sbase + s * (CFG::A_ST + CFG::B_ST), b_base = a_base + CFG::A_ST;
+#pragma unroll
+                    for (int kk = 0; kk < OA::KC / 16; ++kk) {
+                        const uint64_t bd = P.b.desc(b_base, kk, 0);
+#pragma unroll
+                        for (int mb = 0; mb < MB; ++mb)
+                            umma_bf16(acc + mb * BN, P.a.desc(a_base, kk, mb), bd, IDESC,
+                                      (kc > 0 || kk > 0) ? 1u : 0u);
+                    }
+                    umma_commit(&empty[s]);
+                }
+                umma_commit(&acc_full[buf]);  // also arrives when the tile had no chunks
+            }
+        }
+    } else {  // epilogue warps 2..5
+        const int quad = warp & 3;
+        uint32_t tl = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            int prob, split, ta, tb, kc0;
+            decode(t, prob, split, ta, tb);
+            const int nK = chunks(split, kc0);
+            const TmaProb<OA, OB, EP>& P = p.prob[prob];
+            const EP ep = P.ep;
+            const uint32_t buf = tl & 1;
+            mbar_wait(&acc_full[buf], (tl >> 1) & 1);
+            tc_fence_after();
+            const uint32_t acc = tmem + buf * CFG::ACC + ((uint32_t)(quad * 32) << 16);
+#pragma unroll 1
+            for (int mb = 0; mb < MB; ++mb) {
+                const int i = P.a.row(ta, mb * 128 + quad * 32 + lane);
+#pragma unroll 1
+                for (int c0 = 0; c0 < BN; c0 += 16) {
+                    float v[16];
+                    if (nK > 0) {
+                        tmem_ld16(acc + (uint32_t)(mb * BN + c0), v);
+                    } else {
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] = 0.f;
+                    }
+                    if (i >= 0 && tb * BN + c0 < p.N) ep.apply16(i, tb * BN + c0, v, split);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[buf]);
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, CFG::TCOLS);
 }
 
 }  // namespace gorila
