@@ -227,6 +227,33 @@ struct EpMask {  // out[i][j] = round_T(v * 1[act[i][j] > 0])  (ReLU'(0) = 0, re
         const int64_t a = (int64_t)i * ld + j;
         out[a] = fromf<T>(tof(act[a]) > 0.f ? v : 0.f);
     }
+    // epilogue prefetch (issued ahead of the accumulator): the 16 activations of a row chunk
+    struct Pre {
+        uint4 q[sizeof(T)];
+    };
+    GORILA_DEV Pre prefetch(int i, int j0) const {
+        Pre p;
+        if (i < M && j0 + 16 <= N) {
+#pragma unroll
+            for (int u = 0; u < (int)sizeof(T); ++u) p.q[u] = reinterpret_cast<const uint4*>(act + (int64_t)i * ld + j0)[u];
+        } else {
+#pragma unroll
+            for (int u = 0; u < (int)sizeof(T); ++u) p.q[u] = make_uint4(0, 0, 0, 0);
+        }
+        return p;
+    }
+    GORILA_DEV void apply16p(int i, int j0, const float* v, const Pre& p, int s) const {
+        if (i >= M) return;
+        if (j0 + 16 <= N) {
+            float h[16], o[16];
+            load16<T>(reinterpret_cast<const T*>(p.q), h);
+#pragma unroll
+            for (int e = 0; e < 16; ++e) o[e] = h[e] > 0.f ? v[e] : 0.f;
+            store16<T>(out + (int64_t)i * ld + j0, o);
+        } else {
+            for (int e = 0; e < 16; ++e) apply1(i, j0 + e, v[e], s);
+        }
+    }
     GORILA_DEV void apply16(int i, int j0, const float* v, int s) const {
         if (i >= M) return;
         if (j0 + 16 <= N) {
@@ -251,6 +278,21 @@ struct EpMaskT {  // transposed: out[j][i] = round_T(v * 1[act[j][i] > 0])  (coa
         if (i >= M || j >= N) return;
         const int64_t a = (int64_t)j * ld + i;
         out[a] = fromf<T>(tof(act[a]) > 0.f ? v : 0.f);
+    }
+    struct Pre {
+        float h[16];
+    };
+    GORILA_DEV Pre prefetch(int i, int j0) const {
+        Pre p;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) p.h[e] = (i < M && j0 + e < N) ? tof(act[(int64_t)(j0 + e) * ld + i]) : 0.f;
+        return p;
+    }
+    GORILA_DEV void apply16p(int i, int j0, const float* v, const Pre& p, int) const {
+        if (i >= M) return;
+#pragma unroll
+        for (int e = 0; e < 16; ++e)
+            if (j0 + e < N) out[(int64_t)(j0 + e) * ld + i] = fromf<T>(p.h[e] > 0.f ? v[e] : 0.f);
     }
     GORILA_DEV void apply16(int i, int j0, const float* v, int) const {
         if (i >= M) return;
@@ -337,6 +379,24 @@ struct EpAddT {  // G[j*ld + i] (+)= v (fp32, transposed, coalesced across the w
 #pragma unroll
         for (int e = 0; e < 16; ++e)
             if (j0 + e < N) d[(int64_t)e * ld] = o[e] + v[e];
+    }
+};
+
+// prefetch interface: epilogues with a `Pre` type load their inputs ahead of the accumulator
+template <class EP, class = void>
+struct EpPre {
+    struct type {};
+    static GORILA_DEV type load(const EP&, int, int) { return {}; }
+    static GORILA_DEV void apply(const EP& ep, int i, int j0, const float* v, const type&, int s) {
+        ep.apply16(i, j0, v, s);
+    }
+};
+template <class EP>
+struct EpPre<EP, std::void_t<typename EP::Pre>> {
+    using type = typename EP::Pre;
+    static GORILA_DEV type load(const EP& ep, int i, int j0) { return ep.prefetch(i, j0); }
+    static GORILA_DEV void apply(const EP& ep, int i, int j0, const float* v, const type& p, int s) {
+        ep.apply16p(i, j0, v, p, s);
     }
 };
 

@@ -125,7 +125,8 @@ struct gorila_ctx {
     float* td_partial;  // [B][2] per-sample delta^2, |delta|
     int bias_chunks;
     float* part_w[3];  // conv wgrad partials
-    float* part_b;     // bias-gradient partials [4 layers][BIAS_CHUNKS][C]
+    float* part_b;     // bias-gradient partials [4 layers][C][BIAS_CHUNKS]
+    float* part5;      // fc5 weight + bias gradient partials [B/FC5_ROWS][nA*513]
     int split_w[3];
     float* tmp_canon;  // [P]
     float* tmp_int;    // [W*q]
@@ -153,6 +154,7 @@ struct gorila_ctx {
     std::map<std::vector<uint64_t>, CUtensorMap> tmaps;  // TMA descriptors, encoded once per (buffer, view)
     bool tma_failed = false;
     int num_sms = 148;
+    int fc4_normal_min = 256;  // batch from which fc4 runs with M = samples (GORILA_FC4_NORMAL_MIN)
     // side stream for the weight-gradient GEMMs, which are off the dgrad critical path
     // (a fork / join of the round; a graph captures it as parallel branches)
     cudaStream_t side = nullptr;
@@ -806,7 +808,19 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         }                                                                                                      \
         gemm_tma_launch<BN_, 1>(ctx, pr, 2, FC4_OUT / 128, (B + BN_ - 1) / BN_, FC4_IN / 64, 1, 148, B);      \
     }
-            DISPATCH_BN_BATCH(B, FC4F);
+            if (B >= ctx->fc4_normal_min) {  // large batch: M = samples, N = 512 outputs (row-major stores)
+                using OA = OpMatKS<128>; using OB = OpMatKS<128>; using EP = EpAct<float>;
+                TmaProb<OA, OB, EP> pr[2];
+                for (int z = 0; z < 2; ++z) {
+                    pr[z].a = op_matks<128>(ctx, z ? (const void*)t3 : (const void*)a3, B, FC4_IN, FC4_IN);
+                    pr[z].b = op_matks<128>(ctx, z ? (const void*)(tt + RT.w4) : (const void*)(rt + RL.w4), FC4_OUT,
+                                            FC4_IN, FC4_IN);
+                    pr[z].ep = {z ? t4 : a4, FC4_OUT, z ? tf + RT.b4 : rf + RL.b4, 1.f, B, FC4_OUT, 1};
+                }
+                gemm_tma_launch<128, 1>(ctx, pr, 2, (B + 127) / 128, FC4_OUT / 128, FC4_IN / 64, 1, 0, FC4_OUT);
+            } else {
+                DISPATCH_BN_BATCH(B, FC4F);
+            }
 #undef FC4F
         }
     }
@@ -832,8 +846,11 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     mark(ctx, PH_TD);
     PHASE(PH_FC5B) {
     // fc5 bwd: dW5, db5 into G; g4 = mask(dQ W5)
-    launch(ctx, k_fc5_bwd<T>, dim3(148), dim3(256), 0, (const float*)ctx->dQ, (const float*)a4,
-           (const float*)(rf + RL.w5), B, nA, ctx->G, g4, accumulate);
+    {
+        const int nch = (B + FC5_ROWS - 1) / FC5_ROWS;
+        launch(ctx, k_fc5_bwd<T>, dim3(2 * nch + std::min(2 * 148, (B * FC4_OUT + 255) / 256)), dim3(256), 0,
+               (const float*)ctx->dQ, (const float*)a4, (const float*)(rf + RL.w5), B, nA, ctx->part5, nch, g4);
+    }
     }
     mark(ctx, PH_FC5B);
     if (fk) fork_side(ctx, 0);  // g4 ready: fc4 wgrad may start
@@ -855,7 +872,16 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         pr[0].ep = {g3, a3, FC4_IN, FC4_IN, B};                                                                \
         gemm_tma_launch<BN_, 1>(ctx, pr, 1, (FC4_IN + 127) / 128, (B + BN_ - 1) / BN_, FC4_OUT / 64, 1, 148, B); \
     }
-            DISPATCH_BN_BATCH(B, FC4D);
+            if (B >= ctx->fc4_normal_min) {  // large batch: M = samples, N = 3136 (row-major masked stores)
+                using OA = OpMatKS<128>; using OB = OpMatMNS<256>; using EP = EpMask<T>;
+                TmaProb<OA, OB, EP> pr[1];
+                pr[0].a = op_matks<128>(ctx, g4, B, FC4_OUT, FC4_OUT);
+                pr[0].b = op_matmns<256>(ctx, rt + RL.w4, FC4_OUT, FC4_IN, FC4_IN);
+                pr[0].ep = {g3, a3, FC4_IN, B, FC4_IN};
+                gemm_tma_launch<256, 1>(ctx, pr, 1, (B + 127) / 128, (FC4_IN + 255) / 256, FC4_OUT / 64, 1, 0, FC4_IN);
+            } else {
+                DISPATCH_BN_BATCH(B, FC4D);
+            }
 #undef FC4D
         }
     }
@@ -1019,7 +1045,10 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             p.part[3 + l] = bp; p.splits[3 + l] = ctx->bias_chunks; p.count[3 + l] = bc[l]; p.off[3 + l] = boff[l];
             bp += (int64_t)ctx->bias_chunks * bc[l];
         }
-        p.nseg = 7;
+        p.part[7] = ctx->part5; p.splits[7] = (B + FC5_ROWS - 1) / FC5_ROWS;  // W5 and b5 (contiguous)
+        p.count[7] = (int64_t)nA * (FC4_OUT + 1); p.off[7] = OFF_W5;
+        for (int l = 3; l < 7; ++l) p.wide[l] = 1;
+        p.nseg = 8;
         p.accumulate = accumulate;
         launch(ctx, k_wgrad_reduce, dim3(148 * 2), dim3(256), 0, p, ctx->G);
     }
@@ -1130,6 +1159,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         part_w[l] = c.take<float>((int64_t)split_w[l] * wcount[l]);
     }
     float* part_b = c.take<float>((int64_t)bias_chunks * (C1_OUT + C2_OUT + C3_OUT + FC4_OUT));
+    float* part5 = c.take<float>((int64_t)((B + FC5_ROWS - 1) / FC5_ROWS) * nA * (FC4_OUT + 1));
     float* tmp_canon = c.take<float>(P);
     float* tmp_int = c.take<float>(W * q);
     if (ctx) {
@@ -1145,6 +1175,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         ctx->td_partial = td_partial; ctx->bias_chunks = bias_chunks;
         for (int l = 0; l < 3; ++l) { ctx->part_w[l] = part_w[l]; ctx->split_w[l] = split_w[l]; }
         ctx->part_b = part_b;
+        ctx->part5 = part5;
         ctx->tmp_canon = tmp_canon; ctx->tmp_int = tmp_int;
     }
     return c.off + 256;
@@ -1294,6 +1325,8 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     {
         const char* e = getenv("GORILA_PDL");  // GORILA_PDL=0 disables programmatic dependent launch
         ctx->pdl = !(e && atoi(e) == 0);
+        const char* fn = getenv("GORILA_FC4_NORMAL_MIN");
+        if (fn) ctx->fc4_normal_min = atoi(fn);
         const char* f = getenv("GORILA_FORK");  // GORILA_FORK=0 keeps the round on one stream
         ctx->fork = !(f && atoi(f) == 0);
     }

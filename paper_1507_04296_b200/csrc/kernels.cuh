@@ -283,29 +283,56 @@ __global__ void k_mark_not_ready(DevLearnerInfo* info, const LearnerStats* st) {
 // ------------------------------------------------------------------------- fc5 backward
 // dW5[a][n] += sum_b dQ[b][a] a4[b][n]; db5[a] += sum_b dQ[b][a];
 // g4[b][n] = round_T((sum_a dQ[b][a] W5[a][n]) * 1[a4[b][n] > 0])
+// Blocks [0, n_chunks): rows [c*FC5_ROWS, ...) of dW5[a][n] = sum_b dQ[b][a] a4[b][n] and
+// db5[a] = sum_b dQ[b][a] -> part[c][nA*512 + nA] (summed over c in fixed order by K10).
+// Remaining blocks: g4[b][n] = mask(sum_a dQ[b][a] W5[a][n]).
+constexpr int FC5_ROWS = 64;
 template <typename T>
-__global__ void k_fc5_bwd(const float* __restrict__ dQ, const float* __restrict__ a4, const float* __restrict__ w5,
-                          int B, int nA, float* __restrict__ G, T* __restrict__ g4, int accumulate) {
+__global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, const float* __restrict__ a4,
+                                                 const float* __restrict__ w5, int B, int nA, float* __restrict__ part,
+                                                 int n_chunks, T* __restrict__ g4) {
     pdl_wait();
     pdl_trigger();
-    const int n_w = nA * FC4_OUT, n_b = nA, n_g = B * FC4_OUT;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < n_w + n_b + n_g; e += gridDim.x * blockDim.x) {
-        if (e < n_w) {
-            int a = e / FC4_OUT, n = e - a * FC4_OUT;
-            float acc = 0.f;
-            for (int b = 0; b < B; ++b) acc = fmaf(dQ[b * nA + a], a4[(int64_t)b * FC4_OUT + n], acc);
-            G[OFF_W5 + e] = accumulate ? G[OFF_W5 + e] + acc : acc;
-        } else if (e < n_w + n_b) {
-            int a = e - n_w;
-            float acc = 0.f;
-            for (int b = 0; b < B; ++b) acc += dQ[b * nA + a];
-            G[off_b5(nA) + a] = accumulate ? G[off_b5(nA) + a] + acc : acc;
-        } else {
-            int f = e - n_w - n_b, b = f / FC4_OUT, n = f - b * FC4_OUT;
-            float acc = 0.f;
-            for (int a = 0; a < nA; ++a) acc = fmaf(dQ[b * nA + a], w5[a * FC4_OUT + n], acc);
-            g4[f] = fromf<T>(a4[f] > 0.f ? acc : 0.f);
+    if ((int)blockIdx.x < 2 * n_chunks) {  // (chunk, column half)
+        __shared__ float dq[FC5_ROWS * 32];
+        const int c = blockIdx.x >> 1, b0 = c * FC5_ROWS, nb = min(FC5_ROWS, B - b0);
+        const int n = threadIdx.x + 256 * (blockIdx.x & 1);
+        for (int i = threadIdx.x; i < nb * nA; i += 256) dq[i] = dQ[(int64_t)b0 * nA + i];
+        __syncthreads();
+        float acc[32];
+#pragma unroll
+        for (int a = 0; a < 32; ++a) acc[a] = 0.f;
+        const float* xs = a4 + (int64_t)b0 * FC4_OUT + n;
+        for (int bb = 0; bb < nb; bb += 8) {
+            float x[8];  // eight rows' loads in flight before the FMAs
+#pragma unroll
+            for (int u = 0; u < 8; ++u) x[u] = bb + u < nb ? xs[(int64_t)(bb + u) * FC4_OUT] : 0.f;
+#pragma unroll
+            for (int u = 0; u < 8; ++u) {
+                if (bb + u >= nb) break;
+                const float* q = dq + (bb + u) * nA;
+#pragma unroll
+                for (int a = 0; a < 32; ++a)
+                    if (a < nA) acc[a] = fmaf(q[a], x[u], acc[a]);
+            }
         }
+        float* out = part + (int64_t)c * nA * (FC4_OUT + 1);
+#pragma unroll
+        for (int a = 0; a < 32; ++a)
+            if (a < nA) out[a * FC4_OUT + n] = acc[a];
+        if ((blockIdx.x & 1) == 0 && (int)threadIdx.x < nA) {
+            float t = 0.f;
+            for (int b = 0; b < nb; ++b) t += dq[b * nA + threadIdx.x];
+            out[nA * FC4_OUT + threadIdx.x] = t;
+        }
+        return;
+    }
+    const int n_g = B * FC4_OUT, nblk = gridDim.x - 2 * n_chunks;
+    for (int f = (blockIdx.x - 2 * n_chunks) * blockDim.x + threadIdx.x; f < n_g; f += nblk * blockDim.x) {
+        const int b = f / FC4_OUT, n = f - b * FC4_OUT;
+        float acc = 0.f;
+        for (int a = 0; a < nA; ++a) acc = fmaf(dQ[b * nA + a], w5[a * FC4_OUT + n], acc);
+        g4[f] = fromf<T>(a4[f] > 0.f ? acc : 0.f);
     }
 }
 
@@ -349,28 +376,55 @@ __global__ void __launch_bounds__(256) k_bias_partial(const T* __restrict__ g1, 
         const int v = c / 8, k = c % 8;
         float t = 0.f;
         for (int q = 0; q < RG; ++q) t += red[(q * VPR + v) * 8 + k];
-        out[chunk * C + c] = t;
+        out[(int64_t)c * BIAS_CHUNKS + chunk] = t;  // [o][chunk]: K10 reads each bias's partials contiguously
     }
 }
 
 // ------------------------------------------------------------------------- K10 wgrad reduce
 // G[seg] (+)= sum_s partial_seg[s][.] in split order, for the conv weights and the four biases
+constexpr int WRED_SEGS = 8;
 struct WgradReduceParams {
-    const float* part[7];
-    int splits[7];
-    int64_t count[7];
-    int64_t off[7];
+    const float* part[WRED_SEGS];
+    int splits[WRED_SEGS];
+    int64_t count[WRED_SEGS];
+    int64_t off[WRED_SEGS];
+    int wide[WRED_SEGS];  // 1: partials stored [element][split] and summed by one warp per element
     int nseg, accumulate;
 };
 __global__ void k_wgrad_reduce(WgradReduceParams p, float* __restrict__ G) {
     pdl_wait();
     pdl_trigger();
-    int64_t total = 0;
-    for (int l = 0; l < p.nseg; ++l) total += p.count[l];
+    int64_t total = 0, total_w = 0;
+    for (int l = 0; l < p.nseg; ++l) (p.wide[l] ? total_w : total) += p.count[l];
+    // wide segments (many splits, few elements): a warp per element, lanes over the splits,
+    // fixed-order shuffle tree
+    const int64_t gw = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5, nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    for (int64_t e = gw; e < total_w; e += nw) {
+        int l = 0;
+        int64_t f = e;
+        while (!p.wide[l] || f >= p.count[l]) {
+            if (p.wide[l]) f -= p.count[l];
+            ++l;
+        }
+        const int S = p.splits[l];
+        const float* src = p.part[l] + f * S;
+        float acc = 0.f;
+        for (int s = lane; s < S; s += 32) acc += src[s];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+        if (lane == 0) {
+            float* dst = G + p.off[l] + f;
+            *dst = p.accumulate ? *dst + acc : acc;
+        }
+    }
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
         int l = 0;
         int64_t f = e;
-        while (f >= p.count[l]) f -= p.count[l++];
+        while (p.wide[l] || f >= p.count[l]) {
+            if (!p.wide[l]) f -= p.count[l];
+            ++l;
+        }
         // 8 independent partial sums (all loads in flight), combined in a fixed order
         const float* src = p.part[l] + f;
         const int S = p.splits[l];

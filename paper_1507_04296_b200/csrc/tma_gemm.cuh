@@ -580,14 +580,22 @@ __global__ void __launch_bounds__(128) gemm_tma(const __grid_constant__ TmaBatch
     }
     __syncwarp();
     GTRACE(3);
+    // the functor is copied to registers once: indexed by the problem, its fields would otherwise
+    // be re-read from the parameter bank before every store (the compiler cannot rule out aliasing)
+    const EP ep = P.ep;
+    using PT = EpPre<EP>;
+    constexpr int NC = BN / 16, PD = NC < 4 ? NC : 4;  // epilogue prefetch distance (chunks)
+    typename PT::type pre[PD];
+    const int i0 = P.a.row(ta, warp * 32 + lane);
+    if (!(MB == 1 && p.cluster > 1))  // first chunks' epilogue inputs in flight during the main loop
+#pragma unroll
+        for (int d = 0; d < PD; ++d)
+            if (i0 >= 0) pre[d] = PT::load(ep, i0, tb * BN + d * 16);
     if (nK > 0) mbar_wait(done, 0);
     tc_fence_after();
     GTRACE(4);
 
     // ---------------------------------------------------------------- epilogue
-    // the functor is copied to registers once: indexed by the problem, its fields would otherwise
-    // be re-read from the parameter bank before every store (the compiler cannot rule out aliasing)
-    const EP ep = P.ep;
     if (MB == 1 && p.cluster > 1) {
         float* red = reinterpret_cast<float*>(smem);  // the stage ring is dead now
         const int lrow = warp * 32 + lane;
@@ -649,9 +657,14 @@ __global__ void __launch_bounds__(128) gemm_tma(const __grid_constant__ TmaBatch
 #pragma unroll 1
         for (int mb = 0; mb < MB; ++mb) {
             const int i = P.a.row(ta, mb * 128 + warp * 32 + lane);
+            if (mb > 0)
+#pragma unroll
+                for (int d = 0; d < PD; ++d)
+                    if (i >= 0) pre[d] = PT::load(ep, i, tb * BN + d * 16);
             GTRACE(16);
-#pragma unroll 1
-            for (int c0 = 0; c0 < BN; c0 += 16) {
+#pragma unroll
+            for (int c = 0; c < NC; ++c) {
+                const int c0 = c * 16;
                 float v[16];
                 if (nK > 0) {
                     tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)(mb * BN + c0), v);
@@ -659,8 +672,10 @@ __global__ void __launch_bounds__(128) gemm_tma(const __grid_constant__ TmaBatch
 #pragma unroll
                     for (int e = 0; e < 16; ++e) v[e] = 0.f;
                 }
+                const typename PT::type cur = pre[c % PD];
+                if (c + PD < NC && i >= 0) pre[c % PD] = PT::load(ep, i, tb * BN + c0 + PD * 16);
                 if (c0 < 64) GTRACE(17 + 2 * (c0 / 16));
-                if (i >= 0 && tb * BN + c0 < p.N) ep.apply16(i, tb * BN + c0, v, split);
+                if (i >= 0 && tb * BN + c0 < p.N) PT::apply(ep, i, tb * BN + c0, v, cur, split);
                 if (c0 < 64) GTRACE(18 + 2 * (c0 / 16));
             }
         }
@@ -808,15 +823,29 @@ __global__ void __launch_bounds__(192) gemm_tma_p(const __grid_constant__ TmaBat
             const int nK = chunks(split, kc0);
             const TmaProb<OA, OB, EP>& P = p.prob[prob];
             const EP ep = P.ep;
+            using PT = EpPre<EP>;
+            constexpr int NC = BN / 16, PD = NC < 4 ? NC : 4;  // epilogue prefetch distance (chunks)
+            typename PT::type pre[PD];
             const uint32_t buf = tl & 1;
+            {  // the first chunks' epilogue inputs are requested before the accumulator is ready
+                const int i = P.a.row(ta, quad * 32 + lane);
+#pragma unroll
+                for (int d = 0; d < PD; ++d)
+                    if (i >= 0) pre[d] = PT::load(ep, i, tb * BN + d * 16);
+            }
             mbar_wait(&acc_full[buf], (tl >> 1) & 1);
             tc_fence_after();
             const uint32_t acc = tmem + buf * CFG::ACC + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
             for (int mb = 0; mb < MB; ++mb) {
                 const int i = P.a.row(ta, mb * 128 + quad * 32 + lane);
-#pragma unroll 1
-                for (int c0 = 0; c0 < BN; c0 += 16) {
+                if (mb > 0)
+#pragma unroll
+                    for (int d = 0; d < PD; ++d)
+                        if (i >= 0) pre[d] = PT::load(ep, i, tb * BN + d * 16);
+#pragma unroll
+                for (int c = 0; c < NC; ++c) {
+                    const int c0 = c * 16;
                     float v[16];
                     if (nK > 0) {
                         tmem_ld16(acc + (uint32_t)(mb * BN + c0), v);
@@ -824,7 +853,9 @@ __global__ void __launch_bounds__(192) gemm_tma_p(const __grid_constant__ TmaBat
 #pragma unroll
                         for (int e = 0; e < 16; ++e) v[e] = 0.f;
                     }
-                    if (i >= 0 && tb * BN + c0 < p.N) ep.apply16(i, tb * BN + c0, v, split);
+                    const typename PT::type cur = pre[c % PD];
+                    if (c + PD < NC && i >= 0) pre[c % PD] = PT::load(ep, i, tb * BN + c0 + PD * 16);
+                    if (i >= 0 && tb * BN + c0 < p.N) PT::apply(ep, i, tb * BN + c0, v, cur, split);
                 }
             }
             tc_fence_before();

@@ -142,6 +142,22 @@ def test_learner_update_parity_ragged_shapes(math, nA, B):
 
 
 @pytest.mark.parametrize("math", ["fp32", "bf16"])
+@pytest.mark.parametrize("B,normal_min", [(300, None), (33, "1")])
+def test_learner_update_parity_large_batch_paths(math, B, normal_min, monkeypatch):
+    """Batch above the fc4 orientation switch (M = samples for fc4 fwd / dgrad) and above one
+    tile per SM (persistent engine, double-buffered accumulators); B = 33 with the switch forced
+    covers a ragged M tile in that orientation."""
+    if normal_min is not None:
+        monkeypatch.setenv("GORILA_FC4_NORMAL_MIN", normal_min)
+    nA = 18
+    g, orc = make_pair(nA=nA, B=B, C=4000, n_insert=4000, math=math, outlier_enabled=False)
+    teacher_force(g, orc)
+    th = orc.theta.copy()
+    gpu, res = run_round_both(g, orc, 0, [0])
+    _check_round(gpu, res, math, nA, [0], orc, {0: th})
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
 def test_multi_learner_staleness_outlier_and_sync(math):
     """3 learners on one rank, fixed-staleness schedule (history 3), poison rewards, target sync."""
     nA = 6
