@@ -847,7 +847,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     PHASE(PH_FC5B) {
     // fc5 bwd: dW5, db5 into G; g4 = mask(dQ W5)
     {
-        const int nch = (B + FC5_ROWS - 1) / FC5_ROWS;
+        const int nch = (B + fc5_rows(B) - 1) / fc5_rows(B);
         launch(ctx, k_fc5_bwd<T>, dim3(2 * nch + std::min(2 * 148, (B * FC4_OUT + 255) / 256)), dim3(256), 0,
                (const float*)ctx->dQ, (const float*)a4, (const float*)(rf + RL.w5), B, nA, ctx->part5, nch, g4);
     }
@@ -1045,7 +1045,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             p.part[3 + l] = bp; p.splits[3 + l] = ctx->bias_chunks; p.count[3 + l] = bc[l]; p.off[3 + l] = boff[l];
             bp += (int64_t)ctx->bias_chunks * bc[l];
         }
-        p.part[7] = ctx->part5; p.splits[7] = (B + FC5_ROWS - 1) / FC5_ROWS;  // W5 and b5 (contiguous)
+        p.part[7] = ctx->part5; p.splits[7] = (B + fc5_rows(B) - 1) / fc5_rows(B);  // W5 and b5 (contiguous)
         p.count[7] = (int64_t)nA * (FC4_OUT + 1); p.off[7] = OFF_W5;
         for (int l = 3; l < 7; ++l) p.wide[l] = 1;
         p.nseg = 8;
@@ -1159,7 +1159,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         part_w[l] = c.take<float>((int64_t)split_w[l] * wcount[l]);
     }
     float* part_b = c.take<float>((int64_t)bias_chunks * (C1_OUT + C2_OUT + C3_OUT + FC4_OUT));
-    float* part5 = c.take<float>((int64_t)((B + FC5_ROWS - 1) / FC5_ROWS) * nA * (FC4_OUT + 1));
+    float* part5 = c.take<float>((int64_t)((B + fc5_rows(B) - 1) / fc5_rows(B)) * nA * (FC4_OUT + 1));
     float* tmp_canon = c.take<float>(P);
     float* tmp_int = c.take<float>(W * q);
     if (ctx) {

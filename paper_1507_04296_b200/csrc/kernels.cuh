@@ -283,10 +283,14 @@ __global__ void k_mark_not_ready(DevLearnerInfo* info, const LearnerStats* st) {
 // ------------------------------------------------------------------------- fc5 backward
 // dW5[a][n] += sum_b dQ[b][a] a4[b][n]; db5[a] += sum_b dQ[b][a];
 // g4[b][n] = round_T((sum_a dQ[b][a] W5[a][n]) * 1[a4[b][n] > 0])
-// Blocks [0, n_chunks): rows [c*FC5_ROWS, ...) of dW5[a][n] = sum_b dQ[b][a] a4[b][n] and
+// Blocks [0, 2 n_chunks): rows [c*fc5_rows(B), ...) and one half of the columns of dW5[a][n] = sum_b dQ[b][a] a4[b][n] and
 // db5[a] = sum_b dQ[b][a] -> part[c][nA*512 + nA] (summed over c in fixed order by K10).
 // Remaining blocks: g4[b][n] = mask(sum_a dQ[b][a] W5[a][n]).
-constexpr int FC5_ROWS = 64;
+constexpr int FC5_ROWS_MAX = 64;
+// rows per chunk: small batches use short chunks (more blocks, one round of loads each)
+__host__ __device__ constexpr int fc5_rows(int B) {
+    return B / 64 < 8 ? 8 : B / 64 > FC5_ROWS_MAX ? FC5_ROWS_MAX : (B / 64 + 7) / 8 * 8;
+}
 template <typename T>
 __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, const float* __restrict__ a4,
                                                  const float* __restrict__ w5, int B, int nA, float* __restrict__ part,
@@ -294,8 +298,8 @@ __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, c
     pdl_wait();
     pdl_trigger();
     if ((int)blockIdx.x < 2 * n_chunks) {  // (chunk, column half)
-        __shared__ float dq[FC5_ROWS * 32];
-        const int c = blockIdx.x >> 1, b0 = c * FC5_ROWS, nb = min(FC5_ROWS, B - b0);
+        __shared__ float dq[FC5_ROWS_MAX * 32];
+        const int rows = fc5_rows(B), c = blockIdx.x >> 1, b0 = c * rows, nb = min(rows, B - b0);
         const int n = threadIdx.x + 256 * (blockIdx.x & 1);
         for (int i = threadIdx.x; i < nb * nA; i += 256) dq[i] = dQ[(int64_t)b0 * nA + i];
         __syncthreads();
