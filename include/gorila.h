@@ -214,6 +214,14 @@ GORILA_API gorila_status gorila_set_learner_state(gorila_ctx* ctx, int32_t learn
 GORILA_API gorila_status gorila_get_grad(gorila_ctx* ctx, float* g);
 /* Q and Q-hat [B][nA] of the last learner_step of local learner `learner`. */
 GORILA_API gorila_status gorila_get_q(gorila_ctx* ctx, int32_t learner, float* q, float* qhat);
+/* Intermediate tensors of the last learner step (diagnostics; the scratch is
+ * shared by the local learners, so this is the last learner that ran). which:
+ * 0 s, 1 a1, 2 a2, 3 a3 (NHWC [B][H][W][C], element type of the math mode:
+ * bf16 as uint16 or fp32), 4 a4 ([B][512] fp32), 5 g1, 6 g2, 7 g3, 8 g4 (the
+ * masked output gradients, same layouts / types as a1..a4 except g4 in the math
+ * type). bytes must equal the tensor size (GORILA_E_SHAPE otherwise); host is a
+ * host pointer; the call synchronises the library stream. */
+GORILA_API gorila_status gorila_get_activation(gorila_ctx* ctx, int32_t which, void* host, uint64_t bytes);
 /* Per-phase device timing (diagnostics for the roofline report). When enabled,
  * learner_step / ps_apply_shard / sync_target record a CUDA event after each
  * phase on the stream; gorila_profile_read synchronises, returns the summed

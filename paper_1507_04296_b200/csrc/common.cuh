@@ -211,11 +211,12 @@ GORILA_DEV uint64_t umma_desc(uint32_t saddr, uint32_t lbo, uint32_t sbo) {
     d |= (uint64_t)1 << 46;  // version
     return d;                // base_offset 0, lbo_mode 0, layout_type 0 (SWIZZLE_NONE)
 }
-// K-major swizzled layouts written by TMA with SWIZZLE_128B / SWIZZLE_64B: rows of 128 / 64 B,
-// 8-row atoms (SBO = 1024 / 512 B), K steps of 16 elements advance the start address by 32 B
-// inside the row; layout_type 2 = SWIZZLE_128B, 4 = SWIZZLE_64B (atoms 1024 / 512-B aligned).
+// K-major swizzled layouts written by TMA with SWIZZLE_128B / 64B / 32B: rows of 128 / 64 / 32 B,
+// 8-row atoms (SBO = 8 rows), K steps of 16 elements advance the start address by 32 B inside the
+// row; layout_type 2 / 4 / 6. The swizzle follows the absolute shared-memory address, so a start
+// address shifted by whole rows (not atoms) is valid with base offset 0 (tools/umma_shift_probe.cu).
 GORILA_DEV uint64_t umma_desc_sw(uint32_t saddr, uint32_t row_bytes) {
-    const uint64_t layout = row_bytes == 128 ? 2ull : 4ull;
+    const uint64_t layout = row_bytes == 128 ? 2ull : row_bytes == 64 ? 4ull : 6ull;  // 6: SWIZZLE_32B
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
     d |= (uint64_t)1 << 16;                            // LBO (unused for swizzled K-major)

@@ -25,6 +25,7 @@
 #include "kernels.cuh"
 #include "layout.cuh"
 #include "tma_gemm.cuh"
+#include "shift_gemm.cuh"
 
 using namespace gorila;
 
@@ -155,6 +156,10 @@ struct gorila_ctx {
     bool tma_failed = false;
     int num_sms = 148;
     int fc4_normal_min = 256;  // batch from which fc4 runs with M = samples (GORILA_FC4_NORMAL_MIN)
+    // shifted-window implicit GEMM per layer (bit 1 conv1 fwd, 2 conv2 fwd, 4 conv3 fwd, 8 conv3 dgrad,
+    // 16 conv2 dgrad; the forward layers only when there are more tiles than SMs);
+    // GORILA_SHIFT=<mask> selects, 0 = im2col boxes everywhere
+    int shift = 31;
     // side stream for the weight-gradient GEMMs, which are off the dgrad critical path
     // (a fork / join of the round; a graph captures it as parallel branches)
     cudaStream_t side = nullptr;
@@ -279,6 +284,7 @@ CUtensorMap tmap(gorila_ctx* ctx, const void* base, int rank, const uint64_t* di
                            CU_TENSOR_MAP_INTERLEAVE_NONE,
                            swizzle == 128  ? CU_TENSOR_MAP_SWIZZLE_128B
                            : swizzle == 64 ? CU_TENSOR_MAP_SWIZZLE_64B
+                           : swizzle == 32 ? CU_TENSOR_MAP_SWIZZLE_32B
                                            : CU_TENSOR_MAP_SWIZZLE_NONE,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE)
                      : CUDA_ERROR_NOT_INITIALIZED;
@@ -484,6 +490,77 @@ void gemm_tma_p_launch(gorila_ctx* ctx, const TmaProb<OA, OB, EP>* probs, int np
     cfg.numAttrs = na;
     cudaLaunchKernelEx(&cfg, gemm_tma_p<BN, MB, OA, OB, EP>, gb, tilesA, tilesB, nprob);
     ctx->launches++;
+}
+
+// shifted-window engine: one CTA per SM, A-buffer ring as deep as shared memory allows (2..4)
+template <int BN, int MB, class OA, class OB, class EP>
+void gemm_shift_launch(gorila_ctx* ctx, const ShiftProb<OA, OB, EP>* probs, int nprob, int N) {
+    using CFG = ShiftCfg<BN, MB, OA, OB>;
+    constexpr int SMEM_MAX = 227 * 1024;
+    int nbuf = SHIFT_MAX_BUF;
+    while (nbuf > 2 && CFG::smem(nprob, nbuf) > SMEM_MAX) --nbuf;
+    const int smem = CFG::smem(nprob, nbuf);
+    static bool attr_set = false;
+    if (!attr_set) {
+        cudaFuncSetAttribute(gemm_shift<BN, MB, OA, OB, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, SMEM_MAX);
+        attr_set = true;
+    }
+    ShiftBatch<OA, OB, EP> gb;
+    memset((void*)&gb, 0, sizeof(gb));
+    for (int i = 0; i < nprob; ++i) gb.prob[i] = probs[i];
+    gb.nprob = nprob;
+    gb.nbuf = nbuf;
+    gb.N = N;
+    const int tiles = probs[0].a.ntiles() * nprob;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(std::min(tiles, ctx->num_sms));
+    cfg.blockDim = dim3(CFG::THREADS);
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = ctx->stream;
+    cudaLaunchAttribute at[1];
+    int na = 0;
+    if (ctx->pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    cfg.attrs = at;
+    cfg.numAttrs = na;
+    cudaLaunchKernelEx(&cfg, gemm_shift<BN, MB, OA, OB, EP>, gb);
+    ctx->launches++;
+}
+// tensor maps of the shifted-window operands
+CUtensorMap sh_conv3_map(gorila_ctx* ctx, const void* a2, int B) {  // flat (64, B*81), box (64, 148)
+    const uint64_t dims[2] = {64, (uint64_t)B * 81}, str[1] = {128};
+    const uint32_t box[2] = {64, ShConv3Fwd::ROWS};
+    return tmap(ctx, a2, 2, dims, str, box, nullptr, 128);
+}
+template <class SH>  // output gradient (64, OW, OH, B), box (64, 11, 11, 1)
+CUtensorMap sh_grad_map(gorila_ctx* ctx, const void* g, int B) {
+    const uint64_t dims[4] = {64, (uint64_t)SH::OW, (uint64_t)SH::OH, (uint64_t)B};
+    const uint64_t str[3] = {128, (uint64_t)SH::OW * 128, (uint64_t)SH::OH * SH::OW * 128};
+    const uint32_t box[4] = {64, 11, 11, 1};
+    return tmap(ctx, g, 4, dims, str, box, nullptr, 128);
+}
+CUtensorMap sh_conv2_map(gorila_ctx* ctx, const void* a1, int B) {  // phase planes of a1 (64-B rows)
+    const uint64_t dims[4] = {32, 20, 20, (uint64_t)B};
+    const uint64_t str[3] = {64, 20 * 64, 400 * 64};
+    const uint32_t box[4] = {32, 20, 20, 1}, es[4] = {1, 2, 2, 1};
+    return tmap(ctx, a1, 4, dims, str, box, es, 64);
+}
+CUtensorMap sh_conv1_map(gorila_ctx* ctx, const void* s, int B) {  // row phases of s (32-B rows)
+    const uint64_t dims[4] = {16, 21, 84, (uint64_t)B};
+    const uint64_t str[3] = {32, 84 * 8, 84 * 84 * 8};
+    const uint32_t box[4] = {16, 21, 84, 1}, es[4] = {1, 1, 4, 1};
+    return tmap(ctx, s, 4, dims, str, box, es, 32);
+}
+template <int CO, int RB, int NCH, int KOFF>  // K-major weight [CO][Ktot], box (RB/2, CO)
+ShWeightK<CO, RB, NCH, KOFF> sh_wk(gorila_ctx* ctx, const void* w, int ktot) {
+    ShWeightK<CO, RB, NCH, KOFF> o;
+    const uint64_t dims[2] = {(uint64_t)ktot, CO}, str[1] = {(uint64_t)ktot * 2};
+    const uint32_t box[2] = {RB / 2, CO};
+    o.map = tmap(ctx, w, 2, dims, str, box, nullptr, RB);
+    return o;
 }
 
 // grid + launch of the TMA engine (cluster split-K when cluster_target > 0)
@@ -720,6 +797,21 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                 {{s, M}, {rt + RL.w1, K1, C1_OUT, K1}, {a1, C1_OUT, rf + RL.b1, in_scale, M, C1_OUT, 1}},
                 {{s2, M}, {tt + RT.w1, K1, C1_OUT, K1}, {t1, C1_OUT, tf + RT.b1, in_scale, M, C1_OUT, 1}}};
             gemm<T, 32>(ctx, pr, 2, M, C1_OUT, K1, 1);
+        } else if ((ctx->shift & 1) && 2 * B > ctx->num_sms) {  // shifted windows over the row phases of s
+#define SH_C1(MS_, MB_)                                                                                        \
+    {                                                                                                          \
+        using OA = ShConv1Fwd<MS_>; using OB = ShWeightK<32, 32, 16, 2>; using EP = EpAct<T>;                  \
+        ShiftProb<OA, OB, EP> pr[2];                                                                           \
+        for (int z = 0; z < 2; ++z) {                                                                          \
+            pr[z].a.map = sh_conv1_map(ctx, z ? (const void*)s2 : (const void*)s, B);                          \
+            pr[z].a.batch = B;                                                                                 \
+            pr[z].b = sh_wk<32, 32, 16, 2>(ctx, z ? (const void*)(tt + RT.w1) : (const void*)(rt + RL.w1), K1); \
+            pr[z].ep = {z ? t1 : a1, C1_OUT, z ? tf + RT.b1 : rf + RL.b1, in_scale, M, C1_OUT, 1};             \
+        }                                                                                                      \
+        gemm_shift_launch<32, MB_>(ctx, pr, 2, C1_OUT);                                                        \
+    }
+            SH_C1(1, 4)
+#undef SH_C1
         } else {  // TMA: one sample (400 rows = 4 M-blocks) per tile, pixel-pair im2col boxes
             using OA = OpConv1FwdS<4>; using OB = OpMatKS<32>; using EP = EpAct<T>;
             TmaProb<OA, OB, EP> pr[2];
@@ -745,6 +837,16 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                 {{a1, M}, {rt + RL.w2, K2, C2_OUT, K2}, {a2, C2_OUT, rf + RL.b2, 1.f, M, C2_OUT, 1}},
                 {{t1, M}, {tt + RT.w2, K2, C2_OUT, K2}, {t2, C2_OUT, tf + RT.b2, 1.f, M, C2_OUT, 1}}};
             gemm<T, 64>(ctx, pr, 2, M, C2_OUT, K2, 1, 148);
+        } else if ((ctx->shift & 2) && 2 * B > ctx->num_sms) {  // shifted windows over the stride phases of a1
+            using OA = ShConv2Fwd; using OB = ShWeightK<64, 64, 16, 1>; using EP = EpAct<T>;
+            ShiftProb<OA, OB, EP> pr[2];
+            for (int z = 0; z < 2; ++z) {
+                pr[z].a.map = sh_conv2_map(ctx, z ? (const void*)t1 : (const void*)a1, B);
+                pr[z].a.batch = B;
+                pr[z].b = sh_wk<64, 64, 16, 1>(ctx, z ? (const void*)(tt + RT.w2) : (const void*)(rt + RL.w2), K2);
+                pr[z].ep = {z ? t2 : a2, C2_OUT, z ? tf + RT.b2 : rf + RL.b2, 1.f, M, C2_OUT, 1};
+            }
+            gemm_shift_launch<64, 1>(ctx, pr, 2, C2_OUT);
         } else {  // TMA: one sample (81 rows) per tile, stride-2 boxes; in-cluster split of K = 512
             using OA = OpConvFwdS<Conv2, 1>; using OB = OpMatKS<64>; using EP = EpAct<T>;
             TmaProb<OA, OB, EP> pr[2];
@@ -770,6 +872,16 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                 {{a2, M}, {rt + RL.w3, K3, C3_OUT, K3}, {a3, C3_OUT, rf + RL.b3, 1.f, M, C3_OUT, 1}},
                 {{t2, M}, {tt + RT.w3, K3, C3_OUT, K3}, {t3, C3_OUT, tf + RT.b3, 1.f, M, C3_OUT, 1}}};
             gemm<T, 64>(ctx, pr, 2, M, C3_OUT, K3, 1, 148);
+        } else if ((ctx->shift & 4) && 2 * B > ctx->num_sms) {  // shifted windows over the pixel rows of a2
+            using OA = ShConv3Fwd; using OB = ShWeightK<64, 128, 9, 0>; using EP = EpAct<T>;
+            ShiftProb<OA, OB, EP> pr[2];
+            for (int z = 0; z < 2; ++z) {
+                pr[z].a.map = sh_conv3_map(ctx, z ? (const void*)t2 : (const void*)a2, B);
+                pr[z].a.batch = B;
+                pr[z].b = sh_wk<64, 128, 9, 0>(ctx, z ? (const void*)(tt + RT.w3) : (const void*)(rt + RL.w3), K3);
+                pr[z].ep = {z ? t3 : a3, C3_OUT, z ? tf + RT.b3 : rf + RL.b3, 1.f, M, C3_OUT, 1};
+            }
+            gemm_shift_launch<64, 1>(ctx, pr, 2, C3_OUT);
         } else {  // TMA: two samples (98 rows) per tile, one tap per K-chunk
             using OA = OpConvFwdS<Conv3, 1>; using OB = OpMatKS<64>; using EP = EpAct<T>;
             TmaProb<OA, OB, EP> pr[2];
@@ -916,6 +1028,14 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             using LA = LdDgrad<T, Conv3>; using LB = LdWdgradMN<T, Conv3>; using EP = EpMask<T>;
             GemmProb<LA, LB, EP> pr[1] = {{{g3, M}, {rt + RL.w3}, {g2, a2, C2_OUT, M, C2_OUT}}};
             gemm<T, 64>(ctx, pr, 1, M, C2_OUT, K3, 1, 148);
+        } else if (ctx->shift & 8) {  // shifted windows over the zero-padded g3 of each sample
+            using OA = ShDgrad3; using OB = ShWeightDgrad<Conv3, false>; using EP = EpMask<T>;
+            ShiftProb<OA, OB, EP> pr[1];
+            pr[0].a.map = sh_grad_map<Conv3>(ctx, g3, B);
+            pr[0].a.batch = B;
+            pr[0].b.map = wdgrad_map_sw<Conv3>(ctx, rt + RL.w3);
+            pr[0].ep = {g2, a2, C2_OUT, M, C2_OUT};
+            gemm_shift_launch<64, 1>(ctx, pr, 1, C2_OUT);
         } else {  // TMA: one sample (81 input pixels) per tile, shifted boxes with zero fill
             using OA = OpDgradS<Conv3, 1>; using OB = OpWdgradMNS<Conv3>; using EP = EpMask<T>;
             TmaProb<OA, OB, EP> pr[1];
@@ -961,6 +1081,19 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             using LA = LdDgrad<T, Conv2>; using LB = LdWdgradMN<T, Conv2>; using EP = EpMask<T>;
             GemmProb<LA, LB, EP> pr[1] = {{{g2, M}, {rt + RL.w2}, {g1, a1, C1_OUT, M, C1_OUT}}};
             gemm<T, 32>(ctx, pr, 1, M, C1_OUT, Conv2::RD, 1, 296);
+        } else if (ctx->shift & 16) {  // the four output phases as M-blocks over one padded g2 per sample
+#define SH_D2(MS_, MB_)                                                                                        \
+    {                                                                                                          \
+        using OA = ShDgrad2<MS_>; using OB = ShWeightDgrad<Conv2, true>; using EP = EpMask<T>;                 \
+        ShiftProb<OA, OB, EP> pr[1];                                                                           \
+        pr[0].a.map = sh_grad_map<Conv2>(ctx, g2, B);                                                          \
+        pr[0].a.batch = B;                                                                                     \
+        pr[0].b.map = wdgrad_map_sw<Conv2>(ctx, rt + RL.w2);                                                   \
+        pr[0].ep = {g1, a1, C1_OUT, M, C1_OUT};                                                                \
+        gemm_shift_launch<32, MB_>(ctx, pr, 1, C1_OUT);                                                        \
+    }
+            if (B < ctx->num_sms) SH_D2(4, 1) else SH_D2(1, 4)  // few samples: one phase per tile
+#undef SH_D2
         } else {  // TMA: the stride-2 transpose as 4 phase problems of 2x2 taps (no zero taps)
             using OA = OpDgradS<Conv2, 1>; using OB = OpWdgradMNS<Conv2>; using EP = EpMask<T>;
             TmaProb<OA, OB, EP> pr[4];
@@ -1325,6 +1458,8 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     {
         const char* e = getenv("GORILA_PDL");  // GORILA_PDL=0 disables programmatic dependent launch
         ctx->pdl = !(e && atoi(e) == 0);
+        const char* sh = getenv("GORILA_SHIFT");
+        if (sh) ctx->shift = atoi(sh);
         const char* fn = getenv("GORILA_FC4_NORMAL_MIN");
         if (fn) ctx->fc4_normal_min = atoi(fn);
         const char* f = getenv("GORILA_FORK");  // GORILA_FORK=0 keeps the round on one stream
@@ -1842,6 +1977,29 @@ gorila_status gorila_get_grad(gorila_ctx* ctx, float* g) {
     ctx->launches++;
     CU(cudaMemcpyAsync(g, ctx->tmp_canon, sizeof(float) * ctx->P, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));
+    return GORILA_OK;
+}
+
+gorila_status gorila_get_activation(gorila_ctx* ctx, int32_t which, void* host, uint64_t bytes) {
+    if (!ctx || !host) return fail(GORILA_E_INVALID, "null argument");
+    const uint64_t B = ctx->B, e = ctx->esz;
+    const void* src = nullptr;
+    uint64_t n = 0;
+    switch (which) {
+        case 0: src = ctx->s; n = B * IMG * IMG * NSTACK * e; break;
+        case 1: src = ctx->a1; n = B * H1 * H1 * C1_OUT * e; break;
+        case 2: src = ctx->a2; n = B * H2 * H2 * C2_OUT * e; break;
+        case 3: src = ctx->a3; n = B * H3 * H3 * C3_OUT * e; break;
+        case 4: src = ctx->a4; n = B * FC4_OUT * 4; break;
+        case 5: src = ctx->g1; n = B * H1 * H1 * C1_OUT * e; break;
+        case 6: src = ctx->g2; n = B * H2 * H2 * C2_OUT * e; break;
+        case 7: src = ctx->g3; n = B * H3 * H3 * C3_OUT * e; break;
+        case 8: src = ctx->g4; n = B * FC4_OUT * e; break;
+        default: return fail(GORILA_E_RANGE, "which must be in [0, 8]");
+    }
+    if (bytes != n) return fail(GORILA_E_SHAPE, "bytes must be " + std::to_string(n));
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaMemcpy(host, src, n, cudaMemcpyDeviceToHost));
     return GORILA_OK;
 }
 

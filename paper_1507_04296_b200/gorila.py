@@ -60,7 +60,7 @@ class RoundInfo(ctypes.Structure):
 EXPORTS = ["gorila_param_count", "gorila_workspace_bytes", "gorila_init", "gorila_destroy", "gorila_last_error",
            "replay_insert", "replay_sample", "learner_step", "ps_apply_shard", "sync_target", "gorila_get_state",
            "gorila_set_state", "gorila_get_learner_state", "gorila_set_learner_state", "gorila_get_grad",
-           "gorila_get_q", "gorila_kernel_launches", "gorila_profile_enable", "gorila_profile_read",
+           "gorila_get_q", "gorila_get_activation", "gorila_kernel_launches", "gorila_profile_enable", "gorila_profile_read",
            "gorila_profile_phase_count", "gorila_profile_phase_name", "gorila_nccl_unique_id", "gorila_round",
            "gorila_bench_phase", "gorila_debug_trace"]
 
@@ -95,6 +95,7 @@ def load(build_if_missing=True):
     L.gorila_set_learner_state.argtypes = [P, i32, P, P]
     L.gorila_get_grad.argtypes = [P, P]
     L.gorila_get_q.argtypes = [P, i32, P, P]
+    L.gorila_get_activation.argtypes = [P, i32, P, u64]
     L.gorila_kernel_launches.argtypes = [P]
     L.gorila_kernel_launches.restype = u64
     L.gorila_profile_enable.argtypes = [P, i32]
@@ -158,6 +159,7 @@ class Gorila:
         # a dedicated stream by default (the legacy default stream cannot be graph-captured)
         self.stream = stream if stream is not None else torch.cuda.Stream(self.device)
         self.n_actions, self.batch, self.L = n_actions, batch, n_learners_local
+        self.math = math
         self.P = param_count(n_actions)
         theta0 = np.ascontiguousarray(theta0, dtype=np.float32)
         assert theta0.shape == (self.P,)
@@ -305,6 +307,18 @@ class Gorila:
         qh = np.zeros_like(q)
         _check(load().gorila_get_q(self.h, learner, q.ctypes.data, qh.ctypes.data))
         return q, qh
+
+    _ACT = {"s": (0, (84, 84, 4)), "a1": (1, (20, 20, 32)), "a2": (2, (9, 9, 64)), "a3": (3, (7, 7, 64)),
+            "a4": (4, (512,)), "g1": (5, (20, 20, 32)), "g2": (6, (9, 9, 64)), "g3": (7, (7, 7, 64)),
+            "g4": (8, (512,))}
+
+    def get_activation(self, name):
+        """Intermediate tensor of the last learner step as float32 (bf16 mode values widened)."""
+        which, shp = self._ACT[name]
+        bf = self.math == "bf16" and name != "a4"
+        out = np.zeros((self.batch,) + shp, np.uint16 if bf else np.float32)
+        _check(load().gorila_get_activation(self.h, which, out.ctypes.data, out.nbytes))
+        return (out.astype(np.uint32) << 16).view(np.float32) if bf else out
 
     def kernel_launches(self):
         return int(load().gorila_kernel_launches(self.h))

@@ -85,11 +85,11 @@ def _check_round(gpu, res, math, nA, learners, orc=None, thetas=None):
         assert gi["base_version"] == oi["base_version"]
         if oi["accepted"]:
             G_ref += oi["G"]
-            if math == "fp32" and orc is not None and thetas is not None:
+            if orc is not None and thetas is not None:
                 s, _, _, _, _ = orc.learners[j].ring.gather(oi["tau"])
-                kink = max(kink, ambiguous_layer(thetas[j], s, nA))
+                kink = max(kink, ambiguous_layer(thetas[j], s, nA, mode="exact" if math == "fp32" else "bf16"))
     if np.any(G_ref):
-        relaxed = TOL["bf16"]["g"]
+        relaxed = tol["g_kink"]
         e_all = rel_l2(gpu["G"], G_ref)
         assert e_all <= (tol["g"] if kink == 0 else relaxed), ("G", e_all, kink)
         for name, e in per_tensor_rel_l2(gpu["G"], G_ref, nA).items():
