@@ -214,6 +214,30 @@ struct EpAct {  // out[i][j] = round_T(act(v * scale + bias[j]))   (ld % 8 == 0)
             for (int e = 0; e < 16; ++e) apply1(i, j0 + e, v[e], s);
         }
     }
+    // prefetch: the 16 biases of a column chunk, requested ahead of the accumulator
+    struct Pre {
+        float b[16];
+    };
+    GORILA_DEV Pre prefetch(int, int j0) const {
+        Pre p;
+#pragma unroll
+        for (int e = 0; e < 16; ++e) p.b[e] = j0 + e < N ? bias[j0 + e] : 0.f;
+        return p;
+    }
+    GORILA_DEV void apply16p(int i, int j0, const float* v, const Pre& p, int s) const {
+        if (i >= M) return;
+        if (j0 + 16 <= N) {
+            float o[16];
+#pragma unroll
+            for (int e = 0; e < 16; ++e) {
+                const float z = v[e] * scale + p.b[e];
+                o[e] = relu ? fmaxf(z, 0.f) : z;
+            }
+            store16<T>(out + (int64_t)i * ld + j0, o);
+        } else {
+            for (int e = 0; e < 16; ++e) apply1(i, j0 + e, v[e], s);
+        }
+    }
 };
 
 template <typename T>

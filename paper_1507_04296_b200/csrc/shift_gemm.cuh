@@ -160,7 +160,8 @@ struct ShConv1Fwd {
 
 // ---------------------------------------------------------------- B operands (resident weights)
 // Interface: kMN, CHUNK (bytes per chunk, multiple of 1024), NCH (chunks incl. M-block variants),
-// load(dst, bar) -> bytes (all chunks), desc(base, c, kk, mb).
+// load_chunk(ch, dst, bar) -> bytes, chunk_of(c, mb), desc0(base) (descriptor of the block start)
+// and off(c, kk, mb) (byte offset of a K step: a descriptor's address field is linear).
 
 // K-major weight [CO][Ktot] (conv forward): chunk c = the CO x (RB/2) block at K offset koff(c).
 // map (Ktot, CO), box (RB/2, CO), swizzle RB. KOFF: 0 = c*RB/2; 1 = conv2 phase chunks; 2 = conv1.
@@ -182,10 +183,9 @@ struct ShWeightK {
         tma_load(&map, dst, bar, koff(c), 0);
         return CO * RB;
     }
-    GORILA_DEV uint64_t desc(uint32_t base, int c, int kk, int) const {
-        return umma_desc_sw(base + c * CHUNK + kk * 32, RB);
-    }
-    GORILA_DEV int chunk_of(int c, int) const { return c; }
+    GORILA_DEV static uint64_t desc0(uint32_t base) { return umma_desc_sw(base, RB); }
+    GORILA_DEV static uint32_t off(int c, int kk, int) { return c * CHUNK + kk * 32; }
+    GORILA_DEV static int chunk_of(int c, int) { return c; }
 };
 
 // MN-major conv weight for the data gradient: W [CO=64][K][K][C] over c (N = C), chunk = one tap
@@ -205,10 +205,9 @@ struct ShWeightDgrad {
         tma_load(&map, dst, bar, 0, 0, tap(ch));
         return 64 * RB;
     }
-    GORILA_DEV int chunk_of(int c, int mb) const { return PHASED ? mb * 4 + c : c; }
-    GORILA_DEV uint64_t desc(uint32_t base, int c, int kk, int mb) const {
-        return umma_desc_mn_sw(base + chunk_of(c, mb) * CHUNK + kk * 16 * RB, 0, RB);
-    }
+    GORILA_DEV static int chunk_of(int c, int mb) { return PHASED ? mb * 4 + c : c; }
+    GORILA_DEV static uint64_t desc0(uint32_t base) { return umma_desc_mn_sw(base, 0, RB); }
+    GORILA_DEV static uint32_t off(int c, int kk, int mb) { return chunk_of(c, mb) * CHUNK + kk * 16 * RB; }
 };
 
 // ---------------------------------------------------------------- the engine
@@ -321,22 +320,22 @@ __global__ void __launch_bounds__(192) gemm_shift(const __grid_constant__ ShiftB
                 const uint32_t acc = tmem + abuf * CFG::ACC;
                 const uint32_t a0 = abase + buf * OA::BUF, b0 = bbase + prob * OB::NCH * OB::CHUNK;
                 const int m0 = P.a.mb0(t - prob * tiles_per);
-                for (int c = 0; c < OA::NCHUNK; ++c) {
+                const bool first = !(waited & (1u << prob));  // the problem's weights may still be landing
+                waited |= 1u << prob;
+                const uint64_t ad0 = umma_desc_sw(a0, OA::RB), bd0 = OB::desc0(b0);
 #pragma unroll
-                    for (int mb = 0; mb < MB; ++mb) {
-                        const int bc = P.b.chunk_of(c, m0 + mb);
-                        if (!(waited & (1u << (prob * SHIFT_MAX_BCH + bc)))) {  // weights land once
-                            mbar_wait(&b_full[prob * SHIFT_MAX_BCH + bc], 0);
-                            waited |= 1u << (prob * SHIFT_MAX_BCH + bc);
-                            tc_fence_after();
-                        }
+                for (int c = 0; c < OA::NCHUNK; ++c) {
+                    if (first) {
+#pragma unroll
+                        for (int mb = 0; mb < MB; ++mb) mbar_wait(&b_full[prob * SHIFT_MAX_BCH + OB::chunk_of(c, m0 + mb)], 0);
+                        tc_fence_after();
                     }
 #pragma unroll
                     for (int kk = 0; kk < OA::KSTEPS; ++kk)
 #pragma unroll
                         for (int mb = 0; mb < MB; ++mb)
-                            umma_bf16(acc + mb * BN, umma_desc_sw(P.a.addr(a0, c, m0 + mb) + kk * 32, OA::RB),
-                                      P.b.desc(b0, c, kk, m0 + mb), IDESC, (c > 0 || kk > 0) ? 1u : 0u);
+                            umma_bf16(acc + mb * BN, ad0 + ((P.a.addr(0, c, m0 + mb) + kk * 32) >> 4),
+                                      bd0 + (OB::off(c, kk, m0 + mb) >> 4), IDESC, (c > 0 || kk > 0) ? 1u : 0u);
                 }
                 umma_commit(&a_empty[buf]);
                 umma_commit(&acc_full[abuf]);
