@@ -562,17 +562,28 @@ __global__ void __launch_bounds__(128) gemm_tma(const __grid_constant__ TmaBatch
             GTRACE(8 + (kc & 7));
         }
     } else if (tid == 32) {  // MMA issuer
+        // a K step / M-block only moves a descriptor's start address: per stage one base
+        // descriptor plus these address-field deltas
+        constexpr int KS = OA::KC / 16;
+        uint32_t adl[KS][MB], bdl[KS];
+        const uint64_t a00 = P.a.desc(0, 0, 0), b00 = P.b.desc(0, 0, 0);
+#pragma unroll
+        for (int kk = 0; kk < KS; ++kk) {
+            bdl[kk] = (uint32_t)(P.b.desc(0, kk, 0) - b00);
+#pragma unroll
+            for (int mb = 0; mb < MB; ++mb) adl[kk][mb] = (uint32_t)(P.a.desc(0, kk, mb) - a00);
+        }
         for (int kc = 0; kc < nK; ++kc) {
             const int s = kc % STAGES;
             mbar_wait(&full[s], (kc / STAGES) & 1);
             tc_fence_after();
             const uint32_t a_base = sbase + s * (CFG::A_ST + CFG::B_ST), b_base = a_base + CFG::A_ST;
+            const uint64_t ad0 = P.a.desc(a_base, 0, 0), bd0 = P.b.desc(b_base, 0, 0);
 #pragma unroll
-            for (int kk = 0; kk < OA::KC / 16; ++kk) {
-                const uint64_t bd = P.b.desc(b_base, kk, 0);
+            for (int kk = 0; kk < KS; ++kk) {
 #pragma unroll
                 for (int mb = 0; mb < MB; ++mb)
-                    umma_bf16(tmem + mb * BN, P.a.desc(a_base, kk, mb), bd, IDESC, (kc > 0 || kk > 0) ? 1u : 0u);
+                    umma_bf16(tmem + mb * BN, ad0 + adl[kk][mb], bd0 + bdl[kk], IDESC, (kc > 0 || kk > 0) ? 1u : 0u);
             }
             umma_commit(&empty[s]);
         }
@@ -796,19 +807,27 @@ __global__ void __launch_bounds__(192) gemm_tma_p(const __grid_constant__ TmaBat
                 if (tl >= 2) mbar_wait(&acc_empty[buf], ((tl >> 1) - 1) & 1);
                 tc_fence_after();
                 const uint32_t acc = tmem + buf * CFG::ACC;
+                constexpr int KS = OA::KC / 16;  // descriptor deltas of the K steps / M-blocks
+                uint32_t adl[KS][MB], bdl[KS];
+                const uint64_t a00 = P.a.desc(0, 0, 0), b00 = P.b.desc(0, 0, 0);
+#pragma unroll
+                for (int kk = 0; kk < KS; ++kk) {
+                    bdl[kk] = (uint32_t)(P.b.desc(0, kk, 0) - b00);
+#pragma unroll
+                    for (int mb = 0; mb < MB; ++mb) adl[kk][mb] = (uint32_t)(P.a.desc(0, kk, mb) - a00);
+                }
                 for (int kc = 0; kc < nK; ++kc, ++it) {
                     const int s = it % STAGES;
                     mbar_wait(&full[s], (it / STAGES) & 1);
                     tc_fence_after();
                     const uint32_t a_base = sbase + s * (CFG::A_ST + CFG::B_ST), b_base = a_base + CFG::A_ST;
+                    const uint64_t ad0 = P.a.desc(a_base, 0, 0), bd0 = P.b.desc(b_base, 0, 0);
 #pragma unroll
-                    for (int kk = 0; kk < OA::KC / 16; ++kk) {
-                        const uint64_t bd = P.b.desc(b_base, kk, 0);
+                    for (int kk = 0; kk < KS; ++kk)
 #pragma unroll
                         for (int mb = 0; mb < MB; ++mb)
-                            umma_bf16(acc + mb * BN, P.a.desc(a_base, kk, mb), bd, IDESC,
+                            umma_bf16(acc + mb * BN, ad0 + adl[kk][mb], bd0 + bdl[kk], IDESC,
                                       (kc > 0 || kk > 0) ? 1u : 0u);
-                    }
                     umma_commit(&empty[s]);
                 }
                 umma_commit(&acc_full[buf]);  // also arrives when the tile had no chunks
