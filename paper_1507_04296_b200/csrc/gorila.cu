@@ -155,6 +155,20 @@ struct gorila_ctx {
     std::map<std::vector<uint64_t>, CUtensorMap> tmaps;  // TMA descriptors, encoded once per (buffer, view)
     bool tma_failed = false;
     int num_sms = 148;
+    // fused PS exchange over NVLink peer memory (W > 1; CUDA IPC mappings of the peers' workspaces)
+    bool p2p = false;
+    uint8_t* ws_local = nullptr;
+    uint8_t* peer_ws[MAX_W] = {};   // peer q's workspace base in this process (nullptr for self)
+    void* peer_raw[MAX_W] = {};     // the opened IPC allocations (closed in gorila_destroy)
+    uint64_t* pflags = nullptr;     // [4 * MAX_W] ready / done flags (two phases) written by the peers
+    // gorila_round overlaps the exchange of the fc4 weight region (95% of theta) with the conv
+    // backward: phase 0 of the apply runs on side2 right after the last learner's fc4 wgrad
+    bool in_round = false, early_pending = false;
+    int early_learner = -1;
+    cudaStream_t side2 = nullptr;
+    cudaEvent_t ev_s2_fork = nullptr, ev_s2_join = nullptr;
+    uint64_t* p2p_epoch = nullptr;
+    unsigned int* p2p_counter = nullptr;
     int fc4_normal_min = 256;  // batch from which fc4 runs with M = samples (GORILA_FC4_NORMAL_MIN)
     // shifted-window implicit GEMM per layer (bit 1 conv1 fwd, 2 conv2 fwd, 4 conv3 fwd, 8 conv3 dgrad,
     // 16 conv2 dgrad; the forward layers only when there are more tiles than SMs);
@@ -166,6 +180,8 @@ struct gorila_ctx {
     cudaEvent_t ev_fork[4] = {}, ev_join = nullptr;
     bool fork = true;
 };
+
+extern "C" void early_apply_p2p(gorila_ctx* ctx, uint64_t round);  // defined with the PS calls below
 
 namespace {
 
@@ -213,6 +229,12 @@ struct OnSide {
         if (on) c->stream = c->side;
     }
     ~OnSide() { c->stream = saved; }
+};
+struct OnSide2 {
+    gorila_ctx* c;
+    cudaStream_t saved;
+    explicit OnSide2(gorila_ctx* c_) : c(c_), saved(c_->stream) { c->stream = c->side2; }
+    ~OnSide2() { c->stream = saved; }
 };
 
 // fold recorded marks into the per-phase accumulators (events must be complete)
@@ -1019,6 +1041,12 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }
     }
     mark(ctx, PH_FC4WG);
+    if (fk && j == ctx->early_learner) {  // this rank's fc4 weight gradient is complete on the side stream
+        cudaStream_t m = ctx->stream;
+        ctx->stream = ctx->side;
+        early_apply_p2p(ctx, round);
+        ctx->stream = m;
+    }
     if (fk) fork_side(ctx, 1);  // g3 ready (fc4 dgrad is on the main stream before this point)
     PHASE(PH_CONV3DG) {
     // conv3 dgrad: g2 = mask(conv3^T(g3))
@@ -1207,6 +1235,86 @@ gorila_status pack_any(gorila_ctx* ctx, const float* theta, void* rt, float* rf,
     return pack_replica<__nv_bfloat16>(ctx, theta, rt, rf, pred, vhist_dst);
 }
 
+// ---------------------------------------------------------------- NVLink peer mappings
+// Every rank maps every peer's workspace (same carve on every rank, so a peer's buffer is at the
+// same offset): IPC handle of the workspace's allocation + the workspace offset inside it,
+// exchanged with one NCCL all-gather. Any failure leaves p2p off (NCCL collectives are used).
+bool p2p_setup(gorila_ctx* ctx) {
+    typedef CUresult (*GetRange)(CUdeviceptr*, size_t*, CUdeviceptr);
+    static GetRange get_range = [] {
+        void* f = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuMemGetAddressRange", &f, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+            f = nullptr;
+        return reinterpret_cast<GetRange>(f);
+    }();
+    const int W = ctx->W, r = ctx->rank;
+    struct Rec {
+        cudaIpcMemHandle_t h;
+        uint64_t off;
+        int32_t ok, dev;
+        uint8_t pad[128 - sizeof(cudaIpcMemHandle_t) - 16];
+    };
+    static_assert(sizeof(Rec) == 128, "record size");
+    Rec mine;
+    memset(&mine, 0, sizeof(mine));
+    ctx->ws_local = (uint8_t*)ctx->cfg.workspace;
+    CUdeviceptr base = 0;
+    size_t size = 0;
+    mine.ok = get_range && get_range(&base, &size, (CUdeviceptr)ctx->ws_local) == CUDA_SUCCESS &&
+              cudaIpcGetMemHandle(&mine.h, (void*)base) == cudaSuccess;
+    cudaGetLastError();
+    mine.off = (uint64_t)((CUdeviceptr)ctx->ws_local - base);
+    cudaGetDevice(&mine.dev);
+    uint8_t* dbuf = reinterpret_cast<uint8_t*>(ctx->tmp_int);  // scratch: [W][128 B] records
+    if (cudaMemcpyAsync(dbuf + (size_t)r * 128, &mine, 128, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+        ncclAllGather(dbuf + (size_t)r * 128, dbuf, 128, ncclChar, ctx->comm, ctx->stream) != ncclSuccess)
+        return false;
+    std::vector<Rec> all(W);
+    if (cudaMemcpyAsync(all.data(), dbuf, (size_t)W * 128, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+        return false;
+    bool ok = true;
+    for (int q = 0; q < W; ++q) ok = ok && all[q].ok;
+    for (int q = 0; q < W && ok; ++q) {
+        if (q == r) continue;
+        void* p = nullptr;
+        if (cudaIpcOpenMemHandle(&p, all[q].h, cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            cudaGetLastError();
+            ok = false;
+            break;
+        }
+        ctx->peer_raw[q] = p;
+        ctx->peer_ws[q] = (uint8_t*)p + all[q].off;
+    }
+    // every rank must agree: all-reduce the verdict (min)
+    int32_t* vb = reinterpret_cast<int32_t*>(dbuf);
+    const int32_t v = ok ? 1 : 0;
+    if (cudaMemcpyAsync(vb, &v, 4, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+        ncclAllReduce(vb, vb, 1, ncclInt32, ncclMin, ctx->comm, ctx->stream) != ncclSuccess)
+        return false;
+    int32_t all_ok = 0;
+    cudaMemcpyAsync(&all_ok, vb, 4, cudaMemcpyDeviceToHost, ctx->stream);
+    cudaStreamSynchronize(ctx->stream);
+    if (!all_ok) {
+        for (int q = 0; q < MAX_W; ++q)
+            if (ctx->peer_raw[q]) {
+                cudaIpcCloseMemHandle(ctx->peer_raw[q]);
+                ctx->peer_raw[q] = nullptr;
+                ctx->peer_ws[q] = nullptr;
+            }
+        cudaGetLastError();
+    }
+    return all_ok != 0;
+}
+// rank q's copy of a workspace pointer
+template <typename P>
+P* peer_ptr(gorila_ctx* ctx, int q, P* local) {
+    if (q == ctx->rank) return local;
+    return reinterpret_cast<P*>(ctx->peer_ws[q] + ((uint8_t*)local - ctx->ws_local));
+}
+
 uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) {
     // computes the carve; if ctx != nullptr and base != nullptr fills the pointers
     const int nA = cfg->n_actions, B = cfg->batch, L = cfg->n_learners_local, W = cfg->world;
@@ -1228,6 +1336,9 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     uint64_t* Vhist = c.take<uint64_t>(H);
     uint64_t* dev_round = c.take<uint64_t>(1);
     unsigned int* head_counter = c.take<unsigned int>(1);
+    uint64_t* pflags = c.take<uint64_t>(4 * MAX_W);
+    uint64_t* p2p_epoch = c.take<uint64_t>(1);
+    unsigned int* p2p_counter = c.take<unsigned int>(2);
     std::vector<void*> rep_t(H);
     std::vector<float*> rep_f(H);
     for (int h = 0; h < H; ++h) {
@@ -1300,7 +1411,8 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         ctx->rl = rl; ctx->H = H;
         ctx->theta = theta; ctx->m = m; ctx->v = v; ctx->G = G; ctx->counts = counts; ctx->V = V;
         ctx->round_info = rinfo;
-        ctx->n_acc_local = nacc; ctx->Vhist = Vhist; ctx->dev_round = dev_round; ctx->head_counter = head_counter; ctx->rep_t = rep_t; ctx->rep_f = rep_f; ctx->learners = lrs;
+        ctx->n_acc_local = nacc; ctx->Vhist = Vhist; ctx->dev_round = dev_round; ctx->head_counter = head_counter;
+        ctx->pflags = pflags; ctx->p2p_epoch = p2p_epoch; ctx->p2p_counter = p2p_counter; ctx->rep_t = rep_t; ctx->rep_f = rep_f; ctx->learners = lrs;
         ctx->s = s; ctx->s2 = s2; ctx->a1 = a1; ctx->a2 = a2; ctx->a3 = a3; ctx->a4 = a4;
         ctx->t1 = t1; ctx->t2 = t2; ctx->t3 = t3; ctx->t4 = t4;
         ctx->g1 = g1; ctx->g2 = g2; ctx->g3 = g3; ctx->g4 = g4;
@@ -1454,6 +1566,9 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     CU(cudaMemsetAsync(ctx->Vhist, 0, sizeof(uint64_t) * ctx->H, st));
     CU(cudaMemsetAsync(ctx->head_counter, 0, sizeof(unsigned int), st));
     CU(cudaMemsetAsync(ctx->dev_round, 0, sizeof(uint64_t), st));
+    CU(cudaMemsetAsync(ctx->pflags, 0, sizeof(uint64_t) * 4 * MAX_W, st));
+    CU(cudaMemsetAsync(ctx->p2p_epoch, 0, sizeof(uint64_t), st));
+    CU(cudaMemsetAsync(ctx->p2p_counter, 0, sizeof(unsigned int) * 2, st));
     ctx->dev_round_expect = 0;
     {
         const char* e = getenv("GORILA_PDL");  // GORILA_PDL=0 disables programmatic dependent launch
@@ -1471,6 +1586,9 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
         CU(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev));
     }
     CU(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
+    CU(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
+    CU(cudaEventCreateWithFlags(&ctx->ev_s2_fork, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&ctx->ev_s2_join, cudaEventDisableTiming));
     for (auto& e : ctx->ev_fork) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
     for (auto& l : ctx->learners) {
@@ -1492,6 +1610,8 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
         ncclUniqueId id;
         memcpy(&id, cfg->nccl_unique_id, sizeof(id));
         NC(ncclCommInitRank(&ctx->comm, cfg->world, id, cfg->rank));
+        const char* pe = getenv("GORILA_P2P");  // GORILA_P2P=0: NCCL reduce-scatter / all-gather
+        if (!(pe && atoi(pe) == 0) && cfg->world <= MAX_W) ctx->p2p = p2p_setup(ctx);
     }
     CU(cudaStreamSynchronize(st));
     *out = ctx;
@@ -1509,9 +1629,17 @@ void gorila_destroy(gorila_ctx* ctx) {
     for (auto e : ctx->ev_fork)
         if (e) cudaEventDestroy(e);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->side2) {
+        cudaStreamSynchronize(ctx->side2);
+        cudaStreamDestroy(ctx->side2);
+    }
+    if (ctx->ev_s2_fork) cudaEventDestroy(ctx->ev_s2_fork);
+    if (ctx->ev_s2_join) cudaEventDestroy(ctx->ev_s2_join);
     for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : ctx->graph_marks)
         for (auto& m : kv.second) cudaEventDestroy(m.second);
+    for (int q = 0; q < MAX_W; ++q)
+        if (ctx->peer_raw[q]) cudaIpcCloseMemHandle(ctx->peer_raw[q]);
     if (ctx->comm) {
         if (ctx->poisoned) ncclCommAbort(ctx->comm);
         else ncclCommDestroy(ctx->comm);
@@ -1626,6 +1754,20 @@ gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
         ctx->dev_round_expect = round;
     }
     mark(ctx, PH_STEP_MISC);
+    ctx->early_learner = -1;
+    static const bool early_env = [] {
+        // GORILA_EARLY=1: overlap the fc4-region exchange with the conv backward (measured slower at
+        // N=2: 122 vs 118.5 us/step, so off by default)
+        const char* e = getenv("GORILA_EARLY");
+        return e && atoi(e) != 0;
+    }();
+    if (early_env && ctx->in_round && ctx->p2p && ctx->W > 1 && ctx->H >= 2 && ctx->fork && !ctx->prof &&
+        !ctx->early_pending)
+        for (int i = 0; i < n; ++i) {  // the last learner that runs
+            const Learner& l = ctx->learners[learners[i]];
+            const int64_t size = std::min<int64_t>(l.n_host, ctx->cfg.replay_capacity);
+            if (size - 1 >= std::max<int64_t>(1, ctx->cfg.min_replay)) ctx->early_learner = learners[i];
+        }
     int ran = 0;  // the first learner that runs stores G, later ones accumulate (no memset)
     for (int i = 0; i < n; ++i) {
         const int j = learners[i];
@@ -1656,6 +1798,111 @@ gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
     return GORILA_OK;
 }
 
+// W > 1 over peer memory: k_apply_p2p (gradient sum + optimizer + replica broadcast) and
+// k_peer_wait (everyone done) instead of reduce-scatter / apply / all-gather / pack
+void p2p_params(gorila_ctx* ctx, uint64_t round, ApplyParams& p, P2PParams& x) {
+    const int W = ctx->W, r = ctx->rank;
+    const int64_t lo = (int64_t)r * ctx->q;
+    const int slot = (int)((round + 1) % (uint64_t)ctx->H);
+    p = ApplyParams{};
+    p.m = ctx->m;
+    p.v = ctx->v;
+    p.dev_round = ctx->dev_round;
+    p.period = ctx->cfg.target_period;
+    if (ctx->fused_sync)
+        for (int i = 0; i < ctx->sync_n; ++i) {
+            p.sync_stats[p.n_sync] = ctx->learners[ctx->sync_ids[i]].stats;
+            p.sync_flag[p.n_sync] = ctx->learners[ctx->sync_ids[i]].sync_flag;
+            ++p.n_sync;
+        }
+    p.n_real = std::max<int64_t>(0, std::min<int64_t>(ctx->q, ctx->P - lo));
+    p.optimizer = ctx->cfg.optimizer;
+    p.lr = ctx->cfg.lr; p.rho = ctx->cfg.rms_rho; p.eps = ctx->cfg.rms_eps; p.ada_eps = ctx->cfg.ada_eps;
+    p.V = ctx->V;
+    p.round_info = ctx->round_info;
+    p.vhist_dst = ctx->Vhist + slot;
+    p.nA = ctx->nA;
+    p.base = lo;
+    x = P2PParams{};
+    x.W = W;
+    x.rank = r;
+    for (int q = 0; q < W; ++q) {
+        x.G[q] = peer_ptr(ctx, q, ctx->G) + lo;
+        x.nacc[q] = peer_ptr(ctx, q, ctx->n_acc_local);
+        x.theta[q] = peer_ptr(ctx, q, ctx->theta) + lo;
+        x.rep_t[q] = peer_ptr(ctx, q, (uint8_t*)ctx->rep_t[slot]);
+        x.rep_f[q] = peer_ptr(ctx, q, ctx->rep_f[slot]);
+        x.flags[q] = peer_ptr(ctx, q, ctx->pflags);
+    }
+    x.epoch = ctx->p2p_epoch;
+    x.counter = ctx->p2p_counter;
+}
+// the fc4 weight region of this rank's slice, float4 units relative to the slice start
+void w4_range(gorila_ctx* ctx, int64_t& a, int64_t& b) {
+    const int64_t lo = (int64_t)ctx->rank * ctx->q, n = std::max<int64_t>(0, std::min<int64_t>(ctx->q, ctx->P - lo));
+    a = std::min(n, std::max<int64_t>(0, OFF_W4 - lo));
+    b = std::min(n, std::max<int64_t>(0, OFF_W4 + (int64_t)FC4_OUT * FC4_IN - lo));
+    a = (a + 3) / 4;
+    b = (b + 3) / 4;
+    if (b < a) b = a;
+}
+void launch_apply_p2p(gorila_ctx* ctx, const ApplyParams& p, const P2PParams& x, int phase, int64_t lo0, int64_t hi0,
+                      int64_t lo1, int64_t hi1, int book, int blocks) {
+    if (ctx->cfg.math == GORILA_MATH_FP32)
+        launch(ctx, k_apply_p2p<float>, dim3(blocks), dim3(256), 0, p, x, phase, lo0, hi0, lo1, hi1, book);
+    else
+        launch(ctx, k_apply_p2p<__nv_bfloat16>, dim3(blocks), dim3(256), 0, p, x, phase, lo0, hi0, lo1, hi1, book);
+}
+// phase 0 (gorila_round): the fc4 weight part of the slice, on side2 once this rank's fc4
+// weight gradient (the last learner's) is in G
+void early_apply_p2p(gorila_ctx* ctx, uint64_t round) {
+    ApplyParams p;
+    P2PParams x;
+    p2p_params(ctx, round, p, x);
+    int64_t a, b;
+    w4_range(ctx, a, b);
+    cudaEventRecord(ctx->ev_s2_fork, ctx->stream);
+    cudaStreamWaitEvent(ctx->side2, ctx->ev_s2_fork, 0);
+    OnSide2 on(ctx);
+    launch_apply_p2p(ctx, p, x, 0, a, b, 0, 0, 0, 148);
+    ctx->early_pending = true;
+}
+
+gorila_status ps_apply_p2p(gorila_ctx* ctx, uint64_t round, gorila_round_info* info_out) {
+    ApplyParams p;
+    P2PParams x;
+    p2p_params(ctx, round, p, x);
+    const int64_t n4 = (p.n_real + 3) / 4;
+    const bool early = ctx->early_pending;
+    if (early) {  // the rest of the slice (at most two pieces around the fc4 weight region)
+        int64_t a, b;
+        w4_range(ctx, a, b);
+        launch_apply_p2p(ctx, p, x, 1, 0, a, b, n4, 1, 148 * 2);
+    } else {
+        launch_apply_p2p(ctx, p, x, 1, 0, n4, 0, 0, 1, 148 * 2);
+    }
+    ctx->dev_round_expect = round + 1;
+    mark(ctx, PH_APPLY);
+    if (early) {
+        cudaEventRecord(ctx->ev_s2_join, ctx->side2);
+        cudaStreamWaitEvent(ctx->stream, ctx->ev_s2_join, 0);
+        ctx->early_pending = false;
+    }
+    launch(ctx, k_peer_wait, dim3(1), dim3(32), 0, x, early ? 1 : 0);
+    mark(ctx, PH_AG);
+    if (info_out) {
+        uint64_t tmp[3];
+        CU(cudaMemcpyAsync(tmp, ctx->round_info, sizeof(tmp), cudaMemcpyDeviceToHost, ctx->stream));
+        CU(cudaStreamSynchronize(ctx->stream));
+        info_out->n_accepted = (uint32_t)tmp[0];
+        info_out->pad_ = 0;
+        info_out->version_before = tmp[1];
+        info_out->version_after = tmp[2];
+    }
+    CU(cudaGetLastError());
+    return GORILA_OK;
+}
+
 gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info* info_out) {
     if (!ctx) return fail(GORILA_E_INVALID, "null context");
     if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned");
@@ -1663,6 +1910,7 @@ gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info*
     const int W = ctx->W, r = ctx->rank;
     float* gsl = ctx->G + (int64_t)r * ctx->q;
     mark(ctx, -1);
+    if (W > 1 && ctx->p2p) return ps_apply_p2p(ctx, round, info_out);
     if (W > 1) {  // gradient + accepted counts onto the owning shard, one grouped launch
         NC(ncclGroupStart());
         NC(ncclReduceScatter(ctx->G, gsl, ctx->q, ncclFloat, ncclSum, ctx->comm, st));
@@ -1767,7 +2015,9 @@ gorila_status gorila_round(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
     key.push_back(ctx->prof ? 1 : 0);  // profiling graphs carry event-record nodes
     gorila_status s;
     auto eager = [&]() -> gorila_status {
+        ctx->in_round = true;
         gorila_status r = learner_step(ctx, learners, n, round, staleness, nullptr);
+        ctx->in_round = false;
         if (r != GORILA_OK) return r;
         ctx->fused_sync = n <= 8;  // k_apply takes the target-sync decisions (same predicate, R13)
         ctx->sync_n = n;

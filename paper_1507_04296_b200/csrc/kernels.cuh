@@ -548,6 +548,159 @@ __global__ void __launch_bounds__(256) k_apply(ApplyParams p) {
     }
 }
 
+// ------------------------------------------------------------------------- fused PS exchange (W > 1)
+// One kernel replaces reduce-scatter -> apply -> all-gather -> pack over NVLink peer memory (CUDA
+// IPC mappings of every rank's workspace): signal "my G is complete" into every peer's flag area,
+// wait for every peer's, then for this rank's shard slice sum the peers' gradient slices in rank
+// order (reading peer HBM through NVLink), apply the optimizer, and store the new theta slice and
+// its next-round replica chunk into every rank. The last block signals "done"; k_peer_wait holds
+// the stream until every peer is done (so no rank starts the next round while a peer still reads
+// its G / count or writes its replicas).
+constexpr int MAX_W = 8;
+GORILA_DEV void st_release_sys(uint64_t* p, uint64_t v) {
+    asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+GORILA_DEV uint64_t ld_acquire_sys(const uint64_t* p) {
+    uint64_t v;
+    asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+    return v;
+}
+// wait until a peer-written flag reaches ep; a peer that never arrives (protocol error, dead
+// rank) traps after ~2^25 polls (seconds) instead of hanging the device
+GORILA_DEV void wait_flag(const uint64_t* p, uint64_t ep) {
+    for (uint32_t n = 0; ld_acquire_sys(p) < ep; ++n) {
+        if (n > (1u << 25)) __trap();
+        __nanosleep(64);
+    }
+}
+struct P2PParams {
+    int W, rank;
+    const float* G[MAX_W];        // rank q's gradient buffer at this rank's slice
+    const uint32_t* nacc[MAX_W];  // rank q's accepted count of the round
+    float* theta[MAX_W];          // rank q's theta^+ at this rank's slice
+    void* rep_t[MAX_W];           // rank q's next-round replica (T area, fp32 area)
+    float* rep_f[MAX_W];
+    uint64_t* flags[MAX_W];       // rank q's flag area: phase f: [2f MAX_W, +MAX_W) ready, [(2f+1) MAX_W, ..) done
+    uint64_t* epoch;              // local round epoch (advanced by k_peer_wait)
+    unsigned int* counter;        // local: finished blocks, one counter per phase (phases may overlap)
+};
+
+template <typename T>
+GORILA_DEV void emit4_to(void* rep_t, float* rep_f, int nA, int64_t idx, const float* tv) {
+    const ReplicaLayout L = replica_layout(nA);
+    const int64_t slot = replica_slot(L, idx);
+    if (slot >= 0) {
+        T* dst = reinterpret_cast<T*>(rep_t) + slot;
+        if constexpr (sizeof(T) == 2) {
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(tv[0], tv[1]), h1 = __floats2bfloat162_rn(tv[2], tv[3]);
+            *reinterpret_cast<uint2*>(dst) =
+                make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+        } else {
+            *reinterpret_cast<float4*>(dst) = make_float4(tv[0], tv[1], tv[2], tv[3]);
+        }
+    } else {
+        *reinterpret_cast<float4*>(rep_f + (-slot - 1)) = make_float4(tv[0], tv[1], tv[2], tv[3]);
+    }
+}
+
+// phase: flag set (0 = the fc4 weight region, launched early by gorila_round; 1 = the rest);
+// [lo0, hi0) and [lo1, hi1): float4 ranges of the slice this launch updates; book: V, round
+// info, version history and sync decisions (the last phase only).
+template <typename T>
+__global__ void __launch_bounds__(256) k_apply_p2p(ApplyParams p, P2PParams x, int phase, int64_t lo0,
+                                                   int64_t hi0, int64_t lo1, int64_t hi1, int book) {
+    pdl_wait();
+    pdl_trigger();
+    const uint64_t ep = *x.epoch + 1;
+    const int RDY = 2 * phase * MAX_W, DONE = RDY + MAX_W;
+    uint64_t* mine = x.flags[x.rank];
+    if (blockIdx.x == 0 && (int)threadIdx.x < x.W)  // this rank's G range and count are complete
+        st_release_sys(x.flags[threadIdx.x] + RDY + x.rank, ep);
+    if (threadIdx.x == 0)
+        for (int q = 0; q < x.W; ++q)
+            wait_flag(mine + RDY + q, ep);
+    __syncthreads();
+    float cnt = 0.f;
+    for (int q = 0; q < x.W; ++q) cnt += (float)__ldcg(x.nacc[q]);
+    if (book && blockIdx.x == 0 && threadIdx.x == 0) {
+        const uint64_t v0 = *p.V;
+        const uint64_t n_acc = (uint64_t)(cnt + 0.5f);
+        p.round_info[0] = n_acc;
+        p.round_info[1] = v0;
+        p.round_info[2] = v0 + n_acc;
+        *p.V = v0 + n_acc;
+        if (p.vhist_dst) *p.vhist_dst = v0 + n_acc;
+        if (p.dev_round) *p.dev_round += 1;
+        for (int i = 0; i < p.n_sync; ++i) {
+            LearnerStats* st = p.sync_stats[i];
+            const bool doit = v0 + n_acc >= st->last_sync + (uint64_t)p.period;
+            if (doit) st->last_sync = v0 + n_acc;
+            *p.sync_flag[i] = doit;
+        }
+    }
+    const bool update = cnt > 0.5f;
+    const float inv = update ? 1.0f / cnt : 0.f;
+    float* th_local = x.theta[x.rank];
+    const int64_t len0 = hi0 - lo0, n = len0 + (hi1 - lo1);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t e = i < len0 ? lo0 + i : lo1 + (i - len0);
+        float4 th = reinterpret_cast<const float4*>(th_local)[e];
+        float tv[4] = {th.x, th.y, th.z, th.w};
+        if (update) {
+            float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
+            for (int q = 0; q < x.W; ++q) {  // fixed rank order
+                const float4 gq = __ldcg(reinterpret_cast<const float4*>(x.G[q]) + e);
+                g.x += gq.x; g.y += gq.y; g.z += gq.z; g.w += gq.w;
+            }
+            float4 m = reinterpret_cast<float4*>(p.m)[e];
+            float4 v = reinterpret_cast<float4*>(p.v)[e];
+            float gv[4] = {g.x * inv, g.y * inv, g.z * inv, g.w * inv};
+            float mv[4] = {m.x, m.y, m.z, m.w}, vv[4] = {v.x, v.y, v.z, v.w};
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                if (p.optimizer == 0) {
+                    mv[c] = p.rho * mv[c] + (1.f - p.rho) * gv[c];
+                    vv[c] = p.rho * vv[c] + (1.f - p.rho) * gv[c] * gv[c];
+                    tv[c] -= p.lr * gv[c] / sqrtf(vv[c] - mv[c] * mv[c] + p.eps);
+                } else {
+                    vv[c] += gv[c] * gv[c];
+                    tv[c] -= p.lr * gv[c] / (sqrtf(vv[c]) + p.ada_eps);
+                }
+            }
+            reinterpret_cast<float4*>(p.m)[e] = make_float4(mv[0], mv[1], mv[2], mv[3]);
+            reinterpret_cast<float4*>(p.v)[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+            const float4 t4 = make_float4(tv[0], tv[1], tv[2], tv[3]);
+            for (int q = 0; q < x.W; ++q) reinterpret_cast<float4*>(x.theta[q])[e] = t4;
+        }
+        for (int q = 0; q < x.W; ++q) emit4_to<T>(x.rep_t[q], x.rep_f[q], p.nA, p.base + 4 * e, tv);
+    }
+    // done: every block's peer stores are system-visible before the last block signals
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        unsigned int* ctr = x.counter + phase;
+        const unsigned int prev = atomicAdd(ctr, 1u);
+        if (prev == gridDim.x - 1) {
+            *ctr = 0;
+            __threadfence_system();
+            for (int q = 0; q < x.W; ++q) st_release_sys(x.flags[q] + DONE + x.rank, ep);
+        }
+    }
+}
+
+__global__ void k_peer_wait(P2PParams x, int phase0) {  // waits for phase 1 (and phase 0 if phase0)
+    pdl_wait();
+    pdl_trigger();
+    const uint64_t ep = *x.epoch + 1;
+    const uint64_t* mine = x.flags[x.rank];
+    if ((int)threadIdx.x < x.W) {
+        wait_flag(mine + 3 * MAX_W + threadIdx.x, ep);
+        if (phase0) wait_flag(mine + MAX_W + threadIdx.x, ep);
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) *x.epoch = ep;
+}
+
 // this rank's accepted count, once per destination shard (reduce-scattered with G)
 __global__ void k_write_counts(float* counts, int W, const uint32_t* n_acc_local) {
     pdl_wait();
