@@ -973,7 +973,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         t.outlier_enabled = cfg.outlier_enabled; t.outlier_warmup = cfg.outlier_warmup;
         t.outlier_k = cfg.outlier_k; t.outlier_beta = cfg.outlier_beta;
         p.per_sample = ctx->td_partial;
-        launch(ctx, k_fc5_td, dim3(B), dim3(256), 0, p);
+        launch(ctx, k_fc5_td, dim3(std::min(B, 2 * 148)), dim3(512), 0, p);
     }
     }
     mark(ctx, PH_FC5F);
@@ -1396,7 +1396,14 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
             split_w[l] = eff_splits(fp32, Mred[l], want);
         } else {  // TMA engine: chunks are 80-pixel rows (conv1) or whole samples (conv2, conv3)
             const int nch = l == 0 ? 5 * B : B, ta = l == 0 ? 2 : l == 1 ? 4 : 5;
-            const int want = std::max(1, std::min(nch, (148 + ta - 1) / ta));
+            static const int cap = [] {  // partials per weight (the critical-path reduce reads them all)
+                const char* e = getenv("GORILA_WSPLIT_MAX");
+                return e ? std::max(1, atoi(e)) : 16;
+            }();
+            // small batches: the weight-gradient GEMMs run beside the dgrad chain and can afford
+            // fewer, longer splits; large batches need every SM on them
+            const int lim = B <= 256 ? std::min(nch, cap) : nch;
+            const int want = std::max(1, std::min(lim, (148 + ta - 1) / ta));
             const int cps = (nch + want - 1) / want;
             split_w[l] = (nch + cps - 1) / cps;
         }

@@ -196,47 +196,64 @@ struct Fc5TdParams {
     float* per_sample;      // [B][2]
     TdParams td;
 };
-__global__ void __launch_bounds__(256) k_fc5_td(Fc5TdParams p) {
+// 16 warps: warps 0..7 the online net, 8..15 the target net; every operand of a warp's (up to
+// four) actions is requested before the first FMA (one memory round trip for the whole layer)
+__global__ void __launch_bounds__(512) k_fc5_td(Fc5TdParams p) {
     pdl_wait();
     pdl_trigger();
     const TdParams& t = p.td;
-    const int b = blockIdx.x, nA = t.nA;
+    const int nA = t.nA;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    __shared__ float q[2][32];
-    for (int z = 0; z < 2; ++z) {
+    const int z = warp >> 3, wz = warp & 7;
+    __shared__ float q[2][2][32];  // [sample parity][net][action]
+    // this warp's W5 rows stay in registers for all the block's samples
+    const float* w5 = z ? p.w5t : p.w5;
+    const float* b5 = z ? p.b5t : p.b5;
+    float wv[4][FC4_OUT / 32];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+        const int a = wz + 8 * u;
+#pragma unroll
+        for (int k = 0; k < FC4_OUT / 32; ++k) wv[u][k] = a < nA ? w5[a * FC4_OUT + lane + 32 * k] : 0.f;
+    }
+    int it = 0;
+    for (int b = blockIdx.x; b < t.B; b += gridDim.x, ++it) {
+        const int par = it & 1;
         const float* x = (z ? p.t4 : p.a4) + (int64_t)b * FC4_OUT;
-        const float* w5 = z ? p.w5t : p.w5;
-        const float* b5 = z ? p.b5t : p.b5;
         float xv[FC4_OUT / 32];
 #pragma unroll
         for (int k = 0; k < FC4_OUT / 32; ++k) xv[k] = x[lane + 32 * k];
-        for (int a = warp; a < nA; a += 8) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int a = wz + 8 * u;
+            if (a >= nA) break;
             float acc = 0.f;
 #pragma unroll
-            for (int k = 0; k < FC4_OUT / 32; ++k) acc = fmaf(xv[k], w5[a * FC4_OUT + lane + 32 * k], acc);
+            for (int k = 0; k < FC4_OUT / 32; ++k) acc = fmaf(xv[k], wv[u][k], acc);
             acc = warp_sum(acc);
-            if (lane == 0) q[z][a] = acc + b5[a];
+            if (lane == 0) q[par][z][a] = acc + b5[a];
         }
-    }
-    __syncthreads();
-    if (warp == 0) {
-        const float qv = lane < nA ? q[0][lane] : 0.f, qh = lane < nA ? q[1][lane] : -INFINITY;
-        if (lane < nA) {
-            const_cast<float*>(t.Q)[b * nA + lane] = qv;
-            const_cast<float*>(t.Qhat)[b * nA + lane] = q[1][lane];
+        __syncthreads();
+        if (warp == 0) {
+            const float qv = lane < nA ? q[par][0][lane] : 0.f, qh = lane < nA ? q[par][1][lane] : -INFINITY;
+            if (lane < nA) {
+                const_cast<float*>(t.Q)[b * nA + lane] = qv;
+                const_cast<float*>(t.Qhat)[b * nA + lane] = qh;
+            }
+            const float mx = warp_max(qh);
+            const int ab = t.a[b];
+            const float y = t.d[b] ? t.r[b] : t.r[b] + t.gamma * mx;  // Alg.1
+            const float delta = y - q[par][0][ab];
+            if (lane < nA) {
+                const float cl = fminf(fmaxf(delta, -1.f), 1.f);  // reading R3
+                t.dQ[b * nA + lane] = (lane == ab) ? -cl / (float)t.B : 0.f;
+            }
+            if (lane == 0) {
+                p.per_sample[2 * b] = delta * delta;
+                p.per_sample[2 * b + 1] = fabsf(delta);
+            }
         }
-        const float mx = warp_max(qh);
-        const int ab = t.a[b];
-        const float y = t.d[b] ? t.r[b] : t.r[b] + t.gamma * mx;  // Alg.1
-        const float delta = y - q[0][ab];
-        if (lane < nA) {
-            const float cl = fminf(fmaxf(delta, -1.f), 1.f);  // reading R3
-            t.dQ[b * nA + lane] = (lane == ab) ? -cl / (float)t.B : 0.f;
-        }
-        if (lane == 0) {
-            p.per_sample[2 * b] = delta * delta;
-            p.per_sample[2 * b + 1] = fabsf(delta);
-        }
+        // the next sample writes the other parity of q: one barrier per sample suffices
     }
     __shared__ unsigned int s_last;
     __threadfence();
@@ -246,7 +263,7 @@ __global__ void __launch_bounds__(256) k_fc5_td(Fc5TdParams p) {
     if (!s_last) return;
     __threadfence();
     // last block: fixed-order batch sums (8 interleaved partials, then in order), decisions
-    __shared__ float s_sq[8], s_ab[8];
+    __shared__ float s_sq[16], s_ab[16];
     __shared__ int s_keep;
     float sq = 0.f, sa = 0.f;
     for (int i = threadIdx.x; i < t.B; i += blockDim.x) {
@@ -261,7 +278,7 @@ __global__ void __launch_bounds__(256) k_fc5_td(Fc5TdParams p) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        s_keep = td_decide(t, s_sq, s_ab, 8);
+        s_keep = td_decide(t, s_sq, s_ab, 16);
         *p.counter = 0;
     }
     __syncthreads();
