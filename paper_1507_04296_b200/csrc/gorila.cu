@@ -1336,7 +1336,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     uint64_t* Vhist = c.take<uint64_t>(H);
     uint64_t* dev_round = c.take<uint64_t>(1);
     unsigned int* head_counter = c.take<unsigned int>(1);
-    uint64_t* pflags = c.take<uint64_t>(4 * MAX_W);
+    uint64_t* pflags = c.take<uint64_t>(5 * MAX_W);
     uint64_t* p2p_epoch = c.take<uint64_t>(1);
     unsigned int* p2p_counter = c.take<unsigned int>(2);
     std::vector<void*> rep_t(H);
@@ -1573,7 +1573,7 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     CU(cudaMemsetAsync(ctx->Vhist, 0, sizeof(uint64_t) * ctx->H, st));
     CU(cudaMemsetAsync(ctx->head_counter, 0, sizeof(unsigned int), st));
     CU(cudaMemsetAsync(ctx->dev_round, 0, sizeof(uint64_t), st));
-    CU(cudaMemsetAsync(ctx->pflags, 0, sizeof(uint64_t) * 4 * MAX_W, st));
+    CU(cudaMemsetAsync(ctx->pflags, 0, sizeof(uint64_t) * 5 * MAX_W, st));
     CU(cudaMemsetAsync(ctx->p2p_epoch, 0, sizeof(uint64_t), st));
     CU(cudaMemsetAsync(ctx->p2p_counter, 0, sizeof(unsigned int) * 2, st));
     ctx->dev_round_expect = 0;
@@ -1843,6 +1843,11 @@ void p2p_params(gorila_ctx* ctx, uint64_t round, ApplyParams& p, P2PParams& x) {
     }
     x.epoch = ctx->p2p_epoch;
     x.counter = ctx->p2p_counter;
+    static const int dbg = [] {
+        const char* e = getenv("GORILA_P2P_DBG");
+        return e ? atoi(e) : 0;
+    }();
+    x.dbg = dbg;
 }
 // the fc4 weight region of this rank's slice, float4 units relative to the slice start
 void w4_range(gorila_ctx* ctx, int64_t& a, int64_t& b) {
@@ -1991,7 +1996,15 @@ gorila_status sync_target(gorila_ctx* ctx, const int32_t* learners, int32_t n, i
         if (!ctx->fused_sync)  // gorila_round: k_apply already took the decision
             launch(ctx, k_sync_decide, dim3(1), dim3(1), 0, l.stats, (const uint64_t*)ctx->V,
                    (int64_t)ctx->cfg.target_period, (int)force, l.sync_flag);
-        if ((s = pack_any(ctx, ctx->theta, l.tminus_t, l.tminus_f, l.sync_flag, nullptr)) != GORILA_OK) return s;
+        if (ctx->p2p && ctx->W > 1) {  // ranks hold only their own fp32 slice: copy the latest replica
+            const int slot = (int)(ctx->dev_round_expect % (uint64_t)ctx->H);
+            const int64_t nt = (int64_t)ctx->rl.n_t * ctx->esz;
+            launch(ctx, k_copy_replica, dim3(148 * 2), dim3(256), 0, (const uint4*)ctx->rep_t[slot],
+                   (uint4*)l.tminus_t, nt / 16, (const float4*)ctx->rep_f[slot], (float4*)l.tminus_f,
+                   (int64_t)ctx->rl.n_f / 4, (const uint8_t*)l.sync_flag);
+        } else if ((s = pack_any(ctx, ctx->theta, l.tminus_t, l.tminus_f, l.sync_flag, nullptr)) != GORILA_OK) {
+            return s;
+        }
         if (synced_out) CU(cudaMemcpyAsync(&synced_out[i], l.sync_flag, 1, cudaMemcpyDeviceToHost, st));
     }
     mark(ctx, PH_SYNC);
@@ -2120,7 +2133,12 @@ gorila_status gorila_get_state(gorila_ctx* ctx, float* theta, float* m, float* v
         {ctx->theta, theta, true}, {ctx->m, m, false}, {ctx->v, v, false}};
     for (auto& it : items) {
         if (!it.dst) continue;
-        if (it.full) {
+        if (it.full && ctx->p2p && ctx->W > 1) {  // each rank holds only its own fp32 slice: gather them
+            CU(cudaStreamSynchronize(st));
+            for (int q = 0; q < ctx->W; ++q)
+                CU(cudaMemcpyAsync(ctx->tmp_int + (int64_t)q * ctx->q, peer_ptr(ctx, q, ctx->theta) + (int64_t)q * ctx->q,
+                                   sizeof(float) * ctx->q, cudaMemcpyDefault, st));
+        } else if (it.full) {
             CU(cudaMemcpyAsync(ctx->tmp_int, it.src_slice, sizeof(float) * ctx->W * ctx->q, cudaMemcpyDeviceToDevice, st));
         } else {  // own slice only; other slices zero
             CU(cudaMemsetAsync(ctx->tmp_int, 0, sizeof(float) * ctx->W * ctx->q, st));

@@ -584,6 +584,18 @@ GORILA_DEV uint64_t ld_acquire_sys(const uint64_t* p) {
 }
 // wait until a peer-written flag reaches ep; a peer that never arrives (protocol error, dead
 // rank) traps after ~2^25 polls (seconds) instead of hanging the device
+GORILA_DEV uint64_t gtimer() {
+    uint64_t t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+// trace build: accumulated ns of the exchange (slots 40..: wait-for-peers, work after the wait,
+// peer-done wait, rounds) — tools/trace_p2p.py
+#ifdef GORILA_TRACE
+#define P2PTRACE(slot, v) atomicAdd(&gorila_trace_buf[(slot)], (unsigned long long)(v))
+#else
+#define P2PTRACE(slot, v)
+#endif
 GORILA_DEV void wait_flag(const uint64_t* p, uint64_t ep) {
     for (uint32_t n = 0; ld_acquire_sys(p) < ep; ++n) {
         if (n > (1u << 25)) __trap();
@@ -597,9 +609,11 @@ struct P2PParams {
     float* theta[MAX_W];          // rank q's theta^+ at this rank's slice
     void* rep_t[MAX_W];           // rank q's next-round replica (T area, fp32 area)
     float* rep_f[MAX_W];
-    uint64_t* flags[MAX_W];       // rank q's flag area: phase f: [2f MAX_W, +MAX_W) ready, [(2f+1) MAX_W, ..) done
+    uint64_t* flags[MAX_W];       // rank q's flag area: phase f: [2f MAX_W, +MAX_W) ready, [(2f+1) MAX_W, ..) done;
+                                  // [4 MAX_W, 5 MAX_W): the ranks' accepted counts (sent with the ready flag)
     uint64_t* epoch;              // local round epoch (advanced by k_peer_wait)
     unsigned int* counter;        // local: finished blocks, one counter per phase (phases may overlap)
+    int dbg;                      // diagnostics (GORILA_P2P_DBG): 1 = skip peer gradient loads, 2 = skip peer replica stores
 };
 
 template <typename T>
@@ -630,15 +644,32 @@ __global__ void __launch_bounds__(256) k_apply_p2p(ApplyParams p, P2PParams x, i
     pdl_trigger();
     const uint64_t ep = *x.epoch + 1;
     const int RDY = 2 * phase * MAX_W, DONE = RDY + MAX_W;
+#ifdef GORILA_TRACE
+    const uint64_t t_in = gtimer();
+#endif
     uint64_t* mine = x.flags[x.rank];
-    if (blockIdx.x == 0 && (int)threadIdx.x < x.W)  // this rank's G range and count are complete
+    if (blockIdx.x == 0 && (int)threadIdx.x < x.W) {  // this rank's G range and count are complete
+        x.flags[threadIdx.x][4 * MAX_W + x.rank] = (uint64_t)*x.nacc[x.rank];  // ordered by the release
         st_release_sys(x.flags[threadIdx.x] + RDY + x.rank, ep);
-    if (threadIdx.x == 0)
-        for (int q = 0; q < x.W; ++q)
+    }
+    __shared__ float s_cnt;
+    if (threadIdx.x == 0) {
+        float c = 0.f;
+        for (int q = 0; q < x.W; ++q) {
             wait_flag(mine + RDY + q, ep);
+            c += (float)__ldcg(mine + 4 * MAX_W + q);  // local copy of rank q's count
+        }
+        s_cnt = c;
+    }
     __syncthreads();
-    float cnt = 0.f;
-    for (int q = 0; q < x.W; ++q) cnt += (float)__ldcg(x.nacc[q]);
+#ifdef GORILA_TRACE
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const uint64_t t = gtimer();
+        P2PTRACE(40, t - t_in);
+        gorila_trace_buf[47] = t;
+    }
+#endif
+    const float cnt = s_cnt;
     if (book && blockIdx.x == 0 && threadIdx.x == 0) {
         const uint64_t v0 = *p.V;
         const uint64_t n_acc = (uint64_t)(cnt + 0.5f);
@@ -664,11 +695,16 @@ __global__ void __launch_bounds__(256) k_apply_p2p(ApplyParams p, P2PParams x, i
         float4 th = reinterpret_cast<const float4*>(th_local)[e];
         float tv[4] = {th.x, th.y, th.z, th.w};
         if (update) {
+            float4 gq[MAX_W];  // every rank's slice element requested before the first add
+#pragma unroll
+            for (int q = 0; q < MAX_W; ++q)
+                if (q < x.W) gq[q] = __ldcg(reinterpret_cast<const float4*>(x.G[(x.dbg & 1) ? x.rank : q]) + e);
             float4 g = make_float4(0.f, 0.f, 0.f, 0.f);
-            for (int q = 0; q < x.W; ++q) {  // fixed rank order
-                const float4 gq = __ldcg(reinterpret_cast<const float4*>(x.G[q]) + e);
-                g.x += gq.x; g.y += gq.y; g.z += gq.z; g.w += gq.w;
-            }
+#pragma unroll
+            for (int q = 0; q < MAX_W; ++q)  // fixed rank order
+                if (q < x.W) {
+                    g.x += gq[q].x; g.y += gq[q].y; g.z += gq[q].z; g.w += gq[q].w;
+                }
             float4 m = reinterpret_cast<float4*>(p.m)[e];
             float4 v = reinterpret_cast<float4*>(p.v)[e];
             float gv[4] = {g.x * inv, g.y * inv, g.z * inv, g.w * inv};
@@ -686,22 +722,40 @@ __global__ void __launch_bounds__(256) k_apply_p2p(ApplyParams p, P2PParams x, i
             }
             reinterpret_cast<float4*>(p.m)[e] = make_float4(mv[0], mv[1], mv[2], mv[3]);
             reinterpret_cast<float4*>(p.v)[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
-            const float4 t4 = make_float4(tv[0], tv[1], tv[2], tv[3]);
-            for (int q = 0; q < x.W; ++q) reinterpret_cast<float4*>(x.theta[q])[e] = t4;
+            // the fp32 master stays with the owner; the peers get only the replica chunk
+            reinterpret_cast<float4*>(th_local)[e] = make_float4(tv[0], tv[1], tv[2], tv[3]);
         }
-        for (int q = 0; q < x.W; ++q) emit4_to<T>(x.rep_t[q], x.rep_f[q], p.nA, p.base + 4 * e, tv);
+        for (int q = 0; q < x.W; ++q)
+            if (!(x.dbg & 2) || q == x.rank) emit4_to<T>(x.rep_t[q], x.rep_f[q], p.nA, p.base + 4 * e, tv);
     }
-    // done: every block's peer stores are system-visible before the last block signals
-    __threadfence_system();
+    // done: a GPU-scope fence per block before the counter; the last block's system-scope
+    // fence then releases every block's peer stores (cumulativity) before the flag
     __syncthreads();
     if (threadIdx.x == 0) {
+        __threadfence();
         unsigned int* ctr = x.counter + phase;
         const unsigned int prev = atomicAdd(ctr, 1u);
         if (prev == gridDim.x - 1) {
             *ctr = 0;
+            P2PTRACE(41, gtimer() - gorila_trace_buf[47]);
+            __threadfence();
             __threadfence_system();
             for (int q = 0; q < x.W; ++q) st_release_sys(x.flags[q] + DONE + x.rank, ep);
         }
+    }
+}
+
+// target sync from the replica (peer-memory mode, where each rank holds only its own slice of
+// the fp32 theta^+): theta^- <- the replica the round just emitted, if *pred (R13)
+__global__ void k_copy_replica(const uint4* __restrict__ st, uint4* __restrict__ dt, int64_t nt16,
+                               const float4* __restrict__ sf, float4* __restrict__ df, int64_t nf4,
+                               const uint8_t* __restrict__ pred) {
+    pdl_wait();
+    pdl_trigger();
+    if (pred && !*pred) return;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nt16 + nf4; i += (int64_t)gridDim.x * blockDim.x) {
+        if (i < nt16) dt[i] = st[i];
+        else df[i - nt16] = sf[i - nt16];
     }
 }
 
@@ -710,12 +764,19 @@ __global__ void k_peer_wait(P2PParams x, int phase0) {  // waits for phase 1 (an
     pdl_trigger();
     const uint64_t ep = *x.epoch + 1;
     const uint64_t* mine = x.flags[x.rank];
+#ifdef GORILA_TRACE
+    const uint64_t t_in = gtimer();
+#endif
     if ((int)threadIdx.x < x.W) {
         wait_flag(mine + 3 * MAX_W + threadIdx.x, ep);
         if (phase0) wait_flag(mine + MAX_W + threadIdx.x, ep);
     }
     __syncthreads();
-    if (threadIdx.x == 0) *x.epoch = ep;
+    if (threadIdx.x == 0) {
+        *x.epoch = ep;
+        P2PTRACE(42, gtimer() - t_in);
+        P2PTRACE(43, 1);
+    }
 }
 
 // this rank's accepted count, once per destination shard (reduce-scattered with G)
