@@ -139,8 +139,10 @@ GORILA_API const char* gorila_last_error(void);
  * local replay; reading R14). frames: count*84*84 u8 (row-major 84x84 each,
  * "84x84" preprocessed luminance); actions u8 (< nA, else E_RANGE is
  * NOT checked on device data), rewards f32, terminals u8 (d_t = 1 iff s_{t+1}
- * is terminal, Alg.1). src_on_device != 0: all four are device pointers.
- * Host pointers are copied before the call returns. */
+ * is terminal, Alg.1). src_on_device != 0: all four are device pointers,
+ * read asynchronously on the library stream: the caller must not overwrite them
+ * until that stream has passed this call (order its own stream after ours, as
+ * the Python binding does). Host pointers are copied before the call returns. */
 GORILA_API gorila_status replay_insert(gorila_ctx* ctx, int32_t learner, int64_t count, const uint8_t* frames,
                             const uint8_t* actions, const float* rewards, const uint8_t* terminals,
                             int32_t src_on_device);

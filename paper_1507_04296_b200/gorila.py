@@ -206,6 +206,8 @@ class Gorila:
         rp, _ = _ptr(rewards)
         dp, _ = _ptr(terminals)
         _check(load().replay_insert(self.h, learner, count, fp, ap, rp, dp, int(dev)))
+        if dev:  # the copies read the sources on our stream: the caller's stream may reuse them after
+            self.torch.cuda.current_stream(self.device).wait_stream(self.stream)
 
     def replay_sample(self, learner, rnd):
         B = self.batch

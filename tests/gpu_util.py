@@ -88,6 +88,26 @@ def run_round_both(g, orc, k, learners, staleness=None):
     return gpu, res
 
 
+def round_bf16_vec(t):
+    """Vectorised oracle/oracle.c::orc_round_bf16 (frexp, 8 significant bits, ties to even)."""
+    m, e = np.frexp(np.asarray(t, np.float64))
+    return np.ldexp(np.rint(np.ldexp(m, 8)), e - 8)
+
+
+def replica_of(theta, nA, math):
+    """theta^- as the replica holds it: conv / fc4 weights bf16 in bf16 mode, the rest fp32 (R16)."""
+    out = np.asarray(theta, np.float64).copy()
+    if math != "bf16":
+        return out
+    off = 0
+    for name, shp in O.param_shapes(nA):
+        n = int(np.prod(shp))
+        if name in ("W1", "W2", "W3", "W4"):
+            out[off:off + n] = round_bf16_vec(out[off:off + n])
+        off += n
+    return out
+
+
 LAYER_OF = {"W1": 1, "b1": 1, "W2": 2, "b2": 2, "W3": 3, "b3": 3, "W4": 4, "b4": 4, "W5": 5, "b5": 5}
 
 
@@ -100,11 +120,8 @@ def ambiguous_layer(theta, s, nA, rel=1e-6, mode="exact"):
     p = O.unflatten(np.asarray(theta, np.float64), nA)
     bf = mode == "bf16"
 
-    def q(t):  # vectorised oracle/oracle.c::orc_round_bf16 (frexp, 8 significant bits, ties to even)
-        if not bf:
-            return t
-        m, e = np.frexp(t)
-        return np.ldexp(np.rint(np.ldexp(m, 8)), e - 8)
+    def q(t):
+        return round_bf16_vec(t) if bf else t
 
     if bf:  # oracle BF16 mode: bf16 weights and a1..a3, raw bytes into conv1, 1/255 (fp32) on its sum
         z1 = O.conv2d_fwd(s.astype(np.float64), q(p["W1"]), None, 4) * float(np.float32(1.0) / np.float32(255.0))
