@@ -126,7 +126,7 @@ def barrier(world):
         dist.barrier()
 
 
-def fill_replay(g, learner, capacity, n_actions, seed, learner_gid, chunk=131072):
+def fill_replay(g, learner, capacity, n_actions, seed, learner_gid, chunk=131072, p_poison=0.0):
     import torch
     import synth
     fr = torch.empty((chunk, 84, 84), dtype=torch.uint8, device="cuda")
@@ -138,7 +138,7 @@ def fill_replay(g, learner, capacity, n_actions, seed, learner_gid, chunk=131072
     while t < capacity:
         n = min(chunk, capacity - t)
         synth.fill_frames_dev(seed, learner_gid, t, n, fr.data_ptr(), st)
-        synth.fill_meta_dev(seed, learner_gid, t, n, n_actions, 0.0, a.data_ptr(), r.data_ptr(), d.data_ptr(), st)
+        synth.fill_meta_dev(seed, learner_gid, t, n, n_actions, p_poison, a.data_ptr(), r.data_ptr(), d.data_ptr(), st)
         g.replay_insert(learner, fr[:n], a[:n], r[:n], d[:n])
         t += n
     torch.cuda.synchronize()
@@ -210,10 +210,20 @@ def run_reference(args, json_out):
 
 
 def config_dict(args, world):
-    return {"workload": "configs[1]: 1 learner/GPU, |A|=18, batch 32, 1M-frame device replay, target sync every 100",
-            "n_actions": args.n_actions, "batch_per_learner": args.batch, "global_batch": args.batch * world,
+    if args.learners == 1 and args.batch == 32 and args.capacity == 1_000_000 and args.target_period == 100:
+        wl = "configs[1]: 1 learner/GPU, |A|=18, batch 32, 1M-frame device replay, target sync every 100"
+    elif args.learners > 1:
+        wl = (f"configs[4]-shaped: {args.learners} logical learners/GPU, batch {args.batch}, {args.capacity}-frame "
+              f"replay each, target sync every {args.target_period}, scheduled staleness {args.staleness}, "
+              f"max delay {args.max_staleness}, poison {args.poison}")
+    else:
+        wl = f"configs[3] sweep point: 1 learner/GPU, batch {args.batch}, {args.capacity}-frame replay"
+    return {"workload": wl,
+            "n_actions": args.n_actions, "batch_per_learner": args.batch, "learners_per_gpu": args.learners,
+            "global_batch": args.batch * world * args.learners,
             "replay_frames_per_learner": args.capacity, "target_period": args.target_period,
-            "ps_shards": world, "parallelism": f"dp{world} learners + {world}-way sharded PS (NCCL RS/AG)",
+            "ps_shards": world, "parallelism": f"dp{world} learners + {world}-way sharded PS "
+                                               f"({'NVLink peer-memory exchange' if world > 1 else 'local'})",
             "math": args.math, "l2": "inputs larger than L2: 7.06 GB replay per GPU (126 MB L2); the 27 MB "
                                      "parameter/optimizer state stays L2-resident across steps as in training"}
 
@@ -232,6 +242,10 @@ def main():
     ap.add_argument("--n-actions", type=int, default=18)
     ap.add_argument("--capacity", type=int, default=1_000_000)
     ap.add_argument("--target-period", type=int, default=100)
+    ap.add_argument("--learners", type=int, default=1, help="logical learners per GPU (configs[4]: 12-25)")
+    ap.add_argument("--staleness", type=int, default=0, help="scheduled staleness of every learner (rounds)")
+    ap.add_argument("--max-staleness", type=int, default=-1, help="discard threshold in versions (-1: off)")
+    ap.add_argument("--poison", type=float, default=0.0, help="probability of a 1e6 poison reward")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=200)
@@ -258,14 +272,18 @@ def main():
         uid = obj[0]
     stream = torch.cuda.Stream()
     torch.cuda.set_stream(stream)
-    g = Gorila(n_actions=args.n_actions, batch=args.batch, replay_capacity=args.capacity, n_learners_local=1,
-               learner_id_base=rank, rank=rank, world=world, nccl_unique_id=uid, stream=stream,
-               theta0=synth.theta0(args.n_actions), math=args.math, target_period=args.target_period, history=2)
-    fill_replay(g, 0, args.capacity, args.n_actions, synth.SEED_DATA, rank)
-    ids = np.array([0], np.int32)
+    L = args.learners
+    g = Gorila(n_actions=args.n_actions, batch=args.batch, replay_capacity=args.capacity, n_learners_local=L,
+               learner_id_base=rank * L, rank=rank, world=world, nccl_unique_id=uid, stream=stream,
+               theta0=synth.theta0(args.n_actions), math=args.math, target_period=args.target_period,
+               history=max(2, args.staleness + 1), max_staleness=args.max_staleness)
+    for j in range(L):
+        fill_replay(g, j, args.capacity, args.n_actions, synth.SEED_DATA, rank * L + j, p_poison=args.poison)
+    ids = np.arange(L, dtype=np.int32)
+    stal = np.full(L, args.staleness, np.int32) if args.staleness else None
 
     def step(k):
-        g.round(ids, k)  # learner_step + ps_apply_shard + sync_target, replayed as one CUDA graph
+        g.round(ids, k, stal)  # learner_step + ps_apply_shard + sync_target, replayed as one CUDA graph
 
     def step_eager(k):
         g.learner_step_async(ids, k)
@@ -295,7 +313,7 @@ def main():
     launches = g.kernel_launches() - launches0
     ms_local = ev0.elapsed_time(ev1)
     ms = max_over_ranks(ms_local, world)
-    value = world * args.steps / (ms / 1000.0)
+    value = world * L * args.steps / (ms / 1000.0)
 
     # ---------------- end to end through the public API with host buffers
     f1 = torch.empty((1, 84, 84), dtype=torch.uint8).pin_memory()
@@ -312,12 +330,12 @@ def main():
         f1.numpy()[0] = hf[i]
         a1.numpy()[0], r1.numpy()[0], d1.numpy()[0] = ha[i], hr[i], hd[i]
         g.replay_insert(0, f1, a1, r1, d1)           # this step's new experience, pinned host -> device
-        info = g.round(ids, k, want_info=True)        # the round; its result (loss, decisions) device -> host
+        info = g.round(ids, k, stal, want_info=True)  # the round; its result (loss, decisions) device -> host
         k += 1
     e1.record(stream)
     stream.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
-    e2e_value = world * args.e2e_steps / (e2e_ms / 1000.0)
+    e2e_value = world * L * args.e2e_steps / (e2e_ms / 1000.0)
     _ = info
 
     # ---------------- per-phase device timing (roofline of the dominant kernel)
