@@ -604,7 +604,11 @@ void gemm_tma_launch(gorila_ctx* ctx, const TmaProb<OA, OB, EP>* probs, int npro
     if (MB == 1 && cluster_target > 0 && cluster_env_on()) {
         const int tiles = tilesA * tilesB * nprob;
         const int want = std::max(1, (cluster_target + tiles - 1) / tiles);
-        while (cl * 2 <= std::min(16, std::min(want, nchunks))) cl *= 2;
+        static const int cl_max = [] {
+            const char* e = getenv("GORILA_CLUSTER_MAX");  // in-cluster split-K size cap (default 8)
+            return e ? std::max(1, std::min(16, atoi(e))) : 8;
+        }();
+        while (cl * 2 <= std::min(cl_max, std::min(want, nchunks))) cl *= 2;
     }
     if (persist_env && cl == 1 &&
         (int64_t)tilesA * tilesB * nprob * std::max(1, std::min(splits, nchunks)) > ctx->num_sms) {
@@ -1396,10 +1400,17 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
             split_w[l] = eff_splits(fp32, Mred[l], want);
         } else {  // TMA engine: chunks are 80-pixel rows (conv1) or whole samples (conv2, conv3)
             const int nch = l == 0 ? 5 * B : B, ta = l == 0 ? 2 : l == 1 ? 4 : 5;
-            static const int cap = [] {  // partials per weight (the critical-path reduce reads them all)
+            // partials per weight (the critical-path reduce reads them all); conv1's weight gradient
+            // is itself on the critical path (the last GEMM of the dgrad chain): it keeps more splits
+            static const int cap23 = [] {
                 const char* e = getenv("GORILA_WSPLIT_MAX");
                 return e ? std::max(1, atoi(e)) : 16;
             }();
+            static const int cap1 = [] {
+                const char* e = getenv("GORILA_WSPLIT1_MAX");
+                return e ? std::max(1, atoi(e)) : 16;
+            }();
+            const int cap = l == 0 ? cap1 : cap23;
             // small batches: the weight-gradient GEMMs run beside the dgrad chain and can afford
             // fewer, longer splits; large batches need every SM on them
             const int lim = B <= 256 ? std::min(nch, cap) : nch;

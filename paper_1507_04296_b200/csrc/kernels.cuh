@@ -38,6 +38,15 @@ __global__ void __launch_bounds__(256) k_sample(const uint8_t* __restrict__ fram
     const int64_t tau = (n - size) + (int64_t)__umul64hi(u, M);
     const int64_t oldest = n - size;
 
+    const int chunk = blockIdx.x * blockDim.x + threadIdx.x;
+    uint4 f[5];  // issued with the d-flag loads (not after them): the keep masks zero channels later
+#pragma unroll
+    for (int t = 0; t < 5; ++t) {
+        int64_t st = tau - 3 + t;
+        f[t] = (st >= 0 && chunk < FRAME_BYTES / 16)
+                   ? *reinterpret_cast<const uint4*>(frames + (st % C) * FRAME_BYTES + chunk * 16)
+                   : make_uint4(0, 0, 0, 0);
+    }
     // keep[f] for frames tau-3+f, f = 0..4 (s uses f = 0..3, s' uses f = 1..4)
     bool keep_s[4], keep_s2[4];
     {
@@ -59,16 +68,7 @@ __global__ void __launch_bounds__(256) k_sample(const uint8_t* __restrict__ fram
             keep_s2[c] = k2;
         }
     }
-    const int chunk = blockIdx.x * blockDim.x + threadIdx.x;
     if (chunk < FRAME_BYTES / 16) {
-        uint4 f[5];
-#pragma unroll
-        for (int t = 0; t < 5; ++t) {
-            int64_t st = tau - 3 + t;
-            bool need = (t < 4 && keep_s[t]) || (t >= 1 && keep_s2[t - 1]);
-            f[t] = need ? *reinterpret_cast<const uint4*>(frames + (st % C) * FRAME_BYTES + chunk * 16)
-                        : make_uint4(0, 0, 0, 0);
-        }
         const uint8_t* fb[5];
 #pragma unroll
         for (int t = 0; t < 5; ++t) fb[t] = reinterpret_cast<const uint8_t*>(&f[t]);
