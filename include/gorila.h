@@ -99,6 +99,12 @@ typedef struct {
     int32_t history;           /* parameter-replica history depth H >= 1: learner_step accepts
                                   scheduled staleness s < H (deterministic fixed-staleness mode) */
     const float* theta0;       /* host, canonical layout, P floats: theta^+ = theta = theta^- at init (Alg.1) */
+    int32_t ps_mode;           /* 0: aggregate, one optimizer step per round on the mean of the accepted
+                                  gradients (reading R12); 1: per message (NEXT row f1, reading R32): every
+                                  accepted learner gradient is its own optimizer step, in ascending global
+                                  learner id, V += 1 each. 1 needs world == 1 or the
+                                  peer-memory exchange (E_INVALID on the NCCL fallback) and
+                                  world * n_learners_local <= 64. */
 } gorila_config;
 
 /* Per-learner outcome of one learner_step (Alg.1). */

@@ -356,6 +356,9 @@ class Config:
     seed_sample: int = 1507
     mode: str = "exact"             # "exact" (fp64) or "bf16" (emulates the GPU rounding points)
     n_shards: int = 1
+    ps_mode: str = "aggregate"      # "aggregate": one step on the mean of the accepted gradients (R12);
+                                    # "per_message": NEXT row f1, one optimizer step per accepted
+                                    # message in ascending learner id, V += 1 each (R32)
 
 
 @dataclasses.dataclass
@@ -392,6 +395,7 @@ class GorilaOracle:
         per = {}
         G_sum = np.zeros_like(self.theta)
         n_acc = 0
+        messages = []  # accepted gradients in ascending learner id (f1)
         for j in sorted(self.learners):
             L = self.learners[j]
             # O1
@@ -431,9 +435,20 @@ class GorilaOracle:
                     info["accepted"] = True
                     G_sum += G
                     n_acc += 1
+                    messages.append(G)
             per[j] = info
+        # f1 (R32): every accepted message is its own optimizer step, in ascending learner id
+        if cfg.ps_mode == "per_message":
+            for G in messages:
+                for lo, hi in shard_bounds(len(self.theta), cfg.n_shards):
+                    if cfg.optimizer == "rmsprop":
+                        rmsprop_apply(self.theta[lo:hi], self.m[lo:hi], self.v[lo:hi], G[lo:hi],
+                                      cfg.lr, cfg.rms_rho, cfg.rms_eps)
+                    else:
+                        adagrad_apply(self.theta[lo:hi], self.v[lo:hi], G[lo:hi], cfg.lr, cfg.ada_eps)
+            self.V = V0 + n_acc
         # O10 (one PS step per round on the mean of accepted gradients; R12, R25)
-        if n_acc > 0:
+        elif n_acc > 0:
             g = G_sum / n_acc
             for lo, hi in shard_bounds(len(self.theta), cfg.n_shards):
                 if cfg.optimizer == "rmsprop":

@@ -164,6 +164,9 @@ struct gorila_ctx {
     // gorila_round overlaps the exchange of the fc4 weight region (95% of theta) with the conv
     // backward: phase 0 of the apply runs on side2 right after the last learner's fc4 wgrad
     bool in_round = false, early_pending = false;
+    // per-message PS (f1, cfg.ps_mode == 1): every local learner keeps its own gradient buffer
+    bool per_msg = false;
+    float* G_all = nullptr;  // [L][W*q]; G points at learner 0's
     int early_learner = -1;
     cudaStream_t side2 = nullptr;
     cudaEvent_t ev_s2_fork = nullptr, ev_s2_join = nullptr;
@@ -787,6 +790,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     constexpr bool fp32v = std::is_same<T, float>::value;
     const uint64_t k_src = round >= (uint64_t)s_j ? round - (uint64_t)s_j : 0;
     const int slot = (int)(k_src % (uint64_t)ctx->H);
+    // gradient destination: the shared sum, or (per-message mode) this learner's own buffer
+    float* const Gd = ctx->per_msg ? ctx->G_all + (int64_t)j * ctx->W * ctx->q : ctx->G;
+    if (ctx->per_msg) accumulate = 0;
     const T* rt = P_<T>(ctx->rep_t[slot]);
     const float* rf = ctx->rep_f[slot];
     const T* tt = P_<T>(Lr.tminus_t);
@@ -1032,14 +1038,14 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         if constexpr (fp32v) {
             using LA = LdRowsMN<T>; using LB = LdRowsMN<T>; using EP = EpAddT;
             GemmProb<LA, LB, EP> pr[1] = {{{a3, FC4_IN, FC4_IN, B}, {g4, FC4_OUT, FC4_OUT, B},
-                                           {ctx->G + OFF_W4, FC4_IN, FC4_IN, FC4_OUT, accumulate}}};
+                                           {Gd + OFF_W4, FC4_IN, FC4_IN, FC4_OUT, accumulate}}};
             gemm<T, 64>(ctx, pr, 1, FC4_IN, FC4_OUT, B, 1);
         } else {
             using OA = OpMatMNS<128>; using OB = OpMatMNS<64>; using EP = EpAddT;
             TmaProb<OA, OB, EP> pr[1];
             pr[0].a = op_matmns<128>(ctx, a3, B, FC4_IN, FC4_IN);
             pr[0].b = op_matmns<64>(ctx, g4, B, FC4_OUT, FC4_OUT);
-            pr[0].ep = {ctx->G + OFF_W4, FC4_IN, FC4_IN, FC4_OUT, accumulate};
+            pr[0].ep = {Gd + OFF_W4, FC4_IN, FC4_IN, FC4_OUT, accumulate};
             gemm_tma_launch<64, 1>(ctx, pr, 1, (FC4_IN + 127) / 128, FC4_OUT / 64, (B + 63) / 64, 1, 0, FC4_OUT);
         }
     }
@@ -1215,7 +1221,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         for (int l = 3; l < 7; ++l) p.wide[l] = 1;
         p.nseg = 8;
         p.accumulate = accumulate;
-        launch(ctx, k_wgrad_reduce, dim3(148 * 2), dim3(256), 0, p, ctx->G);
+        launch(ctx, k_wgrad_reduce, dim3(148 * 2), dim3(256), 0, p, Gd);
     }
     }
     mark(ctx, PH_WGRED);
@@ -1332,7 +1338,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     float* theta = c.take<float>(W * q);
     float* m = c.take<float>(q);
     float* v = c.take<float>(q);
-    float* G = c.take<float>(W * q);
+    float* G = c.take<float>((cfg->ps_mode == 1 ? L : 1) * W * q);  // per-message mode: one per learner
     float* counts = c.take<float>(W + 64);
     uint64_t* V = c.take<uint64_t>(4);
     uint64_t* rinfo = c.take<uint64_t>(4);
@@ -1340,7 +1346,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     uint64_t* Vhist = c.take<uint64_t>(H);
     uint64_t* dev_round = c.take<uint64_t>(1);
     unsigned int* head_counter = c.take<unsigned int>(1);
-    uint64_t* pflags = c.take<uint64_t>(5 * MAX_W);
+    uint64_t* pflags = c.take<uint64_t>(6 * MAX_W);
     uint64_t* p2p_epoch = c.take<uint64_t>(1);
     unsigned int* p2p_counter = c.take<unsigned int>(2);
     std::vector<void*> rep_t(H);
@@ -1428,6 +1434,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         ctx->nA = nA; ctx->B = B; ctx->L = L; ctx->W = W; ctx->P = P; ctx->q = q; ctx->esz = esz;
         ctx->rl = rl; ctx->H = H;
         ctx->theta = theta; ctx->m = m; ctx->v = v; ctx->G = G; ctx->counts = counts; ctx->V = V;
+        ctx->G_all = G; ctx->per_msg = cfg->ps_mode == 1;
         ctx->round_info = rinfo;
         ctx->n_acc_local = nacc; ctx->Vhist = Vhist; ctx->dev_round = dev_round; ctx->head_counter = head_counter;
         ctx->pflags = pflags; ctx->p2p_epoch = p2p_epoch; ctx->p2p_counter = p2p_counter; ctx->rep_t = rep_t; ctx->rep_f = rep_f; ctx->learners = lrs;
@@ -1560,6 +1567,9 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
         return fail(GORILA_E_INVALID, "bad optimizer");
     if (cfg->history < 1 || cfg->history > 64) return fail(GORILA_E_INVALID, "history must be in [1, 64]");
     if (cfg->target_period < 1) return fail(GORILA_E_INVALID, "target_period must be >= 1");
+    if (cfg->ps_mode != 0 && cfg->ps_mode != 1) return fail(GORILA_E_INVALID, "ps_mode must be 0 or 1");
+    if (cfg->ps_mode == 1 && (cfg->n_learners_local > 32 || cfg->world * cfg->n_learners_local > 64))
+        return fail(GORILA_E_INVALID, "per-message mode: at most 32 learners per rank, 64 in total");
     if (!cfg->theta0) return fail(GORILA_E_INVALID, "theta0 is required");
     if (!cfg->workspace) return fail(GORILA_E_INVALID, "workspace is required");
     if (((uintptr_t)cfg->workspace) % 256) return fail(GORILA_E_INVALID, "workspace must be 256-byte aligned");
@@ -1578,13 +1588,13 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     CU(cudaMemsetAsync(ctx->theta, 0, sizeof(float) * ctx->W * ctx->q, st));
     CU(cudaMemsetAsync(ctx->m, 0, sizeof(float) * ctx->q, st));
     CU(cudaMemsetAsync(ctx->v, 0, sizeof(float) * ctx->q, st));
-    CU(cudaMemsetAsync(ctx->G, 0, sizeof(float) * ctx->W * ctx->q, st));
+    CU(cudaMemsetAsync(ctx->G, 0, sizeof(float) * ctx->W * ctx->q * (ctx->per_msg ? ctx->L : 1), st));
     CU(cudaMemsetAsync(ctx->V, 0, sizeof(uint64_t) * 4, st));
     CU(cudaMemsetAsync(ctx->n_acc_local, 0, sizeof(uint32_t) * 4, st));
     CU(cudaMemsetAsync(ctx->Vhist, 0, sizeof(uint64_t) * ctx->H, st));
     CU(cudaMemsetAsync(ctx->head_counter, 0, sizeof(unsigned int), st));
     CU(cudaMemsetAsync(ctx->dev_round, 0, sizeof(uint64_t), st));
-    CU(cudaMemsetAsync(ctx->pflags, 0, sizeof(uint64_t) * 5 * MAX_W, st));
+    CU(cudaMemsetAsync(ctx->pflags, 0, sizeof(uint64_t) * 6 * MAX_W, st));
     CU(cudaMemsetAsync(ctx->p2p_epoch, 0, sizeof(uint64_t), st));
     CU(cudaMemsetAsync(ctx->p2p_counter, 0, sizeof(unsigned int) * 2, st));
     ctx->dev_round_expect = 0;
@@ -1630,6 +1640,10 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
         NC(ncclCommInitRank(&ctx->comm, cfg->world, id, cfg->rank));
         const char* pe = getenv("GORILA_P2P");  // GORILA_P2P=0: NCCL reduce-scatter / all-gather
         if (!(pe && atoi(pe) == 0) && cfg->world <= MAX_W) ctx->p2p = p2p_setup(ctx);
+        if (ctx->per_msg && !ctx->p2p) {
+            gorila_destroy(ctx);
+            return fail(GORILA_E_INVALID, "per-message mode needs the peer-memory exchange (world > 1)");
+        }
     }
     CU(cudaStreamSynchronize(st));
     *out = ctx;
@@ -1772,6 +1786,8 @@ gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
         ctx->dev_round_expect = round;
     }
     mark(ctx, PH_STEP_MISC);
+    if (ctx->per_msg && n != ctx->L)
+        return fail(GORILA_E_INVALID, "per-message mode: every local learner runs each round");
     ctx->early_learner = -1;
     static const bool early_env = [] {
         // GORILA_EARLY=1: overlap the fc4-region exchange with the conv backward (measured slower at
@@ -1851,7 +1867,12 @@ void p2p_params(gorila_ctx* ctx, uint64_t round, ApplyParams& p, P2PParams& x) {
         x.rep_t[q] = peer_ptr(ctx, q, (uint8_t*)ctx->rep_t[slot]);
         x.rep_f[q] = peer_ptr(ctx, q, ctx->rep_f[slot]);
         x.flags[q] = peer_ptr(ctx, q, ctx->pflags);
+        if (ctx->per_msg)
+            for (int j = 0; j < ctx->L; ++j)
+                x.Gm[q * ctx->L + j] = peer_ptr(ctx, q, ctx->G_all + (int64_t)j * W * ctx->q) + lo;
     }
+    x.L = ctx->per_msg ? ctx->L : 0;
+    for (int j = 0; j < (ctx->per_msg ? ctx->L : 0); ++j) x.info[j] = ctx->learners[j].info;
     x.epoch = ctx->p2p_epoch;
     x.counter = ctx->p2p_counter;
     static const int dbg = [] {
@@ -1970,8 +1991,20 @@ gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info*
         p.rep_f = ctx->rep_f[slot];
         p.vhist_dst = ctx->Vhist + slot;
     }
-    if (ctx->cfg.math == GORILA_MATH_FP32) launch(ctx, k_apply<float>, dim3(148 * 4), dim3(256), 0, p);
-    else launch(ctx, k_apply<__nv_bfloat16>, dim3(148 * 4), dim3(256), 0, p);
+    if (ctx->per_msg) {  // W == 1 here (W > 1 runs the peer-memory exchange)
+        MsgParams mp{};
+        mp.nmsg = ctx->L;
+        for (int j = 0; j < ctx->L; ++j) {
+            mp.G[j] = ctx->G_all + (int64_t)j * ctx->W * ctx->q;
+            mp.info[j] = ctx->learners[j].info;
+        }
+        if (ctx->cfg.math == GORILA_MATH_FP32) launch(ctx, k_apply_msg<float>, dim3(148 * 4), dim3(256), 0, p, mp);
+        else launch(ctx, k_apply_msg<__nv_bfloat16>, dim3(148 * 4), dim3(256), 0, p, mp);
+    } else if (ctx->cfg.math == GORILA_MATH_FP32) {
+        launch(ctx, k_apply<float>, dim3(148 * 4), dim3(256), 0, p);
+    } else {
+        launch(ctx, k_apply<__nv_bfloat16>, dim3(148 * 4), dim3(256), 0, p);
+    }
     ctx->dev_round_expect = round + 1;
     mark(ctx, PH_APPLY);
     if (W > 1) {
@@ -2259,7 +2292,19 @@ gorila_status gorila_set_learner_state(gorila_ctx* ctx, int32_t learner, const f
 gorila_status gorila_get_grad(gorila_ctx* ctx, float* g) {
     if (!ctx || !g) return fail(GORILA_E_INVALID, "null argument");
     cudaStream_t st = ctx->stream;
-    k_convert<<<148 * 4, 256, 0, st>>>(ctx->G, ctx->tmp_canon, ctx->P, 1);
+    const float* src = ctx->G;
+    if (ctx->per_msg && ctx->L > 1) {  // the sum over this rank's learners (as the aggregate mode's G)
+        const int64_t n = (int64_t)ctx->W * ctx->q;
+        std::vector<float> acc(n, 0.f), one(n);
+        CU(cudaStreamSynchronize(st));
+        for (int j = 0; j < ctx->L; ++j) {
+            CU(cudaMemcpy(one.data(), ctx->G_all + (int64_t)j * n, sizeof(float) * n, cudaMemcpyDeviceToHost));
+            for (int64_t i = 0; i < n; ++i) acc[i] += one[i];
+        }
+        CU(cudaMemcpy(ctx->tmp_int, acc.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
+        src = ctx->tmp_int;
+    }
+    k_convert<<<148 * 4, 256, 0, st>>>(src, ctx->tmp_canon, ctx->P, 1);
     ctx->launches++;
     CU(cudaMemcpyAsync(g, ctx->tmp_canon, sizeof(float) * ctx->P, cudaMemcpyDeviceToHost, st));
     CU(cudaStreamSynchronize(st));

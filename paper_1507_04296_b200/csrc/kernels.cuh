@@ -573,6 +573,21 @@ __global__ void __launch_bounds__(256) k_apply(ApplyParams p) {
 // its next-round replica chunk into every rank. The last block signals "done"; k_peer_wait holds
 // the stream until every peer is done (so no rank starts the next round while a peer still reads
 // its G / count or writes its replicas).
+// one optimizer step on 4 elements (R2 centered RMSProp / P:169 AdaGrad), the gradient unscaled
+GORILA_DEV void opt_step4(const ApplyParams& p, float* tv, float* mv, float* vv, const float4 g) {
+    const float gv[4] = {g.x, g.y, g.z, g.w};
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+        if (p.optimizer == 0) {
+            mv[c] = p.rho * mv[c] + (1.f - p.rho) * gv[c];
+            vv[c] = p.rho * vv[c] + (1.f - p.rho) * gv[c] * gv[c];
+            tv[c] -= p.lr * gv[c] / sqrtf(vv[c] - mv[c] * mv[c] + p.eps);
+        } else {
+            vv[c] += gv[c] * gv[c];
+            tv[c] -= p.lr * gv[c] / (sqrtf(vv[c]) + p.ada_eps);
+        }
+    }
+}
 constexpr int MAX_W = 8;
 GORILA_DEV void st_release_sys(uint64_t* p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
@@ -610,10 +625,15 @@ struct P2PParams {
     void* rep_t[MAX_W];           // rank q's next-round replica (T area, fp32 area)
     float* rep_f[MAX_W];
     uint64_t* flags[MAX_W];       // rank q's flag area: phase f: [2f MAX_W, +MAX_W) ready, [(2f+1) MAX_W, ..) done;
-                                  // [4 MAX_W, 5 MAX_W): the ranks' accepted counts (sent with the ready flag)
+                                  // [4 MAX_W, 5 MAX_W): the ranks' accepted counts (sent with the ready flag);
+                                  // [5 MAX_W, 6 MAX_W): their per-learner acceptance masks (f1)
     uint64_t* epoch;              // local round epoch (advanced by k_peer_wait)
     unsigned int* counter;        // local: finished blocks, one counter per phase (phases may overlap)
     int dbg;                      // diagnostics (GORILA_P2P_DBG): 1 = skip peer gradient loads, 2 = skip peer replica stores
+    // per-message mode (f1): L messages per rank, message (q, j) = rank q's learner j at Gm[q * L + j]
+    int L;                        // 0: aggregate mode
+    const float* Gm[64];
+    const DevLearnerInfo* info[32];  // this rank's learners' decisions (acceptance mask sent with the flag)
 };
 
 template <typename T>
@@ -650,18 +670,28 @@ __global__ void __launch_bounds__(256) k_apply_p2p(ApplyParams p, P2PParams x, i
     uint64_t* mine = x.flags[x.rank];
     if (blockIdx.x == 0 && (int)threadIdx.x < x.W) {  // this rank's G range and count are complete
         x.flags[threadIdx.x][4 * MAX_W + x.rank] = (uint64_t)*x.nacc[x.rank];  // ordered by the release
+        if (x.L) {
+            uint64_t m = 0;
+            for (int j = 0; j < x.L; ++j) m |= (uint64_t)(x.info[j]->accepted ? 1 : 0) << j;
+            x.flags[threadIdx.x][5 * MAX_W + x.rank] = m;
+        }
         st_release_sys(x.flags[threadIdx.x] + RDY + x.rank, ep);
     }
     __shared__ float s_cnt;
+    __shared__ unsigned long long s_gmask;
     if (threadIdx.x == 0) {
         float c = 0.f;
+        unsigned long long gm = 0;
         for (int q = 0; q < x.W; ++q) {
             wait_flag(mine + RDY + q, ep);
             c += (float)__ldcg(mine + 4 * MAX_W + q);  // local copy of rank q's count
+            if (x.L) gm |= (unsigned long long)__ldcg(mine + 5 * MAX_W + q) << (q * x.L);
         }
         s_cnt = c;
+        s_gmask = gm;
     }
     __syncthreads();
+    const unsigned long long gmask = s_gmask;
 #ifdef GORILA_TRACE
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         const uint64_t t = gtimer();
@@ -694,7 +724,16 @@ __global__ void __launch_bounds__(256) k_apply_p2p(ApplyParams p, P2PParams x, i
         const int64_t e = i < len0 ? lo0 + i : lo1 + (i - len0);
         float4 th = reinterpret_cast<const float4*>(th_local)[e];
         float tv[4] = {th.x, th.y, th.z, th.w};
-        if (update) {
+        if (update && x.L) {  // f1: one optimizer step per accepted message, in global learner order
+            float4 m = reinterpret_cast<float4*>(p.m)[e];
+            float4 v = reinterpret_cast<float4*>(p.v)[e];
+            float mv[4] = {m.x, m.y, m.z, m.w}, vv[4] = {v.x, v.y, v.z, v.w};
+            for (int msg = 0; msg < x.W * x.L; ++msg)
+                if (gmask >> msg & 1ull) opt_step4(p, tv, mv, vv, __ldcg(reinterpret_cast<const float4*>(x.Gm[msg]) + e));
+            reinterpret_cast<float4*>(p.m)[e] = make_float4(mv[0], mv[1], mv[2], mv[3]);
+            reinterpret_cast<float4*>(p.v)[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+            reinterpret_cast<float4*>(th_local)[e] = make_float4(tv[0], tv[1], tv[2], tv[3]);
+        } else if (update) {
             float4 gq[MAX_W];  // every rank's slice element requested before the first add
 #pragma unroll
             for (int q = 0; q < MAX_W; ++q)
@@ -776,6 +815,62 @@ __global__ void k_peer_wait(P2PParams x, int phase0) {  // waits for phase 1 (an
         *x.epoch = ep;
         P2PTRACE(42, gtimer() - t_in);
         P2PTRACE(43, 1);
+    }
+}
+
+// ------------------------------------------------------------------------- per-message PS (f1)
+// NEXT row f1 (reading R32): each accepted learner gradient is its own optimizer step, applied in
+// ascending global learner id ("applies the updates", P:160 version per update). The
+// sequence is elementwise, so every thread runs the whole message sequence on its elements.
+constexpr int MAX_MSG = 64;
+struct MsgParams {
+    const float* G[32];                 // local learner j's gradient (this rank's slice)
+    const DevLearnerInfo* info[32];     // its decisions of the round
+    int nmsg;
+};
+template <typename T>
+__global__ void __launch_bounds__(256) k_apply_msg(ApplyParams p, MsgParams mp) {
+    pdl_wait();
+    pdl_trigger();
+    __shared__ uint32_t s_mask;
+    if (threadIdx.x == 0) {
+        uint32_t mask = 0;
+        for (int j = 0; j < mp.nmsg; ++j) mask |= (mp.info[j]->accepted ? 1u : 0u) << j;
+        s_mask = mask;
+    }
+    __syncthreads();
+    const uint32_t mask = s_mask;
+    const int n_acc = __popc(mask);
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        const uint64_t v0 = *p.V;
+        p.round_info[0] = n_acc;
+        p.round_info[1] = v0;
+        p.round_info[2] = v0 + n_acc;
+        *p.V = v0 + n_acc;
+        if (p.vhist_dst) *p.vhist_dst = v0 + n_acc;
+        if (p.dev_round) *p.dev_round += 1;
+        for (int i = 0; i < p.n_sync; ++i) {
+            LearnerStats* st = p.sync_stats[i];
+            const bool doit = v0 + n_acc >= st->last_sync + (uint64_t)p.period;
+            if (doit) st->last_sync = v0 + n_acc;
+            *p.sync_flag[i] = doit;
+        }
+    }
+    const int64_t n4 = (p.n_real + 3) / 4;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n4; e += (int64_t)gridDim.x * blockDim.x) {
+        float4 th = reinterpret_cast<float4*>(p.theta)[e];
+        float tv[4] = {th.x, th.y, th.z, th.w};
+        if (mask) {
+            float4 m = reinterpret_cast<float4*>(p.m)[e];
+            float4 v = reinterpret_cast<float4*>(p.v)[e];
+            float mv[4] = {m.x, m.y, m.z, m.w}, vv[4] = {v.x, v.y, v.z, v.w};
+            for (int j = 0; j < mp.nmsg; ++j)
+                if (mask >> j & 1u) opt_step4(p, tv, mv, vv, reinterpret_cast<const float4*>(mp.G[j])[e]);
+            reinterpret_cast<float4*>(p.theta)[e] = make_float4(tv[0], tv[1], tv[2], tv[3]);
+            reinterpret_cast<float4*>(p.m)[e] = make_float4(mv[0], mv[1], mv[2], mv[3]);
+            reinterpret_cast<float4*>(p.v)[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
+        }
+        if (p.rep_t) emit4<T>(p, e, tv);
     }
 }
 

@@ -39,7 +39,7 @@ class Config(ctypes.Structure):
                 ("outlier_enabled", ctypes.c_int32), ("outlier_warmup", ctypes.c_int32),
                 ("outlier_k", ctypes.c_float), ("outlier_beta", ctypes.c_double), ("min_replay", ctypes.c_int64),
                 ("seed", ctypes.c_uint64), ("math", ctypes.c_int32), ("history", ctypes.c_int32),
-                ("theta0", ctypes.c_void_p)]
+                ("theta0", ctypes.c_void_p), ("ps_mode", ctypes.c_int32)]
 
 
 class LearnerInfo(ctypes.Structure):
@@ -151,7 +151,7 @@ class Gorila:
                  learner_id_base=0, rank=0, world=1, nccl_unique_id=None, stream=None, theta0=None,
                  optimizer="rmsprop", lr=2.5e-4, rms_rho=0.95, rms_eps=0.01, ada_eps=1e-8, target_period=100,
                  max_staleness=-1, outlier_enabled=True, outlier_warmup=100, outlier_k=3.0, outlier_beta=0.999,
-                 min_replay=1, seed=1507, math="bf16", history=2, device=None):
+                 min_replay=1, seed=1507, math="bf16", history=2, device=None, ps_mode="aggregate"):
         import torch
         L = load()
         self.torch = torch
@@ -174,6 +174,7 @@ class Gorila:
                      ada_eps=ada_eps, target_period=target_period, max_staleness=max_staleness,
                      outlier_enabled=int(outlier_enabled), outlier_warmup=outlier_warmup, outlier_k=outlier_k,
                      outlier_beta=outlier_beta, min_replay=min_replay, seed=seed,
+                     ps_mode={"aggregate": 0, "per_message": 1}[ps_mode],
                      math={"fp32": 0, "bf16": 2}[math], history=history, theta0=theta0.ctypes.data)
         nbytes = int(L.gorila_workspace_bytes(ctypes.byref(cfg)))
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)

@@ -157,6 +157,50 @@ def test_learner_update_parity_large_batch_paths(math, B, normal_min, monkeypatc
     _check_round(gpu, res, math, nA, [0], orc, {0: th})
 
 
+def _check_dtheta(gpu, orc, th_before, math, nA, tol_dtheta=None, n_round=1):
+    """Delta-theta per tensor vs the oracle's update rounded to the fp32 state (R31 floor; the
+    state is rounded n_round times, once per optimizer step)."""
+    tol = dict(TOL[math])
+    if tol_dtheta is not None:
+        tol["dtheta"] = tol_dtheta
+    d_gpu = gpu["theta1"].astype(np.float64) - gpu["theta0"]
+    th1_ref = orc.theta.astype(np.float32)
+    d_ref = th1_ref.astype(np.float64) - th_before
+    ulp = np.spacing(np.abs(th1_ref)).astype(np.float64)
+    off = 0
+    for name, shp in O.param_shapes(nA):
+        n = int(np.prod(shp))
+        sl = slice(off, off + n)
+        if np.any(d_ref[sl]):
+            e = rel_l2(d_gpu[sl], d_ref[sl])
+            floor = n_round * np.linalg.norm(ulp[sl]) / max(np.linalg.norm(d_ref[sl]), 1e-300)
+            assert e <= tol["dtheta"] + floor, ("dtheta", name, e, floor)
+        off += n
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
+@pytest.mark.parametrize("opt", ["adagrad", "rmsprop"])
+def test_f1_per_message_ps_parity(math, opt):
+    """NEXT row f1 (R32): three learners' accepted gradients applied as three optimizer steps in
+    ascending learner id (AdaGrad, the paper's rule P:169, and RMSProp), V += 1 each."""
+    nA, L = 6, 3
+    # R34: AdaGrad's step lr*g/(sqrt(sum g^2) + eps) is a sign function at g = 0 for eps far below the
+    # gradient's round-off; eps = 1e-6 keeps round-off-level elements from flipping an lr-sized step
+    g, orc = make_pair(nA=nA, B=16, C=2000, n_insert=2000, math=math, L=L, optimizer=opt,
+                       ps_mode="per_message", outlier_warmup=2, lr=1e-3, ada_eps=1e-6)
+    ids = list(range(L))
+    for k in range(4):
+        teacher_force(g, orc)
+        th_before = orc.theta.copy()
+        gpu, res = run_round_both(g, orc, k, ids)
+        _check_round(gpu, res, math, nA, ids, orc, {j: th_before for j in ids})
+        # R33: after the first message each step depends on ratios of gradient elements
+        # (g_m / sqrt(sum g^2)), so the update inherits the gradient tolerance once per message
+        n_msg = max(1, res["n_accepted"])
+        _check_dtheta(gpu, orc, th_before, math, nA,
+                      tol_dtheta=max(TOL[math]["dtheta"], n_msg * TOL[math]["g"]), n_round=n_msg + 1)
+
+
 @pytest.mark.parametrize("math", ["fp32", "bf16"])
 def test_multi_learner_staleness_outlier_and_sync(math):
     """3 learners on one rank, fixed-staleness schedule (history 3), poison rewards, target sync."""

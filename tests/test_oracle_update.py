@@ -309,3 +309,48 @@ def test_descent_on_frozen_batch():
         losses.append(loss)
         O.rmsprop_apply(theta, m, v, O.qnet_backward(theta, s, acts, dQ, nA), 2.5e-4, 0.95, 0.01)
     assert all(l1 < l0 for l0, l1 in zip(losses, losses[1:]))
+
+
+# ---------------------------------------------------------------- NEXT row f1: per-message PS (R32)
+def _f1_pair(ps_mode, learners, optimizer="adagrad", rounds=2):
+    nA, B, C = 4, 8, 400
+    cfg = O.Config(n_actions=nA, batch=B, capacity=C, learners=learners, outlier_warmup=1,
+                   optimizer=optimizer, lr=1e-3, ps_mode=ps_mode)
+    orc = O.GorilaOracle(cfg, synth.theta0(nA))
+    for j in learners:
+        f = synth.frames(synth.SEED_DATA, j, 0, C)
+        a, r, d = synth.meta(synth.SEED_DATA, j, 0, C, nA)
+        orc.insert(j, f, a, r, d)
+    return orc
+
+
+def test_f1_single_message_equals_aggregate():
+    """One accepted message per round: a step on it == a step on the mean of one (bitwise)."""
+    for opt in ("adagrad", "rmsprop"):
+        a, b = _f1_pair("aggregate", (0,), opt), _f1_pair("per_message", (0,), opt)
+        for k in range(3):
+            a.round(k)
+            b.round(k)
+        assert np.array_equal(a.theta, b.theta) and np.array_equal(a.v, b.v) and a.V == b.V
+
+
+def test_f1_messages_applied_one_step_each_in_learner_order():
+    """Two learners: theta moves by the optimizer applied to G_0 then G_1 (the PS
+    applies each learner's gradient as its own update), V += 1 per message, and it differs from
+    one step on the mean (the optimizer is nonlinear in its state)."""
+    for opt in ("adagrad", "rmsprop"):
+        orc = _f1_pair("per_message", (0, 1), opt)
+        agg = _f1_pair("aggregate", (0, 1), opt)
+        th0, m0, v0 = orc.theta.copy(), orc.m.copy(), orc.v.copy()
+        res = orc.round(0)
+        agg.round(0)
+        G0, G1 = res["learners"][0]["G"], res["learners"][1]["G"]
+        assert res["learners"][0]["accepted"] and res["learners"][1]["accepted"]
+        th, m, v = th0.copy(), m0.copy(), v0.copy()
+        for G in (G0, G1):  # the pinned primitives, composed in ascending learner id
+            if opt == "adagrad":
+                O.adagrad_apply(th, v, G, 1e-3, 1e-8)
+            else:
+                O.rmsprop_apply(th, m, v, G, 1e-3, 0.95, 0.01)
+        assert np.array_equal(orc.theta, th) and orc.V == 2 and res["n_accepted"] == 2
+        assert not np.allclose(orc.theta, agg.theta, rtol=0, atol=1e-12)

@@ -9,3 +9,7 @@ timeout -s KILL 240 python -m torch.distributed.run --nnodes=1 --nproc-per-node 
 echo "bench n$N exit $?"; tail -3 gpurun_out/bench_n$N.err
 python -c "
 import json;d=json.load(open('gpurun_out/bench_n$N.json'));print('N', d['n_gpus'], d['value'], d['ms_per_step'], d.get('clocks'))"
+for m in fp32 bf16; do
+  PS_MODE=per_message MATH=$m ROUNDS=4 timeout -s KILL 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node $N --master-addr 127.0.0.1 --master-port 29521 tools/multi_gpu_check.py > gpurun_out/multi_pm_$m.log 2>&1
+  echo "multi per-message $m exit $?"; grep -E "round|CHECK" gpurun_out/multi_pm_$m.log | tail -5
+done
