@@ -34,8 +34,9 @@ def fc5_mac(nA):
     return 512 * nA
 
 
-def phase_work(phase, B, nA, P, esz):
-    """(bound, algorithmic amount per launch-group, unit) of a profiled phase."""
+def phase_work(phase, B, nA, P, esz, n_msg=1):
+    """(bound, algorithmic amount per launch-group, unit) of a profiled phase. n_msg: gradient
+    buffers the apply reads (per-message mode reads one per local learner)."""
     fl = lambda mac: 2.0 * mac * B  # noqa: E731
     table = {
         "conv1_fwd": ("tensor", 2 * fl(MAC["conv1"])), "conv2_fwd": ("tensor", 2 * fl(MAC["conv2"])),
@@ -48,7 +49,7 @@ def phase_work(phase, B, nA, P, esz):
         "sample": ("hbm", B * (5 * 7056 + 6 + 2 * 4 * 7056 * esz)),
         # centered RMSProp: read theta, m, v, g (16 B) + write theta, m, v (12 B) per parameter, plus the
         # fused emission of the next replica (esz bytes per parameter)
-        "apply": ("hbm", (28.0 + esz) * P),
+        "apply": ("hbm", (28.0 + esz + 4.0 * (n_msg - 1)) * P),
         # replica pack (world > 1, after the all-gather): read fp32 theta, write the replica
         "pack": ("hbm", (4.0 + esz) * P),
     }
@@ -222,6 +223,7 @@ def config_dict(args, world):
             "n_actions": args.n_actions, "batch_per_learner": args.batch, "learners_per_gpu": args.learners,
             "global_batch": args.batch * world * args.learners,
             "replay_frames_per_learner": args.capacity, "target_period": args.target_period,
+            "ps_mode": args.ps_mode, "optimizer": args.optimizer,
             "ps_shards": world, "parallelism": f"dp{world} learners + {world}-way sharded PS "
                                                f"({'NVLink peer-memory exchange' if world > 1 else 'local'})",
             "math": args.math, "l2": "inputs larger than L2: 7.06 GB replay per GPU (126 MB L2); the 27 MB "
@@ -246,6 +248,9 @@ def main():
     ap.add_argument("--staleness", type=int, default=0, help="scheduled staleness of every learner (rounds)")
     ap.add_argument("--max-staleness", type=int, default=-1, help="discard threshold in versions (-1: off)")
     ap.add_argument("--poison", type=float, default=0.0, help="probability of a 1e6 poison reward")
+    ap.add_argument("--ps-mode", default="aggregate", choices=["aggregate", "per_message"],
+                    help="per_message: NEXT row f1 (one optimizer step per accepted learner gradient)")
+    ap.add_argument("--optimizer", default="rmsprop", choices=["rmsprop", "adagrad"])
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=200)
@@ -276,7 +281,8 @@ def main():
     g = Gorila(n_actions=args.n_actions, batch=args.batch, replay_capacity=args.capacity, n_learners_local=L,
                learner_id_base=rank * L, rank=rank, world=world, nccl_unique_id=uid, stream=stream,
                theta0=synth.theta0(args.n_actions), math=args.math, target_period=args.target_period,
-               history=max(2, args.staleness + 1), max_staleness=args.max_staleness)
+               history=max(2, args.staleness + 1), max_staleness=args.max_staleness, ps_mode=args.ps_mode,
+               optimizer=args.optimizer)
     for j in range(L):
         fill_replay(g, j, args.capacity, args.n_actions, synth.SEED_DATA, rank * L + j, p_poison=args.poison)
     ids = np.arange(L, dtype=np.int32)
@@ -356,6 +362,7 @@ def main():
 
     peaks = read_peaks()
     P = g.P
+    n_msg = L if args.ps_mode == "per_message" else 1
     esz = 2 if args.math == "bf16" else 4
     total_prof = sum(phases.values())
     per_launch_ms = {p: v / max(n_prof, 1) for p, v in phases.items()}
@@ -363,7 +370,7 @@ def main():
     dom = max(iso_ms, key=lambda p: iso_ms[p])
 
     def roof(p):
-        w = phase_work(p, args.batch, args.n_actions, P, esz)
+        w = phase_work(p, args.batch, args.n_actions, P, esz, n_msg)
         if w is None or iso_ms.get(p, 0.0) <= 0.0:
             return None
         bound, amount = w
@@ -381,7 +388,7 @@ def main():
 
     dom_roof = roof(dom)
     if dom_roof is None:  # dominant phase without an algorithmic model: report the biggest modelled one
-        modelled = [p for p in iso_ms if phase_work(p, args.batch, args.n_actions, P, esz)]
+        modelled = [p for p in iso_ms if phase_work(p, args.batch, args.n_actions, P, esz, n_msg)]
         dom = max(modelled, key=lambda p: iso_ms[p])
         dom_roof = roof(dom)
     traffic = None

@@ -864,8 +864,15 @@ __global__ void __launch_bounds__(256) k_apply_msg(ApplyParams p, MsgParams mp) 
             float4 m = reinterpret_cast<float4*>(p.m)[e];
             float4 v = reinterpret_cast<float4*>(p.v)[e];
             float mv[4] = {m.x, m.y, m.z, m.w}, vv[4] = {v.x, v.y, v.z, v.w};
-            for (int j = 0; j < mp.nmsg; ++j)
-                if (mask >> j & 1u) opt_step4(p, tv, mv, vv, reinterpret_cast<const float4*>(mp.G[j])[e]);
+            for (int j0 = 0; j0 < mp.nmsg; j0 += 8) {  // 8 messages' gradients in flight, then their steps
+                float4 gq[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (j0 + u < mp.nmsg && (mask >> (j0 + u) & 1u)) gq[u] = reinterpret_cast<const float4*>(mp.G[j0 + u])[e];
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    if (j0 + u < mp.nmsg && (mask >> (j0 + u) & 1u)) opt_step4(p, tv, mv, vv, gq[u]);
+            }
             reinterpret_cast<float4*>(p.theta)[e] = make_float4(tv[0], tv[1], tv[2], tv[3]);
             reinterpret_cast<float4*>(p.m)[e] = make_float4(mv[0], mv[1], mv[2], mv[3]);
             reinterpret_cast<float4*>(p.v)[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
