@@ -155,6 +155,10 @@ struct gorila_ctx {
     std::map<std::vector<uint64_t>, CUtensorMap> tmaps;  // TMA descriptors, encoded once per (buffer, view)
     bool tma_failed = false;
     int num_sms = 148;
+    // L2 persistence window over the parameter-server state (theta, m, v, G, replicas): the
+    // optimizer's working set stays resident across rounds (GORILA_L2_PERSIST=1: on)
+    cudaAccessPolicyWindow l2win{};
+    bool l2_on = false;
     // fused PS exchange over NVLink peer memory (W > 1; CUDA IPC mappings of the peers' workspaces)
     bool p2p = false;
     uint8_t* ws_local = nullptr;
@@ -252,6 +256,22 @@ cudaError_t fold_marks(gorila_ctx* ctx, const std::vector<std::pair<int, cudaEve
     return cudaSuccess;
 }
 
+// launch attributes shared by every kernel of the library: programmatic dependent launch and the
+// L2 persistence window; returns the number written (at has room for 2 more after `na`)
+int base_attrs(const gorila_ctx* ctx, cudaLaunchAttribute* at, int na, bool pdl) {
+    if (pdl) {
+        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[na].val.programmaticStreamSerializationAllowed = 1;
+        ++na;
+    }
+    if (ctx->l2_on) {
+        at[na].id = cudaLaunchAttributeAccessPolicyWindow;
+        at[na].val.accessPolicyWindow = ctx->l2win;
+        ++na;
+    }
+    return na;
+}
+
 // every kernel of the round goes through here: programmatic dependent launch (the next kernel's
 // launch / prologue overlaps this one; kernels griddepcontrol.wait before reading inputs)
 template <typename... KP, typename... A>
@@ -261,11 +281,9 @@ void launch(gorila_ctx* ctx, void (*kern)(KP...), dim3 grid, dim3 block, size_t 
     cfg.blockDim = block;
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->stream;
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchAttribute at[3];
     cfg.attrs = at;
-    cfg.numAttrs = ctx->pdl ? 1 : 0;
+    cfg.numAttrs = base_attrs(ctx, at, 0, ctx->pdl);
     cudaLaunchKernelEx(&cfg, kern, std::forward<A>(args)...);
     ctx->launches++;
 }
@@ -504,15 +522,9 @@ void gemm_tma_p_launch(gorila_ctx* ctx, const TmaProb<OA, OB, EP>* probs, int np
     cfg.blockDim = dim3(CFG::THREADS);
     cfg.dynamicSmemBytes = CFG::SMEM;
     cfg.stream = ctx->stream;
-    cudaLaunchAttribute at[1];
-    int na = 0;
-    if (ctx->pdl) {
-        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[na].val.programmaticStreamSerializationAllowed = 1;
-        ++na;
-    }
+    cudaLaunchAttribute at[3];
     cfg.attrs = at;
-    cfg.numAttrs = na;
+    cfg.numAttrs = base_attrs(ctx, at, 0, ctx->pdl);
     cudaLaunchKernelEx(&cfg, gemm_tma_p<BN, MB, OA, OB, EP>, gb, tilesA, tilesB, nprob);
     ctx->launches++;
 }
@@ -542,15 +554,9 @@ void gemm_shift_launch(gorila_ctx* ctx, const ShiftProb<OA, OB, EP>* probs, int 
     cfg.blockDim = dim3(CFG::THREADS);
     cfg.dynamicSmemBytes = smem;
     cfg.stream = ctx->stream;
-    cudaLaunchAttribute at[1];
-    int na = 0;
-    if (ctx->pdl) {
-        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[na].val.programmaticStreamSerializationAllowed = 1;
-        ++na;
-    }
+    cudaLaunchAttribute at[3];
     cfg.attrs = at;
-    cfg.numAttrs = na;
+    cfg.numAttrs = base_attrs(ctx, at, 0, ctx->pdl);
     cudaLaunchKernelEx(&cfg, gemm_shift<BN, MB, OA, OB, EP>, gb);
     ctx->launches++;
 }
@@ -637,7 +643,7 @@ void gemm_tma_launch(gorila_ctx* ctx, const TmaProb<OA, OB, EP>* probs, int npro
     cfg.blockDim = dim3(128);
     cfg.dynamicSmemBytes = CFG::SMEM;
     cfg.stream = ctx->stream;
-    cudaLaunchAttribute at[2];
+    cudaLaunchAttribute at[4];
     int na = 0;
     if (gb.cluster > 1) {
         at[na].id = cudaLaunchAttributeClusterDimension;
@@ -646,11 +652,7 @@ void gemm_tma_launch(gorila_ctx* ctx, const TmaProb<OA, OB, EP>* probs, int npro
         at[na].val.clusterDim.z = gb.cluster;
         ++na;
     }
-    if (ctx->pdl) {
-        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[na].val.programmaticStreamSerializationAllowed = 1;
-        ++na;
-    }
+    na = base_attrs(ctx, at, na, ctx->pdl);
     cfg.attrs = at;
     cfg.numAttrs = na;
     cudaLaunchKernelEx(&cfg, gemm_tma<BN, MB, OA, OB, EP>, gb);
@@ -1612,6 +1614,26 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
         int dev = 0;
         CU(cudaGetDevice(&dev));
         CU(cudaDeviceGetAttribute(&ctx->num_sms, cudaDevAttrMultiProcessorCount, dev));
+    }
+    {  // L2 persistence window: theta, m, v, G, counters and the replica history (carved contiguously)
+        const char* e = getenv("GORILA_L2_PERSIST");
+        int dev = 0, maxwin = 0, maxpersist = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        cudaDeviceGetAttribute(&maxpersist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        const uint8_t* lo = (const uint8_t*)ctx->theta;
+        const uint8_t* hi = (const uint8_t*)(ctx->rep_f[ctx->H - 1] + ctx->rl.n_f);
+        size_t bytes = std::min<size_t>((size_t)(hi - lo), (size_t)std::min(maxwin, maxpersist));
+        if (e && atoi(e) != 0 && bytes > 0 &&  // opt-in: measured no gain at B = 32 (12.07k vs 12.08k)
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes) == cudaSuccess) {
+            ctx->l2win.base_ptr = (void*)lo;
+            ctx->l2win.num_bytes = bytes;
+            ctx->l2win.hitRatio = 1.0f;
+            ctx->l2win.hitProp = cudaAccessPropertyPersisting;
+            ctx->l2win.missProp = cudaAccessPropertyStreaming;
+            ctx->l2_on = true;
+        }
+        cudaGetLastError();
     }
     CU(cudaStreamCreateWithFlags(&ctx->side, cudaStreamNonBlocking));
     CU(cudaStreamCreateWithFlags(&ctx->side2, cudaStreamNonBlocking));
