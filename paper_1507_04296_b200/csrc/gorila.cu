@@ -26,6 +26,7 @@
 #include "layout.cuh"
 #include "tma_gemm.cuh"
 #include "shift_gemm.cuh"
+#include "tower.cuh"
 
 using namespace gorila;
 
@@ -181,6 +182,7 @@ struct gorila_ctx {
     // 16 conv2 dgrad; the forward layers only when there are more tiles than SMs);
     // GORILA_SHIFT=<mask> selects, 0 = im2col boxes everywhere
     int shift = 31;
+    bool tower = true;  // small-batch bf16 forward: conv1..conv3 fused per (net, sample) (GORILA_TOWER=0: off)
     // side stream for the weight-gradient GEMMs, which are off the dgrad critical path
     // (a fork / join of the round; a graph captures it as parallel branches)
     cudaStream_t side = nullptr;
@@ -821,7 +823,32 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }
     }
     mark(ctx, PH_SAMPLE);
-    PHASE(PH_CONV1F) {
+    // small batches (bf16): conv1 -> conv2 -> conv3 of a (net, sample) in one CTA (tower.cuh)
+    const bool use_tower = !fp32v && ctx->tower && 2 * B <= ctx->num_sms;
+    PHASE(PH_CONV1F) if (use_tower) {
+        TowerParams tp{};
+        tp.in_scale = in_scale;
+        tp.batch = B;
+        for (int z = 0; z < 2; ++z) {
+            TowerNet& N = tp.net[z];
+            N.s_map = sh_conv1_map(ctx, z ? (const void*)s2 : (const void*)s, B);
+            N.w1_map = sh_wk<32, 32, 16, 2>(ctx, z ? (const void*)(tt + RT.w1) : (const void*)(rt + RL.w1), K1).map;
+            N.w2_map = sh_wk<64, 64, 16, 1>(ctx, z ? (const void*)(tt + RT.w2) : (const void*)(rt + RL.w2), K2).map;
+            N.w3_map = sh_wk<64, 128, 9, 0>(ctx, z ? (const void*)(tt + RT.w3) : (const void*)(rt + RL.w3), K3).map;
+            N.a1 = (__nv_bfloat16*)(z ? t1 : a1);
+            N.a2 = (__nv_bfloat16*)(z ? t2 : a2);
+            N.a3 = (__nv_bfloat16*)(z ? t3 : a3);
+            N.b1 = z ? tf + RT.b1 : rf + RL.b1;
+            N.b2 = z ? tf + RT.b2 : rf + RL.b2;
+            N.b3 = z ? tf + RT.b3 : rf + RL.b3;
+        }
+        static bool attr = false;
+        if (!attr) {
+            cudaFuncSetAttribute(k_conv_tower, cudaFuncAttributeMaxDynamicSharedMemorySize, tower::SMEM);
+            attr = true;
+        }
+        launch(ctx, k_conv_tower, dim3(B, 2), dim3(192), tower::SMEM, tp);
+    } else {
     // conv1 fwd (online on s with theta, target on s' with theta^-)
     {
         const int M = B * H1 * H1;
@@ -861,7 +888,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }
     }
     mark(ctx, PH_CONV1F);
-    PHASE(PH_CONV2F) {
+    PHASE(PH_CONV2F) if (!use_tower) {
     // conv2 fwd
     {
         const int M = B * H2 * H2;
@@ -896,7 +923,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }
     }
     mark(ctx, PH_CONV2F);
-    PHASE(PH_CONV3F) {
+    PHASE(PH_CONV3F) if (!use_tower) {
     // conv3 fwd
     {
         const int M = B * H3 * H3;
@@ -1603,6 +1630,8 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     {
         const char* e = getenv("GORILA_PDL");  // GORILA_PDL=0 disables programmatic dependent launch
         ctx->pdl = !(e && atoi(e) == 0);
+        const char* tw = getenv("GORILA_TOWER");
+        if (tw && atoi(tw) == 0) ctx->tower = false;
         const char* sh = getenv("GORILA_SHIFT");
         if (sh) ctx->shift = atoi(sh);
         const char* fn = getenv("GORILA_FC4_NORMAL_MIN");

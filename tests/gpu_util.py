@@ -89,6 +89,34 @@ def run_round_both(g, orc, k, learners, staleness=None):
     return gpu, res
 
 
+def mask_flip_layer(g, acts, max_frac=1e-4, rel=1e-3):
+    """Observed kink rule (R30): the deepest conv / fc4 layer whose ReLU mask differs between
+    the GPU's saved activations of its last learner step (gorila_get_activation) and the oracle's (acts
+    of O.qnet_forward on the same batch), 0 if none. Only ambiguous decisions qualify: at most max_frac
+    of the layer's elements, every one with both values within rel * max|a| of zero; anything else is a
+    real discrepancy and fails here."""
+    B = acts.shape[0]
+    sizes = [("a1", (20, 20, 32)), ("a2", (9, 9, 64)), ("a3", (7, 7, 64)), ("a4", (512,))]
+    off, deepest = 0, 0
+    for l, (name, shp) in enumerate(sizes, start=1):
+        n = int(np.prod(shp))
+        ref = acts[:, off:off + n]
+        off += n
+        got = g.get_activation(name).reshape(B, -1)
+        if len(shp) == 3:  # GPU NHWC -> oracle CHW
+            got = got.reshape((B,) + shp).transpose(0, 3, 1, 2).reshape(B, -1)
+        flips = (got > 0) != (ref > 0)
+        nf = int(flips.sum())
+        if nf == 0:
+            continue
+        big = max(float(np.abs(ref).max()), 1e-30)
+        assert nf <= max(1, max_frac * ref.size), (name, "mask flips", nf, ref.size)
+        assert np.all(np.abs(got[flips]) <= rel * big) and np.all(np.abs(ref[flips]) <= rel * big), \
+            (name, "flipped elements not near zero", float(np.abs(got[flips]).max()), float(np.abs(ref[flips]).max()), big)
+        deepest = l
+    return deepest
+
+
 def round_bf16_vec(t):
     """Vectorised oracle/oracle.c::orc_round_bf16 (frexp, 8 significant bits, ties to even)."""
     m, e = np.frexp(np.asarray(t, np.float64))

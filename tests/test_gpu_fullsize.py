@@ -15,7 +15,7 @@ import pytest
 
 import oracle as O
 import synth
-from gpu_util import LAYER_OF, TOL, ambiguous_layer, per_tensor_rel_l2, rel_inf, rel_l2, replica_of
+from gpu_util import LAYER_OF, TOL, ambiguous_layer, mask_flip_layer, per_tensor_rel_l2, rel_inf, rel_l2, replica_of
 
 pytestmark = pytest.mark.gpu
 
@@ -108,7 +108,7 @@ def test_c2_full_size_sampled_parity(math, check):
         # O8: gradient per tensor (kink rule R30)
         if accepted:
             G_ref = O.qnet_backward(th0, s, acts, dQ, NA, mode)
-            kink = ambiguous_layer(th0, s, NA, mode=mode)
+            kink = max(ambiguous_layer(th0, s, NA, mode=mode), mask_flip_layer(g, acts))
             for name, e in per_tensor_rel_l2(G, G_ref, NA).items():
                 assert e <= (tol["g"] if LAYER_OF[name] > kink else tol["g_kink"]), (k, "G", name, e, kink)
             # O10: the RMSProp step from the GPU's optimizer state, per tensor (+ fp32 state floor R31)
