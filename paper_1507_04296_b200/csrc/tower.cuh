@@ -44,9 +44,26 @@ constexpr int A2_OFF = A_OFF + 4 * A1_PLANE;        // 148 rows x 128 B
 constexpr int A2_BYTES = 19456;
 constexpr int BAR_OFF = A_OFF + 4 * S_PLANE;        // 221184
 constexpr int NB_W = 16 + 16 + 9;
-constexpr int SMEM = BAR_OFF + 8 * (NB_W + 8) + 16 + 1024;
+constexpr int BIAS_OFF = BAR_OFF + 8 * (NB_W + 8);  // 160 floats: b1, b2, b3
+constexpr int SMEM = BIAS_OFF + 160 * 4 + 1024;
 static_assert(A2_OFF + A2_BYTES <= BAR_OFF, "a1 / a2 fit in the s-plane region");
 }  // namespace tower
+
+// trace build: clock64 of CTA (0, 0) at the tower's hand-off points (slots 48.., tools/trace_tower.py)
+#ifdef GORILA_TRACE
+#define TTRACE(slot)                                                        \
+    do {                                                                    \
+        if (blockIdx.x == 0 && blockIdx.y == 0) {                           \
+            unsigned long long t_;                                          \
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_));              \
+            gorila_trace_buf[(slot)] = t_;                                  \
+        }                                                                   \
+    } while (0)
+#else
+#define TTRACE(slot) \
+    do {             \
+    } while (0)
+#endif
 
 // swizzled 16-B store: logical byte offset o inside a region aligned to the swizzle atom;
 // SWIZZLE_{32,64,128}B XOR address bits [4, 4+b) with bits [7, 7+b), b = 1, 2, 3
@@ -76,7 +93,8 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
             *reinterpret_cast<uint4*>(sm + A_OFF + q * S_PLANE + o) = make_uint4(0, 0, 0, 0);
     fence_proxy_async_smem();
     if (tid == 32) {
-        for (int i = 0; i < NB_W + 6; ++i) mbar_init(&w_full[i], i >= NB_W + 4 ? 128 : 1);
+        // act_ready[0]: 128 epilogue threads + warp 0 (which zeroes the operand tails); [1]: 128
+        for (int i = 0; i < NB_W + 6; ++i) mbar_init(&w_full[i], i == NB_W + 4 ? 160 : i == NB_W + 5 ? 128 : 1);
         fence_mbar_init();
     }
     tc_fence_before();
@@ -86,7 +104,9 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
     pdl_trigger();
     const uint32_t tmem = *tmem_slot;
     const uint32_t base = smem_u32(sm);
+    float* s_bias = reinterpret_cast<float*>(sm + BIAS_OFF);
 
+    if (tid == 0) TTRACE(48);
     if (warp == 0) {
         if (lane == 0) {  // loads: the sample's planes first, then the weights in use order
 #pragma unroll
@@ -105,10 +125,22 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
                 mbar_expect_tx(&w_full[32 + c], 64 * 128);
             }
         }
+        // once conv1's MMAs are done the s planes are dead: zero the rows of the a1 planes and of
+        // the a2 buffer that no output row writes (read only by dropped output rows)
+        __syncwarp();
+        mbar_wait(&acc_full[0], 0);
+        for (int q = 0; q < 4; ++q)
+            for (int o = 100 * 64 + lane * 16; o < A1_PLANE; o += 32 * 16)
+                *reinterpret_cast<uint4*>(sm + A_OFF + q * A1_PLANE + o) = make_uint4(0, 0, 0, 0);
+        for (int o = 81 * 128 + lane * 16; o < A2_BYTES; o += 32 * 16)
+            *reinterpret_cast<uint4*>(sm + A2_OFF + o) = make_uint4(0, 0, 0, 0);
+        fence_proxy_async_smem();
+        mbar_arrive(&act_ready[0]);
     } else if (warp == 1) {
         if (lane == 0) {  // MMA issuer: conv1 -> TMEM [0,128), conv2 -> [128,192), conv3 -> [192,256)
             constexpr uint32_t ID32 = umma_idesc_bf16(128, 32), ID64 = umma_idesc_bf16(128, 64);
             mbar_wait(s_full, 0);
+            TTRACE(49);
             tc_fence_after();
             {
                 const uint64_t ad0 = umma_desc_sw(base + A_OFF, 32), bd0 = umma_desc_sw(base + W1_OFF, 32);
@@ -123,8 +155,10 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
                                   bd0 + ((c * W1_CH) >> 4), ID32, c > 0 ? 1u : 0u);
                 }
                 umma_commit(&acc_full[0]);
+                TTRACE(50);
             }
             mbar_wait(&act_ready[0], 0);  // a1 planes written by the epilogue warps
+            TTRACE(51);
             tc_fence_after();
             {
                 const uint64_t ad0 = umma_desc_sw(base + A_OFF, 64), bd0 = umma_desc_sw(base + W2_OFF, 64);
@@ -139,8 +173,10 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
                                   bd0 + ((c * W2_CH + kk * 32) >> 4), ID64, (c > 0 || kk > 0) ? 1u : 0u);
                 }
                 umma_commit(&acc_full[1]);
+                TTRACE(52);
             }
             mbar_wait(&act_ready[1], 0);  // a2 rows written
+            TTRACE(53);
             tc_fence_after();
             {
                 const uint64_t ad0 = umma_desc_sw(base + A2_OFF, 128), bd0 = umma_desc_sw(base + W3_OFF, 128);
@@ -155,21 +191,22 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
                                   bd0 + ((c * W3_CH + kk * 32) >> 4), ID64, (c > 0 || kk > 0) ? 1u : 0u);
                 }
                 umma_commit(&acc_full[2]);
+                TTRACE(54);
             }
         }
     } else {  // epilogue warps 2..5
         const int quad = warp & 3, etid = tid - 64;  // etid 0..127
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
+        for (int i = etid; i < 160; i += 128)  // the layers' biases, once (not per output element)
+            s_bias[i] = i < 32 ? N.b1[i] : i < 96 ? N.b2[i - 32] : N.b3[i - 96];
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // the epilogue warps only
+        const float* sb1 = s_bias;
+        const float* sb2 = s_bias + 32;
+        const float* sb3 = s_bias + 96;
         // ---- conv1: a1 = bf16(ReLU(v / 255 + b1)) -> global and conv2's phase planes
         mbar_wait(&acc_full[0], 0);
+        if (etid == 0) TTRACE(55);
         tc_fence_after();
-        // the s planes are dead (conv1's MMAs completed): zero the rows of the a1 planes / a2
-        // buffer that no output row writes (read only by dropped output rows)
-        for (int q = 0; q < 4; ++q)
-            for (int o = 100 * 64 + etid * 16; o < A1_PLANE; o += 128 * 16)
-                *reinterpret_cast<uint4*>(sm + A_OFF + q * A1_PLANE + o) = make_uint4(0, 0, 0, 0);
-        for (int o = 81 * 128 + etid * 16; o < A2_BYTES; o += 128 * 16)
-            *reinterpret_cast<uint4*>(sm + A2_OFF + o) = make_uint4(0, 0, 0, 0);
 #pragma unroll 1
         for (int mb = 0; mb < 4; ++mb) {
             const int m = mb * 128 + quad * 32 + lane, Y = m / 21, X = m - 21 * Y;
@@ -184,8 +221,8 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
                 uint32_t w[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    const float x0 = fmaxf(v[2 * e] * p.in_scale + N.b1[h * 16 + 2 * e], 0.f);
-                    const float x1 = fmaxf(v[2 * e + 1] * p.in_scale + N.b1[h * 16 + 2 * e + 1], 0.f);
+                    const float x0 = fmaxf(v[2 * e] * p.in_scale + sb1[h * 16 + 2 * e], 0.f);
+                    const float x1 = fmaxf(v[2 * e + 1] * p.in_scale + sb1[h * 16 + 2 * e + 1], 0.f);
                     __nv_bfloat162 t = __floats2bfloat162_rn(x0, x1);
                     w[e] = *reinterpret_cast<uint32_t*>(&t);
                 }
@@ -199,9 +236,11 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
         }
         fence_proxy_async_smem();  // generic-proxy smem stores -> visible to tcgen05.mma
         tc_fence_before();
+        if (etid == 0) TTRACE(56);
         mbar_arrive(&act_ready[0]);
         // ---- conv2: a2 -> global and conv3's flat rows
         mbar_wait(&acc_full[1], 0);
+        if (etid == 0) TTRACE(57);
         tc_fence_after();
         {
             const int r = quad * 32 + lane, Y = r / 10, X = r - 10 * Y;
@@ -216,8 +255,8 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
                 uint32_t w[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    const float x0 = fmaxf(v[2 * e] + N.b2[h * 16 + 2 * e], 0.f);
-                    const float x1 = fmaxf(v[2 * e + 1] + N.b2[h * 16 + 2 * e + 1], 0.f);
+                    const float x0 = fmaxf(v[2 * e] + sb2[h * 16 + 2 * e], 0.f);
+                    const float x1 = fmaxf(v[2 * e + 1] + sb2[h * 16 + 2 * e + 1], 0.f);
                     __nv_bfloat162 t = __floats2bfloat162_rn(x0, x1);
                     w[e] = *reinterpret_cast<uint32_t*>(&t);
                 }
@@ -230,9 +269,11 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
         }
         fence_proxy_async_smem();
         tc_fence_before();
+        if (etid == 0) TTRACE(58);
         mbar_arrive(&act_ready[1]);
         // ---- conv3: a3 -> global
         mbar_wait(&acc_full[2], 0);
+        if (etid == 0) TTRACE(59);
         tc_fence_after();
         {
             const int r = quad * 32 + lane, y = r / 9, x = r - 9 * y;
@@ -246,8 +287,8 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
                 uint32_t w[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    const float x0 = fmaxf(v[2 * e] + N.b3[h * 16 + 2 * e], 0.f);
-                    const float x1 = fmaxf(v[2 * e + 1] + N.b3[h * 16 + 2 * e + 1], 0.f);
+                    const float x0 = fmaxf(v[2 * e] + sb3[h * 16 + 2 * e], 0.f);
+                    const float x1 = fmaxf(v[2 * e + 1] + sb3[h * 16 + 2 * e + 1], 0.f);
                     __nv_bfloat162 t = __floats2bfloat162_rn(x0, x1);
                     w[e] = *reinterpret_cast<uint32_t*>(&t);
                 }
@@ -256,6 +297,7 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
             }
         }
     }
+    if (tid == 64) TTRACE(60);
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, 256);
