@@ -222,6 +222,19 @@ GORILA_API gorila_status gorila_set_learner_state(gorila_ctx* ctx, int32_t learn
 GORILA_API gorila_status gorila_get_grad(gorila_ctx* ctx, float* g);
 /* Q and Q-hat [B][nA] of the last learner_step of local learner `learner`. */
 GORILA_API gorila_status gorila_get_q(gorila_ctx* ctx, int32_t learner, float* q, float* qhat);
+/* NEXT row f3 (acting). epsilon-greedy actions for n <= batch stacked states on the
+ * latest theta^+ replica (Alg.1 P:118 "select a_t with the epsilon-greedy policy on
+ * Q(s; theta)"; P:187 epsilon annealed linearly from 1 to eps_final over anneal_steps
+ * global steps). states: u8 [n][4][84][84] (replay_sample's s layout), device pointer if
+ * states_on_device else host. Per state i, x = Philox4x32-10(ctr = {i, actor_id,
+ * step lo, (step hi & 0xffffff) | 5 << 24}, key = seed): explore iff x0 < eps * 2^32
+ * (fp64), action = floor(x1 * nA / 2^32); else the argmax of Q with the lowest index on
+ * ties. actions_out: host int32 [n]; q_out (nullable): host f32 [n][nA]. Synchronises the
+ * library stream; uses the learner scratch (not concurrently with learner_step).
+ * E_SHAPE if n < 1 or n > batch. */
+GORILA_API gorila_status gorila_act(gorila_ctx* ctx, const uint8_t* states, int32_t n, uint64_t global_step,
+                                    uint64_t actor_id, double eps_final, int64_t anneal_steps,
+                                    int32_t states_on_device, int32_t* actions_out, float* q_out);
 /* Intermediate tensors of the last learner step (diagnostics; the scratch is
  * shared by the local learners, so this is the last learner that ran). which:
  * 0 s, 1 a1, 2 a2, 3 a3 (NHWC [B][H][W][C], element type of the math mode:

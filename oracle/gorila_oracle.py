@@ -468,3 +468,44 @@ class GorilaOracle:
                 L.last_sync = self.V
         return {"learners": per, "n_accepted": n_acc, "version_before": V0, "version_after": self.V,
                 "synced": synced}
+
+
+# ----------------------------------------------------------------- NEXT row f3: acting
+# Alg.1 P:118 "select an action a_t with the epsilon-greedy policy on Q(s; theta)"; epsilon
+# annealed linearly from 1 to its final value over the first million updates.
+TAG_ACT = 5
+
+
+def epsilon(global_step, eps_final, anneal_steps):
+    """Linear anneal from 1 to eps_final over anneal_steps global steps, then constant."""
+    if anneal_steps <= 0 or global_step >= anneal_steps:
+        return float(eps_final)
+    return 1.0 - (1.0 - float(eps_final)) * (float(global_step) / float(anneal_steps))
+
+
+def act_draws(n, actor_id, global_step, seed):
+    """Per state i: Philox4x32-10(ctr = {i, actor, step lo, (step hi & 0xffffff) | TAG_ACT << 24},
+    key = {seed lo, seed hi}) -> (u = x0 * 2^-32 for the explore test, x1 for the random action)."""
+    key = np.array([seed & 0xffffffff, (seed >> 32) & 0xffffffff], np.uint32)
+    out = []
+    for i in range(n):
+        ctr = np.array([i, actor_id & 0xffffffff, global_step & 0xffffffff,
+                        ((global_step >> 32) & 0xffffff) | (TAG_ACT << 24)], np.uint32)
+        x = philox(ctr, key)
+        out.append((int(x[0]), int(x[1])))
+    return out
+
+
+def act(theta, s, n_actions, mode, global_step, actor_id, eps_final, anneal_steps, seed):
+    """epsilon-greedy actions on Q(s; theta): explore iff x0 < eps * 2^32 (compared in fp64 on the
+    integer x0), then a = floor(x1 * nA / 2^32); else the argmax with the lowest index on ties.
+    Returns (actions, Q)."""
+    Q, _ = qnet_forward(theta, s, n_actions, mode)
+    eps = epsilon(global_step, eps_final, anneal_steps)
+    acts = np.zeros(len(s), np.int32)
+    for i, (x0, x1) in enumerate(act_draws(len(s), actor_id, global_step, seed)):
+        if float(x0) < eps * 4294967296.0:
+            acts[i] = (x1 * n_actions) >> 32
+        else:
+            acts[i] = int(np.argmax(Q[i]))  # numpy argmax: first maximal index
+    return acts, Q

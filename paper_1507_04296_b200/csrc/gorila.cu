@@ -2362,6 +2362,45 @@ gorila_status gorila_get_grad(gorila_ctx* ctx, float* g) {
     return GORILA_OK;
 }
 
+gorila_status gorila_act(gorila_ctx* ctx, const uint8_t* states, int32_t n, uint64_t global_step,
+                        uint64_t actor_id, double eps_final, int64_t anneal_steps, int32_t states_on_device,
+                        int32_t* actions_out, float* q_out) {
+    if (!ctx || !states || !actions_out) return fail(GORILA_E_INVALID, "null argument");
+    if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned");
+    if (n < 1 || n > ctx->B) return fail(GORILA_E_SHAPE, "n must be in [1, batch]");
+    cudaStream_t st = ctx->stream;
+    const size_t sbytes = (size_t)n * NSTACK * FRAME_BYTES;
+    const uint8_t* src = states;
+    if (!states_on_device) {  // stage through the (idle) conversion scratch
+        CU(cudaMemcpyAsync(ctx->tmp_int, states, sbytes, cudaMemcpyHostToDevice, st));
+        src = reinterpret_cast<const uint8_t*>(ctx->tmp_int);
+    }
+    const bool fp32 = ctx->cfg.math == GORILA_MATH_FP32;
+    const int64_t total = (int64_t)n * (FRAME_BYTES / 4);
+    const int grid = (int)std::min<int64_t>(148 * 8, (total + 255) / 256);
+    if (fp32) launch(ctx, k_stage_states<float>, dim3(grid), dim3(256), 0, src, n, (float*)ctx->s);
+    else launch(ctx, k_stage_states<__nv_bfloat16>, dim3(grid), dim3(256), 0, src, n, (__nv_bfloat16*)ctx->s);
+    // the forward phases of a learner step on the latest replica (slot of round dev_round_expect)
+    const uint32_t fwd = (1u << PH_CONV1F) | (1u << PH_CONV2F) | (1u << PH_CONV3F) | (1u << PH_FC4F);
+    const uint64_t rnd = ctx->dev_round_expect == ~0ull ? 0 : ctx->dev_round_expect;
+    gorila_status s = fp32 ? run_learner<float>(ctx, 0, rnd, 0, 0, fwd) : run_learner<__nv_bfloat16>(ctx, 0, rnd, 0, 0, fwd);
+    if (s != GORILA_OK) return s;
+    const int slot = (int)(rnd % (uint64_t)ctx->H);
+    const float* rf = ctx->rep_f[slot];
+    const double eps = anneal_steps <= 0 || (int64_t)global_step >= anneal_steps
+                           ? eps_final
+                           : 1.0 - (1.0 - eps_final) * ((double)global_step / (double)anneal_steps);
+    const uint2 key = make_uint2((uint32_t)ctx->cfg.seed, (uint32_t)(ctx->cfg.seed >> 32));
+    int32_t* dact = reinterpret_cast<int32_t*>(ctx->sidx);  // learner scratch (rewritten by the sampler)
+    float* dq = ctx->dQ;                                     // learner scratch [B][nA]
+    launch(ctx, k_act_head, dim3(n), dim3(256), 0, (const float*)ctx->a4, rf + ctx->rl.w5, rf + ctx->rl.b5, ctx->nA,
+           global_step, (uint32_t)actor_id, key, eps, dact, dq);
+    CU(cudaMemcpyAsync(actions_out, dact, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, st));
+    if (q_out) CU(cudaMemcpyAsync(q_out, dq, sizeof(float) * n * ctx->nA, cudaMemcpyDeviceToHost, st));
+    CU(cudaStreamSynchronize(st));
+    return GORILA_OK;
+}
+
 gorila_status gorila_get_activation(gorila_ctx* ctx, int32_t which, void* host, uint64_t bytes) {
     if (!ctx || !host) return fail(GORILA_E_INVALID, "null argument");
     const uint64_t B = ctx->B, e = ctx->esz;

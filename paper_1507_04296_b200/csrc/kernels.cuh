@@ -357,6 +357,55 @@ __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, c
     }
 }
 
+// ------------------------------------------------------------------------- acting (NEXT row f3)
+// states u8 [n][4][84][84] -> the conv input layout (NHWC, T), 4 pixels per thread
+template <typename T>
+__global__ void k_stage_states(const uint8_t* __restrict__ st, int n, T* __restrict__ s_out) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t total = (int64_t)n * (FRAME_BYTES / 4);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / (FRAME_BYTES / 4), px = (i - b * (FRAME_BYTES / 4)) * 4;
+        uint32_t c4[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) c4[c] = *reinterpret_cast<const uint32_t*>(st + (b * 4 + c) * FRAME_BYTES + px);
+        T* dst = s_out + (b * FRAME_BYTES + px) * NSTACK;
+#pragma unroll
+        for (int p = 0; p < 4; ++p)
+#pragma unroll
+            for (int c = 0; c < 4; ++c) dst[p * 4 + c] = fromf<T>((float)((c4[c] >> (8 * p)) & 0xffu));
+    }
+}
+// Q = a4 . W5^T + b5 (fp32), then the epsilon-greedy decision (one block per state)
+constexpr uint32_t TAG_ACT = 5u;
+__global__ void __launch_bounds__(256) k_act_head(const float* __restrict__ a4, const float* __restrict__ w5,
+                                                  const float* __restrict__ b5, int nA, uint64_t step,
+                                                  uint32_t actor, uint2 key, double eps, int32_t* actions,
+                                                  float* q) {
+    pdl_wait();
+    pdl_trigger();
+    const int i = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    __shared__ float qs[32];
+    const float* x = a4 + (int64_t)i * FC4_OUT;
+    for (int a = warp; a < nA; a += 8) {
+        float acc = 0.f;
+        for (int k = lane; k < FC4_OUT; k += 32) acc = fmaf(x[k], w5[a * FC4_OUT + k], acc);
+        acc = warp_sum(acc);
+        if (lane == 0) qs[a] = acc + b5[a];
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int best = 0;
+        for (int a = 1; a < nA; ++a)
+            if (qs[a] > qs[best]) best = a;  // lowest index on ties
+        const uint4 r = philox4x32_10(
+            make_uint4((uint32_t)i, actor, (uint32_t)step, (uint32_t)((step >> 32) & 0xffffffu) | (TAG_ACT << 24)), key);
+        const bool explore = (double)r.x < eps * 4294967296.0;
+        actions[i] = explore ? (int32_t)(((uint64_t)r.y * (uint64_t)nA) >> 32) : best;
+        for (int a = 0; a < nA; ++a) q[i * nA + a] = qs[a];
+    }
+}
+
 // ------------------------------------------------------------------------- bias gradients
 // db_l[o] = sum_m g_l[m][o], layers 1..4: block (chunk, l) sums rows [chunk*rows_per, ...) with
 // coalesced row reads and a fixed-order in-block reduction -> part[l][chunk][o]; K10 sums chunks.

@@ -60,7 +60,7 @@ class RoundInfo(ctypes.Structure):
 EXPORTS = ["gorila_param_count", "gorila_workspace_bytes", "gorila_init", "gorila_destroy", "gorila_last_error",
            "replay_insert", "replay_sample", "learner_step", "ps_apply_shard", "sync_target", "gorila_get_state",
            "gorila_set_state", "gorila_get_learner_state", "gorila_set_learner_state", "gorila_get_grad",
-           "gorila_get_q", "gorila_get_activation", "gorila_kernel_launches", "gorila_profile_enable", "gorila_profile_read",
+           "gorila_get_q", "gorila_get_activation", "gorila_act", "gorila_kernel_launches", "gorila_profile_enable", "gorila_profile_read",
            "gorila_profile_phase_count", "gorila_profile_phase_name", "gorila_nccl_unique_id", "gorila_round",
            "gorila_bench_phase", "gorila_debug_trace"]
 
@@ -96,6 +96,7 @@ def load(build_if_missing=True):
     L.gorila_get_grad.argtypes = [P, P]
     L.gorila_get_q.argtypes = [P, i32, P, P]
     L.gorila_get_activation.argtypes = [P, i32, P, u64]
+    L.gorila_act.argtypes = [P, P, i32, u64, u64, ctypes.c_double, i64, i32, P, P]
     L.gorila_kernel_launches.argtypes = [P]
     L.gorila_kernel_launches.restype = u64
     L.gorila_profile_enable.argtypes = [P, i32]
@@ -322,6 +323,19 @@ class Gorila:
         out = np.zeros((self.batch,) + shp, np.uint16 if bf else np.float32)
         _check(load().gorila_get_activation(self.h, which, out.ctypes.data, out.nbytes))
         return (out.astype(np.uint32) << 16).view(np.float32) if bf else out
+
+    def act(self, states, global_step, actor_id=0, eps_final=0.1, anneal_steps=1_000_000):
+        """NEXT row f3: epsilon-greedy actions (and Q) for stacked u8 states [n][4][84][84] (host
+        numpy or device tensor) on the latest theta^+ replica."""
+        n = int(states.shape[0])
+        sp, dev = _ptr(states)
+        if dev:
+            self.stream.wait_stream(self.torch.cuda.current_stream(self.device))
+        acts = np.zeros(n, np.int32)
+        q = np.zeros((n, self.n_actions), np.float32)
+        _check(load().gorila_act(self.h, sp, n, int(global_step), int(actor_id), float(eps_final), int(anneal_steps),
+                                 int(dev), acts.ctypes.data, q.ctypes.data))
+        return acts, q
 
     def kernel_launches(self):
         return int(load().gorila_kernel_launches(self.h))
