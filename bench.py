@@ -34,10 +34,15 @@ def fc5_mac(nA):
     return 512 * nA
 
 
-def phase_work(phase, B, nA, P, esz, n_msg=1):
+def phase_work(phase, B, nA, P, esz, n_msg=1, tower=False):
     """(bound, algorithmic amount per launch-group, unit) of a profiled phase. n_msg: gradient
-    buffers the apply reads (per-message mode reads one per local learner)."""
+    buffers the apply reads (per-message mode reads one per local learner). tower: the small-batch
+    conv tower runs conv1..conv3 of both nets inside the conv1_fwd phase."""
     fl = lambda mac: 2.0 * mac * B  # noqa: E731
+    if tower and phase in ("conv2_fwd", "conv3_fwd"):
+        return None
+    if tower and phase == "conv1_fwd":
+        return ("tensor", 2 * fl(MAC["conv1"] + MAC["conv2"] + MAC["conv3"]))
     table = {
         "conv1_fwd": ("tensor", 2 * fl(MAC["conv1"])), "conv2_fwd": ("tensor", 2 * fl(MAC["conv2"])),
         "conv3_fwd": ("tensor", 2 * fl(MAC["conv3"])), "fc4_fwd": ("tensor", 2 * fl(MAC["fc4"])),
@@ -363,6 +368,9 @@ def main():
     peaks = read_peaks()
     P = g.P
     n_msg = L if args.ps_mode == "per_message" else 1
+    # the library's small-batch conv tower (tower.cuh): bf16, 2B <= SMs, not disabled
+    tower = (args.math == "bf16" and os.environ.get("GORILA_TOWER", "1") != "0"
+             and 2 * args.batch <= torch.cuda.get_device_properties(local_rank).multi_processor_count)
     esz = 2 if args.math == "bf16" else 4
     total_prof = sum(phases.values())
     per_launch_ms = {p: v / max(n_prof, 1) for p, v in phases.items()}
@@ -370,7 +378,7 @@ def main():
     dom = max(iso_ms, key=lambda p: iso_ms[p])
 
     def roof(p):
-        w = phase_work(p, args.batch, args.n_actions, P, esz, n_msg)
+        w = phase_work(p, args.batch, args.n_actions, P, esz, n_msg, tower)
         if w is None or iso_ms.get(p, 0.0) <= 0.0:
             return None
         bound, amount = w
@@ -388,7 +396,7 @@ def main():
 
     dom_roof = roof(dom)
     if dom_roof is None:  # dominant phase without an algorithmic model: report the biggest modelled one
-        modelled = [p for p in iso_ms if phase_work(p, args.batch, args.n_actions, P, esz, n_msg)]
+        modelled = [p for p in iso_ms if phase_work(p, args.batch, args.n_actions, P, esz, n_msg, tower)]
         dom = max(modelled, key=lambda p: iso_ms[p])
         dom_roof = roof(dom)
     traffic = None
