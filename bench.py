@@ -361,7 +361,9 @@ def main():
     # per-phase marginal device time, kernels re-launched back to back (warm L2, PDL as in the round)
     iso = {}
     for ph in phases:
-        if ph in ("td", "step_misc", "reduce_scatter", "all_gather") or (ph == "pack" and world == 1):
+        # not kernels of the round: td / misc are markers, the replica pack is fused into the apply
+        # (1 GPU) or the peer-memory exchange (N > 1); RS / AG are the NCCL fallback's
+        if ph in ("td", "step_misc", "reduce_scatter", "all_gather", "pack"):
             continue
         iso[ph] = g.bench_phase(ph, iters=200)
 
