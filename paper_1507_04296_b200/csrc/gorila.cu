@@ -156,6 +156,8 @@ struct gorila_ctx {
     std::map<std::vector<uint64_t>, CUtensorMap> tmaps;  // TMA descriptors, encoded once per (buffer, view)
     bool tma_failed = false;
     int num_sms = 148;
+    unsigned int* apply_counter = nullptr;  // last-block detection of k_apply's fused sync copy
+    bool sync_fused_now = false;            // this round's k_apply did the target-sync copy
     // L2 persistence window over the parameter-server state (theta, m, v, G, replicas): the
     // optimizer's working set stays resident across rounds (GORILA_L2_PERSIST=1: on)
     cudaAccessPolicyWindow l2win{};
@@ -1220,38 +1222,57 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }
     }
     mark(ctx, PH_CONV1WG);
+    // K10's segments: 0 W1, 1 W2, 2 W3, 3..6 b1..b4 (wide: many partials per element), 7 W5 + b5
+    WgradReduceParams all{};
+    {
+        all.part[0] = ctx->part_w[0]; all.part[1] = ctx->part_w[1]; all.part[2] = ctx->part_w[2];
+        all.splits[0] = ctx->split_w[0];
+        all.splits[1] = ctx->split_w[1];
+        all.splits[2] = ctx->split_w[2];
+        all.count[0] = (int64_t)C1_OUT * K1; all.count[1] = (int64_t)C2_OUT * K2; all.count[2] = (int64_t)C3_OUT * K3;
+        all.off[0] = OFF_W1; all.off[1] = OFF_W2; all.off[2] = OFF_W3;
+        const int bc[4] = {C1_OUT, C2_OUT, C3_OUT, FC4_OUT};
+        const int64_t boff[4] = {OFF_B1, OFF_B2, OFF_B3, OFF_B4};
+        const float* bp = ctx->part_b;
+        for (int l = 0; l < 4; ++l) {
+            all.part[3 + l] = bp; all.splits[3 + l] = ctx->bias_chunks; all.count[3 + l] = bc[l];
+            all.off[3 + l] = boff[l];
+            bp += (int64_t)ctx->bias_chunks * bc[l];
+        }
+        all.part[7] = ctx->part5; all.splits[7] = (B + fc5_rows(B) - 1) / fc5_rows(B);  // W5 and b5 (contiguous)
+        all.count[7] = (int64_t)nA * (FC4_OUT + 1); all.off[7] = OFF_W5;
+        for (int l = 3; l < 7; ++l) all.wide[l] = 1;
+        all.nseg = 8;
+        all.accumulate = accumulate;
+    }
+    auto pick = [&](std::initializer_list<int> segs) {
+        WgradReduceParams p{};
+        for (int l : segs) {
+            p.part[p.nseg] = all.part[l]; p.splits[p.nseg] = all.splits[l]; p.count[p.nseg] = all.count[l];
+            p.off[p.nseg] = all.off[l]; p.wide[p.nseg] = all.wide[l];
+            ++p.nseg;
+        }
+        p.accumulate = all.accumulate;
+        return p;
+    };
+    static const bool split_red = [] {  // GORILA_SPLIT_REDUCE=0: one K10 after the join
+        const char* e = getenv("GORILA_SPLIT_REDUCE");
+        return !(e && atoi(e) == 0);
+    }();
     PHASE(PH_BIASG) {
     // bias gradients b1..b4 (coalesced partials; reduced by K10)
     OnSide on_side(ctx, fk);
     launch(ctx, k_bias_partial<T>, dim3(ctx->bias_chunks, 4), dim3(256), 0, (const T*)g1, (const T*)g2, (const T*)g3,
            (const T*)g4, B, ctx->part_b, ctx->bias_chunks);
+    // forked round: the side stream reduces what it produced (conv2 / conv3 weights, the biases)
+    // while the main stream finishes conv1's weight gradient
+    if (split_red && fk && (phases & (1u << PH_WGRED))) launch(ctx, k_wgrad_reduce, dim3(148 * 2), dim3(256), 0, pick({1, 2, 3, 4, 5, 6}), Gd);
     }
     mark(ctx, PH_BIASG);
     if (fk) join_side(ctx);
     PHASE(PH_WGRED) {
-    // K10: fixed-order reduction of the conv wgrad partials into G
-    {
-        WgradReduceParams p{};
-        p.part[0] = ctx->part_w[0]; p.part[1] = ctx->part_w[1]; p.part[2] = ctx->part_w[2];
-        p.splits[0] = ctx->split_w[0];
-        p.splits[1] = ctx->split_w[1];
-        p.splits[2] = ctx->split_w[2];
-        p.count[0] = (int64_t)C1_OUT * K1; p.count[1] = (int64_t)C2_OUT * K2; p.count[2] = (int64_t)C3_OUT * K3;
-        p.off[0] = OFF_W1; p.off[1] = OFF_W2; p.off[2] = OFF_W3;
-        const int bc[4] = {C1_OUT, C2_OUT, C3_OUT, FC4_OUT};
-        const int64_t boff[4] = {OFF_B1, OFF_B2, OFF_B3, OFF_B4};
-        const float* bp = ctx->part_b;
-        for (int l = 0; l < 4; ++l) {
-            p.part[3 + l] = bp; p.splits[3 + l] = ctx->bias_chunks; p.count[3 + l] = bc[l]; p.off[3 + l] = boff[l];
-            bp += (int64_t)ctx->bias_chunks * bc[l];
-        }
-        p.part[7] = ctx->part5; p.splits[7] = (B + fc5_rows(B) - 1) / fc5_rows(B);  // W5 and b5 (contiguous)
-        p.count[7] = (int64_t)nA * (FC4_OUT + 1); p.off[7] = OFF_W5;
-        for (int l = 3; l < 7; ++l) p.wide[l] = 1;
-        p.nseg = 8;
-        p.accumulate = accumulate;
-        launch(ctx, k_wgrad_reduce, dim3(148 * 2), dim3(256), 0, p, Gd);
-    }
+    // K10: fixed-order reduction of the conv wgrad partials into G (the rest of it when forked)
+    launch(ctx, k_wgrad_reduce, dim3(148 * 2), dim3(256), 0, (fk && split_red) ? pick({0, 7}) : all, Gd);
     }
     mark(ctx, PH_WGRED);
     CU(cudaGetLastError());
@@ -1378,6 +1399,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     uint64_t* pflags = c.take<uint64_t>(6 * MAX_W);
     uint64_t* p2p_epoch = c.take<uint64_t>(1);
     unsigned int* p2p_counter = c.take<unsigned int>(2);
+    unsigned int* apply_counter = c.take<unsigned int>(1);
     std::vector<void*> rep_t(H);
     std::vector<float*> rep_f(H);
     for (int h = 0; h < H; ++h) {
@@ -1466,7 +1488,8 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         ctx->G_all = G; ctx->per_msg = cfg->ps_mode == 1;
         ctx->round_info = rinfo;
         ctx->n_acc_local = nacc; ctx->Vhist = Vhist; ctx->dev_round = dev_round; ctx->head_counter = head_counter;
-        ctx->pflags = pflags; ctx->p2p_epoch = p2p_epoch; ctx->p2p_counter = p2p_counter; ctx->rep_t = rep_t; ctx->rep_f = rep_f; ctx->learners = lrs;
+        ctx->pflags = pflags; ctx->p2p_epoch = p2p_epoch; ctx->p2p_counter = p2p_counter;
+        ctx->apply_counter = apply_counter; ctx->rep_t = rep_t; ctx->rep_f = rep_f; ctx->learners = lrs;
         ctx->s = s; ctx->s2 = s2; ctx->a1 = a1; ctx->a2 = a2; ctx->a3 = a3; ctx->a4 = a4;
         ctx->t1 = t1; ctx->t2 = t2; ctx->t3 = t3; ctx->t4 = t4;
         ctx->g1 = g1; ctx->g2 = g2; ctx->g3 = g3; ctx->g4 = g4;
@@ -1626,6 +1649,7 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     CU(cudaMemsetAsync(ctx->pflags, 0, sizeof(uint64_t) * 6 * MAX_W, st));
     CU(cudaMemsetAsync(ctx->p2p_epoch, 0, sizeof(uint64_t), st));
     CU(cudaMemsetAsync(ctx->p2p_counter, 0, sizeof(unsigned int) * 2, st));
+    CU(cudaMemsetAsync(ctx->apply_counter, 0, sizeof(unsigned int), st));
     ctx->dev_round_expect = 0;
     {
         const char* e = getenv("GORILA_PDL");  // GORILA_PDL=0 disables programmatic dependent launch
@@ -2041,6 +2065,21 @@ gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info*
         p.rep_t = ctx->rep_t[slot];
         p.rep_f = ctx->rep_f[slot];
         p.vhist_dst = ctx->Vhist + slot;
+        // gorila_round: the optimizer also writes theta^- of the learners whose sync fires
+        static const bool sync_fuse = [] {  // opt-in: measured 0.9 us/step slower than the predicated pack
+            const char* e = getenv("GORILA_SYNC_FUSE");
+            return e && atoi(e) != 0;
+        }();
+        ctx->sync_fused_now = sync_fuse && ctx->fused_sync && !ctx->per_msg;
+        if (ctx->sync_fused_now) {
+            p.sync_copy = 1;
+            p.counter = ctx->apply_counter;
+            for (int i = 0; i < p.n_sync; ++i) {
+                const Learner& l = ctx->learners[ctx->sync_ids[i]];
+                p.sync_tm_t[i] = l.tminus_t;
+                p.sync_tm_f[i] = l.tminus_f;
+            }
+        }
     }
     if (ctx->per_msg) {  // W == 1 here (W > 1 runs the peer-memory exchange)
         MsgParams mp{};
@@ -2091,7 +2130,8 @@ gorila_status sync_target(gorila_ctx* ctx, const int32_t* learners, int32_t n, i
         if (!ctx->fused_sync)  // gorila_round: k_apply already took the decision
             launch(ctx, k_sync_decide, dim3(1), dim3(1), 0, l.stats, (const uint64_t*)ctx->V,
                    (int64_t)ctx->cfg.target_period, (int)force, l.sync_flag);
-        if (ctx->p2p && ctx->W > 1) {  // ranks hold only their own fp32 slice: copy the latest replica
+        if (ctx->sync_fused_now) {  // k_apply wrote theta^- when it fired
+        } else if (ctx->p2p && ctx->W > 1) {  // ranks hold only their own fp32 slice: copy the latest replica
             const int slot = (int)(ctx->dev_round_expect % (uint64_t)ctx->H);
             const int64_t nt = (int64_t)ctx->rl.n_t * ctx->esz;
             launch(ctx, k_copy_replica, dim3(148 * 2), dim3(256), 0, (const uint4*)ctx->rep_t[slot],
@@ -2140,6 +2180,7 @@ gorila_status gorila_round(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
         r = ps_apply_shard(ctx, round, nullptr);
         if (r == GORILA_OK) r = sync_target(ctx, learners, n, 0, nullptr);
         ctx->fused_sync = false;
+        ctx->sync_fused_now = false;
         return r;
     };
     auto it = graphable ? ctx->graphs.find(key) : ctx->graphs.end();

@@ -537,6 +537,12 @@ struct ApplyParams {
     uint64_t* vhist_dst;
     int nA;
     int64_t base;          // internal index of this slice's element 0
+    // fused target-sync copy (gorila_round, 1 GPU): when learner i's sync fires, the new replica is
+    // also written into its theta^- (no separate pack); bookkeeping then moves to the last block
+    void* sync_tm_t[8];
+    float* sync_tm_f[8];
+    int sync_copy;
+    unsigned int* counter;
 };
 // Centered RMSProp (reading R2) / AdaGrad on the mean of the accepted gradients
 // (reading R12, R25); V += |Acc|. float4-vectorised, grid-stride.
@@ -559,11 +565,37 @@ GORILA_DEV void emit4(const ApplyParams& p, int64_t e4, const float* tv) {
 }
 
 template <typename T>
+GORILA_DEV void emit4_to(void* rep_t, float* rep_f, int nA, int64_t idx, const float* tv) {
+    const ReplicaLayout L = replica_layout(nA);
+    const int64_t slot = replica_slot(L, idx);
+    if (slot >= 0) {
+        T* dst = reinterpret_cast<T*>(rep_t) + slot;
+        if constexpr (sizeof(T) == 2) {
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(tv[0], tv[1]), h1 = __floats2bfloat162_rn(tv[2], tv[3]);
+            *reinterpret_cast<uint2*>(dst) =
+                make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+        } else {
+            *reinterpret_cast<float4*>(dst) = make_float4(tv[0], tv[1], tv[2], tv[3]);
+        }
+    } else {
+        *reinterpret_cast<float4*>(rep_f + (-slot - 1)) = make_float4(tv[0], tv[1], tv[2], tv[3]);
+    }
+}
+
+template <typename T>
 __global__ void __launch_bounds__(256) k_apply(ApplyParams p) {
     pdl_wait();
     pdl_trigger();
     const float cnt = p.count_local ? (float)*p.count_local : *p.count;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
+    // fused sync copy: every block takes the (same) decisions from the state before this round;
+    // only the last block writes that state back, after every block has read it
+    uint32_t doit_mask = 0;
+    if (p.sync_copy) {
+        const uint64_t v1 = *p.V + (uint64_t)(cnt + 0.5f);
+        for (int i = 0; i < p.n_sync; ++i)
+            if (v1 >= p.sync_stats[i]->last_sync + (uint64_t)p.period) doit_mask |= 1u << i;
+    }
+    if (!p.sync_copy && blockIdx.x == 0 && threadIdx.x == 0) {
         const uint64_t v0 = *p.V;
         const uint64_t n_acc = (uint64_t)(cnt + 0.5f);
         p.round_info[0] = n_acc;
@@ -611,6 +643,31 @@ __global__ void __launch_bounds__(256) k_apply(ApplyParams p) {
         reinterpret_cast<float4*>(p.m)[e] = make_float4(mv[0], mv[1], mv[2], mv[3]);
         reinterpret_cast<float4*>(p.v)[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
         if (p.rep_t) emit4<T>(p, e, tv);
+        if (doit_mask)
+            for (int i = 0; i < p.n_sync; ++i)
+                if (doit_mask >> i & 1u) emit4_to<T>(p.sync_tm_t[i], p.sync_tm_f[i], p.nA, p.base + 4 * e, tv);
+    }
+    if (!p.sync_copy) return;
+    __shared__ unsigned int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(p.counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    *p.counter = 0;
+    const uint64_t v0 = *p.V;
+    const uint64_t n_acc = (uint64_t)(cnt + 0.5f);
+    p.round_info[0] = n_acc;
+    p.round_info[1] = v0;
+    p.round_info[2] = v0 + n_acc;
+    *p.V = v0 + n_acc;
+    if (p.vhist_dst) *p.vhist_dst = v0 + n_acc;
+    if (p.dev_round) *p.dev_round += 1;
+    for (int i = 0; i < p.n_sync; ++i) {
+        const bool doit = doit_mask >> i & 1u;
+        if (doit) p.sync_stats[i]->last_sync = v0 + n_acc;
+        *p.sync_flag[i] = doit;
     }
 }
 
@@ -685,23 +742,6 @@ struct P2PParams {
     const DevLearnerInfo* info[32];  // this rank's learners' decisions (acceptance mask sent with the flag)
 };
 
-template <typename T>
-GORILA_DEV void emit4_to(void* rep_t, float* rep_f, int nA, int64_t idx, const float* tv) {
-    const ReplicaLayout L = replica_layout(nA);
-    const int64_t slot = replica_slot(L, idx);
-    if (slot >= 0) {
-        T* dst = reinterpret_cast<T*>(rep_t) + slot;
-        if constexpr (sizeof(T) == 2) {
-            __nv_bfloat162 h0 = __floats2bfloat162_rn(tv[0], tv[1]), h1 = __floats2bfloat162_rn(tv[2], tv[3]);
-            *reinterpret_cast<uint2*>(dst) =
-                make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
-        } else {
-            *reinterpret_cast<float4*>(dst) = make_float4(tv[0], tv[1], tv[2], tv[3]);
-        }
-    } else {
-        *reinterpret_cast<float4*>(rep_f + (-slot - 1)) = make_float4(tv[0], tv[1], tv[2], tv[3]);
-    }
-}
 
 // phase: flag set (0 = the fc4 weight region, launched early by gorila_round; 1 = the rest);
 // [lo0, hi0) and [lo1, hi1): float4 ranges of the slice this launch updates; book: V, round
