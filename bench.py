@@ -337,12 +337,17 @@ def main():
     stream.synchronize()
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     e0.record(stream)
+    pending = None
     for i in range(args.e2e_steps):
         f1.numpy()[0] = hf[i]
         a1.numpy()[0], r1.numpy()[0], d1.numpy()[0] = ha[i], hr[i], hd[i]
         g.replay_insert(0, f1, a1, r1, d1)           # this step's new experience, pinned host -> device
-        info = g.round(ids, k, stal, want_info=True)  # the round; its result (loss, decisions) device -> host
+        h = g.round_async(ids, k, stal)               # the round; its result (loss, decisions) -> pinned host
+        if pending is not None:
+            info = g.round_result(pending)            # the previous round's result, read while this one runs
+        pending = h
         k += 1
+    info = g.round_result(pending)
     e1.record(stream)
     stream.synchronize()
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
@@ -421,8 +426,11 @@ def main():
             "clocks": clocks,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 7056 + 1 + 4 + 1,
                     "d2h_bytes_per_step": 48 + 24 + 1,
-                    "note": "per step: replay_insert of 1 new transition from pinned host memory, learner_step "
-                            "with its learner info read back, ps_apply_shard with round info, sync_target flag"},
+                    "note": "per step: replay_insert of 1 new transition from pinned host memory (library "
+                            "staging ring, no stream sync), gorila_round_async (learner_step + ps_apply_shard + "
+                            "sync_target as one graph) whose learner info, round info and sync flag are copied "
+                            "device -> pinned host and read by the host one step later (while the next round "
+                            "runs)"},
             "roofline": {"kernel": dom, "bound": dom_roof["bound"], "achieved": dom_roof["achieved"],
                          "peak": dom_roof["peak"], "unit": dom_roof["unit"], "frac": dom_roof["frac"],
                          "traffic": traffic, "peak_src": peaks["src"],

@@ -205,6 +205,13 @@ GORILA_API gorila_status sync_target(gorila_ctx* ctx, const int32_t* learners, i
 GORILA_API gorila_status gorila_round(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
                                       const int32_t* staleness, gorila_learner_info* info_out,
                                       gorila_round_info* round_info_out, uint8_t* synced_out);
+/* As gorila_round, but the result copies (info_out, round_info_out, synced_out) are only
+ * enqueued on the library stream: they must point to pinned host (or device) memory that
+ * stays valid until the stream passes them (synchronise the stream or an event recorded on
+ * it after this call). Lets a caller read round k's result while round k+1 runs. */
+GORILA_API gorila_status gorila_round_async(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
+                                           const int32_t* staleness, gorila_learner_info* info_out,
+                                           gorila_round_info* round_info_out, uint8_t* synced_out);
 
 /* State access for checkpointing and teacher-forced parity (canonical layout,
  * host buffers, any may be NULL; synchronises the stream). m / v are the full

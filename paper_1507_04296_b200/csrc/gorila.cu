@@ -156,6 +156,15 @@ struct gorila_ctx {
     std::map<std::vector<uint64_t>, CUtensorMap> tmaps;  // TMA descriptors, encoded once per (buffer, view)
     bool tma_failed = false;
     int num_sms = 148;
+    // pinned staging ring for host-source replay_insert: the call copies the caller's bytes here
+    // (CPU memcpy) and enqueues the upload without synchronising; a slot is reused only after the
+    // event of its previous upload has completed
+    static constexpr int kStage = 4;
+    uint8_t* stage[kStage] = {};
+    size_t stage_bytes = 0;
+    cudaEvent_t stage_ev[kStage] = {};
+    int stage_next = 0;
+    uint8_t* stage_dev = nullptr;  // device landing buffer of a staged insert (4 MB)
     unsigned int* apply_counter = nullptr;  // last-block detection of k_apply's fused sync copy
     bool sync_fused_now = false;            // this round's k_apply did the target-sync copy
     // L2 persistence window over the parameter-server state (theta, m, v, G, replicas): the
@@ -1747,6 +1756,14 @@ void gorila_destroy(gorila_ctx* ctx) {
         for (auto& m : kv.second) cudaEventDestroy(m.second);
     for (int q = 0; q < MAX_W; ++q)
         if (ctx->peer_raw[q]) cudaIpcCloseMemHandle(ctx->peer_raw[q]);
+    for (int i = 0; i < gorila_ctx::kStage; ++i) {
+        if (ctx->stage_ev[i]) {
+            cudaEventSynchronize(ctx->stage_ev[i]);
+            cudaEventDestroy(ctx->stage_ev[i]);
+        }
+        if (ctx->stage[i]) cudaFreeHost(ctx->stage[i]);
+    }
+    if (ctx->stage_dev) cudaFree(ctx->stage_dev);
     if (ctx->comm) {
         if (ctx->poisoned) ncclCommAbort(ctx->comm);
         else ncclCommDestroy(ctx->comm);
@@ -1764,8 +1781,59 @@ gorila_status replay_insert(gorila_ctx* ctx, int32_t learner, int64_t count, con
     if (!frames || !actions || !rewards || !terminals) return fail(GORILA_E_INVALID, "null buffer");
     Learner& l = ctx->learners[learner];
     const int64_t C = ctx->cfg.replay_capacity;
-    const cudaMemcpyKind kind = src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
+    cudaMemcpyKind kind = src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
     cudaStream_t st = ctx->stream;
+    // host sources of a small insert go through the pinned staging ring (no stream synchronisation)
+    const int64_t keep = std::min<int64_t>(count, C);
+    const size_t need = (size_t)keep * (FRAME_BYTES + 1 + sizeof(float) + 1) + 64;
+    bool staged = false;
+    if (!src_on_device && need <= ((size_t)1 << 22)) {
+        const int k = ctx->stage_next;
+        if (!ctx->stage[k] || ctx->stage_bytes < need) {
+            for (int i = 0; i < gorila_ctx::kStage; ++i) {  // (re)allocate the ring once
+                if (ctx->stage[i]) {
+                    cudaEventSynchronize(ctx->stage_ev[i]);
+                    cudaFreeHost(ctx->stage[i]);
+                    ctx->stage[i] = nullptr;
+                }
+                if (!ctx->stage_ev[i]) CU(cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming));
+            }
+            ctx->stage_bytes = (size_t)1 << 22;
+            for (int i = 0; i < gorila_ctx::kStage; ++i) CU(cudaHostAlloc((void**)&ctx->stage[i], ctx->stage_bytes, 0));
+            for (int i = 0; i < gorila_ctx::kStage; ++i) CU(cudaEventRecord(ctx->stage_ev[i], st));
+            if (!ctx->stage_dev) CU(cudaMalloc((void**)&ctx->stage_dev, ctx->stage_bytes));
+        }
+        CU(cudaEventSynchronize(ctx->stage_ev[k]));  // its previous upload is done (normally long ago)
+        const int64_t skip0 = count - keep;
+        uint8_t* sb = ctx->stage[k];
+        memcpy(sb, frames + skip0 * FRAME_BYTES, (size_t)keep * FRAME_BYTES);
+        uint8_t* sa = sb + (size_t)keep * FRAME_BYTES;
+        memcpy(sa, actions + skip0, keep);
+        float* sr = reinterpret_cast<float*>(sa + ((keep + 15) / 16) * 16);
+        memcpy(sr, rewards + skip0, keep * sizeof(float));
+        uint8_t* sd = reinterpret_cast<uint8_t*>(sr + keep);
+        memcpy(sd, terminals + skip0, keep);
+        frames = sb - skip0 * FRAME_BYTES;  // the loop below indexes from the original start
+        actions = sa - skip0;
+        rewards = sr - skip0;
+        terminals = sd - skip0;
+        staged = true;
+    }
+    if (staged) {  // one upload + one scatter kernel (the staging ring slot is reused after its event)
+        const uint8_t* sb = ctx->stage[ctx->stage_next];
+        const size_t bytes = (size_t)keep * FRAME_BYTES + ((keep + 15) / 16) * 16 + keep * sizeof(float) + keep;
+        CU(cudaMemcpyAsync(ctx->stage_dev, sb, bytes, cudaMemcpyHostToDevice, st));
+        CU(cudaEventRecord(ctx->stage_ev[ctx->stage_next], st));
+        ctx->stage_next = (ctx->stage_next + 1) % gorila_ctx::kStage;
+        const int64_t t0 = l.n_host + (count - keep);
+        l.n_host += count;
+        const int64_t work = keep * (FRAME_BYTES / 16) + keep;
+        k_insert_scatter<<<(unsigned)std::min<int64_t>(148 * 4, (work + 255) / 256), 256, 0, st>>>(
+            ctx->stage_dev, keep, t0, C, l.frames, l.a, l.r, l.d, l.n_dev, (uint64_t)l.n_host);
+        ctx->launches++;
+        CU(cudaGetLastError());
+        return GORILA_OK;
+    }
     // only the last min(count, C) steps survive; copy them in at most two contiguous segments
     int64_t skip = count > C ? count - C : 0;
     int64_t t = l.n_host + skip, left = count - skip, src = skip;
@@ -1777,7 +1845,9 @@ gorila_status replay_insert(gorila_ctx* ctx, int32_t learner, int64_t count, con
         CU(cudaMemcpyAsync(l.d + slot, terminals + src, seg, kind, st));
         t += seg; src += seg; left -= seg;
     }
-    if (!src_on_device) CU(cudaStreamSynchronize(st));  // host buffers may be reused on return
+    if (!src_on_device) {
+        CU(cudaStreamSynchronize(st));  // large host inserts: the caller's buffers may be reused on return
+    }
     l.n_host += count;
     k_set_u64<<<1, 1, 0, st>>>(l.n_dev, (uint64_t)l.n_host);
     ctx->launches++;
@@ -2147,9 +2217,9 @@ gorila_status sync_target(gorila_ctx* ctx, const int32_t* learners, int32_t n, i
     return GORILA_OK;
 }
 
-gorila_status gorila_round(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
-                           const int32_t* staleness, gorila_learner_info* info_out, gorila_round_info* round_info_out,
-                           uint8_t* synced_out) {
+static gorila_status round_impl(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
+                                const int32_t* staleness, gorila_learner_info* info_out,
+                                gorila_round_info* round_info_out, uint8_t* synced_out, bool sync) {
     if (!ctx) return fail(GORILA_E_INVALID, "null context");
     if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned");
     if (!learners || n < 1 || n > ctx->L) return fail(GORILA_E_SHAPE, "bad learner list");
@@ -2247,7 +2317,10 @@ gorila_status gorila_round(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
     if (synced_out)
         for (int i = 0; i < n; ++i)
             CU(cudaMemcpyAsync(&synced_out[i], ctx->learners[learners[i]].sync_flag, 1, cudaMemcpyDeviceToHost, st));
-    if (round_info_out) {
+    static_assert(sizeof(gorila_round_info) == 3 * sizeof(uint64_t), "round info = [n_acc, V_before, V_after]");
+    if (round_info_out && !sync)  // same bytes: n_accepted (+ zero pad) and the two versions
+        CU(cudaMemcpyAsync(round_info_out, ctx->round_info, sizeof(gorila_round_info), cudaMemcpyDeviceToHost, st));
+    if (round_info_out && sync) {
         uint64_t tmp[3];
         CU(cudaMemcpyAsync(tmp, ctx->round_info, sizeof(tmp), cudaMemcpyDeviceToHost, st));
         CU(cudaStreamSynchronize(st));
@@ -2256,9 +2329,21 @@ gorila_status gorila_round(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
         round_info_out->version_before = tmp[1];
         round_info_out->version_after = tmp[2];
     }
-    if (info_out || synced_out) CU(cudaStreamSynchronize(st));
+    if (sync && (info_out || synced_out)) CU(cudaStreamSynchronize(st));
     CU(cudaGetLastError());
     return GORILA_OK;
+}
+
+gorila_status gorila_round(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
+                           const int32_t* staleness, gorila_learner_info* info_out, gorila_round_info* round_info_out,
+                           uint8_t* synced_out) {
+    return round_impl(ctx, learners, n, round, staleness, info_out, round_info_out, synced_out, true);
+}
+
+gorila_status gorila_round_async(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
+                                 const int32_t* staleness, gorila_learner_info* info_out,
+                                 gorila_round_info* round_info_out, uint8_t* synced_out) {
+    return round_impl(ctx, learners, n, round, staleness, info_out, round_info_out, synced_out, false);
 }
 
 gorila_status gorila_get_state(gorila_ctx* ctx, float* theta, float* m, float* v, uint64_t* version) {

@@ -357,6 +357,31 @@ __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, c
     }
 }
 
+// ------------------------------------------------------------------------- staged replay insert
+// one upload of [frames | a | r | d] (the host call's packed staging bytes) scattered into the
+// ring slots (t0 + i) mod C, then the device step counter (replay_insert, small host inserts)
+__global__ void k_insert_scatter(const uint8_t* __restrict__ src, int64_t keep, int64_t t0, int64_t C,
+                                 uint8_t* __restrict__ frames, uint8_t* __restrict__ ra, float* __restrict__ rr,
+                                 uint8_t* __restrict__ rd, uint64_t* __restrict__ n_dev, uint64_t n_new) {
+    const uint8_t* sa = src + keep * FRAME_BYTES;
+    const float* sr = reinterpret_cast<const float*>(sa + ((keep + 15) / 16) * 16);
+    const uint8_t* sd = reinterpret_cast<const uint8_t*>(sr + keep);
+    const int64_t vec = keep * (FRAME_BYTES / 16);
+    for (int64_t v = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; v < vec + keep; v += (int64_t)gridDim.x * blockDim.x) {
+        if (v < vec) {
+            const int64_t i = v / (FRAME_BYTES / 16), c = v - i * (FRAME_BYTES / 16);
+            reinterpret_cast<uint4*>(frames + ((t0 + i) % C) * FRAME_BYTES)[c] =
+                reinterpret_cast<const uint4*>(src + i * FRAME_BYTES)[c];
+        } else {
+            const int64_t i = v - vec, slot = (t0 + i) % C;
+            ra[slot] = sa[i];
+            rr[slot] = sr[i];
+            rd[slot] = sd[i];
+        }
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = n_new;
+}
+
 // ------------------------------------------------------------------------- acting (NEXT row f3)
 // states u8 [n][4][84][84] -> the conv input layout (NHWC, T), 4 pixels per thread
 template <typename T>

@@ -62,6 +62,7 @@ EXPORTS = ["gorila_param_count", "gorila_workspace_bytes", "gorila_init", "goril
            "gorila_set_state", "gorila_get_learner_state", "gorila_set_learner_state", "gorila_get_grad",
            "gorila_get_q", "gorila_get_activation", "gorila_act", "gorila_kernel_launches", "gorila_profile_enable", "gorila_profile_read",
            "gorila_profile_phase_count", "gorila_profile_phase_name", "gorila_nccl_unique_id", "gorila_round",
+           "gorila_round_async",
            "gorila_bench_phase", "gorila_debug_trace"]
 
 
@@ -106,6 +107,7 @@ def load(build_if_missing=True):
     L.gorila_profile_phase_name.restype = ctypes.c_char_p
     L.gorila_nccl_unique_id.argtypes = [P]
     L.gorila_round.argtypes = [P, P, i32, u64, P, P, P, P]
+    L.gorila_round_async.argtypes = [P, P, i32, u64, P, P, P, P]
     L.gorila_bench_phase.argtypes = [P, i32, i32, i32, P]
     L.gorila_debug_trace.argtypes = [P]
     _lib = L
@@ -255,6 +257,38 @@ class Gorila:
         return ([self._info[i].as_dict() for i in range(len(learners_arr))],
                 {"n_accepted": ri.n_accepted, "version_before": ri.version_before,
                  "version_after": ri.version_after}, synced.astype(bool))
+
+    def round_async(self, learners_arr, rnd, staleness_arr=None):
+        """gorila_round_async: the round's result lands in a pinned slot; returns a handle for
+        round_result (read it while later rounds run)."""
+        torch = self.torch
+        if not hasattr(self, "_slots"):
+            n = self.L
+            self._slots = [{"info": torch.empty(n * ctypes.sizeof(LearnerInfo), dtype=torch.uint8).pin_memory(),
+                            "ri": torch.empty(ctypes.sizeof(RoundInfo), dtype=torch.uint8).pin_memory(),
+                            "sy": torch.empty(n, dtype=torch.uint8).pin_memory(),
+                            "ev": torch.cuda.Event()} for _ in range(4)]
+            self._slot_next = 0
+        k = self._slot_next
+        self._slot_next = (k + 1) % len(self._slots)
+        sl = self._slots[k]
+        sl["ev"].synchronize()  # the slot's previous result has been read back
+        _check(load().gorila_round_async(self.h, learners_arr.ctypes.data, len(learners_arr), rnd,
+                                         None if staleness_arr is None else staleness_arr.ctypes.data,
+                                         sl["info"].data_ptr(), sl["ri"].data_ptr(), sl["sy"].data_ptr()))
+        sl["ev"].record(self.stream)
+        return (k, len(learners_arr))
+
+    def round_result(self, handle):
+        """Wait for a round_async handle; returns (learner infos, round info, synced) like round()."""
+        k, n = handle
+        sl = self._slots[k]
+        sl["ev"].synchronize()
+        infos = (LearnerInfo * n).from_buffer_copy(sl["info"].numpy().tobytes()[:n * ctypes.sizeof(LearnerInfo)])
+        ri = RoundInfo.from_buffer_copy(sl["ri"].numpy().tobytes())
+        return ([infos[i].as_dict() for i in range(n)],
+                {"n_accepted": ri.n_accepted, "version_before": ri.version_before, "version_after": ri.version_after},
+                sl["sy"].numpy()[:n].astype(bool))
 
     def ps_apply_shard(self, rnd, want_info=True):
         ri = RoundInfo() if want_info else None

@@ -54,6 +54,26 @@ def test_replay_sample_bitexact_with_wraparound_and_terminals(math):
     assert g.kernel_launches() > 0
 
 
+def test_replay_single_host_inserts_staged_ring():
+    """One transition per replay_insert from host memory (the staged, unsynchronised path), across a
+    ring wrap: the ring equals the oracle's, checked through bit-exact sampled windows."""
+    from paper_1507_04296_b200 import Gorila
+    nA, C, n = 6, 50, 137
+    g = Gorila(n_actions=nA, batch=16, replay_capacity=C, theta0=synth.theta0(nA), math="bf16")
+    ring = O.Ring(C)
+    f = synth.frames(synth.SEED_DATA, 0, 0, n)
+    a, r, d = synth.meta(synth.SEED_DATA, 0, 0, n, nA)
+    for t in range(n):
+        g.replay_insert(0, f[t:t + 1], a[t:t + 1], r[t:t + 1], d[t:t + 1])
+        ring.insert(f[t:t + 1], a[t:t + 1], r[t:t + 1], d[t:t + 1])
+    for k in (0, 3):
+        out = g.replay_sample(0, k)
+        tau = O.sample_indices(ring.n, ring.size, 16, 1507, 0, k)
+        s, s2, aa, rr, dd = ring.gather(tau)
+        assert (out["tau"] == tau).all() and (out["s"] == s).all() and (out["s2"] == s2).all()
+        assert (out["a"] == aa).all() and (out["r"] == rr).all() and (out["d"] == dd).all()
+
+
 def test_replay_not_ready():
     from paper_1507_04296_b200 import GorilaError
     g, orc = make_pair(nA=4, B=8, C=100, n_insert=1, math="fp32")
@@ -285,3 +305,29 @@ def test_round_graph_matches_eager_bitwise(math):
     tb, mb, vb, Vb = gb.get_state()
     assert (ta == tb).all() and (ma == mb).all() and (va == vb).all() and Va == Vb
     assert (ga.get_learner_state(0)[0] == gb.get_learner_state(0)[0]).all()
+
+
+def test_round_async_matches_round_bitwise():
+    """gorila_round_async (results read one round later) == gorila_round, state and results."""
+    ga, _ = make_pair(nA=18, B=32, C=3000, n_insert=3000, math="bf16", target_period=3, outlier_warmup=2)
+    gb, _ = make_pair(nA=18, B=32, C=3000, n_insert=3000, math="bf16", target_period=3, outlier_warmup=2)
+    ids = np.array([0], np.int32)
+    pend, res_b = None, []
+    for k in range(8):
+        ra = ga.round(ids, k, want_info=True)
+        h = gb.round_async(ids, k)
+        if pend is not None:
+            res_b.append(gb.round_result(pend))
+        pend = h
+        if k < 7:
+            continue
+    res_b.append(gb.round_result(pend))
+    ta, ma, va, Va = ga.get_state()
+    tb, mb, vb, Vb = gb.get_state()
+    assert (ta == tb).all() and (ma == mb).all() and (va == vb).all() and Va == Vb
+    last_a = ga.round(ids, 8, want_info=True)
+    h = gb.round_async(ids, 8)
+    last_b = gb.round_result(h)
+    assert last_a[0] == last_b[0] and last_a[1] == last_b[1] and list(last_a[2]) == list(last_b[2])
+    assert len(res_b) == 8 and all(r[1]["version_after"] >= 1 for r in res_b)
+
