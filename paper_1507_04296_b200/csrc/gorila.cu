@@ -156,6 +156,7 @@ struct gorila_ctx {
     std::map<std::vector<uint64_t>, CUtensorMap> tmaps;  // TMA descriptors, encoded once per (buffer, view)
     bool tma_failed = false;
     int num_sms = 148;
+    unsigned int* fc5_gen = nullptr;  // [2] generation counters of the fused fc5 backward
     // pinned staging ring for host-source replay_insert: the call copies the caller's bytes here
     // (CPU memcpy) and enqueues the upload without synchronising; a slot is reused only after the
     // event of its previous upload has completed
@@ -834,6 +835,14 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }
     }
     mark(ctx, PH_SAMPLE);
+    // GORILA_FC5_FUSE=1 (B <= 32): the fc5 backward runs inside k_fc5_td after a grid-wide wait on
+    // the TD decision (one launch fewer). Opt-in: measured 12.39k vs 12.57k updates/s unfused, the
+    // spin on the decision costs more than the launch it saves.
+    static const bool fc5_fuse_env = [] {
+        const char* e = getenv("GORILA_FC5_FUSE");
+        return e && atoi(e) != 0;
+    }();
+    const bool fc5_fused = fc5_fuse_env && B <= 32 && (phases & (1u << PH_FC5F)) && (phases & (1u << PH_FC5B));
     // small batches (bf16): conv1 -> conv2 -> conv3 of a (net, sample) in one CTA (tower.cuh)
     const bool use_tower = !fp32v && ctx->tower && 2 * B <= ctx->num_sms;
     PHASE(PH_CONV1F) if (use_tower) {
@@ -1023,12 +1032,19 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         t.outlier_enabled = cfg.outlier_enabled; t.outlier_warmup = cfg.outlier_warmup;
         t.outlier_k = cfg.outlier_k; t.outlier_beta = cfg.outlier_beta;
         p.per_sample = ctx->td_partial;
-        launch(ctx, k_fc5_td, dim3(std::min(B, 2 * 148)), dim3(512), 0, p);
+        if (fc5_fused) {
+            p.fuse_bwd = 1;
+            p.gen = ctx->fc5_gen;
+            p.part5 = ctx->part5;
+            p.g4 = g4;
+            p.bf16 = !fp32v;
+        }
+        launch(ctx, k_fc5_td, dim3(fc5_fused ? B : std::min(B, 2 * 148)), dim3(512), 0, p);
     }
     }
     mark(ctx, PH_FC5F);
     mark(ctx, PH_TD);
-    PHASE(PH_FC5B) {
+    PHASE(PH_FC5B) if (!fc5_fused) {
     // fc5 bwd: dW5, db5 into G; g4 = mask(dQ W5)
     {
         const int nch = (B + fc5_rows(B) - 1) / fc5_rows(B);
@@ -1248,7 +1264,8 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             all.off[3 + l] = boff[l];
             bp += (int64_t)ctx->bias_chunks * bc[l];
         }
-        all.part[7] = ctx->part5; all.splits[7] = (B + fc5_rows(B) - 1) / fc5_rows(B);  // W5 and b5 (contiguous)
+        all.part[7] = ctx->part5;  // W5 and b5 (contiguous); the fused head writes one chunk
+        all.splits[7] = fc5_fused ? 1 : (B + fc5_rows(B) - 1) / fc5_rows(B);
         all.count[7] = (int64_t)nA * (FC4_OUT + 1); all.off[7] = OFF_W5;
         for (int l = 3; l < 7; ++l) all.wide[l] = 1;
         all.nseg = 8;
@@ -1409,6 +1426,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     uint64_t* p2p_epoch = c.take<uint64_t>(1);
     unsigned int* p2p_counter = c.take<unsigned int>(2);
     unsigned int* apply_counter = c.take<unsigned int>(1);
+    unsigned int* fc5_gen = c.take<unsigned int>(2);
     std::vector<void*> rep_t(H);
     std::vector<float*> rep_f(H);
     for (int h = 0; h < H; ++h) {
@@ -1498,7 +1516,8 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         ctx->round_info = rinfo;
         ctx->n_acc_local = nacc; ctx->Vhist = Vhist; ctx->dev_round = dev_round; ctx->head_counter = head_counter;
         ctx->pflags = pflags; ctx->p2p_epoch = p2p_epoch; ctx->p2p_counter = p2p_counter;
-        ctx->apply_counter = apply_counter; ctx->rep_t = rep_t; ctx->rep_f = rep_f; ctx->learners = lrs;
+        ctx->apply_counter = apply_counter;
+        ctx->fc5_gen = fc5_gen; ctx->rep_t = rep_t; ctx->rep_f = rep_f; ctx->learners = lrs;
         ctx->s = s; ctx->s2 = s2; ctx->a1 = a1; ctx->a2 = a2; ctx->a3 = a3; ctx->a4 = a4;
         ctx->t1 = t1; ctx->t2 = t2; ctx->t3 = t3; ctx->t4 = t4;
         ctx->g1 = g1; ctx->g2 = g2; ctx->g3 = g3; ctx->g4 = g4;
@@ -1659,6 +1678,7 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     CU(cudaMemsetAsync(ctx->p2p_epoch, 0, sizeof(uint64_t), st));
     CU(cudaMemsetAsync(ctx->p2p_counter, 0, sizeof(unsigned int) * 2, st));
     CU(cudaMemsetAsync(ctx->apply_counter, 0, sizeof(unsigned int), st));
+    CU(cudaMemsetAsync(ctx->fc5_gen, 0, sizeof(unsigned int) * 2, st));
     ctx->dev_round_expect = 0;
     {
         const char* e = getenv("GORILA_PDL");  // GORILA_PDL=0 disables programmatic dependent launch

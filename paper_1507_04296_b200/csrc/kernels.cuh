@@ -195,7 +195,49 @@ struct Fc5TdParams {
     unsigned int* counter;  // zero between launches (the last block resets it)
     float* per_sample;      // [B][2]
     TdParams td;
+    // fused fc5 backward (gridDim == B <= 32, every block resident): after the decision every block
+    // writes its sample's g4 row and a column slice of the single-chunk fc5 gradient partial
+    int fuse_bwd;
+    unsigned int* gen;      // [2]: launch generation, decision-published generation
+    float* part5;           // [nA * 513]
+    void* g4;               // T [B][512]
+    int bf16;               // g4 element type
 };
+// fused fc5 backward of one block (fuse_bwd): wait until the last block published the decision
+// (dQ final), then this block's sample's g4 row and its column slice of dW5 / db5 (one chunk)
+GORILA_DEV void fc5_bwd_fused(const Fc5TdParams& p, unsigned int gen) {
+    if (threadIdx.x == 0)
+        while (*(volatile unsigned int*)&p.gen[1] != gen + 1) __nanosleep(32);
+    __syncthreads();
+    __threadfence();
+    const TdParams& t = p.td;
+    const int B = t.B, nA = t.nA, b = blockIdx.x;
+    __shared__ float dq[32 * 32];
+    for (int i = threadIdx.x; i < B * nA; i += blockDim.x) dq[i] = __ldcg(&t.dQ[i]);
+    __syncthreads();
+    for (int n = threadIdx.x; n < FC4_OUT; n += blockDim.x) {  // g4[b][n] = mask(sum_a dQ[b][a] W5[a][n])
+        float g = 0.f;
+        for (int a = 0; a < nA; ++a) g = fmaf(dq[b * nA + a], p.w5[a * FC4_OUT + n], g);
+        const float x = p.a4[(int64_t)b * FC4_OUT + n];
+        const float v = x > 0.f ? g : 0.f;
+        if (p.bf16) reinterpret_cast<__nv_bfloat16*>(p.g4)[(int64_t)b * FC4_OUT + n] = __float2bfloat16_rn(v);
+        else reinterpret_cast<float*>(p.g4)[(int64_t)b * FC4_OUT + n] = v;
+    }
+    // dW5[a][n] = sum_b dQ[b][a] a4[b][n] for this block's columns; db5 by block 0
+    const int per = (FC4_OUT + gridDim.x - 1) / gridDim.x, n0 = b * per, n1 = min(FC4_OUT, n0 + per);
+    for (int e = threadIdx.x; e < nA * (n1 - n0); e += blockDim.x) {
+        const int a = e / (n1 - n0), n = n0 + (e - a * (n1 - n0));
+        float acc = 0.f;
+        for (int bb = 0; bb < B; ++bb) acc = fmaf(dq[bb * nA + a], p.a4[(int64_t)bb * FC4_OUT + n], acc);
+        p.part5[a * FC4_OUT + n] = acc;
+    }
+    if (b == 0 && (int)threadIdx.x < nA) {
+        float sb = 0.f;
+        for (int bb = 0; bb < B; ++bb) sb += dq[bb * nA + threadIdx.x];
+        p.part5[nA * FC4_OUT + threadIdx.x] = sb;
+    }
+}
+
 // 16 warps: warps 0..7 the online net, 8..15 the target net; every operand of a warp's (up to
 // four) actions is requested before the first FMA (one memory round trip for the whole layer)
 __global__ void __launch_bounds__(512) k_fc5_td(Fc5TdParams p) {
@@ -255,12 +297,16 @@ __global__ void __launch_bounds__(512) k_fc5_td(Fc5TdParams p) {
         }
         // the next sample writes the other parity of q: one barrier per sample suffices
     }
-    __shared__ unsigned int s_last;
+    __shared__ unsigned int s_last, s_gen;
+    if (threadIdx.x == 0 && p.fuse_bwd) s_gen = *(volatile unsigned int*)&p.gen[0];
     __threadfence();
     __syncthreads();
     if (threadIdx.x == 0) s_last = (atomicAdd(p.counter, 1u) == gridDim.x - 1);
     __syncthreads();
-    if (!s_last) return;
+    if (!s_last) {
+        if (p.fuse_bwd) fc5_bwd_fused(p, s_gen);
+        return;
+    }
     __threadfence();
     // last block: fixed-order batch sums (8 interleaved partials, then in order), decisions
     __shared__ float s_sq[16], s_ab[16];
@@ -284,6 +330,15 @@ __global__ void __launch_bounds__(512) k_fc5_td(Fc5TdParams p) {
     __syncthreads();
     if (!s_keep)
         for (int e = threadIdx.x; e < t.B * nA; e += blockDim.x) t.dQ[e] = 0.f;
+    if (p.fuse_bwd) {
+        __threadfence();
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            p.gen[0] = s_gen + 1;                               // the next launch's generation
+            atomicExch(&p.gen[1], s_gen + 1);                   // publish: dQ is final
+        }
+        fc5_bwd_fused(p, s_gen);
+    }
 }
 
 __global__ void k_mark_not_ready(DevLearnerInfo* info, const LearnerStats* st) {
