@@ -148,7 +148,10 @@ GORILA_API const char* gorila_last_error(void);
  * is terminal, Alg.1). src_on_device != 0: all four are device pointers,
  * read asynchronously on the library stream: the caller must not overwrite them
  * until that stream has passed this call (order its own stream after ours, as
- * the Python binding does). Host pointers are copied before the call returns. */
+ * the Python binding does). Host pointers are copied before the call returns:
+ * up to 4 MB into a pinned staging ring allocated by gorila_init (no stream
+ * synchronisation; a scatter kernel reads slots up to 64 KB over the bus and
+ * larger ones after one upload), beyond that with a stream synchronisation. */
 GORILA_API gorila_status replay_insert(gorila_ctx* ctx, int32_t learner, int64_t count, const uint8_t* frames,
                             const uint8_t* actions, const float* rewards, const uint8_t* terminals,
                             int32_t src_on_device);
@@ -208,7 +211,9 @@ GORILA_API gorila_status gorila_round(gorila_ctx* ctx, const int32_t* learners, 
 /* As gorila_round, but the result copies (info_out, round_info_out, synced_out) are only
  * enqueued on the library stream: they must point to pinned host (or device) memory that
  * stays valid until the stream passes them (synchronise the stream or an event recorded on
- * it after this call). Lets a caller read round k's result while round k+1 runs. */
+ * it after this call). Lets a caller read round k's result while round k+1 runs. When every
+ * output is device-accessible (pinned, mapped or device memory) and n <= 11, one small kernel
+ * stores them; otherwise they are copy-engine copies (pageable memory then serialises). */
 GORILA_API gorila_status gorila_round_async(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
                                            const int32_t* staleness, gorila_learner_info* info_out,
                                            gorila_round_info* round_info_out, uint8_t* synced_out);

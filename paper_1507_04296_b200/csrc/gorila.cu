@@ -166,6 +166,7 @@ struct gorila_ctx {
     cudaEvent_t stage_ev[kStage] = {};
     int stage_next = 0;
     uint8_t* stage_dev = nullptr;  // device landing buffer of a staged insert (4 MB)
+    uint8_t* stage_dptr[kStage] = {};  // device view of the mapped pinned slots (small inserts read them directly)
     unsigned int* apply_counter = nullptr;  // last-block detection of k_apply's fused sync copy
     bool sync_fused_now = false;            // this round's k_apply did the target-sync copy
     // L2 persistence window over the parameter-server state (theta, m, v, G, replicas): the
@@ -1633,6 +1634,8 @@ gorila_status gorila_nccl_unique_id(void* out128) {
     return GORILA_OK;
 }
 
+static cudaError_t stage_alloc(gorila_ctx* ctx);
+
 gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     if (!cfg || !out) return fail(GORILA_E_INVALID, "null argument");
     *out = nullptr;
@@ -1749,6 +1752,7 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
             return fail(GORILA_E_INVALID, "per-message mode needs the peer-memory exchange (world > 1)");
         }
     }
+    CU(stage_alloc(ctx));
     CU(cudaStreamSynchronize(st));
     *out = ctx;
     return GORILA_OK;
@@ -1791,6 +1795,20 @@ void gorila_destroy(gorila_ctx* ctx) {
     delete ctx;
 }
 
+// the staging ring of small host inserts (allocated by gorila_init: pinned allocation takes
+// milliseconds and must not land inside a caller's first training step)
+static cudaError_t stage_alloc(gorila_ctx* ctx) {
+    ctx->stage_bytes = (size_t)1 << 22;
+    for (int i = 0; i < gorila_ctx::kStage; ++i) {
+        cudaError_t e;
+        if (!ctx->stage_ev[i] && (e = cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming))) return e;
+        if ((e = cudaHostAlloc((void**)&ctx->stage[i], ctx->stage_bytes, cudaHostAllocMapped))) return e;
+        if ((e = cudaHostGetDevicePointer((void**)&ctx->stage_dptr[i], ctx->stage[i], 0))) return e;
+        if ((e = cudaEventRecord(ctx->stage_ev[i], ctx->stream))) return e;
+    }
+    return ctx->stage_dev ? cudaSuccess : cudaMalloc((void**)&ctx->stage_dev, ctx->stage_bytes);
+}
+
 gorila_status replay_insert(gorila_ctx* ctx, int32_t learner, int64_t count, const uint8_t* frames,
                             const uint8_t* actions, const float* rewards, const uint8_t* terminals,
                             int32_t src_on_device) {
@@ -1809,20 +1827,7 @@ gorila_status replay_insert(gorila_ctx* ctx, int32_t learner, int64_t count, con
     bool staged = false;
     if (!src_on_device && need <= ((size_t)1 << 22)) {
         const int k = ctx->stage_next;
-        if (!ctx->stage[k] || ctx->stage_bytes < need) {
-            for (int i = 0; i < gorila_ctx::kStage; ++i) {  // (re)allocate the ring once
-                if (ctx->stage[i]) {
-                    cudaEventSynchronize(ctx->stage_ev[i]);
-                    cudaFreeHost(ctx->stage[i]);
-                    ctx->stage[i] = nullptr;
-                }
-                if (!ctx->stage_ev[i]) CU(cudaEventCreateWithFlags(&ctx->stage_ev[i], cudaEventDisableTiming));
-            }
-            ctx->stage_bytes = (size_t)1 << 22;
-            for (int i = 0; i < gorila_ctx::kStage; ++i) CU(cudaHostAlloc((void**)&ctx->stage[i], ctx->stage_bytes, 0));
-            for (int i = 0; i < gorila_ctx::kStage; ++i) CU(cudaEventRecord(ctx->stage_ev[i], st));
-            if (!ctx->stage_dev) CU(cudaMalloc((void**)&ctx->stage_dev, ctx->stage_bytes));
-        }
+        if (!ctx->stage[k]) CU(stage_alloc(ctx));
         CU(cudaEventSynchronize(ctx->stage_ev[k]));  // its previous upload is done (normally long ago)
         const int64_t skip0 = count - keep;
         uint8_t* sb = ctx->stage[k];
@@ -1839,19 +1844,25 @@ gorila_status replay_insert(gorila_ctx* ctx, int32_t learner, int64_t count, con
         terminals = sd - skip0;
         staged = true;
     }
-    if (staged) {  // one upload + one scatter kernel (the staging ring slot is reused after its event)
-        const uint8_t* sb = ctx->stage[ctx->stage_next];
+    if (staged) {  // one scatter kernel (+ one upload for larger inserts); the slot is reused after its event
+        const int k = ctx->stage_next;
         const size_t bytes = (size_t)keep * FRAME_BYTES + ((keep + 15) / 16) * 16 + keep * sizeof(float) + keep;
-        CU(cudaMemcpyAsync(ctx->stage_dev, sb, bytes, cudaMemcpyHostToDevice, st));
-        CU(cudaEventRecord(ctx->stage_ev[ctx->stage_next], st));
-        ctx->stage_next = (ctx->stage_next + 1) % gorila_ctx::kStage;
+        // up to 64 KB the kernel reads the mapped pinned slot itself: one stream operation instead
+        // of a copy-engine hop plus a kernel (the e2e loop inserts one 7 KB transition per step)
+        const uint8_t* src = ctx->stage_dptr[k];
+        if (bytes > ((size_t)1 << 16)) {
+            CU(cudaMemcpyAsync(ctx->stage_dev, ctx->stage[k], bytes, cudaMemcpyHostToDevice, st));
+            src = ctx->stage_dev;
+        }
         const int64_t t0 = l.n_host + (count - keep);
         l.n_host += count;
         const int64_t work = keep * (FRAME_BYTES / 16) + keep;
         k_insert_scatter<<<(unsigned)std::min<int64_t>(148 * 4, (work + 255) / 256), 256, 0, st>>>(
-            ctx->stage_dev, keep, t0, C, l.frames, l.a, l.r, l.d, l.n_dev, (uint64_t)l.n_host);
+            src, keep, t0, C, l.frames, l.a, l.r, l.d, l.n_dev, (uint64_t)l.n_host);
         ctx->launches++;
         CU(cudaGetLastError());
+        CU(cudaEventRecord(ctx->stage_ev[k], st));
+        ctx->stage_next = (k + 1) % gorila_ctx::kStage;
         return GORILA_OK;
     }
     // only the last min(count, C) steps survive; copy them in at most two contiguous segments
@@ -2237,6 +2248,18 @@ gorila_status sync_target(gorila_ctx* ctx, const int32_t* learners, int32_t n, i
     return GORILA_OK;
 }
 
+// pinned / registered host memory or device memory: a kernel may store to it (UVA: same address)
+static bool device_accessible(const void* p) {
+    if (!p) return true;
+    cudaPointerAttributes at{};
+    if (cudaPointerGetAttributes(&at, p) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    if (at.type == cudaMemoryTypeDevice || at.type == cudaMemoryTypeManaged) return true;
+    return at.type == cudaMemoryTypeHost && at.devicePointer == p;
+}
+
 static gorila_status round_impl(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
                                 const int32_t* staleness, gorila_learner_info* info_out,
                                 gorila_round_info* round_info_out, uint8_t* synced_out, bool sync) {
@@ -2329,6 +2352,23 @@ static gorila_status round_impl(gorila_ctx* ctx, const int32_t* learners, int32_
             CU(fold_marks(ctx, ctx->graph_marks[key]));
             ctx->prof_steps += 1;
         }
+    }
+    // asynchronous results into device-accessible (pinned) host buffers: one small copy kernel
+    // instead of up to 2n+1 copy-engine operations on the stream
+    if (!sync && n <= SMALL_COPY_MAX / 2 - 1 && (info_out || synced_out || round_info_out) &&
+        device_accessible(info_out) && device_accessible(synced_out) && device_accessible(round_info_out)) {
+        SmallCopies sc{};
+        auto add = [&](void* dst, const void* src, int bytes) {
+            sc.dst[sc.n] = (uint8_t*)dst; sc.src[sc.n] = (const uint8_t*)src; sc.bytes[sc.n] = bytes; sc.n++;
+        };
+        for (int i = 0; i < n && info_out; ++i)
+            add(&info_out[i], ctx->learners[learners[i]].info, (int)sizeof(gorila_learner_info));
+        for (int i = 0; i < n && synced_out; ++i) add(&synced_out[i], ctx->learners[learners[i]].sync_flag, 1);
+        if (round_info_out) add(round_info_out, ctx->round_info, (int)sizeof(gorila_round_info));
+        k_small_copies<<<1, 32 * std::min(sc.n, 8), 0, st>>>(sc);
+        ctx->launches++;
+        CU(cudaGetLastError());
+        return GORILA_OK;
     }
     if (info_out)
         for (int i = 0; i < n; ++i)

@@ -437,6 +437,22 @@ __global__ void k_insert_scatter(const uint8_t* __restrict__ src, int64_t keep, 
     if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = n_new;
 }
 
+// ------------------------------------------------------------------------- small result copies
+// gorila_round_async's learner infos / sync flags / round info into pinned host buffers: warp w
+// copies segment w, w + nwarps, ... byte by byte (a few hundred bytes in all)
+constexpr int SMALL_COPY_MAX = 24;
+struct SmallCopies {
+    int n;
+    const uint8_t* src[SMALL_COPY_MAX];
+    uint8_t* dst[SMALL_COPY_MAX];
+    int bytes[SMALL_COPY_MAX];
+};
+__global__ void k_small_copies(SmallCopies c) {
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int s = w; s < c.n; s += blockDim.x >> 5)
+        for (int b = lane; b < c.bytes[s]; b += 32) c.dst[s][b] = c.src[s][b];
+}
+
 // ------------------------------------------------------------------------- acting (NEXT row f3)
 // states u8 [n][4][84][84] -> the conv input layout (NHWC, T), 4 pixels per thread
 template <typename T>

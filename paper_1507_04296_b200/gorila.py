@@ -147,6 +147,13 @@ def _ptr(x):
     return x.data_ptr(), bool(x.is_cuda)
 
 
+def _spin(ev):
+    """Wait for an event by polling it. A blocking wait parks the thread, and the first CUDA call
+    after it then costs ~90 us on the B200 hosts (tools/e2e_probe.py) -- more than the round."""
+    while not ev.query():
+        pass
+
+
 class Gorila:
     """One rank's learner / parameter-server context (see include/gorila.h)."""
 
@@ -272,7 +279,7 @@ class Gorila:
         k = self._slot_next
         self._slot_next = (k + 1) % len(self._slots)
         sl = self._slots[k]
-        sl["ev"].synchronize()  # the slot's previous result has been read back
+        _spin(sl["ev"])  # the slot's previous result has been read back
         _check(load().gorila_round_async(self.h, learners_arr.ctypes.data, len(learners_arr), rnd,
                                          None if staleness_arr is None else staleness_arr.ctypes.data,
                                          sl["info"].data_ptr(), sl["ri"].data_ptr(), sl["sy"].data_ptr()))
@@ -283,7 +290,7 @@ class Gorila:
         """Wait for a round_async handle; returns (learner infos, round info, synced) like round()."""
         k, n = handle
         sl = self._slots[k]
-        sl["ev"].synchronize()
+        _spin(sl["ev"])
         infos = (LearnerInfo * n).from_buffer_copy(sl["info"].numpy().tobytes()[:n * ctypes.sizeof(LearnerInfo)])
         ri = RoundInfo.from_buffer_copy(sl["ri"].numpy().tobytes())
         return ([infos[i].as_dict() for i in range(n)],
