@@ -56,6 +56,8 @@ def lib():
         L.orc_philox.argtypes = [P, P, P]
         L.orc_sample_indices.argtypes = [i64, i64, i32, u64, i32, u64, P]
         L.orc_sample_indices.restype = ctypes.c_int
+        L.orc_sample_indices_global.argtypes = [i32, P, i64, i32, u64, i32, u64, P, P]
+        L.orc_sample_indices_global.restype = ctypes.c_int
         L.orc_stack.argtypes = [i64, i64, P, P, i64, P]
         L.orc_gather.argtypes = [i64, i64, P, P, P, P, i32, P, P, P, P, P, P]
         for f in ("orc_conv2d_fwd", "orc_conv2d_bwd_data", "orc_conv2d_bwd_weight"):
@@ -97,6 +99,23 @@ def sample_indices(n, size, batch, seed, learner, rnd):
     if lib().orc_sample_indices(n, size, batch, seed, learner, rnd, _p(tau)) != 0:
         raise ValueError("replay has no valid transition")
     return tau
+
+
+def sample_indices_global(ns, capacity, batch, seed, learner, rnd):
+    """f4 (R36): (shard, tau) per sample, uniform over the union of the shards' valid transitions.
+    ns: n_j of every shard in ascending global learner id; shard = position in ns."""
+    ns = np.ascontiguousarray(ns, dtype=np.int64)
+    shard = np.zeros(batch, np.int32)
+    tau = np.zeros(batch, np.int64)
+    if lib().orc_sample_indices_global(len(ns), _p(ns), capacity, batch, seed, learner, rnd, _p(shard), _p(tau)) != 0:
+        raise ValueError("global replay has no valid transition")
+    return shard, tau
+
+
+def gather_global(rings, shard, tau):
+    """O3 per sample from the ring of its shard (f4): the same stacking as Ring.gather."""
+    parts = [rings[int(q)].gather(np.array([t], np.int64)) for q, t in zip(shard, tau)]
+    return tuple(np.concatenate([p[f] for p in parts]) for f in range(5))
 
 
 def round_bf16(x):
@@ -359,6 +378,9 @@ class Config:
     ps_mode: str = "aggregate"      # "aggregate": one step on the mean of the accepted gradients (R12);
                                     # "per_message": NEXT row f1, one optimizer step per accepted
                                     # message in ascending learner id, V += 1 each (R32)
+    replay_mode: str = "local"      # "local": each learner samples its own ring (P:140 first form);
+                                    # "global": NEXT row f4, uniform over the union of all learners'
+                                    # rings as of the round's start (P:140 second form; R36)
 
 
 @dataclasses.dataclass
@@ -408,9 +430,16 @@ class GorilaOracle:
                 info["not_ready"] = True
                 per[j] = info
                 continue
-            tau = sample_indices(L.ring.n, L.ring.size, cfg.batch, cfg.seed_sample, j, k)
-            # O3
-            s, s2, a, r, d = L.ring.gather(tau)
+            if cfg.replay_mode == "global":  # f4: draw (shard, tau) from the union, gather from that ring
+                ids = sorted(self.learners)
+                shard, tau = sample_indices_global([self.learners[q].ring.n for q in ids], cfg.capacity,
+                                                   cfg.batch, cfg.seed_sample, j, k)
+                s, s2, a, r, d = gather_global([self.learners[q].ring for q in ids], shard, tau)
+            else:
+                shard = None
+                tau = sample_indices(L.ring.n, L.ring.size, cfg.batch, cfg.seed_sample, j, k)
+                # O3
+                s, s2, a, r, d = L.ring.gather(tau)
             # O4
             Q, acts = qnet_forward(theta_j, s, cfg.n_actions, cfg.mode)
             Qhat, _ = qnet_forward(L.theta_minus, s2, cfg.n_actions, cfg.mode)
@@ -423,7 +452,7 @@ class GorilaOracle:
             L.stats.update(ell, cfg.outlier_beta)
             # O9
             stale = is_stale(V0, b_j, cfg.max_staleness)
-            info.update(tau=tau, Q=Q, Qhat=Qhat, y=y, delta=delta, loss=loss, abs_loss=ell,
+            info.update(tau=tau, shard=shard, Q=Q, Qhat=Qhat, y=y, delta=delta, loss=loss, abs_loss=ell,
                         threshold=thr, stats_count_before=stats_count_before,
                         rejected_outlier=rejected, stale=stale, mu=L.stats.mu, var=L.stats.var,
                         a=a, r=r, d=d)

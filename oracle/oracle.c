@@ -65,6 +65,46 @@ EXPORT int orc_sample_indices(int64_t n, int64_t size, int32_t B, uint64_t seed,
     return 0;
 }
 
+/* f4 (reading R36): a minibatch drawn uniformly from the GLOBAL
+ * replay memory D ("a global replay memory aggregates the experience into a distributed
+ * database", §4; "sampled from either a local or global experience replay memory D",
+ * P:142; uniform sampling from D, §3.3). D is the union of the G shards' valid transitions,
+ * enumerated shard by shard (ascending global learner id j) and within shard j by tau ascending
+ * over [n_j - size_j, n_j - 2], size_j = min(n_j, C). With T = |D| and u the same 64-bit word as
+ * O2 (counter of the drawing learner), g = floor(u*T / 2^64) and (shard, tau) is the g-th element
+ * of that enumeration, found here by walking the enumeration. Returns 0, or -1 if T = 0. */
+EXPORT int orc_sample_indices_global(int32_t G, const int64_t* n, int64_t C, int32_t B, uint64_t seed,
+                                     int32_t learner, uint64_t round, int32_t* shard, int64_t* tau) {
+    uint64_t T = 0;
+    for (int32_t j = 0; j < G; ++j) {
+        int64_t size = n[j] < C ? n[j] : C;
+        if (size >= 2) T += (uint64_t)(size - 1);
+    }
+    if (T == 0) return -1;
+    uint32_t key[2] = {(uint32_t)seed, (uint32_t)(seed >> 32)};
+    for (int32_t i = 0; i < B; ++i) {
+        uint32_t ctr[4] = {(uint32_t)(i / 2), (uint32_t)learner, (uint32_t)round,
+                           (uint32_t)((round >> 32) & 0xffffffu) | (ORC_TAG_SAMPLE << 24)};
+        uint32_t x[4];
+        orc_philox(ctr, key, x);
+        uint64_t u = (i % 2 == 0) ? ((uint64_t)x[0] | ((uint64_t)x[1] << 32))
+                                  : ((uint64_t)x[2] | ((uint64_t)x[3] << 32));
+        uint64_t g = (uint64_t)(((unsigned __int128)u * (unsigned __int128)T) >> 64);
+        uint64_t pos = 0;  /* index of the first element of shard j in the enumeration */
+        for (int32_t j = 0; j < G; ++j) {
+            int64_t size = n[j] < C ? n[j] : C;
+            uint64_t M = size >= 2 ? (uint64_t)(size - 1) : 0;
+            if (g < pos + M) {
+                shard[i] = j;
+                tau[i] = (n[j] - size) + (int64_t)(g - pos);
+                break;
+            }
+            pos += M;
+        }
+    }
+    return 0;
+}
+
 /* O3: stack(t)[c] = o_{t-3+c}, c = 0..3 (oldest -> newest; "concatenating the
  * images from four previous preprocessed frames"). Frame t-3+c is
  * replaced by zeros if it is no longer (or never was) in the ring
