@@ -224,7 +224,9 @@ def config_dict(args, world):
               f"max delay {args.max_staleness}, poison {args.poison}")
     else:
         wl = f"configs[3] sweep point: 1 learner/GPU, batch {args.batch}, {args.capacity}-frame replay"
-    return {"workload": wl,
+    if args.replay == "global":
+        wl += "; global replay (NEXT row f4): every batch drawn from the union of all learners' rings on all GPUs"
+    return {"workload": wl, "replay": args.replay,
             "n_actions": args.n_actions, "batch_per_learner": args.batch, "learners_per_gpu": args.learners,
             "global_batch": args.batch * world * args.learners,
             "replay_frames_per_learner": args.capacity, "target_period": args.target_period,
@@ -256,6 +258,8 @@ def main():
     ap.add_argument("--ps-mode", default="aggregate", choices=["aggregate", "per_message"],
                     help="per_message: NEXT row f1 (one optimizer step per accepted learner gradient)")
     ap.add_argument("--optimizer", default="rmsprop", choices=["rmsprop", "adagrad"])
+    ap.add_argument("--replay", default="local", choices=["local", "global"],
+                    help="global: NEXT row f4 (uniform over all learners' rings, NVLink gathers)")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--e2e-steps", type=int, default=1000)
@@ -286,7 +290,7 @@ def main():
     g = Gorila(n_actions=args.n_actions, batch=args.batch, replay_capacity=args.capacity, n_learners_local=L,
                learner_id_base=rank * L, rank=rank, world=world, nccl_unique_id=uid, stream=stream,
                theta0=synth.theta0(args.n_actions), math=args.math, target_period=args.target_period,
-               history=max(2, args.staleness + 1), max_staleness=args.max_staleness, ps_mode=args.ps_mode,
+               history=max(2, args.staleness + 1), max_staleness=args.max_staleness, ps_mode=args.ps_mode, replay_mode=args.replay,
                optimizer=args.optimizer)
     for j in range(L):
         fill_replay(g, j, args.capacity, args.n_actions, synth.SEED_DATA, rank * L + j, p_poison=args.poison)

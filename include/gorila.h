@@ -105,6 +105,17 @@ typedef struct {
                                   learner id, V += 1 each. 1 needs world == 1 or the
                                   peer-memory exchange (E_INVALID on the NCCL fallback) and
                                   world * n_learners_local <= 64. */
+    int32_t replay_mode;       /* 0: local, each learner samples its own ring (P:140 first form);
+                                  1: global (NEXT row f4, reading R36): every minibatch is drawn uniformly
+                                  from the union D of all learners' rings on all ranks ("a global replay
+                                  memory aggregates the experience into a distributed database", P:140;
+                                  "sampled from either a local or global experience replay memory D",
+                                  P:142), gathered from peer HBM over NVLink. Needs learner_id_base ==
+                                  rank * n_learners_local, world * n_learners_local <= 256 and, when
+                                  world > 1, the peer-memory mapping (E_INVALID otherwise). learner_step,
+                                  gorila_round and replay_sample then start with a device barrier over
+                                  the ranks (COLLECTIVE): inserts issued before them on any rank are
+                                  part of D. */
 } gorila_config;
 
 /* Per-learner outcome of one learner_step (Alg.1). */
@@ -165,6 +176,10 @@ GORILA_API gorila_status replay_insert(gorila_ctx* ctx, int32_t learner, int64_t
  * s_out / s2_out u8 [B][4][84][84], a_out u8[B], r_out f32[B], d_out u8[B].
  * Returns E_NOT_READY (no side effects) if size-1 < max(1, min_replay).
  * Synchronises the stream (parity / debugging entry point). */
+/* The shard of each sample of the most recent draw (replay_sample, or the last learner of
+ * learner_step): the global learner id whose ring it was gathered from (global replay), 0 in
+ * local mode. shard_out: host int32[B]. Synchronises the stream. */
+GORILA_API gorila_status replay_sample_shards(gorila_ctx* ctx, int32_t* shard_out);
 GORILA_API gorila_status replay_sample(gorila_ctx* ctx, int32_t learner, uint64_t round, int64_t* idx_out,
                             uint8_t* s_out, uint8_t* s2_out, uint8_t* a_out, float* r_out,
                             uint8_t* d_out);

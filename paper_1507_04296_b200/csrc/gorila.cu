@@ -123,6 +123,14 @@ struct gorila_ctx {
     uint8_t *sa, *sd;
     float* sr;
     int64_t* sidx;
+    int32_t* sshard;         // shard (global learner id) of each sample of the last draw (f4)
+    // global replay (NEXT row f4, cfg.replay_mode == 1): every learner's ring on every rank
+    bool replay_global = false;
+    ShardPtrs* shard_tab = nullptr;  // [W * L], rank-major (q, j): index = global learner id
+    int n_shards = 0;
+    uint64_t* rflags = nullptr;      // [MAX_W] replay-barrier epochs published by each rank
+    uint64_t* replay_epoch = nullptr;
+    uint64_t* n_snap = nullptr;      // [W * L] ring counters pushed by every rank at the replay barrier
     float* dQ;
     float* td_partial;  // [B][2] per-sample delta^2, |delta|
     int bias_chunks;
@@ -793,6 +801,15 @@ int eff_splits(bool fp32, int R, int splits) {
     } while (0)
 
 // ------------------------------------------------------------------ one learner update
+// GORILA_REPLAY_BARRIER=0: diagnostics only (timing; no parity guarantee across ranks)
+static bool replay_barrier_off() {
+    static const bool off = [] {
+        const char* e = getenv("GORILA_REPLAY_BARRIER");
+        return e && atoi(e) == 0;
+    }();
+    return off;
+}
+
 template <typename T>
 gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int accumulate,
                           uint32_t phases = 0xffffffffu) {
@@ -830,7 +847,10 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         dim3 grid((FRAME_BYTES / 16 + 255) / 256, B);
         uint2 key = make_uint2((uint32_t)cfg.seed, (uint32_t)(cfg.seed >> 32));
         launch(ctx, k_sample<T>, grid, dim3(256), 0, (const uint8_t*)Lr.frames, (const uint8_t*)Lr.a,
-               (const float*)Lr.r, (const uint8_t*)Lr.d, (int64_t)cfg.replay_capacity, (const uint64_t*)Lr.n_dev, key,
+               (const float*)Lr.r, (const uint8_t*)Lr.d, (int64_t)cfg.replay_capacity, (const uint64_t*)Lr.n_dev,
+               (const ShardPtrs*)(ctx->replay_global ? ctx->shard_tab : nullptr), ctx->n_shards,
+               (const uint64_t*)(ctx->replay_global && ctx->W > 1 && !replay_barrier_off() ? ctx->n_snap : nullptr),
+               ctx->sshard, key,
                (uint32_t)(cfg.learner_id_base + j), (const uint64_t*)ctx->dev_round, B, s, s2, ctx->sa, ctx->sr,
                ctx->sd, ctx->sidx, accumulate ? (uint32_t*)nullptr : ctx->n_acc_local);
     }
@@ -1469,6 +1489,11 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     uint8_t* sd = c.take<uint8_t>(Bs);
     float* sr = c.take<float>(Bs);
     int64_t* sidx = c.take<int64_t>(Bs);
+    int32_t* sshard = c.take<int32_t>(Bs);
+    ShardPtrs* shard_tab = c.take<ShardPtrs>((int64_t)W * L);
+    uint64_t* rflags = c.take<uint64_t>(MAX_W);
+    uint64_t* replay_epoch = c.take<uint64_t>(1);
+    uint64_t* n_snap = c.take<uint64_t>((int64_t)W * L);
     float* dQ = c.take<float>(Bs * nA);
     float* td_partial = c.take<float>(Bs * 2);
     const int bias_chunks = std::max(64, std::min(2048, 2 * B));
@@ -1523,6 +1548,9 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         ctx->t1 = t1; ctx->t2 = t2; ctx->t3 = t3; ctx->t4 = t4;
         ctx->g1 = g1; ctx->g2 = g2; ctx->g3 = g3; ctx->g4 = g4;
         ctx->sa = sa; ctx->sd = sd; ctx->sr = sr; ctx->sidx = sidx; ctx->dQ = dQ;
+        ctx->sshard = sshard; ctx->shard_tab = shard_tab; ctx->rflags = rflags; ctx->replay_epoch = replay_epoch;
+        ctx->n_snap = n_snap;
+        ctx->n_shards = W * L; ctx->replay_global = cfg->replay_mode == 1;
         ctx->td_partial = td_partial; ctx->bias_chunks = bias_chunks;
         for (int l = 0; l < 3; ++l) { ctx->part_w[l] = part_w[l]; ctx->split_w[l] = split_w[l]; }
         ctx->part_b = part_b;
@@ -1651,6 +1679,11 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     if (cfg->history < 1 || cfg->history > 64) return fail(GORILA_E_INVALID, "history must be in [1, 64]");
     if (cfg->target_period < 1) return fail(GORILA_E_INVALID, "target_period must be >= 1");
     if (cfg->ps_mode != 0 && cfg->ps_mode != 1) return fail(GORILA_E_INVALID, "ps_mode must be 0 or 1");
+    if (cfg->replay_mode != 0 && cfg->replay_mode != 1) return fail(GORILA_E_INVALID, "replay_mode must be 0 or 1");
+    if (cfg->replay_mode == 1 && (cfg->learner_id_base != cfg->rank * cfg->n_learners_local ||
+                                  cfg->world * cfg->n_learners_local > MAX_SHARDS))
+        return fail(GORILA_E_INVALID, "global replay: learner_id_base must be rank * n_learners_local, "
+                                      "at most 256 learners in total");
     if (cfg->ps_mode == 1 && (cfg->n_learners_local > 32 || cfg->world * cfg->n_learners_local > 64))
         return fail(GORILA_E_INVALID, "per-message mode: at most 32 learners per rank, 64 in total");
     if (!cfg->theta0) return fail(GORILA_E_INVALID, "theta0 is required");
@@ -1682,6 +1715,8 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     CU(cudaMemsetAsync(ctx->p2p_counter, 0, sizeof(unsigned int) * 2, st));
     CU(cudaMemsetAsync(ctx->apply_counter, 0, sizeof(unsigned int), st));
     CU(cudaMemsetAsync(ctx->fc5_gen, 0, sizeof(unsigned int) * 2, st));
+    CU(cudaMemsetAsync(ctx->rflags, 0, sizeof(uint64_t) * MAX_W, st));
+    CU(cudaMemsetAsync(ctx->replay_epoch, 0, sizeof(uint64_t), st));
     ctx->dev_round_expect = 0;
     {
         const char* e = getenv("GORILA_PDL");  // GORILA_PDL=0 disables programmatic dependent launch
@@ -1751,6 +1786,18 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
             gorila_destroy(ctx);
             return fail(GORILA_E_INVALID, "per-message mode needs the peer-memory exchange (world > 1)");
         }
+        if (ctx->replay_global && !ctx->p2p) {
+            gorila_destroy(ctx);
+            return fail(GORILA_E_INVALID, "global replay needs the peer-memory mapping (world > 1)");
+        }
+    }
+    if (ctx->replay_global) {  // f4: the shard table, every rank's rings at their address in this process
+        std::vector<ShardPtrs> tab;
+        for (int q = 0; q < cfg->world; ++q)
+            for (const Learner& l : ctx->learners)
+                tab.push_back({peer_ptr(ctx, q, l.frames), peer_ptr(ctx, q, l.a), peer_ptr(ctx, q, l.r),
+                               peer_ptr(ctx, q, l.d), peer_ptr(ctx, q, l.n_dev)});
+        CU(cudaMemcpyAsync(ctx->shard_tab, tab.data(), sizeof(ShardPtrs) * tab.size(), cudaMemcpyHostToDevice, st));
     }
     CU(stage_alloc(ctx));
     CU(cudaStreamSynchronize(st));
@@ -1886,6 +1933,15 @@ gorila_status replay_insert(gorila_ctx* ctx, int32_t learner, int64_t count, con
     return GORILA_OK;
 }
 
+static void replay_barrier(gorila_ctx* ctx);
+
+gorila_status replay_sample_shards(gorila_ctx* ctx, int32_t* shard_out) {
+    if (!ctx || !shard_out) return fail(GORILA_E_INVALID, "null argument");
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaMemcpy(shard_out, ctx->sshard, sizeof(int32_t) * ctx->B, cudaMemcpyDeviceToHost));
+    return GORILA_OK;
+}
+
 gorila_status replay_sample(gorila_ctx* ctx, int32_t learner, uint64_t round, int64_t* idx_out, uint8_t* s_out,
                             uint8_t* s2_out, uint8_t* a_out, float* r_out, uint8_t* d_out) {
     gorila_status s = check_learner(ctx, learner);
@@ -1901,12 +1957,17 @@ gorila_status replay_sample(gorila_ctx* ctx, int32_t learner, uint64_t round, in
     ctx->dev_round_expect = round;
     dim3 grid((FRAME_BYTES / 16 + 255) / 256, B);
     uint2 key = make_uint2((uint32_t)cfg.seed, (uint32_t)(cfg.seed >> 32));
+    replay_barrier(ctx);
+    const ShardPtrs* tab = ctx->replay_global ? ctx->shard_tab : nullptr;
+    const uint64_t* snap = ctx->replay_global && ctx->W > 1 && !replay_barrier_off() ? ctx->n_snap : nullptr;
     if (cfg.math == GORILA_MATH_FP32)
-        k_sample<float><<<grid, 256, 0, st>>>(l.frames, l.a, l.r, l.d, cfg.replay_capacity, l.n_dev, key,
+        k_sample<float><<<grid, 256, 0, st>>>(l.frames, l.a, l.r, l.d, cfg.replay_capacity, l.n_dev, tab,
+                                              ctx->n_shards, snap, ctx->sshard, key,
                                               (uint32_t)(cfg.learner_id_base + learner), ctx->dev_round, B, (float*)ctx->s,
                                               (float*)ctx->s2, ctx->sa, ctx->sr, ctx->sd, ctx->sidx, nullptr);
     else
-        k_sample<__nv_bfloat16><<<grid, 256, 0, st>>>(l.frames, l.a, l.r, l.d, cfg.replay_capacity, l.n_dev, key,
+        k_sample<__nv_bfloat16><<<grid, 256, 0, st>>>(l.frames, l.a, l.r, l.d, cfg.replay_capacity, l.n_dev, tab,
+                                                      ctx->n_shards, snap, ctx->sshard, key,
                                                       (uint32_t)(cfg.learner_id_base + learner), ctx->dev_round,
                                                       B, (__nv_bfloat16*)ctx->s, (__nv_bfloat16*)ctx->s2, ctx->sa,
                                                       ctx->sr, ctx->sd, ctx->sidx, nullptr);
@@ -1941,6 +2002,22 @@ gorila_status replay_sample(gorila_ctx* ctx, int32_t learner, uint64_t round, in
                 }
     }
     return GORILA_OK;
+}
+
+// global replay across ranks (f4): the device barrier of k_replay_barrier (no-op otherwise)
+static void replay_barrier(gorila_ctx* ctx) {
+    if (!ctx->replay_global || ctx->W == 1 || replay_barrier_off()) return;
+    ReplayBarrier p{};
+    p.epoch = ctx->replay_epoch;
+    for (int q = 0; q < ctx->W; ++q) {
+        p.flags[q] = peer_ptr(ctx, q, ctx->rflags);
+        p.n_snap[q] = peer_ptr(ctx, q, ctx->n_snap);
+    }
+    p.tab = ctx->shard_tab;
+    p.W = ctx->W;
+    p.rank = ctx->rank;
+    p.L = ctx->L;
+    launch(ctx, k_replay_barrier, dim3(1), dim3(32), 0, p);
 }
 
 gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
@@ -1978,6 +2055,7 @@ gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
             const int64_t size = std::min<int64_t>(l.n_host, ctx->cfg.replay_capacity);
             if (size - 1 >= std::max<int64_t>(1, ctx->cfg.min_replay)) ctx->early_learner = learners[i];
         }
+    replay_barrier(ctx);  // f4: every rank's earlier inserts visible before the first draw
     int ran = 0;  // the first learner that runs stores G, later ones accumulate (no memset)
     for (int i = 0; i < n; ++i) {
         const int j = learners[i];

@@ -7,6 +7,16 @@ namespace gorila {
 
 constexpr uint32_t TAG_SAMPLE = 3u;
 
+// one learner's replay ring as seen from this rank (local or a peer's, mapped over NVLink)
+struct ShardPtrs {
+    const uint8_t* frames;
+    const uint8_t* a;
+    const float* r;
+    const uint8_t* d;
+    const uint64_t* n;  // steps inserted so far (device counter)
+};
+constexpr int MAX_SHARDS = 256;
+
 
 // ------------------------------------------------------------------------- K1 sampler
 // Alg.1 P:121 "Sample random mini-batch from D"; "(s,a,r,s') ~ U(D)"; P:181 4-frame stack.
@@ -14,10 +24,17 @@ constexpr uint32_t TAG_SAMPLE = 3u;
 // tau = (n - size) + floor(u * (size-1) / 2^64); thread = one 16-pixel chunk of the 84x84
 // frame: reads the 5 frames o_{tau-3} .. o_{tau+1} (16 B each, coalesced), applies the
 // episode / eviction zero mask and writes s, s' as NHWC [B][84][84][4] in T.
+// Global replay (NEXT row f4, reading R36; tab != nullptr): the draw is over the union of the G
+// shards' valid transitions, T = sum_j (size_j - 1), g = floor(u * T / 2^64), and (shard, tau) is
+// the g-th transition in (shard, tau) order; the gather then reads that shard's ring, local or in
+// a peer's HBM over NVLink. G = 1 is exactly the local draw.
 template <typename T>
 __global__ void __launch_bounds__(256) k_sample(const uint8_t* __restrict__ frames, const uint8_t* __restrict__ ring_a,
                                                 const float* __restrict__ ring_r, const uint8_t* __restrict__ ring_d,
-                                                int64_t C, const uint64_t* __restrict__ ring_n, uint2 key,
+                                                int64_t C, const uint64_t* __restrict__ ring_n,
+                                                const ShardPtrs* __restrict__ tab, int G,
+                                                const uint64_t* __restrict__ n_snap, int32_t* __restrict__ shard_out,
+                                                uint2 key,
                                                 uint32_t learner_gid, const uint64_t* __restrict__ round_ptr, int B,
                                                 T* __restrict__ s_out,
                                                 T* __restrict__ s2_out, uint8_t* __restrict__ a_out,
@@ -28,34 +45,103 @@ __global__ void __launch_bounds__(256) k_sample(const uint8_t* __restrict__ fram
     const int b = blockIdx.y;
     if (n_acc_reset && b == 0 && blockIdx.x == 0 && threadIdx.x == 0) *n_acc_reset = 0;  // first learner of a round
     const uint64_t round = *round_ptr;  // device-resident round counter (graph replay friendly)
-    const int64_t n = (int64_t)*ring_n;
-    const int64_t size = n < C ? n : C;
-    const uint64_t M = (uint64_t)(size - 1);
     const uint4 x = philox4x32_10(make_uint4((uint32_t)(b >> 1), learner_gid, (uint32_t)round,
                                              (uint32_t)((round >> 32) & 0xffffffu) | (TAG_SAMPLE << 24)),
                                   key);
     const uint64_t u = (b & 1) ? ((uint64_t)x.z | ((uint64_t)x.w << 32)) : ((uint64_t)x.x | ((uint64_t)x.y << 32));
-    const int64_t tau = (n - size) + (int64_t)__umul64hi(u, M);
+    int64_t n, tau;
+    int shard = 0;
+#ifdef GORILA_TRACE
+    long long tr[5] = {clock64(), 0, 0, 0, 0};
+    bool tr_own = true;
+#endif
+    if (tab) {  // f4: every shard's counter (read after the round's replay barrier), then the union index
+        __shared__ uint64_t s_n[MAX_SHARDS];
+        __shared__ int64_t s_tau;
+        __shared__ int s_shard;
+        // world > 1: the counters every rank pushed into n_snap with its barrier flag (local reads)
+        for (int j = threadIdx.x; j < G; j += blockDim.x)
+            s_n[j] = n_snap ? n_snap[j] : *(volatile const uint64_t*)tab[j].n;
+        __syncthreads();
+#ifdef GORILA_TRACE
+        tr[1] = clock64();
+#endif
+        if (threadIdx.x == 0) {
+            uint64_t Tot = 0;
+            for (int j = 0; j < G; ++j) {
+                const int64_t sz = (int64_t)s_n[j] < C ? (int64_t)s_n[j] : C;
+                Tot += sz >= 2 ? (uint64_t)(sz - 1) : 0;
+            }
+            const uint64_t g = __umul64hi(u, Tot);
+            uint64_t pos = 0;
+            for (int j = 0; j < G; ++j) {
+                const int64_t nj = (int64_t)s_n[j], sz = nj < C ? nj : C;
+                const uint64_t M = sz >= 2 ? (uint64_t)(sz - 1) : 0;
+                if (g < pos + M) {
+                    s_shard = j;
+                    s_tau = (nj - sz) + (int64_t)(g - pos);
+                    break;
+                }
+                pos += M;
+            }
+        }
+        __syncthreads();
+        shard = s_shard;
+        tau = s_tau;
+        n = (int64_t)s_n[shard];
+#ifdef GORILA_TRACE
+        tr[2] = clock64();
+        tr_own = tab[shard].frames == frames;
+#endif
+        frames = tab[shard].frames;
+        ring_a = tab[shard].a;
+        ring_r = tab[shard].r;
+        ring_d = tab[shard].d;
+    } else {
+        n = (int64_t)*ring_n;
+        const int64_t size = n < C ? n : C;
+        tau = (n - size) + (int64_t)__umul64hi(u, (uint64_t)(size - 1));
+    }
+    const int64_t size = n < C ? n : C;
     const int64_t oldest = n - size;
 
+    // the four episode flags and a_tau / r_tau: loaded once per block (a peer's ring is read over
+    // NVLink, where 441 threads re-reading the same bytes would be 441 remote requests each), and
+    // issued before the frame loads so that they do not queue behind the frame traffic
+    __shared__ uint8_t s_d[4], s_a;
+    __shared__ float s_r;
+    uint8_t dv = 1, av = 0;
+    float rv = 0.f;
+    if (threadIdx.x < 4) {
+        const int64_t st = tau - 3 + threadIdx.x;
+        if (st >= oldest) dv = __ldcg(ring_d + st % C);  // d_tau itself: tau >= oldest always
+    } else if (threadIdx.x == 32) {
+        av = __ldcg(ring_a + tau % C);
+    } else if (threadIdx.x == 64) {
+        rv = __ldcg(ring_r + tau % C);
+    }
     const int chunk = blockIdx.x * blockDim.x + threadIdx.x;
-    uint4 f[5];  // issued with the d-flag loads (not after them): the keep masks zero channels later
+    uint4 f[5];  // issued before the flags are used: the keep masks zero channels later
 #pragma unroll
     for (int t = 0; t < 5; ++t) {
         int64_t st = tau - 3 + t;
         f[t] = (st >= 0 && chunk < FRAME_BYTES / 16)
-                   ? *reinterpret_cast<const uint4*>(frames + (st % C) * FRAME_BYTES + chunk * 16)
+                   ? __ldcg(reinterpret_cast<const uint4*>(frames + (st % C) * FRAME_BYTES + chunk * 16))
                    : make_uint4(0, 0, 0, 0);
     }
+    if (threadIdx.x < 4) s_d[threadIdx.x] = dv != 0;
+    else if (threadIdx.x == 32) s_a = av;
+    else if (threadIdx.x == 64) s_r = rv;
+    __syncthreads();
+#ifdef GORILA_TRACE
+    tr[3] = clock64();
+#endif
     // keep[f] for frames tau-3+f, f = 0..4 (s uses f = 0..3, s' uses f = 1..4)
     bool keep_s[4], keep_s2[4];
     {
-        bool dflag[4];  // d_{tau-3+t}, t = 0..3 (only read when the frame is retained)
+        bool dflag[4];  // d_{tau-3+t}, t = 0..3 (only used when the frame is retained)
 #pragma unroll
-        for (int t = 0; t < 4; ++t) {
-            int64_t st = tau - 3 + t;
-            dflag[t] = (st >= oldest) ? (ring_d[st % C] != 0) : true;
-        }
+        for (int t = 0; t < 4; ++t) dflag[t] = s_d[t] != 0;
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
             // s channel c = frame tau-3+c: zero if evicted or an episode ended at t' in [tau-3+c, tau-1]
@@ -102,10 +188,17 @@ __global__ void __launch_bounds__(256) k_sample(const uint8_t* __restrict__ fram
         }
     }
     if (blockIdx.x == 0 && threadIdx.x == 0) {
-        a_out[b] = ring_a[tau % C];
-        r_out[b] = ring_r[tau % C];
-        d_out[b] = ring_d[tau % C];
+        a_out[b] = s_a;
+        r_out[b] = s_r;
+        d_out[b] = s_d[3];
         idx_out[b] = tau;
+        if (shard_out) shard_out[b] = shard;
+#ifdef GORILA_TRACE
+        tr[4] = clock64();
+        const int o = tr_own ? 0 : 8;
+        for (int i = 1; i < 5; ++i) atomicAdd(&gorila_trace_buf[o + i - 1], (unsigned long long)(tr[i] - tr[i - 1]));
+        atomicAdd(&gorila_trace_buf[o + 4], 1ull);
+#endif
     }
 }
 
@@ -818,6 +911,43 @@ GORILA_DEV void wait_flag(const uint64_t* p, uint64_t ep) {
         if (n > (1u << 25)) __trap();
         __nanosleep(64);
     }
+}
+
+// global replay (f4, R36): before a round's first draw every rank's earlier inserts must be
+// visible to every rank. Rank r bumps its epoch, publishes it into slot r of every peer's flag
+// array (system-scope release after a system fence: cumulative over the insert kernels that
+// completed before this one on the stream) and waits until all peers' epochs reached it.
+// A peer cannot overwrite a slot this round reads before the round ends: its next insert
+// follows its own round, whose parameter exchange needs this rank's gradient, i.e. this draw.
+// With the flag, rank r pushes its learners' ring counters into every rank's n_snap (slots r*L ..
+// r*L+L-1), so the sampler finds all G counters in local memory once the flags have arrived.
+struct ReplayBarrier {
+    uint64_t* epoch;             // this rank's round epoch (device counter)
+    uint64_t* flags[MAX_W];      // rank q's flag array [MAX_W]
+    uint64_t* n_snap[MAX_W];     // rank q's counter snapshot [G]
+    const ShardPtrs* tab;
+    int W, rank, L;
+};
+__global__ void k_replay_barrier(ReplayBarrier p) {
+    pdl_wait();
+    for (int j = threadIdx.x; j < p.L; j += blockDim.x) {
+        const int gid = p.rank * p.L + j;
+        const uint64_t v = *(volatile const uint64_t*)p.tab[gid].n;
+        for (int q = 0; q < p.W; ++q) p.n_snap[q][gid] = v;
+    }
+    __threadfence_system();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        const uint64_t e = *p.epoch + 1;
+        *p.epoch = e;
+        __threadfence_system();
+        for (int q = 0; q < p.W; ++q)
+            if (q != p.rank) st_release_sys(p.flags[q] + p.rank, e);
+        for (int q = 0; q < p.W; ++q)
+            if (q != p.rank) wait_flag(p.flags[p.rank] + q, e);
+    }
+    __syncthreads();
+    pdl_trigger();
 }
 struct P2PParams {
     int W, rank;

@@ -39,7 +39,8 @@ class Config(ctypes.Structure):
                 ("outlier_enabled", ctypes.c_int32), ("outlier_warmup", ctypes.c_int32),
                 ("outlier_k", ctypes.c_float), ("outlier_beta", ctypes.c_double), ("min_replay", ctypes.c_int64),
                 ("seed", ctypes.c_uint64), ("math", ctypes.c_int32), ("history", ctypes.c_int32),
-                ("theta0", ctypes.c_void_p), ("ps_mode", ctypes.c_int32)]
+                ("theta0", ctypes.c_void_p), ("ps_mode", ctypes.c_int32),
+                ("replay_mode", ctypes.c_int32)]
 
 
 class LearnerInfo(ctypes.Structure):
@@ -58,7 +59,7 @@ class RoundInfo(ctypes.Structure):
 
 
 EXPORTS = ["gorila_param_count", "gorila_workspace_bytes", "gorila_init", "gorila_destroy", "gorila_last_error",
-           "replay_insert", "replay_sample", "learner_step", "ps_apply_shard", "sync_target", "gorila_get_state",
+           "replay_insert", "replay_sample", "replay_sample_shards", "learner_step", "ps_apply_shard", "sync_target", "gorila_get_state",
            "gorila_set_state", "gorila_get_learner_state", "gorila_set_learner_state", "gorila_get_grad",
            "gorila_get_q", "gorila_get_activation", "gorila_act", "gorila_kernel_launches", "gorila_profile_enable", "gorila_profile_read",
            "gorila_profile_phase_count", "gorila_profile_phase_name", "gorila_nccl_unique_id", "gorila_round",
@@ -87,6 +88,7 @@ def load(build_if_missing=True):
     L.gorila_last_error.restype = ctypes.c_char_p
     L.replay_insert.argtypes = [P, i32, i64, P, P, P, P, i32]
     L.replay_sample.argtypes = [P, i32, u64, P, P, P, P, P, P]
+    L.replay_sample_shards.argtypes = [P, P]
     L.learner_step.argtypes = [P, P, i32, u64, P, P]
     L.ps_apply_shard.argtypes = [P, u64, P]
     L.sync_target.argtypes = [P, P, i32, i32, P]
@@ -161,7 +163,8 @@ class Gorila:
                  learner_id_base=0, rank=0, world=1, nccl_unique_id=None, stream=None, theta0=None,
                  optimizer="rmsprop", lr=2.5e-4, rms_rho=0.95, rms_eps=0.01, ada_eps=1e-8, target_period=100,
                  max_staleness=-1, outlier_enabled=True, outlier_warmup=100, outlier_k=3.0, outlier_beta=0.999,
-                 min_replay=1, seed=1507, math="bf16", history=2, device=None, ps_mode="aggregate"):
+                 min_replay=1, seed=1507, math="bf16", history=2, device=None, ps_mode="aggregate",
+                 replay_mode="local"):
         import torch
         L = load()
         self.torch = torch
@@ -185,6 +188,7 @@ class Gorila:
                      outlier_enabled=int(outlier_enabled), outlier_warmup=outlier_warmup, outlier_k=outlier_k,
                      outlier_beta=outlier_beta, min_replay=min_replay, seed=seed,
                      ps_mode={"aggregate": 0, "per_message": 1}[ps_mode],
+                     replay_mode={"local": 0, "global": 1}[replay_mode],
                      math={"fp32": 0, "bf16": 2}[math], history=history, theta0=theta0.ctypes.data)
         nbytes = int(L.gorila_workspace_bytes(ctypes.byref(cfg)))
         self.workspace = torch.empty(nbytes, dtype=torch.uint8, device=self.device)
@@ -219,6 +223,12 @@ class Gorila:
         _check(load().replay_insert(self.h, learner, count, fp, ap, rp, dp, int(dev)))
         if dev:  # the copies read the sources on our stream: the caller's stream may reuse them after
             self.torch.cuda.current_stream(self.device).wait_stream(self.stream)
+
+    def replay_sample_shards(self):
+        """Shard (global learner id) of each sample of the most recent draw (f4)."""
+        out = np.zeros(self.batch, np.int32)
+        _check(load().replay_sample_shards(self.h, out.ctypes.data))
+        return out
 
     def replay_sample(self, learner, rnd):
         B = self.batch

@@ -106,7 +106,10 @@ def _check_round(gpu, res, math, nA, learners, orc=None, thetas=None):
         if oi["accepted"]:
             G_ref += oi["G"]
             if orc is not None and thetas is not None:
-                s, _, _, _, _ = orc.learners[j].ring.gather(oi["tau"])
+                if oi.get("shard") is not None:  # f4: the batch came from the union of the rings
+                    s = O.gather_global([orc.learners[q].ring for q in sorted(orc.learners)], oi["shard"], oi["tau"])[0]
+                else:
+                    s, _, _, _, _ = orc.learners[j].ring.gather(oi["tau"])
                 kink = max(kink, ambiguous_layer(thetas[j], s, nA, mode="exact" if math == "fp32" else "bf16"))
     if np.any(G_ref):
         relaxed = tol["g_kink"]
@@ -219,6 +222,47 @@ def test_f1_per_message_ps_parity(math, opt):
         n_msg = max(1, res["n_accepted"])
         _check_dtheta(gpu, orc, th_before, math, nA,
                       tol_dtheta=max(TOL[math]["dtheta"], n_msg * TOL[math]["g"]), n_round=n_msg + 1)
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
+def test_f4_global_replay_parity(math):
+    """NEXT row f4 (R36): three learners draw from the union of their rings -- unequal fills, one
+    ring wrapped -- (shard, tau), frames, a / r / d bit-exact; then whole rounds against the oracle."""
+    nA, L, C, B = 6, 3, 1200, 24
+    g, orc = make_pair(nA=nA, B=B, C=C, n_insert=300, math=math, L=L, replay_mode="global",
+                       outlier_warmup=2, target_period=3)
+    f = synth.frames(synth.SEED_DATA, 1, 300, 1500)  # learner 1: 1800 steps in a 1200-slot ring
+    a, r, d = synth.meta(synth.SEED_DATA, 1, 300, 1500, nA)
+    g.replay_insert(1, f, a, r, d)
+    orc.insert(1, f, a, r, d)
+    ids = list(range(L))
+    rings = [orc.learners[q].ring for q in ids]
+    seen = set()
+    for k in range(4):
+        for j in ids:
+            gs = g.replay_sample(j, k)
+            shard, tau = O.sample_indices_global([rg.n for rg in rings], C, B, 1507, j, k)
+            assert np.array_equal(g.replay_sample_shards(), shard) and np.array_equal(gs["tau"], tau)
+            s, s2, a_, r_, d_ = O.gather_global(rings, shard, tau)
+            assert np.array_equal(gs["s"], s) and np.array_equal(gs["s2"], s2)
+            assert np.array_equal(gs["a"], a_) and np.array_equal(gs["r"], r_) and np.array_equal(gs["d"], d_)
+            seen |= set(shard.tolist())
+        teacher_force(g, orc)
+        th = orc.theta.copy()
+        gpu, res = run_round_both(g, orc, k, ids)
+        _check_round(gpu, res, math, nA, ids, orc, {j: th for j in ids})
+        _check_dtheta(gpu, orc, th, math, nA)
+    assert seen == {0, 1, 2}
+
+
+def test_f4_global_replay_single_learner_is_local():
+    """G = 1: the global draw is the local one (same indices, same batch)."""
+    gl, _ = make_pair(nA=4, B=16, C=500, n_insert=700, math="fp32", replay_mode="global")
+    lo, _ = make_pair(nA=4, B=16, C=500, n_insert=700, math="fp32")
+    for k in range(3):
+        a, b = gl.replay_sample(0, k), lo.replay_sample(0, k)
+        assert all(np.array_equal(a[x], b[x]) for x in a)
+        assert not gl.replay_sample_shards().any()
 
 
 @pytest.mark.parametrize("math", ["fp32", "bf16"])

@@ -8,6 +8,9 @@ runs the CPU oracle with all N learners on one parameter server and checks, each
 decisions and versions exactly, Q of its own learner, and the parameter update (normalised
 L2 of the update, fp32 check mode: 1e-5 + the fp32 state floor). All ranks check that their
 theta+ replicas are bitwise identical after the all-gather. Exits non-zero on failure.
+REPLAY=global (NEXT row f4): every learner draws from the union of all ranks' rings (unequal
+fills, one wrapped), gathered over NVLink; each rank also checks its own draw (shard, tau,
+frames, a / r / d) bit-exact against the oracle's global draw.
 """
 import os
 import sys
@@ -31,28 +34,47 @@ def main():
     math = os.environ.get("MATH", "fp32")
     ps_mode = os.environ.get("PS_MODE", "aggregate")  # "per_message": NEXT row f1 over the peer-memory exchange
     rounds = int(os.environ.get("ROUNDS", "4"))
+    replay = os.environ.get("REPLAY", "local")
+    fill = (lambda j: [1500, 700, 1000, 400][j % 4]) if replay == "global" else (lambda j: C)
     nA, B, C = 6, 16, 1200
     obj = [nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     theta0 = synth.theta0(nA)
     g = Gorila(n_actions=nA, batch=B, replay_capacity=C, n_learners_local=1, learner_id_base=rank, rank=rank,
                world=world, nccl_unique_id=obj[0], theta0=theta0, math=math, target_period=3, outlier_warmup=2,
-               ps_mode=ps_mode)
-    f = synth.frames(synth.SEED_DATA, rank, 0, C)
-    a, r, d = synth.meta(synth.SEED_DATA, rank, 0, C, nA)
+               ps_mode=ps_mode, replay_mode=replay)
+    f = synth.frames(synth.SEED_DATA, rank, 0, fill(rank))
+    a, r, d = synth.meta(synth.SEED_DATA, rank, 0, fill(rank), nA)
     g.replay_insert(0, f, a, r, d)
+    rings = None
+    if replay == "global":  # every rank holds the oracle's copy of all rings to check its own draws
+        rings = []
+        for j in range(world):
+            rg = O.Ring(C)
+            rg.insert(synth.frames(synth.SEED_DATA, j, 0, fill(j)), *synth.meta(synth.SEED_DATA, j, 0, fill(j), nA))
+            rings.append(rg)
     orc = None
     if rank == 0:
         orc = O.GorilaOracle(O.Config(n_actions=nA, batch=B, capacity=C, learners=tuple(range(world)),
                                       mode="exact" if math == "fp32" else "bf16", target_period=3,
-                                      outlier_warmup=2, ps_mode=ps_mode), theta0)
+                                      outlier_warmup=2, ps_mode=ps_mode, replay_mode=replay), theta0)
         for j in range(world):
-            fj = synth.frames(synth.SEED_DATA, j, 0, C)
-            aj, rj, dj = synth.meta(synth.SEED_DATA, j, 0, C, nA)
+            fj = synth.frames(synth.SEED_DATA, j, 0, fill(j))
+            aj, rj, dj = synth.meta(synth.SEED_DATA, j, 0, fill(j), nA)
             orc.insert(j, fj, aj, rj, dj)
     ok = True
     tol = 1e-5 if math == "fp32" else 5e-3
     for k in range(rounds):
+        if rings is not None:  # f4: this rank's draw, bit-exact (replay_sample is collective here)
+            gs = g.replay_sample(0, k)
+            shard, tau = O.sample_indices_global([rg.n for rg in rings], C, B, 1507, rank, k)
+            s_, s2_, a_, r_, d_ = O.gather_global(rings, shard, tau)
+            same = (np.array_equal(g.replay_sample_shards(), shard) and np.array_equal(gs["tau"], tau) and
+                    np.array_equal(gs["s"], s_) and np.array_equal(gs["s2"], s2_) and np.array_equal(gs["a"], a_)
+                    and np.array_equal(gs["r"], r_) and np.array_equal(gs["d"], d_))
+            print(f"[rank {rank}] round {k}: global draw shards {np.bincount(shard, minlength=world).tolist()} "
+                  f"{'bit-exact' if same else 'MISMATCH'}", flush=True)
+            ok = ok and same
         th0 = g.get_state()[0]
         info = g.learner_step([0], k)[0]
         q = g.get_q(0)[0]
