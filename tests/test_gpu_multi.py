@@ -10,13 +10,15 @@ pytestmark = pytest.mark.gpu
 
 
 @pytest.mark.parametrize("math", ["fp32", "bf16"])
-def test_sharded_ps_over_nccl_matches_oracle(math):
+@pytest.mark.parametrize("mode", [{}, {"PS_MODE": "per_message"}, {"REPLAY": "global"}],
+                         ids=["aggregate", "per_message_f1", "global_replay_f4"])
+def test_sharded_ps_over_nccl_matches_oracle(math, mode):
     import torch
     n = torch.cuda.device_count()
     if n < 2:
         pytest.skip("needs >= 2 GPUs")
     n = min(n, 4)
-    env = dict(os.environ, MATH=math, ROUNDS="4")
+    env = dict(os.environ, MATH=math, ROUNDS="4", **mode)
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
            "--master-addr", "127.0.0.1", "--master-port", str(29600 + (os.getpid() % 500)),
            os.path.join(ROOT, "tools", "multi_gpu_check.py")]
