@@ -888,7 +888,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             cudaFuncSetAttribute(k_conv_tower, cudaFuncAttributeMaxDynamicSharedMemorySize, tower::SMEM);
             attr = true;
         }
-        launch(ctx, k_conv_tower, dim3(B, 2), dim3(192), tower::SMEM, tp);
+        launch(ctx, k_conv_tower, dim3(B, 2), dim3(tower::THREADS), tower::SMEM, tp);
     } else {
     // conv1 fwd (online on s with theta, target on s' with theta^-)
     {

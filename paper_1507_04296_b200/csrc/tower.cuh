@@ -9,7 +9,11 @@
 // stores visible to the tensor core. a1, a2, a3 also go to global memory (the backward reads them).
 // The weights of all three layers (152 KB, bf16, per-chunk TMA boxes with their own mbarriers)
 // and the sample's conv1 input planes arrive by TMA at the start.
-// Warp 0: TMA; warp 1: tcgen05.mma issuer; warps 2..5: epilogues (TMEM lanes 32*(w%4)..).
+// Warp 0: TMA; warp 1: tcgen05.mma issuer; warps 2..9: epilogues (TMEM lanes 32*(w%4).., warps
+// 2..5 the first half of each layer's columns, 6..9 the second). conv1 is committed per M-block:
+// the epilogue of block mb (TMEM -> bias, ReLU, bf16 -> global) runs under the MMAs of mb+1 and
+// keeps its packed a1 in registers; the scatter into conv2's planes (which overlap the conv1 input
+// planes) waits for the last block.
 #pragma once
 #include "common.cuh"
 #include "gemm.cuh"
@@ -44,7 +48,9 @@ constexpr int A2_OFF = A_OFF + 4 * A1_PLANE;        // 148 rows x 128 B
 constexpr int A2_BYTES = 19456;
 constexpr int BAR_OFF = A_OFF + 4 * S_PLANE;        // 221184
 constexpr int NB_W = 16 + 16 + 9;
-constexpr int BIAS_OFF = BAR_OFF + 8 * (NB_W + 8);  // 160 floats: b1, b2, b3
+constexpr int NB_ACC = 6;                           // conv1 per M-block [0, 4), conv2 [4], conv3 [5]
+constexpr int BIAS_OFF = BAR_OFF + 8 * (NB_W + 12);  // 160 floats: b1, b2, b3
+constexpr int THREADS = 320;
 constexpr int SMEM = BIAS_OFF + 160 * 4 + 1024;
 static_assert(A2_OFF + A2_BYTES <= BAR_OFF, "a1 / a2 fit in the s-plane region");
 }  // namespace tower
@@ -73,14 +79,14 @@ GORILA_DEV void st_swz16(uint8_t* region, uint32_t o, int b, uint4 v) {
     *reinterpret_cast<uint4*>(region + po) = v;
 }
 
-__global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ TowerParams p) {
+__global__ void __launch_bounds__(tower::THREADS) k_conv_tower(const __grid_constant__ TowerParams p) {
     using namespace tower;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* sm = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint64_t* w_full = reinterpret_cast<uint64_t*>(sm + BAR_OFF);  // [41] weight chunks
     uint64_t* s_full = w_full + NB_W;                               // conv1 input planes
-    uint64_t* acc_full = s_full + 1;                                // [3] MMA -> epilogue, per layer
-    uint64_t* act_ready = acc_full + 3;                             // [2] a1 / a2 in smem (epilogue -> MMA)
+    uint64_t* acc_full = s_full + 1;                                // [NB_ACC] MMA -> epilogue
+    uint64_t* act_ready = acc_full + NB_ACC;                        // [2] a1 / a2 in smem (epilogue -> MMA)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_ready + 2);
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
     const int z = blockIdx.y, b = blockIdx.x;
@@ -89,12 +95,13 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
     if (warp == 0) tmem_alloc(tmem_slot, 256);
     // rows of the s planes past the 441 loaded ones are read by dropped output rows only
     for (int q = 0; q < 4; ++q)
-        for (int o = 441 * 32 + tid * 16; o < S_PLANE; o += 192 * 16)
+        for (int o = 441 * 32 + tid * 16; o < S_PLANE; o += THREADS * 16)
             *reinterpret_cast<uint4*>(sm + A_OFF + q * S_PLANE + o) = make_uint4(0, 0, 0, 0);
     fence_proxy_async_smem();
     if (tid == 32) {
-        // act_ready[0]: 128 epilogue threads + warp 0 (which zeroes the operand tails); [1]: 128
-        for (int i = 0; i < NB_W + 6; ++i) mbar_init(&w_full[i], i == NB_W + 4 ? 160 : i == NB_W + 5 ? 128 : 1);
+        // act_ready[0]: 256 epilogue threads + warp 0 (which zeroes the operand tails); [1]: 256
+        const int n_bar = NB_W + 1 + NB_ACC + 2;
+        for (int i = 0; i < n_bar; ++i) mbar_init(&w_full[i], i == n_bar - 2 ? 288 : i == n_bar - 1 ? 256 : 1);
         fence_mbar_init();
     }
     tc_fence_before();
@@ -128,7 +135,7 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
         // once conv1's MMAs are done the s planes are dead: zero the rows of the a1 planes and of
         // the a2 buffer that no output row writes (read only by dropped output rows)
         __syncwarp();
-        mbar_wait(&acc_full[0], 0);
+        mbar_wait(&acc_full[3], 0);  // the last conv1 block: every MMA reading the s planes is done
         for (int q = 0; q < 4; ++q)
             for (int o = 100 * 64 + lane * 16; o < A1_PLANE; o += 32 * 16)
                 *reinterpret_cast<uint4*>(sm + A_OFF + q * A1_PLANE + o) = make_uint4(0, 0, 0, 0);
@@ -145,16 +152,19 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
             {
                 const uint64_t ad0 = umma_desc_sw(base + A_OFF, 32), bd0 = umma_desc_sw(base + W1_OFF, 32);
 #pragma unroll
-                for (int c = 0; c < 16; ++c) {
-                    mbar_wait(&w_full[c], 0);
-                    tc_fence_after();
-                    const int q = c >> 2, dy = (c >> 1) & 1, dx = c & 1;
+                for (int mb = 0; mb < 4; ++mb) {
 #pragma unroll
-                    for (int mb = 0; mb < 4; ++mb)
+                    for (int c = 0; c < 16; ++c) {
+                        if (mb == 0) {
+                            mbar_wait(&w_full[c], 0);
+                            tc_fence_after();
+                        }
+                        const int q = c >> 2, dy = (c >> 1) & 1, dx = c & 1;
                         umma_bf16(tmem + mb * 32, ad0 + ((q * S_PLANE + (mb * 128 + dy * 21 + dx) * 32) >> 4),
                                   bd0 + ((c * W1_CH) >> 4), ID32, c > 0 ? 1u : 0u);
+                    }
+                    umma_commit(&acc_full[mb]);  // block mb's epilogue runs under the next block's MMAs
                 }
-                umma_commit(&acc_full[0]);
                 TTRACE(50);
             }
             mbar_wait(&act_ready[0], 0);  // a1 planes written by the epilogue warps
@@ -172,7 +182,7 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
                         umma_bf16(tmem + 128, ad0 + ((q * A1_PLANE + (dy * 10 + dx) * 64 + kk * 32) >> 4),
                                   bd0 + ((c * W2_CH + kk * 32) >> 4), ID64, (c > 0 || kk > 0) ? 1u : 0u);
                 }
-                umma_commit(&acc_full[1]);
+                umma_commit(&acc_full[4]);
                 TTRACE(52);
             }
             mbar_wait(&act_ready[1], 0);  // a2 rows written
@@ -190,56 +200,63 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
                         umma_bf16(tmem + 192, ad0 + (((ky * 9 + kx) * 128 + kk * 32) >> 4),
                                   bd0 + ((c * W3_CH + kk * 32) >> 4), ID64, (c > 0 || kk > 0) ? 1u : 0u);
                 }
-                umma_commit(&acc_full[2]);
+                umma_commit(&acc_full[5]);
                 TTRACE(54);
             }
         }
-    } else {  // epilogue warps 2..5
-        const int quad = warp & 3, etid = tid - 64;  // etid 0..127
+    } else {  // epilogue warps 2..9
+        const int quad = warp & 3, half = (warp - 2) >> 2, etid = tid - 64;  // etid 0..255
         const uint32_t lane_base = tmem + ((uint32_t)(quad * 32) << 16);
-        for (int i = etid; i < 160; i += 128)  // the layers' biases, once (not per output element)
+        for (int i = etid; i < 160; i += 256)  // the layers' biases, once (not per output element)
             s_bias[i] = i < 32 ? N.b1[i] : i < 96 ? N.b2[i - 32] : N.b3[i - 96];
-        asm volatile("bar.sync 1, 128;" ::: "memory");  // the epilogue warps only
-        const float* sb1 = s_bias;
-        const float* sb2 = s_bias + 32;
-        const float* sb3 = s_bias + 96;
-        // ---- conv1: a1 = bf16(ReLU(v / 255 + b1)) -> global and conv2's phase planes
-        mbar_wait(&acc_full[0], 0);
-        if (etid == 0) TTRACE(55);
-        tc_fence_after();
-#pragma unroll 1
+        asm volatile("bar.sync 1, 256;" ::: "memory");  // the epilogue warps only
+        const float* sb1 = s_bias + half * 16;
+        const float* sb2 = s_bias + 32 + half * 32;
+        const float* sb3 = s_bias + 96 + half * 32;
+        // ---- conv1: a1 = bf16(ReLU(v / 255 + b1)), columns [16 half, 16 half + 16) -> global now,
+        // -> conv2's phase planes once the last block's MMAs no longer read the s planes
+        uint4 a1r[4][2];
+#pragma unroll
         for (int mb = 0; mb < 4; ++mb) {
+            mbar_wait(&acc_full[mb], 0);
+            if (etid == 0 && mb == 0) TTRACE(55);
+            tc_fence_after();
             const int m = mb * 128 + quad * 32 + lane, Y = m / 21, X = m - 21 * Y;
             const bool ok = m < 441 && Y < 20 && X < 20;
-            __nv_bfloat16* g = N.a1 + ((int64_t)b * 400 + Y * 20 + X) * 32;
-            const int pq = (Y & 1) * 2 + (X & 1), prow = (Y >> 1) * 10 + (X >> 1);
+            float v[16];
+            tmem_ld16(lane_base + (uint32_t)(mb * 32 + half * 16), v);
+            uint32_t w[8];
 #pragma unroll
-            for (int h = 0; h < 2; ++h) {
-                float v[16];
-                tmem_ld16(lane_base + (uint32_t)(mb * 32 + h * 16), v);
-                if (!ok) continue;
-                uint32_t w[8];
+            for (int e = 0; e < 8; ++e) {
+                const float x0 = fmaxf(v[2 * e] * p.in_scale + sb1[2 * e], 0.f);
+                const float x1 = fmaxf(v[2 * e + 1] * p.in_scale + sb1[2 * e + 1], 0.f);
+                __nv_bfloat162 t = __floats2bfloat162_rn(x0, x1);
+                w[e] = *reinterpret_cast<uint32_t*>(&t);
+            }
+            a1r[mb][0] = make_uint4(w[0], w[1], w[2], w[3]);
+            a1r[mb][1] = make_uint4(w[4], w[5], w[6], w[7]);
+            if (ok) {
+                uint4* g = reinterpret_cast<uint4*>(N.a1 + ((int64_t)b * 400 + Y * 20 + X) * 32);
+                g[2 * half] = a1r[mb][0];
+                g[2 * half + 1] = a1r[mb][1];
+            }
+        }
 #pragma unroll
-                for (int e = 0; e < 8; ++e) {
-                    const float x0 = fmaxf(v[2 * e] * p.in_scale + sb1[h * 16 + 2 * e], 0.f);
-                    const float x1 = fmaxf(v[2 * e + 1] * p.in_scale + sb1[h * 16 + 2 * e + 1], 0.f);
-                    __nv_bfloat162 t = __floats2bfloat162_rn(x0, x1);
-                    w[e] = *reinterpret_cast<uint32_t*>(&t);
-                }
-                const uint4 u0 = make_uint4(w[0], w[1], w[2], w[3]), u1 = make_uint4(w[4], w[5], w[6], w[7]);
-                reinterpret_cast<uint4*>(g)[2 * h] = u0;
-                reinterpret_cast<uint4*>(g)[2 * h + 1] = u1;
-                uint8_t* plane = sm + A_OFF + pq * A1_PLANE;
-                st_swz16(plane, prow * 64 + (2 * h) * 16, 2, u0);
-                st_swz16(plane, prow * 64 + (2 * h + 1) * 16, 2, u1);
+        for (int mb = 0; mb < 4; ++mb) {
+            const int m = mb * 128 + quad * 32 + lane, Y = m / 21, X = m - 21 * Y;
+            if (m < 441 && Y < 20 && X < 20) {
+                uint8_t* plane = sm + A_OFF + ((Y & 1) * 2 + (X & 1)) * A1_PLANE;
+                const int prow = (Y >> 1) * 10 + (X >> 1);
+                st_swz16(plane, prow * 64 + (2 * half) * 16, 2, a1r[mb][0]);
+                st_swz16(plane, prow * 64 + (2 * half + 1) * 16, 2, a1r[mb][1]);
             }
         }
         fence_proxy_async_smem();  // generic-proxy smem stores -> visible to tcgen05.mma
         tc_fence_before();
         if (etid == 0) TTRACE(56);
         mbar_arrive(&act_ready[0]);
-        // ---- conv2: a2 -> global and conv3's flat rows
-        mbar_wait(&acc_full[1], 0);
+        // ---- conv2: a2 -> global and conv3's flat rows (columns [32 half, 32 half + 32))
+        mbar_wait(&acc_full[4], 0);
         if (etid == 0) TTRACE(57);
         tc_fence_after();
         {
@@ -247,16 +264,17 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
             const bool ok = r < 100 && Y < 9 && X < 9;
             __nv_bfloat16* g = N.a2 + ((int64_t)b * 81 + Y * 9 + X) * 64;
             const int frow = Y * 9 + X;
+            float v[32];
+            tmem_ld16x2(lane_base + (uint32_t)(128 + half * 32), v);
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                float v[16];
-                tmem_ld16(lane_base + (uint32_t)(128 + h * 16), v);
+            for (int hh = 0; hh < 2; ++hh) {
+                const int h = 2 * half + hh;
                 if (!ok) continue;
                 uint32_t w[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    const float x0 = fmaxf(v[2 * e] + sb2[h * 16 + 2 * e], 0.f);
-                    const float x1 = fmaxf(v[2 * e + 1] + sb2[h * 16 + 2 * e + 1], 0.f);
+                    const float x0 = fmaxf(v[hh * 16 + 2 * e] + sb2[hh * 16 + 2 * e], 0.f);
+                    const float x1 = fmaxf(v[hh * 16 + 2 * e + 1] + sb2[hh * 16 + 2 * e + 1], 0.f);
                     __nv_bfloat162 t = __floats2bfloat162_rn(x0, x1);
                     w[e] = *reinterpret_cast<uint32_t*>(&t);
                 }
@@ -272,23 +290,24 @@ __global__ void __launch_bounds__(192) k_conv_tower(const __grid_constant__ Towe
         if (etid == 0) TTRACE(58);
         mbar_arrive(&act_ready[1]);
         // ---- conv3: a3 -> global
-        mbar_wait(&acc_full[2], 0);
+        mbar_wait(&acc_full[5], 0);
         if (etid == 0) TTRACE(59);
         tc_fence_after();
         {
             const int r = quad * 32 + lane, y = r / 9, x = r - 9 * y;
             const bool ok = r < 81 && y < 7 && x < 7;
             __nv_bfloat16* g = N.a3 + ((int64_t)b * 49 + y * 7 + x) * 64;
+            float v[32];
+            tmem_ld16x2(lane_base + (uint32_t)(192 + half * 32), v);
 #pragma unroll
-            for (int h = 0; h < 4; ++h) {
-                float v[16];
-                tmem_ld16(lane_base + (uint32_t)(192 + h * 16), v);
+            for (int hh = 0; hh < 2; ++hh) {
+                const int h = 2 * half + hh;
                 if (!ok) continue;
                 uint32_t w[8];
 #pragma unroll
                 for (int e = 0; e < 8; ++e) {
-                    const float x0 = fmaxf(v[2 * e] + sb3[h * 16 + 2 * e], 0.f);
-                    const float x1 = fmaxf(v[2 * e + 1] + sb3[h * 16 + 2 * e + 1], 0.f);
+                    const float x0 = fmaxf(v[hh * 16 + 2 * e] + sb3[hh * 16 + 2 * e], 0.f);
+                    const float x1 = fmaxf(v[hh * 16 + 2 * e + 1] + sb3[hh * 16 + 2 * e + 1], 0.f);
                     __nv_bfloat162 t = __floats2bfloat162_rn(x0, x1);
                     w[e] = *reinterpret_cast<uint32_t*>(&t);
                 }
