@@ -1512,9 +1512,9 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
             const int nch = l == 0 ? 5 * B : B, ta = l == 0 ? 2 : l == 1 ? 4 : 5;
             // partials per weight (the critical-path reduce reads them all); conv1's weight gradient
             // is itself on the critical path (the last GEMM of the dgrad chain): it keeps more splits
-            static const int cap23 = [] {
-                const char* e = getenv("GORILA_WSPLIT_MAX");
-                return e ? std::max(1, atoi(e)) : 16;
+            static const int cap23 = [] {  // B = 32 sweep (tools/knob_sweep2.sh): 4: 76.9, 6: 76.9,
+                const char* e = getenv("GORILA_WSPLIT_MAX");  // 8: 75.7, 11: 78.5, 16: 78.5 us/step
+                return e ? std::max(1, atoi(e)) : 8;
             }();
             static const int cap1 = [] {
                 const char* e = getenv("GORILA_WSPLIT1_MAX");

@@ -74,6 +74,31 @@ def test_replay_single_host_inserts_staged_ring():
         assert (out["a"] == aa).all() and (out["r"] == rr).all() and (out["d"] == dd).all()
 
 
+@pytest.mark.parametrize("sizes", [(1, 9, 1, 30, 2, 600, 1), (12, 150, 3, 560, 7)])
+def test_replay_host_inserts_mixed_sizes(sizes):
+    """Host inserts of mixed sizes through every path: one-step zero-copy reads of the staging slot
+    (<= 64 KB), staged uploads (<= 4 MB), a synchronous large insert (> 4 MB) and inserts longer
+    than the ring; the ring must equal the oracle's (bit-exact sampled windows after each)."""
+    from paper_1507_04296_b200 import Gorila
+    nA, C = 5, 400
+    g = Gorila(n_actions=nA, batch=24, replay_capacity=C, theta0=synth.theta0(nA), math="bf16")
+    ring = O.Ring(C)
+    t = 0
+    for k, n in enumerate(sizes):
+        f = synth.frames(synth.SEED_DATA, 0, t, n)
+        a, r, d = synth.meta(synth.SEED_DATA, 0, t, n, nA)
+        g.replay_insert(0, f, a, r, d)
+        ring.insert(f, a, r, d)
+        t += n
+        if ring.size < 2:
+            continue
+        out = g.replay_sample(0, k)
+        tau = O.sample_indices(ring.n, ring.size, 24, 1507, 0, k)
+        s, s2, aa, rr, dd = ring.gather(tau)
+        assert (out["tau"] == tau).all() and (out["s"] == s).all() and (out["s2"] == s2).all()
+        assert (out["a"] == aa).all() and (out["r"] == rr).all() and (out["d"] == dd).all()
+
+
 def test_replay_not_ready():
     from paper_1507_04296_b200 import GorilaError
     g, orc = make_pair(nA=4, B=8, C=100, n_insert=1, math="fp32")
