@@ -1313,7 +1313,11 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
            (const T*)g4, B, ctx->part_b, ctx->bias_chunks);
     // forked round: the side stream reduces what it produced (conv2 / conv3 weights, the biases)
     // while the main stream finishes conv1's weight gradient
-    if (split_red && fk && (phases & (1u << PH_WGRED))) launch(ctx, k_wgrad_reduce, dim3(148 * 2), dim3(256), 0, pick({1, 2, 3, 4, 5, 6}), Gd);
+    static const int side_red_ctas = [] {
+        const char* e = getenv("GORILA_SIDE_RED_CTAS");
+        return e ? std::max(1, atoi(e)) : 148 * 2;
+    }();
+    if (split_red && fk && (phases & (1u << PH_WGRED))) launch(ctx, k_wgrad_reduce, dim3(side_red_ctas), dim3(256), 0, pick({1, 2, 3, 4, 5, 6}), Gd);
     }
     mark(ctx, PH_BIASG);
     if (fk) join_side(ctx);
@@ -1496,7 +1500,11 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     uint64_t* n_snap = c.take<uint64_t>((int64_t)W * L);
     float* dQ = c.take<float>(Bs * nA);
     float* td_partial = c.take<float>(Bs * 2);
-    const int bias_chunks = std::max(64, std::min(2048, 2 * B));
+    static const int bias_min = [] {
+        const char* e = getenv("GORILA_BIAS_CHUNKS");
+        return e ? std::max(1, atoi(e)) : 64;
+    }();
+    const int bias_chunks = std::max(bias_min, std::min(2048, 2 * B));
     // split choices (reduction chunks of 64 for tc, 16 for simt)
     const int chunk = fp32 ? SM_BR : TC_BK;
     int split_w[3];
