@@ -334,8 +334,6 @@ GORILA_DEV void fc5_bwd_fused(const Fc5TdParams& p, unsigned int gen) {
 // 16 warps: warps 0..7 the online net, 8..15 the target net; every operand of a warp's (up to
 // four) actions is requested before the first FMA (one memory round trip for the whole layer)
 __global__ void __launch_bounds__(512) k_fc5_td(Fc5TdParams p) {
-    pdl_wait();
-    pdl_trigger();
     const TdParams& t = p.td;
     const int nA = t.nA;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -351,6 +349,13 @@ __global__ void __launch_bounds__(512) k_fc5_td(Fc5TdParams p) {
 #pragma unroll
         for (int k = 0; k < FC4_OUT / 32; ++k) wv[u][k] = a < nA ? w5[a * FC4_OUT + lane + 32 * k] : 0.f;
     }
+    // W5 / b5 (the replica and theta^-) were written two or more kernels back: loaded before the
+    // wait for fc4's output (PDL: the preceding kernel has passed its own wait when this one starts)
+    float bv[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) bv[u] = wz + 8 * u < nA ? b5[wz + 8 * u] : 0.f;
+    pdl_wait();
+    pdl_trigger();
     int it = 0;
     for (int b = blockIdx.x; b < t.B; b += gridDim.x, ++it) {
         const int par = it & 1;
@@ -366,7 +371,7 @@ __global__ void __launch_bounds__(512) k_fc5_td(Fc5TdParams p) {
 #pragma unroll
             for (int k = 0; k < FC4_OUT / 32; ++k) acc = fmaf(xv[k], wv[u][k], acc);
             acc = warp_sum(acc);
-            if (lane == 0) q[par][z][a] = acc + b5[a];
+            if (lane == 0) q[par][z][a] = acc + bv[u];
         }
         __syncthreads();
         if (warp == 0) {

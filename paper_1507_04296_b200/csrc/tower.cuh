@@ -107,30 +107,35 @@ __global__ void __launch_bounds__(tower::THREADS) k_conv_tower(const __grid_cons
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    pdl_wait();
-    pdl_trigger();
     const uint32_t tmem = *tmem_slot;
     const uint32_t base = smem_u32(sm);
     float* s_bias = reinterpret_cast<float*>(sm + BIAS_OFF);
-
+    // The weights (this round's replica / theta^-) were written by the previous round's apply and
+    // target sync, two or more kernels back: with PDL those are complete when this grid starts
+    // (the kernel just before has passed its own griddepcontrol.wait), so they stream in while the
+    // sampler finishes. Only the sample's planes wait for the sampler.
+    if (warp == 0 && lane == 0) {
+        for (int c = 0; c < 16; ++c) {
+            tma_load(&N.w1_map, base + W1_OFF + c * W1_CH, &w_full[c], ShWeightK<32, 32, 16, 2>::koff(c), 0);
+            mbar_expect_tx(&w_full[c], 32 * 32);
+        }
+        for (int c = 0; c < 16; ++c) {
+            tma_load(&N.w2_map, base + W2_OFF + c * W2_CH, &w_full[16 + c], ShWeightK<64, 64, 16, 1>::koff(c), 0);
+            mbar_expect_tx(&w_full[16 + c], 64 * 64);
+        }
+        for (int c = 0; c < 9; ++c) {
+            tma_load(&N.w3_map, base + W3_OFF + c * W3_CH, &w_full[32 + c], c * 64, 0);
+            mbar_expect_tx(&w_full[32 + c], 64 * 128);
+        }
+    }
+    pdl_wait();
+    pdl_trigger();
     if (tid == 0) TTRACE(48);
     if (warp == 0) {
-        if (lane == 0) {  // loads: the sample's planes first, then the weights in use order
+        if (lane == 0) {  // the sample's conv1 input planes
 #pragma unroll
             for (int q = 0; q < 4; ++q) tma_load(&N.s_map, base + A_OFF + q * S_PLANE, s_full, 0, 0, q, b);
             mbar_expect_tx(s_full, 4 * 441 * 32);
-            for (int c = 0; c < 16; ++c) {
-                tma_load(&N.w1_map, base + W1_OFF + c * W1_CH, &w_full[c], ShWeightK<32, 32, 16, 2>::koff(c), 0);
-                mbar_expect_tx(&w_full[c], 32 * 32);
-            }
-            for (int c = 0; c < 16; ++c) {
-                tma_load(&N.w2_map, base + W2_OFF + c * W2_CH, &w_full[16 + c], ShWeightK<64, 64, 16, 1>::koff(c), 0);
-                mbar_expect_tx(&w_full[16 + c], 64 * 64);
-            }
-            for (int c = 0; c < 9; ++c) {
-                tma_load(&N.w3_map, base + W3_OFF + c * W3_CH, &w_full[32 + c], c * 64, 0);
-                mbar_expect_tx(&w_full[32 + c], 64 * 128);
-            }
         }
         // once conv1's MMAs are done the s planes are dead: zero the rows of the a1 planes and of
         // the a2 buffer that no output row writes (read only by dropped output rows)
