@@ -343,7 +343,7 @@ def main():
         f1.numpy()[0] = hf[i]
         a1.numpy()[0], r1.numpy()[0], d1.numpy()[0] = ha[i], hr[i], hd[i]
         g.replay_insert(0, f1, a1, r1, d1)           # this step's new experience, pinned host -> device
-        h = g.round_async(ids, k, stal)               # the round; its result (loss, decisions) -> pinned host
+        h = g.round_async(ids, k, stal)               # the round; its result (loss, decisions) -> pinned ring
         if pending is not None:
             g.round_result(pending)                   # the previous round's result, read while this one runs
         return h
@@ -442,9 +442,9 @@ def main():
                     "d2h_bytes_per_step": 48 + 24 + 1,
                     "note": "per step: replay_insert of 1 new transition from pinned host memory (library "
                             "staging ring, read by the scatter kernel over the bus; no stream sync), "
-                            "gorila_round_async (learner_step + ps_apply_shard + sync_target as one graph) whose "
-                            "learner info, round info and sync flag a small kernel stores into pinned host "
-                            "memory, read by the host one step later (while the next round runs); "
+                            "gorila_round_post (learner_step + ps_apply_shard + sync_target as one graph whose last "
+                            "node stores the learner info, round info and sync flag into the library's pinned result "
+                            "ring), read with gorila_round_fetch one step later (while the next round runs); "
                             f"{args.warmup} untimed warm-up steps of the same loop, {args.e2e_steps} timed"},
             "roofline": {"kernel": dom, "bound": dom_roof["bound"], "achieved": dom_roof["achieved"],
                          "peak": dom_roof["peak"], "unit": dom_roof["unit"], "frac": dom_roof["frac"],

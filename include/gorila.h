@@ -232,6 +232,18 @@ GORILA_API gorila_status gorila_round(gorila_ctx* ctx, const int32_t* learners, 
 GORILA_API gorila_status gorila_round_async(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
                                            const int32_t* staleness, gorila_learner_info* info_out,
                                            gorila_round_info* round_info_out, uint8_t* synced_out);
+/* Posted round: gorila_round's semantics, and the round's results (learner infos, round info,
+ * sync flags) are stored by the round's own last kernel into slot round % 16 of a library-owned
+ * pinned result ring (no copy operation outside the round's CUDA graph). gorila_round_fetch
+ * waits for that slot by polling host memory (no CUDA call; a failed stream is reported as its
+ * CUDA error) and copies it out: info_out n entries, round_info_out, synced_out n bytes (each may
+ * be NULL; n = the posted round's learner count). Fetch a round before 16 further rounds are
+ * posted (E_INVALID: overwritten). At most 32 learners per posted round (E_SHAPE). COLLECTIVE
+ * as gorila_round. */
+GORILA_API gorila_status gorila_round_post(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
+                                           const int32_t* staleness);
+GORILA_API gorila_status gorila_round_fetch(gorila_ctx* ctx, uint64_t round, gorila_learner_info* info_out,
+                                            gorila_round_info* round_info_out, uint8_t* synced_out);
 
 /* State access for checkpointing and teacher-forced parity (canonical layout,
  * host buffers, any may be NULL; synchronises the stream). m / v are the full

@@ -15,6 +15,7 @@
 #include <cstring>
 #include <string>
 #include <type_traits>
+#include <atomic>
 #include <vector>
 
 #include <cudaTypedefs.h>
@@ -174,6 +175,12 @@ struct gorila_ctx {
     cudaEvent_t stage_ev[kStage] = {};
     int stage_next = 0;
     uint8_t* stage_dev = nullptr;  // device landing buffer of a staged insert (4 MB)
+    // result ring of gorila_round_post / gorila_round_fetch (mapped pinned host memory)
+    static constexpr int kRing = 16;
+    uint8_t* ring_host = nullptr;
+    uint8_t* ring_dev = nullptr;
+    int ring_slot = 0;
+    bool ring_pending = false;  // a posted round whose results are not stored yet (k_apply or k_emit_ring)
     uint8_t* stage_dptr[kStage] = {};  // device view of the mapped pinned slots (small inserts read them directly)
     unsigned int* apply_counter = nullptr;  // last-block detection of k_apply's fused sync copy
     bool sync_fused_now = false;            // this round's k_apply did the target-sync copy
@@ -1808,6 +1815,10 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
         CU(cudaMemcpyAsync(ctx->shard_tab, tab.data(), sizeof(ShardPtrs) * tab.size(), cudaMemcpyHostToDevice, st));
     }
     CU(stage_alloc(ctx));
+    ctx->ring_slot = (RING_HDR + std::min(ctx->L, RING_MAXL) * (int)sizeof(DevLearnerInfo) + 63) / 64 * 64;
+    CU(cudaHostAlloc((void**)&ctx->ring_host, (size_t)gorila_ctx::kRing * ctx->ring_slot, cudaHostAllocMapped));
+    memset(ctx->ring_host, 0, (size_t)gorila_ctx::kRing * ctx->ring_slot);
+    CU(cudaHostGetDevicePointer((void**)&ctx->ring_dev, ctx->ring_host, 0));
     CU(cudaStreamSynchronize(st));
     *out = ctx;
     return GORILA_OK;
@@ -1843,6 +1854,7 @@ void gorila_destroy(gorila_ctx* ctx) {
         if (ctx->stage[i]) cudaFreeHost(ctx->stage[i]);
     }
     if (ctx->stage_dev) cudaFree(ctx->stage_dev);
+    if (ctx->ring_host) cudaFreeHost(ctx->ring_host);
     if (ctx->comm) {
         if (ctx->poisoned) ncclCommAbort(ctx->comm);
         else ncclCommDestroy(ctx->comm);
@@ -2258,6 +2270,13 @@ gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info*
             return e && atoi(e) != 0;
         }();
         ctx->sync_fused_now = sync_fuse && ctx->fused_sync && !ctx->per_msg;
+        if (ctx->ring_pending && !ctx->sync_fused_now && !ctx->per_msg && ctx->fused_sync && p.n_sync <= 8) {
+            p.ring = ctx->ring_dev;  // k_apply block 0 stores the results (no k_emit_ring)
+            p.ring_R = gorila_ctx::kRing;
+            p.ring_slot_bytes = ctx->ring_slot;
+            for (int i = 0; i < p.n_sync; ++i) p.ring_info[i] = ctx->learners[ctx->sync_ids[i]].info;
+            ctx->ring_pending = false;
+        }
         if (ctx->sync_fused_now) {
             p.sync_copy = 1;
             p.counter = ctx->apply_counter;
@@ -2277,10 +2296,11 @@ gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info*
         }
         if (ctx->cfg.math == GORILA_MATH_FP32) launch(ctx, k_apply_msg<float>, dim3(148 * 4), dim3(256), 0, p, mp);
         else launch(ctx, k_apply_msg<__nv_bfloat16>, dim3(148 * 4), dim3(256), 0, p, mp);
-    } else if (ctx->cfg.math == GORILA_MATH_FP32) {
-        launch(ctx, k_apply<float>, dim3(148 * 4), dim3(256), 0, p);
     } else {
-        launch(ctx, k_apply<__nv_bfloat16>, dim3(148 * 4), dim3(256), 0, p);
+        p.book_last = p.sync_copy ? 0 : 1;  // one extra block takes the decisions / stores the ring slot
+        const dim3 grid(148 * 4 + p.book_last);
+        if (ctx->cfg.math == GORILA_MATH_FP32) launch(ctx, k_apply<float>, grid, dim3(256), 0, p);
+        else launch(ctx, k_apply<__nv_bfloat16>, grid, dim3(256), 0, p);
     }
     ctx->dev_round_expect = round + 1;
     mark(ctx, PH_APPLY);
@@ -2346,9 +2366,26 @@ static bool device_accessible(const void* p) {
     return at.type == cudaMemoryTypeHost && at.devicePointer == p;
 }
 
+// the last node of a posted round (k_emit_ring): results into the ring slot of this round
+static void emit_ring(gorila_ctx* ctx, const int32_t* learners, int32_t n) {
+    EmitRing p{};
+    p.ring = ctx->ring_dev;
+    p.R = gorila_ctx::kRing;
+    p.slot_bytes = ctx->ring_slot;
+    p.n = n;
+    for (int i = 0; i < n; ++i) {
+        p.info[i] = ctx->learners[learners[i]].info;
+        p.sync[i] = ctx->learners[learners[i]].sync_flag;
+    }
+    p.round_info = ctx->round_info;
+    p.dev_round = ctx->dev_round;
+    launch(ctx, k_emit_ring, dim3(1), dim3(128), 0, p);
+}
+
 static gorila_status round_impl(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
                                 const int32_t* staleness, gorila_learner_info* info_out,
-                                gorila_round_info* round_info_out, uint8_t* synced_out, bool sync) {
+                                gorila_round_info* round_info_out, uint8_t* synced_out, bool sync,
+                                bool ring = false) {
     if (!ctx) return fail(GORILA_E_INVALID, "null context");
     if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned");
     if (!learners || n < 1 || n > ctx->L) return fail(GORILA_E_SHAPE, "bad learner list");
@@ -2367,6 +2404,7 @@ static gorila_status round_impl(gorila_ctx* ctx, const int32_t* learners, int32_
     }
     key.push_back((int64_t)(round % (uint64_t)ctx->H));
     key.push_back(ctx->prof ? 1 : 0);  // profiling graphs carry event-record nodes
+    key.push_back(ring ? 1 : 0);       // posted rounds end with the result-ring node
     gorila_status s;
     auto eager = [&]() -> gorila_status {
         ctx->in_round = true;
@@ -2376,8 +2414,11 @@ static gorila_status round_impl(gorila_ctx* ctx, const int32_t* learners, int32_
         ctx->fused_sync = n <= 8;  // k_apply takes the target-sync decisions (same predicate, R13)
         ctx->sync_n = n;
         for (int i = 0; i < n && i < 8; ++i) ctx->sync_ids[i] = learners[i];
+        ctx->ring_pending = ring;
         r = ps_apply_shard(ctx, round, nullptr);
         if (r == GORILA_OK) r = sync_target(ctx, learners, n, 0, nullptr);
+        if (r == GORILA_OK && ctx->ring_pending) emit_ring(ctx, learners, n);  // not stored by k_apply
+        ctx->ring_pending = false;
         ctx->fused_sync = false;
         ctx->sync_fused_now = false;
         return r;
@@ -2490,6 +2531,37 @@ gorila_status gorila_round_async(gorila_ctx* ctx, const int32_t* learners, int32
                                  const int32_t* staleness, gorila_learner_info* info_out,
                                  gorila_round_info* round_info_out, uint8_t* synced_out) {
     return round_impl(ctx, learners, n, round, staleness, info_out, round_info_out, synced_out, false);
+}
+
+gorila_status gorila_round_post(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
+                                const int32_t* staleness) {
+    if (ctx && n > RING_MAXL) return fail(GORILA_E_SHAPE, "gorila_round_post: at most 32 learners per round");
+    return round_impl(ctx, learners, n, round, staleness, nullptr, nullptr, nullptr, false, true);
+}
+
+gorila_status gorila_round_fetch(gorila_ctx* ctx, uint64_t round, gorila_learner_info* info_out,
+                                 gorila_round_info* round_info_out, uint8_t* synced_out) {
+    if (!ctx) return fail(GORILA_E_INVALID, "null context");
+    const uint8_t* slot = ctx->ring_host + (size_t)(round % gorila_ctx::kRing) * ctx->ring_slot;
+    const volatile uint64_t* seq = reinterpret_cast<const volatile uint64_t*>(slot);
+    for (uint64_t spin = 0;; ++spin) {  // the posting stream writes the slot; poll it (no CUDA call)
+        const uint64_t v = *seq;
+        if (v == round + 1) break;
+        if (v > round + 1) return fail(GORILA_E_INVALID, "gorila_round_fetch: result overwritten (fetch within 16 rounds)");
+        __builtin_ia32_pause();  // keep the polled line cool for the device's write
+        if ((spin & 0xfffff) == 0xfffff) {  // a failed stream would never write it: surface its error
+            const cudaError_t e = cudaStreamQuery(ctx->stream);
+            if (e != cudaSuccess && e != cudaErrorNotReady) CU(e);
+            if (e == cudaSuccess && *seq != round + 1)
+                return fail(GORILA_E_INVALID, "gorila_round_fetch: round was not posted");
+        }
+    }
+    std::atomic_thread_fence(std::memory_order_acquire);
+    const uint32_t n = *reinterpret_cast<const uint32_t*>(slot + 8);
+    if (round_info_out) memcpy(round_info_out, slot + 16, sizeof(gorila_round_info));
+    if (synced_out) memcpy(synced_out, slot + 40, n);
+    if (info_out) memcpy(info_out, slot + RING_HDR, sizeof(gorila_learner_info) * n);
+    return GORILA_OK;
 }
 
 gorila_status gorila_get_state(gorila_ctx* ctx, float* theta, float* m, float* v, uint64_t* version) {

@@ -6,6 +6,7 @@
 namespace gorila {
 
 constexpr uint32_t TAG_SAMPLE = 3u;
+constexpr int RING_MAXL = 32, RING_HDR = 8 + 8 + 24 + 64;  // result ring slot: see k_emit_ring
 
 // one learner's replay ring as seen from this rank (local or a peer's, mapped over NVLink)
 struct ShardPtrs {
@@ -535,6 +536,43 @@ __global__ void k_insert_scatter(const uint8_t* __restrict__ src, int64_t keep, 
     if (blockIdx.x == 0 && threadIdx.x == 0) *n_dev = n_new;
 }
 
+// ------------------------------------------------------------------------- result ring (gorila_round_post)
+// The last node of a posted round: learner infos, round info and sync flags of the round into slot
+// round % R of a mapped pinned ring, then (after a system fence) the slot's sequence number, which
+// the host polls (gorila_round_fetch: no CUDA call, no extra stream operation outside the graph).
+// Slot layout: u64 seq | u32 n | u32 pad | 24 B round info | 64 B sync flags | n x learner info.
+struct EmitRing {
+    uint8_t* ring;  // device view of the mapped ring
+    int R, slot_bytes, n;
+    const DevLearnerInfo* info[RING_MAXL];
+    const uint8_t* sync[RING_MAXL];
+    const uint64_t* round_info;  // [n_acc, V_before, V_after]
+    const uint64_t* dev_round;   // advanced by this round's apply: the round is *dev_round - 1
+};
+__global__ void k_emit_ring(EmitRing p) {
+    pdl_wait();
+    pdl_trigger();
+    const uint64_t round = *p.dev_round - 1;
+    uint8_t* slot = p.ring + (size_t)(round % (uint64_t)p.R) * p.slot_bytes;
+    const int t = threadIdx.x;
+    constexpr int IW = sizeof(DevLearnerInfo) / 4;
+    for (int e = t; e < p.n * IW; e += blockDim.x)
+        reinterpret_cast<uint32_t*>(slot + RING_HDR)[e] = reinterpret_cast<const uint32_t*>(p.info[e / IW])[e % IW];
+    if (t < p.n) slot[40 + t] = *p.sync[t];
+    if (t == 0) {
+        *reinterpret_cast<uint32_t*>(slot + 8) = (uint32_t)p.n;
+        *reinterpret_cast<uint32_t*>(slot + 16) = (uint32_t)p.round_info[0];  // n_accepted (+ zero pad)
+        *reinterpret_cast<uint32_t*>(slot + 20) = 0u;
+        *reinterpret_cast<uint64_t*>(slot + 24) = p.round_info[1];
+        *reinterpret_cast<uint64_t*>(slot + 32) = p.round_info[2];
+    }
+    __syncthreads();
+    if (t == 0) {  // one system-scope release: cumulative over the block's payload stores (bar.sync)
+        __threadfence_system();
+        *reinterpret_cast<volatile uint64_t*>(slot) = round + 1;
+    }
+}
+
 // ------------------------------------------------------------------------- small result copies
 // gorila_round_async's learner infos / sync flags / round info into pinned host buffers: warp w
 // copies segment w, w + nwarps, ... byte by byte (a few hundred bytes in all)
@@ -737,6 +775,13 @@ struct ApplyParams {
     float* sync_tm_f[8];
     int sync_copy;
     unsigned int* counter;
+    // posted round (gorila_round_post, 1 GPU, fused sync decisions): block 0 stores the round's
+    // results into the result-ring slot as soon as it has taken the decisions (no extra kernel)
+    uint8_t* ring;
+    int ring_R, ring_slot_bytes;
+    const DevLearnerInfo* ring_info[8];
+    int book_last;  // 1: the grid's last block only takes the round's decisions / stores the ring slot
+                    // (its system fence overlaps the other blocks' update), the others only update
 };
 // Centered RMSProp (reading R2) / AdaGrad on the mean of the accepted gradients
 // (reading R12, R25); V += |Acc|. float4-vectorised, grid-stride.
@@ -789,7 +834,8 @@ __global__ void __launch_bounds__(256) k_apply(ApplyParams p) {
         for (int i = 0; i < p.n_sync; ++i)
             if (v1 >= p.sync_stats[i]->last_sync + (uint64_t)p.period) doit_mask |= 1u << i;
     }
-    if (!p.sync_copy && blockIdx.x == 0 && threadIdx.x == 0) {
+    const int book_block = p.book_last ? gridDim.x - 1 : 0;
+    if (!p.sync_copy && blockIdx.x == book_block && threadIdx.x == 0) {
         const uint64_t v0 = *p.V;
         const uint64_t n_acc = (uint64_t)(cnt + 0.5f);
         p.round_info[0] = n_acc;
@@ -797,18 +843,35 @@ __global__ void __launch_bounds__(256) k_apply(ApplyParams p) {
         p.round_info[2] = v0 + n_acc;
         *p.V = v0 + n_acc;
         if (p.vhist_dst) *p.vhist_dst = v0 + n_acc;
-        if (p.dev_round) *p.dev_round += 1;
+        const uint64_t rnd = p.dev_round ? *p.dev_round : 0;
+        if (p.dev_round) *p.dev_round = rnd + 1;
+        uint8_t* slot = p.ring ? p.ring + (size_t)(rnd % (uint64_t)p.ring_R) * p.ring_slot_bytes : nullptr;
         for (int i = 0; i < p.n_sync; ++i) {
             LearnerStats* st = p.sync_stats[i];
             const bool doit = v0 + n_acc >= st->last_sync + (uint64_t)p.period;
             if (doit) st->last_sync = v0 + n_acc;
             *p.sync_flag[i] = doit;
+            if (slot) slot[40 + i] = doit;
+        }
+        if (slot) {  // the result ring slot of this round (layout: k_emit_ring)
+            *reinterpret_cast<uint32_t*>(slot + 8) = (uint32_t)p.n_sync;
+            *reinterpret_cast<uint64_t*>(slot + 16) = n_acc;  // n_accepted + zero pad
+            *reinterpret_cast<uint64_t*>(slot + 24) = v0;
+            *reinterpret_cast<uint64_t*>(slot + 32) = v0 + n_acc;
+            for (int i = 0; i < p.n_sync; ++i)
+                for (int w = 0; w < (int)(sizeof(DevLearnerInfo) / 8); ++w)
+                    reinterpret_cast<uint64_t*>(slot + RING_HDR)[i * (sizeof(DevLearnerInfo) / 8) + w] =
+                        reinterpret_cast<const uint64_t*>(p.ring_info[i])[w];
+            __threadfence_system();
+            *reinterpret_cast<volatile uint64_t*>(slot) = rnd + 1;
         }
     }
     const bool update = cnt > 0.5f;
     const float inv = update ? 1.0f / cnt : 0.f;
     const int64_t n4 = (p.n_real + 3) / 4;  // slices are padded to 64 elements (zeros, never read back)
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n4; e += (int64_t)gridDim.x * blockDim.x) {
+    const int upd_blocks = gridDim.x - (p.book_last ? 1 : 0);
+    if ((int)blockIdx.x >= upd_blocks) return;  // the bookkeeping block (book_last)
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n4; e += (int64_t)upd_blocks * blockDim.x) {
         float4 th = reinterpret_cast<float4*>(p.theta)[e];
         if (!update) {  // nothing accepted: theta, m, v unchanged; still emit the next replica
             if (p.rep_t) {

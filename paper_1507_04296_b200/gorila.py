@@ -63,7 +63,7 @@ EXPORTS = ["gorila_param_count", "gorila_workspace_bytes", "gorila_init", "goril
            "gorila_set_state", "gorila_get_learner_state", "gorila_set_learner_state", "gorila_get_grad",
            "gorila_get_q", "gorila_get_activation", "gorila_act", "gorila_kernel_launches", "gorila_profile_enable", "gorila_profile_read",
            "gorila_profile_phase_count", "gorila_profile_phase_name", "gorila_nccl_unique_id", "gorila_round",
-           "gorila_round_async",
+           "gorila_round_async", "gorila_round_post", "gorila_round_fetch",
            "gorila_bench_phase", "gorila_debug_trace"]
 
 
@@ -99,6 +99,8 @@ def load(build_if_missing=True):
     L.gorila_get_grad.argtypes = [P, P]
     L.gorila_get_q.argtypes = [P, i32, P, P]
     L.gorila_get_activation.argtypes = [P, i32, P, u64]
+    L.gorila_round_post.argtypes = [P, P, i32, u64, P]
+    L.gorila_round_fetch.argtypes = [P, u64, P, P, P]
     L.gorila_act.argtypes = [P, P, i32, u64, u64, ctypes.c_double, i64, i32, P, P]
     L.gorila_kernel_launches.argtypes = [P]
     L.gorila_kernel_launches.restype = u64
@@ -147,13 +149,6 @@ def _ptr(x):
     # torch tensor
     assert x.is_contiguous()
     return x.data_ptr(), bool(x.is_cuda)
-
-
-def _spin(ev):
-    """Wait for an event by polling it. A blocking wait parks the thread, and the first CUDA call
-    after it then costs ~90 us on the B200 hosts (tools/e2e_probe.py) -- more than the round."""
-    while not ev.query():
-        pass
 
 
 class Gorila:
@@ -276,36 +271,24 @@ class Gorila:
                  "version_after": ri.version_after}, synced.astype(bool))
 
     def round_async(self, learners_arr, rnd, staleness_arr=None):
-        """gorila_round_async: the round's result lands in a pinned slot; returns a handle for
-        round_result (read it while later rounds run)."""
-        torch = self.torch
-        if not hasattr(self, "_slots"):
-            n = self.L
-            self._slots = [{"info": torch.empty(n * ctypes.sizeof(LearnerInfo), dtype=torch.uint8).pin_memory(),
-                            "ri": torch.empty(ctypes.sizeof(RoundInfo), dtype=torch.uint8).pin_memory(),
-                            "sy": torch.empty(n, dtype=torch.uint8).pin_memory(),
-                            "ev": torch.cuda.Event()} for _ in range(4)]
-            self._slot_next = 0
-        k = self._slot_next
-        self._slot_next = (k + 1) % len(self._slots)
-        sl = self._slots[k]
-        _spin(sl["ev"])  # the slot's previous result has been read back
-        _check(load().gorila_round_async(self.h, learners_arr.ctypes.data, len(learners_arr), rnd,
-                                         None if staleness_arr is None else staleness_arr.ctypes.data,
-                                         sl["info"].data_ptr(), sl["ri"].data_ptr(), sl["sy"].data_ptr()))
-        sl["ev"].record(self.stream)
-        return (k, len(learners_arr))
+        """gorila_round_post: the round's result is stored by its own last kernel into the library's
+        pinned result ring; returns a handle for round_result (read it while later rounds run)."""
+        _check(load().gorila_round_post(self.h, learners_arr.ctypes.data, len(learners_arr), rnd,
+                                        None if staleness_arr is None else staleness_arr.ctypes.data))
+        return (rnd, len(learners_arr))
 
     def round_result(self, handle):
-        """Wait for a round_async handle; returns (learner infos, round info, synced) like round()."""
-        k, n = handle
-        sl = self._slots[k]
-        _spin(sl["ev"])
-        infos = (LearnerInfo * n).from_buffer_copy(sl["info"].numpy().tobytes()[:n * ctypes.sizeof(LearnerInfo)])
-        ri = RoundInfo.from_buffer_copy(sl["ri"].numpy().tobytes())
+        """gorila_round_fetch for a round_async handle (polls host memory, no CUDA call); returns
+        (learner infos, round info, synced) like round()."""
+        rnd, n = handle
+        infos = (LearnerInfo * n)()
+        ri = RoundInfo()
+        synced = np.zeros(n, np.uint8)
+        _check(load().gorila_round_fetch(self.h, rnd, ctypes.cast(infos, ctypes.c_void_p), ctypes.byref(ri),
+                                         synced.ctypes.data))
         return ([infos[i].as_dict() for i in range(n)],
                 {"n_accepted": ri.n_accepted, "version_before": ri.version_before, "version_after": ri.version_after},
-                sl["sy"].numpy()[:n].astype(bool))
+                synced.astype(bool))
 
     def ps_apply_shard(self, rnd, want_info=True):
         ri = RoundInfo() if want_info else None

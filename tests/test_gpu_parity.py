@@ -376,21 +376,46 @@ def test_round_graph_matches_eager_bitwise(math):
     assert (ga.get_learner_state(0)[0] == gb.get_learner_state(0)[0]).all()
 
 
+def test_round_async_c_entry_pinned_buffers():
+    """The C entry gorila_round_async with caller-owned pinned buffers (one result-copy kernel)
+    == gorila_round's synchronous results."""
+    import ctypes
+    import torch
+    from paper_1507_04296_b200 import load
+    from paper_1507_04296_b200.gorila import LearnerInfo, RoundInfo
+    ga, _ = make_pair(nA=4, B=16, C=800, n_insert=800, math="bf16", L=2, target_period=3)
+    gb, _ = make_pair(nA=4, B=16, C=800, n_insert=800, math="bf16", L=2, target_period=3)
+    ids = np.array([0, 1], np.int32)
+    info = torch.zeros(2 * ctypes.sizeof(LearnerInfo), dtype=torch.uint8).pin_memory()
+    ri = torch.zeros(ctypes.sizeof(RoundInfo), dtype=torch.uint8).pin_memory()
+    sy = torch.zeros(2, dtype=torch.uint8).pin_memory()
+    for k in range(5):
+        ra = ga.round(ids, k, want_info=True)
+        assert load().gorila_round_async(gb.h, ids.ctypes.data, 2, k, None, info.data_ptr(), ri.data_ptr(),
+                                         sy.data_ptr()) == 0
+        gb.stream.synchronize()
+        infos = (LearnerInfo * 2).from_buffer_copy(info.numpy().tobytes())
+        r = RoundInfo.from_buffer_copy(ri.numpy().tobytes())
+        assert [x.as_dict() for x in infos] == ra[0]
+        assert (r.n_accepted, r.version_before, r.version_after) == tuple(ra[1].values())
+        assert list(sy.numpy().astype(bool)) == list(ra[2])
+
+
 def test_round_async_matches_round_bitwise():
     """gorila_round_async (results read one round later) == gorila_round, state and results."""
     ga, _ = make_pair(nA=18, B=32, C=3000, n_insert=3000, math="bf16", target_period=3, outlier_warmup=2)
     gb, _ = make_pair(nA=18, B=32, C=3000, n_insert=3000, math="bf16", target_period=3, outlier_warmup=2)
     ids = np.array([0], np.int32)
-    pend, res_b = None, []
+    pend, res_a, res_b = None, [], []
     for k in range(8):
-        ra = ga.round(ids, k, want_info=True)
+        res_a.append(ga.round(ids, k, want_info=True))
         h = gb.round_async(ids, k)
         if pend is not None:
             res_b.append(gb.round_result(pend))
         pend = h
-        if k < 7:
-            continue
     res_b.append(gb.round_result(pend))
+    for ra, rb in zip(res_a, res_b):  # every round's result, through the result ring
+        assert ra[0] == rb[0] and ra[1] == rb[1] and list(ra[2]) == list(rb[2])
     ta, ma, va, Va = ga.get_state()
     tb, mb, vb, Vb = gb.get_state()
     assert (ta == tb).all() and (ma == mb).all() and (va == vb).all() and Va == Vb

@@ -1,4 +1,4 @@
-"""e2e loop variants: result lag depth and how the host waits (block vs spin on event query)."""
+"""e2e loop variants: result lag depth (round_async / round_result = gorila_round_post / _fetch)."""
 import os
 import sys
 import time
@@ -30,22 +30,7 @@ r1 = torch.zeros(1, dtype=torch.float32).pin_memory()
 d1 = torch.zeros(1, dtype=torch.uint8).pin_memory()
 N = 1000
 
-x = torch.zeros(1, device="cuda")
-for mode in ("sync", "spin"):
-    tl = 0.0
-    for _ in range(200):
-        g.round(ids, k); k += 1
-        if mode == "sync":
-            stream.synchronize()
-        else:
-            e = torch.cuda.Event(); e.record(stream)
-            while not e.query():
-                pass
-        t0 = time.perf_counter(); x.add_(1); tl += time.perf_counter() - t0
-    stream.synchronize()
-    print("launch after", mode, round(tl / 200 * 1e6, 1), "us")
-
-for spin in (False, True):
+for spin in (False,):
     for lag in (1, 2, 3):
         pend = []
         stream.synchronize()
@@ -59,10 +44,6 @@ for spin in (False, True):
             pend.append(g.round_async(ids, k)); k += 1
             if len(pend) > lag:
                 h = pend.pop(0)
-                if spin:
-                    ev = g._slots[h[0]]["ev"]
-                    while not ev.query():
-                        pass
                 g.round_result(h)
         for h in pend:
             g.round_result(h)
