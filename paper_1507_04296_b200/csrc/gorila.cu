@@ -411,14 +411,6 @@ CUtensorMap nhwc_map(gorila_ctx* ctx, const void* x, int B, int bw, int bh, int 
     const uint32_t es[5] = {1, (uint32_t)s, (uint32_t)s, 1, 1};
     return tmap(ctx, x, 5, dims, str, box, es);
 }
-// conv1 pixel-pair view of s [B][84][84][4]: (8, 42 pairs, 84 rows, B, 4 pair offsets)
-CUtensorMap conv1_map(gorila_ctx* ctx, const void* s, int B, int bh_rows, int bb) {
-    const uint64_t dims[5] = {8, 42, 84, (uint64_t)B, 4};
-    const uint64_t str[4] = {16, 84 * 8, 84 * 84 * 8, 16};
-    const uint32_t box[5] = {8, 40, (uint32_t)(bh_rows * 4), (uint32_t)bb, 4};
-    const uint32_t es[5] = {1, 2, 4, 1, 1};
-    return tmap(ctx, s, 5, dims, str, box, es);
-}
 // swizzled forward im2col views (OpConvFwdS): 128-B rows of 64 K-elements per output pixel.
 // conv3: (64 c, W, H, B); conv2: (64 = 2 pixels x 32 c, W-1 [x stride C*2], H, B), element strides 2
 template <class SH>
@@ -827,7 +819,6 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     const gorila_config& cfg = ctx->cfg;
     Learner& Lr = ctx->learners[j];
     const int B = ctx->B, nA = ctx->nA;
-    const bool fp32 = std::is_same<T, float>::value;
     constexpr bool fp32v = std::is_same<T, float>::value;
     const uint64_t k_src = round >= (uint64_t)s_j ? round - (uint64_t)s_j : 0;
     const int slot = (int)(k_src % (uint64_t)ctx->H);
