@@ -466,12 +466,17 @@ template <typename T>
 __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, const float* __restrict__ a4,
                                                  const float* __restrict__ w5, int B, int nA, float* __restrict__ part,
                                                  int n_chunks, T* __restrict__ g4) {
-    pdl_wait();
-    pdl_trigger();
+    // a4 (fc4's output) and W5 (the replica) were written two or more kernels back: loaded before
+    // the wait (PDL: complete once this grid runs); only dQ comes from the kernel just before
     if ((int)blockIdx.x < 2 * n_chunks) {  // (chunk, column half)
         __shared__ float dq[FC5_ROWS_MAX * 32];
         const int rows = fc5_rows(B), c = blockIdx.x >> 1, b0 = c * rows, nb = min(rows, B - b0);
         const int n = threadIdx.x + 256 * (blockIdx.x & 1);
+        float xpre[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) xpre[u] = u < nb ? a4[(int64_t)(b0 + u) * FC4_OUT + n] : 0.f;
+        pdl_wait();
+        pdl_trigger();
         for (int i = threadIdx.x; i < nb * nA; i += 256) dq[i] = dQ[(int64_t)b0 * nA + i];
         __syncthreads();
         float acc[32];
@@ -479,9 +484,9 @@ __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, c
         for (int a = 0; a < 32; ++a) acc[a] = 0.f;
         const float* xs = a4 + (int64_t)b0 * FC4_OUT + n;
         for (int bb = 0; bb < nb; bb += 8) {
-            float x[8];  // eight rows' loads in flight before the FMAs
+            float x[8];  // eight rows' loads in flight before the FMAs (the first eight prefetched)
 #pragma unroll
-            for (int u = 0; u < 8; ++u) x[u] = bb + u < nb ? xs[(int64_t)(bb + u) * FC4_OUT] : 0.f;
+            for (int u = 0; u < 8; ++u) x[u] = bb == 0 ? xpre[u] : bb + u < nb ? xs[(int64_t)(bb + u) * FC4_OUT] : 0.f;
 #pragma unroll
             for (int u = 0; u < 8; ++u) {
                 if (bb + u >= nb) break;
@@ -503,11 +508,28 @@ __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, c
         return;
     }
     const int n_g = B * FC4_OUT, nblk = gridDim.x - 2 * n_chunks;
-    for (int f = (blockIdx.x - 2 * n_chunks) * blockDim.x + threadIdx.x; f < n_g; f += nblk * blockDim.x) {
+    const int f0 = (blockIdx.x - 2 * n_chunks) * blockDim.x + threadIdx.x;
+    float wv[32], x0 = 0.f;  // this thread's first output: its W5 column and a4 value, before the wait
+    {
+        const int n = f0 % FC4_OUT;
+#pragma unroll
+        for (int a = 0; a < 32; ++a) wv[a] = a < nA ? w5[a * FC4_OUT + n] : 0.f;
+        if (f0 < n_g) x0 = a4[f0];
+    }
+    pdl_wait();
+    pdl_trigger();
+    for (int f = f0; f < n_g; f += nblk * blockDim.x) {
         const int b = f / FC4_OUT, n = f - b * FC4_OUT;
         float acc = 0.f;
-        for (int a = 0; a < nA; ++a) acc = fmaf(dQ[b * nA + a], w5[a * FC4_OUT + n], acc);
-        g4[f] = fromf<T>(a4[f] > 0.f ? acc : 0.f);
+        if (f == f0) {
+#pragma unroll
+            for (int a = 0; a < 32; ++a)
+                if (a < nA) acc = fmaf(dQ[b * nA + a], wv[a], acc);
+        } else {
+            for (int a = 0; a < nA; ++a) acc = fmaf(dQ[b * nA + a], w5[a * FC4_OUT + n], acc);
+        }
+        const float x = f == f0 ? x0 : a4[f];
+        g4[f] = fromf<T>(x > 0.f ? acc : 0.f);
     }
 }
 
