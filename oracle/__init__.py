@@ -10,8 +10,10 @@ none of the method's arithmetic).
 Pins: every function is pinned by a ``-m "not gpu"`` test in
 ``tests/test_oracle_*.py`` against something other than itself (Philox
 known-answer vectors, closed forms, finite differences, torch CPU library
-routines, brute force, SPEC worked examples). The whole learner update as a
-composition has no worked example in the paper: "parity unpinned" for the
-composition as such (its parts are pinned) — see DESIGN.md.
+routines, brute force, SPEC worked examples). The paper prints no worked
+example of the whole learner update; the composed round (sample → forward →
+TD → backward → RMSProp step) is pinned by a closed form instead: with W1 = 0
+every activation is spatially constant and the round reduces to written-out
+sums (tests/test_oracle_round_closed_form.py) — see DESIGN.md §3.
 """
 from .gorila_oracle import *  # noqa: F401,F403
