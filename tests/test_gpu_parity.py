@@ -425,3 +425,23 @@ def test_round_async_matches_round_bitwise():
     assert last_a[0] == last_b[0] and last_a[1] == last_b[1] and list(last_a[2]) == list(last_b[2])
     assert len(res_b) == 8 and all(r[1]["version_after"] >= 1 for r in res_b)
 
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
+def test_constant_activation_round_parity(math):
+    """The oracle's closed-form case (tests/test_oracle_round_closed_form.py: W1 = 0, every
+    activation plane constant) through the CUDA path: Q equal across the batch, then the whole
+    round against the oracle, which that test pins to the written-out sums."""
+    from test_oracle_round_closed_form import constant_activation_params
+    nA, B, C = 6, 12, 400
+    p = constant_activation_params(nA)
+    theta0 = np.concatenate([p[n].ravel() for n, _ in O.param_shapes(nA)]).astype(np.float32)
+    g, orc = make_pair(nA=nA, B=B, C=C, n_insert=C, math=math, theta0=theta0, gamma=0.9,
+                       outlier_enabled=False, terminals=lambda j, d: np.where(np.arange(len(d)) % 5 == 0, 1, d).astype(d.dtype))
+    teacher_force(g, orc)
+    th = orc.theta.copy()
+    gpu, res = run_round_both(g, orc, 0, [0])
+    q, qh = gpu["q"][0]
+    q = np.asarray(q, np.float64)
+    assert np.abs(q - q[0]).max() <= TOL[math]["q"] * np.abs(q).max()
+    _check_round(gpu, res, math, nA, [0], orc, {0: th})

@@ -34,12 +34,10 @@ def _convT(W, dz, stride, in_hw):
     return dx
 
 
-def test_round_closed_form_constant_activations():
-    nA, B, C = 6, 12, 400
-    gamma, lr, rho, eps = 0.9, 2.5e-4, 0.95, 0.01
-    cfg = O.Config(n_actions=nA, batch=B, capacity=C, gamma=gamma, lr=lr, rms_rho=rho, rms_eps=eps,
-                   outlier_enabled=False, target_period=1000)
-    rng = np.random.default_rng(150704296)
+def constant_activation_params(nA, seed=150704296):
+    """θ with W1 = 0 (so every activation plane is constant) and mixed-sign ReLU masks.
+    Values are fp32-representable so that the GPU tests can reuse it unchanged."""
+    rng = np.random.default_rng(seed)
     p = {
         "W1": np.zeros((32, 4, 8, 8)), "b1": rng.normal(0, 1, 32),
         "W2": rng.normal(0, 0.05, (64, 32, 4, 4)), "b2": rng.normal(0, 0.5, 64),
@@ -47,6 +45,15 @@ def test_round_closed_form_constant_activations():
         "W4": rng.normal(0, 0.02, (512, 3136)), "b4": rng.normal(0, 0.5, 512),
         "W5": rng.normal(0, 0.1, (nA, 512)), "b5": rng.normal(0, 0.5, nA),
     }
+    return {k: v.astype(np.float32).astype(np.float64) for k, v in p.items()}
+
+
+def test_round_closed_form_constant_activations():
+    nA, B, C = 6, 12, 400
+    gamma, lr, rho, eps = 0.9, 2.5e-4, 0.95, 0.01
+    cfg = O.Config(n_actions=nA, batch=B, capacity=C, gamma=gamma, lr=lr, rms_rho=rho, rms_eps=eps,
+                   outlier_enabled=False, target_period=1000)
+    p = constant_activation_params(nA)
     theta0 = np.concatenate([p[n].ravel() for n, _ in O.param_shapes(nA)])
     orc = O.GorilaOracle(cfg, theta0)
     f = synth.frames(synth.SEED_DATA, 0, 0, C)
