@@ -17,6 +17,7 @@ order), a missing 1/255, a wrong stride in any dgrad, or a wrong sign in TD / th
 fails it.
 """
 import numpy as np
+import pytest
 
 import oracle as O
 import synth
@@ -48,10 +49,12 @@ def constant_activation_params(nA, seed=150704296):
     return {k: v.astype(np.float32).astype(np.float64) for k, v in p.items()}
 
 
-def test_round_closed_form_constant_activations():
+@pytest.mark.parametrize("optimizer,ps_mode", [("rmsprop", "aggregate"), ("adagrad", "per_message")])
+def test_round_closed_form_constant_activations(optimizer, ps_mode):
     nA, B, C = 6, 12, 400
-    gamma, lr, rho, eps = 0.9, 2.5e-4, 0.95, 0.01
+    gamma, lr, rho, eps, ada_eps = 0.9, 2.5e-4, 0.95, 0.01, 1e-8
     cfg = O.Config(n_actions=nA, batch=B, capacity=C, gamma=gamma, lr=lr, rms_rho=rho, rms_eps=eps,
+                   optimizer=optimizer, ada_eps=ada_eps, ps_mode=ps_mode,
                    outlier_enabled=False, target_period=1000)
     p = constant_activation_params(nA)
     theta0 = np.concatenate([p[n].ravel() for n, _ in O.param_shapes(nA)])
@@ -114,7 +117,9 @@ def test_round_closed_form_constant_activations():
         assert np.abs(G[n]).max() > 0, n
         np.testing.assert_allclose(got, G[n].ravel(), rtol=0, atol=1e-11 * scale, err_msg=n)
 
-    # first centered-RMSProp step from m = v = 0 (reading R2), closed form
-    theta1 = theta0 - lr * g / np.sqrt(rho * (1 - rho) * g * g + eps)
+    if optimizer == "rmsprop":  # first centered-RMSProp step from m = v = 0 (reading R2), closed form
+        theta1 = theta0 - lr * g / np.sqrt(rho * (1 - rho) * g * g + eps)
+    else:  # first AdaGrad step from an empty accumulator: θ − η g / (|g| + ε)
+        theta1 = theta0 - lr * g / (np.abs(g) + ada_eps)
     np.testing.assert_allclose(orc.theta, theta1, rtol=0, atol=1e-15)
     assert orc.V == 1
