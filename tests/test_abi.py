@@ -76,3 +76,51 @@ def test_sass_contains_tcgen05_and_tmem_loads():
     except FileNotFoundError:
         pytest.skip("cuobjdump not available")
     assert "UTCHMMA" in sass and "LDTM" in sass
+
+
+def _base_cfg(G, theta):
+    c = G.Config()
+    c.n_actions, c.batch, c.gamma, c.replay_capacity = 18, 32, 0.99, 1000
+    c.n_learners_local, c.learner_id_base, c.rank, c.world = 1, 0, 0, 1
+    c.optimizer, c.lr, c.rms_rho, c.rms_eps, c.ada_eps = G.GORILA_OPT_RMSPROP, 2.5e-4, 0.95, 0.01, 1e-8
+    c.target_period, c.max_staleness, c.history = 100, -1, 2
+    c.math, c.ps_mode, c.replay_mode = G.GORILA_MATH_FP32, 0, 0
+    c.theta0 = theta.ctypes.data
+    c.workspace = None  # validated last: the only error a valid config reaches without a GPU
+    return c
+
+
+@pytest.mark.parametrize("field,value,msg", [
+    ("n_actions", 0, "n_actions"), ("n_actions", 33, "n_actions"),   # P:182 one output per action, <= 32 (R5)
+    ("batch", 0, "batch"), ("batch", 4097, "batch"),
+    ("replay_capacity", 1, "replay_capacity"), ("n_learners_local", 0, "n_learners_local"),
+    ("world", 0, "rank/world"), ("rank", 1, "rank/world"), ("math", 1, "math"),
+    ("history", 0, "history"), ("history", 65, "history"), ("target_period", 0, "target_period"),
+    ("ps_mode", 2, "ps_mode"), ("replay_mode", 2, "replay_mode"), ("theta0", None, "theta0"),
+    (None, None, "workspace"),
+])
+def test_init_rejects_invalid_config_before_any_cuda_call(field, value, msg):
+    """Error behaviour of gorila_init (include/gorila.h): E_INVALID, a message naming the field,
+    *out set to NULL — all decided before the library touches the device."""
+    import numpy as np
+    from paper_1507_04296_b200 import gorila as G
+    lib = G.load()
+    theta = np.zeros(lib.gorila_param_count(18), np.float32)
+    c = _base_cfg(G, theta)
+    if field is not None:
+        setattr(c, field, value)
+    out = ctypes.c_void_p(1)
+    st = lib.gorila_init(ctypes.byref(c), ctypes.byref(out))
+    assert G.STATUS[st] == "E_INVALID"
+    assert msg in lib.gorila_last_error().decode()
+    assert out.value is None
+
+
+def test_calls_on_a_null_context_fail_cleanly():
+    from paper_1507_04296_b200 import gorila as G
+    lib = G.load()
+    assert G.STATUS[lib.gorila_init(None, None)] == "E_INVALID"
+    assert G.STATUS[lib.replay_insert(None, 0, 1, None, None, None, None, 0)] == "E_INVALID"
+    assert G.STATUS[lib.learner_step(None, None, 1, 0, None, None)] == "E_INVALID"
+    assert G.STATUS[lib.ps_apply_shard(None, 0, None)] == "E_INVALID"
+    assert "null" in lib.gorila_last_error().decode()
