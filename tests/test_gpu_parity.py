@@ -445,3 +445,34 @@ def test_constant_activation_round_parity(math):
     q = np.asarray(q, np.float64)
     assert np.abs(q - q[0]).max() <= TOL[math]["q"] * np.abs(q).max()
     _check_round(gpu, res, math, nA, [0], orc, {0: th})
+
+
+def test_error_behaviour_on_a_live_context():
+    """include/gorila.h error classes on a live context: bad learner id -> E_RANGE, negative count ->
+    E_SHAPE, count 0 -> OK and no effect, unsorted learner list -> E_INVALID, staleness >= history ->
+    E_RANGE; none of them poisons the context (a valid round still matches the oracle afterwards)."""
+    from paper_1507_04296_b200 import GorilaError
+    from paper_1507_04296_b200 import gorila as G
+    nA = 4
+    g, orc = make_pair(nA=nA, B=8, C=300, n_insert=300, math="fp32", L=2, history=2, outlier_enabled=False)
+    lib = G.load()
+    f = np.zeros((1, 84, 84), np.uint8)
+    a = np.zeros(1, np.uint8)
+    r = np.zeros(1, np.float32)
+    d = np.zeros(1, np.uint8)
+    with pytest.raises(GorilaError) as e:
+        g.replay_insert(2, f, a, r, d)
+    assert e.value.status == 3
+    st = lib.replay_insert(g.h, 0, -1, f.ctypes.data, a.ctypes.data, r.ctypes.data, d.ctypes.data, 0)
+    assert G.STATUS[st] == "E_SHAPE"
+    assert lib.replay_insert(g.h, 0, 0, None, None, None, None, 0) == 0
+    with pytest.raises(GorilaError) as e:
+        g.learner_step([1, 0], 0)
+    assert e.value.status == 1
+    with pytest.raises(GorilaError) as e:
+        g.learner_step([0, 1], 0, staleness=[0, 2])
+    assert e.value.status == 3
+    teacher_force(g, orc)
+    th = orc.theta.copy()
+    gpu, res = run_round_both(g, orc, 0, [0, 1])
+    _check_round(gpu, res, "fp32", nA, [0, 1], orc, {0: th, 1: th})
