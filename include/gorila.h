@@ -7,8 +7,11 @@
  * The library implements Algorithm 1's learner half and the
  * sharded parameter server for the Nature-DQN Q-network
  * (§5.1), one process per GPU. All compute runs in the library's own
- * sm_100a kernels; NCCL (the copy torch loads) carries the gradient
- * reduce-scatter and the parameter all-gather when world > 1.
+ * sm_100a kernels. When world > 1 the gradient sum and the parameter broadcast
+ * run inside one library kernel over NVLink peer memory (every rank maps every
+ * peer's workspace through CUDA IPC); NCCL (the copy torch loads) is used only
+ * to bootstrap those mappings and, if peer mappings are unavailable, as the
+ * fallback reduce-scatter / all-gather.
  *
  * Conventions (all entry points):
  *  - Ownership: the caller owns the workspace (device memory, e.g. a torch
@@ -199,11 +202,13 @@ GORILA_API gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, 
 
 /* Parameter-server step for `round` ("split disjointly across N_param
  * machines", "applies the updates that are accumulated from many
- * learners"; reading R12): reduce-scatter of the gradient buffers onto the
- * owning shard (NCCL when world > 1), one optimizer step on this rank's shard
- * with the mean of the accepted gradients (skipped if none), V += |Acc|,
- * all-gather of the updated theta^+ (Alg.1 P:116/"Update theta from
- * theta^+"), and the next replica. COLLECTIVE. info_out may be NULL. */
+ * learners"; reading R12): the gradient slices of this rank's shard summed in
+ * rank order, one optimizer step on the shard with the mean of the accepted
+ * gradients (skipped if none), V += |Acc|, and the updated slice broadcast into
+ * every rank's next replica (Alg.1 P:116/"Update theta from theta^+").
+ * When world > 1 this is one kernel reading and writing the peers' workspaces
+ * over NVLink (k_apply_p2p); without peer mappings, NCCL reduce-scatter +
+ * all-gather. COLLECTIVE. info_out may be NULL. */
 GORILA_API gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info* info_out);
 
 /* Target sync (Alg.1 P:130 "Every global N steps sync theta^- with theta^+";
@@ -282,6 +287,16 @@ GORILA_API gorila_status gorila_act(gorila_ctx* ctx, const uint8_t* states, int3
  * type). bytes must equal the tensor size (GORILA_E_SHAPE otherwise); host is a
  * host pointer; the call synchronises the library stream. */
 GORILA_API gorila_status gorila_get_activation(gorila_ctx* ctx, int32_t which, void* host, uint64_t bytes);
+/* Parity diagnostics (teacher-forced ReLU decisions, R30): enable != 0 makes every
+ * later learner_step copy each learner's a1..a3 (NHWC, math type) and a4 ([B][512] fp32) after its
+ * forward into a per-learner buffer (cudaMalloc'ed by the library on first enable, L x the
+ * activation bytes; freed by gorila_destroy); 0 stops the copies. Drops the cached round graphs.
+ * gorila_get_learner_activation reads learner `learner`'s copy of its last step: which 1..4 =
+ * a1..a4 with gorila_get_activation's layouts and sizes (E_SHAPE on a size mismatch, E_RANGE on a
+ * bad learner / which, E_INVALID while capture is off); synchronises the library stream. */
+GORILA_API gorila_status gorila_capture_activations(gorila_ctx* ctx, int32_t enable);
+GORILA_API gorila_status gorila_get_learner_activation(gorila_ctx* ctx, int32_t learner, int32_t which, void* host,
+                                                       uint64_t bytes);
 /* Per-phase device timing (diagnostics for the roofline report). When enabled,
  * learner_step / ps_apply_shard / sync_target record a CUDA event after each
  * phase on the stream; gorila_profile_read synchronises, returns the summed

@@ -70,7 +70,7 @@ def lib():
         L.orc_param_count.argtypes = [ctypes.c_int]
         L.orc_param_count.restype = i64
         L.orc_acts_per_sample.restype = i64
-        L.orc_qnet_forward.argtypes = [ctypes.c_int, ctypes.c_int, P, P, ctypes.c_int, P, P]
+        L.orc_qnet_forward.argtypes = [ctypes.c_int, ctypes.c_int, P, P, ctypes.c_int, P, P, P]
         L.orc_qnet_backward.argtypes = [ctypes.c_int, ctypes.c_int, P, P, P, P, ctypes.c_int, P]
         _lib = L
     return _lib
@@ -206,15 +206,17 @@ def acts_per_sample():
     return int(lib().orc_acts_per_sample())
 
 
-def qnet_forward(theta, s, n_actions, mode="exact"):
-    """O4: Q(s,.;theta) for s u8 [B][4][84][84]. Returns (Q [B][nA], saved activations)."""
+def qnet_forward(theta, s, n_actions, mode="exact", want_z=False):
+    """O4: Q(s,.;theta) for s u8 [B][4][84][84]. Returns (Q [B][nA], saved activations), plus the
+    pre-activations z1..z4 (same layout, the values each ReLU decides on) if want_z."""
     theta = _c(theta, np.float64)
     s = _c(s, np.uint8)
     B = s.shape[0]
     Q = np.zeros((B, n_actions))
     acts = np.zeros((B, acts_per_sample()))
-    lib().orc_qnet_forward(n_actions, B, _p(theta), _p(s), MODES[mode], _p(Q), _p(acts))
-    return Q, acts
+    zs = np.zeros((B, acts_per_sample())) if want_z else None
+    lib().orc_qnet_forward(n_actions, B, _p(theta), _p(s), MODES[mode], _p(Q), _p(acts), _p(zs))
+    return (Q, acts, zs) if want_z else (Q, acts)
 
 
 def qnet_backward(theta, s, acts, dQ, n_actions, mode="exact"):
@@ -409,7 +411,10 @@ class GorilaOracle:
     def insert(self, j, frames, a, r, d):
         self.learners[j].ring.insert(frames, a, r, d)
 
-    def round(self, k, staleness=None):
+    def round(self, k, staleness=None, acts_hook=None):
+        """One round O1-O12. acts_hook (test teacher forcing, SURVEY §8(c) parity protocol):
+        acts_hook(j, acts, zs) -> the activations learner j's backward (O8) takes instead of its own
+        O4 activations; None = the oracle's own."""
         cfg = self.cfg
         staleness = staleness or {}
         self.history[k] = (self.theta.copy(), self.V)
@@ -441,7 +446,9 @@ class GorilaOracle:
                 # O3
                 s, s2, a, r, d = L.ring.gather(tau)
             # O4
-            Q, acts = qnet_forward(theta_j, s, cfg.n_actions, cfg.mode)
+            Q, acts, zs = qnet_forward(theta_j, s, cfg.n_actions, cfg.mode, want_z=True)
+            if acts_hook is not None:
+                acts = acts_hook(j, acts, zs)
             Qhat, _ = qnet_forward(L.theta_minus, s2, cfg.n_actions, cfg.mode)
             # O5, O6
             y, delta, dQ, loss, ell = td_terms(Q, Qhat, a, r, d, cfg.gamma)

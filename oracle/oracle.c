@@ -306,9 +306,15 @@ static void relu_store(double* z, int64_t n, int mode) {
  * EXACT: x = u8/255, everything fp64. BF16: x = u8 (exact integers), conv1..fc4
  * weights rounded to bf16, conv1 pre-activation = acc * fp32(1/255) + b1, the
  * conv activations a1..a3 rounded to bf16 after the ReLU (they are tensor-core
- * operands); a4, fc5 weights / biases and Q unrounded (fc5 runs in fp32). acts (nullable) receives [B][a1|a2|a3|a4] (CHW per sample). */
+ * operands); a4, fc5 weights / biases and Q unrounded (fc5 runs in fp32). acts (nullable) receives [B][a1|a2|a3|a4] (CHW per sample).
+ * zs (nullable) receives the pre-activations z1..z4 in the same layout (the values the ReLU decides
+ * on, before rounding) — read-only diagnostics for the parity tests; nothing below depends on it. */
+static void save_pre(double* zs, const double* z, int B, int64_t per, int64_t off) {
+    if (!zs) return;
+    for (int b = 0; b < B; ++b) memcpy(zs + (int64_t)b * ACTS_PER_SAMPLE + off, z + (int64_t)b * per, sizeof(double) * per);
+}
 EXPORT void orc_qnet_forward(int nA, int B, const double* theta, const uint8_t* s, int mode, double* Q,
-                             double* acts) {
+                             double* acts, double* zs) {
     double* x0 = (double*)malloc(sizeof(double) * (size_t)B * 4 * 84 * 84);
     for (int64_t i = 0; i < (int64_t)B * 4 * 84 * 84; ++i)
         x0[i] = (mode == ORC_BF16) ? (double)s[i] : (double)s[i] / 255.0;
@@ -332,13 +338,17 @@ EXPORT void orc_qnet_forward(int nA, int B, const double* theta, const uint8_t* 
     } else {
         orc_conv2d_fwd(B, 4, 84, 84, 32, 8, 4, x0, w1, theta + OFF_B1, a1);
     }
+    save_pre(zs, a1, B, L1_OUT, 0);
     relu_store(a1, (int64_t)B * L1_OUT, mode);
     orc_conv2d_fwd(B, 32, 20, 20, 64, 4, 2, a1, w2, theta + OFF_B2, a2);
+    save_pre(zs, a2, B, L2_OUT, L1_OUT);
     relu_store(a2, (int64_t)B * L2_OUT, mode);
     orc_conv2d_fwd(B, 64, 9, 9, 64, 3, 1, a2, w3, theta + OFF_B3, a3);
+    save_pre(zs, a3, B, L3_OUT, L1_OUT + L2_OUT);
     relu_store(a3, (int64_t)B * L3_OUT, mode);
     /* fc4 input = a3 flattened in (C,H,W) order (reading R18) — the NCHW memory order */
     orc_linear_fwd(B, 3136, 512, a3, w4, theta + OFF_B4, a4);
+    save_pre(zs, a4, B, L4_OUT, L1_OUT + L2_OUT + L3_OUT);
     /* a4 feeds only the fp32 fc5 layer (not a tensor-core operand): never rounded (R16) */
     relu_store(a4, (int64_t)B * L4_OUT, ORC_EXACT);
     orc_linear_fwd(B, 512, nA, a4, theta + OFF_W5, theta + OFF_W5 + 512 * nA, Q);

@@ -13,11 +13,9 @@
 // over batch x pixels). Both are staged with 16-byte vector loads into the matching
 // UMMA canonical (SWIZZLE_NONE) shared-memory layout.
 //
-// Two engines share the loaders / epilogues:
-//   gemm_tc   — sm_100a tensor cores: tcgen05.mma kind::f16 (M=128, N=BN, K=16) issued by
-//               one thread, fp32 accumulator in TMEM, tcgen05.commit -> mbarrier pipeline
-//               (2 smem stages + register prefetch of the next stage), tcgen05.ld epilogue.
-//   gemm_simt — fp32 FFMA tiles for the fp32 check mode (parity 1e-5).
+// gemm_simt (fp32 FFMA tiles) runs the fp32 check mode (parity 1e-5) on these loaders and
+// epilogues; the bf16 path runs the tcgen05 engines of tma_gemm.cuh / shift_gemm.cuh / tower.cuh,
+// which share the epilogues and the split / cluster helpers below.
 #pragma once
 #include "common.cuh"
 #include "layout.cuh"
@@ -449,219 +447,7 @@ __host__ __device__ constexpr uint32_t tmem_cols_for(int bn) {
 }
 // fp32 partial tile for the cluster reduction: [BN/16][128 rows][20 floats] (80-B row pitch: conflict-free)
 __host__ __device__ constexpr int tc_red_bytes(int bn) { return (bn / 16) * TC_BM * 80; }
-__host__ __device__ constexpr int tc_stages(int bn) { return bn <= 64 ? 4 : bn <= 128 ? 3 : 2; }
-__host__ __device__ constexpr int tc_stage_bytes(int bn) { return tc_stages(bn) * (TC_BM * TC_BK * 2 + bn * TC_BK * 2); }
 __host__ __device__ constexpr int tc_slice_bytes(int bn) { return 64 * (bn + 4) * 4; }
-__host__ __device__ constexpr int tc_smem_bytes(int bn) {
-    return (tc_stage_bytes(bn) > tc_red_bytes(bn) + tc_slice_bytes(bn) ? tc_stage_bytes(bn)
-                                                                        : tc_red_bytes(bn) + tc_slice_bytes(bn)) +
-           64;
-}
-
-// Stage one operand tile (ROWS x 64 reduction elements, bf16) in the canonical layout.
-// K-major : core matrix (8 rows x 16 B) at (row/8, kchunk): offset (row/8)*1024 + kch*128 + (row%8)*16
-//           -> descriptor LBO = 128 (K step), SBO = 1024 (8-row step); MMA kk starts at +kk*256.
-// MN-major: core matrix (8 k x 16 B = 8 rows) at (k/8, row/8): offset (k/8)*ROWS*16 + (row/8)*128 + (k%8)*16
-//           -> descriptor LBO = ROWS*16 (K step), SBO = 128 (8-row step); MMA kk starts at +kk*2*ROWS*16.
-template <int ROWS, bool MN>
-struct Stage {
-    static constexpr int ITERS = ROWS * 8 / TC_THREADS;  // 16-B chunks per thread
-    GORILA_DEV static void coords(int idx, int& row, int& k) {
-        if constexpr (!MN) {
-            row = (idx >> 6) * 8 + (idx & 7);
-            k = ((idx >> 3) & 7) * 8;  // first reduction element of the chunk
-        } else {
-            constexpr int G = ROWS / 8;
-            const int g = (idx >> 3) % G, khi = (idx >> 3) / G;
-            row = g * 8;
-            k = khi * 8 + (idx & 7);
-        }
-    }
-    GORILA_DEV static uint32_t offset(int idx) {
-        if constexpr (!MN) {
-            const int row = (idx >> 6) * 8 + (idx & 7), kch = (idx >> 3) & 7;
-            return (uint32_t)((row >> 3) * 1024 + kch * 128 + (row & 7) * 16);
-        } else {
-            constexpr int G = ROWS / 8;
-            const int g = (idx >> 3) % G, khi = (idx >> 3) / G;
-            return (uint32_t)(khi * ROWS * 16 + g * 128 + (idx & 7) * 16);
-        }
-    }
-    GORILA_DEV static uint64_t desc(uint32_t base, int kk) {
-        if constexpr (!MN) return umma_desc(base + kk * 256, 128, 1024);
-        else return umma_desc(base + kk * 2 * ROWS * 16, ROWS * 16, 128);
-    }
-    // this thread's 16-B chunks of the tile: cp.async global -> shared, zero-fill where the
-    // loader has no data (out of range rows, missing conv taps)
-    template <typename LD>
-    GORILA_DEV static void issue(const LD& ld, int row0, int r0, uint32_t st) {
-#pragma unroll
-        for (int q = 0; q < ITERS; ++q) {
-            const int idx = threadIdx.x + TC_THREADS * q;
-            int row, k;
-            coords(idx, row, k);
-            const void* src = ld.src8(row0 + row, r0 + k);
-            cp_async16(st + offset(idx), src ? src : ld.gptr(), src ? 16u : 0u);
-        }
-    }
-};
-
-template <int BN, typename LA, typename LB, typename EP>
-__global__ void __launch_bounds__(TC_THREADS) gemm_tc(const __grid_constant__ GemmBatch<LA, LB, EP> p) {
-    constexpr int A_BYTES = TC_BM * TC_BK * 2, B_BYTES = BN * TC_BK * 2, STAGES = tc_stages(BN);
-    static_assert(BN % 16 == 0 && BN >= 16 && BN <= 256, "UMMA N for M=128");
-    static_assert((BN * 8) % TC_THREADS == 0, "B tile split");
-    using SA = Stage<TC_BM, LA::kMN>;
-    using SB = Stage<BN, LB::kMN>;
-    extern __shared__ __align__(1024) uint8_t smem[];
-    uint8_t* sA = smem;                     // [STAGES][A_BYTES]
-    uint8_t* sB = smem + STAGES * A_BYTES;  // [STAGES][B_BYTES]
-    uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + tc_smem_bytes(BN) - 64);  // [STAGES]
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(mbar + STAGES);
-
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    GTRACE(0);
-    const int prob = blockIdx.z / p.splits, split = blockIdx.z - prob * p.splits;
-    const GemmProb<LA, LB, EP>& P = p.prob[prob];
-    const int i0 = blockIdx.x * TC_BM, j0 = blockIdx.y * BN;
-    const int n_chunks_total = (p.R + TC_BK - 1) / TC_BK;
-    const int kc_begin = split * p.chunks_per_split;
-    const int nK = max(0, min(n_chunks_total, kc_begin + p.chunks_per_split) - kc_begin);
-
-    if (warp == 0) tmem_alloc(tmem_slot, tmem_cols_for(BN));
-    GTRACE(1);
-    if (tid == 0) {
-        for (int st = 0; st < STAGES; ++st) mbar_init(&mbar[st], 1);
-        fence_mbar_init();
-    }
-    tc_fence_before();
-    __syncthreads();
-    tc_fence_after();
-    GTRACE(2);
-    pdl_wait();     // operands come from the preceding kernel(s)
-    pdl_trigger();  // the next kernel may start its prologue
-    GTRACE(3);
-    const uint32_t tmem = *tmem_slot;
-    constexpr uint32_t IDESC =
-        umma_idesc_bf16(TC_BM, BN) | (LA::kMN ? (1u << 15) : 0u) | (LB::kMN ? (1u << 16) : 0u);
-    const uint32_t sA0 = smem_u32(sA), sB0 = smem_u32(sB);
-
-    // multi-stage cp.async pipeline: up to STAGES-1 chunks in flight ahead of the MMA
-    auto issue = [&](int kc) {
-        const int st = kc % STAGES;
-        SA::issue(P.a, i0, (kc_begin + kc) * TC_BK, sA0 + st * A_BYTES);
-        SB::issue(P.b, j0, (kc_begin + kc) * TC_BK, sB0 + st * B_BYTES);
-    };
-#pragma unroll 1
-    for (int kc = 0; kc < STAGES - 1; ++kc) {
-        if (kc < nK) issue(kc);
-        cp_async_commit();
-    }
-    GTRACE(4);
-#pragma unroll 1
-    for (int kc = 0; kc < nK; ++kc) {
-        const int nxt = kc + STAGES - 1;
-        if (nxt < nK) {
-            // stage nxt % STAGES was last read by the MMAs of chunk nxt - STAGES = kc - 1
-            if (nxt >= STAGES) mbar_wait(&mbar[nxt % STAGES], ((nxt - STAGES) / STAGES) & 1);
-            issue(nxt);
-        }
-        cp_async_commit();
-        cp_async_wait<STAGES - 1>();  // this thread's copies of chunk kc have landed
-        GTRACE(8 + 2 * (kc & 7));
-        fence_proxy_async_smem();     // ... and are visible to the tensor core
-        __syncthreads();
-        GTRACE(9 + 2 * (kc & 7));
-        if (tid == 0) {
-            tc_fence_after();
-            const int st = kc % STAGES;
-            const uint32_t a_base = sA0 + st * A_BYTES, b_base = sB0 + st * B_BYTES;
-#pragma unroll
-            for (int kk = 0; kk < TC_BK / 16; ++kk)
-                umma_bf16(tmem, SA::desc(a_base, kk), SB::desc(b_base, kk), IDESC, (kc > 0 || kk > 0) ? 1u : 0u);
-            umma_commit(&mbar[st]);
-        }
-    }
-    cp_async_wait<0>();
-    // the last MMAs are done when the commits of the final chunks arrive (drain the most recent
-    // pending completion of every stage so no arrive is in flight at exit)
-    GTRACE(5);
-    for (int c = max(0, nK - STAGES); c < nK; ++c) mbar_wait(&mbar[c % STAGES], (c / STAGES) & 1);
-    tc_fence_after();
-    GTRACE(6);
-
-    // epilogue: warp w owns TMEM lanes (= tile rows) 32w .. 32w+31
-    const int lrow = warp * 32 + lane, row = i0 + lrow;
-    if (p.cluster > 1) {
-        // in-cluster split-K: every CTA parks its fp32 tile in its own smem (the stage buffers are
-        // free now); then CTA q reduces rows [q*128/CL, (q+1)*128/CL) over all CL tiles in rank
-        // order (DSMEM reads) and applies the epilogue to them.
-        float* red = reinterpret_cast<float*>(smem);
-        __syncthreads();
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-            float v[16];
-            if (nK > 0) tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-            else
-#pragma unroll
-                for (int e = 0; e < 16; ++e) v[e] = 0.f;
-            float4* dst = reinterpret_cast<float4*>(red + ((c0 / 16) * TC_BM + lrow) * 20);
-#pragma unroll
-            for (int e = 0; e < 4; ++e) dst[e] = make_float4(v[4 * e], v[4 * e + 1], v[4 * e + 2], v[4 * e + 3]);
-        }
-        cluster_sync();
-        // CTA q reduces rows [q*rows_per, (q+1)*rows_per): every thread owns float4 items of that
-        // slice and issues the CL peer reads at once (in flight together), sums them in rank order
-        // and parks the result in a private smem area; then the epilogue runs on the slice.
-        const int CL = p.cluster, rows_per = TC_BM / CL;
-        const int q = (int)cluster_ctarank();
-        float* slice = reinterpret_cast<float*>(smem + tc_red_bytes(BN));  // [rows_per][BN + 4]
-        const int n4 = rows_per * BN / 4;
-        for (int it = tid; it < n4; it += TC_THREADS) {
-            const int r_loc = it / (BN / 4), c4 = (it % (BN / 4)) * 4;
-            const int r_glob = q * rows_per + r_loc;
-            const uint32_t a = smem_u32(red + ((c4 / 16) * TC_BM + r_glob) * 20 + (c4 % 16));
-            float4 x[16];
-#pragma unroll
-            for (int pr = 0; pr < 16; ++pr)
-                if (pr < CL) x[pr] = dsmem_ld4(dsmem_map(a, (uint32_t)pr));
-            float4 acc = x[0];
-#pragma unroll
-            for (int pr = 1; pr < 16; ++pr)
-                if (pr < CL) {
-                    acc.x += x[pr].x; acc.y += x[pr].y; acc.z += x[pr].z; acc.w += x[pr].w;
-                }
-            *reinterpret_cast<float4*>(slice + r_loc * (BN + 4) + c4) = acc;
-        }
-        __syncthreads();
-        for (int item = tid; item < rows_per * (BN / 16); item += TC_THREADS) {
-            const int r_loc = item % rows_per, c0 = (item / rows_per) * 16;
-            float v[16];
-#pragma unroll
-            for (int e = 0; e < 16; ++e) v[e] = slice[r_loc * (BN + 4) + c0 + e];
-            if (j0 + c0 < p.N) P.ep.apply16(i0 + q * rows_per + r_loc, j0 + c0, v, 0);
-        }
-        cluster_sync();  // peers keep their smem alive until everyone has read it
-    } else {
-#pragma unroll 1
-        for (int c0 = 0; c0 < BN; c0 += 16) {
-            float v[16];
-            if (nK > 0) {
-                tmem_ld16(tmem + ((uint32_t)(warp * 32) << 16) + (uint32_t)c0, v);
-            } else {
-#pragma unroll
-                for (int e = 0; e < 16; ++e) v[e] = 0.f;
-            }
-            if (j0 + c0 < p.N) P.ep.apply16(row, j0 + c0, v, split);
-        }
-    }
-    GTRACE(7);
-    tc_fence_before();
-    __syncthreads();
-    if (warp == 0) tmem_dealloc(tmem, tmem_cols_for(BN));
-    GTRACE(30);
-}
-
 // ====================================================================== fp32 SIMT engine
 constexpr int SM_BI = 64, SM_BJ = 64, SM_BR = 16;
 

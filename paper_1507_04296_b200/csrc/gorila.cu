@@ -216,6 +216,10 @@ struct gorila_ctx {
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork[4] = {}, ev_join = nullptr;
     bool fork = true;
+    // parity diagnostics (gorila_capture_activations): every learner's a1..a4 copied after its
+    // forward, so that tests can read the ReLU decisions of each learner of a multi-learner step
+    bool cap_acts = false;
+    uint8_t* cap_buf = nullptr;  // [L][a1 | a2 | a3 (B x A* x esz) | a4 (B x 512 fp32)], cudaMalloc'ed
 };
 
 extern "C" void early_apply_p2p(gorila_ctx* ctx, uint64_t round);  // defined with the PS calls below
@@ -688,40 +692,6 @@ int pick_splits(int64_t chunks_total, int64_t base_ctas, int target_ctas, int ma
 }
 
 // ------------------------------------------------------------------ GEMM dispatch
-template <int BN, typename LA, typename LB, typename EP>
-void launch_tc(GemmBatch<LA, LB, EP> gb, int nprob, cudaStream_t st, bool pdl) {
-    const int smem = tc_smem_bytes(BN);
-    static bool attr_set = false;
-    if (!attr_set) {
-        cudaFuncSetAttribute(gemm_tc<BN, LA, LB, EP>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-        cudaFuncSetAttribute(gemm_tc<BN, LA, LB, EP>, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-        attr_set = true;
-    }
-    dim3 grid((gb.M + TC_BM - 1) / TC_BM, (gb.N + BN - 1) / BN, nprob * gb.splits);
-    cudaLaunchConfig_t cfg{};
-    cfg.gridDim = grid;
-    cfg.blockDim = dim3(TC_THREADS);
-    cfg.dynamicSmemBytes = smem;
-    cfg.stream = st;
-    cudaLaunchAttribute at[2];
-    int na = 0;
-    if (gb.cluster > 1) {
-        at[na].id = cudaLaunchAttributeClusterDimension;
-        at[na].val.clusterDim.x = 1;
-        at[na].val.clusterDim.y = 1;
-        at[na].val.clusterDim.z = gb.cluster;
-        ++na;
-    }
-    if (pdl) {
-        at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-        at[na].val.programmaticStreamSerializationAllowed = 1;
-        ++na;
-    }
-    cfg.attrs = at;
-    cfg.numAttrs = na;
-    cudaLaunchKernelEx(&cfg, gemm_tc<BN, LA, LB, EP>, gb);
-}
-
 template <typename LA, typename LB, typename EP>
 void launch_simt(GemmBatch<LA, LB, EP> gb, int nprob, cudaStream_t st, bool pdl) {
     cudaLaunchConfig_t cfg{};
@@ -736,46 +706,25 @@ void launch_simt(GemmBatch<LA, LB, EP> gb, int nprob, cudaStream_t st, bool pdl)
     cudaLaunchKernelEx(&cfg, gemm_simt<LA, LB, EP>, gb);
 }
 
-// C[M][N] = sum_r A(i,r) B(j,r): bf16 -> tcgen05 engine (BN = N tile), fp32 -> SIMT engine.
-// `splits` requested split of the reduction (rounded to whole chunks) into partial outputs
-// (epilogue gets the split index). cluster_target > 0 (tc only): instead reduce the split
-// inside a thread-block cluster (size <= 8) so that about cluster_target CTAs run, with the
-// epilogue applied once by the leader — no partial buffers.
+// fp32 check mode: C[M][N] = sum_r A(i,r) B(j,r) on the SIMT engine. `splits` requested split of
+// the reduction (rounded to whole chunks) into partial outputs (the epilogue gets the split index).
+// The last argument is ignored (call sites keep the CTA target their bf16 twin uses).
 template <typename T, int BN, typename LA, typename LB, typename EP>
 void gemm(gorila_ctx* ctx, const GemmProb<LA, LB, EP>* probs, int nprob, int M, int N, int R, int splits,
-          int cluster_target = 0) {
+          int = 0) {
+    static_assert(std::is_same<T, float>::value, "the bf16 path runs the TMA / shifted-window engines");
     GemmBatch<LA, LB, EP> gb{};
     for (int i = 0; i < nprob; ++i) gb.prob[i] = probs[i];
     if (nprob == 1) gb.prob[1] = probs[0];
     gb.M = M;
     gb.N = N;
     gb.R = R;
-    const int chunk = std::is_same<T, float>::value ? SM_BR : TC_BK;
-    const int chunks = std::max(1, (R + chunk - 1) / chunk);
+    const int chunks = std::max(1, (R + SM_BR - 1) / SM_BR);
     splits = std::max(1, std::min(splits, chunks));
     gb.chunks_per_split = (chunks + splits - 1) / splits;
     gb.splits = (chunks + gb.chunks_per_split - 1) / gb.chunks_per_split;
     gb.cluster = 1;
-    static const int cluster_env = [] {  // GORILA_CLUSTER=0 disables in-cluster split-K (experiments)
-        const char* e = getenv("GORILA_CLUSTER");
-        return e ? atoi(e) : 1;
-    }();
-    if (!std::is_same<T, float>::value && cluster_target > 0 && cluster_env) {
-        const int tiles = ((M + TC_BM - 1) / TC_BM) * ((N + BN - 1) / BN) * nprob;
-        const int want = std::max(1, (cluster_target + tiles - 1) / tiles);
-        int cl = 1;  // a power of two <= 16 (the reduction splits the 128 tile rows evenly)
-        while (cl * 2 <= std::min(16, std::min(want, chunks))) cl *= 2;
-        if (cl > 1) {
-            gb.cluster = cl;
-            gb.splits = cl;
-            gb.chunks_per_split = (chunks + cl - 1) / cl;
-        }
-    }
-    if constexpr (std::is_same<T, float>::value) {
-        launch_simt(gb, nprob, ctx->stream, ctx->pdl);
-    } else {
-        launch_tc<BN>(gb, nprob, ctx->stream, ctx->pdl);
-    }
+    launch_simt(gb, nprob, ctx->stream, ctx->pdl);
     LAUNCHED();
 }
 
@@ -824,6 +773,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     const int slot = (int)(k_src % (uint64_t)ctx->H);
     // gradient destination: the shared sum, or (per-message mode) this learner's own buffer
     float* const Gd = ctx->per_msg ? ctx->G_all + (int64_t)j * ctx->W * ctx->q : ctx->G;
+    // the round's first learner resets the accepted count; the others add to it (also in
+    // per-message mode, where every learner writes its own gradient buffer: accumulate = 0)
+    const bool first_learner = accumulate == 0;
     if (ctx->per_msg) accumulate = 0;
     const T* rt = P_<T>(ctx->rep_t[slot]);
     const float* rf = ctx->rep_f[slot];
@@ -850,7 +802,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                (const uint64_t*)(ctx->replay_global && ctx->W > 1 && !replay_barrier_off() ? ctx->n_snap : nullptr),
                ctx->sshard, key,
                (uint32_t)(cfg.learner_id_base + j), (const uint64_t*)ctx->dev_round, B, s, s2, ctx->sa, ctx->sr,
-               ctx->sd, ctx->sidx, accumulate ? (uint32_t*)nullptr : ctx->n_acc_local);
+               ctx->sd, ctx->sidx, first_learner ? ctx->n_acc_local : (uint32_t*)nullptr);
     }
     }
     mark(ctx, PH_SAMPLE);
@@ -1699,6 +1651,10 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     if (cfg->workspace_bytes < need) return fail(GORILA_E_OOM, "workspace too small: need " + std::to_string(need));
 
     gorila_ctx* ctx = new gorila_ctx();
+    struct InitGuard {  // any early return below destroys the partial context (streams, pinned buffers, comm)
+        gorila_ctx* c;
+        ~InitGuard() { if (c) gorila_destroy(c); }
+    } guard{ctx};
     ctx->cfg = *cfg;
     ctx->cfg.theta0 = nullptr;
     ctx->cfg.nccl_unique_id = nullptr;
@@ -1789,11 +1745,9 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
         const char* pe = getenv("GORILA_P2P");  // GORILA_P2P=0: NCCL reduce-scatter / all-gather
         if (!(pe && atoi(pe) == 0) && cfg->world <= MAX_W) ctx->p2p = p2p_setup(ctx);
         if (ctx->per_msg && !ctx->p2p) {
-            gorila_destroy(ctx);
             return fail(GORILA_E_INVALID, "per-message mode needs the peer-memory exchange (world > 1)");
         }
         if (ctx->replay_global && !ctx->p2p) {
-            gorila_destroy(ctx);
             return fail(GORILA_E_INVALID, "global replay needs the peer-memory mapping (world > 1)");
         }
     }
@@ -1811,6 +1765,7 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     memset(ctx->ring_host, 0, (size_t)gorila_ctx::kRing * ctx->ring_slot);
     CU(cudaHostGetDevicePointer((void**)&ctx->ring_dev, ctx->ring_host, 0));
     CU(cudaStreamSynchronize(st));
+    guard.c = nullptr;
     *out = ctx;
     return GORILA_OK;
 }
@@ -1845,6 +1800,7 @@ void gorila_destroy(gorila_ctx* ctx) {
         if (ctx->stage[i]) cudaFreeHost(ctx->stage[i]);
     }
     if (ctx->stage_dev) cudaFree(ctx->stage_dev);
+    if (ctx->cap_buf) cudaFree(ctx->cap_buf);
     if (ctx->ring_host) cudaFreeHost(ctx->ring_host);
     if (ctx->comm) {
         if (ctx->poisoned) ncclCommAbort(ctx->comm);
@@ -1875,6 +1831,13 @@ gorila_status replay_insert(gorila_ctx* ctx, int32_t learner, int64_t count, con
     if (count < 0) return fail(GORILA_E_SHAPE, "negative count");
     if (count == 0) return GORILA_OK;
     if (!frames || !actions || !rewards || !terminals) return fail(GORILA_E_INVALID, "null buffer");
+    if (!src_on_device) {  // a host action outside [0, nA) would index past the TD kernel's Q rows
+        const int64_t from = count > ctx->cfg.replay_capacity ? count - ctx->cfg.replay_capacity : 0;
+        for (int64_t i = from; i < count; ++i)
+            if (actions[i] >= ctx->nA)
+                return fail(GORILA_E_RANGE, "action " + std::to_string((int)actions[i]) + " at " + std::to_string(i) +
+                                                " is not below n_actions");
+    }
     Learner& l = ctx->learners[learner];
     const int64_t C = ctx->cfg.replay_capacity;
     cudaMemcpyKind kind = src_on_device ? cudaMemcpyDeviceToDevice : cudaMemcpyHostToDevice;
@@ -2080,6 +2043,15 @@ gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
         gorila_status s = ctx->cfg.math == GORILA_MATH_FP32 ? run_learner<float>(ctx, j, round, s_j, ran > 0)
                                                              : run_learner<__nv_bfloat16>(ctx, j, round, s_j, ran > 0);
         if (s != GORILA_OK) return s;
+        if (ctx->cap_acts) {  // a1..a4 are final once the forward ran (the backward only reads them)
+            const size_t e = ctx->esz, Bs = (size_t)ctx->B;
+            const size_t n1 = Bs * A1 * e, n2 = Bs * A2 * e, n3 = Bs * A3 * e, n4 = Bs * A4 * 4;
+            uint8_t* dst = ctx->cap_buf + (size_t)j * (n1 + n2 + n3 + n4);
+            CU(cudaMemcpyAsync(dst, ctx->a1, n1, cudaMemcpyDeviceToDevice, st));
+            CU(cudaMemcpyAsync(dst + n1, ctx->a2, n2, cudaMemcpyDeviceToDevice, st));
+            CU(cudaMemcpyAsync(dst + n1 + n2, ctx->a3, n3, cudaMemcpyDeviceToDevice, st));
+            CU(cudaMemcpyAsync(dst + n1 + n2 + n3, ctx->a4, n4, cudaMemcpyDeviceToDevice, st));
+        }
         ++ran;
     }
     if (ran == 0) {
@@ -2706,9 +2678,10 @@ gorila_status gorila_act(gorila_ctx* ctx, const uint8_t* states, int32_t n, uint
     cudaStream_t st = ctx->stream;
     const size_t sbytes = (size_t)n * NSTACK * FRAME_BYTES;
     const uint8_t* src = states;
-    if (!states_on_device) {  // stage through the (idle) conversion scratch
-        CU(cudaMemcpyAsync(ctx->tmp_int, states, sbytes, cudaMemcpyHostToDevice, st));
-        src = reinterpret_cast<const uint8_t*>(ctx->tmp_int);
+    if (!states_on_device) {  // land the u8 states in the s' staging buffer: B * 4 * 7056 * sizeof(T) >= sbytes
+        static_assert(NSTACK * FRAME_BYTES > 0, "");
+        CU(cudaMemcpyAsync(ctx->s2, states, sbytes, cudaMemcpyHostToDevice, st));
+        src = reinterpret_cast<const uint8_t*>(ctx->s2);
     }
     const bool fp32 = ctx->cfg.math == GORILA_MATH_FP32;
     const int64_t total = (int64_t)n * (FRAME_BYTES / 4);
@@ -2756,6 +2729,39 @@ gorila_status gorila_get_activation(gorila_ctx* ctx, int32_t which, void* host, 
     if (bytes != n) return fail(GORILA_E_SHAPE, "bytes must be " + std::to_string(n));
     CU(cudaStreamSynchronize(ctx->stream));
     CU(cudaMemcpy(host, src, n, cudaMemcpyDeviceToHost));
+    return GORILA_OK;
+}
+
+gorila_status gorila_capture_activations(gorila_ctx* ctx, int32_t enable) {
+    if (!ctx) return fail(GORILA_E_INVALID, "null context");
+    if (enable && !ctx->cap_buf) {
+        const size_t e = ctx->esz, Bs = (size_t)ctx->B;
+        const size_t per = Bs * (A1 + A2 + A3) * e + Bs * A4 * 4;
+        CU(cudaMalloc((void**)&ctx->cap_buf, per * (size_t)ctx->L));
+    }
+    ctx->cap_acts = enable != 0;
+    // the cached round graphs were captured without (or with) the copies: re-capture
+    for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
+    ctx->graphs.clear();
+    ctx->graph_kernels.clear();
+    ctx->graph_seen.clear();
+    return GORILA_OK;
+}
+
+gorila_status gorila_get_learner_activation(gorila_ctx* ctx, int32_t learner, int32_t which, void* host,
+                                            uint64_t bytes) {
+    gorila_status s = check_learner(ctx, learner);
+    if (s != GORILA_OK) return s;
+    if (!host) return fail(GORILA_E_INVALID, "null argument");
+    if (!ctx->cap_acts) return fail(GORILA_E_INVALID, "activation capture is off (gorila_capture_activations)");
+    if (which < 1 || which > 4) return fail(GORILA_E_RANGE, "which must be in [1, 4]");
+    const uint64_t e = ctx->esz, Bs = (uint64_t)ctx->B;
+    const uint64_t n[4] = {Bs * A1 * e, Bs * A2 * e, Bs * A3 * e, Bs * A4 * 4};
+    uint64_t off = (uint64_t)learner * (n[0] + n[1] + n[2] + n[3]);
+    for (int i = 1; i < which; ++i) off += n[i - 1];
+    if (bytes != n[which - 1]) return fail(GORILA_E_SHAPE, "bytes must be " + std::to_string(n[which - 1]));
+    CU(cudaStreamSynchronize(ctx->stream));
+    CU(cudaMemcpy(host, ctx->cap_buf + off, bytes, cudaMemcpyDeviceToHost));
     return GORILA_OK;
 }
 

@@ -64,7 +64,8 @@ EXPORTS = ["gorila_param_count", "gorila_workspace_bytes", "gorila_init", "goril
            "gorila_get_q", "gorila_get_activation", "gorila_act", "gorila_kernel_launches", "gorila_profile_enable", "gorila_profile_read",
            "gorila_profile_phase_count", "gorila_profile_phase_name", "gorila_nccl_unique_id", "gorila_round",
            "gorila_round_async", "gorila_round_post", "gorila_round_fetch",
-           "gorila_bench_phase", "gorila_debug_trace"]
+           "gorila_bench_phase", "gorila_debug_trace", "gorila_capture_activations",
+           "gorila_get_learner_activation"]
 
 
 def load(build_if_missing=True):
@@ -99,6 +100,8 @@ def load(build_if_missing=True):
     L.gorila_get_grad.argtypes = [P, P]
     L.gorila_get_q.argtypes = [P, i32, P, P]
     L.gorila_get_activation.argtypes = [P, i32, P, u64]
+    L.gorila_capture_activations.argtypes = [P, i32]
+    L.gorila_get_learner_activation.argtypes = [P, i32, i32, P, u64]
     L.gorila_round_post.argtypes = [P, P, i32, u64, P]
     L.gorila_round_fetch.argtypes = [P, u64, P, P, P]
     L.gorila_act.argtypes = [P, P, i32, u64, u64, ctypes.c_double, i64, i32, P, P]
@@ -356,6 +359,18 @@ class Gorila:
         bf = self.math == "bf16" and name != "a4"
         out = np.zeros((self.batch,) + shp, np.uint16 if bf else np.float32)
         _check(load().gorila_get_activation(self.h, which, out.ctypes.data, out.nbytes))
+        return (out.astype(np.uint32) << 16).view(np.float32) if bf else out
+
+    def capture_activations(self, on=True):
+        """Parity diagnostics: keep every learner's a1..a4 of each later learner step."""
+        _check(load().gorila_capture_activations(self.h, int(bool(on))))
+
+    def get_learner_activation(self, learner, name):
+        """Learner `learner`'s a1..a4 of its last step (capture_activations must be on), as float32."""
+        which, shp = self._ACT[name]
+        bf = self.math == "bf16" and name != "a4"
+        out = np.zeros((self.batch,) + shp, np.uint16 if bf else np.float32)
+        _check(load().gorila_get_learner_activation(self.h, learner, which, out.ctypes.data, out.nbytes))
         return (out.astype(np.uint32) << 16).view(np.float32) if bf else out
 
     def act(self, states, global_step, actor_id=0, eps_final=0.1, anneal_steps=1_000_000):

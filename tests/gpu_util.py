@@ -5,8 +5,20 @@ import numpy as np
 import oracle as O
 import synth
 
-TOL = {"fp32": {"q": 1e-5, "g": 1e-5, "dtheta": 1e-5, "loss": 1e-5, "g_kink": 5e-3},
-       "bf16": {"q": 1e-3, "g": 5e-3, "dtheta": 5e-3, "loss": 1e-3, "g_kink": 2e-2}}
+TOL = {"fp32": {"q": 1e-5, "g": 1e-5, "dtheta": 1e-5, "loss": 1e-5},
+       "bf16": {"q": 1e-3, "g": 5e-3, "dtheta": 5e-3, "loss": 1e-3}}
+
+# DESIGN.md R30 (teacher-forced ReLU decisions). A ReLU whose pre-activation lies within accumulation
+# error of 0 is decided by rounding order (fp32 vs fp64 sums; in bf16 mode also by a one-ulp different
+# rounding of an input activation), and its decision switches a whole gradient path on or off. Where
+# the GPU and the oracle decide such an element differently, the oracle's backward takes the GPU's
+# activation value for that element (its mask bit and its wgrad input) -- only there: the oracle's
+# pre-activation and the GPU's value must both lie within BAND * max|z_l| of 0, and at most
+# FORCED_MAX_FRAC of the layer may be forced. Every gradient and update is then compared at the full
+# tolerance above.
+BAND = {"fp32": 1e-4, "bf16": 2e-3}
+FORCED_MAX_FRAC = 1e-4
+ACT_LAYERS = (("a1", (20, 20, 32)), ("a2", (9, 9, 64)), ("a3", (7, 7, 64)), ("a4", (512,)))
 
 
 def make_pair(nA=4, B=32, C=2000, n_insert=2000, math="fp32", L=1, history=2, p_poison=0.0, terminals=None, **kw):
@@ -34,6 +46,50 @@ def make_pair(nA=4, B=32, C=2000, n_insert=2000, math="fp32", L=1, history=2, p_
         g.replay_insert(j, f, a, r, d)
         orc.insert(j, f, a, r, d)
     return g, orc
+
+
+def gpu_acts(g, learner=None):
+    """The GPU's a1..a4 of its last learner step in the oracle's layout ([B][a1|a2|a3|a4], CHW per
+    sample, float64): learner None = the shared scratch (the last learner that ran), else learner's
+    captured copy (Gorila.capture_activations)."""
+    parts = []
+    for name, shp in ACT_LAYERS:
+        x = g.get_activation(name) if learner is None else g.get_learner_activation(learner, name)
+        x = x.reshape((g.batch,) + shp)
+        if len(shp) == 3:  # NHWC -> CHW
+            x = x.transpose(0, 3, 1, 2)
+        parts.append(x.reshape(g.batch, -1))
+    return np.concatenate(parts, axis=1).astype(np.float64)
+
+
+def teacher_forced_acts(gpu, acts, zs, math, log=None):
+    """R30: the oracle's activations `acts` (pre-activations `zs`) with the GPU's value `gpu` taken at
+    every element whose ReLU decision differs -- asserting that each such decision is ambiguous (both
+    |z_oracle| and |a_gpu| within BAND * max|z_l|) and that they are few (<= FORCED_MAX_FRAC of the
+    layer). Any other difference is a real discrepancy and fails here. log (list) receives the number
+    of forced elements per layer."""
+    out = np.array(acts, np.float64, copy=True)
+    off, forced = 0, {}
+    for name, shp in ACT_LAYERS:
+        n = int(np.prod(shp))
+        sl = slice(off, off + n)
+        off += n
+        ref, got, z = acts[:, sl], gpu[:, sl], zs[:, sl]
+        flips = (got > 0) != (ref > 0)
+        nf = int(flips.sum())
+        forced[name] = nf
+        if nf == 0:
+            continue
+        band = BAND[math] * float(np.abs(z).max())
+        assert nf <= max(2, FORCED_MAX_FRAC * ref.size), (name, "ReLU decisions differ at", nf, "of", ref.size)
+        assert float(np.abs(z[flips]).max()) <= band and float(np.abs(got[flips]).max()) <= band, \
+            (name, "differing ReLU decision outside the ambiguity band", float(np.abs(z[flips]).max()),
+             float(np.abs(got[flips]).max()), band)
+        blk = out[:, sl]
+        blk[flips] = got[flips]
+    if log is not None:
+        log.append(forced)
+    return out
 
 
 def teacher_force(g, orc):
@@ -74,47 +130,25 @@ def per_tensor_rel_l2(x, ref, nA):
 
 
 def run_round_both(g, orc, k, learners, staleness=None):
-    """One round on both sides. Returns (gpu dict, oracle dict)."""
+    """One round on both sides; the oracle's backward is teacher-forced to the GPU's ReLU decisions
+    where they are ambiguous (R30). Returns (gpu dict, oracle dict)."""
     stal = None if staleness is None else [staleness.get(j, 0) for j in learners]
     th0 = g.get_state()[0]
+    g.capture_activations(True)
     info = g.learner_step(learners, k, staleness=stal)
     G = g.get_grad()
     qs = {j: g.get_q(j) for j in learners}
+    info_by = dict(zip(learners, info))
+    acts = {j: gpu_acts(g, j) for j in learners if not info_by[j]["not_ready"]}
     ri = g.ps_apply_shard(k)
     synced = g.sync_target(learners)
     th1, m1, v1, V1 = g.get_state()
-    gpu = {"info": dict(zip(learners, info)), "G": G, "q": qs, "round": ri, "synced": dict(zip(learners, synced)),
-           "theta0": th0, "theta1": th1, "V": V1}
-    res = orc.round(k, staleness=staleness)
+    forced = []
+    gpu = {"info": info_by, "G": G, "q": qs, "round": ri, "synced": dict(zip(learners, synced)),
+           "theta0": th0, "theta1": th1, "V": V1, "forced": forced}
+    res = orc.round(k, staleness=staleness,
+                    acts_hook=lambda j, a, z: teacher_forced_acts(acts[j], a, z, g.math, forced))
     return gpu, res
-
-
-def mask_flip_layer(g, acts, max_frac=1e-4, rel=1e-3):
-    """Observed kink rule (R30): the deepest conv / fc4 layer whose ReLU mask differs between
-    the GPU's saved activations of its last learner step (gorila_get_activation) and the oracle's (acts
-    of O.qnet_forward on the same batch), 0 if none. Only ambiguous decisions qualify: at most max_frac
-    of the layer's elements, every one with both values within rel * max|a| of zero; anything else is a
-    real discrepancy and fails here."""
-    B = acts.shape[0]
-    sizes = [("a1", (20, 20, 32)), ("a2", (9, 9, 64)), ("a3", (7, 7, 64)), ("a4", (512,))]
-    off, deepest = 0, 0
-    for l, (name, shp) in enumerate(sizes, start=1):
-        n = int(np.prod(shp))
-        ref = acts[:, off:off + n]
-        off += n
-        got = g.get_activation(name).reshape(B, -1)
-        if len(shp) == 3:  # GPU NHWC -> oracle CHW
-            got = got.reshape((B,) + shp).transpose(0, 3, 1, 2).reshape(B, -1)
-        flips = (got > 0) != (ref > 0)
-        nf = int(flips.sum())
-        if nf == 0:
-            continue
-        big = max(float(np.abs(ref).max()), 1e-30)
-        assert nf <= max(1, max_frac * ref.size), (name, "mask flips", nf, ref.size)
-        assert np.all(np.abs(got[flips]) <= rel * big) and np.all(np.abs(ref[flips]) <= rel * big), \
-            (name, "flipped elements not near zero", float(np.abs(got[flips]).max()), float(np.abs(ref[flips]).max()), big)
-        deepest = l
-    return deepest
 
 
 def round_bf16_vec(t):
@@ -135,33 +169,3 @@ def replica_of(theta, nA, math):
             out[off:off + n] = round_bf16_vec(out[off:off + n])
         off += n
     return out
-
-
-LAYER_OF = {"W1": 1, "b1": 1, "W2": 2, "b2": 2, "W3": 3, "b3": 3, "W4": 4, "b4": 4, "W5": 5, "b5": 5}
-
-
-def ambiguous_layer(theta, s, nA, rel=1e-6, mode="exact"):
-    """Kink rule (R30): the deepest hidden layer l (1..4) with a pre-activation |z| <= rel * max|z|,
-    recomputed with the oracle's layer primitives at the oracle's rounding points for `mode`; 0 if none.
-    A ReLU decision that close to 0 is decided differently by fp32 accumulation (and, in bf16 mode, by a
-    one-ulp difference of a rounded input activation), which moves the gradients of tensors at and below
-    layer l."""
-    p = O.unflatten(np.asarray(theta, np.float64), nA)
-    bf = mode == "bf16"
-
-    def q(t):
-        return round_bf16_vec(t) if bf else t
-
-    if bf:  # oracle BF16 mode: bf16 weights and a1..a3, raw bytes into conv1, 1/255 (fp32) on its sum
-        z1 = O.conv2d_fwd(s.astype(np.float64), q(p["W1"]), None, 4) * float(np.float32(1.0) / np.float32(255.0))
-        z1 = z1 + p["b1"][None, :, None, None]
-    else:
-        z1 = O.conv2d_fwd(s.astype(np.float64) / 255.0, p["W1"], p["b1"], 4)
-    z2 = O.conv2d_fwd(q(np.maximum(z1, 0)), q(p["W2"]), p["b2"], 2)
-    z3 = O.conv2d_fwd(q(np.maximum(z2, 0)), q(p["W3"]), p["b3"], 1)
-    z4 = O.linear_fwd(q(np.maximum(z3, 0)).reshape(len(s), -1), q(p["W4"]), p["b4"])
-    deepest = 0
-    for l, z in enumerate((z1, z2, z3, z4), start=1):
-        if np.any(np.abs(z) <= rel * np.max(np.abs(z))):
-            deepest = l
-    return deepest

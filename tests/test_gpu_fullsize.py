@@ -15,7 +15,7 @@ import pytest
 
 import oracle as O
 import synth
-from gpu_util import LAYER_OF, TOL, ambiguous_layer, mask_flip_layer, per_tensor_rel_l2, rel_inf, rel_l2, replica_of
+from gpu_util import TOL, gpu_acts, per_tensor_rel_l2, rel_inf, rel_l2, replica_of, teacher_forced_acts
 
 pytestmark = pytest.mark.gpu
 
@@ -66,6 +66,7 @@ def test_c2_full_size_sampled_parity(math, check):
     _fill_device(g, NA, C)
     ids = np.array([0], np.int32)
     n_checked = 0
+    forced = []  # teacher-forced ReLU decisions per checked round and layer (R30)
     for k in range(max(check) + 1):
         if k not in check:
             g.round(ids, k)
@@ -88,7 +89,7 @@ def test_c2_full_size_sampled_parity(math, check):
         assert np.array_equal(gpu_s["a"], a) and np.array_equal(gpu_s["r"], r) and np.array_equal(gpu_s["d"], d)
 
         # O4 - O6 from the GPU's parameters before the round
-        Q, acts = O.qnet_forward(th0, s, NA, mode)
+        Q, acts, zs = O.qnet_forward(th0, s, NA, mode, want_z=True)
         Qh, _ = O.qnet_forward(tm0, s2, NA, mode)
         assert rel_inf(q, Q) <= tol["q"] and rel_inf(qh, Qh) <= tol["q"], (k, rel_inf(q, Q), rel_inf(qh, Qh))
         _, _, dQ, loss, ell = O.td_terms(Q, Qh, a, r, d, GAMMA)
@@ -105,13 +106,15 @@ def test_c2_full_size_sampled_parity(math, check):
         assert accepted == (not bool(info["rejected_outlier"]))
         assert rinfo["n_accepted"] == int(accepted) and V1 == V0 + int(accepted)
 
-        # O8: gradient per tensor (kink rule R30)
+        # O8: gradient per tensor, the oracle's backward teacher-forced to the GPU's ambiguous ReLU
+        # decisions (R30; gpu_acts = the round's learner activations, read after the graph round)
         if accepted:
-            G_ref = O.qnet_backward(th0, s, acts, dQ, NA, mode)
-            kink = max(ambiguous_layer(th0, s, NA, mode=mode), mask_flip_layer(g, acts))
+            acts_tf = teacher_forced_acts(gpu_acts(g), acts, zs, math, forced)
+            G_ref = O.qnet_backward(th0, s, acts_tf, dQ, NA, mode)
+            assert rel_l2(G, G_ref) <= tol["g"], (k, "G", rel_l2(G, G_ref), forced[-1])
             for name, e in per_tensor_rel_l2(G, G_ref, NA).items():
-                assert e <= (tol["g"] if LAYER_OF[name] > kink else tol["g_kink"]), (k, "G", name, e, kink)
-            # O10: the RMSProp step from the GPU's optimizer state, per tensor (+ fp32 state floor R31)
+                assert e <= tol["g"], (k, "G", name, e, forced[-1])
+            # O10: the RMSProp step from the GPU's optimizer state, every tensor (+ fp32 state floor R31)
             th_ref, m_ref, v_ref = th0.astype(np.float64), m0.astype(np.float64), v0.astype(np.float64)
             O.rmsprop_apply(th_ref, m_ref, v_ref, G_ref, LR, RHO, EPS)
             d_gpu = th1.astype(np.float64) - th0
@@ -122,7 +125,7 @@ def test_c2_full_size_sampled_parity(math, check):
             for name, shp in O.param_shapes(NA):
                 n = int(np.prod(shp))
                 sl = slice(off, off + n)
-                if np.any(d_ref[sl]) and LAYER_OF[name] > kink:
+                if np.any(d_ref[sl]):
                     e = rel_l2(d_gpu[sl], d_ref[sl])
                     floor = np.linalg.norm(ulp[sl]) / np.linalg.norm(d_ref[sl])
                     assert e <= tol["dtheta"] + floor, (k, "dtheta", name, e, floor)

@@ -6,13 +6,15 @@ Q, Q-hat, loss within 1e-3 relative (bf16 tensor-core mode vs the bf16-emulating
 oracle) / 1e-5 (fp32 check mode vs the exact oracle); gradients and parameter
 updates within 5e-3 / 1e-5 normalised L2, on the whole vector and per tensor.
 """
+import json
+import os
+
 import numpy as np
 import pytest
 
 import oracle as O
 import synth
-from gpu_util import (LAYER_OF, TOL, ambiguous_layer, make_pair, per_tensor_rel_l2, rel_inf, rel_l2,
-                      run_round_both, teacher_force)
+from gpu_util import TOL, make_pair, per_tensor_rel_l2, rel_inf, rel_l2, run_round_both, teacher_force
 
 pytestmark = pytest.mark.gpu
 
@@ -111,9 +113,10 @@ def test_replay_not_ready():
 
 
 def _check_round(gpu, res, math, nA, learners, orc=None, thetas=None):
+    """Every learner's Q / Q-hat / loss / decisions, then G on the whole vector and per tensor at the
+    full tolerance (the oracle's backward teacher-forced to the GPU's ambiguous ReLU decisions, R30)."""
     tol = TOL[math]
     G_ref = np.zeros_like(gpu["G"], dtype=np.float64)
-    kink = 0  # fp32 check mode: deepest layer with an ambiguous ReLU decision (kink rule)
     for j in learners:
         gi, oi = gpu["info"][j], res["learners"][j]
         q, qh = gpu["q"][j]
@@ -130,18 +133,11 @@ def _check_round(gpu, res, math, nA, learners, orc=None, thetas=None):
         assert gi["base_version"] == oi["base_version"]
         if oi["accepted"]:
             G_ref += oi["G"]
-            if orc is not None and thetas is not None:
-                if oi.get("shard") is not None:  # f4: the batch came from the union of the rings
-                    s = O.gather_global([orc.learners[q].ring for q in sorted(orc.learners)], oi["shard"], oi["tau"])[0]
-                else:
-                    s, _, _, _, _ = orc.learners[j].ring.gather(oi["tau"])
-                kink = max(kink, ambiguous_layer(thetas[j], s, nA, mode="exact" if math == "fp32" else "bf16"))
     if np.any(G_ref):
-        relaxed = tol["g_kink"]
         e_all = rel_l2(gpu["G"], G_ref)
-        assert e_all <= (tol["g"] if kink == 0 else relaxed), ("G", e_all, kink)
+        assert e_all <= tol["g"], ("G", e_all, gpu["forced"])
         for name, e in per_tensor_rel_l2(gpu["G"], G_ref, nA).items():
-            assert e <= (tol["g"] if LAYER_OF[name] > kink else relaxed), ("G", name, e, kink)
+            assert e <= tol["g"], ("G", name, e, gpu["forced"])
     else:
         assert not np.any(gpu["G"])
     assert gpu["round"]["n_accepted"] == res["n_accepted"]
@@ -155,11 +151,25 @@ def test_learner_update_parity_c1_teacher_forced(math):
     nA = 4
     g, orc = make_pair(nA=nA, B=32, C=10_000, n_insert=10_000, math=math, target_period=5, outlier_warmup=2)
     tol = TOL[math]
+    context = []  # SURVEY §8(c) context number: the bf16 GPU result against the EXACT oracle (not graded)
     for k in range(10):
         teacher_force(g, orc)
         th_before = orc.theta.copy()
+        tm_before = orc.learners[0].theta_minus.copy()
         gpu, res = run_round_both(g, orc, k, [0])
         _check_round(gpu, res, math, nA, [0], orc, {0: th_before})
+        oi = res["learners"][0]
+        if math == "bf16" and oi["accepted"]:
+            s, s2, a, r, d = orc.learners[0].ring.gather(oi["tau"])
+            Qx, ax = O.qnet_forward(th_before, s, nA, "exact")
+            Qhx, _ = O.qnet_forward(tm_before, s2, nA, "exact")
+            _, _, dQx, lx, _ = O.td_terms(Qx, Qhx, a, r, d, 0.99)
+            Gx = O.qnet_backward(th_before, s, ax, dQx, nA, "exact")
+            context.append({"round": k, "q_rel_inf": rel_inf(gpu["q"][0][0], Qx),
+                            "loss_rel": abs(gpu["info"][0]["loss"] - lx) / abs(lx),
+                            "g_rel_l2": rel_l2(gpu["G"], Gx),
+                            "g_rel_l2_per_tensor": per_tensor_rel_l2(gpu["G"], Gx, nA),
+                            "forced_relu_decisions": gpu["forced"]})
         # theta^+ is stored in fp32 (reading R16): the reference update is the oracle's exact
         # update rounded to the state's precision, fp32(theta0 + dtheta_exact) - theta0
         # The GPU result can differ from that by one fp32 ulp wherever its (tolerance-close) step
@@ -176,6 +186,12 @@ def test_learner_update_parity_c1_teacher_forced(math):
                 floor = np.linalg.norm(ulp[sl]) / max(np.linalg.norm(d_ref[sl]), 1e-300)
                 assert e <= tol["dtheta"] + floor, ("dtheta", k, name, e, floor)
                 off += 0 if name == "all" else int(np.prod(shp))
+    out = os.environ.get("GORILA_CONTEXT_OUT")
+    if context and out:
+        with open(out, "w") as f:
+            json.dump({"what": "bf16 GPU (configs[0], teacher-forced rounds) vs the EXACT fp64 oracle on the "
+                               "same state and batch; SURVEY 8(c) context number, not graded", "rounds": context},
+                      f, indent=1)
 
 
 @pytest.mark.parametrize("math", ["fp32", "bf16"])
@@ -449,7 +465,7 @@ def test_constant_activation_round_parity(math):
 
 def test_error_behaviour_on_a_live_context():
     """include/gorila.h error classes on a live context: bad learner id -> E_RANGE, negative count ->
-    E_SHAPE, count 0 -> OK and no effect, unsorted learner list -> E_INVALID, staleness >= history ->
+    E_SHAPE, count 0 -> OK and no effect, a host action >= n_actions -> E_RANGE, unsorted learner list -> E_INVALID, staleness >= history ->
     E_RANGE; none of them poisons the context (a valid round still matches the oracle afterwards)."""
     from paper_1507_04296_b200 import GorilaError
     from paper_1507_04296_b200 import gorila as G
@@ -466,6 +482,9 @@ def test_error_behaviour_on_a_live_context():
     st = lib.replay_insert(g.h, 0, -1, f.ctypes.data, a.ctypes.data, r.ctypes.data, d.ctypes.data, 0)
     assert G.STATUS[st] == "E_SHAPE"
     assert lib.replay_insert(g.h, 0, 0, None, None, None, None, 0) == 0
+    bad_a = np.full(1, nA, np.uint8)  # host action == n_actions: E_RANGE, the ring is untouched
+    st = lib.replay_insert(g.h, 0, 1, f.ctypes.data, bad_a.ctypes.data, r.ctypes.data, d.ctypes.data, 0)
+    assert G.STATUS[st] == "E_RANGE"
     with pytest.raises(GorilaError) as e:
         g.learner_step([1, 0], 0)
     assert e.value.status == 1
