@@ -73,42 +73,88 @@ def read_peaks():
 
 
 class ClockSampler:
-    """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
+    """SM clocks and throttle reasons sampled during the timed region: NVML (nvidia_ml_py) in a
+    background thread every 20 ms, nvidia-smi's loop mode as the fallback (B200_PROFILING.md clocks
+    line). summary() reports the samples taken while the device was busy with the bench."""
     Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
          "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
          "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+    # nvmlClocksEventReason* bits
+    BITS = {"sw_power_cap": 0x4, "hw_slowdown": 0x8, "sw_thermal_slowdown": 0x20, "hw_thermal_slowdown": 0x40}
 
     def __init__(self, gpu_index):
         self.idx = gpu_index
+        self.rows = []  # (sm_mhz, max_mhz, reasons)
+        self.src = None
         self.proc = None
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        self.stop = None
+        self.f = None
+
+    def _nvml_loop(self, h, nv):
+        import time as _t
+        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        while not self.stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+                try:
+                    r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
+                except AttributeError:
+                    r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
+                self.rows.append((float(sm), float(mx), {k for k, bit in self.BITS.items() if r & bit}))
+            except Exception:
+                pass
+            _t.sleep(0.02)
 
     def __enter__(self):
+        import threading
         try:
+            import pynvml as nv
+            nv.nvmlInit()
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            phys = int(vis.split(",")[self.idx]) if vis and vis.split(",")[0].isdigit() else self.idx
+            h = nv.nvmlDeviceGetHandleByIndex(phys)
+            self.stop = threading.Event()
+            self.th = threading.Thread(target=self._nvml_loop, args=(h, nv), daemon=True)
+            self.th.start()
+            self.src = "nvml"
+            return self
+        except Exception:
+            pass
+        try:
+            self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
             self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.Q,
                                           "--format=csv,noheader,nounits", "-lms", "50"], stdout=self.f,
                                          stderr=subprocess.DEVNULL)
+            self.src = "nvidia-smi"
         except FileNotFoundError:
             self.proc = None
         return self
 
     def __exit__(self, *a):
+        if self.stop is not None:
+            self.stop.set()
+            self.th.join()
         if self.proc:
             self.proc.terminate()
             self.proc.wait()
+            self.f.flush()
+            self.f.seek(0)
+            names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+            for r in [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]:
+                try:
+                    self.rows.append((float(r[1]), float(r[2]),
+                                      {names[i] for i in range(4) if len(r) > 5 + i and r[5 + i].strip() == "Active"}))
+                except (ValueError, IndexError):
+                    pass
 
     def summary(self):
-        self.f.flush()
-        self.f.seek(0)
-        rows = [r.split(",") for r in self.f.read().strip().splitlines() if r.strip()]
-        if not rows:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"], "samples": 0}
-        sm = [float(r[1]) for r in rows if r[1].strip().replace(".", "").isdigit()]
-        mx = [float(r[2]) for r in rows if r[2].strip().replace(".", "").isdigit()]
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        reasons = sorted({names[i] for r in rows for i in range(4) if len(r) > 5 + i and r[5 + i].strip() == "Active"})
-        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
-                "reasons": reasons, "samples": len(rows)}
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"], "samples": 0,
+                    "src": self.src}
+        sm = [r[0] for r in self.rows]
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in self.rows),
+                "reasons": sorted(set().union(*[r[2] for r in self.rows])), "samples": len(self.rows),
+                "src": self.src}
 
 
 def dist_env():
@@ -305,6 +351,9 @@ def main():
         g.ps_apply_shard(k, want_info=False)
         g.sync_target(ids, want_info=False)
 
+    # clocks: sampled from the warm-up through the end-to-end loop (the timed region alone can be
+    # shorter than one sampling period)
+    clk = ClockSampler(local_rank).__enter__()
     k = 0
     for _ in range(args.warmup):
         step(k)
@@ -315,15 +364,14 @@ def main():
     # ---------------- timed region (device time, CUDA events on the launching stream)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches0 = g.kernel_launches()
-    with ClockSampler(local_rank) as clk:
-        stream.synchronize()
-        barrier(world)
-        ev0.record(stream)
-        for _ in range(args.steps):
-            step(k)
-            k += 1
-        ev1.record(stream)
-        stream.synchronize()
+    stream.synchronize()
+    barrier(world)
+    ev0.record(stream)
+    for _ in range(args.steps):
+        step(k)
+        k += 1
+    ev1.record(stream)
+    stream.synchronize()
     barrier(world)
     launches = g.kernel_launches() - launches0
     ms_local = ev0.elapsed_time(ev1)
@@ -364,6 +412,7 @@ def main():
     info = g.round_result(pending)
     e1.record(stream)
     stream.synchronize()
+    clk.__exit__(None, None, None)
     e2e_ms = max_over_ranks(e0.elapsed_time(e1), world)
     e2e_value = world * L * args.e2e_steps / (e2e_ms / 1000.0)
     _ = info
@@ -386,6 +435,17 @@ def main():
             continue
         iso[ph] = g.bench_phase(ph, iters=200)
 
+    # the optimizer's state (theta, m, v, G: 27 MB) stays L2-resident between back-to-back launches;
+    # the same kernel with L2 flushed before every launch (a 512 MB write on the stream) is its DRAM
+    # figure (the round itself runs it warm: the state is touched every step)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device="cuda")
+    cold = []
+    for i in range(21):
+        flush.fill_(i & 0xff)
+        cold.append(g.bench_phase("apply", iters=1))
+    apply_cold_us = float(np.median(cold[1:]))
+    del flush
+
     peaks = read_peaks()
     P = g.P
     n_msg = L if args.ps_mode == "per_message" else 1
@@ -406,7 +466,9 @@ def main():
         t = iso_ms[p] / 1000.0
         if bound == "tensor":
             ach = amount / t / 1e12
-            peak = peaks["tensor"] if args.math == "bf16" else peaks["tensor"] / 16  # fp32 SIMT: not tensor
+            # the phase is timed alone, re-launched back to back: the burst peak (B200_PROFILING.md);
+            # fp32 check mode runs the SIMT engine (no tensor cores): the bf16 peak / 16 as a marker
+            peak = peaks["tensor_burst"] if args.math == "bf16" else peaks["tensor_burst"] / 16
             unit = "TFLOP/s"
         else:
             ach = amount / t / 1e9
@@ -454,6 +516,13 @@ def main():
                                    "gorila_bench_phase; share = that time / device ms per step",
                          "ms_per_launch": dom_roof["ms_per_launch"],
                          "algorithmic_per_launch": dom_roof["algorithmic_per_launch"]},
+            "apply_dram_cold": {"us_per_launch": apply_cold_us,
+                                "achieved_gbs": phase_work("apply", args.batch, args.n_actions, P, esz, n_msg)[1]
+                                / (apply_cold_us * 1e-6) / 1e9,
+                                "peak_gbs": peaks["hbm"],
+                                "note": "k_apply with L2 flushed before each launch (event-timed, median of 20); "
+                                        "phase_rooflines.apply is the same kernel back to back with its 27 MB state "
+                                        "L2-resident, as inside the training loop"},
             "phases_ms_per_step": {p: v for p, v in per_launch_ms.items() if v > 0},
             "phases_isolated_us": iso,
             "phase_rooflines": {p: roof(p) for p in phases if roof(p) is not None},

@@ -81,7 +81,8 @@ typedef struct {
     int32_t n_learners_local;  /* learners (bundles) hosted by this rank, >= 1 */
     int32_t learner_id_base;   /* global id of local learner 0 (ids feed the sampler's Philox counter) */
     int32_t rank, world;       /* this rank; number of ranks = parameter-server shards */
-    const void* nccl_unique_id;/* 128-byte ncclUniqueId broadcast by the caller; NULL iff world == 1 */
+    const void* nccl_unique_id;/* 128-byte ncclUniqueId broadcast by the caller; NULL if world == 1 or
+                                  the caller bootstraps the peer mappings (gorila_peer_connect) */
     void* stream;              /* cudaStream_t every call enqueues on (0 = legacy default stream) */
     void* workspace;           /* device memory, >= gorila_workspace_bytes(cfg), 256-B aligned */
     uint64_t workspace_bytes;
@@ -148,8 +149,10 @@ GORILA_API int64_t gorila_param_count(int32_t n_actions);
 /* Device workspace bytes cfg needs (all learners' replay included). */
 GORILA_API uint64_t gorila_workspace_bytes(const gorila_config* cfg);
 /* Validate cfg, carve the workspace, set theta^+ = theta = theta^- = theta0,
- * m = v = 0, V = 0, last_sync = 0, empty loss stats, empty replays; create the
- * NCCL communicator when world > 1 (collective). Synchronises the stream. */
+ * m = v = 0, V = 0, last_sync = 0, empty loss stats, empty replays. When world > 1
+ * with an NCCL id: create the communicator and map the peers' workspaces (collective);
+ * without one, the caller connects the peers afterwards (gorila_peer_connect).
+ * Synchronises the stream. */
 GORILA_API gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out);
 GORILA_API void gorila_destroy(gorila_ctx* ctx);
 GORILA_API const char* gorila_last_error(void);
@@ -318,6 +321,18 @@ GORILA_API gorila_status gorila_bench_phase(gorila_ctx* ctx, int32_t learner, in
 GORILA_API gorila_status gorila_debug_trace(uint64_t* out64);
 /* Writes a fresh 128-byte ncclUniqueId (rank 0 calls it and broadcasts the bytes). */
 GORILA_API gorila_status gorila_nccl_unique_id(void* out128);
+/* Caller-bootstrapped exchange (world > 1 and config.nccl_unique_id == NULL; e.g. a gloo process
+ * group, or several ranks sharing one GPU, where NCCL cannot form a communicator): after
+ * gorila_init, every rank writes its 128-byte peer record (the CUDA IPC handle of its workspace
+ * allocation + the workspace's offset in it) with gorila_peer_record, the caller all-gathers the
+ * records in rank order, and every rank passes all `world` of them to gorila_peer_connect, which
+ * maps every peer's workspace ("split disjointly": each shard owner then reads the peers'
+ * gradient slices and writes the new replica chunks over NVLink peer memory, k_apply_p2p). Until
+ * then learner_step / ps_apply_shard / replay_sample return E_INVALID. E_CUDA if the workspace
+ * cannot be exported or a peer's cannot be opened (nothing stays mapped; the caller should agree
+ * on the outcome across ranks); E_SHAPE if world differs from config.world; world <= 8. */
+GORILA_API gorila_status gorila_peer_record(gorila_ctx* ctx, void* out128);
+GORILA_API gorila_status gorila_peer_connect(gorila_ctx* ctx, const void* records, int32_t world);
 /* Number of kernels this library launched so far (evidence counter). */
 GORILA_API uint64_t gorila_kernel_launches(gorila_ctx* ctx);
 

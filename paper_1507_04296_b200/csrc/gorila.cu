@@ -1298,9 +1298,19 @@ gorila_status pack_any(gorila_ctx* ctx, const float* theta, void* rt, float* rf,
 
 // ---------------------------------------------------------------- NVLink peer mappings
 // Every rank maps every peer's workspace (same carve on every rank, so a peer's buffer is at the
-// same offset): IPC handle of the workspace's allocation + the workspace offset inside it,
-// exchanged with one NCCL all-gather. Any failure leaves p2p off (NCCL collectives are used).
-bool p2p_setup(gorila_ctx* ctx) {
+// same offset): IPC handle of the workspace's allocation + the workspace offset inside it. The
+// 128-byte records are exchanged either with one NCCL all-gather (gorila_init with an NCCL id) or by
+// the caller (gorila_peer_record / gorila_peer_connect: any process group, e.g. gloo, which also
+// covers several ranks sharing one GPU, where NCCL cannot form a communicator).
+struct PeerRec {
+    cudaIpcMemHandle_t h;
+    uint64_t off;
+    int32_t ok, dev;
+    uint8_t pad[128 - sizeof(cudaIpcMemHandle_t) - 16];
+};
+static_assert(sizeof(PeerRec) == 128, "record size");
+
+void peer_record(gorila_ctx* ctx, PeerRec* mine) {
     typedef CUresult (*GetRange)(CUdeviceptr*, size_t*, CUdeviceptr);
     static GetRange get_range = [] {
         void* f = nullptr;
@@ -1310,32 +1320,30 @@ bool p2p_setup(gorila_ctx* ctx) {
             f = nullptr;
         return reinterpret_cast<GetRange>(f);
     }();
-    const int W = ctx->W, r = ctx->rank;
-    struct Rec {
-        cudaIpcMemHandle_t h;
-        uint64_t off;
-        int32_t ok, dev;
-        uint8_t pad[128 - sizeof(cudaIpcMemHandle_t) - 16];
-    };
-    static_assert(sizeof(Rec) == 128, "record size");
-    Rec mine;
-    memset(&mine, 0, sizeof(mine));
+    memset(mine, 0, sizeof(*mine));
     ctx->ws_local = (uint8_t*)ctx->cfg.workspace;
     CUdeviceptr base = 0;
     size_t size = 0;
-    mine.ok = get_range && get_range(&base, &size, (CUdeviceptr)ctx->ws_local) == CUDA_SUCCESS &&
-              cudaIpcGetMemHandle(&mine.h, (void*)base) == cudaSuccess;
+    mine->ok = get_range && get_range(&base, &size, (CUdeviceptr)ctx->ws_local) == CUDA_SUCCESS &&
+               cudaIpcGetMemHandle(&mine->h, (void*)base) == cudaSuccess;
     cudaGetLastError();
-    mine.off = (uint64_t)((CUdeviceptr)ctx->ws_local - base);
-    cudaGetDevice(&mine.dev);
-    uint8_t* dbuf = reinterpret_cast<uint8_t*>(ctx->tmp_int);  // scratch: [W][128 B] records
-    if (cudaMemcpyAsync(dbuf + (size_t)r * 128, &mine, 128, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
-        ncclAllGather(dbuf + (size_t)r * 128, dbuf, 128, ncclChar, ctx->comm, ctx->stream) != ncclSuccess)
-        return false;
-    std::vector<Rec> all(W);
-    if (cudaMemcpyAsync(all.data(), dbuf, (size_t)W * 128, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
-        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
-        return false;
+    mine->off = (uint64_t)((CUdeviceptr)ctx->ws_local - base);
+    cudaGetDevice(&mine->dev);
+}
+
+void peer_close(gorila_ctx* ctx) {
+    for (int q = 0; q < MAX_W; ++q)
+        if (ctx->peer_raw[q]) {
+            cudaIpcCloseMemHandle(ctx->peer_raw[q]);
+            ctx->peer_raw[q] = nullptr;
+            ctx->peer_ws[q] = nullptr;
+        }
+    cudaGetLastError();
+}
+
+// open every peer's record (all: W records in rank order); false (nothing left open) on any failure
+bool peer_open(gorila_ctx* ctx, const PeerRec* all) {
+    const int W = ctx->W, r = ctx->rank;
     bool ok = true;
     for (int q = 0; q < W; ++q) ok = ok && all[q].ok;
     for (int q = 0; q < W && ok; ++q) {
@@ -1349,7 +1357,24 @@ bool p2p_setup(gorila_ctx* ctx) {
         ctx->peer_raw[q] = p;
         ctx->peer_ws[q] = (uint8_t*)p + all[q].off;
     }
-    // every rank must agree: all-reduce the verdict (min)
+    if (!ok) peer_close(ctx);
+    return ok;
+}
+
+// NCCL bootstrap: records all-gathered on the library's communicator, the verdict all-reduced (min)
+bool p2p_setup(gorila_ctx* ctx) {
+    const int W = ctx->W, r = ctx->rank;
+    PeerRec mine;
+    peer_record(ctx, &mine);
+    uint8_t* dbuf = reinterpret_cast<uint8_t*>(ctx->tmp_int);  // scratch: [W][128 B] records
+    if (cudaMemcpyAsync(dbuf + (size_t)r * 128, &mine, 128, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
+        ncclAllGather(dbuf + (size_t)r * 128, dbuf, 128, ncclChar, ctx->comm, ctx->stream) != ncclSuccess)
+        return false;
+    std::vector<PeerRec> all(W);
+    if (cudaMemcpyAsync(all.data(), dbuf, (size_t)W * 128, cudaMemcpyDeviceToHost, ctx->stream) != cudaSuccess ||
+        cudaStreamSynchronize(ctx->stream) != cudaSuccess)
+        return false;
+    const bool ok = peer_open(ctx, all.data());
     int32_t* vb = reinterpret_cast<int32_t*>(dbuf);
     const int32_t v = ok ? 1 : 0;
     if (cudaMemcpyAsync(vb, &v, 4, cudaMemcpyHostToDevice, ctx->stream) != cudaSuccess ||
@@ -1358,15 +1383,7 @@ bool p2p_setup(gorila_ctx* ctx) {
     int32_t all_ok = 0;
     cudaMemcpyAsync(&all_ok, vb, 4, cudaMemcpyDeviceToHost, ctx->stream);
     cudaStreamSynchronize(ctx->stream);
-    if (!all_ok) {
-        for (int q = 0; q < MAX_W; ++q)
-            if (ctx->peer_raw[q]) {
-                cudaIpcCloseMemHandle(ctx->peer_raw[q]);
-                ctx->peer_raw[q] = nullptr;
-                ctx->peer_ws[q] = nullptr;
-            }
-        cudaGetLastError();
-    }
+    if (!all_ok) peer_close(ctx);
     return all_ok != 0;
 }
 // rank q's copy of a workspace pointer
@@ -1622,6 +1639,44 @@ gorila_status gorila_nccl_unique_id(void* out128) {
 
 static cudaError_t stage_alloc(gorila_ctx* ctx);
 
+// f4: the shard table, every rank's rings at their address in this process (after the peer mappings)
+static cudaError_t shard_table(gorila_ctx* ctx) {
+    if (!ctx->replay_global) return cudaSuccess;
+    std::vector<ShardPtrs> tab;
+    for (int q = 0; q < ctx->W; ++q)
+        for (const Learner& l : ctx->learners)
+            tab.push_back({peer_ptr(ctx, q, l.frames), peer_ptr(ctx, q, l.a), peer_ptr(ctx, q, l.r),
+                           peer_ptr(ctx, q, l.d), peer_ptr(ctx, q, l.n_dev)});
+    cudaError_t e = cudaMemcpyAsync(ctx->shard_tab, tab.data(), sizeof(ShardPtrs) * tab.size(),
+                                    cudaMemcpyHostToDevice, ctx->stream);
+    return e ? e : cudaStreamSynchronize(ctx->stream);
+}
+
+// world > 1: the exchange is set up (peer mappings, or the NCCL fallback)
+static bool exchange_ready(const gorila_ctx* ctx) { return ctx->W == 1 || ctx->p2p || ctx->comm; }
+
+gorila_status gorila_peer_record(gorila_ctx* ctx, void* out128) {
+    if (!ctx || !out128) return fail(GORILA_E_INVALID, "null argument");
+    PeerRec r;
+    peer_record(ctx, &r);
+    memcpy(out128, &r, sizeof(r));
+    if (!r.ok) return fail(GORILA_E_CUDA, "cannot export the workspace allocation (cudaIpcGetMemHandle)");
+    return GORILA_OK;
+}
+
+gorila_status gorila_peer_connect(gorila_ctx* ctx, const void* records, int32_t world) {
+    if (!ctx || !records) return fail(GORILA_E_INVALID, "null argument");
+    if (ctx->W == 1) return GORILA_OK;
+    if (world != ctx->W) return fail(GORILA_E_SHAPE, "records must hold world entries");
+    if (ctx->comm || ctx->p2p) return fail(GORILA_E_INVALID, "peers already connected");
+    if (ctx->W > MAX_W) return fail(GORILA_E_INVALID, "peer-memory exchange: world <= 8");
+    if (!peer_open(ctx, reinterpret_cast<const PeerRec*>(records)))
+        return fail(GORILA_E_CUDA, "cudaIpcOpenMemHandle of a peer's workspace failed");
+    ctx->p2p = true;
+    CU(shard_table(ctx));
+    return GORILA_OK;
+}
+
 gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     if (!cfg || !out) return fail(GORILA_E_INVALID, "null argument");
     *out = nullptr;
@@ -1630,7 +1685,6 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     if (cfg->replay_capacity < 2) return fail(GORILA_E_INVALID, "replay_capacity must be >= 2");
     if (cfg->n_learners_local < 1) return fail(GORILA_E_INVALID, "n_learners_local must be >= 1");
     if (cfg->world < 1 || cfg->rank < 0 || cfg->rank >= cfg->world) return fail(GORILA_E_INVALID, "bad rank/world");
-    if (cfg->world > 1 && !cfg->nccl_unique_id) return fail(GORILA_E_INVALID, "world > 1 needs nccl_unique_id");
     if (cfg->math != GORILA_MATH_FP32 && cfg->math != GORILA_MATH_BF16) return fail(GORILA_E_INVALID, "bad math");
     if (cfg->optimizer != GORILA_OPT_RMSPROP && cfg->optimizer != GORILA_OPT_ADAGRAD)
         return fail(GORILA_E_INVALID, "bad optimizer");
@@ -1738,7 +1792,9 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     if ((s = pack_any(ctx, ctx->theta, ctx->rep_t[0], ctx->rep_f[0], nullptr, ctx->Vhist)) != GORILA_OK) return s;
     for (auto& l : ctx->learners)
         if ((s = pack_any(ctx, ctx->theta, l.tminus_t, l.tminus_f, nullptr, nullptr)) != GORILA_OK) return s;
-    if (cfg->world > 1) {
+    if (cfg->world > 1 && cfg->world > MAX_W && (!cfg->nccl_unique_id || ctx->per_msg || ctx->replay_global))
+        return fail(GORILA_E_INVALID, "world > 8 runs only the NCCL aggregate exchange (needs nccl_unique_id)");
+    if (cfg->world > 1 && cfg->nccl_unique_id) {
         ncclUniqueId id;
         memcpy(&id, cfg->nccl_unique_id, sizeof(id));
         NC(ncclCommInitRank(&ctx->comm, cfg->world, id, cfg->rank));
@@ -1751,14 +1807,8 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
             return fail(GORILA_E_INVALID, "global replay needs the peer-memory mapping (world > 1)");
         }
     }
-    if (ctx->replay_global) {  // f4: the shard table, every rank's rings at their address in this process
-        std::vector<ShardPtrs> tab;
-        for (int q = 0; q < cfg->world; ++q)
-            for (const Learner& l : ctx->learners)
-                tab.push_back({peer_ptr(ctx, q, l.frames), peer_ptr(ctx, q, l.a), peer_ptr(ctx, q, l.r),
-                               peer_ptr(ctx, q, l.d), peer_ptr(ctx, q, l.n_dev)});
-        CU(cudaMemcpyAsync(ctx->shard_tab, tab.data(), sizeof(ShardPtrs) * tab.size(), cudaMemcpyHostToDevice, st));
-    }
+    // world > 1 without an NCCL id: the caller exchanges the peer records (gorila_peer_connect)
+    if (cfg->world == 1 || ctx->p2p) CU(shard_table(ctx));
     CU(stage_alloc(ctx));
     ctx->ring_slot = (RING_HDR + std::min(ctx->L, RING_MAXL) * (int)sizeof(DevLearnerInfo) + 63) / 64 * 64;
     CU(cudaHostAlloc((void**)&ctx->ring_host, (size_t)gorila_ctx::kRing * ctx->ring_slot, cudaHostAllocMapped));
@@ -1790,8 +1840,7 @@ void gorila_destroy(gorila_ctx* ctx) {
     for (auto& kv : ctx->graphs) cudaGraphExecDestroy(kv.second);
     for (auto& kv : ctx->graph_marks)
         for (auto& m : kv.second) cudaEventDestroy(m.second);
-    for (int q = 0; q < MAX_W; ++q)
-        if (ctx->peer_raw[q]) cudaIpcCloseMemHandle(ctx->peer_raw[q]);
+    peer_close(ctx);
     for (int i = 0; i < gorila_ctx::kStage; ++i) {
         if (ctx->stage_ev[i]) {
             cudaEventSynchronize(ctx->stage_ev[i]);
@@ -1920,6 +1969,7 @@ gorila_status replay_sample(gorila_ctx* ctx, int32_t learner, uint64_t round, in
                             uint8_t* s2_out, uint8_t* a_out, float* r_out, uint8_t* d_out) {
     gorila_status s = check_learner(ctx, learner);
     if (s != GORILA_OK) return s;
+    if (!exchange_ready(ctx)) return fail(GORILA_E_INVALID, "world > 1: connect the peers first (gorila_peer_connect)");
     Learner& l = ctx->learners[learner];
     const int64_t size = std::min<int64_t>(l.n_host, ctx->cfg.replay_capacity);
     if (size - 1 < std::max<int64_t>(1, ctx->cfg.min_replay)) return fail(GORILA_E_NOT_READY, "replay not ready");
@@ -1998,6 +2048,7 @@ gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, 
                            const int32_t* staleness, gorila_learner_info* info_out) {
     if (!ctx) return fail(GORILA_E_INVALID, "null context");
     if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned");
+    if (!exchange_ready(ctx)) return fail(GORILA_E_INVALID, "world > 1: connect the peers first (gorila_peer_connect)");
     if (!learners || n < 1 || n > ctx->L) return fail(GORILA_E_SHAPE, "bad learner list");
     for (int i = 0; i < n; ++i) {
         if (learners[i] < 0 || learners[i] >= ctx->L) return fail(GORILA_E_RANGE, "learner id out of range");
@@ -2187,6 +2238,7 @@ gorila_status ps_apply_p2p(gorila_ctx* ctx, uint64_t round, gorila_round_info* i
 gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info* info_out) {
     if (!ctx) return fail(GORILA_E_INVALID, "null context");
     if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned");
+    if (!exchange_ready(ctx)) return fail(GORILA_E_INVALID, "world > 1: connect the peers first (gorila_peer_connect)");
     cudaStream_t st = ctx->stream;
     const int W = ctx->W, r = ctx->rank;
     float* gsl = ctx->G + (int64_t)r * ctx->q;

@@ -65,7 +65,7 @@ EXPORTS = ["gorila_param_count", "gorila_workspace_bytes", "gorila_init", "goril
            "gorila_profile_phase_count", "gorila_profile_phase_name", "gorila_nccl_unique_id", "gorila_round",
            "gorila_round_async", "gorila_round_post", "gorila_round_fetch",
            "gorila_bench_phase", "gorila_debug_trace", "gorila_capture_activations",
-           "gorila_get_learner_activation"]
+           "gorila_get_learner_activation", "gorila_peer_record", "gorila_peer_connect"]
 
 
 def load(build_if_missing=True):
@@ -101,6 +101,8 @@ def load(build_if_missing=True):
     L.gorila_get_q.argtypes = [P, i32, P, P]
     L.gorila_get_activation.argtypes = [P, i32, P, u64]
     L.gorila_capture_activations.argtypes = [P, i32]
+    L.gorila_peer_record.argtypes = [P, P]
+    L.gorila_peer_connect.argtypes = [P, P, i32]
     L.gorila_get_learner_activation.argtypes = [P, i32, i32, P, u64]
     L.gorila_round_post.argtypes = [P, P, i32, u64, P]
     L.gorila_round_fetch.argtypes = [P, u64, P, P, P]
@@ -196,7 +198,28 @@ class Gorila:
         h = ctypes.c_void_p()
         _check(L.gorila_init(ctypes.byref(cfg), ctypes.byref(h)))
         self.h = h
+        if world > 1 and nccl_unique_id is None:
+            self._connect_peers()
         self._info = (LearnerInfo * max(1, n_learners_local))()
+
+    def _connect_peers(self):
+        """Caller-bootstrapped peer mappings (include/gorila.h gorila_peer_connect): the 128-byte
+        records all-gathered over torch.distributed's default process group (any backend: gloo works
+        for several ranks sharing one GPU); every rank raises if any rank failed."""
+        import torch.distributed as dist
+        L = load()
+        rec = ctypes.create_string_buffer(128)
+        st = L.gorila_peer_record(self.h, rec)
+        recs = [None] * dist.get_world_size()
+        dist.all_gather_object(recs, rec.raw if st == 0 else None)
+        ok = all(r is not None for r in recs)
+        st2 = L.gorila_peer_connect(self.h, ctypes.create_string_buffer(b"".join(recs), 128 * len(recs)),
+                                    len(recs)) if ok else 1
+        verdict = [None] * dist.get_world_size()
+        dist.all_gather_object(verdict, st2 == 0)
+        if not all(verdict):
+            msg = L.gorila_last_error().decode() if st2 != 0 else "a peer failed to connect"
+            raise GorilaError(st2 if st2 != 0 else 5, "peer mapping failed: " + msg)
 
     def close(self):
         if self.h:
