@@ -1010,7 +1010,17 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             p.g4 = g4;
             p.bf16 = !fp32v;
         }
-        launch(ctx, k_fc5_td, dim3(fc5_fused ? B : std::min(B, 2 * 148)), dim3(512), 0, p);
+        if (B >= 256 && !fc5_fused) {  // large batch: one warp per sample, W5 in shared memory
+            const size_t smem = (size_t)(2 * nA * FC4_OUT + 64) * sizeof(float);
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_fc5_td_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * 32 * FC4_OUT + 64) * 4);
+                attr = true;
+            }
+            launch(ctx, k_fc5_td_wide, dim3(std::min((B + 31) / 32, 148)), dim3(256), smem, p);
+        } else {
+            launch(ctx, k_fc5_td, dim3(fc5_fused ? B : std::min(B, 2 * 148)), dim3(512), 0, p);
+        }
     }
     }
     mark(ctx, PH_FC5F);
@@ -1019,8 +1029,10 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     // fc5 bwd: dW5, db5 into G; g4 = mask(dQ W5)
     {
         const int nch = (B + fc5_rows(B) - 1) / fc5_rows(B);
-        launch(ctx, k_fc5_bwd<T>, dim3(2 * nch + std::min(2 * 148, (B * FC4_OUT + 255) / 256)), dim3(256), 0,
-               (const float*)ctx->dQ, (const float*)a4, (const float*)(rf + RL.w5), B, nA, ctx->part5, nch, g4);
+        const int g4_blocks = (B * (FC4_OUT / 4) + 255) / 256;  // one thread per (sample, 4 columns)
+        launch(ctx, k_fc5_bwd<T>, dim3(2 * nch + g4_blocks), dim3(256), 0,
+               (const float*)ctx->dQ, (const float*)a4, (const float*)(rf + RL.w5), B, nA, ctx->part5, nch, g4,
+               (const uint8_t*)ctx->sa);
     }
     }
     mark(ctx, PH_FC5B);

@@ -440,6 +440,115 @@ __global__ void __launch_bounds__(512) k_fc5_td(Fc5TdParams p) {
     }
 }
 
+// Large batches (B >= 256): the same fc5 forward + TD + decisions with one warp per sample (both
+// nets) instead of all warps on one sample at a time. W5 / W5t sit in shared memory (loaded before
+// the PDL wait: written two or more kernels back); a warp takes four samples at a time, so each W5
+// element read from shared memory feeds four FMAs. The last block sums the per-sample terms in
+// sample order and decides (td_decide), as k_fc5_td.
+__global__ void __launch_bounds__(256) k_fc5_td_wide(Fc5TdParams p) {
+    const TdParams& t = p.td;
+    const int nA = t.nA;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    extern __shared__ __align__(16) float sw[];  // [2][nA][512] weights, then [2][32] biases
+    __shared__ __align__(8) uint64_t wbar;
+    if (threadIdx.x == 0) {  // the two W5 matrices: one bulk copy each (contiguous [nA][512] fp32)
+        mbar_init(&wbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        mbar_expect_tx(&wbar, 2u * nA * FC4_OUT * 4u);
+        bulk_load(smem_u32(sw), p.w5, nA * FC4_OUT * 4u, &wbar);
+        bulk_load(smem_u32(sw + nA * FC4_OUT), p.w5t, nA * FC4_OUT * 4u, &wbar);
+    }
+    float* sb = sw + 2 * nA * FC4_OUT;
+    if (threadIdx.x < 64) sb[threadIdx.x] = (threadIdx.x & 31) < nA ? (threadIdx.x < 32 ? p.b5 : p.b5t)[threadIdx.x & 31] : 0.f;
+    __syncthreads();
+    mbar_wait(&wbar, 0);
+    pdl_wait();
+    pdl_trigger();
+    // four samples per warp at a time: every W5 element read from shared memory feeds four FMAs
+    constexpr int S = 4;
+    __shared__ float qs[8][2][S][32];  // [warp][net][sample][action]
+    for (int b0 = (blockIdx.x * 8 + warp) * S; b0 < t.B; b0 += gridDim.x * 8 * S) {
+#pragma unroll
+        for (int z = 0; z < 2; ++z) {
+            float xv[S][FC4_OUT / 32];
+#pragma unroll
+            for (int s = 0; s < S; ++s) {
+                const float* x = (z ? p.t4 : p.a4) + (int64_t)min(b0 + s, t.B - 1) * FC4_OUT;
+#pragma unroll
+                for (int k = 0; k < FC4_OUT / 32; ++k) xv[s][k] = x[lane + 32 * k];
+            }
+            const float* w = sw + z * nA * FC4_OUT;
+            for (int a = 0; a < nA; ++a) {
+                float acc[S] = {};
+#pragma unroll
+                for (int k = 0; k < FC4_OUT / 32; ++k) {
+                    const float wk = w[a * FC4_OUT + lane + 32 * k];
+#pragma unroll
+                    for (int s = 0; s < S; ++s) acc[s] = fmaf(xv[s][k], wk, acc[s]);
+                }
+#pragma unroll
+                for (int s = 0; s < S; ++s) {
+                    const float v = warp_sum(acc[s]);
+                    if (lane == 0) qs[warp][z][s][a] = v;
+                }
+            }
+        }
+        __syncwarp();
+#pragma unroll
+        for (int s = 0; s < S; ++s) {
+            const int b = b0 + s;
+            if (b >= t.B) break;
+            const float qv = lane < nA ? qs[warp][0][s][lane] + sb[lane] : 0.f;
+            const float qh = lane < nA ? qs[warp][1][s][lane] + sb[32 + lane] : -INFINITY;
+            if (lane < nA) {
+                const_cast<float*>(t.Q)[b * nA + lane] = qv;
+                const_cast<float*>(t.Qhat)[b * nA + lane] = qh;
+            }
+            const float mx = warp_max(qh);
+            const int ab = t.a[b];
+            const float y = t.d[b] ? t.r[b] : t.r[b] + t.gamma * mx;  // Alg.1
+            const float delta = y - __shfl_sync(0xffffffffu, qv, ab);
+            if (lane < nA) {
+                const float cl = fminf(fmaxf(delta, -1.f), 1.f);  // reading R3
+                t.dQ[b * nA + lane] = (lane == ab) ? -cl / (float)t.B : 0.f;
+            }
+            if (lane == 0) {
+                p.per_sample[2 * b] = delta * delta;
+                p.per_sample[2 * b + 1] = fabsf(delta);
+            }
+        }
+        __syncwarp();
+    }
+    __shared__ unsigned int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = (atomicAdd(p.counter, 1u) == gridDim.x - 1);
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    __shared__ float s_sq[8], s_ab[8];
+    __shared__ int s_keep;
+    float sq = 0.f, sa = 0.f;
+    for (int i = threadIdx.x; i < t.B; i += blockDim.x) {
+        sq += __ldcg(&p.per_sample[2 * i]);
+        sa += __ldcg(&p.per_sample[2 * i + 1]);
+    }
+    sq = warp_sum(sq);
+    sa = warp_sum(sa);
+    if (lane == 0) {
+        s_sq[warp] = sq;
+        s_ab[warp] = sa;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        s_keep = td_decide(t, s_sq, s_ab, 8);
+        *p.counter = 0;
+    }
+    __syncthreads();
+    if (!s_keep)
+        for (int e = threadIdx.x; e < t.B * nA; e += blockDim.x) t.dQ[e] = 0.f;
+}
+
 __global__ void k_mark_not_ready(DevLearnerInfo* info, const LearnerStats* st) {
     pdl_wait();
     pdl_trigger();
@@ -465,7 +574,7 @@ __host__ __device__ constexpr int fc5_rows(int B) {
 template <typename T>
 __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, const float* __restrict__ a4,
                                                  const float* __restrict__ w5, int B, int nA, float* __restrict__ part,
-                                                 int n_chunks, T* __restrict__ g4) {
+                                                 int n_chunks, T* __restrict__ g4, const uint8_t* __restrict__ act) {
     // a4 (fc4's output) and W5 (the replica) were written two or more kernels back: loaded before
     // the wait (PDL: complete once this grid runs); only dQ comes from the kernel just before
     if ((int)blockIdx.x < 2 * n_chunks) {  // (chunk, column half)
@@ -483,12 +592,13 @@ __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, c
 #pragma unroll
         for (int a = 0; a < 32; ++a) acc[a] = 0.f;
         const float* xs = a4 + (int64_t)b0 * FC4_OUT + n;
-        for (int bb = 0; bb < nb; bb += 8) {
-            float x[8];  // eight rows' loads in flight before the FMAs (the first eight prefetched)
+        for (int bb = 0; bb < nb; bb += 16) {
+            float x[16];  // sixteen rows' loads in flight before the FMAs (the first eight prefetched)
 #pragma unroll
-            for (int u = 0; u < 8; ++u) x[u] = bb == 0 ? xpre[u] : bb + u < nb ? xs[(int64_t)(bb + u) * FC4_OUT] : 0.f;
+            for (int u = 0; u < 16; ++u)
+                x[u] = (bb == 0 && u < 8) ? xpre[u] : bb + u < nb ? xs[(int64_t)(bb + u) * FC4_OUT] : 0.f;
 #pragma unroll
-            for (int u = 0; u < 8; ++u) {
+            for (int u = 0; u < 16; ++u) {
                 if (bb + u >= nb) break;
                 const float* q = dq + (bb + u) * nA;
 #pragma unroll
@@ -507,29 +617,23 @@ __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, c
         }
         return;
     }
-    const int n_g = B * FC4_OUT, nblk = gridDim.x - 2 * n_chunks;
-    const int f0 = (blockIdx.x - 2 * n_chunks) * blockDim.x + threadIdx.x;
-    float wv[32], x0 = 0.f;  // this thread's first output: its W5 column and a4 value, before the wait
-    {
-        const int n = f0 % FC4_OUT;
-#pragma unroll
-        for (int a = 0; a < 32; ++a) wv[a] = a < nA ? w5[a * FC4_OUT + n] : 0.f;
-        if (f0 < n_g) x0 = a4[f0];
-    }
+    // g4[b][n] = mask(dQ[b][a_b] W5[a_b][n]): dQ has one nonzero entry per sample (the action taken,
+    // k_fc5_td), so the sum over actions is that single product (exact: the other terms are zeros).
+    // One thread per (sample, 4 columns).
     pdl_wait();
     pdl_trigger();
-    for (int f = f0; f < n_g; f += nblk * blockDim.x) {
-        const int b = f / FC4_OUT, n = f - b * FC4_OUT;
-        float acc = 0.f;
-        if (f == f0) {
+    const int64_t n_g4 = (int64_t)B * (FC4_OUT / 4), nblk = gridDim.x - 2 * n_chunks;
+    for (int64_t f = (blockIdx.x - 2 * n_chunks) * (int64_t)blockDim.x + threadIdx.x; f < n_g4; f += nblk * blockDim.x) {
+        const int b = (int)(f / (FC4_OUT / 4)), n = (int)(f - (int64_t)b * (FC4_OUT / 4)) * 4;
+        const int ab = act[b];
+        const float dq = dQ[b * nA + ab];
+        const float4 w = *reinterpret_cast<const float4*>(w5 + ab * FC4_OUT + n);
+        const float4 x = *reinterpret_cast<const float4*>(a4 + (int64_t)b * FC4_OUT + n);
+        const float v[4] = {x.x > 0.f ? dq * w.x : 0.f, x.y > 0.f ? dq * w.y : 0.f, x.z > 0.f ? dq * w.z : 0.f,
+                            x.w > 0.f ? dq * w.w : 0.f};
+        T* dst = g4 + (int64_t)b * FC4_OUT + n;
 #pragma unroll
-            for (int a = 0; a < 32; ++a)
-                if (a < nA) acc = fmaf(dQ[b * nA + a], wv[a], acc);
-        } else {
-            for (int a = 0; a < nA; ++a) acc = fmaf(dQ[b * nA + a], w5[a * FC4_OUT + n], acc);
-        }
-        const float x = f == f0 ? x0 : a4[f];
-        g4[f] = fromf<T>(x > 0.f ? acc : 0.f);
+        for (int c = 0; c < 4; ++c) dst[c] = fromf<T>(v[c]);
     }
 }
 

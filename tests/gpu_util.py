@@ -48,17 +48,19 @@ def make_pair(nA=4, B=32, C=2000, n_insert=2000, math="fp32", L=1, history=2, p_
     return g, orc
 
 
-def gpu_acts(g, learner=None):
+def gpu_acts(g, learner=None, rows=None):
     """The GPU's a1..a4 of its last learner step in the oracle's layout ([B][a1|a2|a3|a4], CHW per
     sample, float64): learner None = the shared scratch (the last learner that ran), else learner's
-    captured copy (Gorila.capture_activations)."""
+    captured copy (Gorila.capture_activations). rows: only these samples."""
     parts = []
     for name, shp in ACT_LAYERS:
         x = g.get_activation(name) if learner is None else g.get_learner_activation(learner, name)
         x = x.reshape((g.batch,) + shp)
+        if rows is not None:
+            x = x[rows]
         if len(shp) == 3:  # NHWC -> CHW
             x = x.transpose(0, 3, 1, 2)
-        parts.append(x.reshape(g.batch, -1))
+        parts.append(x.reshape(x.shape[0], -1))
     return np.concatenate(parts, axis=1).astype(np.float64)
 
 

@@ -18,6 +18,7 @@ ap.add_argument("--steps", type=int, default=3000)
 ap.add_argument("--capacity", type=int, default=200_000)
 ap.add_argument("--reps", type=int, default=3)
 ap.add_argument("--math", default="bf16")
+ap.add_argument("--phases", default="", help="comma list of phases to time in isolation (gorila_bench_phase)")
 a = ap.parse_args()
 st = torch.cuda.Stream()
 torch.cuda.set_stream(st)
@@ -44,4 +45,6 @@ ap_us = g.bench_phase("apply", iters=200)
 tw_us = g.bench_phase("conv1_fwd", iters=200)
 print(f"B={a.batch} us/step {min(res):.2f} (reps {' '.join(f'{r:.2f}' for r in res)}) "
       f"updates/s {1e6 / min(res):.0f} apply(iso) {ap_us:.2f} us tower(iso) {tw_us:.2f} us knobs {knobs}", flush=True)
+if a.phases:
+    print({ph: round(g.bench_phase(ph, iters=50), 2) for ph in a.phases.split(",")}, flush=True)
 g.close()
