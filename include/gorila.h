@@ -104,11 +104,18 @@ typedef struct {
                                   scheduled staleness s < H (deterministic fixed-staleness mode) */
     const float* theta0;       /* host, canonical layout, P floats: theta^+ = theta = theta^- at init (Alg.1) */
     int32_t ps_mode;           /* 0: aggregate, one optimizer step per round on the mean of the accepted
-                                  gradients (reading R12); 1: per message (NEXT row f1, reading R32): every
-                                  accepted learner gradient is its own optimizer step, in ascending global
-                                  learner id, V += 1 each. 1 needs world == 1 or the
-                                  peer-memory exchange (E_INVALID on the NCCL fallback) and
-                                  world * n_learners_local <= 64. */
+                                  gradients (reading R12); 1: per message (NEXT row f1, readings R32, R37):
+                                  the learners' gradients arrive at the PS in ascending global learner id;
+                                  each is discarded if stale against the version at its arrival (V0 + the
+                                  messages applied before it), else applied as its own
+                                  optimizer step (V += 1), after which every learner's target net
+                                  syncs if V >= last + N, possibly inside the round: theta^- is
+                                  theta^+ at that version. In this mode the stale / accepted fields of
+                                  learner_step's info are provisional (accepted = message sent); the final
+                                  decisions are in gorila_round's info and after ps_apply_shard, which also
+                                  takes every learner's sync decisions (sync_target only reports them,
+                                  unless force). 1 needs world == 1 or the peer-memory exchange (E_INVALID
+                                  on the NCCL fallback) and world * n_learners_local <= 64. */
     int32_t replay_mode;       /* 0: local, each learner samples its own ring (P:140 first form);
                                   1: global (NEXT row f4, reading R36): every minibatch is drawn uniformly
                                   from the union D of all learners' rings on all ranks ("a global replay

@@ -422,7 +422,7 @@ class GorilaOracle:
         per = {}
         G_sum = np.zeros_like(self.theta)
         n_acc = 0
-        messages = []  # accepted gradients in ascending learner id (f1)
+        messages = []  # learners with a message (not rejected), ascending id (f1)
         for j in sorted(self.learners):
             L = self.learners[j]
             # O1
@@ -457,8 +457,8 @@ class GorilaOracle:
             thr = L.stats.mu + cfg.outlier_k * np.sqrt(L.stats.var)
             stats_count_before = L.stats.count
             L.stats.update(ell, cfg.outlier_beta)
-            # O9
-            stale = is_stale(V0, b_j, cfg.max_staleness)
+            # O9 (per-message mode: judged at the PS, message by message, below)
+            stale = is_stale(V0, b_j, cfg.max_staleness) if cfg.ps_mode != "per_message" else False
             info.update(tau=tau, shard=shard, Q=Q, Qhat=Qhat, y=y, delta=delta, loss=loss, abs_loss=ell,
                         threshold=thr, stats_count_before=stats_count_before,
                         rejected_outlier=rejected, stale=stale, mu=L.stats.mu, var=L.stats.var,
@@ -467,22 +467,44 @@ class GorilaOracle:
             if not rejected:
                 G = qnet_backward(theta_j, s, acts, dQ, cfg.n_actions, cfg.mode)
                 info["G"] = G
-                if not stale:
+                if cfg.ps_mode == "per_message":
+                    messages.append(j)
+                elif not stale:
                     info["accepted"] = True
                     G_sum += G
                     n_acc += 1
-                    messages.append(G)
             per[j] = info
-        # f1 (R32): every accepted message is its own optimizer step, in ascending learner id
+        synced = {j: False for j in self.learners}
+        # f1 (R32, R37): the messages arrive at the PS one by one in ascending learner id. Each is judged
+        # against the PS version when it arrives ("older than a threshold"; V counts the
+        # updates applied so far), applied as its own optimizer step if fresh (V += 1), and
+        # after every step each learner's target net syncs if V >= last + N ("after every N
+        # gradient updates in the central parameter server") -- possibly inside the round.
         if cfg.ps_mode == "per_message":
-            for G in messages:
+            V = V0
+            for j in messages:
+                info = per[j]
+                info["stale"] = is_stale(V, info["base_version"], cfg.max_staleness)
+                info["version_at_arrival"] = V
+                if info["stale"]:
+                    continue
+                info["accepted"] = True
+                G = info["G"]
                 for lo, hi in shard_bounds(len(self.theta), cfg.n_shards):
                     if cfg.optimizer == "rmsprop":
                         rmsprop_apply(self.theta[lo:hi], self.m[lo:hi], self.v[lo:hi], G[lo:hi],
                                       cfg.lr, cfg.rms_rho, cfg.rms_eps)
                     else:
                         adagrad_apply(self.theta[lo:hi], self.v[lo:hi], G[lo:hi], cfg.lr, cfg.ada_eps)
-            self.V = V0 + n_acc
+                V += 1
+                n_acc += 1
+                for i in sorted(self.learners):
+                    Li = self.learners[i]
+                    if should_sync(V, Li.last_sync, cfg.target_period):
+                        Li.theta_minus = self.theta.copy()
+                        Li.last_sync = V
+                        synced[i] = True
+            self.V = V
         # O10 (one PS step per round on the mean of accepted gradients; R12, R25)
         elif n_acc > 0:
             g = G_sum / n_acc
@@ -494,10 +516,11 @@ class GorilaOracle:
                     adagrad_apply(self.theta[lo:hi], self.v[lo:hi], g[lo:hi], cfg.lr, cfg.ada_eps)
             self.V = V0 + n_acc
         # O11 is implicit: the next round reads self.theta / self.V (history)
-        # O12
-        synced = {}
+        # O12 (per-message mode: taken after every step above)
         for j in sorted(self.learners):
             L = self.learners[j]
+            if cfg.ps_mode == "per_message":
+                continue
             synced[j] = should_sync(self.V, L.last_sync, cfg.target_period)
             if synced[j]:
                 L.theta_minus = self.theta.copy()

@@ -999,7 +999,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         TdParams& t = p.td;
         t.Q = Lr.Q; t.Qhat = Lr.Qhat; t.a = ctx->sa; t.r = ctx->sr; t.d = ctx->sd; t.dQ = ctx->dQ;
         t.B = B; t.nA = nA; t.gamma = cfg.gamma; t.stats = Lr.stats; t.info = Lr.info; t.V = ctx->V;
-        t.base_V = ctx->Vhist + slot; t.n_acc_local = ctx->n_acc_local; t.max_staleness = cfg.max_staleness;
+        t.base_V = ctx->Vhist + slot; t.n_acc_local = ctx->n_acc_local; t.max_staleness = ctx->per_msg ? -1 : cfg.max_staleness;  // per-message: judged at the PS (R37)
         t.outlier_enabled = cfg.outlier_enabled; t.outlier_warmup = cfg.outlier_warmup;
         t.outlier_k = cfg.outlier_k; t.outlier_beta = cfg.outlier_beta;
         p.per_sample = ctx->td_partial;
@@ -1426,7 +1426,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     uint64_t* Vhist = c.take<uint64_t>(H);
     uint64_t* dev_round = c.take<uint64_t>(1);
     unsigned int* head_counter = c.take<unsigned int>(1);
-    uint64_t* pflags = c.take<uint64_t>(6 * MAX_W);
+    uint64_t* pflags = c.take<uint64_t>(FLAG_WORDS);
     uint64_t* p2p_epoch = c.take<uint64_t>(1);
     unsigned int* p2p_counter = c.take<unsigned int>(2);
     unsigned int* apply_counter = c.take<unsigned int>(1);
@@ -1738,7 +1738,7 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     CU(cudaMemsetAsync(ctx->Vhist, 0, sizeof(uint64_t) * ctx->H, st));
     CU(cudaMemsetAsync(ctx->head_counter, 0, sizeof(unsigned int), st));
     CU(cudaMemsetAsync(ctx->dev_round, 0, sizeof(uint64_t), st));
-    CU(cudaMemsetAsync(ctx->pflags, 0, sizeof(uint64_t) * 6 * MAX_W, st));
+    CU(cudaMemsetAsync(ctx->pflags, 0, sizeof(uint64_t) * FLAG_WORDS, st));
     CU(cudaMemsetAsync(ctx->p2p_epoch, 0, sizeof(uint64_t), st));
     CU(cudaMemsetAsync(ctx->p2p_counter, 0, sizeof(unsigned int) * 2, st));
     CU(cudaMemsetAsync(ctx->apply_counter, 0, sizeof(unsigned int), st));
@@ -2172,7 +2172,21 @@ void p2p_params(gorila_ctx* ctx, uint64_t round, ApplyParams& p, P2PParams& x) {
                 x.Gm[q * ctx->L + j] = peer_ptr(ctx, q, ctx->G_all + (int64_t)j * W * ctx->q) + lo;
     }
     x.L = ctx->per_msg ? ctx->L : 0;
-    for (int j = 0; j < (ctx->per_msg ? ctx->L : 0); ++j) x.info[j] = ctx->learners[j].info;
+    for (int j = 0; j < (ctx->per_msg ? ctx->L : 0); ++j) {
+        const Learner& l = ctx->learners[j];
+        x.info[j] = l.info;
+        x.stats[j] = l.stats;
+        x.sync_flag[j] = l.sync_flag;
+    }
+    if (ctx->per_msg)  // f1: every global learner's theta^- (in-round target syncs write this rank's slice)
+        for (int q = 0; q < W; ++q)
+            for (int j = 0; j < ctx->L; ++j) {
+                const Learner& l = ctx->learners[j];
+                x.tm_t[q * ctx->L + j] = peer_ptr(ctx, q, (uint8_t*)l.tminus_t);
+                x.tm_f[q * ctx->L + j] = peer_ptr(ctx, q, l.tminus_f);
+            }
+    x.max_delay = ctx->cfg.max_staleness;
+    x.period = ctx->cfg.target_period;
     x.epoch = ctx->p2p_epoch;
     x.counter = ctx->p2p_counter;
     static const int dbg = [] {
@@ -2318,9 +2332,16 @@ gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info*
         MsgParams mp{};
         mp.nmsg = ctx->L;
         for (int j = 0; j < ctx->L; ++j) {
+            const Learner& l = ctx->learners[j];
             mp.G[j] = ctx->G_all + (int64_t)j * ctx->W * ctx->q;
-            mp.info[j] = ctx->learners[j].info;
+            mp.info[j] = l.info;
+            mp.stats[j] = l.stats;
+            mp.sync_flag[j] = l.sync_flag;
+            mp.tm_t[j] = l.tminus_t;
+            mp.tm_f[j] = l.tminus_f;
         }
+        mp.max_delay = ctx->cfg.max_staleness;
+        mp.counter = ctx->apply_counter;
         if (ctx->cfg.math == GORILA_MATH_FP32) launch(ctx, k_apply_msg<float>, dim3(148 * 4), dim3(256), 0, p, mp);
         else launch(ctx, k_apply_msg<__nv_bfloat16>, dim3(148 * 4), dim3(256), 0, p, mp);
     } else {
@@ -2361,10 +2382,13 @@ gorila_status sync_target(gorila_ctx* ctx, const int32_t* learners, int32_t n, i
         gorila_status s = check_learner(ctx, learners[i]);
         if (s != GORILA_OK) return s;
         Learner& l = ctx->learners[learners[i]];
-        if (!ctx->fused_sync)  // gorila_round: k_apply already took the decision
+        // per-message mode (f1, R37): ps_apply_shard took every learner's in-round sync decisions and
+        // wrote theta^- at the version each fired; only a forced sync acts here
+        const bool msg_done = ctx->per_msg && !force;
+        if (!ctx->fused_sync && !msg_done)  // gorila_round: k_apply already took the decision
             launch(ctx, k_sync_decide, dim3(1), dim3(1), 0, l.stats, (const uint64_t*)ctx->V,
                    (int64_t)ctx->cfg.target_period, (int)force, l.sync_flag);
-        if (ctx->sync_fused_now) {  // k_apply wrote theta^- when it fired
+        if (msg_done || (ctx->sync_fused_now && !force)) {  // k_apply wrote theta^- when it fired
         } else if (ctx->p2p && ctx->W > 1) {  // ranks hold only their own fp32 slice: copy the latest replica
             const int slot = (int)(ctx->dev_round_expect % (uint64_t)ctx->H);
             const int64_t nt = (int64_t)ctx->rl.n_t * ctx->esz;
@@ -2723,7 +2747,9 @@ gorila_status gorila_get_grad(gorila_ctx* ctx, float* g) {
             CU(cudaMemcpy(one.data(), ctx->G_all + (int64_t)j * n, sizeof(float) * n, cudaMemcpyDeviceToHost));
             for (int64_t i = 0; i < n; ++i) acc[i] += one[i];
         }
-        CU(cudaMemcpy(ctx->tmp_int, acc.data(), sizeof(float) * n, cudaMemcpyHostToDevice));
+        // on the library stream: a pageable cudaMemcpy may return before its DMA lands, and the
+        // (non-blocking) library stream would not wait for it
+        CU(cudaMemcpyAsync(ctx->tmp_int, acc.data(), sizeof(float) * n, cudaMemcpyHostToDevice, st));
         src = ctx->tmp_int;
     }
     k_convert<<<148 * 4, 256, 0, st>>>(src, ctx->tmp_canon, ctx->P, 1);

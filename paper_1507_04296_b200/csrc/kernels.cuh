@@ -1078,6 +1078,45 @@ GORILA_DEV void opt_step4(const ApplyParams& p, float* tv, float* mv, float* vv,
     }
 }
 constexpr int MAX_W = 8;
+// f1 per-message PS (R32, R37): the messages of a round arrive in ascending global learner id. Message
+// m (sent unless its learner was not ready or outlier-rejected) is stale iff max_delay >= 0 and
+// V - base_m > max_delay with V the PS version when it arrives (V0 + messages applied before it;
+// P:160); a fresh one is its own optimizer step and V += 1, after which every learner i
+// with V >= last_i + N syncs its target net (theta^- = theta after that step, last_i = V;
+// P:158-160). Computed by one thread from the round's inputs; every block computes the same.
+constexpr int MAX_MSG = 64;
+struct MsgSchedule {
+    uint64_t acc;                 // applied messages
+    uint64_t vend;                // V after the round
+    uint64_t last[MAX_MSG];       // every learner's last sync after the round
+    uint64_t sync_after[MAX_MSG]; // learners whose (last) in-round sync follows message m
+    int8_t sync_at[MAX_MSG];      // message after which learner i last synced this round, -1: none
+};
+GORILA_DEV void msg_schedule(int n, uint64_t has, const uint64_t* base, const uint64_t* last0, uint64_t V0,
+                             int64_t max_delay, int64_t period, MsgSchedule& s) {
+    uint64_t V = V0;
+    s.acc = 0;
+    for (int i = 0; i < n; ++i) {
+        s.last[i] = last0[i];
+        s.sync_at[i] = -1;
+        s.sync_after[i] = 0;
+    }
+    for (int m = 0; m < n; ++m) {
+        if (!(has >> m & 1ull)) continue;
+        if (max_delay >= 0 && (int64_t)(V - base[m]) > max_delay) continue;  // stale at arrival
+        s.acc |= 1ull << m;
+        V += 1;
+        for (int i = 0; i < n; ++i)
+            if (V >= s.last[i] + (uint64_t)period) {
+                s.last[i] = V;
+                s.sync_at[i] = (int8_t)m;
+            }
+    }
+    for (int i = 0; i < n; ++i)
+        if (s.sync_at[i] >= 0) s.sync_after[s.sync_at[i]] |= 1ull << i;
+    s.vend = V;
+}
+
 GORILA_DEV void st_release_sys(uint64_t* p, uint64_t v) {
     asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
 }
@@ -1159,8 +1198,17 @@ struct P2PParams {
     // per-message mode (f1): L messages per rank, message (q, j) = rank q's learner j at Gm[q * L + j]
     int L;                        // 0: aggregate mode
     const float* Gm[64];
-    const DevLearnerInfo* info[32];  // this rank's learners' decisions (acceptance mask sent with the flag)
+    DevLearnerInfo* info[32];     // this rank's learners' records (sent mask / bases published with the flag;
+                                  // the final stale / accepted decisions written back by the book block)
+    LearnerStats* stats[32];      // this rank's learners' target-sync state
+    uint8_t* sync_flag[32];
+    void* tm_t[64];               // every global learner's theta^- replica, at its address in this process
+    float* tm_f[64];
+    int64_t max_delay, period;
 };
+// flag-area slots (u64) of the per-message exchange, besides the ready / done flags and counts
+constexpr int FLAG_BASE = 6 * MAX_W, FLAG_LAST = FLAG_BASE + MAX_MSG, FLAG_V0 = FLAG_LAST + MAX_MSG,
+              FLAG_WORDS = FLAG_V0 + MAX_W;
 
 
 // phase: flag set (0 = the fc4 weight region, launched early by gorila_round; 1 = the rest);
@@ -1179,15 +1227,21 @@ __global__ void __launch_bounds__(256) k_apply_p2p(ApplyParams p, P2PParams x, i
     uint64_t* mine = x.flags[x.rank];
     if (blockIdx.x == 0 && (int)threadIdx.x < x.W) {  // this rank's G range and count are complete
         x.flags[threadIdx.x][4 * MAX_W + x.rank] = (uint64_t)*x.nacc[x.rank];  // ordered by the release
-        if (x.L) {
+        if (x.L) {  // f1: which learners sent a message, their replica versions, target-sync state, V0
             uint64_t m = 0;
-            for (int j = 0; j < x.L; ++j) m |= (uint64_t)(x.info[j]->accepted ? 1 : 0) << j;
+            for (int j = 0; j < x.L; ++j) {
+                m |= (uint64_t)(x.info[j]->accepted ? 1 : 0) << j;
+                x.flags[threadIdx.x][FLAG_BASE + x.rank * x.L + j] = x.info[j]->base_version;
+                x.flags[threadIdx.x][FLAG_LAST + x.rank * x.L + j] = x.stats[j]->last_sync;
+            }
             x.flags[threadIdx.x][5 * MAX_W + x.rank] = m;
+            x.flags[threadIdx.x][FLAG_V0 + x.rank] = *p.V;
         }
         st_release_sys(x.flags[threadIdx.x] + RDY + x.rank, ep);
     }
     __shared__ float s_cnt;
     __shared__ unsigned long long s_gmask;
+    __shared__ MsgSchedule sch;
     if (threadIdx.x == 0) {
         float c = 0.f;
         unsigned long long gm = 0;
@@ -1195,6 +1249,17 @@ __global__ void __launch_bounds__(256) k_apply_p2p(ApplyParams p, P2PParams x, i
             wait_flag(mine + RDY + q, ep);
             c += (float)__ldcg(mine + 4 * MAX_W + q);  // local copy of rank q's count
             if (x.L) gm |= (unsigned long long)__ldcg(mine + 5 * MAX_W + q) << (q * x.L);
+        }
+        if (x.L) {  // the per-message schedule over every rank's messages (identical on every rank)
+            uint64_t base[MAX_MSG], last0[MAX_MSG];
+            const int n = x.W * x.L;
+            for (int i = 0; i < n; ++i) {
+                base[i] = __ldcg(mine + FLAG_BASE + i);
+                last0[i] = __ldcg(mine + FLAG_LAST + i);
+            }
+            msg_schedule(n, gm, base, last0, __ldcg(mine + FLAG_V0), x.max_delay, x.period, sch);
+            gm = sch.acc;
+            c = (float)__popcll(gm);
         }
         s_cnt = c;
         s_gmask = gm;
@@ -1209,7 +1274,24 @@ __global__ void __launch_bounds__(256) k_apply_p2p(ApplyParams p, P2PParams x, i
     }
 #endif
     const float cnt = s_cnt;
-    if (book && blockIdx.x == 0 && threadIdx.x == 0) {
+    if (book && x.L && blockIdx.x == 0 && threadIdx.x == 0) {  // f1: the schedule's versions and decisions
+        const uint64_t v0 = __ldcg(mine + FLAG_V0), n_acc = (uint64_t)__popcll(gmask);
+        p.round_info[0] = n_acc;
+        p.round_info[1] = v0;
+        p.round_info[2] = sch.vend;
+        *p.V = sch.vend;
+        if (p.vhist_dst) *p.vhist_dst = sch.vend;
+        if (p.dev_round) *p.dev_round += 1;
+        for (int j = 0; j < x.L; ++j) {
+            const int gid = x.rank * x.L + j;
+            DevLearnerInfo* inf = x.info[j];
+            const bool sent = inf->accepted;
+            inf->accepted = (gmask >> gid & 1ull) ? 1 : 0;
+            inf->stale = (sent && !inf->accepted) ? 1 : 0;
+            x.stats[j]->last_sync = sch.last[gid];
+            *x.sync_flag[j] = sch.sync_at[gid] >= 0;
+        }
+    } else if (book && blockIdx.x == 0 && threadIdx.x == 0) {
         const uint64_t v0 = *p.V;
         const uint64_t n_acc = (uint64_t)(cnt + 0.5f);
         p.round_info[0] = n_acc;
@@ -1237,8 +1319,14 @@ __global__ void __launch_bounds__(256) k_apply_p2p(ApplyParams p, P2PParams x, i
             float4 m = reinterpret_cast<float4*>(p.m)[e];
             float4 v = reinterpret_cast<float4*>(p.v)[e];
             float mv[4] = {m.x, m.y, m.z, m.w}, vv[4] = {v.x, v.y, v.z, v.w};
-            for (int msg = 0; msg < x.W * x.L; ++msg)
-                if (gmask >> msg & 1ull) opt_step4(p, tv, mv, vv, __ldcg(reinterpret_cast<const float4*>(x.Gm[msg]) + e));
+            for (int msg = 0; msg < x.W * x.L; ++msg) {
+                if (!(gmask >> msg & 1ull)) continue;
+                opt_step4(p, tv, mv, vv, __ldcg(reinterpret_cast<const float4*>(x.Gm[msg]) + e));
+                for (uint64_t sm = sch.sync_after[msg]; sm; sm &= sm - 1) {  // in-round target syncs (any rank)
+                    const int i = __ffsll((long long)sm) - 1;
+                    emit4_to<T>(x.tm_t[i], x.tm_f[i], p.nA, p.base + 4 * e, tv);
+                }
+            }
             reinterpret_cast<float4*>(p.m)[e] = make_float4(mv[0], mv[1], mv[2], mv[3]);
             reinterpret_cast<float4*>(p.v)[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
             reinterpret_cast<float4*>(th_local)[e] = make_float4(tv[0], tv[1], tv[2], tv[3]);
@@ -1331,45 +1419,43 @@ __global__ void k_peer_wait(P2PParams x, int phase0) {  // waits for phase 1 (an
 // NEXT row f1 (reading R32): each accepted learner gradient is its own optimizer step, applied in
 // ascending global learner id ("applies the updates", P:160 version per update). The
 // sequence is elementwise, so every thread runs the whole message sequence on its elements.
-constexpr int MAX_MSG = 64;
 struct MsgParams {
-    const float* G[32];                 // local learner j's gradient (this rank's slice)
-    const DevLearnerInfo* info[32];     // its decisions of the round
+    const float* G[32];           // local learner j's gradient (this rank's slice)
+    DevLearnerInfo* info[32];     // its learner record (sent = accepted from the learner step; the
+                                  // final stale / accepted decisions are written back here)
+    LearnerStats* stats[32];      // its target-sync state
+    uint8_t* sync_flag[32];
+    void* tm_t[32];               // its target replica (T area, fp32 area)
+    float* tm_f[32];
     int nmsg;
+    int64_t max_delay;
+    unsigned int* counter;        // last-block detection (zero between launches)
 };
+// W == 1: every block takes the schedule from the state before this round; the last block to finish
+// writes the decisions / versions / sync state back (after every block has read them).
 template <typename T>
 __global__ void __launch_bounds__(256) k_apply_msg(ApplyParams p, MsgParams mp) {
     pdl_wait();
     pdl_trigger();
-    __shared__ uint32_t s_mask;
+    __shared__ MsgSchedule sch;
+    __shared__ uint64_t s_v0;
     if (threadIdx.x == 0) {
-        uint32_t mask = 0;
-        for (int j = 0; j < mp.nmsg; ++j) mask |= (mp.info[j]->accepted ? 1u : 0u) << j;
-        s_mask = mask;
+        uint64_t has = 0, base[32], last0[32];
+        for (int j = 0; j < mp.nmsg; ++j) {
+            has |= (uint64_t)(mp.info[j]->accepted ? 1 : 0) << j;
+            base[j] = mp.info[j]->base_version;
+            last0[j] = mp.stats[j]->last_sync;
+        }
+        s_v0 = *p.V;
+        msg_schedule(mp.nmsg, has, base, last0, s_v0, mp.max_delay, p.period, sch);
     }
     __syncthreads();
-    const uint32_t mask = s_mask;
-    const int n_acc = __popc(mask);
-    if (blockIdx.x == 0 && threadIdx.x == 0) {
-        const uint64_t v0 = *p.V;
-        p.round_info[0] = n_acc;
-        p.round_info[1] = v0;
-        p.round_info[2] = v0 + n_acc;
-        *p.V = v0 + n_acc;
-        if (p.vhist_dst) *p.vhist_dst = v0 + n_acc;
-        if (p.dev_round) *p.dev_round += 1;
-        for (int i = 0; i < p.n_sync; ++i) {
-            LearnerStats* st = p.sync_stats[i];
-            const bool doit = v0 + n_acc >= st->last_sync + (uint64_t)p.period;
-            if (doit) st->last_sync = v0 + n_acc;
-            *p.sync_flag[i] = doit;
-        }
-    }
+    const uint64_t acc = sch.acc;
     const int64_t n4 = (p.n_real + 3) / 4;
     for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n4; e += (int64_t)gridDim.x * blockDim.x) {
         float4 th = reinterpret_cast<float4*>(p.theta)[e];
         float tv[4] = {th.x, th.y, th.z, th.w};
-        if (mask) {
+        if (acc) {
             float4 m = reinterpret_cast<float4*>(p.m)[e];
             float4 v = reinterpret_cast<float4*>(p.v)[e];
             float mv[4] = {m.x, m.y, m.z, m.w}, vv[4] = {v.x, v.y, v.z, v.w};
@@ -1377,16 +1463,45 @@ __global__ void __launch_bounds__(256) k_apply_msg(ApplyParams p, MsgParams mp) 
                 float4 gq[8];
 #pragma unroll
                 for (int u = 0; u < 8; ++u)
-                    if (j0 + u < mp.nmsg && (mask >> (j0 + u) & 1u)) gq[u] = reinterpret_cast<const float4*>(mp.G[j0 + u])[e];
+                    if (j0 + u < mp.nmsg && (acc >> (j0 + u) & 1ull)) gq[u] = reinterpret_cast<const float4*>(mp.G[j0 + u])[e];
 #pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    if (j0 + u < mp.nmsg && (mask >> (j0 + u) & 1u)) opt_step4(p, tv, mv, vv, gq[u]);
+                for (int u = 0; u < 8; ++u) {
+                    if (j0 + u >= mp.nmsg || !(acc >> (j0 + u) & 1ull)) continue;
+                    opt_step4(p, tv, mv, vv, gq[u]);
+                    for (uint64_t sm = sch.sync_after[j0 + u]; sm; sm &= sm - 1) {  // in-round target syncs
+                        const int i = __ffsll((long long)sm) - 1;
+                        emit4_to<T>(mp.tm_t[i], mp.tm_f[i], p.nA, p.base + 4 * e, tv);
+                    }
+                }
             }
             reinterpret_cast<float4*>(p.theta)[e] = make_float4(tv[0], tv[1], tv[2], tv[3]);
             reinterpret_cast<float4*>(p.m)[e] = make_float4(mv[0], mv[1], mv[2], mv[3]);
             reinterpret_cast<float4*>(p.v)[e] = make_float4(vv[0], vv[1], vv[2], vv[3]);
         }
         if (p.rep_t) emit4<T>(p, e, tv);
+    }
+    __shared__ unsigned int s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(mp.counter, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last || threadIdx.x != 0) return;
+    __threadfence();
+    *mp.counter = 0;
+    const uint64_t v0 = s_v0, n_acc = (uint64_t)__popcll(acc);
+    p.round_info[0] = n_acc;
+    p.round_info[1] = v0;
+    p.round_info[2] = sch.vend;
+    *p.V = sch.vend;
+    if (p.vhist_dst) *p.vhist_dst = sch.vend;
+    if (p.dev_round) *p.dev_round += 1;
+    for (int j = 0; j < mp.nmsg; ++j) {
+        DevLearnerInfo* inf = mp.info[j];
+        const bool sent = inf->accepted;
+        inf->accepted = (acc >> j & 1ull) ? 1 : 0;
+        inf->stale = (sent && !inf->accepted) ? 1 : 0;
+        mp.stats[j]->last_sync = sch.last[j];
+        *mp.sync_flag[j] = sch.sync_at[j] >= 0;
     }
 }
 

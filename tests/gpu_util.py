@@ -132,18 +132,19 @@ def per_tensor_rel_l2(x, ref, nA):
 
 
 def run_round_both(g, orc, k, learners, staleness=None):
-    """One round on both sides; the oracle's backward is teacher-forced to the GPU's ReLU decisions
-    where they are ambiguous (R30). Returns (gpu dict, oracle dict)."""
-    stal = None if staleness is None else [staleness.get(j, 0) for j in learners]
+    """One round on both sides (gorila_round: learner_step + ps_apply_shard + sync_target; the learner
+    records are read after the round, when the per-message mode's PS-side decisions are final); the
+    oracle's backward is teacher-forced to the GPU's ambiguous ReLU decisions (R30). The gradient
+    buffers, Q and the captured activations are intact after the round (the apply only reads them).
+    Returns (gpu dict, oracle dict)."""
+    stal = None if staleness is None else np.array([staleness.get(j, 0) for j in learners], np.int32)
     th0 = g.get_state()[0]
     g.capture_activations(True)
-    info = g.learner_step(learners, k, staleness=stal)
+    info, ri, synced = g.round(np.array(learners, np.int32), k, stal, want_info=True)
     G = g.get_grad()
     qs = {j: g.get_q(j) for j in learners}
     info_by = dict(zip(learners, info))
     acts = {j: gpu_acts(g, j) for j in learners if not info_by[j]["not_ready"]}
-    ri = g.ps_apply_shard(k)
-    synced = g.sync_target(learners)
     th1, m1, v1, V1 = g.get_state()
     forced = []
     gpu = {"info": info_by, "G": G, "q": qs, "round": ri, "synced": dict(zip(learners, synced)),

@@ -131,7 +131,10 @@ def _check_round(gpu, res, math, nA, learners, orc=None, thetas=None):
             assert bool(gi["rejected_outlier"]) == bool(oi["rejected_outlier"])
         assert bool(gi["accepted"]) == bool(oi["accepted"])
         assert gi["base_version"] == oi["base_version"]
-        if oi["accepted"]:
+        # G: the accepted gradients; per-message mode (R37) judges staleness at the PS, so every sent
+        # (not outlier-rejected) message's gradient is in the learner's buffer
+        per_msg = orc is not None and orc.cfg.ps_mode == "per_message"
+        if oi["accepted"] or (per_msg and "G" in oi):
             G_ref += oi["G"]
     if np.any(G_ref):
         e_all = rel_l2(gpu["G"], G_ref)
@@ -263,6 +266,47 @@ def test_f1_per_message_ps_parity(math, opt):
         n_msg = max(1, res["n_accepted"])
         _check_dtheta(gpu, orc, th_before, math, nA,
                       tol_dtheta=max(TOL[math]["dtheta"], n_msg * TOL[math]["g"]), n_round=n_msg + 1)
+
+
+@pytest.mark.parametrize("math", ["fp32", "bf16"])
+@pytest.mark.parametrize("case", ["stale_at_arrival", "sync_inside_round"])
+def test_f1_paper_exact_staleness_and_sync(math, case):
+    """f1 paper-exact (R37; tests/test_oracle_update.py pins the oracle by hand), three learners per round.
+    stale_at_arrival: max delay 1 -> the third message of every round arrives two versions late and is
+    discarded (judged against V0 alone it would pass). sync_inside_round: target period 2 with three
+    fresh messages -> the target nets sync after the message that reaches last + 2, inside the round;
+    theta^- is theta at that version, not at the round's end."""
+    nA, L = 6, 3
+    kw = dict(max_staleness=1, target_period=100) if case == "stale_at_arrival" else dict(target_period=2)
+    g, orc = make_pair(nA=nA, B=16, C=2000, n_insert=2000, math=math, L=L, optimizer="adagrad",
+                       ps_mode="per_message", outlier_enabled=False, lr=1e-3, ada_eps=1e-6, **kw)
+    ids = list(range(L))
+    mid_round_syncs = 0
+    for k in range(3):
+        teacher_force(g, orc)
+        th_before = orc.theta.copy()
+        gpu, res = run_round_both(g, orc, k, ids)
+        _check_round(gpu, res, math, nA, ids, orc, {j: th_before for j in ids})
+        n_msg = res["n_accepted"]
+        _check_dtheta(gpu, orc, th_before, math, nA, tol_dtheta=max(TOL[math]["dtheta"], n_msg * TOL[math]["g"]),
+                      n_round=n_msg + 1)
+        if case == "stale_at_arrival":
+            assert [bool(gpu["info"][j]["stale"]) for j in ids] == [False, False, True] and n_msg == 2
+            continue
+        assert n_msg == 3 and all(bool(gpu["synced"][j]) for j in ids)
+        for j in ids:
+            tm, st = g.get_learner_state(j)
+            assert st["last_sync"] == orc.learners[j].last_sync
+            mid = st["last_sync"] < gpu["round"]["version_after"]  # the round's last sync came before its end
+            mid_round_syncs += int(mid)
+            if math == "fp32":  # theta^- = theta at the sync's version (the oracle's)
+                d_gpu = tm.astype(np.float64) - th_before
+                d_ref = orc.learners[j].theta_minus.astype(np.float32).astype(np.float64) - th_before
+                floor = 3 * np.linalg.norm(np.spacing(np.abs(tm))) / np.linalg.norm(d_ref)
+                assert rel_l2(d_gpu, d_ref) <= 3e-5 + floor
+                if mid:  # ... which is not the round-end theta
+                    assert rel_l2(gpu["theta1"].astype(np.float64) - th_before, d_ref) > 10 * (3e-5 + floor)
+    assert case == "stale_at_arrival" or mid_round_syncs >= L  # round 0 syncs at V = 2 of 3
 
 
 @pytest.mark.parametrize("math", ["fp32", "bf16"])

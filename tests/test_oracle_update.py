@@ -354,3 +354,66 @@ def test_f1_messages_applied_one_step_each_in_learner_order():
                 O.rmsprop_apply(th, m, v, G, 1e-3, 0.95, 0.01)
         assert np.array_equal(orc.theta, th) and orc.V == 2 and res["n_accepted"] == 2
         assert not np.allclose(orc.theta, agg.theta, rtol=0, atol=1e-12)
+
+
+def _f1_pair_cfg(learners, **kw):
+    nA, B, C = 4, 8, 400
+    cfg = O.Config(n_actions=nA, batch=B, capacity=C, learners=learners, outlier_warmup=1, outlier_enabled=False,
+                   optimizer="adagrad", lr=1e-3, ps_mode="per_message", **kw)
+    orc = O.GorilaOracle(cfg, synth.theta0(nA))
+    for j in learners:
+        f = synth.frames(synth.SEED_DATA, j, 0, C)
+        a, r, d = synth.meta(synth.SEED_DATA, j, 0, C, nA)
+        orc.insert(j, f, a, r, d)
+    return orc
+
+
+def test_f1_staleness_judged_against_the_version_at_arrival():
+    """Hand case ("discards gradients older than a threshold"; P:160 V counts PS updates):
+    max delay 1, three messages computed on the replica of version V0. Message 1 arrives at V0 (delay
+    0: applied, V = V0 + 1), message 2 at V0 + 1 (delay 1: applied, V = V0 + 2), message 3 at V0 + 2
+    (delay 2 > 1: discarded). Judged against V0 alone (round-start reading) all three would pass."""
+    orc = _f1_pair_cfg((0, 1, 2), max_staleness=1)
+    th0, v0 = orc.theta.copy(), orc.v.copy()
+    res = orc.round(0)
+    L = res["learners"]
+    assert [L[j]["base_version"] for j in (0, 1, 2)] == [0, 0, 0]
+    assert [L[j]["version_at_arrival"] for j in (0, 1, 2)] == [0, 1, 2]
+    assert [bool(L[j]["accepted"]) for j in (0, 1, 2)] == [True, True, False]
+    assert [bool(L[j]["stale"]) for j in (0, 1, 2)] == [False, False, True]
+    assert res["n_accepted"] == 2 and orc.V == 2
+    th, v = th0.copy(), v0.copy()
+    for j in (0, 1):  # the pinned AdaGrad primitive, the two fresh messages in learner order
+        O.adagrad_apply(th, v, L[j]["G"], 1e-3, 1e-8)
+    assert np.array_equal(orc.theta, th) and np.array_equal(orc.v, v)
+    # next round: both delays restart from the new replica (base V = 2)
+    res = orc.round(1)
+    assert [res["learners"][j]["base_version"] for j in (0, 1, 2)] == [2, 2, 2]
+    assert [bool(res["learners"][j]["accepted"]) for j in (0, 1, 2)] == [True, True, False]
+
+
+def test_f1_target_sync_at_the_first_version_inside_the_round():
+    """N = 2, three fresh messages from V = 0 (theta^- = theta^+ "after every N gradient
+    updates in the central parameter server"): the sync fires after message 2 (V = 2 >= 0 + 2), so
+    theta^- is theta after two steps and last = 2; message 3 (V = 3 < 4) does not sync again. A
+    round-end reading would copy theta after three steps with last = 3."""
+    orc = _f1_pair_cfg((0, 1, 2), target_period=2)
+    th0, v0 = orc.theta.copy(), orc.v.copy()
+    res = orc.round(0)
+    L = res["learners"]
+    th, v = th0.copy(), v0.copy()
+    O.adagrad_apply(th, v, L[0]["G"], 1e-3, 1e-8)
+    O.adagrad_apply(th, v, L[1]["G"], 1e-3, 1e-8)
+    th2 = th.copy()
+    O.adagrad_apply(th, v, L[2]["G"], 1e-3, 1e-8)
+    assert np.array_equal(orc.theta, th) and orc.V == 3
+    for j in (0, 1, 2):
+        assert res["synced"][j]
+        assert np.array_equal(orc.learners[j].theta_minus, th2)
+        assert orc.learners[j].last_sync == 2
+    assert not np.array_equal(th2, th)
+    # N = 1: every step syncs; theta^- ends at the round's last version
+    orc = _f1_pair_cfg((0, 1, 2), target_period=1)
+    orc.round(0)
+    assert all(np.array_equal(orc.learners[j].theta_minus, orc.theta) and orc.learners[j].last_sync == 3
+               for j in (0, 1, 2))

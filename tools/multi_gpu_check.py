@@ -108,12 +108,12 @@ def main():
         # the state every rank starts the round from (teacher forcing of the oracle)
         th0, m0, v0, V0 = g.get_state()
         lstate = {rank * Ll + j: g.get_learner_state(j) for j in ids}
-        info = g.learner_step(ids, k)
+        # one round (learner_step + ps_apply_shard + sync_target; records read after it, when the
+        # per-message PS decisions are final); G, Q and the captured activations are intact after it
+        info, ri, synced = g.round(np.array(ids, np.int32), k, want_info=True)
         qs = {rank * Ll + j: g.get_q(j) for j in ids}
         acts = {rank * Ll + j: gpu_acts(g, j) for j in ids if not info[j]["not_ready"]}
         Gr = g.get_grad()
-        ri = g.ps_apply_shard(k)
-        synced = g.sync_target(ids)
         th1, _, _, V1 = g.get_state()
         allth = gather(th1, world)
         if not all(np.array_equal(allth[0], x) for x in allth):
@@ -161,14 +161,24 @@ def main():
             for q_rank, e in enumerate(every):  # each rank's gradient sum, per tensor
                 ref = np.zeros(len(th0))
                 for gid in range(q_rank * Ll, (q_rank + 1) * Ll):
-                    if res["learners"][gid]["accepted"]:
-                        ref += res["learners"][gid]["G"]
+                    oi = res["learners"][gid]
+                    # per-message mode judges staleness at the PS: every sent message's gradient is there
+                    if oi["accepted"] or (ps_mode == "per_message" and "G" in oi):
+                        ref += oi["G"]
                 if not np.any(ref):
                     if np.any(e["G"]):
                         fails.append(f"round {k} rank {q_rank}: nonzero G without an accepted learner")
                     continue
                 errs = per_tensor_rel_l2(e["G"], ref, nA)
                 bad = {n_: v_ for n_, v_ in errs.items() if v_ > tol["g"]}
+                if bad and os.environ.get("DEBUG_G"):
+                    for gid in range(q_rank * Ll, (q_rank + 1) * Ll):
+                        oi = res["learners"][gid]
+                        print(f"  dbg round {k} gid {gid}: gpu {infos[gid]} oracle acc {oi['accepted']} "
+                              f"rej {oi['rejected_outlier']} stale {oi['stale']} hasG {'G' in oi}", flush=True)
+                        if "G" in oi:
+                            print("   vs this learner alone:", {n_: round(v_, 4) for n_, v_ in
+                                                                per_tensor_rel_l2(e["G"], oi["G"], nA).items()}, flush=True)
                 if rel_l2(e["G"], ref) > tol["g"] or bad:
                     fails.append(f"round {k} rank {q_rank}: G {rel_l2(e['G'], ref):.2e} per tensor {bad}")
             ri0 = every[0]["ri"]
