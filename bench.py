@@ -283,6 +283,59 @@ def config_dict(args, world):
                                      "parameter/optimizer state stays L2-resident across steps as in training"}
 
 
+def run_async(args, g, ids, world, rank, local_rank, json_out):
+    """NEXT row f2: learner steps/s of gorila_async_run (learners and shard servers decoupled), device-timed
+    around the call on the library stream, max over ranks; the shards' accept / stale counts and the
+    learners' outlier rejections of the timed run."""
+    import torch
+    L = len(ids)
+    stream = g.stream
+    g.async_run(ids, args.warmup, round0=0, server_blocks=args.server_blocks)  # warm-up (also loads kernels)
+    barrier(world)
+    clk = ClockSampler(local_rank).__enter__()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    stream.synchronize()
+    barrier(world)
+    e0.record(stream)
+    st = g.async_run(ids, args.steps, round0=args.warmup, server_blocks=args.server_blocks)
+    e1.record(stream)
+    stream.synchronize()
+    clk.__exit__(None, None, None)
+    ms = max_over_ranks(e0.elapsed_time(e1), world) if args.bootstrap == "nccl" else e0.elapsed_time(e1)
+    if world > 1 and args.bootstrap == "ipc":
+        import torch.distributed as dist
+        allms = [None] * world
+        dist.all_gather_object(allms, ms)
+        ms = max(allms)
+    stats = [st]
+    if world > 1:
+        import torch.distributed as dist
+        stats = [None] * world
+        dist.all_gather_object(stats, st)
+    value = world * L * args.steps / (ms / 1000.0)
+    if rank == 0:
+        cfg = config_dict(args, world)
+        cfg["workload"] += "; NEXT row f2: asynchronous PS (gorila_async_run), learner steps counted"
+        cfg["bootstrap"] = args.bootstrap
+        cfg["server_blocks"] = args.server_blocks
+        out = {"metric": METRIC + " [asynchronous PS, f2]", "value": value, "unit": UNIT, "n_gpus": world,
+               "gpus_physical": torch.cuda.device_count() if args.bootstrap == "ipc" else world,
+               "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps, "higher_is_better": True,
+               "scaling": "weak", "vs_baseline": None, "dtype": "bf16" if args.math == "bf16" else "f32",
+               "data": "synthetic", "config": cfg, "clocks": clk.summary(),
+               "async": {"per_shard": stats,
+                         "sent": sum(s["sent"] for s in stats), "rejected_outlier": sum(s["rejected"] for s in stats),
+                         "fresh_per_shard": [s["fresh"] for s in stats], "stale_per_shard": [s["stale"] for s in stats],
+                         "stale_fraction": [s["stale"] / max(1, s["fresh"] + s["stale"]) for s in stats],
+                         "note": "one message per shard per non-rejected learner step; each shard judges staleness "
+                                 "against its own live version (V_arrival - base > max_delay is discarded)"}}
+        print(json.dumps(out), file=json_out, flush=True)
+    g.close()
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
 def main():
     # the contract's stdout is ONE JSON line: everything else (NCCL banners, warnings) goes to stderr
     json_out = os.fdopen(os.dup(1), "w")
@@ -301,8 +354,13 @@ def main():
     ap.add_argument("--staleness", type=int, default=0, help="scheduled staleness of every learner (rounds)")
     ap.add_argument("--max-staleness", type=int, default=-1, help="discard threshold in versions (-1: off)")
     ap.add_argument("--poison", type=float, default=0.0, help="probability of a 1e6 poison reward")
-    ap.add_argument("--ps-mode", default="aggregate", choices=["aggregate", "per_message"],
-                    help="per_message: NEXT row f1 (one optimizer step per accepted learner gradient)")
+    ap.add_argument("--ps-mode", default="aggregate", choices=["aggregate", "per_message", "async"],
+                    help="per_message: NEXT row f1 (one optimizer step per accepted learner gradient); "
+                         "async: NEXT row f2 (learners and shard servers decoupled, gorila_async_run)")
+    ap.add_argument("--bootstrap", default="nccl", choices=["nccl", "ipc"],
+                    help="ipc: gloo process group + caller-exchanged peer mappings (several ranks may share "
+                         "one GPU: rank r on cuda:(r mod #GPUs))")
+    ap.add_argument("--server-blocks", type=int, default=32, help="async: blocks of each shard's server kernel")
     ap.add_argument("--optimizer", default="rmsprop", choices=["rmsprop", "adagrad"])
     ap.add_argument("--replay", default="local", choices=["local", "global"],
                     help="global: NEXT row f4 (uniform over all learners' rings, NVLink gathers)")
@@ -317,15 +375,20 @@ def main():
 
     import torch
     world, rank, local_rank = dist_env()
+    if args.bootstrap == "ipc":
+        local_rank = local_rank % torch.cuda.device_count()
     torch.cuda.set_device(local_rank)
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if args.bootstrap == "ipc":
+            dist.init_process_group("gloo")
+        else:
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     import synth
     from paper_1507_04296_b200 import Gorila, nccl_unique_id
     synth.build()
     uid = None
-    if world > 1:
+    if world > 1 and args.bootstrap == "nccl":
         import torch.distributed as dist
         obj = [nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
@@ -342,6 +405,8 @@ def main():
         fill_replay(g, j, args.capacity, args.n_actions, synth.SEED_DATA, rank * L + j, p_poison=args.poison)
     ids = np.arange(L, dtype=np.int32)
     stal = np.full(L, args.staleness, np.int32) if args.staleness else None
+    if args.ps_mode == "async":
+        return run_async(args, g, ids, world, rank, local_rank, json_out)
 
     def step(k):
         g.round(ids, k, stal)  # learner_step + ps_apply_shard + sync_target, replayed as one CUDA graph

@@ -326,6 +326,31 @@ GORILA_API gorila_status gorila_bench_phase(gorila_ctx* ctx, int32_t learner, in
                                             double* us_per_iter);
 /* Diagnostics build only (-DGORILA_TRACE): clock64 timeline of CTA (0,0,0) of the last GEMM. */
 GORILA_API gorila_status gorila_debug_trace(uint64_t* out64);
+/* NEXT row f2: the asynchronous parameter server (config.ps_mode == 2; §3.1, P:144,
+ * P:165-169). Runs `steps` learner steps for each listed local learner (ascending ids; round robin on
+ * the library stream, rounds round0 .. round0 + steps - 1 for the sampler) while this rank's shard is
+ * served by a persistent kernel of server_blocks blocks (<= 0: 32) on a second stream. A learner step
+ * fetches the live replica (waiting only until its own previous message was consumed), records every
+ * shard's live version as its base, syncs its target net if min V >= last + N, runs the learner update
+ * and sends one message per shard unless outlier-rejected. Each shard's server applies messages in
+ * arrival order, discarding those with V_arrival - base > max_staleness, one optimizer
+ * step each (V += 1). Nothing orders learners and servers beyond those device counters: the result is
+ * not deterministic and has no parity oracle (throughput and discard statistics); the deterministic
+ * modes stay the parity path. COLLECTIVE when world > 1 (peer-memory mapping required). Returns after
+ * every rank's messages are drained; the deterministic entry points (learner_step, ps_apply_shard,
+ * gorila_round) return E_INVALID in this mode. out (may be NULL): counts and observed delays. */
+typedef struct {
+    uint64_t steps;          /* learner steps run on this rank */
+    uint64_t sent;           /* messages sent by this rank's learners (to every shard) */
+    uint64_t fresh, stale;   /* messages applied / discarded by this rank's shard */
+    uint64_t rejected;       /* this rank's outlier-rejected steps (no message) */
+    uint64_t version_after;  /* this shard's version at the end */
+    uint64_t max_delay;      /* largest V_arrival - base this shard saw */
+    double mean_delay;       /* mean V_arrival - base over this shard's messages */
+} gorila_async_stats;
+GORILA_API gorila_status gorila_async_run(gorila_ctx* ctx, const int32_t* learners, int32_t n, int64_t steps,
+                                          uint64_t round0, int32_t server_blocks, gorila_async_stats* out);
+
 /* Writes a fresh 128-byte ncclUniqueId (rank 0 calls it and broadcasts the bytes). */
 GORILA_API gorila_status gorila_nccl_unique_id(void* out128);
 /* Caller-bootstrapped exchange (world > 1 and config.nccl_unique_id == NULL; e.g. a gloo process

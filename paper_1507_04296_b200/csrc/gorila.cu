@@ -28,6 +28,7 @@
 #include "tma_gemm.cuh"
 #include "shift_gemm.cuh"
 #include "tower.cuh"
+#include "async.cuh"
 
 using namespace gorila;
 
@@ -198,7 +199,10 @@ struct gorila_ctx {
     // backward: phase 0 of the apply runs on side2 right after the last learner's fc4 wgrad
     bool in_round = false, early_pending = false;
     // per-message PS (f1, cfg.ps_mode == 1): every local learner keeps its own gradient buffer
-    bool per_msg = false;
+    bool per_msg = false;    // ps_mode 1 or 2: one gradient buffer per learner
+    bool async_mode = false; // ps_mode 2 (NEXT row f2): gorila_async_run only
+    AsyncState* ast = nullptr;
+    uint64_t async_epoch = 0;  // gorila_async_run calls (the cross-rank start barrier's epoch)
     float* G_all = nullptr;  // [L][W*q]; G points at learner 0's
     int early_learner = -1;
     cudaStream_t side2 = nullptr;
@@ -770,7 +774,8 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     const int B = ctx->B, nA = ctx->nA;
     constexpr bool fp32v = std::is_same<T, float>::value;
     const uint64_t k_src = round >= (uint64_t)s_j ? round - (uint64_t)s_j : 0;
-    const int slot = (int)(k_src % (uint64_t)ctx->H);
+    // asynchronous mode (f2): the replica the learner fetched (slot 1; slot 0 is the servers' live one)
+    const int slot = ctx->async_mode ? 1 : (int)(k_src % (uint64_t)ctx->H);
     // gradient destination: the shared sum, or (per-message mode) this learner's own buffer
     float* const Gd = ctx->per_msg ? ctx->G_all + (int64_t)j * ctx->W * ctx->q : ctx->G;
     // the round's first learner resets the accepted count; the others add to it (also in
@@ -1418,7 +1423,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     float* theta = c.take<float>(W * q);
     float* m = c.take<float>(q);
     float* v = c.take<float>(q);
-    float* G = c.take<float>((cfg->ps_mode == 1 ? L : 1) * W * q);  // per-message mode: one per learner
+    float* G = c.take<float>((cfg->ps_mode >= 1 ? L : 1) * W * q);  // per-message / async: one per learner
     float* counts = c.take<float>(W + 64);
     uint64_t* V = c.take<uint64_t>(4);
     uint64_t* rinfo = c.take<uint64_t>(4);
@@ -1521,11 +1526,13 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     float* part5 = c.take<float>((int64_t)((B + fc5_rows(B) - 1) / fc5_rows(B)) * nA * (FC4_OUT + 1));
     float* tmp_canon = c.take<float>(P);
     float* tmp_int = c.take<float>(W * q);
+    AsyncState* ast = c.take<AsyncState>(1);  // f2 queue / counters (small; carved in every mode)
     if (ctx) {
         ctx->nA = nA; ctx->B = B; ctx->L = L; ctx->W = W; ctx->P = P; ctx->q = q; ctx->esz = esz;
         ctx->rl = rl; ctx->H = H;
         ctx->theta = theta; ctx->m = m; ctx->v = v; ctx->G = G; ctx->counts = counts; ctx->V = V;
-        ctx->G_all = G; ctx->per_msg = cfg->ps_mode == 1;
+        ctx->G_all = G; ctx->per_msg = cfg->ps_mode >= 1; ctx->async_mode = cfg->ps_mode == 2;
+        ctx->ast = ast;
         ctx->round_info = rinfo;
         ctx->n_acc_local = nacc; ctx->Vhist = Vhist; ctx->dev_round = dev_round; ctx->head_counter = head_counter;
         ctx->pflags = pflags; ctx->p2p_epoch = p2p_epoch; ctx->p2p_counter = p2p_counter;
@@ -1702,14 +1709,18 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
         return fail(GORILA_E_INVALID, "bad optimizer");
     if (cfg->history < 1 || cfg->history > 64) return fail(GORILA_E_INVALID, "history must be in [1, 64]");
     if (cfg->target_period < 1) return fail(GORILA_E_INVALID, "target_period must be >= 1");
-    if (cfg->ps_mode != 0 && cfg->ps_mode != 1) return fail(GORILA_E_INVALID, "ps_mode must be 0 or 1");
+    if (cfg->ps_mode < 0 || cfg->ps_mode > 2) return fail(GORILA_E_INVALID, "ps_mode must be 0, 1 or 2");
+    if (cfg->ps_mode == 2 && cfg->replay_mode != 0)
+        return fail(GORILA_E_INVALID, "asynchronous mode (ps_mode 2) runs local replay only");
+    if (cfg->ps_mode == 2 && cfg->history < 2)
+        return fail(GORILA_E_INVALID, "asynchronous mode (ps_mode 2) needs history >= 2 (live + fetched replica)");
     if (cfg->replay_mode != 0 && cfg->replay_mode != 1) return fail(GORILA_E_INVALID, "replay_mode must be 0 or 1");
     if (cfg->replay_mode == 1 && (cfg->learner_id_base != cfg->rank * cfg->n_learners_local ||
                                   cfg->world * cfg->n_learners_local > MAX_SHARDS))
         return fail(GORILA_E_INVALID, "global replay: learner_id_base must be rank * n_learners_local, "
                                       "at most 256 learners in total");
-    if (cfg->ps_mode == 1 && (cfg->n_learners_local > 32 || cfg->world * cfg->n_learners_local > 64))
-        return fail(GORILA_E_INVALID, "per-message mode: at most 32 learners per rank, 64 in total");
+    if (cfg->ps_mode >= 1 && (cfg->n_learners_local > 32 || cfg->world * cfg->n_learners_local > 64))
+        return fail(GORILA_E_INVALID, "per-message / asynchronous mode: at most 32 learners per rank, 64 in total");
     if (!cfg->theta0) return fail(GORILA_E_INVALID, "theta0 is required");
     if (!cfg->workspace) return fail(GORILA_E_INVALID, "workspace is required");
     if (((uintptr_t)cfg->workspace) % 256) return fail(GORILA_E_INVALID, "workspace must be 256-byte aligned");
@@ -2059,6 +2070,7 @@ static void replay_barrier(gorila_ctx* ctx) {
 gorila_status learner_step(gorila_ctx* ctx, const int32_t* learners, int32_t n, uint64_t round,
                            const int32_t* staleness, gorila_learner_info* info_out) {
     if (!ctx) return fail(GORILA_E_INVALID, "null context");
+    if (ctx->async_mode) return fail(GORILA_E_INVALID, "asynchronous mode (ps_mode 2): use gorila_async_run");
     if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned");
     if (!exchange_ready(ctx)) return fail(GORILA_E_INVALID, "world > 1: connect the peers first (gorila_peer_connect)");
     if (!learners || n < 1 || n > ctx->L) return fail(GORILA_E_SHAPE, "bad learner list");
@@ -2263,6 +2275,7 @@ gorila_status ps_apply_p2p(gorila_ctx* ctx, uint64_t round, gorila_round_info* i
 
 gorila_status ps_apply_shard(gorila_ctx* ctx, uint64_t round, gorila_round_info* info_out) {
     if (!ctx) return fail(GORILA_E_INVALID, "null context");
+    if (ctx->async_mode) return fail(GORILA_E_INVALID, "asynchronous mode (ps_mode 2): use gorila_async_run");
     if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned");
     if (!exchange_ready(ctx)) return fail(GORILA_E_INVALID, "world > 1: connect the peers first (gorila_peer_connect)");
     cudaStream_t st = ctx->stream;
@@ -2568,6 +2581,155 @@ static gorila_status round_impl(gorila_ctx* ctx, const int32_t* learners, int32_
         round_info_out->version_after = tmp[2];
     }
     if (sync && (info_out || synced_out)) CU(cudaStreamSynchronize(st));
+    CU(cudaGetLastError());
+    return GORILA_OK;
+}
+
+// ---------------------------------------------------------------- NEXT row f2: asynchronous PS
+gorila_status gorila_async_run(gorila_ctx* ctx, const int32_t* learners, int32_t n, int64_t steps, uint64_t round0,
+                               int32_t server_blocks, gorila_async_stats* out) {
+    if (!ctx) return fail(GORILA_E_INVALID, "null context");
+    if (ctx->poisoned) return fail(GORILA_E_INVALID, "context poisoned");
+    if (!ctx->async_mode) return fail(GORILA_E_INVALID, "gorila_async_run needs ps_mode 2 (asynchronous)");
+    if (!exchange_ready(ctx)) return fail(GORILA_E_INVALID, "world > 1: connect the peers first (gorila_peer_connect)");
+    if (ctx->W > 1 && !ctx->p2p) return fail(GORILA_E_INVALID, "asynchronous mode needs the peer-memory mapping");
+    if (!learners || n < 1 || n > ctx->L || steps < 0) return fail(GORILA_E_SHAPE, "bad learner list / steps");
+    for (int i = 0; i < n; ++i) {
+        if (learners[i] < 0 || learners[i] >= ctx->L) return fail(GORILA_E_RANGE, "learner id out of range");
+        if (i && learners[i] <= learners[i - 1]) return fail(GORILA_E_INVALID, "learners must be ascending");
+        const Learner& l = ctx->learners[learners[i]];
+        if (std::min<int64_t>(l.n_host, ctx->cfg.replay_capacity) - 1 < std::max<int64_t>(1, ctx->cfg.min_replay))
+            return fail(GORILA_E_NOT_READY, "replay not ready");
+    }
+    cudaStream_t st = ctx->stream;
+    const int W = ctx->W, r = ctx->rank, L = ctx->L;
+    const bool fp32 = ctx->cfg.math == GORILA_MATH_FP32;
+    // the live replica (slot 0) = the latest one; the state and counters start from zero
+    const int latest = (int)(ctx->dev_round_expect % (uint64_t)ctx->H);
+    if (latest != 0)
+        launch(ctx, k_copy_replica, dim3(148 * 2), dim3(256), 0, (const uint4*)ctx->rep_t[latest], (uint4*)ctx->rep_t[0],
+               (int64_t)ctx->rl.n_t * (int64_t)ctx->esz / 16, (const float4*)ctx->rep_f[latest], (float4*)ctx->rep_f[0],
+               (int64_t)ctx->rl.n_f / 4, (const uint8_t*)nullptr);
+    // CUDA's lazy module loading blocks a kernel's first launch until the running kernels finish, which
+    // would stall every learner kernel behind the persistent server: load them all now, with one learner
+    // step whose only lasting effect (the outlier statistics, info) is undone
+    {
+        Learner& l0 = ctx->learners[learners[0]];
+        CU(cudaMemcpyAsync(ctx->tmp_canon, l0.stats, sizeof(LearnerStats), cudaMemcpyDeviceToDevice, st));
+        CU(cudaMemcpyAsync((uint8_t*)ctx->tmp_canon + 256, l0.info, sizeof(DevLearnerInfo), cudaMemcpyDeviceToDevice, st));
+        launch(ctx, k_set_u64, dim3(1), dim3(1), 0, ctx->dev_round, round0);
+        gorila_status s0 = fp32 ? run_learner<float>(ctx, learners[0], round0, 0, 0)
+                                : run_learner<__nv_bfloat16>(ctx, learners[0], round0, 0, 0);
+        if (s0 != GORILA_OK) return s0;
+        CU(cudaMemcpyAsync(l0.stats, ctx->tmp_canon, sizeof(LearnerStats), cudaMemcpyDeviceToDevice, st));
+        CU(cudaMemcpyAsync(l0.info, (uint8_t*)ctx->tmp_canon + 256, sizeof(DevLearnerInfo), cudaMemcpyDeviceToDevice, st));
+        cudaFuncAttributes fa;
+        CU(cudaFuncGetAttributes(&fa, k_async_fetch));
+        CU(cudaFuncGetAttributes(&fa, k_async_send));
+        CU(cudaFuncGetAttributes(&fa, k_async_done));
+        CU(cudaFuncGetAttributes(&fa, k_async_barrier));
+        CU(cudaFuncGetAttributes(&fa, k_copy_replica));
+        CU(cudaFuncGetAttributes(&fa, k_set_u64));
+        CU(cudaFuncGetAttributes(&fa, k_copy_u64));
+        CU(cudaFuncGetAttributes(&fa, k_ps_server<float>));
+        CU(cudaFuncGetAttributes(&fa, k_ps_server<__nv_bfloat16>));
+    }
+    CU(cudaMemsetAsync(ctx->ast, 0, sizeof(AsyncState), st));
+    k_copy_u64<<<1, 1, 0, st>>>(&ctx->ast->V, ctx->V);  // the shard's versions continue from V
+    ctx->launches++;
+    ApplyParams ap{};
+    P2PParams x{};
+    p2p_params(ctx, round0, ap, x);  // this rank's slice bounds / optimizer constants; peer flag areas
+    const uint64_t ep = ++ctx->async_epoch;
+    if (W > 1) launch(ctx, k_async_barrier, dim3(1), dim3(32), 0, x, ep);  // every rank reset before any send
+    CU(cudaStreamSynchronize(st));
+    // the server: a persistent kernel on side2, beside the learner stream
+    ServerParams sp{};
+    sp.p = ap;
+    sp.p.theta = ctx->theta + (int64_t)r * ctx->q;
+    sp.st = ctx->ast;
+    for (int q = 0; q < W; ++q)
+        for (int j = 0; j < L; ++j) {
+            sp.G[q * L + j] = peer_ptr(ctx, q, ctx->G_all + (int64_t)j * W * ctx->q) + (int64_t)r * ctx->q;
+            sp.consumed[q * L + j] = peer_ptr(ctx, q, &ctx->ast->consumed[r][j]);
+        }
+    for (int q = 0; q < W; ++q) {
+        sp.live_t[q] = peer_ptr(ctx, q, (uint8_t*)ctx->rep_t[0]);
+        sp.live_f[q] = peer_ptr(ctx, q, ctx->rep_f[0]);
+    }
+    sp.W = W;
+    sp.max_delay = ctx->cfg.max_staleness;
+    const int nsrv = server_blocks > 0 ? server_blocks : 32;
+    {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(nsrv);
+        cfg.blockDim = dim3(256);
+        cfg.stream = ctx->side2;
+        if (fp32) CU(cudaLaunchKernelEx(&cfg, k_ps_server<float>, sp));
+        else CU(cudaLaunchKernelEx(&cfg, k_ps_server<__nv_bfloat16>, sp));
+        ctx->launches++;
+    }
+    // the learners, round robin on the library stream
+    FetchParams fp{};
+    fp.st = ctx->ast;
+    fp.W = W;
+    fp.period = ctx->cfg.target_period;
+    fp.vhist = ctx->Vhist + 1;
+    for (int q = 0; q < W; ++q) fp.V[q] = &peer_ptr(ctx, q, ctx->ast)->V;
+    SendParams sd{};
+    sd.st = ctx->ast;
+    sd.W = W;
+    for (int q = 0; q < W; ++q) sd.shard[q] = peer_ptr(ctx, q, ctx->ast);
+    const int64_t nt16 = (int64_t)ctx->rl.n_t * (int64_t)ctx->esz / 16, nf4 = (int64_t)ctx->rl.n_f / 4;
+    for (int64_t k = 0; k < steps; ++k) {
+        launch(ctx, k_set_u64, dim3(1), dim3(1), 0, ctx->dev_round, round0 + (uint64_t)k);
+        ctx->dev_round_expect = round0 + (uint64_t)k;
+        for (int i = 0; i < n; ++i) {
+            const int j = learners[i];
+            Learner& l = ctx->learners[j];
+            fp.j = j;
+            fp.stats = l.stats;
+            fp.sync_flag = l.sync_flag;
+            fp.info = l.info;
+            launch(ctx, k_async_fetch, dim3(1), dim3(1), 0, fp);
+            launch(ctx, k_copy_replica, dim3(148), dim3(256), 0, (const uint4*)ctx->rep_t[0], (uint4*)ctx->rep_t[1],
+                   nt16, (const float4*)ctx->rep_f[0], (float4*)ctx->rep_f[1], nf4, (const uint8_t*)nullptr);
+            launch(ctx, k_copy_replica, dim3(148), dim3(256), 0, (const uint4*)ctx->rep_t[1], (uint4*)l.tminus_t, nt16,
+                   (const float4*)ctx->rep_f[1], (float4*)l.tminus_f, nf4, (const uint8_t*)l.sync_flag);
+            gorila_status s = fp32 ? run_learner<float>(ctx, j, round0 + (uint64_t)k, 0, 0)
+                                   : run_learner<__nv_bfloat16>(ctx, j, round0 + (uint64_t)k, 0, 0);
+            if (s != GORILA_OK) return s;
+            sd.j = j;
+            sd.gid = ctx->cfg.learner_id_base + j;
+            sd.info = l.info;
+            launch(ctx, k_async_send, dim3(1), dim3(1), 0, sd);
+        }
+    }
+    launch(ctx, k_async_done, dim3(1), dim3(1), 0, sd);
+    CU(cudaStreamSynchronize(st));
+    CU(cudaStreamSynchronize(ctx->side2));
+    AsyncState h;
+    CU(cudaMemcpy(&h, ctx->ast, sizeof(AsyncState), cudaMemcpyDeviceToHost));
+    if (h.err)
+        return fail(GORILA_E_CUDA, "asynchronous run: a bounded wait timed out (code " + std::to_string(h.err) +
+                                       "; 1 server/message, 2 server/decision, 3 learner/consumed; learner progress " +
+                                       std::to_string(h.progress) + ", tail " + std::to_string(h.tail) + ")");
+    // the deterministic API's version record and next replica slot follow the live state
+    launch(ctx, k_set_u64, dim3(1), dim3(1), 0, ctx->V, h.V);
+    ctx->dev_round_expect = 0;  // the live replica is slot 0
+    CU(cudaStreamSynchronize(st));
+    if (out) {
+        out->steps = (uint64_t)steps * (uint64_t)n;
+        uint64_t sent = 0;
+        for (int j = 0; j < L; ++j) sent += h.sent[j];
+        out->sent = sent;
+        out->fresh = h.n_fresh;
+        out->stale = h.n_stale;
+        out->rejected = h.n_rejected;
+        out->version_after = h.V;
+        out->max_delay = h.max_delay_seen;
+        out->mean_delay = (h.n_fresh + h.n_stale) ? (double)h.delay_sum / (double)(h.n_fresh + h.n_stale) : 0.0;
+    }
     CU(cudaGetLastError());
     return GORILA_OK;
 }

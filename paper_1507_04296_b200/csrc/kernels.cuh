@@ -1208,7 +1208,7 @@ struct P2PParams {
 };
 // flag-area slots (u64) of the per-message exchange, besides the ready / done flags and counts
 constexpr int FLAG_BASE = 6 * MAX_W, FLAG_LAST = FLAG_BASE + MAX_MSG, FLAG_V0 = FLAG_LAST + MAX_MSG,
-              FLAG_WORDS = FLAG_V0 + MAX_W;
+              FLAG_ASYNC = FLAG_V0 + MAX_W, FLAG_WORDS = FLAG_ASYNC + MAX_W;
 
 
 // phase: flag set (0 = the fc4 weight region, launched early by gorila_round; 1 = the rest);

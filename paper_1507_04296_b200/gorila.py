@@ -58,6 +58,15 @@ class RoundInfo(ctypes.Structure):
                 ("version_after", ctypes.c_uint64)]
 
 
+class AsyncStats(ctypes.Structure):
+    _fields_ = [("steps", ctypes.c_uint64), ("sent", ctypes.c_uint64), ("fresh", ctypes.c_uint64),
+                ("stale", ctypes.c_uint64), ("rejected", ctypes.c_uint64), ("version_after", ctypes.c_uint64),
+                ("max_delay", ctypes.c_uint64), ("mean_delay", ctypes.c_double)]
+
+    def as_dict(self):
+        return {k: getattr(self, k) for k, _ in self._fields_}
+
+
 EXPORTS = ["gorila_param_count", "gorila_workspace_bytes", "gorila_init", "gorila_destroy", "gorila_last_error",
            "replay_insert", "replay_sample", "replay_sample_shards", "learner_step", "ps_apply_shard", "sync_target", "gorila_get_state",
            "gorila_set_state", "gorila_get_learner_state", "gorila_set_learner_state", "gorila_get_grad",
@@ -65,7 +74,7 @@ EXPORTS = ["gorila_param_count", "gorila_workspace_bytes", "gorila_init", "goril
            "gorila_profile_phase_count", "gorila_profile_phase_name", "gorila_nccl_unique_id", "gorila_round",
            "gorila_round_async", "gorila_round_post", "gorila_round_fetch",
            "gorila_bench_phase", "gorila_debug_trace", "gorila_capture_activations",
-           "gorila_get_learner_activation", "gorila_peer_record", "gorila_peer_connect"]
+           "gorila_get_learner_activation", "gorila_peer_record", "gorila_peer_connect", "gorila_async_run"]
 
 
 def load(build_if_missing=True):
@@ -103,6 +112,7 @@ def load(build_if_missing=True):
     L.gorila_capture_activations.argtypes = [P, i32]
     L.gorila_peer_record.argtypes = [P, P]
     L.gorila_peer_connect.argtypes = [P, P, i32]
+    L.gorila_async_run.argtypes = [P, P, i32, i64, u64, i32, ctypes.POINTER(AsyncStats)]
     L.gorila_get_learner_activation.argtypes = [P, i32, i32, P, u64]
     L.gorila_round_post.argtypes = [P, P, i32, u64, P]
     L.gorila_round_fetch.argtypes = [P, u64, P, P, P]
@@ -187,7 +197,7 @@ class Gorila:
                      ada_eps=ada_eps, target_period=target_period, max_staleness=max_staleness,
                      outlier_enabled=int(outlier_enabled), outlier_warmup=outlier_warmup, outlier_k=outlier_k,
                      outlier_beta=outlier_beta, min_replay=min_replay, seed=seed,
-                     ps_mode={"aggregate": 0, "per_message": 1}[ps_mode],
+                     ps_mode={"aggregate": 0, "per_message": 1, "async": 2}[ps_mode],
                      replay_mode={"local": 0, "global": 1}[replay_mode],
                      math={"fp32": 0, "bf16": 2}[math], history=history, theta0=theta0.ctypes.data)
         nbytes = int(L.gorila_workspace_bytes(ctypes.byref(cfg)))
@@ -383,6 +393,15 @@ class Gorila:
         out = np.zeros((self.batch,) + shp, np.uint16 if bf else np.float32)
         _check(load().gorila_get_activation(self.h, which, out.ctypes.data, out.nbytes))
         return (out.astype(np.uint32) << 16).view(np.float32) if bf else out
+
+    def async_run(self, learners, steps, round0=0, server_blocks=0):
+        """NEXT row f2 (ps_mode="async"): `steps` asynchronous learner steps per listed learner while the
+        persistent shard server applies their messages; returns the counts (include/gorila.h)."""
+        arr = np.ascontiguousarray(learners, np.int32)
+        st = AsyncStats()
+        _check(load().gorila_async_run(self.h, arr.ctypes.data, len(arr), int(steps), int(round0), int(server_blocks),
+                                       ctypes.byref(st)))
+        return st.as_dict()
 
     def capture_activations(self, on=True):
         """Parity diagnostics: keep every learner's a1..a4 of each later learner step."""

@@ -36,7 +36,8 @@ def make_pair(nA=4, B=32, C=2000, n_insert=2000, math="fp32", L=1, history=2, p_
                     outlier_enabled=bool(kw.get("outlier_enabled", True)), outlier_warmup=kw.get("outlier_warmup", 100),
                     outlier_k=kw.get("outlier_k", 3.0), outlier_beta=kw.get("outlier_beta", 0.999),
                     min_replay=kw.get("min_replay", 1), seed_sample=kw.get("seed", 1507),
-                    ps_mode=kw.get("ps_mode", "aggregate"), replay_mode=kw.get("replay_mode", "local"))
+                    ps_mode=kw.get("ps_mode", "aggregate") if kw.get("ps_mode") != "async" else "per_message",
+                    replay_mode=kw.get("replay_mode", "local"))
     orc = O.GorilaOracle(ocfg, theta0)
     for j in range(L):
         f = synth.frames(synth.SEED_DATA, j, 0, n_insert)

@@ -96,7 +96,7 @@ def _base_cfg(G, theta):
     ("replay_capacity", 1, "replay_capacity"), ("n_learners_local", 0, "n_learners_local"),
     ("world", 0, "rank/world"), ("rank", 1, "rank/world"), ("math", 1, "math"),
     ("history", 0, "history"), ("history", 65, "history"), ("target_period", 0, "target_period"),
-    ("ps_mode", 2, "ps_mode"), ("replay_mode", 2, "replay_mode"), ("theta0", None, "theta0"),
+    ("ps_mode", 3, "ps_mode"), ("ps_mode", -1, "ps_mode"), ("replay_mode", 2, "replay_mode"), ("theta0", None, "theta0"),
     (None, None, "workspace"),
 ])
 def test_init_rejects_invalid_config_before_any_cuda_call(field, value, msg):

@@ -56,3 +56,16 @@ def test_sharded_ps_one_rank_per_gpu_nccl(math, mode):
 def _first_gpu():
     v = os.environ.get("CUDA_VISIBLE_DEVICES")
     return v.split(",")[0] if v else "0"
+
+
+@pytest.mark.parametrize("n", [2, 4])
+def test_async_ps_several_ranks_one_gpu(n):
+    """NEXT row f2 across ranks: every rank's shard server applies every rank's messages as they arrive
+    (tools/async_check.py: counts add up on every shard, theta^+ agrees across ranks)."""
+    env = dict(os.environ, BOOTSTRAP="ipc", CUDA_VISIBLE_DEVICES=_first_gpu(), STEPS="8")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={n}",
+           "--master-addr", "127.0.0.1", "--master-port", str(29950 + (os.getpid() % 40) + 3 * n),
+           os.path.join(ROOT, "tools", "async_check.py")]
+    out = subprocess.run(cmd, env=env, capture_output=True, text=True, timeout=900)
+    assert out.returncode == 0 and "ASYNC CHECK OK" in out.stdout, out.stdout[-4000:] + out.stderr[-3000:]
+    print(out.stdout)
