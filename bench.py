@@ -223,6 +223,67 @@ def cpu_baseline(args, budget_s):
                       f"{cap}-frame replay (per-update work does not depend on replay size), {el:.1f} s"}
 
 
+C1_SCRIPT = r"""
+import os, sys, time
+sys.path.insert(0, {root!r})
+import oracle as O, synth
+cfg = O.Config(n_actions=4, batch=32, capacity=10_000, mode="exact", target_period=100)
+orc = O.GorilaOracle(cfg, synth.theta0(4))
+f = synth.frames(synth.SEED_DATA, 0, 0, 10_000)
+a, r, d = synth.meta(synth.SEED_DATA, 0, 0, 10_000, 4)
+orc.insert(0, f, a, r, d)
+t0 = time.perf_counter()
+for k in range(10):
+    orc.round(k)
+print("C1_SECONDS", time.perf_counter() - t0)
+"""
+
+
+def c1_timing(g_factory):
+    """BASELINE configs[0] (C1: nA=4, B=32, 10k transitions, 10 RMSProp steps) in seconds: the oracle as it
+    stands at 1 OpenMP thread and at nproc threads (separate processes so the OpenMP
+    runtime takes each thread count), and the GPU path's device time for the same 10 rounds."""
+    out = {"nproc": os.cpu_count(), "cpu_model": None}
+    try:
+        with open("/proc/cpuinfo") as f:
+            out["cpu_model"] = next((l.split(":", 1)[1].strip() for l in f if l.startswith("model name")), None)
+    except OSError:
+        pass
+    for key, threads in (("oracle_s_1thread", 1), ("oracle_s_nproc", os.cpu_count() or 1)):
+        env = dict(os.environ, OMP_NUM_THREADS=str(threads))
+        r = subprocess.run([sys.executable, "-c", C1_SCRIPT.format(root=ROOT)], env=env, capture_output=True, text=True,
+                           timeout=600)
+        vals = [l.split()[1] for l in r.stdout.splitlines() if l.startswith("C1_SECONDS")]
+        out[key] = float(vals[0]) if vals else None
+    out["gpu_s"] = g_factory()
+    out["note"] = "10 learner updates of configs[0]; oracle wall clock (steady perf_counter) per process; GPU: " \
+                  "device time of 10 graph rounds after 10 warm-up rounds (CUDA events)"
+    return out
+
+
+def gpu_c1_seconds():
+    import torch
+    import synth
+    from paper_1507_04296_b200 import Gorila
+    st = torch.cuda.current_stream()
+    g = Gorila(n_actions=4, batch=32, replay_capacity=10_000, theta0=synth.theta0(4), stream=st, math="bf16")
+    f = synth.frames(synth.SEED_DATA, 0, 0, 10_000)
+    a, r, d = synth.meta(synth.SEED_DATA, 0, 0, 10_000, 4)
+    g.replay_insert(0, f, a, r, d)
+    ids = np.zeros(1, np.int32)
+    for k in range(10):
+        g.round(ids, k)
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    st.synchronize()
+    e0.record(st)
+    for k in range(10, 20):
+        g.round(ids, k)
+    e1.record(st)
+    st.synchronize()
+    g.close()
+    return e0.elapsed_time(e1) / 1000.0
+
+
 def run_reference(args, json_out):
     world, rank, _ = dist_env()
     if rank != 0:
@@ -594,6 +655,7 @@ def main():
         }
         if world == 1 and not args.no_cpu_baseline:
             out["cpu_baseline"] = cpu_baseline(args, args.cpu_seconds)
+            out["c1_seconds"] = c1_timing(gpu_c1_seconds)
         print(json.dumps(out), file=json_out, flush=True)
     g.close()
     if world > 1:
