@@ -155,7 +155,45 @@ __global__ void __launch_bounds__(256) k_sample(const uint8_t* __restrict__ fram
             keep_s2[c] = k2;
         }
     }
-    if (chunk < FRAME_BYTES / 16) {
+    if constexpr (sizeof(T) == 2) {
+        // bf16: each thread's 16 pixels x 4 channels = 8 uint4 per stack, staged in shared memory
+        // (rows XOR-rotated: conflict-free) and written out block-contiguously (every warp store one
+        // 512-B run instead of 32 runs of 16 B at a 128-B stride)
+        __shared__ uint4 stage[256 * 8];
+        const uint8_t* fb[5];
+#pragma unroll
+        for (int t = 0; t < 5; ++t) fb[t] = reinterpret_cast<const uint8_t*>(&f[t]);
+        const int nvalid = min(FRAME_BYTES / 16 - (int)(blockIdx.x * blockDim.x), (int)blockDim.x);
+#pragma unroll
+        for (int half = 0; half < 2; ++half) {
+            if (chunk < FRAME_BYTES / 16) {
+#pragma unroll
+                for (int v = 0; v < 8; ++v) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int e = 0; e < 4; ++e) {
+                        float x2[2];
+#pragma unroll
+                        for (int h = 0; h < 2; ++h) {
+                            const int el = v * 8 + 2 * e + h, px = el >> 2, c = el & 3;
+                            const bool keep = half ? keep_s2[c] : keep_s[c];
+                            x2[h] = keep ? (float)fb[c + half][px] : 0.f;
+                        }
+                        __nv_bfloat162 hh = __floats2bfloat162_rn(x2[0], x2[1]);
+                        w[e] = *reinterpret_cast<uint32_t*>(&hh);
+                    }
+                    stage[threadIdx.x * 8 + ((v + threadIdx.x) & 7)] = make_uint4(w[0], w[1], w[2], w[3]);
+                }
+            }
+            __syncthreads();
+            T* dst = (half ? s2_out : s_out) + ((int64_t)b * FRAME_BYTES + (int64_t)blockIdx.x * blockDim.x * 16) * NSTACK;
+            for (int o = threadIdx.x; o < nvalid * 8; o += blockDim.x) {
+                const int i = o >> 3, v = o & 7;
+                reinterpret_cast<uint4*>(dst)[o] = stage[i * 8 + ((v + i) & 7)];
+            }
+            __syncthreads();
+        }
+    } else if (chunk < FRAME_BYTES / 16) {
         const uint8_t* fb[5];
 #pragma unroll
         for (int t = 0; t < 5; ++t) fb[t] = reinterpret_cast<const uint8_t*>(&f[t]);

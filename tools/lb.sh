@@ -1,3 +1,3 @@
-KREGEX="k_fc5" EXTRA="--batch 4096 --capacity 100000 --e2e-steps 2" SKIP=2 COUNT=4 OUT=fc5 bash tools/ncu_full.sh
-python tools/ncu_summary.py gpurun_out/fc5.ncu-rep
-ncu -i gpurun_out/fc5.ncu-rep --page details --csv 2>/dev/null | grep -i "warp cycles per issued\|Stall\|Issued Warp\|Achieved Occupancy\|Duration" | head -40
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "replay or c1" 2>&1 | tail -2
+timeout 300 python tools/qbench.py --batch 4096 --steps 30 --reps 2 --phases sample 2>&1 | tail -2
+timeout 300 python tools/qbench.py --steps 3000 --reps 2 --phases sample 2>&1 | tail -2
