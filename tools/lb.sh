@@ -1,3 +1,4 @@
-timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "replay or c1" 2>&1 | tail -2
-timeout 300 python tools/qbench.py --batch 4096 --steps 30 --reps 2 --phases sample 2>&1 | tail -2
-timeout 300 python tools/qbench.py --steps 3000 --reps 2 --phases sample 2>&1 | tail -2
+KREGEX="gemm|k_conv_tower|k_sample|k_apply|k_fc5|k_bias|k_wgrad" EXTRA="--batch 4096 --capacity 100000 --e2e-steps 2" SKIP=40 COUNT=20 OUT=b4096 bash tools/ncu_full.sh
+python tools/ncu_summary.py gpurun_out/b4096.ncu-rep > gpurun_out/b4096_summary.txt; cat gpurun_out/b4096_summary.txt
+KREGEX="gemm|k_conv_tower|k_sample|k_apply|k_fc5|k_bias|k_wgrad|k_pack" EXTRA="--e2e-steps 2" SKIP=100 COUNT=17 OUT=b32 bash tools/ncu_full.sh
+python tools/ncu_summary.py gpurun_out/b32.ncu-rep > gpurun_out/b32_summary.txt; cat gpurun_out/b32_summary.txt
