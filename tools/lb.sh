@@ -1,4 +1,2 @@
-KREGEX="gemm|k_conv_tower|k_sample|k_apply|k_fc5|k_bias|k_wgrad" EXTRA="--batch 4096 --capacity 100000 --e2e-steps 2" SKIP=40 COUNT=20 OUT=b4096 bash tools/ncu_full.sh
-python tools/ncu_summary.py gpurun_out/b4096.ncu-rep > gpurun_out/b4096_summary.txt; cat gpurun_out/b4096_summary.txt
-KREGEX="gemm|k_conv_tower|k_sample|k_apply|k_fc5|k_bias|k_wgrad|k_pack" EXTRA="--e2e-steps 2" SKIP=100 COUNT=17 OUT=b32 bash tools/ncu_full.sh
-python tools/ncu_summary.py gpurun_out/b32.ncu-rep > gpurun_out/b32_summary.txt; cat gpurun_out/b32_summary.txt
+timeout 300 python -m pytest tests/test_gpu_parity.py -q -x -k "c1 or graph or ragged" 2>&1 | tail -2
+for kv in "GORILA_FUSE_SAMPLE=0" "X=1" "GORILA_FUSE_SAMPLE=0" "X=1"; do env $kv timeout 200 python tools/qbench.py --reps 2 2>&1 | tail -1; done
