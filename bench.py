@@ -484,8 +484,16 @@ def main():
     for _ in range(args.warmup):
         step(k)
         k += 1
+    # the timed region must contain target syncs (every target_period versions, one per accepted round
+    # here): with fewer timed steps than the period, run untimed rounds up to half a period before a sync
+    if args.steps < args.target_period and args.learners == 1:
+        for _ in range(max(0, args.target_period - k - args.steps // 2)):
+            step(k)
+            k += 1
     stream.synchronize()
     barrier(world)
+    sync0 = g.get_learner_state(0)[1]["last_sync"]
+    V0 = g.get_state()[3]
 
     # ---------------- timed region (device time, CUDA events on the launching stream)
     ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
@@ -500,6 +508,8 @@ def main():
     stream.synchronize()
     barrier(world)
     launches = g.kernel_launches() - launches0
+    sync1 = g.get_learner_state(0)[1]["last_sync"]
+    V1 = g.get_state()[3]
     ms_local = ev0.elapsed_time(ev1)
     ms = max_over_ranks(ms_local, world)
     value = world * L * args.steps / (ms / 1000.0)
@@ -625,6 +635,9 @@ def main():
             "frames_per_s": value * args.batch,
             "config": config_dict(args, world),
             "gpu_launches": int(launches),
+            "timed_region_versions": {"V_before": int(V0), "V_after": int(V1), "last_target_sync_before": int(sync0),
+                                      "last_target_sync_after": int(sync1),
+                                      "target_syncs": int((V1 - sync0) // args.target_period) if V1 > sync0 else 0},
             "clocks": clocks,
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": 7056 + 1 + 4 + 1,
                     "d2h_bytes_per_step": 48 + 24 + 1,
