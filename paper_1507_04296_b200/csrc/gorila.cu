@@ -1758,8 +1758,13 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     CU(cudaMemsetAsync(ctx->replay_epoch, 0, sizeof(uint64_t), st));
     ctx->dev_round_expect = 0;
     {
-        const char* e = getenv("GORILA_PDL");  // GORILA_PDL=0 disables programmatic dependent launch
-        ctx->pdl = !(e && atoi(e) == 0);
+        // programmatic dependent launch: on for small batches (a kernel's launch and prologue overlap its
+        // predecessor: the B = 32 step is a latency chain); off from B = 2048, where the early-resident
+        // CTAs of the next persistent GEMM measured 1.5% slower at B = 4096 (965 vs 980 us/step; at
+        // B <= 1024 it is 3-8% faster).
+        // GORILA_PDL=0 / 1 forces it.
+        const char* e = getenv("GORILA_PDL");
+        ctx->pdl = e ? atoi(e) != 0 : cfg->batch < 2048;
         const char* tw = getenv("GORILA_TOWER");
         if (tw && atoi(tw) == 0) ctx->tower = false;
         const char* sh = getenv("GORILA_SHIFT");
