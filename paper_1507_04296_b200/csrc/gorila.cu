@@ -1504,14 +1504,18 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
             const int nch = l == 0 ? 5 * B : B, ta = l == 0 ? 2 : l == 1 ? 4 : 5;
             // partials per weight (the critical-path reduce reads them all); conv1's weight gradient
             // is itself on the critical path (the last GEMM of the dgrad chain): it keeps more splits
-            static const int cap23 = [] {  // B = 32 sweep (tools/knob_sweep2.sh): 4: 76.9, 6: 76.9,
+            static const int cap23_env = [] {  // B = 32 sweep (tools/knob_sweep2.sh): 4: 76.9, 6: 76.9,
                 const char* e = getenv("GORILA_WSPLIT_MAX");  // 8: 75.7, 11: 78.5, 16: 78.5 us/step
-                return e ? std::max(1, atoi(e)) : 8;
+                return e ? std::max(1, atoi(e)) : 0;
             }();
-            static const int cap1 = [] {
+            static const int cap1_env = [] {
                 const char* e = getenv("GORILA_WSPLIT1_MAX");
-                return e ? std::max(1, atoi(e)) : 16;
+                return e ? std::max(1, atoi(e)) : 0;
             }();
+            // B = 256 sweep (r02): conv1 37 / conv2-3 16 splits: 162.9 us/step vs 173.7 with 16 / 8;
+            // no change at B = 128
+            const int cap1 = cap1_env ? cap1_env : (B <= 128 ? 16 : 37);
+            const int cap23 = cap23_env ? cap23_env : (B <= 128 ? 8 : 16);
             const int cap = l == 0 ? cap1 : cap23;
             // small batches: the weight-gradient GEMMs run beside the dgrad chain and can afford
             // fewer, longer splits; large batches need every SM on them

@@ -1,6 +1,3 @@
 #!/bin/bash
-for b in 2048; do
-  for kv in "GORILA_PDL=1" "GORILA_PDL=0"; do
-    env $kv timeout 120 python tools/qbench.py --batch $b --steps 40 --reps 2 --capacity 100000 2>&1 | tail -1
-  done
-done
+for b in 32 256; do timeout 120 python tools/qbench.py --batch $b --steps 1000 --reps 2 --capacity 100000 2>&1 | tail -1; done
+timeout 600 python -m pytest tests/test_gpu_parity.py -q -x -k "large_batch or c1" 2>&1 | tail -2
