@@ -95,6 +95,30 @@ GORILA_DEV void umma_bf16(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint3
         "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
         : "memory");
 }
+// Warp-uniform issue: the whole warp executes the call and elect.sync picks the issuing lane. With
+// the issuing loop and its operands warp-uniform (warp_uniform() / uniform_u32() make that visible
+// to the compiler), descriptors and TMEM addresses stay in uniform registers and an MMA issues with
+// no R2UR moves or ELECT waterfall per instruction (tools/mma_rate_probe.cu, every SM issuing:
+// M64 N32 24 vs 45 cycles per MMA, M128 N32 40 vs 45).
+GORILA_DEV void umma_bf16_w(uint32_t d_tmem, uint64_t adesc, uint64_t bdesc, uint32_t idesc, uint32_t accumulate) {
+    asm volatile(
+        "{\n\t.reg .pred p, e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "setp.ne.b32 p, %4, 0;\n\t"
+        "@e tcgen05.mma.cta_group::1.kind::f16 [%0], %1, %2, %3, p;\n\t}" ::"r"(d_tmem),
+        "l"(adesc), "l"(bdesc), "r"(idesc), "r"(accumulate)
+        : "memory");
+}
+GORILA_DEV void umma_commit_w(uint64_t* bar) {
+    asm volatile(
+        "{\n\t.reg .pred e;\n\t"
+        "elect.sync _|e, 0xffffffff;\n\t"
+        "@e tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];\n\t}" ::"r"(smem_u32(bar))
+        : "memory");
+}
+GORILA_DEV int warp_uniform() { return __shfl_sync(0xffffffffu, (int)(threadIdx.x >> 5), 0); }
+GORILA_DEV uint32_t uniform_u32(uint32_t v) { return __shfl_sync(0xffffffffu, v, 0); }
+GORILA_DEV uint64_t uniform_u64(uint64_t v) { return __shfl_sync(0xffffffffu, (unsigned long long)v, 0); }
 // arrive on an mbarrier once all previously issued tcgen05.mma of this thread complete
 GORILA_DEV void umma_commit(uint64_t* bar) {
     asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
@@ -249,11 +273,11 @@ GORILA_DEV uint64_t umma_desc_sw(uint32_t saddr, uint32_t row_bytes) {
     d |= layout << 61;
     return d;
 }
-// MN-major swizzled layouts (TMA SWIZZLE_128B / 64B, boxes of 64 / 32 MN elements): K rows of
-// 128 / 64 B, 8-row atoms; LBO = byte stride between MN blocks of 64 / 32 elements, SBO = byte
-// stride between 8-row K groups (the roles are swapped relative to the no-swizzle layout).
+// MN-major swizzled layouts (SWIZZLE_128B / 64B / 32B, blocks of 64 / 32 / 16 MN elements): K rows
+// of 128 / 64 / 32 B, 8-row atoms; LBO = byte stride between MN blocks, SBO = byte stride between
+// 8-row K groups (the roles are swapped relative to the no-swizzle layout).
 GORILA_DEV uint64_t umma_desc_mn_sw(uint32_t saddr, uint32_t lbo, uint32_t row_bytes) {
-    const uint64_t layout = row_bytes == 128 ? 2ull : 4ull;
+    const uint64_t layout = row_bytes == 128 ? 2ull : row_bytes == 64 ? 4ull : 6ull;
     uint64_t d = 0;
     d |= (uint64_t)((saddr >> 4) & 0x3FFF);
     d |= (uint64_t)((lbo >> 4) & 0x3FFF) << 16;

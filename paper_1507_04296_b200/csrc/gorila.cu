@@ -215,6 +215,9 @@ struct gorila_ctx {
     // GORILA_SHIFT=<mask> selects, 0 = im2col boxes everywhere
     int shift = 31;
     bool tower = true;  // small-batch bf16 forward: conv1..conv3 fused per (net, sample) (GORILA_TOWER=0: off)
+    // large-batch bf16 (B > 74): s / s' staged as u8 in row-phase-major order, expanded to bf16 inside
+    // conv1's forward and weight-gradient kernels (shift_gemm.cuh U8Planes; GORILA_U8=0: bf16 NHWC)
+    bool u8 = false;
     // side stream for the weight-gradient GEMMs, which are off the dgrad critical path
     // (a fork / join of the round; a graph captures it as parallel branches)
     cudaStream_t side = nullptr;
@@ -801,6 +804,16 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     {
         dim3 grid((FRAME_BYTES / 16 + 255) / 256, B);
         uint2 key = make_uint2((uint32_t)cfg.seed, (uint32_t)(cfg.seed >> 32));
+        using ST = std::conditional_t<fp32v, T, uint8_t>;  // (bf16: u8 staging when ctx->u8)
+        if (!fp32v && ctx->u8)
+            launch(ctx, k_sample<ST>, grid, dim3(256), 0, (const uint8_t*)Lr.frames, (const uint8_t*)Lr.a,
+                   (const float*)Lr.r, (const uint8_t*)Lr.d, (int64_t)cfg.replay_capacity, (const uint64_t*)Lr.n_dev,
+                   (const ShardPtrs*)(ctx->replay_global ? ctx->shard_tab : nullptr), ctx->n_shards,
+                   (const uint64_t*)(ctx->replay_global && ctx->W > 1 && !replay_barrier_off() ? ctx->n_snap : nullptr),
+                   ctx->sshard, key,
+                   (uint32_t)(cfg.learner_id_base + j), (const uint64_t*)ctx->dev_round, B, (ST*)ctx->s, (ST*)ctx->s2,
+                   ctx->sa, ctx->sr, ctx->sd, ctx->sidx, first_learner ? ctx->n_acc_local : (uint32_t*)nullptr);
+        else
         launch(ctx, k_sample<T>, grid, dim3(256), 0, (const uint8_t*)Lr.frames, (const uint8_t*)Lr.a,
                (const float*)Lr.r, (const uint8_t*)Lr.d, (int64_t)cfg.replay_capacity, (const uint64_t*)Lr.n_dev,
                (const ShardPtrs*)(ctx->replay_global ? ctx->shard_tab : nullptr), ctx->n_shards,
@@ -854,6 +867,16 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                 {{s, M}, {rt + RL.w1, K1, C1_OUT, K1}, {a1, C1_OUT, rf + RL.b1, in_scale, M, C1_OUT, 1}},
                 {{s2, M}, {tt + RT.w1, K1, C1_OUT, K1}, {t1, C1_OUT, tf + RT.b1, in_scale, M, C1_OUT, 1}}};
             gemm<T, 32>(ctx, pr, 2, M, C1_OUT, K1, 1);
+        } else if (ctx->u8) {  // shifted windows over the row phases, expanded from the u8 staging
+            using OA = ShConv1FwdU8; using OB = ShWeightK<32, 32, 16, 2>; using EP = EpAct<T>;
+            ShiftProb<OA, OB, EP> pr[2];
+            for (int z = 0; z < 2; ++z) {
+                pr[z].a.src = (const uint8_t*)(z ? ctx->s2 : ctx->s);
+                pr[z].a.batch = B;
+                pr[z].b = sh_wk<32, 32, 16, 2>(ctx, z ? (const void*)(tt + RT.w1) : (const void*)(rt + RL.w1), K1);
+                pr[z].ep = {z ? t1 : a1, C1_OUT, z ? tf + RT.b1 : rf + RL.b1, in_scale, M, C1_OUT, 1};
+            }
+            gemm_shift_launch<32, 4>(ctx, pr, 2, C1_OUT);
         } else if ((ctx->shift & 1) && 2 * B > ctx->num_sms) {  // shifted windows over the row phases of s
 #define SH_C1(MS_, MB_)                                                                                        \
     {                                                                                                          \
@@ -1224,6 +1247,23 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             GemmProb<LA, LB, EP> pr[1] = {{{s, Mred}, {g1, C1_OUT, C1_OUT, Mred},
                                            {ctx->part_w[0], K1, (int64_t)C1_OUT * K1, in_scale, K1, C1_OUT}}};
             gemm<T, 32>(ctx, pr, 1, K1, C1_OUT, Mred, ctx->split_w[0]);
+        } else if (ctx->u8) {  // shifted windows over the u8-staged s, one partial per CTA
+            Conv1WgradU8 wp;
+            {
+                const uint64_t dims[4] = {32, 20, 20, (uint64_t)B}, str[3] = {64, 20 * 64, 400 * 64};
+                const uint32_t box[4] = {32, 21, 20, 1};
+                wp.g1_map = tmap(ctx, g1, 4, dims, str, box, nullptr, 64);
+            }
+            wp.s8 = (const uint8_t*)ctx->s;
+            wp.part = ctx->part_w[0];
+            wp.scale = in_scale;
+            wp.batch = B;
+            static bool attr = false;
+            if (!attr) {
+                cudaFuncSetAttribute(k_conv1_wgrad_u8, cudaFuncAttributeMaxDynamicSharedMemorySize, c1wg::SMEM);
+                attr = true;
+            }
+            launch(ctx, k_conv1_wgrad_u8, dim3(ctx->split_w[0]), dim3(c1wg::THREADS), c1wg::SMEM, wp);
         } else {  // TMA: K-chunk = 4 output rows (80 pixels) of one sample
             using OA = OpWgradIn1S; using OB = OpWgradOutS<32, 80, true>; using EP = EpStoreT;
             TmaProb<OA, OB, EP> pr[1];
@@ -1410,6 +1450,19 @@ P* peer_ptr(gorila_ctx* ctx, int q, P* local) {
     return reinterpret_cast<P*>(ctx->peer_ws[q] + ((uint8_t*)local - ctx->ws_local));
 }
 
+// the u8 staging of s / s' (large-batch bf16, conv1 on the shifted-window path)
+bool u8_staging(const gorila_config* cfg) {
+    static const bool off = [] {
+        const char* e = getenv("GORILA_U8");
+        return e && atoi(e) == 0;
+    }();
+    static const int shift = [] {
+        const char* e = getenv("GORILA_SHIFT");
+        return e ? atoi(e) : 31;
+    }();
+    return !off && (shift & 1) && cfg->math != GORILA_MATH_FP32 && 2 * cfg->batch > 148;
+}
+
 uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) {
     // computes the carve; if ctx != nullptr and base != nullptr fills the pointers
     const int nA = cfg->n_actions, B = cfg->batch, L = cfg->n_learners_local, W = cfg->world;
@@ -1523,6 +1576,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
             const int want = std::max(1, std::min(lim, (148 + ta - 1) / ta));
             const int cps = (nch + want - 1) / want;
             split_w[l] = (nch + cps - 1) / cps;
+            if (l == 0 && u8_staging(cfg)) split_w[0] = std::min(148, B);  // k_conv1_wgrad_u8: one per CTA
         }
         part_w[l] = c.take<float>((int64_t)split_w[l] * wcount[l]);
     }
@@ -1533,6 +1587,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     AsyncState* ast = c.take<AsyncState>(1);  // f2 queue / counters (small; carved in every mode)
     if (ctx) {
         ctx->nA = nA; ctx->B = B; ctx->L = L; ctx->W = W; ctx->P = P; ctx->q = q; ctx->esz = esz;
+        ctx->u8 = u8_staging(cfg);
         ctx->rl = rl; ctx->H = H;
         ctx->theta = theta; ctx->m = m; ctx->v = v; ctx->G = G; ctx->counts = counts; ctx->V = V;
         ctx->G_all = G; ctx->per_msg = cfg->ps_mode >= 1; ctx->async_mode = cfg->ps_mode == 2;
@@ -2948,6 +3003,7 @@ gorila_status gorila_act(gorila_ctx* ctx, const uint8_t* states, int32_t n, uint
     const int64_t total = (int64_t)n * (FRAME_BYTES / 4);
     const int grid = (int)std::min<int64_t>(148 * 8, (total + 255) / 256);
     if (fp32) launch(ctx, k_stage_states<float>, dim3(grid), dim3(256), 0, src, n, (float*)ctx->s);
+    else if (ctx->u8) launch(ctx, k_stage_states_u8, dim3(grid), dim3(256), 0, src, n, (uint8_t*)ctx->s);
     else launch(ctx, k_stage_states<__nv_bfloat16>, dim3(grid), dim3(256), 0, src, n, (__nv_bfloat16*)ctx->s);
     // the forward phases of a learner step on the latest replica (slot of round dev_round_expect)
     const uint32_t fwd = (1u << PH_CONV1F) | (1u << PH_CONV2F) | (1u << PH_CONV3F) | (1u << PH_FC4F);
@@ -2989,6 +3045,23 @@ gorila_status gorila_get_activation(gorila_ctx* ctx, int32_t which, void* host, 
     }
     if (bytes != n) return fail(GORILA_E_SHAPE, "bytes must be " + std::to_string(n));
     CU(cudaStreamSynchronize(ctx->stream));
+    if (which == 0 && ctx->u8) {  // u8 row-phase-major staging -> bf16 NHWC (the values are integers)
+        std::vector<uint8_t> st((size_t)B * FRAME_BYTES * NSTACK);
+        CU(cudaMemcpy(st.data(), src, st.size(), cudaMemcpyDeviceToHost));
+        uint16_t* out = static_cast<uint16_t*>(host);
+        for (uint64_t b = 0; b < B; ++b)
+            for (int y = 0; y < IMG; ++y)
+                for (int x = 0; x < IMG; ++x)
+                    for (int c = 0; c < NSTACK; ++c) {
+                        const uint8_t u = st[b * FRAME_BYTES * NSTACK +
+                                             ((((y & 3) * 21 + (y >> 2)) * 21 + (x >> 2)) * 16) + (x & 3) * 4 + c];
+                        const float f = (float)u;
+                        uint32_t bits;
+                        memcpy(&bits, &f, 4);
+                        out[((b * IMG + y) * IMG + x) * NSTACK + c] = (uint16_t)(bits >> 16);
+                    }
+        return GORILA_OK;
+    }
     CU(cudaMemcpy(host, src, n, cudaMemcpyDeviceToHost));
     return GORILA_OK;
 }

@@ -155,7 +155,32 @@ __global__ void __launch_bounds__(256) k_sample(const uint8_t* __restrict__ fram
             keep_s2[c] = k2;
         }
     }
-    if constexpr (sizeof(T) == 2) {
+    if constexpr (sizeof(T) == 1) {
+        // u8 staging (large batches, shift_gemm.cuh U8Planes): row-phase-major [q][Y][X][px][c] =
+        // s[4Y+q][4X+px][c]; each thread's 16 pixels are four 4-pixel groups of one image row, each
+        // one 16-B output row (a 4 x 4 byte transpose of the four channels' words)
+        if (chunk < FRAME_BYTES / 16) {
+#pragma unroll
+            for (int half = 0; half < 2; ++half) {
+                uint8_t* dst = (half ? s2_out : s_out) + (int64_t)b * (FRAME_BYTES * NSTACK);
+#pragma unroll
+                for (int g = 0; g < 4; ++g) {
+                    uint32_t w[4];
+#pragma unroll
+                    for (int c = 0; c < 4; ++c) {
+                        const bool keep = half ? keep_s2[c] : keep_s[c];
+                        w[c] = keep ? reinterpret_cast<const uint32_t*>(&f[c + half])[g] : 0u;
+                    }
+                    const uint32_t lo01 = __byte_perm(w[0], w[1], 0x5140u), lo23 = __byte_perm(w[2], w[3], 0x5140u);
+                    const uint32_t hi01 = __byte_perm(w[0], w[1], 0x7362u), hi23 = __byte_perm(w[2], w[3], 0x7362u);
+                    const int px = chunk * 16 + 4 * g, y = px / IMG, X = (px - y * IMG) >> 2;
+                    reinterpret_cast<uint4*>(dst)[((y & 3) * 21 + (y >> 2)) * 21 + X] =
+                        make_uint4(__byte_perm(lo01, lo23, 0x5410u), __byte_perm(lo01, lo23, 0x7632u),
+                                   __byte_perm(hi01, hi23, 0x5410u), __byte_perm(hi01, hi23, 0x7632u));
+                }
+            }
+        }
+    } else if constexpr (sizeof(T) == 2) {
         // bf16: each thread's 16 pixels x 4 channels = 8 uint4 per stack, staged in shared memory
         // (rows XOR-rotated: conflict-free) and written out block-contiguously (every warp store one
         // 512-B run instead of 32 runs of 16 B at a 128-B stride)
@@ -770,6 +795,24 @@ __global__ void k_stage_states(const uint8_t* __restrict__ st, int n, T* __restr
         for (int p = 0; p < 4; ++p)
 #pragma unroll
             for (int c = 0; c < 4; ++c) dst[p * 4 + c] = fromf<T>((float)((c4[c] >> (8 * p)) & 0xffu));
+    }
+}
+// the same states in the u8 row-phase-major staging of the large-batch conv1 (one thread per 4-pixel group)
+__global__ void k_stage_states_u8(const uint8_t* __restrict__ st, int n, uint8_t* __restrict__ s_out) {
+    pdl_wait();
+    pdl_trigger();
+    const int64_t total = (int64_t)n * (FRAME_BYTES / 4);
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = i / (FRAME_BYTES / 4);
+        const int px = (int)(i - b * (FRAME_BYTES / 4)) * 4, y = px / IMG, X = (px - y * IMG) >> 2;
+        uint32_t w[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) w[c] = *reinterpret_cast<const uint32_t*>(st + (b * 4 + c) * FRAME_BYTES + px);
+        const uint32_t lo01 = __byte_perm(w[0], w[1], 0x5140u), lo23 = __byte_perm(w[2], w[3], 0x5140u);
+        const uint32_t hi01 = __byte_perm(w[0], w[1], 0x7362u), hi23 = __byte_perm(w[2], w[3], 0x7362u);
+        reinterpret_cast<uint4*>(s_out + b * (FRAME_BYTES * NSTACK))[((y & 3) * 21 + (y >> 2)) * 21 + X] =
+            make_uint4(__byte_perm(lo01, lo23, 0x5410u), __byte_perm(lo01, lo23, 0x7632u),
+                       __byte_perm(hi01, hi23, 0x5410u), __byte_perm(hi01, hi23, 0x7632u));
     }
 }
 // Q = a4 . W5^T + b5 (fp32), then the epsilon-greedy decision (one block per state)

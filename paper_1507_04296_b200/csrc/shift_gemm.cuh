@@ -158,6 +158,80 @@ struct ShConv1Fwd {
     }
 };
 
+// ---------------------------------------------------------------- u8-staged input (large batches)
+// From B = 75 (the GEMM path) the sampler stages s / s' as u8 in row-phase-major order: per sample
+// [q][Y][X][px][c] = s[4Y+q][4X+px][c] (q < 4, Y, X < 21; one 16-B row per (q, Y, X); 28224 B, a
+// permutation of NHWC), half the bytes of bf16 NHWC and one contiguous run per sample. conv1's
+// operands expand it in shared memory: u8 row (q, r = Y*21 + X) -> 32 B of bf16 at row r of phase
+// plane q of the SWIZZLE_32B planes (16-B half h at byte (r*32 + 16h) with address bit 7 XORed into
+// bit 4), i.e. exactly the image the TMA boxes of ShConv1Fwd write from bf16 NHWC.
+constexpr int U8_ROWS = 4 * 441, U8_SAMPLE = U8_ROWS * 16;  // 28224 B per sample
+
+// bytes (2hi, 2hi + 1) of w as bf16x2: u8 -> fp32 exactly (magic 2^23), the upper halves exact
+GORILA_DEV uint32_t u8x2_bf16x2(uint32_t w, int hi) {
+    const float f0 = __uint_as_float(__byte_perm(w, 0x4B000000u, hi ? 0x7442u : 0x7440u)) - 8388608.f;
+    const float f1 = __uint_as_float(__byte_perm(w, 0x4B000000u, hi ? 0x7443u : 0x7441u)) - 8388608.f;
+    return __byte_perm(__float_as_uint(f0), __float_as_uint(f1), 0x7632u);
+}
+
+// NT threads expand one sample: load() issues its global reads (into registers, so that the next
+// sample's loads are in flight while this one is stored), store() writes the bf16 planes.
+template <int NT>
+struct U8Planes {
+    static constexpr int PER = (U8_ROWS + NT - 1) / NT;
+    uint4 v[PER];
+    GORILA_DEV void load(const uint8_t* __restrict__ sample, int t) {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = t + k * NT;
+            if (i < U8_ROWS) v[k] = __ldcg(reinterpret_cast<const uint4*>(sample) + i);
+        }
+    }
+    GORILA_DEV void store(uint32_t planes, uint32_t plane_bytes, int t) const {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = t + k * NT;
+            if (i >= U8_ROWS) continue;
+            const int q = i / 441, r = i - 441 * q;
+            const uint32_t row = planes + q * plane_bytes + r * 32;
+            const uint32_t w[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const uint32_t a = row + 16 * h, pa = a ^ ((a >> 3) & 16u);
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(pa), "r"(u8x2_bf16x2(w[2 * h], 0)),
+                             "r"(u8x2_bf16x2(w[2 * h], 1)), "r"(u8x2_bf16x2(w[2 * h + 1], 0)),
+                             "r"(u8x2_bf16x2(w[2 * h + 1], 1))
+                             : "memory");
+            }
+        }
+    }
+};
+
+// conv1 forward from the u8 staging: ShConv1Fwd<1>'s planes, written by the engine's converter warps
+struct ShConv1FwdU8 {
+    static constexpr bool CONVERT = true;
+    static constexpr int RB = 32, NCHUNK = 16, KSTEPS = 1, PROWS = 544, PLANE = PROWS * RB;
+    static constexpr int BUF = 4 * PLANE, NPLANE = 4, WRITTEN = 441 * RB, MS = 1;
+    const uint8_t* src;  // [B][U8_SAMPLE]
+    int batch;
+    __host__ __device__ int ntiles() const { return batch; }
+    GORILA_DEV int mb0(int) const { return 0; }
+    GORILA_DEV const uint8_t* sample(int t) const { return src + (int64_t)t * U8_SAMPLE; }
+    GORILA_DEV uint32_t addr(uint32_t base, int c, int mb) const {
+        const int q = c >> 2, dy = (c >> 1) & 1, dx = c & 1;
+        return base + q * PLANE + (mb * 128 + dy * 21 + dx) * RB;
+    }
+    GORILA_DEV int row(int t, int mb, int r) const {
+        const int m = mb * 128 + r, Y = m / 21, X = m - 21 * Y;
+        return (m < 441 && Y < 20 && X < 20) ? t * 400 + Y * 20 + X : -1;
+    }
+};
+template <class O, class = void>
+struct shift_convert : std::false_type {};
+template <class O>
+struct shift_convert<O, std::void_t<decltype(O::CONVERT)>> : std::integral_constant<bool, O::CONVERT> {};
+constexpr int SHIFT_CONV_WARPS = 8;  // converter warps of a CONVERT operand (warps 6 ..)
+
 // ---------------------------------------------------------------- B operands (resident weights)
 // Interface: kMN, CHUNK (bytes per chunk, multiple of 1024), NCH (chunks incl. M-block variants),
 // load_chunk(ch, dst, bar) -> bytes, chunk_of(c, mb), desc0(base) (descriptor of the block start)
@@ -232,7 +306,8 @@ struct ShiftCfg {
     static_assert(2 * MB * BN <= 512, "TMEM columns");
     static_assert(OB::NCH <= SHIFT_MAX_BCH, "weight chunks");
     static constexpr int BAR_BYTES = 8 * (2 * SHIFT_MAX_BCH + 2 * SHIFT_MAX_BUF + 4) + 16;
-    static constexpr int THREADS = 192;
+    static constexpr bool CONV = shift_convert<OA>::value;
+    static constexpr int THREADS = 192 + (CONV ? 32 * SHIFT_CONV_WARPS : 0);
     // dynamic smem for nprob problems and nbuf A buffers
     static constexpr int smem(int nprob, int nbuf) {
         return 1024 + nprob * OB::NCH * OB::CHUNK + nbuf * OA::BUF + BAR_BYTES;
@@ -240,8 +315,10 @@ struct ShiftCfg {
 };
 
 template <int BN, int MB, class OA, class OB, class EP>
-__global__ void __launch_bounds__(192) gemm_shift(const __grid_constant__ ShiftBatch<OA, OB, EP> p) {
+__global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
+    gemm_shift(const __grid_constant__ ShiftBatch<OA, OB, EP> p) {
     using CFG = ShiftCfg<BN, MB, OA, OB>;
+    constexpr bool CONV = CFG::CONV;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     const int nprob = p.nprob, nbuf = p.nbuf;
@@ -255,7 +332,7 @@ __global__ void __launch_bounds__(192) gemm_shift(const __grid_constant__ ShiftB
     uint64_t* acc_empty = acc_full + 2;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
     const int tiles_per = p.prob[0].a.ntiles(), ntiles = tiles_per * nprob;
     if (warp == 0) tmem_alloc(tmem_slot, CFG::TCOLS);
     if (OA::WRITTEN < OA::PLANE)  // rows past the loaded boxes are read by dropped output rows only:
@@ -266,7 +343,7 @@ __global__ void __launch_bounds__(192) gemm_shift(const __grid_constant__ ShiftB
     if (tid == 32) {
         for (int i = 0; i < 2 * SHIFT_MAX_BCH; ++i) mbar_init(&b_full[i], 1);
         for (int i = 0; i < SHIFT_MAX_BUF; ++i) {
-            mbar_init(&a_full[i], 1);
+            mbar_init(&a_full[i], CONV ? SHIFT_CONV_WARPS : 1);
             mbar_init(&a_empty[i], 1);
         }
         for (int i = 0; i < 2; ++i) {
@@ -299,14 +376,17 @@ __global__ void __launch_bounds__(192) gemm_shift(const __grid_constant__ ShiftB
                         mbar_expect_tx(bar, bytes);
                     }
                 }
-                const int buf = tl % nbuf;
-                if (tl >= nbuf) mbar_wait(&a_empty[buf], ((tl / nbuf) - 1) & 1);
-                const uint32_t bytes = p.prob[prob].a.load(tile, abase + buf * OA::BUF, &a_full[buf]);
-                mbar_expect_tx(&a_full[buf], bytes);
+                if constexpr (!CONV) {  // (CONVERT operands: the converter warps fill the buffers)
+                    const int buf = tl % nbuf;
+                    if (tl >= nbuf) mbar_wait(&a_empty[buf], ((tl / nbuf) - 1) & 1);
+                    const uint32_t bytes = p.prob[prob].a.load(tile, abase + buf * OA::BUF, &a_full[buf]);
+                    mbar_expect_tx(&a_full[buf], bytes);
+                }
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // MMA issuer
+        {  // MMA issuer (warp-uniform; one elected lane issues)
+            const uint32_t tmem_u = uniform_u32(tmem), abase_u = uniform_u32(abase), bbase_u = uniform_u32(bbase);
             uint32_t waited = 0;
             int tl = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
@@ -317,8 +397,8 @@ __global__ void __launch_bounds__(192) gemm_shift(const __grid_constant__ ShiftB
                 mbar_wait(&a_full[buf], (tl / nbuf) & 1);
                 if (tl >= 2) mbar_wait(&acc_empty[abuf], ((tl >> 1) - 1) & 1);
                 tc_fence_after();
-                const uint32_t acc = tmem + abuf * CFG::ACC;
-                const uint32_t a0 = abase + buf * OA::BUF, b0 = bbase + prob * OB::NCH * OB::CHUNK;
+                const uint32_t acc = tmem_u + abuf * CFG::ACC;
+                const uint32_t a0 = abase_u + buf * OA::BUF, b0 = bbase_u + prob * OB::NCH * OB::CHUNK;
                 const int m0 = P.a.mb0(t - prob * tiles_per);
                 const bool first = !(waited & (1u << prob));  // the problem's weights may still be landing
                 waited |= 1u << prob;
@@ -334,11 +414,36 @@ __global__ void __launch_bounds__(192) gemm_shift(const __grid_constant__ ShiftB
                     for (int kk = 0; kk < OA::KSTEPS; ++kk)
 #pragma unroll
                         for (int mb = 0; mb < MB; ++mb)
-                            umma_bf16(acc + mb * BN, ad0 + ((P.a.addr(0, c, m0 + mb) + kk * 32) >> 4),
-                                      bd0 + (OB::off(c, kk, m0 + mb) >> 4), IDESC, (c > 0 || kk > 0) ? 1u : 0u);
+                            umma_bf16_w(acc + mb * BN, ad0 + ((P.a.addr(0, c, m0 + mb) + kk * 32) >> 4),
+                                        bd0 + (OB::off(c, kk, m0 + mb) >> 4), IDESC, (c > 0 || kk > 0) ? 1u : 0u);
                 }
-                umma_commit(&a_empty[buf]);
-                umma_commit(&acc_full[abuf]);
+                umma_commit_w(&a_empty[buf]);
+                umma_commit_w(&acc_full[abuf]);
+            }
+        }
+    } else if (CONV && warp >= 6) {  // converter warps: u8 staging -> the tile's bf16 planes
+        if constexpr (CONV) {
+            constexpr int NT = 32 * SHIFT_CONV_WARPS;
+            const int ct = tid - 192;
+            U8Planes<NT> cur, nxt;
+            int tl = 0, t = blockIdx.x;
+            if (t < ntiles) {
+                const int prob = t / tiles_per;
+                cur.load(p.prob[prob].a.sample(t - prob * tiles_per), ct);
+            }
+            for (; t < ntiles; t += gridDim.x, ++tl) {
+                const int tn = t + gridDim.x;
+                if (tn < ntiles) {
+                    const int pn = tn / tiles_per;
+                    nxt.load(p.prob[pn].a.sample(tn - pn * tiles_per), ct);
+                }
+                const int buf = tl % nbuf;
+                if (tl >= nbuf) mbar_wait(&a_empty[buf], ((tl / nbuf) - 1) & 1);
+                cur.store(abase + buf * OA::BUF, OA::PLANE, ct);
+                fence_proxy_async_smem();
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&a_full[buf]);
+                cur = nxt;
             }
         }
     } else {  // epilogue warps 2..5 (warp w reads TMEM lanes 32*(w%4) ..)
@@ -386,6 +491,152 @@ __global__ void __launch_bounds__(192) gemm_shift(const __grid_constant__ ShiftB
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, CFG::TCOLS);
+}
+
+
+// ---------------------------------------------------------------- conv1 weight gradient (u8 staging)
+// dW1[o][ky][kx][c] = sum over samples and output pixels (oy, ox) of g1[oy][ox][o] * s[4oy+ky][4ox+kx][c].
+// With ky = 4dy + py and kx = 4dx + px the input element is row (oy+dy)*21 + (ox+dx) of phase plane
+// py (element (px, c)): the virtual-grid pixel p = oy*21 + ox shifted by dy*21 + dx rows. So per
+// (dy, dx) one M = 64 accumulator (the 4 planes x 16 (px, c): MN-major A, 16-element blocks PLANE
+// bytes apart) runs over K = the sample's 21 x 20 virtual pixels from a shifted start row, against
+// B = g1 on the same virtual grid (MN-major over o, 64-B rows; the 21st column is TMA zero fill, so
+// the rows a shift wraps into contribute nothing). No im2col: the planes are expanded once per
+// sample from the u8 staging (U8Planes) and every tap is a start address.
+// One CTA per sample stride; the four accumulators (M = 64 each: two per TMEM column block, at lane
+// offsets 0 and 16) stay in TMEM across all of the CTA's samples; the epilogue stores the CTA's
+// partial dW1 [o][k] (times the input scale) for the fixed-order reduction (k_wgrad_reduce).
+struct Conv1WgradU8 {
+    CUtensorMap g1_map;  // (32, 20, 20, B) bf16, box (32, 21, 20, 1), SWIZZLE_64B
+    const uint8_t* s8;   // [B][U8_SAMPLE]
+    float* part;         // [gridDim.x][32][256]
+    float scale;
+    int batch;
+};
+namespace c1wg {
+constexpr int KSTEPS = 27;                           // 432 virtual rows, 420 of them g1 rows (21 x 20)
+constexpr int PLANE = ShConv1FwdU8::PLANE;           // 544 rows of 32 B (rows <= 431 + 22 are read)
+constexpr int ABUF = 4 * PLANE, BBUF = KSTEPS * 16 * 64, STAGE = ABUF + BBUF;  // 69632 + 27648
+constexpr int NBUF = 2, CONV_WARPS = 8, THREADS = 64 + 32 * CONV_WARPS;     // warps 2.. convert
+constexpr int SMEM = 1024 + NBUF * STAGE + 128;
+constexpr uint32_t TCOLS = 64;
+}  // namespace c1wg
+
+__global__ void __launch_bounds__(c1wg::THREADS) k_conv1_wgrad_u8(const __grid_constant__ Conv1WgradU8 p) {
+    using namespace c1wg;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NBUF * STAGE);
+    uint64_t* a_full = bars;               // [NBUF] converter warps
+    uint64_t* b_full = a_full + NBUF;      // [NBUF] TMA of g1
+    uint64_t* empty = b_full + NBUF;       // [NBUF] MMA commit
+    uint64_t* done = empty + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
+    const int nt = p.batch > (int)blockIdx.x ? (p.batch - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    if (warp == 0) tmem_alloc(tmem_slot, TCOLS);
+    // plane rows past the 441 written ones and g1 rows past the 420 loaded ones: zero once
+    for (int b = 0; b < NBUF; ++b) {
+        uint8_t* st = smem + b * STAGE;
+        for (int q = 0; q < 4; ++q)
+            for (int o = 441 * 32 + tid * 16; o < PLANE; o += THREADS * 16)
+                *reinterpret_cast<uint4*>(st + q * PLANE + o) = make_uint4(0, 0, 0, 0);
+        for (int o = 420 * 64 + tid * 16; o < BBUF; o += THREADS * 16)
+            *reinterpret_cast<uint4*>(st + ABUF + o) = make_uint4(0, 0, 0, 0);
+    }
+    fence_proxy_async_smem();
+    if (tid == 32) {
+        for (int i = 0; i < NBUF; ++i) {
+            mbar_init(&a_full[i], CONV_WARPS);
+            mbar_init(&b_full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(done, 1);
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    pdl_wait();
+    pdl_trigger();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t sbase = smem_u32(smem);
+    if (warp == 0) {
+        if (lane == 0) {  // g1 of each sample (420 rows of 64 B, x = 20 zero filled)
+            for (int tl = 0; tl < nt; ++tl) {
+                const int b = blockIdx.x + tl * gridDim.x, s = tl % NBUF;
+                if (tl >= NBUF) mbar_wait(&empty[s], ((tl / NBUF) - 1) & 1);
+                tma_load(&p.g1_map, sbase + s * STAGE + ABUF, &b_full[s], 0, 0, 0, b);
+                mbar_expect_tx(&b_full[s], 420 * 64);
+            }
+        }
+    } else if (warp == 1) {
+        {  // MMA issuer (warp-uniform): per sample 27 K-steps x 4 (dy, dx) accumulators
+            constexpr uint32_t IDESC = umma_idesc_bf16(64, 32) | (1u << 15) | (1u << 16);
+            const uint32_t tmem_u = uniform_u32(tmem), sbase_u = uniform_u32(sbase);
+            for (int tl = 0; tl < nt; ++tl) {
+                const int s = tl % NBUF;
+                mbar_wait(&a_full[s], (tl / NBUF) & 1);
+                mbar_wait(&b_full[s], (tl / NBUF) & 1);
+                tc_fence_after();
+                const uint32_t a0 = sbase_u + s * STAGE, b0 = a0 + ABUF;
+#pragma unroll 1
+                for (int kk = 0; kk < KSTEPS; ++kk) {
+                    const uint64_t bd = umma_desc_mn_sw(b0 + kk * 1024, 0, 64);
+#pragma unroll
+                    for (int acc = 0; acc < 4; ++acc) {
+                        const int dy = acc >> 1, dx = acc & 1;
+                        const uint64_t ad = umma_desc_mn_sw(a0 + (kk * 16 + dy * 21 + dx) * 32, PLANE, 32);
+                        umma_bf16_w(tmem_u + ((uint32_t)(16 * dx) << 16) + 32 * dy, ad, bd, IDESC,
+                                    (tl > 0 || kk > 0) ? 1u : 0u);
+                    }
+                }
+                umma_commit_w(&empty[s]);
+            }
+            umma_commit_w(done);
+        }
+    } else {  // converter warps 2..9: the samples' u8 staging -> bf16 planes
+        constexpr int NT = 32 * CONV_WARPS;
+        const int ct = tid - 64;
+        U8Planes<NT> cur, nxt;
+        if (nt > 0) cur.load(p.s8 + (int64_t)blockIdx.x * U8_SAMPLE, ct);
+        for (int tl = 0; tl < nt; ++tl) {
+            if (tl + 1 < nt) nxt.load(p.s8 + (int64_t)(blockIdx.x + (tl + 1) * gridDim.x) * U8_SAMPLE, ct);
+            const int s = tl % NBUF;
+            if (tl >= NBUF) mbar_wait(&empty[s], ((tl / NBUF) - 1) & 1);
+            cur.store(sbase + s * STAGE, PLANE, ct);
+            fence_proxy_async_smem();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&a_full[s]);
+            cur = nxt;
+        }
+        if (warp < 6) {  // epilogue (warps 2..5 = TMEM lane quarters 2, 3, 0, 1)
+            const int quad = warp & 3;
+            if (nt > 0) {
+                mbar_wait(done, 0);
+                tc_fence_after();
+            }
+            float* dst = p.part + (int64_t)blockIdx.x * (32 * K1);
+            // lane l of quarter quad: row 16*quad + (l & 15) of accumulator (dy, dx = l >> 4) in column
+            // block dy -> k = (4dy + quad) * 32 + 16dx + (l & 15) = (4dy + quad) * 32 + l
+#pragma unroll 1
+            for (int dy = 0; dy < 2; ++dy)
+#pragma unroll 1
+                for (int c0 = 0; c0 < 32; c0 += 16) {
+                    float v[16];
+                    if (nt > 0) tmem_ld16(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(32 * dy + c0), v);
+                    else
+#pragma unroll
+                        for (int e = 0; e < 16; ++e) v[e] = 0.f;
+                    const int k = (4 * dy + quad) * 32 + lane;
+#pragma unroll
+                    for (int e = 0; e < 16; ++e) dst[(c0 + e) * K1 + k] = v[e] * p.scale;
+                }
+        }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, TCOLS);
 }
 
 }  // namespace gorila

@@ -513,7 +513,7 @@ __global__ void __launch_bounds__(128) gemm_tma(const __grid_constant__ TmaBatch
     uint64_t* done = empty + STAGES;
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
 
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
     GTRACE(0);
     const int prob = blockIdx.z / p.splits, split = blockIdx.z - prob * p.splits;
     const TmaProb<OA, OB, EP>& P = p.prob[prob];
@@ -549,45 +549,48 @@ __global__ void __launch_bounds__(128) gemm_tma(const __grid_constant__ TmaBatch
         umma_idesc_bf16(TC_BM, BN) | (OA::kMN ? (1u << 15) : 0u) | (OB::kMN ? (1u << 16) : 0u);
     const uint32_t sbase = smem_u32(smem);
 
-    if (tid == 0) {  // TMA producer
-        for (int kc = 0; kc < nK; ++kc) {
-            const int s = kc % STAGES;
-            if (kc >= STAGES) mbar_wait(&empty[s], ((kc / STAGES) - 1) & 1);
-            const uint32_t a_dst = sbase + s * (CFG::A_ST + CFG::B_ST), b_dst = a_dst + CFG::A_ST;
-            // issue first, then arrive with the transaction count (full boxes, zero fill included);
-            // the phase cannot complete before this arrival
-            uint32_t bytes = P.a.issue(ta, kc0 + kc, a_dst, &full[s]);
-            bytes += P.b.issue(tb, kc0 + kc, b_dst, &full[s]);
-            mbar_expect_tx(&full[s], bytes);
-            GTRACE(8 + (kc & 7));
+    if (warp == 0) {  // (warp-uniform branch: keeps the MMA warp's branch below uniform)
+        if (lane == 0) {  // TMA producer
+            for (int kc = 0; kc < nK; ++kc) {
+                const int s = kc % STAGES;
+                if (kc >= STAGES) mbar_wait(&empty[s], ((kc / STAGES) - 1) & 1);
+                const uint32_t a_dst = sbase + s * (CFG::A_ST + CFG::B_ST), b_dst = a_dst + CFG::A_ST;
+                // issue first, then arrive with the transaction count (full boxes, zero fill included);
+                // the phase cannot complete before this arrival
+                uint32_t bytes = P.a.issue(ta, kc0 + kc, a_dst, &full[s]);
+                bytes += P.b.issue(tb, kc0 + kc, b_dst, &full[s]);
+                mbar_expect_tx(&full[s], bytes);
+                GTRACE(8 + (kc & 7));
+            }
         }
-    } else if (tid == 32) {  // MMA issuer
+    } else if (warp == 1) {  // MMA issuer (warp-uniform; one elected lane issues)
         // a K step / M-block only moves a descriptor's start address: per stage one base
         // descriptor plus these address-field deltas
+        const uint32_t tmem_u = uniform_u32(tmem), sbase_u = uniform_u32(sbase);
         constexpr int KS = OA::KC / 16;
         uint32_t adl[KS][MB], bdl[KS];
         const uint64_t a00 = P.a.desc(0, 0, 0), b00 = P.b.desc(0, 0, 0);
 #pragma unroll
         for (int kk = 0; kk < KS; ++kk) {
-            bdl[kk] = (uint32_t)(P.b.desc(0, kk, 0) - b00);
+            bdl[kk] = uniform_u32((uint32_t)(P.b.desc(0, kk, 0) - b00));
 #pragma unroll
-            for (int mb = 0; mb < MB; ++mb) adl[kk][mb] = (uint32_t)(P.a.desc(0, kk, mb) - a00);
+            for (int mb = 0; mb < MB; ++mb) adl[kk][mb] = uniform_u32((uint32_t)(P.a.desc(0, kk, mb) - a00));
         }
         for (int kc = 0; kc < nK; ++kc) {
             const int s = kc % STAGES;
             mbar_wait(&full[s], (kc / STAGES) & 1);
             tc_fence_after();
-            const uint32_t a_base = sbase + s * (CFG::A_ST + CFG::B_ST), b_base = a_base + CFG::A_ST;
-            const uint64_t ad0 = P.a.desc(a_base, 0, 0), bd0 = P.b.desc(b_base, 0, 0);
+            const uint32_t a_base = sbase_u + s * (CFG::A_ST + CFG::B_ST), b_base = a_base + CFG::A_ST;
+            const uint64_t ad0 = uniform_u64(P.a.desc(a_base, 0, 0)), bd0 = uniform_u64(P.b.desc(b_base, 0, 0));
 #pragma unroll
             for (int kk = 0; kk < KS; ++kk) {
 #pragma unroll
                 for (int mb = 0; mb < MB; ++mb)
-                    umma_bf16(tmem + mb * BN, ad0 + adl[kk][mb], bd0 + bdl[kk], IDESC, (kc > 0 || kk > 0) ? 1u : 0u);
+                    umma_bf16_w(tmem_u + mb * BN, ad0 + adl[kk][mb], bd0 + bdl[kk], IDESC, (kc > 0 || kk > 0) ? 1u : 0u);
             }
-            umma_commit(&empty[s]);
+            umma_commit_w(&empty[s]);
         }
-        if (nK > 0) umma_commit(done);
+        if (nK > 0) umma_commit_w(done);
     }
     __syncwarp();
     GTRACE(3);
@@ -734,7 +737,7 @@ __global__ void __launch_bounds__(192) gemm_tma_p(const __grid_constant__ TmaBat
     uint64_t* acc_empty = acc_full + 2;   // [2] epilogue -> MMA
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
 
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
     const int ntiles = tilesA * tilesB * nprob * p.splits;
     if (warp == 0) tmem_alloc(tmem_slot, CFG::TCOLS);
     if (OA::WRITTEN < CFG::A_ST || zero_all<OA>::value)  // zero the never-copied rows of the A stages
@@ -796,7 +799,8 @@ __global__ void __launch_bounds__(192) gemm_tma_p(const __grid_constant__ TmaBat
             }
         }
     } else if (warp == 1) {
-        if (lane == 0) {  // MMA issuer
+        {  // MMA issuer (warp-uniform; one elected lane issues)
+            const uint32_t tmem_u = uniform_u32(tmem), sbase_u = uniform_u32(sbase);
             uint32_t it = 0, tl = 0;
             for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
                 int prob, split, ta, tb, kc0;
@@ -806,7 +810,7 @@ __global__ void __launch_bounds__(192) gemm_tma_p(const __grid_constant__ TmaBat
                 const uint32_t buf = tl & 1;
                 if (tl >= 2) mbar_wait(&acc_empty[buf], ((tl >> 1) - 1) & 1);
                 tc_fence_after();
-                const uint32_t acc = tmem + buf * CFG::ACC;
+                const uint32_t acc = tmem_u + buf * CFG::ACC;
                 constexpr int KS = OA::KC / 16;  // descriptor deltas of the K steps / M-blocks
                 uint32_t adl[KS][MB], bdl[KS];
                 const uint64_t a00 = P.a.desc(0, 0, 0), b00 = P.b.desc(0, 0, 0);
@@ -820,17 +824,17 @@ __global__ void __launch_bounds__(192) gemm_tma_p(const __grid_constant__ TmaBat
                     const int s = it % STAGES;
                     mbar_wait(&full[s], (it / STAGES) & 1);
                     tc_fence_after();
-                    const uint32_t a_base = sbase + s * (CFG::A_ST + CFG::B_ST), b_base = a_base + CFG::A_ST;
+                    const uint32_t a_base = sbase_u + s * (CFG::A_ST + CFG::B_ST), b_base = a_base + CFG::A_ST;
                     const uint64_t ad0 = P.a.desc(a_base, 0, 0), bd0 = P.b.desc(b_base, 0, 0);
 #pragma unroll
                     for (int kk = 0; kk < KS; ++kk)
 #pragma unroll
                         for (int mb = 0; mb < MB; ++mb)
-                            umma_bf16(acc + mb * BN, ad0 + adl[kk][mb], bd0 + bdl[kk], IDESC,
-                                      (kc > 0 || kk > 0) ? 1u : 0u);
-                    umma_commit(&empty[s]);
+                            umma_bf16_w(acc + mb * BN, ad0 + adl[kk][mb], bd0 + bdl[kk], IDESC,
+                                        (kc > 0 || kk > 0) ? 1u : 0u);
+                    umma_commit_w(&empty[s]);
                 }
-                umma_commit(&acc_full[buf]);  // also arrives when the tile had no chunks
+                umma_commit_w(&acc_full[buf]);  // also arrives when the tile had no chunks
             }
         }
     } else {  // epilogue warps 2..5

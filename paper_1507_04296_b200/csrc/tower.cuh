@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(tower::THREADS) k_conv_tower(const __grid_cons
     uint64_t* acc_full = s_full + 1;                                // [NB_ACC] MMA -> epilogue
     uint64_t* act_ready = acc_full + NB_ACC;                        // [2] a1 / a2 in smem (epilogue -> MMA)
     uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(act_ready + 2);
-    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
     const int z = blockIdx.y, b = blockIdx.x;
     const TowerNet& N = p.net[z];
 
@@ -107,8 +107,8 @@ __global__ void __launch_bounds__(tower::THREADS) k_conv_tower(const __grid_cons
     tc_fence_before();
     __syncthreads();
     tc_fence_after();
-    const uint32_t tmem = *tmem_slot;
-    const uint32_t base = smem_u32(sm);
+    const uint32_t tmem_nu = *tmem_slot, base_nu = smem_u32(sm);
+    const uint32_t tmem = tmem_nu, base = base_nu;
     float* s_bias = reinterpret_cast<float*>(sm + BIAS_OFF);
     // The weights (this round's replica / theta^-) were written by the previous round's apply and
     // target sync, two or more kernels back: with PDL those are complete when this grid starts
@@ -149,7 +149,8 @@ __global__ void __launch_bounds__(tower::THREADS) k_conv_tower(const __grid_cons
         fence_proxy_async_smem();
         mbar_arrive(&act_ready[0]);
     } else if (warp == 1) {
-        if (lane == 0) {  // MMA issuer: conv1 -> TMEM [0,128), conv2 -> [128,192), conv3 -> [192,256)
+        {  // MMA issuer (warp-uniform): conv1 -> TMEM [0,128), conv2 -> [128,192), conv3 -> [192,256)
+            const uint32_t tmem = uniform_u32(tmem_nu), base = uniform_u32(base_nu);
             constexpr uint32_t ID32 = umma_idesc_bf16(128, 32), ID64 = umma_idesc_bf16(128, 64);
             mbar_wait(s_full, 0);
             TTRACE(49);
@@ -165,10 +166,10 @@ __global__ void __launch_bounds__(tower::THREADS) k_conv_tower(const __grid_cons
                             tc_fence_after();
                         }
                         const int q = c >> 2, dy = (c >> 1) & 1, dx = c & 1;
-                        umma_bf16(tmem + mb * 32, ad0 + ((q * S_PLANE + (mb * 128 + dy * 21 + dx) * 32) >> 4),
+                        umma_bf16_w(tmem + mb * 32, ad0 + ((q * S_PLANE + (mb * 128 + dy * 21 + dx) * 32) >> 4),
                                   bd0 + ((c * W1_CH) >> 4), ID32, c > 0 ? 1u : 0u);
                     }
-                    umma_commit(&acc_full[mb]);  // block mb's epilogue runs under the next block's MMAs
+                    umma_commit_w(&acc_full[mb]);  // block mb's epilogue runs under the next block's MMAs
                 }
                 TTRACE(50);
             }
@@ -184,10 +185,10 @@ __global__ void __launch_bounds__(tower::THREADS) k_conv_tower(const __grid_cons
                     const int q = c >> 2, dy = (c >> 1) & 1, dx = c & 1;
 #pragma unroll
                     for (int kk = 0; kk < 2; ++kk)
-                        umma_bf16(tmem + 128, ad0 + ((q * A1_PLANE + (dy * 10 + dx) * 64 + kk * 32) >> 4),
+                        umma_bf16_w(tmem + 128, ad0 + ((q * A1_PLANE + (dy * 10 + dx) * 64 + kk * 32) >> 4),
                                   bd0 + ((c * W2_CH + kk * 32) >> 4), ID64, (c > 0 || kk > 0) ? 1u : 0u);
                 }
-                umma_commit(&acc_full[4]);
+                umma_commit_w(&acc_full[4]);
                 TTRACE(52);
             }
             mbar_wait(&act_ready[1], 0);  // a2 rows written
@@ -202,10 +203,10 @@ __global__ void __launch_bounds__(tower::THREADS) k_conv_tower(const __grid_cons
                     const int ky = c / 3, kx = c - 3 * ky;
 #pragma unroll
                     for (int kk = 0; kk < 4; ++kk)
-                        umma_bf16(tmem + 192, ad0 + (((ky * 9 + kx) * 128 + kk * 32) >> 4),
+                        umma_bf16_w(tmem + 192, ad0 + (((ky * 9 + kx) * 128 + kk * 32) >> 4),
                                   bd0 + ((c * W3_CH + kk * 32) >> 4), ID64, (c > 0 || kk > 0) ? 1u : 0u);
                 }
-                umma_commit(&acc_full[5]);
+                umma_commit_w(&acc_full[5]);
                 TTRACE(54);
             }
         }
