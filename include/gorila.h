@@ -326,6 +326,10 @@ GORILA_API gorila_status gorila_bench_phase(gorila_ctx* ctx, int32_t learner, in
                                             double* us_per_iter);
 /* Diagnostics build only (-DGORILA_TRACE): clock64 timeline of CTA (0,0,0) of the last GEMM. */
 GORILA_API gorila_status gorila_debug_trace(uint64_t* out64);
+/* Diagnostics build only: per-tile events of CTA 0 of the last shifted-window GEMM, out512[ev * 64 +
+ * tile] (clock64; ev 0/1 converter start / buffer handed over, 2/3/4 MMA operands ready / accumulator
+ * free / issued, 5/6/7 epilogue wait / accumulator ready / done). E_INVALID in the normal build. */
+GORILA_API gorila_status gorila_debug_trace_tiles(uint64_t* out512);
 /* NEXT row f2: the asynchronous parameter server (config.ps_mode == 2; §3.1, P:144,
  * P:165-169). Runs `steps` learner steps for each listed local learner (ascending ids; round robin on
  * the library stream, rounds round0 .. round0 + steps - 1 for the sampler) while this rank's shard is

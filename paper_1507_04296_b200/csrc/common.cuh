@@ -6,6 +6,7 @@
 #include <stdint.h>
 
 #include <type_traits>
+#include <utility>
 
 #define GORILA_DEV __device__ __forceinline__
 
@@ -166,9 +167,22 @@ __device__ unsigned long long gorila_trace_buf[64];
             gorila_trace_buf[(slot)] = t_;                                                       \
         }                                                                                         \
     } while (0)
+// per-tile events of CTA 0 of a persistent engine: gorila_trace_tiles[ev][tile] (tile < 64)
+__device__ unsigned long long gorila_trace_tiles[8 * 64];
+#define GTRACE_T(ev, tl)                                                                          \
+    do {                                                                                          \
+        if (blockIdx.x == 0 && (tl) < 64) {                                                       \
+            unsigned long long t_;                                                               \
+            asm volatile("mov.u64 %0, %%clock64;" : "=l"(t_));                                  \
+            gorila_trace_tiles[(ev) * 64 + (tl)] = t_;                                           \
+        }                                                                                         \
+    } while (0)
 #else
 #define GTRACE(slot) \
     do {             \
+    } while (0)
+#define GTRACE_T(ev, tl) \
+    do {                 \
     } while (0)
 #endif
 

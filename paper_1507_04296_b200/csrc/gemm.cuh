@@ -158,8 +158,17 @@ GORILA_DEV void store16(T* dst, const float* v) {  // 16 values, 16-B aligned de
             __nv_bfloat162 h = __floats2bfloat162_rn(v[2 * e], v[2 * e + 1]);
             w[e] = *reinterpret_cast<uint32_t*>(&h);
         }
-        reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
-        reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+#ifdef GORILA_EXP_NOSTORE  // timing experiment only: the stores are skipped (results wrong)
+        if ((w[0] ^ w[1] ^ w[2] ^ w[3] ^ w[4] ^ w[5] ^ w[6] ^ w[7]) != 0x12345678u) return;
+#endif
+        if (((uintptr_t)dst & 31u) == 0) {  // one 256-bit store (half the L1 wavefronts of two 128-bit)
+            asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(w[0]), "r"(w[1]),
+                         "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                         : "memory");
+        } else {
+            reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+            reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+        }
     } else {
 #pragma unroll
         for (int e = 0; e < 4; ++e)
@@ -194,6 +203,10 @@ struct EpAct {  // out[i][j] = round_T(act(v * scale + bias[j]))   (ld % 8 == 0)
     const float* bias;
     float scale;
     int M, N, relu;
+    // optional (shifted-window engine, N <= 64): the ReLU decisions of the stored values as bits,
+    // mask[i * (N / 32) + j / 32] bit j % 32 = (out[i][j] > 0), read back by the data gradient
+    // (EpMaskBits) instead of the activation itself
+    uint32_t* mask = nullptr;
     GORILA_DEV float f(float v, int j) const {
         float z = v * scale + bias[j];
         return relu ? fmaxf(z, 0.f) : z;
@@ -212,7 +225,9 @@ struct EpAct {  // out[i][j] = round_T(act(v * scale + bias[j]))   (ld % 8 == 0)
             for (int e = 0; e < 16; ++e) apply1(i, j0 + e, v[e], s);
         }
     }
-    // prefetch: the 16 biases of a column chunk, requested ahead of the accumulator
+    // prefetch: the 16 biases of a column chunk, requested ahead of the accumulator (they depend on
+    // the column only: COL_PRE engines load them once per CTA)
+    static constexpr bool COL_PRE = true;
     struct Pre {
         float b[16];
     };
@@ -221,6 +236,41 @@ struct EpAct {  // out[i][j] = round_T(act(v * scale + bias[j]))   (ld % 8 == 0)
 #pragma unroll
         for (int e = 0; e < 16; ++e) p.b[e] = j0 + e < N ? bias[j0 + e] : 0.f;
         return p;
+    }
+    // apply16p that also returns the 16 decisions (out > 0) of the ROUNDED stored values
+    GORILA_DEV uint32_t apply16m(int i, int j0, const float* v, const Pre& p) const {
+        float o[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) {
+            const float z = v[e] * scale + p.b[e];
+            o[e] = relu ? fmaxf(z, 0.f) : z;
+        }
+        uint32_t bits = 0;
+        if constexpr (sizeof(T) == 2) {  // decided on the packed bf16 words (= the stored values)
+            uint32_t w[8];
+#pragma unroll
+            for (int e = 0; e < 8; ++e) {
+                __nv_bfloat162 h = __floats2bfloat162_rn(o[2 * e], o[2 * e + 1]);
+                w[e] = *reinterpret_cast<uint32_t*>(&h);
+                const bool neg_lo = (w[e] & 0x8000u) != 0, neg_hi = (w[e] & 0x80000000u) != 0;
+                bits |= ((w[e] & 0x7fffu) != 0 && !neg_lo ? 1u : 0u) << (2 * e);
+                bits |= ((w[e] & 0x7fff0000u) != 0 && !neg_hi ? 1u : 0u) << (2 * e + 1);
+            }
+            T* dst = out + (int64_t)i * ld + j0;
+            if (((uintptr_t)dst & 31u) == 0) {
+                asm volatile("st.global.v8.b32 [%0], {%1, %2, %3, %4, %5, %6, %7, %8};" ::"l"(dst), "r"(w[0]), "r"(w[1]),
+                             "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]), "r"(w[7])
+                             : "memory");
+            } else {
+                reinterpret_cast<uint4*>(dst)[0] = make_uint4(w[0], w[1], w[2], w[3]);
+                reinterpret_cast<uint4*>(dst)[1] = make_uint4(w[4], w[5], w[6], w[7]);
+            }
+        } else {
+#pragma unroll
+            for (int e = 0; e < 16; ++e) bits |= (o[e] > 0.f ? 1u : 0u) << e;
+            store16<T>(out + (int64_t)i * ld + j0, o);
+        }
+        return bits;
     }
     GORILA_DEV void apply16p(int i, int j0, const float* v, const Pre& p, int s) const {
         if (i >= M) return;
@@ -238,6 +288,34 @@ struct EpAct {  // out[i][j] = round_T(act(v * scale + bias[j]))   (ld % 8 == 0)
     }
 };
 
+// out[i][j] = round_T(v * 1[act[i][j] > 0]) with the decisions read as bits (EpAct::mask):
+// 4 bytes per row of 32 channels instead of the activation row (64 B), same values as EpMask
+template <typename T>
+struct EpMaskBits {
+    T* out;
+    const uint32_t* bits;
+    int64_t ld;
+    int M, N, words;  // words = N / 32
+    static constexpr bool ROW_PRE = true;
+    struct Pre {
+        uint32_t w;
+    };
+    GORILA_DEV Pre prefetch(int i, int j0) const {
+        Pre p;
+        p.w = i < M ? __ldg(bits + (int64_t)i * words + (j0 >> 5)) : 0u;
+        return p;
+    }
+    GORILA_DEV void apply16p(int i, int j0, const float* v, const Pre& p, int) const {
+        if (i >= M || j0 + 16 > N) return;
+        const uint32_t b = p.w >> (j0 & 16);
+        float o[16];
+#pragma unroll
+        for (int e = 0; e < 16; ++e) o[e] = (b >> e) & 1u ? v[e] : 0.f;
+        store16<T>(out + (int64_t)i * ld + j0, o);
+    }
+    GORILA_DEV void apply16(int i, int j0, const float* v, int s) const { apply16p(i, j0, v, prefetch(i, j0), s); }
+};
+
 template <typename T>
 struct EpMask {  // out[i][j] = round_T(v * 1[act[i][j] > 0])  (ReLU'(0) = 0, reading R19; ld % 8 == 0)
     T* out;
@@ -250,14 +328,31 @@ struct EpMask {  // out[i][j] = round_T(v * 1[act[i][j] > 0])  (ReLU'(0) = 0, re
         out[a] = fromf<T>(tof(act[a]) > 0.f ? v : 0.f);
     }
     // epilogue prefetch (issued ahead of the accumulator): the 16 activations of a row chunk
+    static constexpr bool ROW_PRE = true;
     struct Pre {
         uint4 q[sizeof(T)];
     };
     GORILA_DEV Pre prefetch(int i, int j0) const {
         Pre p;
-        if (i < M && j0 + 16 <= N) {
+#ifdef GORILA_EXP_NOSTORE  // timing experiment only: no mask loads either
+        if (i >= 0) {
 #pragma unroll
-            for (int u = 0; u < (int)sizeof(T); ++u) p.q[u] = reinterpret_cast<const uint4*>(act + (int64_t)i * ld + j0)[u];
+            for (int u = 0; u < (int)sizeof(T); ++u) p.q[u] = make_uint4(i, j0, i, j0);
+            return p;
+        }
+#endif
+        if (i < M && j0 + 16 <= N) {
+            const T* src = act + (int64_t)i * ld + j0;
+            if (sizeof(T) == 2 && ((uintptr_t)src & 31u) == 0) {  // one 256-bit load
+                uint32_t* q = reinterpret_cast<uint32_t*>(p.q);
+                asm volatile("ld.global.v8.b32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+                             : "=r"(q[0]), "=r"(q[1]), "=r"(q[2]), "=r"(q[3]), "=r"(q[4]), "=r"(q[5]), "=r"(q[6]),
+                               "=r"(q[7])
+                             : "l"(src));
+            } else {
+#pragma unroll
+                for (int u = 0; u < (int)sizeof(T); ++u) p.q[u] = reinterpret_cast<const uint4*>(src)[u];
+            }
         } else {
 #pragma unroll
             for (int u = 0; u < (int)sizeof(T); ++u) p.q[u] = make_uint4(0, 0, 0, 0);
@@ -404,6 +499,16 @@ struct EpAddT {  // G[j*ld + i] (+)= v (fp32, transposed, coalesced across the w
     }
 };
 
+// epilogues whose prefetched inputs depend on the output row (ROW_PRE): the shifted-window engine
+// requests a whole tile of them one tile ahead
+template <class EP, class = void>
+struct ep_row_pre : std::false_type {};
+template <class EP>
+struct ep_row_pre<EP, std::void_t<decltype(EP::ROW_PRE)>> : std::integral_constant<bool, EP::ROW_PRE> {};
+template <class EP, class = void>
+struct ep_col_pre : std::false_type {};
+template <class EP>
+struct ep_col_pre<EP, std::void_t<decltype(EP::COL_PRE)>> : std::integral_constant<bool, EP::COL_PRE> {};
 // prefetch interface: epilogues with a `Pre` type load their inputs ahead of the accumulator
 template <class EP, class = void>
 struct EpPre {

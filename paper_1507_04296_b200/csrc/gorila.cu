@@ -218,6 +218,10 @@ struct gorila_ctx {
     // large-batch bf16 (B > 74): s / s' staged as u8 in row-phase-major order, expanded to bf16 inside
     // conv1's forward and weight-gradient kernels (shift_gemm.cuh U8Planes; GORILA_U8=0: bf16 NHWC)
     bool u8 = false;
+    // u8 path: conv1 / conv2 forward also store their ReLU decisions as bits (EpAct::mask), which the
+    // conv2 / conv3 data gradients read (EpMaskBits) instead of the activations
+    uint32_t* mbits1 = nullptr;  // [B * 400] one word (32 channels) per a1 row
+    uint32_t* mbits2 = nullptr;  // [B * 81][2]
     // side stream for the weight-gradient GEMMs, which are off the dgrad critical path
     // (a fork / join of the round; a graph captures it as parallel branches)
     cudaStream_t side = nullptr;
@@ -876,6 +880,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                 pr[z].b = sh_wk<32, 32, 16, 2>(ctx, z ? (const void*)(tt + RT.w1) : (const void*)(rt + RL.w1), K1);
                 pr[z].ep = {z ? t1 : a1, C1_OUT, z ? tf + RT.b1 : rf + RL.b1, in_scale, M, C1_OUT, 1};
             }
+            pr[0].ep.mask = ctx->mbits1;  // the online net's ReLU decisions for conv2's data gradient
             gemm_shift_launch<32, 4>(ctx, pr, 2, C1_OUT);
         } else if ((ctx->shift & 1) && 2 * B > ctx->num_sms) {  // shifted windows over the row phases of s
 #define SH_C1(MS_, MB_)                                                                                        \
@@ -926,6 +931,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                 pr[z].b = sh_wk<64, 64, 16, 1>(ctx, z ? (const void*)(tt + RT.w2) : (const void*)(rt + RL.w2), K2);
                 pr[z].ep = {z ? t2 : a2, C2_OUT, z ? tf + RT.b2 : rf + RL.b2, 1.f, M, C2_OUT, 1};
             }
+            if (ctx->u8) pr[0].ep.mask = ctx->mbits2;
             gemm_shift_launch<64, 1>(ctx, pr, 2, C2_OUT);
         } else {  // TMA: one sample (81 rows) per tile, stride-2 boxes; in-cluster split of K = 512
             using OA = OpConvFwdS<Conv2, 1>; using OB = OpMatKS<64>; using EP = EpAct<T>;
@@ -1133,6 +1139,14 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             using LA = LdDgrad<T, Conv3>; using LB = LdWdgradMN<T, Conv3>; using EP = EpMask<T>;
             GemmProb<LA, LB, EP> pr[1] = {{{g3, M}, {rt + RL.w3}, {g2, a2, C2_OUT, M, C2_OUT}}};
             gemm<T, 64>(ctx, pr, 1, M, C2_OUT, K3, 1, 148);
+        } else if ((ctx->shift & 8) && (ctx->shift & 2) && ctx->u8) {  // as below, decisions as bits (conv2 fwd)
+            using OA = ShDgrad3; using OB = ShWeightDgrad<Conv3, false>; using EP = EpMaskBits<T>;
+            ShiftProb<OA, OB, EP> pr[1];
+            pr[0].a.map = sh_grad_map<Conv3>(ctx, g3, B);
+            pr[0].a.batch = B;
+            pr[0].b.map = wdgrad_map_sw<Conv3>(ctx, rt + RL.w3);
+            pr[0].ep = {g2, ctx->mbits2, C2_OUT, M, C2_OUT, 2};
+            gemm_shift_launch<64, 1>(ctx, pr, 1, C2_OUT);
         } else if (ctx->shift & 8) {  // shifted windows over the zero-padded g3 of each sample
             using OA = ShDgrad3; using OB = ShWeightDgrad<Conv3, false>; using EP = EpMask<T>;
             ShiftProb<OA, OB, EP> pr[1];
@@ -1197,7 +1211,20 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         pr[0].ep = {g1, a1, C1_OUT, M, C1_OUT};                                                                \
         gemm_shift_launch<32, MB_>(ctx, pr, 1, C1_OUT);                                                        \
     }
-            if (B < ctx->num_sms) SH_D2(4, 1) else SH_D2(1, 4)  // few samples: one phase per tile
+#define SH_D2B(MS_, MB_)                                                                                       \
+    {                                                                                                          \
+        using OA = ShDgrad2<MS_>; using OB = ShWeightDgrad<Conv2, true>; using EP = EpMaskBits<T>;             \
+        ShiftProb<OA, OB, EP> pr[1];                                                                           \
+        pr[0].a.map = sh_grad_map<Conv2>(ctx, g2, B);                                                          \
+        pr[0].a.batch = B;                                                                                     \
+        pr[0].b.map = wdgrad_map_sw<Conv2>(ctx, rt + RL.w2);                                                   \
+        pr[0].ep = {g1, ctx->mbits1, C1_OUT, M, C1_OUT, 1};                                                    \
+        gemm_shift_launch<32, MB_>(ctx, pr, 1, C1_OUT);                                                        \
+    }
+            if (ctx->u8) {  // the ReLU decisions as bits (conv1's forward stored them)
+                if (B < ctx->num_sms) SH_D2B(4, 1) else SH_D2B(1, 4)
+            } else if (B < ctx->num_sms) SH_D2(4, 1) else SH_D2(1, 4)  // few samples: one phase per tile
+#undef SH_D2B
 #undef SH_D2
         } else {  // TMA: the stride-2 transpose as 4 phase problems of 2x2 taps (no zero taps)
             using OA = OpDgradS<Conv2, 1>; using OB = OpWdgradMNS<Conv2>; using EP = EpMask<T>;
@@ -1526,6 +1553,8 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     void* g2 = c.take<uint8_t>(Bs * A2 * esz);
     void* g3 = c.take<uint8_t>(Bs * A3 * esz);
     void* g4 = c.take<uint8_t>(Bs * A4 * esz);
+    uint32_t* mbits1 = c.take<uint32_t>(u8_staging(cfg) ? Bs * H1 * H1 : 0);
+    uint32_t* mbits2 = c.take<uint32_t>(u8_staging(cfg) ? Bs * H2 * H2 * 2 : 0);
     uint8_t* sa = c.take<uint8_t>(Bs);
     uint8_t* sd = c.take<uint8_t>(Bs);
     float* sr = c.take<float>(Bs);
@@ -1600,6 +1629,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         ctx->s = s; ctx->s2 = s2; ctx->a1 = a1; ctx->a2 = a2; ctx->a3 = a3; ctx->a4 = a4;
         ctx->t1 = t1; ctx->t2 = t2; ctx->t3 = t3; ctx->t4 = t4;
         ctx->g1 = g1; ctx->g2 = g2; ctx->g3 = g3; ctx->g4 = g4;
+        ctx->mbits1 = mbits1; ctx->mbits2 = mbits2;
         ctx->sa = sa; ctx->sd = sd; ctx->sr = sr; ctx->sidx = sidx; ctx->dQ = dQ;
         ctx->sshard = sshard; ctx->shard_tab = shard_tab; ctx->rflags = rflags; ctx->replay_epoch = replay_epoch;
         ctx->n_snap = n_snap;
@@ -1702,6 +1732,16 @@ gorila_status gorila_debug_trace(uint64_t* out64) {
     return GORILA_OK;
 #else
     (void)out64;
+    return fail(GORILA_E_INVALID, "built without GORILA_TRACE");
+#endif
+}
+
+gorila_status gorila_debug_trace_tiles(uint64_t* out512) {
+#ifdef GORILA_TRACE
+    cudaMemcpyFromSymbol(out512, gorila_trace_tiles, sizeof(unsigned long long) * 512);
+    return GORILA_OK;
+#else
+    (void)out512;
     return fail(GORILA_E_INVALID, "built without GORILA_TRACE");
 #endif
 }

@@ -226,6 +226,10 @@ struct ShConv1FwdU8 {
         return (m < 441 && Y < 20 && X < 20) ? t * 400 + Y * 20 + X : -1;
     }
 };
+template <class E, class = void>
+struct ep_has_mask : std::false_type {};
+template <class E>
+struct ep_has_mask<E, std::void_t<decltype(std::declval<E>().mask)>> : std::true_type {};
 template <class O, class = void>
 struct shift_convert : std::false_type {};
 template <class O>
@@ -395,7 +399,9 @@ __global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
                 const int buf = tl % nbuf;
                 const uint32_t abuf = tl & 1;
                 mbar_wait(&a_full[buf], (tl / nbuf) & 1);
+                if (lane == 0) GTRACE_T(2, tl);
                 if (tl >= 2) mbar_wait(&acc_empty[abuf], ((tl >> 1) - 1) & 1);
+                if (lane == 0) GTRACE_T(3, tl);
                 tc_fence_after();
                 const uint32_t acc = tmem_u + abuf * CFG::ACC;
                 const uint32_t a0 = abase_u + buf * OA::BUF, b0 = bbase_u + prob * OB::NCH * OB::CHUNK;
@@ -419,32 +425,156 @@ __global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
                 }
                 umma_commit_w(&a_empty[buf]);
                 umma_commit_w(&acc_full[abuf]);
+                if (lane == 0) GTRACE_T(4, tl);
             }
         }
     } else if (CONV && warp >= 6) {  // converter warps: u8 staging -> the tile's bf16 planes
         if constexpr (CONV) {
+            // two register sets in turn: a tile's global reads are issued one tile ahead of its
+            // stores (a copy between the sets would wait on the loads in flight)
             constexpr int NT = 32 * SHIFT_CONV_WARPS;
             const int ct = tid - 192;
-            U8Planes<NT> cur, nxt;
-            int tl = 0, t = blockIdx.x;
-            if (t < ntiles) {
-                const int prob = t / tiles_per;
-                cur.load(p.prob[prob].a.sample(t - prob * tiles_per), ct);
-            }
-            for (; t < ntiles; t += gridDim.x, ++tl) {
-                const int tn = t + gridDim.x;
-                if (tn < ntiles) {
-                    const int pn = tn / tiles_per;
-                    nxt.load(p.prob[pn].a.sample(tn - pn * tiles_per), ct);
+            U8Planes<NT> r0, r1;
+            auto fetch = [&](int t, U8Planes<NT>& r) {
+                if (t < ntiles) {
+                    const int pr = t / tiles_per;
+                    r.load(p.prob[pr].a.sample(t - pr * tiles_per), ct);
                 }
+            };
+            auto put = [&](int tl, const U8Planes<NT>& r) {
                 const int buf = tl % nbuf;
+                if (ct == 0) GTRACE_T(0, tl);
                 if (tl >= nbuf) mbar_wait(&a_empty[buf], ((tl / nbuf) - 1) & 1);
-                cur.store(abase + buf * OA::BUF, OA::PLANE, ct);
+                r.store(abase + buf * OA::BUF, OA::PLANE, ct);
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a_full[buf]);
-                cur = nxt;
+                if (ct == 0) GTRACE_T(1, tl);
+            };
+            const int G = gridDim.x;
+            fetch(blockIdx.x, r0);
+            for (int t = blockIdx.x, tl = 0; t < ntiles; t += 2 * G, tl += 2) {
+                fetch(t + G, r1);
+                put(tl, r0);
+                if (t + G >= ntiles) break;
+                fetch(t + 2 * G, r0);
+                put(tl + 1, r1);
             }
+        }
+    } else if constexpr (ep_row_pre<EP>::value && BN <= 64) {
+        // epilogue warps 2..5, per-row inputs (the ReLU masks of a data gradient): every M-block's
+        // inputs of the NEXT tile are requested before this tile's accumulator is read, so their
+        // latency hides under a whole tile (two register sets in turn)
+        const int quad = warp & 3;
+        using PT = EpPre<EP>;
+        using PreT = typename PT::type;
+        constexpr int NC = BN / 16;
+        PreT pa[MB][NC], pb[MB][NC];
+        const int G = gridDim.x;
+        auto fetch = [&](int t, PreT (&pp)[MB][NC]) {
+            if (t >= ntiles) return;
+            const int prob = t / tiles_per, tile = t - prob * tiles_per;
+            const ShiftProb<OA, OB, EP>& P = p.prob[prob];
+            const int m0 = P.a.mb0(tile);
+#pragma unroll
+            for (int mb = 0; mb < MB; ++mb) {
+                const int i = P.a.row(tile, m0 + mb, quad * 32 + lane);
+#pragma unroll
+                for (int c = 0; c < NC; ++c)
+                    if (i >= 0) pp[mb][c] = PT::load(P.ep, i, c * 16);
+            }
+        };
+        auto drain = [&](int t, int tl, const PreT (&pp)[MB][NC]) {
+            const int prob = t / tiles_per, tile = t - prob * tiles_per;
+            const ShiftProb<OA, OB, EP>& P = p.prob[prob];
+            const EP ep = P.ep;
+            const uint32_t abuf = tl & 1;
+            const int m0 = P.a.mb0(tile);
+            if (quad == 2 && lane == 0) GTRACE_T(5, tl);
+            mbar_wait(&acc_full[abuf], (tl >> 1) & 1);
+            if (quad == 2 && lane == 0) GTRACE_T(6, tl);
+            tc_fence_after();
+            const uint32_t acc = tmem + abuf * CFG::ACC + ((uint32_t)(quad * 32) << 16);
+#pragma unroll
+            for (int mb = 0; mb < MB; ++mb) {
+                const int i = P.a.row(tile, m0 + mb, quad * 32 + lane);
+#pragma unroll
+                for (int c2 = 0; c2 < NC; c2 += 2) {
+                    float v[32];
+                    if (c2 + 1 < NC) tmem_ld16x2(acc + (uint32_t)(mb * BN + c2 * 16), v);
+                    else tmem_ld16(acc + (uint32_t)(mb * BN + c2 * 16), v);
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        if (c2 + h < NC && i >= 0 && (c2 + h) * 16 < p.N)
+                            PT::apply(ep, i, (c2 + h) * 16, v + 16 * h, pp[mb][c2 + h], 0);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[abuf]);
+            if (quad == 2 && lane == 0) GTRACE_T(7, tl);
+        };
+        fetch(blockIdx.x, pa);
+        for (int t = blockIdx.x, tl = 0; t < ntiles; t += 2 * G, tl += 2) {
+            fetch(t + G, pb);
+            drain(t, tl, pa);
+            if (t + G >= ntiles) break;
+            fetch(t + 2 * G, pa);
+            drain(t + G, tl + 1, pb);
+        }
+    } else if constexpr (ep_col_pre<EP>::value && BN <= 64) {
+        // epilogue warps 2..5, column-only inputs (the biases): loaded once per CTA (per problem);
+        // the accumulator is read 32 columns per TMEM wait
+        const int quad = warp & 3;
+        using PT = EpPre<EP>;
+        constexpr int NC = BN / 16;
+        typename PT::type pre[NC];
+        int pre_prob = -1;  // a CTA's tiles run in increasing order: its problem changes at most nprob - 1 times
+        int tl = 0;
+        for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+            const int prob = t / tiles_per, tile = t - prob * tiles_per;
+            const ShiftProb<OA, OB, EP>& P = p.prob[prob];
+            const EP ep = P.ep;
+            if (prob != pre_prob) {
+#pragma unroll
+                for (int c = 0; c < NC; ++c) pre[c] = PT::load(ep, 0, c * 16);
+                pre_prob = prob;
+            }
+            const uint32_t abuf = tl & 1;
+            const int m0 = P.a.mb0(tile);
+            if (quad == 2 && lane == 0) GTRACE_T(5, tl);
+            mbar_wait(&acc_full[abuf], (tl >> 1) & 1);
+            if (quad == 2 && lane == 0) GTRACE_T(6, tl);
+            tc_fence_after();
+            const uint32_t acc = tmem + abuf * CFG::ACC + ((uint32_t)(quad * 32) << 16);
+#pragma unroll 1
+            for (int mb = 0; mb < MB; ++mb) {
+                const int i = P.a.row(tile, m0 + mb, quad * 32 + lane);
+#pragma unroll
+                for (int c2 = 0; c2 < NC; c2 += 2) {
+                    float v[32];
+                    if (c2 + 1 < NC) tmem_ld16x2(acc + (uint32_t)(mb * BN + c2 * 16), v);
+                    else tmem_ld16(acc + (uint32_t)(mb * BN + c2 * 16), v);
+                    if constexpr (ep_has_mask<EP>::value) {
+                        if (ep.mask != nullptr) {  // the ReLU decisions as bits, one word per 32 columns
+                            if (i >= 0 && c2 + 1 < NC && (c2 + 2) * 16 <= p.N) {
+                                const uint32_t lo = ep.apply16m(i, c2 * 16, v, pre[c2]);
+                                const uint32_t hi = ep.apply16m(i, c2 * 16 + 16, v + 16, pre[c2 + 1]);
+                                ep.mask[(int64_t)i * (p.N >> 5) + (c2 >> 1)] = lo | (hi << 16);
+                            }
+                            continue;
+                        }
+                    }
+#pragma unroll
+                    for (int h = 0; h < 2; ++h)
+                        if (c2 + h < NC && i >= 0 && (c2 + h) * 16 < p.N)
+                            PT::apply(ep, i, (c2 + h) * 16, v + 16 * h, pre[c2 + h], 0);
+                }
+            }
+            tc_fence_before();
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&acc_empty[abuf]);
+            if (quad == 2 && lane == 0) GTRACE_T(7, tl);
         }
     } else {  // epilogue warps 2..5 (warp w reads TMEM lanes 32*(w%4) ..)
         const int quad = warp & 3;
@@ -464,7 +594,9 @@ __global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
                 for (int d = 0; d < PD; ++d)
                     if (i >= 0) pre[d] = PT::load(ep, i, d * 16);
             }
+            if (quad == 2 && lane == 0) GTRACE_T(5, tl);
             mbar_wait(&acc_full[abuf], (tl >> 1) & 1);
+            if (quad == 2 && lane == 0) GTRACE_T(6, tl);
             tc_fence_after();
             const uint32_t acc = tmem + abuf * CFG::ACC + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
@@ -486,6 +618,7 @@ __global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[abuf]);
+            if (quad == 2 && lane == 0) GTRACE_T(7, tl);
         }
     }
     tc_fence_before();
@@ -598,17 +731,25 @@ __global__ void __launch_bounds__(c1wg::THREADS) k_conv1_wgrad_u8(const __grid_c
     } else {  // converter warps 2..9: the samples' u8 staging -> bf16 planes
         constexpr int NT = 32 * CONV_WARPS;
         const int ct = tid - 64;
-        U8Planes<NT> cur, nxt;
-        if (nt > 0) cur.load(p.s8 + (int64_t)blockIdx.x * U8_SAMPLE, ct);
-        for (int tl = 0; tl < nt; ++tl) {
-            if (tl + 1 < nt) nxt.load(p.s8 + (int64_t)(blockIdx.x + (tl + 1) * gridDim.x) * U8_SAMPLE, ct);
+        U8Planes<NT> r0, r1;  // two register sets in turn (see gemm_shift's converter)
+        auto fetch = [&](int tl, U8Planes<NT>& r) {
+            if (tl < nt) r.load(p.s8 + (int64_t)(blockIdx.x + tl * gridDim.x) * U8_SAMPLE, ct);
+        };
+        auto put = [&](int tl, const U8Planes<NT>& r) {
             const int s = tl % NBUF;
             if (tl >= NBUF) mbar_wait(&empty[s], ((tl / NBUF) - 1) & 1);
-            cur.store(sbase + s * STAGE, PLANE, ct);
+            r.store(sbase + s * STAGE, PLANE, ct);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&a_full[s]);
-            cur = nxt;
+        };
+        fetch(0, r0);
+        for (int tl = 0; tl < nt; tl += 2) {
+            fetch(tl + 1, r1);
+            put(tl, r0);
+            if (tl + 1 >= nt) break;
+            fetch(tl + 2, r0);
+            put(tl + 1, r1);
         }
         if (warp < 6) {  // epilogue (warps 2..5 = TMEM lane quarters 2, 3, 0, 1)
             const int quad = warp & 3;

@@ -73,7 +73,7 @@ EXPORTS = ["gorila_param_count", "gorila_workspace_bytes", "gorila_init", "goril
            "gorila_get_q", "gorila_get_activation", "gorila_act", "gorila_kernel_launches", "gorila_profile_enable", "gorila_profile_read",
            "gorila_profile_phase_count", "gorila_profile_phase_name", "gorila_nccl_unique_id", "gorila_round",
            "gorila_round_async", "gorila_round_post", "gorila_round_fetch",
-           "gorila_bench_phase", "gorila_debug_trace", "gorila_capture_activations",
+           "gorila_bench_phase", "gorila_debug_trace", "gorila_debug_trace_tiles", "gorila_capture_activations",
            "gorila_get_learner_activation", "gorila_peer_record", "gorila_peer_connect", "gorila_async_run"]
 
 
@@ -129,6 +129,7 @@ def load(build_if_missing=True):
     L.gorila_round_async.argtypes = [P, P, i32, u64, P, P, P, P]
     L.gorila_bench_phase.argtypes = [P, i32, i32, i32, P]
     L.gorila_debug_trace.argtypes = [P]
+    L.gorila_debug_trace_tiles.argtypes = [P]
     _lib = L
     return L
 
