@@ -222,6 +222,7 @@ struct gorila_ctx {
     // conv2 / conv3 data gradients read (EpMaskBits) instead of the activations
     uint32_t* mbits1 = nullptr;  // [B * 400] one word (32 channels) per a1 row
     uint32_t* mbits2 = nullptr;  // [B * 81][2]
+    float* part_bias[3] = {};    // u8 path: b1..b3 partials [split_w[l]][C] from the weight-gradient GEMMs
     // side stream for the weight-gradient GEMMs, which are off the dgrad critical path
     // (a fork / join of the round; a graph captures it as parallel branches)
     cudaStream_t side = nullptr;
@@ -596,6 +597,15 @@ void gemm_shift_launch(gorila_ctx* ctx, const ShiftProb<OA, OB, EP>* probs, int 
     cfg.numAttrs = base_attrs(ctx, at, 0, ctx->pdl);
     cudaLaunchKernelEx(&cfg, gemm_shift<BN, MB, OA, OB, EP>, gb);
     ctx->launches++;
+}
+template <class W>
+void wgrad_shift_launch(gorila_ctx* ctx, const WgradShiftParams& wp, int grid) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_wgrad_shift<W>, cudaFuncAttributeMaxDynamicSharedMemorySize, wgs::Cfg<W>::SMEM);
+        attr = true;
+    }
+    launch(ctx, k_wgrad_shift<W>, dim3(grid), dim3(192), wgs::Cfg<W>::SMEM, wp);
 }
 // tensor maps of the shifted-window operands
 CUtensorMap sh_conv3_map(gorila_ctx* ctx, const void* a2, int B) {  // flat (64, B*81), box (64, 148)
@@ -1104,6 +1114,61 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }
     }
     mark(ctx, PH_FC4DG);
+    // K10's segments: 0 W1, 1 W2, 2 W3, 3..6 b1..b4 (wide: many partials per element), 7 W5 + b5
+    WgradReduceParams all{};
+    {
+        all.part[0] = ctx->part_w[0]; all.part[1] = ctx->part_w[1]; all.part[2] = ctx->part_w[2];
+        all.splits[0] = ctx->split_w[0];
+        all.splits[1] = ctx->split_w[1];
+        all.splits[2] = ctx->split_w[2];
+        all.count[0] = (int64_t)C1_OUT * K1; all.count[1] = (int64_t)C2_OUT * K2; all.count[2] = (int64_t)C3_OUT * K3;
+        all.off[0] = OFF_W1; all.off[1] = OFF_W2; all.off[2] = OFF_W3;
+        const int bc[4] = {C1_OUT, C2_OUT, C3_OUT, FC4_OUT};
+        const int64_t boff[4] = {OFF_B1, OFF_B2, OFF_B3, OFF_B4};
+        const float* bp = ctx->part_b;
+        for (int l = 0; l < 4; ++l) {
+            all.part[3 + l] = bp; all.splits[3 + l] = ctx->bias_chunks; all.count[3 + l] = bc[l];
+            all.off[3 + l] = boff[l];
+            bp += (int64_t)ctx->bias_chunks * bc[l];
+        }
+        all.part[7] = ctx->part5;  // W5 and b5 (contiguous); the fused head writes one chunk
+        all.splits[7] = fc5_fused ? 1 : (B + fc5_rows(B) - 1) / fc5_rows(B);
+        all.count[7] = (int64_t)nA * (FC4_OUT + 1); all.off[7] = OFF_W5;
+        for (int l = 3; l < 7; ++l) all.wide[l] = 1;
+        if (ctx->u8)  // b1..b3 from the weight-gradient GEMMs' ones accumulators, one partial per CTA
+            for (int l = 0; l < 3; ++l) {
+                all.part[3 + l] = ctx->part_bias[l]; all.splits[3 + l] = ctx->split_w[l]; all.wide[3 + l] = 0;
+            }
+        all.nseg = 8;
+        all.accumulate = accumulate;
+        for (int l = 0; l < all.nseg; ++l) all.coop |= !all.wide[l] && all.splits[l] >= 64 ? 1 : 0;
+    }
+    auto pick = [&](std::initializer_list<int> segs) {
+        WgradReduceParams p{};
+        for (int l : segs) {
+            p.part[p.nseg] = all.part[l]; p.splits[p.nseg] = all.splits[l]; p.count[p.nseg] = all.count[l];
+            p.off[p.nseg] = all.off[l]; p.wide[p.nseg] = all.wide[l];
+            ++p.nseg;
+        }
+        p.accumulate = all.accumulate;
+        for (int l = 0; l < p.nseg; ++l) p.coop |= !p.wide[l] && p.splits[l] >= 64 ? 1 : 0;
+        return p;
+    };
+    static const bool split_red = [] {  // GORILA_SPLIT_REDUCE=0: one K10 after the join
+        const char* e = getenv("GORILA_SPLIT_REDUCE");
+        return !(e && atoi(e) == 0);
+    }();
+    // grid of a K10 launch: one block per 32 [split][element] elements, one warp per wide element
+    auto red_grid = [](const WgradReduceParams& q) {
+        int64_t tot = 0, totw = 0;
+        for (int l = 0; l < q.nseg; ++l) (q.wide[l] ? totw : tot) += q.count[l];
+        if (!q.coop) return 148 * 2;  // a thread per element
+        return (int)std::min<int64_t>(4096, std::max<int64_t>({148, (tot + 31) / 32, (totw + 7) / 8}));
+    };
+    // u8 path, forked round: b4's partials right after fc4's weight gradient and the side stream's
+    // reduction right after conv2's weight gradient (neither waits for g1), so both run under the
+    // main stream's conv2 data gradient / conv1 weight gradient
+    const bool early_side = fk && ctx->u8 && split_red;
     PHASE(PH_FC4WG) {
     // fc4 wgrad (i = k, j = n, red = b): G[W4][n][k] += sum_b a3[b][k] g4[b][n]
     {
@@ -1129,6 +1194,11 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         ctx->stream = ctx->side;
         early_apply_p2p(ctx, round);
         ctx->stream = m;
+    }
+    if (early_side) {
+        OnSide on_side(ctx, true);
+        launch(ctx, k_bias_partial<T>, dim3(ctx->bias_chunks, 1), dim3(256), 0, (const T*)g1, (const T*)g2,
+               (const T*)g3, (const T*)g4, B, ctx->part_b, ctx->bias_chunks, 3);
     }
     if (fk) fork_side(ctx, 1);  // g3 ready (fc4 dgrad is on the main stream before this point)
     PHASE(PH_CONV3DG) {
@@ -1180,6 +1250,22 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             GemmProb<LA, LB, EP> pr[1] = {{{a2, Mred}, {g3, C3_OUT, C3_OUT, Mred},
                                            {ctx->part_w[2], K3, (int64_t)C3_OUT * K3, 1.f, K3, C3_OUT}}};
             gemm<T, 64>(ctx, pr, 1, K3, C3_OUT, Mred, ctx->split_w[2]);
+        } else if (ctx->u8) {  // shifted windows: every tap a start row of a2 (k_wgrad_shift)
+            WgradShiftParams wp;
+            {
+                const uint64_t dims[3] = {64, 81, (uint64_t)B}, str[2] = {128, 81 * 128};
+                const uint32_t box[3] = {64, 81, 1};
+                wp.a_map = tmap(ctx, a2, 3, dims, str, box, nullptr, 128);
+            }
+            {
+                const uint64_t dims[4] = {64, 7, 7, (uint64_t)B}, str[3] = {128, 7 * 128, 49 * 128};
+                const uint32_t box[4] = {64, 9, 9, 1};
+                wp.g_map = tmap(ctx, g3, 4, dims, str, box, nullptr, 128);
+            }
+            wp.part = ctx->part_w[2];
+            wp.part_b = ctx->part_bias[2];
+            wp.batch = B;
+            wgrad_shift_launch<WgConv3>(ctx, wp, ctx->split_w[2]);
         } else {  // TMA: K-chunk = one sample's 49 pixels (64 rows, zero tail in the gradient operand)
             using OA = OpWgradInS<Conv3, 64>; using OB = OpWgradOutS<64, 64, false>; using EP = EpStoreT;
             TmaProb<OA, OB, EP> pr[1];
@@ -1253,6 +1339,18 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             GemmProb<LA, LB, EP> pr[1] = {{{a1, Mred}, {g2, C2_OUT, C2_OUT, Mred},
                                            {ctx->part_w[1], K2, (int64_t)C2_OUT * K2, 1.f, K2, C2_OUT}}};
             gemm<T, 64>(ctx, pr, 1, K2, C2_OUT, Mred, ctx->split_w[1]);
+        } else if (ctx->u8) {  // shifted windows over the stride phases of a1 (k_wgrad_shift)
+            WgradShiftParams wp;
+            wp.a_map = sh_conv2_map(ctx, a1, B);
+            {
+                const uint64_t dims[4] = {64, 9, 9, (uint64_t)B}, str[3] = {128, 9 * 128, 81 * 128};
+                const uint32_t box[4] = {64, 10, 9, 1};
+                wp.g_map = tmap(ctx, g2, 4, dims, str, box, nullptr, 128);
+            }
+            wp.part = ctx->part_w[1];
+            wp.part_b = ctx->part_bias[1];
+            wp.batch = B;
+            wgrad_shift_launch<WgConv2>(ctx, wp, ctx->split_w[1]);
         } else {  // TMA: K-chunk = one sample's 81 pixels (96 rows, zero tail)
             using OA = OpWgradInS<Conv2, 96>; using OB = OpWgradOutS<64, 96, false>; using EP = EpStoreT;
             TmaProb<OA, OB, EP> pr[1];
@@ -1264,6 +1362,11 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }
     }
     mark(ctx, PH_CONV2WG);
+    if (early_side) {
+        OnSide on_side(ctx, true);
+        const WgradReduceParams q = pick({1, 2, 4, 5, 6});
+        launch(ctx, k_wgrad_reduce, dim3(red_grid(q)), dim3(256), 0, q, Gd);
+    }
     if (fk) fork_side(ctx, 3);  // g1 ready
     PHASE(PH_CONV1WG) {
     // conv1 wgrad (input scale 1/255 folded into the store)
@@ -1283,6 +1386,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             }
             wp.s8 = (const uint8_t*)ctx->s;
             wp.part = ctx->part_w[0];
+            wp.part_b = ctx->part_bias[0];
             wp.scale = in_scale;
             wp.batch = B;
             static bool attr = false;
@@ -1302,62 +1406,28 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }
     }
     mark(ctx, PH_CONV1WG);
-    // K10's segments: 0 W1, 1 W2, 2 W3, 3..6 b1..b4 (wide: many partials per element), 7 W5 + b5
-    WgradReduceParams all{};
-    {
-        all.part[0] = ctx->part_w[0]; all.part[1] = ctx->part_w[1]; all.part[2] = ctx->part_w[2];
-        all.splits[0] = ctx->split_w[0];
-        all.splits[1] = ctx->split_w[1];
-        all.splits[2] = ctx->split_w[2];
-        all.count[0] = (int64_t)C1_OUT * K1; all.count[1] = (int64_t)C2_OUT * K2; all.count[2] = (int64_t)C3_OUT * K3;
-        all.off[0] = OFF_W1; all.off[1] = OFF_W2; all.off[2] = OFF_W3;
-        const int bc[4] = {C1_OUT, C2_OUT, C3_OUT, FC4_OUT};
-        const int64_t boff[4] = {OFF_B1, OFF_B2, OFF_B3, OFF_B4};
-        const float* bp = ctx->part_b;
-        for (int l = 0; l < 4; ++l) {
-            all.part[3 + l] = bp; all.splits[3 + l] = ctx->bias_chunks; all.count[3 + l] = bc[l];
-            all.off[3 + l] = boff[l];
-            bp += (int64_t)ctx->bias_chunks * bc[l];
-        }
-        all.part[7] = ctx->part5;  // W5 and b5 (contiguous); the fused head writes one chunk
-        all.splits[7] = fc5_fused ? 1 : (B + fc5_rows(B) - 1) / fc5_rows(B);
-        all.count[7] = (int64_t)nA * (FC4_OUT + 1); all.off[7] = OFF_W5;
-        for (int l = 3; l < 7; ++l) all.wide[l] = 1;
-        all.nseg = 8;
-        all.accumulate = accumulate;
-    }
-    auto pick = [&](std::initializer_list<int> segs) {
-        WgradReduceParams p{};
-        for (int l : segs) {
-            p.part[p.nseg] = all.part[l]; p.splits[p.nseg] = all.splits[l]; p.count[p.nseg] = all.count[l];
-            p.off[p.nseg] = all.off[l]; p.wide[p.nseg] = all.wide[l];
-            ++p.nseg;
-        }
-        p.accumulate = all.accumulate;
-        return p;
-    };
-    static const bool split_red = [] {  // GORILA_SPLIT_REDUCE=0: one K10 after the join
-        const char* e = getenv("GORILA_SPLIT_REDUCE");
-        return !(e && atoi(e) == 0);
-    }();
-    PHASE(PH_BIASG) {
+    PHASE(PH_BIASG) if (!early_side) {
     // bias gradients b1..b4 (coalesced partials; reduced by K10)
     OnSide on_side(ctx, fk);
-    launch(ctx, k_bias_partial<T>, dim3(ctx->bias_chunks, 4), dim3(256), 0, (const T*)g1, (const T*)g2, (const T*)g3,
-           (const T*)g4, B, ctx->part_b, ctx->bias_chunks);
+    const int l0 = ctx->u8 ? 3 : 0;  // u8 path: only b4 here (b1..b3 came with the weight gradients)
+    launch(ctx, k_bias_partial<T>, dim3(ctx->bias_chunks, 4 - l0), dim3(256), 0, (const T*)g1, (const T*)g2,
+           (const T*)g3, (const T*)g4, B, ctx->part_b, ctx->bias_chunks, l0);
     // forked round: the side stream reduces what it produced (conv2 / conv3 weights, the biases)
     // while the main stream finishes conv1's weight gradient
-    static const int side_red_ctas = [] {
-        const char* e = getenv("GORILA_SIDE_RED_CTAS");
-        return e ? std::max(1, atoi(e)) : 148 * 2;
-    }();
-    if (split_red && fk && (phases & (1u << PH_WGRED))) launch(ctx, k_wgrad_reduce, dim3(side_red_ctas), dim3(256), 0, pick({1, 2, 3, 4, 5, 6}), Gd);
+    if (split_red && fk && (phases & (1u << PH_WGRED))) {
+        const WgradReduceParams q = pick({1, 2, 3, 4, 5, 6});
+        launch(ctx, k_wgrad_reduce, dim3(red_grid(q)), dim3(256), 0, q, Gd);
+    }
     }
     mark(ctx, PH_BIASG);
     if (fk) join_side(ctx);
     PHASE(PH_WGRED) {
     // K10: fixed-order reduction of the conv wgrad partials into G (the rest of it when forked)
-    launch(ctx, k_wgrad_reduce, dim3(148 * 2), dim3(256), 0, (fk && split_red) ? pick({0, 7}) : all, Gd);
+    {
+        // (u8 path: b1 comes from conv1's weight gradient on the main stream, so the main reduce takes it)
+        const WgradReduceParams q = (fk && split_red) ? (ctx->u8 ? pick({0, 3, 7}) : pick({0, 7})) : all;
+        launch(ctx, k_wgrad_reduce, dim3(red_grid(q)), dim3(256), 0, q, Gd);
+    }
     }
     mark(ctx, PH_WGRED);
     CU(cudaGetLastError());
@@ -1605,11 +1675,17 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
             const int want = std::max(1, std::min(lim, (148 + ta - 1) / ta));
             const int cps = (nch + want - 1) / want;
             split_w[l] = (nch + cps - 1) / cps;
-            if (l == 0 && u8_staging(cfg)) split_w[0] = std::min(148, B);  // k_conv1_wgrad_u8: one per CTA
+            // k_conv1_wgrad_u8 / k_wgrad_shift: one partial per CTA
+            if (u8_staging(cfg)) split_w[l] = std::min(148, B);
         }
         part_w[l] = c.take<float>((int64_t)split_w[l] * wcount[l]);
     }
     float* part_b = c.take<float>((int64_t)bias_chunks * (C1_OUT + C2_OUT + C3_OUT + FC4_OUT));
+    float* part_bias[3];
+    {
+        const int bc[3] = {C1_OUT, C2_OUT, C3_OUT};
+        for (int l = 0; l < 3; ++l) part_bias[l] = c.take<float>(u8_staging(cfg) ? (int64_t)split_w[l] * bc[l] : 0);
+    }
     float* part5 = c.take<float>((int64_t)((B + fc5_rows(B) - 1) / fc5_rows(B)) * nA * (FC4_OUT + 1));
     float* tmp_canon = c.take<float>(P);
     float* tmp_int = c.take<float>(W * q);
@@ -1637,6 +1713,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         ctx->td_partial = td_partial; ctx->bias_chunks = bias_chunks;
         for (int l = 0; l < 3; ++l) { ctx->part_w[l] = part_w[l]; ctx->split_w[l] = split_w[l]; }
         ctx->part_b = part_b;
+        for (int l = 0; l < 3; ++l) ctx->part_bias[l] = part_bias[l];
         ctx->part5 = part5;
         ctx->tmp_canon = tmp_canon; ctx->tmp_int = tmp_int;
     }

@@ -851,12 +851,13 @@ __global__ void __launch_bounds__(256) k_act_head(const float* __restrict__ a4, 
 template <typename T>
 __global__ void __launch_bounds__(256) k_bias_partial(const T* __restrict__ g1, const T* __restrict__ g2,
                                                       const T* __restrict__ g3, const T* __restrict__ g4, int B,
-                                                      float* __restrict__ part, int BIAS_CHUNKS) {
+                                                      float* __restrict__ part, int BIAS_CHUNKS, int l0) {
     pdl_wait();
     pdl_trigger();
     // each thread owns 8 consecutive channels (one 16-B vector per row) of rows rg, rg+RG, ...
+    // (layers l0..3: from the u8 path on, b1..b3 come from the weight-gradient GEMMs, l0 = 3)
     __shared__ float red[256 * 8];
-    const int l = blockIdx.y, chunk = blockIdx.x;
+    const int l = blockIdx.y + l0, chunk = blockIdx.x;
     const T* g = l == 0 ? g1 : l == 1 ? g2 : l == 2 ? g3 : g4;
     const int C = l == 0 ? C1_OUT : l == 3 ? FC4_OUT : C2_OUT;
     const int rows = B * (l == 0 ? H1 * H1 : l == 1 ? H2 * H2 : l == 2 ? H3 * H3 : 1);
@@ -899,6 +900,7 @@ struct WgradReduceParams {
     int64_t off[WRED_SEGS];
     int wide[WRED_SEGS];  // 1: partials stored [element][split] and summed by one warp per element
     int nseg, accumulate;
+    int coop;  // 1: [split][element] sums split over a block's 8 warps (many splits: one partial per CTA)
 };
 __global__ void k_wgrad_reduce(WgradReduceParams p, float* __restrict__ G) {
     pdl_wait();
@@ -927,27 +929,66 @@ __global__ void k_wgrad_reduce(WgradReduceParams p, float* __restrict__ G) {
             *dst = p.accumulate ? *dst + acc : acc;
         }
     }
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    if (!p.coop) {  // few splits: a thread per element, 8 independent partial sums in flight
+        for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+            int l = 0;
+            int64_t f = e;
+            while (p.wide[l] || f >= p.count[l]) {
+                if (!p.wide[l]) f -= p.count[l];
+                ++l;
+            }
+            const float* src = p.part[l] + f;
+            const int S = p.splits[l];
+            const int64_t st = p.count[l];
+            float a8[8] = {};
+            int s = 0;
+            for (; s + 8 <= S; s += 8) {
+#pragma unroll
+                for (int u = 0; u < 8; ++u) a8[u] += src[(int64_t)(s + u) * st];
+            }
+            for (int u = 0; s < S; ++s, ++u) a8[u] += src[(int64_t)s * st];
+            const float acc = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
+            float* dst = G + p.off[l] + f;
+            *dst = p.accumulate ? *dst + acc : acc;
+        }
+        return;
+    }
+    // many splits: a block takes 32 consecutive elements, its 8 warps the splits s = w, w + 8, ...
+    // (coalesced 128-B rows, 8 loads in flight per lane), combined in a fixed order through shared
+    // memory (the split count reaches 148 with the one-partial-per-CTA GEMMs)
+    __shared__ float red[8][33];
+    const int x = threadIdx.x & 31, y = threadIdx.x >> 5, ny = blockDim.x >> 5;
+    for (int64_t g0 = (int64_t)blockIdx.x * 32; g0 < total; g0 += (int64_t)gridDim.x * 32) {
+        const int64_t e = g0 + x;
+        float acc = 0.f;
         int l = 0;
         int64_t f = e;
-        while (p.wide[l] || f >= p.count[l]) {
-            if (!p.wide[l]) f -= p.count[l];
-            ++l;
-        }
-        // 8 independent partial sums (all loads in flight), combined in a fixed order
-        const float* src = p.part[l] + f;
-        const int S = p.splits[l];
-        const int64_t st = p.count[l];
-        float a8[8] = {};
-        int s = 0;
-        for (; s + 8 <= S; s += 8) {
+        if (e < total) {
+            while (p.wide[l] || f >= p.count[l]) {
+                if (!p.wide[l]) f -= p.count[l];
+                ++l;
+            }
+            const float* src = p.part[l] + f;
+            const int S = p.splits[l];
+            const int64_t st = p.count[l];
+            float a8[8] = {};  // 8 loads in flight per lane
+            int s = y;
+            for (; s + 7 * ny < S; s += 8 * ny) {
 #pragma unroll
-            for (int u = 0; u < 8; ++u) a8[u] += src[(int64_t)(s + u) * st];
+                for (int u = 0; u < 8; ++u) a8[u] += src[(int64_t)(s + u * ny) * st];
+            }
+            for (int u = 0; s < S; s += ny, ++u) a8[u & 7] += src[(int64_t)s * st];
+            acc = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
         }
-        for (int u = 0; s < S; ++s, ++u) a8[u] += src[(int64_t)s * st];
-        const float acc = ((a8[0] + a8[1]) + (a8[2] + a8[3])) + ((a8[4] + a8[5]) + (a8[6] + a8[7]));
-        float* dst = G + p.off[l] + f;
-        *dst = p.accumulate ? *dst + acc : acc;
+        red[y][x] = acc;
+        __syncthreads();
+        if (y == 0 && e < total) {
+            float t = red[0][x];
+            for (int w = 1; w < ny; ++w) t += red[w][x];
+            float* dst = G + p.off[l] + f;
+            *dst = p.accumulate ? *dst + t : t;
+        }
+        __syncthreads();
     }
 }
 

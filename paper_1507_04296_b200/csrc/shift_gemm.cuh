@@ -643,23 +643,33 @@ struct Conv1WgradU8 {
     CUtensorMap g1_map;  // (32, 20, 20, B) bf16, box (32, 21, 20, 1), SWIZZLE_64B
     const uint8_t* s8;   // [B][U8_SAMPLE]
     float* part;         // [gridDim.x][32][256]
+    float* part_b;       // [gridDim.x][32]: the CTA's sum of g1 (bias b1's gradient)
     float scale;
     int batch;
 };
+// The bias gradient rides along as one more accumulator: D[m][o] += sum_p ONE[m][p] g[p][o] with an
+// A operand of ones (every row of D is the column sum of g). One 16-row block of bf16 ones (M = 64
+// rows of 128 B, MN-major) serves every K step.
+constexpr int ONES_BYTES = 16 * 128;
+GORILA_DEV void fill_ones(uint8_t* dst, int tid, int nthr) {
+    for (int o = tid * 16; o < ONES_BYTES; o += nthr * 16)
+        *reinterpret_cast<uint4*>(dst + o) = make_uint4(0x3F803F80u, 0x3F803F80u, 0x3F803F80u, 0x3F803F80u);
+}
 namespace c1wg {
 constexpr int KSTEPS = 27;                           // 432 virtual rows, 420 of them g1 rows (21 x 20)
 constexpr int PLANE = ShConv1FwdU8::PLANE;           // 544 rows of 32 B (rows <= 431 + 22 are read)
 constexpr int ABUF = 4 * PLANE, BBUF = KSTEPS * 16 * 64, STAGE = ABUF + BBUF;  // 69632 + 27648
 constexpr int NBUF = 2, CONV_WARPS = 8, THREADS = 64 + 32 * CONV_WARPS;     // warps 2.. convert
-constexpr int SMEM = 1024 + NBUF * STAGE + 128;
-constexpr uint32_t TCOLS = 64;
+constexpr int SMEM = 1024 + NBUF * STAGE + ONES_BYTES + 128;
+constexpr uint32_t TCOLS = 128;  // 4 (dy, dx) accumulators in columns 0..63, the ones accumulator 64..95
 }  // namespace c1wg
 
 __global__ void __launch_bounds__(c1wg::THREADS) k_conv1_wgrad_u8(const __grid_constant__ Conv1WgradU8 p) {
     using namespace c1wg;
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
-    uint64_t* bars = reinterpret_cast<uint64_t*>(smem + NBUF * STAGE);
+    uint8_t* ones = smem + NBUF * STAGE;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(ones + ONES_BYTES);
     uint64_t* a_full = bars;               // [NBUF] converter warps
     uint64_t* b_full = a_full + NBUF;      // [NBUF] TMA of g1
     uint64_t* empty = b_full + NBUF;       // [NBUF] MMA commit
@@ -677,6 +687,7 @@ __global__ void __launch_bounds__(c1wg::THREADS) k_conv1_wgrad_u8(const __grid_c
         for (int o = 420 * 64 + tid * 16; o < BBUF; o += THREADS * 16)
             *reinterpret_cast<uint4*>(st + ABUF + o) = make_uint4(0, 0, 0, 0);
     }
+    fill_ones(ones, tid, THREADS);
     fence_proxy_async_smem();
     if (tid == 32) {
         for (int i = 0; i < NBUF; ++i) {
@@ -707,6 +718,7 @@ __global__ void __launch_bounds__(c1wg::THREADS) k_conv1_wgrad_u8(const __grid_c
         {  // MMA issuer (warp-uniform): per sample 27 K-steps x 4 (dy, dx) accumulators
             constexpr uint32_t IDESC = umma_idesc_bf16(64, 32) | (1u << 15) | (1u << 16);
             const uint32_t tmem_u = uniform_u32(tmem), sbase_u = uniform_u32(sbase);
+            const uint64_t od = umma_desc_mn_sw(sbase_u + NBUF * STAGE, 0, 128);  // the ones block
             for (int tl = 0; tl < nt; ++tl) {
                 const int s = tl % NBUF;
                 mbar_wait(&a_full[s], (tl / NBUF) & 1);
@@ -716,6 +728,7 @@ __global__ void __launch_bounds__(c1wg::THREADS) k_conv1_wgrad_u8(const __grid_c
 #pragma unroll 1
                 for (int kk = 0; kk < KSTEPS; ++kk) {
                     const uint64_t bd = umma_desc_mn_sw(b0 + kk * 1024, 0, 64);
+                    umma_bf16_w(tmem_u + 64, od, bd, IDESC, (tl > 0 || kk > 0) ? 1u : 0u);  // sum of g1
 #pragma unroll
                     for (int acc = 0; acc < 4; ++acc) {
                         const int dy = acc >> 1, dx = acc & 1;
@@ -773,11 +786,194 @@ __global__ void __launch_bounds__(c1wg::THREADS) k_conv1_wgrad_u8(const __grid_c
 #pragma unroll
                     for (int e = 0; e < 16; ++e) dst[(c0 + e) * K1 + k] = v[e] * p.scale;
                 }
+            if (quad == 0) {  // row 0 of the ones accumulator (lane 0): the CTA's sum of g1 per channel
+                float v[32];
+                if (nt > 0) tmem_ld16x2(tmem + 64, v);
+                else
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] = 0.f;
+                if (lane == 0)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) p.part_b[blockIdx.x * 32 + e] = v[e];
+            }
         }
     }
     tc_fence_before();
     __syncthreads();
     if (warp == 0) tmem_dealloc(tmem, TCOLS);
+}
+
+
+// ---------------------------------------------------------------- conv2 / conv3 weight gradients
+// Same construction as k_conv1_wgrad_u8 over bf16 activations loaded by TMA: per sample the layer
+// input (MN-major over input channels) and the output gradient g on the layer's virtual grid (the
+// input grid's width; columns / rows past the output are TMA zero fill); tap (ky, kx) of the kernel
+// reads the input rows shifted by its offset on that grid. One CTA per sample stride, all taps'
+// accumulators in TMEM across the CTA's samples, partial dW [o][k] per CTA (k_wgrad_reduce).
+//   conv3 (3x3, stride 1, a2 9x9x64 -> g3 7x7x64): grid 9 wide, 9 taps = 9 accumulators M = 64
+//     (the 64 input channels; two per TMEM column block at lane offsets 0 / 16), k = tap*64 + c.
+//   conv2 (4x4, stride 2, a1 20x20x32 -> g2 9x9x64): the four stride phases of a1 as planes (10 x 10
+//     rows of 32 channels, as conv2's forward loads them); per (dy, dx) one accumulator M = 128 =
+//     4 planes x 32 channels (kernel (2dy + py, 2dx + px)), grid 10 wide.
+struct WgConv3 {
+    static constexpr int NPLANE = 1, A_RB = 128, PROWS = 120, PLANE = PROWS * A_RB, A_LOADED = 81 * A_RB;
+    static constexpr int B_ROWS_LOADED = 81, NACC = 9, M = 64, TCOLS = 512;
+    static GORILA_DEV int shift(int a) { return (a / 3) * 9 + (a % 3); }
+    static GORILA_DEV uint32_t dtmem(int a) { return ((uint32_t)(16 * (a & 1)) << 16) + 64 * (a >> 1); }
+    static constexpr uint32_t ONES_TMEM = (16u << 16) + 256, ONES_LANE = 16;  // the free 10th M = 64 slot
+    static GORILA_DEV void load_a(const CUtensorMap* m, uint32_t dst, uint64_t* bar, int b) { tma_load(m, dst, bar, 0, 0, b); }
+    static GORILA_DEV void load_b(const CUtensorMap* m, uint32_t dst, uint64_t* bar, int b) { tma_load(m, dst, bar, 0, 0, 0, b); }
+};
+struct WgConv2 {
+    static constexpr int NPLANE = 4, A_RB = 64, PROWS = 112, PLANE = PROWS * A_RB, A_LOADED = 4 * 100 * A_RB;
+    static constexpr int B_ROWS_LOADED = 90, NACC = 4, M = 128, TCOLS = 512;
+    static GORILA_DEV int shift(int a) { return (a >> 1) * 10 + (a & 1); }
+    static GORILA_DEV uint32_t dtmem(int a) { return 64 * a; }
+    static constexpr uint32_t ONES_TMEM = 256, ONES_LANE = 0;  // an M = 64 accumulator after the four M = 128
+    static GORILA_DEV void load_a(const CUtensorMap* m, uint32_t dst, uint64_t* bar, int b) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) tma_load(m, dst + q * PLANE, bar, 0, q & 1, q >> 1, b);
+    }
+    static GORILA_DEV void load_b(const CUtensorMap* m, uint32_t dst, uint64_t* bar, int b) { tma_load(m, dst, bar, 0, 0, 0, b); }
+};
+struct WgradShiftParams {
+    CUtensorMap a_map;  // conv3: (64, 81, B) box (64, 81, 1) SW128; conv2: sh_conv2_map (phase planes)
+    CUtensorMap g_map;  // conv3: (64, 7, 7, B) box (64, 9, 9, 1); conv2: (64, 9, 9, B) box (64, 10, 9, 1); SW128
+    float* part;        // [gridDim.x][64][K]
+    float* part_b;      // [gridDim.x][64]: the CTA's sum of g (the layer's bias gradient)
+    int batch;
+};
+namespace wgs {
+constexpr int KSTEPS = 6, B_BUF = KSTEPS * 16 * 128, NBUF = 4;  // 96 virtual rows of g
+template <class W>
+struct Cfg {
+    static constexpr int A_BUF = W::NPLANE * W::PLANE, STAGE = A_BUF + B_BUF;
+    static constexpr int SMEM = 1024 + NBUF * STAGE + ONES_BYTES + 128;
+};
+}  // namespace wgs
+
+template <class W>
+__global__ void __launch_bounds__(192) k_wgrad_shift(const __grid_constant__ WgradShiftParams p) {
+    using CF = wgs::Cfg<W>;
+    constexpr int NBUF = wgs::NBUF, STAGE = CF::STAGE, A_BUF = CF::A_BUF;
+    extern __shared__ __align__(1024) uint8_t smem_raw[];
+    uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+    uint8_t* ones = smem + NBUF * STAGE;
+    uint64_t* full = reinterpret_cast<uint64_t*>(ones + ONES_BYTES);
+    uint64_t* empty = full + NBUF;
+    uint64_t* done = empty + NBUF;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
+    const int nt = p.batch > (int)blockIdx.x ? (p.batch - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
+    if (warp == 0) tmem_alloc(tmem_slot, W::TCOLS);
+    fill_ones(ones, tid, 192);
+    for (int s = 0; s < NBUF; ++s) {  // rows the loads never write (read only against zero rows of g)
+        uint8_t* st = smem + s * STAGE;
+        for (int q = 0; q < W::NPLANE; ++q)
+            for (int o = W::A_LOADED / W::NPLANE + tid * 16; o < W::PLANE; o += 192 * 16)
+                *reinterpret_cast<uint4*>(st + q * W::PLANE + o) = make_uint4(0, 0, 0, 0);
+        for (int o = W::B_ROWS_LOADED * 128 + tid * 16; o < wgs::B_BUF; o += 192 * 16)
+            *reinterpret_cast<uint4*>(st + A_BUF + o) = make_uint4(0, 0, 0, 0);
+    }
+    fence_proxy_async_smem();
+    if (tid == 32) {
+        for (int i = 0; i < NBUF; ++i) {
+            mbar_init(&full[i], 1);
+            mbar_init(&empty[i], 1);
+        }
+        mbar_init(done, 1);
+        fence_mbar_init();
+    }
+    tc_fence_before();
+    __syncthreads();
+    tc_fence_after();
+    pdl_wait();
+    pdl_trigger();
+    const uint32_t tmem = *tmem_slot;
+    const uint32_t sbase = smem_u32(smem);
+    if (warp == 0) {
+        if (lane == 0) {  // per sample: the layer input and the output gradient
+            for (int tl = 0; tl < nt; ++tl) {
+                const int b = blockIdx.x + tl * gridDim.x, s = tl % NBUF;
+                if (tl >= NBUF) mbar_wait(&empty[s], ((tl / NBUF) - 1) & 1);
+                const uint32_t a0 = sbase + s * STAGE;
+                W::load_a(&p.a_map, a0, &full[s], b);
+                W::load_b(&p.g_map, a0 + A_BUF, &full[s], b);
+                mbar_expect_tx(&full[s], W::A_LOADED + W::B_ROWS_LOADED * 128);
+            }
+        }
+    } else if (warp == 1) {  // MMA issuer (warp-uniform)
+        constexpr uint32_t IDESC = umma_idesc_bf16(W::M, 64) | (1u << 15) | (1u << 16);
+        constexpr uint32_t IDESC1 = umma_idesc_bf16(64, 64) | (1u << 15) | (1u << 16);
+        const uint32_t tmem_u = uniform_u32(tmem), sbase_u = uniform_u32(sbase);
+        const uint64_t od = umma_desc_mn_sw(sbase_u + NBUF * STAGE, 0, 128);  // the ones block
+        for (int tl = 0; tl < nt; ++tl) {
+            const int s = tl % NBUF;
+            mbar_wait(&full[s], (tl / NBUF) & 1);
+            tc_fence_after();
+            const uint32_t a0 = sbase_u + s * STAGE, b0 = a0 + A_BUF;
+#pragma unroll 1
+            for (int kk = 0; kk < wgs::KSTEPS; ++kk) {
+                const uint64_t bd = umma_desc_mn_sw(b0 + kk * 16 * 128, 0, 128);
+                umma_bf16_w(tmem_u + W::ONES_TMEM, od, bd, IDESC1, (tl > 0 || kk > 0) ? 1u : 0u);  // sum of g
+#pragma unroll
+                for (int a = 0; a < W::NACC; ++a) {
+                    const uint64_t ad = umma_desc_mn_sw(a0 + (kk * 16 + W::shift(a)) * W::A_RB, W::PLANE, W::A_RB);
+                    umma_bf16_w(tmem_u + W::dtmem(a), ad, bd, IDESC, (tl > 0 || kk > 0) ? 1u : 0u);
+                }
+            }
+            umma_commit_w(&empty[s]);
+        }
+        umma_commit_w(done);
+    } else {  // epilogue warps 2..5: the CTA's partial dW [o][k]
+        const int quad = warp & 3;
+        if (nt > 0) {
+            mbar_wait(done, 0);
+            tc_fence_after();
+        }
+        constexpr int K = W::M == 64 ? 9 * 64 : 16 * 32;
+        float* dst = p.part + (int64_t)blockIdx.x * (64 * K);
+        constexpr int NBLK = W::M == 64 ? (W::NACC + 1) / 2 : W::NACC;
+#pragma unroll 1
+        for (int j = 0; j < NBLK; ++j) {
+            int k;
+            bool ok = true;
+            if (W::M == 64) {  // lanes 0-15: accumulator 2j, 16-31: 2j + 1; row 16 * quad + (lane & 15)
+                const int a = 2 * j + (lane >> 4);
+                ok = a < W::NACC;
+                k = a * 64 + 16 * quad + (lane & 15);
+            } else {  // accumulator j = (dy, dx); lane quarter = phase plane (py, px), lane = channel
+                const int dy = j >> 1, dx = j & 1, py = quad >> 1, px = quad & 1;
+                k = ((2 * dy + py) * 4 + 2 * dx + px) * 32 + lane;
+            }
+#pragma unroll 1
+            for (int c0 = 0; c0 < 64; c0 += 32) {
+                float v[32];
+                if (nt > 0) tmem_ld16x2(tmem + ((uint32_t)(quad * 32) << 16) + (uint32_t)(64 * j + c0), v);
+                else
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] = 0.f;
+                if (ok)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) dst[(c0 + e) * K + k] = v[e];
+            }
+        }
+        if (quad == 0)  // row 0 of the ones accumulator: the CTA's sum of g per output channel
+#pragma unroll 1
+            for (int c0 = 0; c0 < 64; c0 += 32) {
+                float v[32];
+                if (nt > 0) tmem_ld16x2(tmem + W::ONES_TMEM - ((W::ONES_TMEM >> 16) << 16) + (uint32_t)c0, v);
+                else
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) v[e] = 0.f;
+                if (lane == (int)W::ONES_LANE)
+#pragma unroll
+                    for (int e = 0; e < 32; ++e) p.part_b[blockIdx.x * 64 + c0 + e] = v[e];
+            }
+    }
+    tc_fence_before();
+    __syncthreads();
+    if (warp == 0) tmem_dealloc(tmem, W::TCOLS);
 }
 
 }  // namespace gorila
