@@ -223,6 +223,7 @@ struct gorila_ctx {
     uint32_t* mbits1 = nullptr;  // [B * 400] one word (32 channels) per a1 row
     uint32_t* mbits2 = nullptr;  // [B * 81][2]
     float* part_bias[3] = {};    // u8 path: b1..b3 partials [split_w[l]][C] from the weight-gradient GEMMs
+    SampleDesc* sdesc = nullptr; // u8 path: [B] the samples' ring frames (the sampler's output)
     // side stream for the weight-gradient GEMMs, which are off the dgrad critical path
     // (a fork / join of the round; a graph captures it as parallel branches)
     cudaStream_t side = nullptr;
@@ -819,13 +820,13 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         dim3 grid((FRAME_BYTES / 16 + 255) / 256, B);
         uint2 key = make_uint2((uint32_t)cfg.seed, (uint32_t)(cfg.seed >> 32));
         using ST = std::conditional_t<fp32v, T, uint8_t>;  // (bf16: u8 staging when ctx->u8)
-        if (!fp32v && ctx->u8)
-            launch(ctx, k_sample<ST>, grid, dim3(256), 0, (const uint8_t*)Lr.frames, (const uint8_t*)Lr.a,
+        if (!fp32v && ctx->u8)  // the samples' frame addresses only (one block per sample)
+            launch(ctx, k_sample<ST>, dim3(1, B), dim3(256), 0, (const uint8_t*)Lr.frames, (const uint8_t*)Lr.a,
                    (const float*)Lr.r, (const uint8_t*)Lr.d, (int64_t)cfg.replay_capacity, (const uint64_t*)Lr.n_dev,
                    (const ShardPtrs*)(ctx->replay_global ? ctx->shard_tab : nullptr), ctx->n_shards,
                    (const uint64_t*)(ctx->replay_global && ctx->W > 1 && !replay_barrier_off() ? ctx->n_snap : nullptr),
                    ctx->sshard, key,
-                   (uint32_t)(cfg.learner_id_base + j), (const uint64_t*)ctx->dev_round, B, (ST*)ctx->s, (ST*)ctx->s2,
+                   (uint32_t)(cfg.learner_id_base + j), (const uint64_t*)ctx->dev_round, B, (ST*)ctx->sdesc, (ST*)nullptr,
                    ctx->sa, ctx->sr, ctx->sd, ctx->sidx, first_learner ? ctx->n_acc_local : (uint32_t*)nullptr);
         else
         launch(ctx, k_sample<T>, grid, dim3(256), 0, (const uint8_t*)Lr.frames, (const uint8_t*)Lr.a,
@@ -885,7 +886,8 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             using OA = ShConv1FwdU8; using OB = ShWeightK<32, 32, 16, 2>; using EP = EpAct<T>;
             ShiftProb<OA, OB, EP> pr[2];
             for (int z = 0; z < 2; ++z) {
-                pr[z].a.src = (const uint8_t*)(z ? ctx->s2 : ctx->s);
+                pr[z].a.desc = ctx->sdesc;
+                pr[z].a.z = z;
                 pr[z].a.batch = B;
                 pr[z].b = sh_wk<32, 32, 16, 2>(ctx, z ? (const void*)(tt + RT.w1) : (const void*)(rt + RL.w1), K1);
                 pr[z].ep = {z ? t1 : a1, C1_OUT, z ? tf + RT.b1 : rf + RL.b1, in_scale, M, C1_OUT, 1};
@@ -1384,7 +1386,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                 const uint32_t box[4] = {32, 21, 20, 1};
                 wp.g1_map = tmap(ctx, g1, 4, dims, str, box, nullptr, 64);
             }
-            wp.s8 = (const uint8_t*)ctx->s;
+            wp.desc = ctx->sdesc;
             wp.part = ctx->part_w[0];
             wp.part_b = ctx->part_bias[0];
             wp.scale = in_scale;
@@ -1625,6 +1627,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     void* g4 = c.take<uint8_t>(Bs * A4 * esz);
     uint32_t* mbits1 = c.take<uint32_t>(u8_staging(cfg) ? Bs * H1 * H1 : 0);
     uint32_t* mbits2 = c.take<uint32_t>(u8_staging(cfg) ? Bs * H2 * H2 * 2 : 0);
+    SampleDesc* sdesc = c.take<SampleDesc>(Bs);
     uint8_t* sa = c.take<uint8_t>(Bs);
     uint8_t* sd = c.take<uint8_t>(Bs);
     float* sr = c.take<float>(Bs);
@@ -1705,7 +1708,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         ctx->s = s; ctx->s2 = s2; ctx->a1 = a1; ctx->a2 = a2; ctx->a3 = a3; ctx->a4 = a4;
         ctx->t1 = t1; ctx->t2 = t2; ctx->t3 = t3; ctx->t4 = t4;
         ctx->g1 = g1; ctx->g2 = g2; ctx->g3 = g3; ctx->g4 = g4;
-        ctx->mbits1 = mbits1; ctx->mbits2 = mbits2;
+        ctx->mbits1 = mbits1; ctx->mbits2 = mbits2; ctx->sdesc = sdesc;
         ctx->sa = sa; ctx->sd = sd; ctx->sr = sr; ctx->sidx = sidx; ctx->dQ = dQ;
         ctx->sshard = sshard; ctx->shard_tab = shard_tab; ctx->rflags = rflags; ctx->replay_epoch = replay_epoch;
         ctx->n_snap = n_snap;
@@ -3120,7 +3123,7 @@ gorila_status gorila_act(gorila_ctx* ctx, const uint8_t* states, int32_t n, uint
     const int64_t total = (int64_t)n * (FRAME_BYTES / 4);
     const int grid = (int)std::min<int64_t>(148 * 8, (total + 255) / 256);
     if (fp32) launch(ctx, k_stage_states<float>, dim3(grid), dim3(256), 0, src, n, (float*)ctx->s);
-    else if (ctx->u8) launch(ctx, k_stage_states_u8, dim3(grid), dim3(256), 0, src, n, (uint8_t*)ctx->s);
+    else if (ctx->u8) launch(ctx, k_act_desc, dim3((ctx->B + 255) / 256), dim3(256), 0, src, n, ctx->B, ctx->sdesc);
     else launch(ctx, k_stage_states<__nv_bfloat16>, dim3(grid), dim3(256), 0, src, n, (__nv_bfloat16*)ctx->s);
     // the forward phases of a learner step on the latest replica (slot of round dev_round_expect)
     const uint32_t fwd = (1u << PH_CONV1F) | (1u << PH_CONV2F) | (1u << PH_CONV3F) | (1u << PH_FC4F);
@@ -3162,9 +3165,11 @@ gorila_status gorila_get_activation(gorila_ctx* ctx, int32_t which, void* host, 
     }
     if (bytes != n) return fail(GORILA_E_SHAPE, "bytes must be " + std::to_string(n));
     CU(cudaStreamSynchronize(ctx->stream));
-    if (which == 0 && ctx->u8) {  // u8 row-phase-major staging -> bf16 NHWC (the values are integers)
+    if (which == 0 && ctx->u8) {  // u8 path: gathered from the ring (row-phase-major u8), as bf16 NHWC
+        k_stage_from_desc<<<148 * 4, 256, 0, ctx->stream>>>(ctx->sdesc, (int)B, (uint8_t*)ctx->s);
+        CU(cudaStreamSynchronize(ctx->stream));
         std::vector<uint8_t> st((size_t)B * FRAME_BYTES * NSTACK);
-        CU(cudaMemcpy(st.data(), src, st.size(), cudaMemcpyDeviceToHost));
+        CU(cudaMemcpy(st.data(), ctx->s, st.size(), cudaMemcpyDeviceToHost));
         uint16_t* out = static_cast<uint16_t*>(host);
         for (uint64_t b = 0; b < B; ++b)
             for (int y = 0; y < IMG; ++y)

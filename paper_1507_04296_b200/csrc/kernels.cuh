@@ -18,6 +18,16 @@ struct ShardPtrs {
 };
 constexpr int MAX_SHARDS = 256;
 
+// u8 path (large batches): per sample, the addresses of the five ring frames tau-3 .. tau+1 and the
+// episode / eviction masks. conv1's forward and weight-gradient operands gather their input straight
+// from the replay ring through these (shift_gemm.cuh U8Planes): no stacked copy of s / s' is written.
+// s channel c = frame[c], s' channel c = frame[c + 1]; keep bit c (s) / 4 + c (s'): 0 = zero channel.
+struct SampleDesc {
+    const uint8_t* frame[5];
+    uint32_t keep;
+    uint32_t pad_;
+};
+
 
 // ------------------------------------------------------------------------- K1 sampler
 // Alg.1 P:121 "Sample random mini-batch from D"; "(s,a,r,s') ~ U(D)"; P:181 4-frame stack.
@@ -126,7 +136,7 @@ __global__ void __launch_bounds__(256) k_sample(const uint8_t* __restrict__ fram
 #pragma unroll
     for (int t = 0; t < 5; ++t) {
         int64_t st = tau - 3 + t;
-        f[t] = (st >= 0 && chunk < FRAME_BYTES / 16)
+        f[t] = (sizeof(T) != 1 && st >= 0 && chunk < FRAME_BYTES / 16)  // (u8 path: no frame reads here)
                    ? __ldcg(reinterpret_cast<const uint4*>(frames + (st % C) * FRAME_BYTES + chunk * 16))
                    : make_uint4(0, 0, 0, 0);
     }
@@ -156,29 +166,20 @@ __global__ void __launch_bounds__(256) k_sample(const uint8_t* __restrict__ fram
         }
     }
     if constexpr (sizeof(T) == 1) {
-        // u8 staging (large batches, shift_gemm.cuh U8Planes): row-phase-major [q][Y][X][px][c] =
-        // s[4Y+q][4X+px][c]; each thread's 16 pixels are four 4-pixel groups of one image row, each
-        // one 16-B output row (a 4 x 4 byte transpose of the four channels' words)
-        if (chunk < FRAME_BYTES / 16) {
+        // u8 path: the sample's frame addresses and masks only (conv1's operands gather the frames)
+        if (threadIdx.x == 0) {
+            SampleDesc ds;
 #pragma unroll
-            for (int half = 0; half < 2; ++half) {
-                uint8_t* dst = (half ? s2_out : s_out) + (int64_t)b * (FRAME_BYTES * NSTACK);
-#pragma unroll
-                for (int g = 0; g < 4; ++g) {
-                    uint32_t w[4];
-#pragma unroll
-                    for (int c = 0; c < 4; ++c) {
-                        const bool keep = half ? keep_s2[c] : keep_s[c];
-                        w[c] = keep ? reinterpret_cast<const uint32_t*>(&f[c + half])[g] : 0u;
-                    }
-                    const uint32_t lo01 = __byte_perm(w[0], w[1], 0x5140u), lo23 = __byte_perm(w[2], w[3], 0x5140u);
-                    const uint32_t hi01 = __byte_perm(w[0], w[1], 0x7362u), hi23 = __byte_perm(w[2], w[3], 0x7362u);
-                    const int px = chunk * 16 + 4 * g, y = px / IMG, X = (px - y * IMG) >> 2;
-                    reinterpret_cast<uint4*>(dst)[((y & 3) * 21 + (y >> 2)) * 21 + X] =
-                        make_uint4(__byte_perm(lo01, lo23, 0x5410u), __byte_perm(lo01, lo23, 0x7632u),
-                                   __byte_perm(hi01, hi23, 0x5410u), __byte_perm(hi01, hi23, 0x7632u));
-                }
+            for (int t = 0; t < 5; ++t) {
+                const int64_t st = tau - 3 + t;  // frames before the ring start are never kept
+                ds.frame[t] = frames + (st >= 0 ? st % C : 0) * FRAME_BYTES;
             }
+            uint32_t keep = 0;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) keep |= (keep_s[c] ? 1u : 0u) << c | (keep_s2[c] ? 1u : 0u) << (4 + c);
+            ds.keep = keep;
+            ds.pad_ = 0;
+            reinterpret_cast<SampleDesc*>(s_out)[b] = ds;
         }
     } else if constexpr (sizeof(T) == 2) {
         // bf16: each thread's 16 pixels x 4 channels = 8 uint4 per stack, staged in shared memory
@@ -797,22 +798,20 @@ __global__ void k_stage_states(const uint8_t* __restrict__ st, int n, T* __restr
             for (int c = 0; c < 4; ++c) dst[p * 4 + c] = fromf<T>((float)((c4[c] >> (8 * p)) & 0xffu));
     }
 }
-// the same states in the u8 row-phase-major staging of the large-batch conv1 (one thread per 4-pixel group)
-__global__ void k_stage_states_u8(const uint8_t* __restrict__ st, int n, uint8_t* __restrict__ s_out) {
+// the acting path's states (u8 [n][4][7056] in device memory) as sample descriptors of the u8 path:
+// state b's frames, every channel kept (samples n .. B-1 repeat the last state)
+__global__ void k_act_desc(const uint8_t* __restrict__ st, int n, int B, SampleDesc* __restrict__ desc) {
     pdl_wait();
     pdl_trigger();
-    const int64_t total = (int64_t)n * (FRAME_BYTES / 4);
-    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t b = i / (FRAME_BYTES / 4);
-        const int px = (int)(i - b * (FRAME_BYTES / 4)) * 4, y = px / IMG, X = (px - y * IMG) >> 2;
-        uint32_t w[4];
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b < B; b += gridDim.x * blockDim.x) {
+        const int64_t sb = b < n ? b : n - 1;
+        SampleDesc ds;
 #pragma unroll
-        for (int c = 0; c < 4; ++c) w[c] = *reinterpret_cast<const uint32_t*>(st + (b * 4 + c) * FRAME_BYTES + px);
-        const uint32_t lo01 = __byte_perm(w[0], w[1], 0x5140u), lo23 = __byte_perm(w[2], w[3], 0x5140u);
-        const uint32_t hi01 = __byte_perm(w[0], w[1], 0x7362u), hi23 = __byte_perm(w[2], w[3], 0x7362u);
-        reinterpret_cast<uint4*>(s_out + b * (FRAME_BYTES * NSTACK))[((y & 3) * 21 + (y >> 2)) * 21 + X] =
-            make_uint4(__byte_perm(lo01, lo23, 0x5410u), __byte_perm(lo01, lo23, 0x7632u),
-                       __byte_perm(hi01, hi23, 0x5410u), __byte_perm(hi01, hi23, 0x7632u));
+        for (int c = 0; c < 4; ++c) ds.frame[c] = st + (sb * 4 + c) * FRAME_BYTES;
+        ds.frame[4] = ds.frame[3];
+        ds.keep = 0xFFu;
+        ds.pad_ = 0;
+        desc[b] = ds;
     }
 }
 // Q = a4 . W5^T + b5 (fp32), then the epsilon-greedy decision (one block per state)

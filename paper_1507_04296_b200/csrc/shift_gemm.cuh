@@ -158,14 +158,15 @@ struct ShConv1Fwd {
     }
 };
 
-// ---------------------------------------------------------------- u8-staged input (large batches)
-// From B = 75 (the GEMM path) the sampler stages s / s' as u8 in row-phase-major order: per sample
-// [q][Y][X][px][c] = s[4Y+q][4X+px][c] (q < 4, Y, X < 21; one 16-B row per (q, Y, X); 28224 B, a
-// permutation of NHWC), half the bytes of bf16 NHWC and one contiguous run per sample. conv1's
-// operands expand it in shared memory: u8 row (q, r = Y*21 + X) -> 32 B of bf16 at row r of phase
-// plane q of the SWIZZLE_32B planes (16-B half h at byte (r*32 + 16h) with address bit 7 XORed into
-// bit 4), i.e. exactly the image the TMA boxes of ShConv1Fwd write from bf16 NHWC.
-constexpr int U8_ROWS = 4 * 441, U8_SAMPLE = U8_ROWS * 16;  // 28224 B per sample
+// ---------------------------------------------------------------- ring-gathered input (large batches)
+// From B = 75 (the GEMM path) conv1's operands read their input straight from the replay ring: the
+// sampler only records each sample's five frame addresses and masks (SampleDesc). A converter expands
+// a sample into the bf16 row-phase planes of ShConv1Fwd: row (q, r = Y*21 + X) of plane q holds
+// pixels s[4Y+q][4X .. 4X+3] x channels 0..3 (32 B), the same image the TMA boxes of ShConv1Fwd write
+// from a bf16 NHWC stack; the four channels are four frames (net z: frames z .. z+3), one 4-byte
+// load each, byte-transposed to pixel-major order. 16-B half h of a row sits at byte r*32 + 16h of
+// the plane with address bit 7 XORed into bit 4 (SWIZZLE_32B).
+constexpr int U8_ROWS = 4 * 441;  // plane rows per sample
 
 // bytes (2hi, 2hi + 1) of w as bf16x2: u8 -> fp32 exactly (magic 2^23), the upper halves exact
 GORILA_DEV uint32_t u8x2_bf16x2(uint32_t w, int hi) {
@@ -175,16 +176,25 @@ GORILA_DEV uint32_t u8x2_bf16x2(uint32_t w, int hi) {
 }
 
 // NT threads expand one sample: load() issues its global reads (into registers, so that the next
-// sample's loads are in flight while this one is stored), store() writes the bf16 planes.
+// sample's loads are in flight while this one is stored), store() transposes, converts and writes
 template <int NT>
 struct U8Planes {
     static constexpr int PER = (U8_ROWS + NT - 1) / NT;
-    uint4 v[PER];
-    GORILA_DEV void load(const uint8_t* __restrict__ sample, int t) {
+    uint32_t w[PER][4];  // per row: channel c's four pixels
+    GORILA_DEV void load(const SampleDesc* __restrict__ d, int z, int t) {
+        const uint8_t* fr[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c) fr[c] = d->frame[c + z];
+        const uint32_t keep = d->keep >> (4 * z);
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
             const int i = t + k * NT;
-            if (i < U8_ROWS) v[k] = __ldcg(reinterpret_cast<const uint4*>(sample) + i);
+            if (i >= U8_ROWS) continue;
+            const int q = i / 441, r = i - 441 * q, Y = r / 21, X = r - 21 * Y;
+            const int off = (4 * Y + q) * 84 + 4 * X;
+#pragma unroll
+            for (int c = 0; c < 4; ++c)
+                w[k][c] = (keep >> c) & 1u ? __ldcg(reinterpret_cast<const uint32_t*>(fr[c] + off)) : 0u;
         }
     }
     GORILA_DEV void store(uint32_t planes, uint32_t plane_bytes, int t) const {
@@ -194,29 +204,52 @@ struct U8Planes {
             if (i >= U8_ROWS) continue;
             const int q = i / 441, r = i - 441 * q;
             const uint32_t row = planes + q * plane_bytes + r * 32;
-            const uint32_t w[4] = {v[k].x, v[k].y, v[k].z, v[k].w};
+            // 4 x 4 byte transpose: word px = channels 0..3 of pixel px
+            const uint32_t lo01 = __byte_perm(w[k][0], w[k][1], 0x5140u), lo23 = __byte_perm(w[k][2], w[k][3], 0x5140u);
+            const uint32_t hi01 = __byte_perm(w[k][0], w[k][1], 0x7362u), hi23 = __byte_perm(w[k][2], w[k][3], 0x7362u);
+            const uint32_t px[4] = {__byte_perm(lo01, lo23, 0x5410u), __byte_perm(lo01, lo23, 0x7632u),
+                                    __byte_perm(hi01, hi23, 0x5410u), __byte_perm(hi01, hi23, 0x7632u)};
 #pragma unroll
             for (int h = 0; h < 2; ++h) {
                 const uint32_t a = row + 16 * h, pa = a ^ ((a >> 3) & 16u);
-                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(pa), "r"(u8x2_bf16x2(w[2 * h], 0)),
-                             "r"(u8x2_bf16x2(w[2 * h], 1)), "r"(u8x2_bf16x2(w[2 * h + 1], 0)),
-                             "r"(u8x2_bf16x2(w[2 * h + 1], 1))
+                asm volatile("st.shared.v4.b32 [%0], {%1, %2, %3, %4};" ::"r"(pa), "r"(u8x2_bf16x2(px[2 * h], 0)),
+                             "r"(u8x2_bf16x2(px[2 * h], 1)), "r"(u8x2_bf16x2(px[2 * h + 1], 0)),
+                             "r"(u8x2_bf16x2(px[2 * h + 1], 1))
                              : "memory");
             }
         }
     }
 };
 
-// conv1 forward from the u8 staging: ShConv1Fwd<1>'s planes, written by the engine's converter warps
+// diagnostics (gorila_get_activation "s" on the u8 path): sample b's s as row-phase-major u8
+// [q][Y][X][px][c] (4 x 441 rows of 16 B), through the same gather as the converters
+__global__ void k_stage_from_desc(const SampleDesc* __restrict__ desc, int B, uint8_t* __restrict__ out) {
+    const int64_t total = (int64_t)B * U8_ROWS;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = e / U8_ROWS;
+        const int i = (int)(e - b * U8_ROWS), q = i / 441, r = i - 441 * q, Y = r / 21, X = r - 21 * Y;
+        const SampleDesc& d = desc[b];
+        uint32_t w[4];
+#pragma unroll
+        for (int c = 0; c < 4; ++c)
+            w[c] = (d.keep >> c) & 1u ? *reinterpret_cast<const uint32_t*>(d.frame[c] + (4 * Y + q) * 84 + 4 * X) : 0u;
+        const uint32_t lo01 = __byte_perm(w[0], w[1], 0x5140u), lo23 = __byte_perm(w[2], w[3], 0x5140u);
+        const uint32_t hi01 = __byte_perm(w[0], w[1], 0x7362u), hi23 = __byte_perm(w[2], w[3], 0x7362u);
+        reinterpret_cast<uint4*>(out)[e] = make_uint4(__byte_perm(lo01, lo23, 0x5410u), __byte_perm(lo01, lo23, 0x7632u),
+                                                      __byte_perm(hi01, hi23, 0x5410u), __byte_perm(hi01, hi23, 0x7632u));
+    }
+}
+
+// conv1 forward from the ring gather: ShConv1Fwd<1>'s planes, written by the engine's converter warps
 struct ShConv1FwdU8 {
     static constexpr bool CONVERT = true;
     static constexpr int RB = 32, NCHUNK = 16, KSTEPS = 1, PROWS = 544, PLANE = PROWS * RB;
     static constexpr int BUF = 4 * PLANE, NPLANE = 4, WRITTEN = 441 * RB, MS = 1;
-    const uint8_t* src;  // [B][U8_SAMPLE]
+    const SampleDesc* desc;  // [B]
+    int z;                   // 0: s (frames 0..3), 1: s' (frames 1..4)
     int batch;
     __host__ __device__ int ntiles() const { return batch; }
     GORILA_DEV int mb0(int) const { return 0; }
-    GORILA_DEV const uint8_t* sample(int t) const { return src + (int64_t)t * U8_SAMPLE; }
     GORILA_DEV uint32_t addr(uint32_t base, int c, int mb) const {
         const int q = c >> 2, dy = (c >> 1) & 1, dx = c & 1;
         return base + q * PLANE + (mb * 128 + dy * 21 + dx) * RB;
@@ -311,7 +344,11 @@ struct ShiftCfg {
     static_assert(OB::NCH <= SHIFT_MAX_BCH, "weight chunks");
     static constexpr int BAR_BYTES = 8 * (2 * SHIFT_MAX_BCH + 2 * SHIFT_MAX_BUF + 4) + 16;
     static constexpr bool CONV = shift_convert<OA>::value;
-    static constexpr int THREADS = 192 + (CONV ? 32 * SHIFT_CONV_WARPS : 0);
+    // epilogue warp groups: two for the converting multi-block operand (conv1, MB = 4: each group
+    // drains half of a tile's M-blocks, so the accumulator is released twice as fast)
+    static constexpr int ES = (CONV && MB >= 2) ? 2 : 1;
+    static constexpr int EPI_END = 2 + 4 * ES;  // epilogue warps 2 .. EPI_END - 1, converters after
+    static constexpr int THREADS = 32 * EPI_END + (CONV ? 32 * SHIFT_CONV_WARPS : 0);
     // dynamic smem for nprob problems and nbuf A buffers
     static constexpr int smem(int nprob, int nbuf) {
         return 1024 + nprob * OB::NCH * OB::CHUNK + nbuf * OA::BUF + BAR_BYTES;
@@ -352,7 +389,7 @@ __global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
         }
         for (int i = 0; i < 2; ++i) {
             mbar_init(&acc_full[i], 1);
-            mbar_init(&acc_empty[i], 4);
+            mbar_init(&acc_empty[i], 4 * CFG::ES);
         }
         fence_mbar_init();
     }
@@ -428,17 +465,17 @@ __global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
                 if (lane == 0) GTRACE_T(4, tl);
             }
         }
-    } else if (CONV && warp >= 6) {  // converter warps: u8 staging -> the tile's bf16 planes
+    } else if (CONV && warp >= CFG::EPI_END) {  // converter warps: u8 staging -> the tile's bf16 planes
         if constexpr (CONV) {
             // two register sets in turn: a tile's global reads are issued one tile ahead of its
             // stores (a copy between the sets would wait on the loads in flight)
             constexpr int NT = 32 * SHIFT_CONV_WARPS;
-            const int ct = tid - 192;
+            const int ct = tid - 32 * CFG::EPI_END;
             U8Planes<NT> r0, r1;
             auto fetch = [&](int t, U8Planes<NT>& r) {
                 if (t < ntiles) {
                     const int pr = t / tiles_per;
-                    r.load(p.prob[pr].a.sample(t - pr * tiles_per), ct);
+                    r.load(p.prob[pr].a.desc + (t - pr * tiles_per), p.prob[pr].a.z, ct);
                 }
             };
             auto put = [&](int tl, const U8Planes<NT>& r) {
@@ -462,6 +499,7 @@ __global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
             }
         }
     } else if constexpr (ep_row_pre<EP>::value && BN <= 64) {
+        static_assert(CFG::ES == 1, "row-input epilogues run one warp group");
         // epilogue warps 2..5, per-row inputs (the ReLU masks of a data gradient): every M-block's
         // inputs of the NEXT tile are requested before this tile's accumulator is read, so their
         // latency hides under a whole tile (two register sets in turn)
@@ -525,7 +563,7 @@ __global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
     } else if constexpr (ep_col_pre<EP>::value && BN <= 64) {
         // epilogue warps 2..5, column-only inputs (the biases): loaded once per CTA (per problem);
         // the accumulator is read 32 columns per TMEM wait
-        const int quad = warp & 3;
+        const int quad = warp & 3, eh = (warp - 2) >> 2;  // lane quarter, epilogue group
         using PT = EpPre<EP>;
         constexpr int NC = BN / 16;
         typename PT::type pre[NC];
@@ -542,13 +580,13 @@ __global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
             }
             const uint32_t abuf = tl & 1;
             const int m0 = P.a.mb0(tile);
-            if (quad == 2 && lane == 0) GTRACE_T(5, tl);
+            if (quad == 2 && eh == 0 && lane == 0) GTRACE_T(5, tl);
             mbar_wait(&acc_full[abuf], (tl >> 1) & 1);
-            if (quad == 2 && lane == 0) GTRACE_T(6, tl);
+            if (quad == 2 && eh == 0 && lane == 0) GTRACE_T(6, tl);
             tc_fence_after();
             const uint32_t acc = tmem + abuf * CFG::ACC + ((uint32_t)(quad * 32) << 16);
 #pragma unroll 1
-            for (int mb = 0; mb < MB; ++mb) {
+            for (int mb = eh; mb < MB; mb += CFG::ES) {
                 const int i = P.a.row(tile, m0 + mb, quad * 32 + lane);
 #pragma unroll
                 for (int c2 = 0; c2 < NC; c2 += 2) {
@@ -574,9 +612,10 @@ __global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
             tc_fence_before();
             __syncwarp();
             if (lane == 0) mbar_arrive(&acc_empty[abuf]);
-            if (quad == 2 && lane == 0) GTRACE_T(7, tl);
+            if (quad == 2 && eh == 0 && lane == 0) GTRACE_T(7, tl);
         }
     } else {  // epilogue warps 2..5 (warp w reads TMEM lanes 32*(w%4) ..)
+        static_assert(CFG::ES == 1, "generic epilogue runs one warp group");
         const int quad = warp & 3;
         int tl = 0;
         for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
@@ -641,7 +680,7 @@ __global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
 // partial dW1 [o][k] (times the input scale) for the fixed-order reduction (k_wgrad_reduce).
 struct Conv1WgradU8 {
     CUtensorMap g1_map;  // (32, 20, 20, B) bf16, box (32, 21, 20, 1), SWIZZLE_64B
-    const uint8_t* s8;   // [B][U8_SAMPLE]
+    const SampleDesc* desc;  // [B]: the samples' ring frames (s = frames 0..3)
     float* part;         // [gridDim.x][32][256]
     float* part_b;       // [gridDim.x][32]: the CTA's sum of g1 (bias b1's gradient)
     float scale;
@@ -746,7 +785,7 @@ __global__ void __launch_bounds__(c1wg::THREADS) k_conv1_wgrad_u8(const __grid_c
         const int ct = tid - 64;
         U8Planes<NT> r0, r1;  // two register sets in turn (see gemm_shift's converter)
         auto fetch = [&](int tl, U8Planes<NT>& r) {
-            if (tl < nt) r.load(p.s8 + (int64_t)(blockIdx.x + tl * gridDim.x) * U8_SAMPLE, ct);
+            if (tl < nt) r.load(p.desc + (blockIdx.x + tl * gridDim.x), 0, ct);
         };
         auto put = [&](int tl, const U8Planes<NT>& r) {
             const int s = tl % NBUF;
