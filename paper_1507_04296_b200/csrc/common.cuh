@@ -167,9 +167,21 @@ __device__ unsigned long long gorila_trace_buf[64];
             gorila_trace_buf[(slot)] = t_;                                                       \
         }                                                                                         \
     } while (0)
-// per-tile events of CTA 0 of a persistent engine: gorila_trace_tiles[ev][tile] (tile < 64)
+// per-tile events of CTA 0 of a persistent engine: gorila_trace_tiles[ev][tile] (tile < 64);
+// -DGORILA_TRACE_CONV: instead every converter warp's hand-over time (GTRACE_C)
 __device__ unsigned long long gorila_trace_tiles[8 * 64];
-#define GTRACE_T(ev, tl)                                                                          \
+#ifdef GORILA_TRACE_CONV
+#define GTRACE_C(ev, tl) GTRACE_T_(ev, tl)
+#define GTRACE_T(ev, tl) \
+    do {                 \
+    } while (0)
+#else
+#define GTRACE_C(ev, tl) \
+    do {                 \
+    } while (0)
+#define GTRACE_T(ev, tl) GTRACE_T_(ev, tl)
+#endif
+#define GTRACE_T_(ev, tl)                                                                         \
     do {                                                                                          \
         if (blockIdx.x == 0 && (tl) < 64) {                                                       \
             unsigned long long t_;                                                               \
@@ -182,6 +194,9 @@ __device__ unsigned long long gorila_trace_tiles[8 * 64];
     do {             \
     } while (0)
 #define GTRACE_T(ev, tl) \
+    do {                 \
+    } while (0)
+#define GTRACE_C(ev, tl) \
     do {                 \
     } while (0)
 #endif

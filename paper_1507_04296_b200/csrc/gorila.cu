@@ -3118,6 +3118,9 @@ gorila_status gorila_act(gorila_ctx* ctx, const uint8_t* states, int32_t n, uint
         static_assert(NSTACK * FRAME_BYTES > 0, "");
         CU(cudaMemcpyAsync(ctx->s2, states, sbytes, cudaMemcpyHostToDevice, st));
         src = reinterpret_cast<const uint8_t*>(ctx->s2);
+    } else if (ctx->u8 && ((uintptr_t)states & 15u)) {  // the u8 path bulk-copies frames: 16-B aligned
+        CU(cudaMemcpyAsync(ctx->s2, states, sbytes, cudaMemcpyDeviceToDevice, st));
+        src = reinterpret_cast<const uint8_t*>(ctx->s2);
     }
     const bool fp32 = ctx->cfg.math == GORILA_MATH_FP32;
     const int64_t total = (int64_t)n * (FRAME_BYTES / 4);

@@ -197,6 +197,22 @@ struct U8Planes {
                 w[k][c] = (keep >> c) & 1u ? __ldcg(reinterpret_cast<const uint32_t*>(fr[c] + off)) : 0u;
         }
     }
+    // the same rows from the sample's four frames staged in shared memory (channel c at c * 7056)
+    GORILA_DEV void load_smem(uint32_t raw, uint32_t keep, int t) {
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = t + k * NT;
+            if (i >= U8_ROWS) continue;
+            const int q = i / 441, r = i - 441 * q, Y = r / 21, X = r - 21 * Y;
+            const uint32_t off = (4 * Y + q) * 84 + 4 * X;
+#pragma unroll
+            for (int c = 0; c < 4; ++c) {
+                uint32_t v = 0;
+                if ((keep >> c) & 1u) asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(raw + c * FRAME_BYTES + off));
+                w[k][c] = v;
+            }
+        }
+    }
     GORILA_DEV void store(uint32_t planes, uint32_t plane_bytes, int t) const {
 #pragma unroll
         for (int k = 0; k < PER; ++k) {
@@ -342,16 +358,28 @@ struct ShiftCfg {
     static constexpr uint32_t TCOLS = tmem_cols_for(2 * MB * BN);
     static_assert(2 * MB * BN <= 512, "TMEM columns");
     static_assert(OB::NCH <= SHIFT_MAX_BCH, "weight chunks");
-    static constexpr int BAR_BYTES = 8 * (2 * SHIFT_MAX_BCH + 2 * SHIFT_MAX_BUF + 4) + 16;
+    static constexpr int BAR_BYTES = 8 * (2 * SHIFT_MAX_BCH + 2 * SHIFT_MAX_BUF + 8) + 16;
     static constexpr bool CONV = shift_convert<OA>::value;
     // epilogue warp groups: two for the converting multi-block operand (conv1, MB = 4: each group
     // drains half of a tile's M-blocks, so the accumulator is released twice as fast)
     static constexpr int ES = (CONV && MB >= 2) ? 2 : 1;
     static constexpr int EPI_END = 2 + 4 * ES;  // epilogue warps 2 .. EPI_END - 1, converters after
-    static constexpr int THREADS = 32 * EPI_END + (CONV ? 32 * SHIFT_CONV_WARPS : 0);
+    // converter warps avoid the MMA warp's scheduler (warp w runs on sub-partition w % 4; warp 1
+    // issues the MMAs): with ES = 2 they are warps 10, 11, 12, 14, 15, 16, 18, 19 (13, 17 idle)
+    static constexpr int CONV_SPAN = CONV ? (ES == 2 ? 10 : SHIFT_CONV_WARPS) : 0;
+    static constexpr int THREADS = 32 * (EPI_END + CONV_SPAN);
+    static GORILA_DEV int conv_index(int w) {  // converter number 0..7 of warp w, or -1
+        const int o = w - EPI_END;
+        if (o < 0 || o >= CONV_SPAN) return -1;
+        if (ES != 2) return o;
+        if ((w & 3) == 1) return -1;
+        return o - (o > 3) - (o > 7);
+    }
+    // CONVERT: the tile's four ring frames, bulk-copied (cp.async.bulk) by the load warp
+    static constexpr int RAW = CONV ? 2 * 4 * FRAME_BYTES : 0;  // two tiles' frames
     // dynamic smem for nprob problems and nbuf A buffers
     static constexpr int smem(int nprob, int nbuf) {
-        return 1024 + nprob * OB::NCH * OB::CHUNK + nbuf * OA::BUF + BAR_BYTES;
+        return 1024 + nprob * OB::NCH * OB::CHUNK + nbuf * OA::BUF + RAW + BAR_BYTES;
     }
 };
 
@@ -365,13 +393,16 @@ __global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
     const int nprob = p.nprob, nbuf = p.nbuf;
     uint8_t* bsm = smem;                                   // [nprob][NCH][CHUNK]
     uint8_t* asm_ = smem + nprob * OB::NCH * OB::CHUNK;    // [nbuf][BUF]
-    uint64_t* bars = reinterpret_cast<uint64_t*>(asm_ + nbuf * OA::BUF);
+    uint8_t* raw = asm_ + nbuf * OA::BUF;                  // [RAW] (CONVERT)
+    uint64_t* bars = reinterpret_cast<uint64_t*>(raw + CFG::RAW);
     uint64_t* b_full = bars;                               // [2][SHIFT_MAX_BCH]
     uint64_t* a_full = b_full + 2 * SHIFT_MAX_BCH;         // [SHIFT_MAX_BUF]
     uint64_t* a_empty = a_full + SHIFT_MAX_BUF;
     uint64_t* acc_full = a_empty + SHIFT_MAX_BUF;          // [2]
     uint64_t* acc_empty = acc_full + 2;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(acc_empty + 2);
+    uint64_t* raw_full = acc_empty + 2;                    // [2] CONVERT: frames landed / read
+    uint64_t* raw_empty = raw_full + 2;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + 2);
 
     const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
     const int tiles_per = p.prob[0].a.ntiles(), ntiles = tiles_per * nprob;
@@ -390,6 +421,10 @@ __global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
         for (int i = 0; i < 2; ++i) {
             mbar_init(&acc_full[i], 1);
             mbar_init(&acc_empty[i], 4 * CFG::ES);
+        }
+        for (int i = 0; i < 2; ++i) {
+            mbar_init(&raw_full[i], 1);
+            mbar_init(&raw_empty[i], SHIFT_CONV_WARPS);
         }
         fence_mbar_init();
     }
@@ -422,6 +457,16 @@ __global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
                     if (tl >= nbuf) mbar_wait(&a_empty[buf], ((tl / nbuf) - 1) & 1);
                     const uint32_t bytes = p.prob[prob].a.load(tile, abase + buf * OA::BUF, &a_full[buf]);
                     mbar_expect_tx(&a_full[buf], bytes);
+                } else {  // the tile's four frames into the raw buffer once the converters have read it
+                    const int rs = tl & 1;
+                    if (tl >= 2) mbar_wait(&raw_empty[rs], ((tl >> 1) - 1) & 1);
+                    const SampleDesc* d = p.prob[prob].a.desc + tile;
+                    const int z = p.prob[prob].a.z;
+                    const uint32_t rb = smem_u32(raw) + rs * 4 * FRAME_BYTES;
+#pragma unroll
+                    for (int c = 0; c < 4; ++c)
+                        bulk_load(rb + c * FRAME_BYTES, d->frame[c + z], FRAME_BYTES, &raw_full[rs]);
+                    mbar_expect_tx(&raw_full[rs], 4 * FRAME_BYTES);
                 }
             }
         }
@@ -465,100 +510,34 @@ __global__ void __launch_bounds__(ShiftCfg<BN, MB, OA, OB>::THREADS)
                 if (lane == 0) GTRACE_T(4, tl);
             }
         }
-    } else if (CONV && warp >= CFG::EPI_END) {  // converter warps: u8 staging -> the tile's bf16 planes
+    } else if (CONV && warp >= CFG::EPI_END) {  // converter warps: ring frames -> the tile's bf16 planes
         if constexpr (CONV) {
-            // two register sets in turn: a tile's global reads are issued one tile ahead of its
-            // stores (a copy between the sets would wait on the loads in flight)
+            const int cw = CFG::conv_index(warp);
+            // per tile: read the landed frames (releasing the raw buffer for the next tile's copy),
+            // then transpose / convert into the tile's A buffer
             constexpr int NT = 32 * SHIFT_CONV_WARPS;
-            const int ct = tid - 32 * CFG::EPI_END;
-            U8Planes<NT> r0, r1;
-            auto fetch = [&](int t, U8Planes<NT>& r) {
-                if (t < ntiles) {
-                    const int pr = t / tiles_per;
-                    r.load(p.prob[pr].a.desc + (t - pr * tiles_per), p.prob[pr].a.z, ct);
-                }
-            };
-            auto put = [&](int tl, const U8Planes<NT>& r) {
-                const int buf = tl % nbuf;
+            const int ct = cw * 32 + lane;
+            const uint32_t rb = smem_u32(raw);
+            U8Planes<NT> r;
+            int tl = 0;
+            for (int t = cw < 0 ? ntiles : (int)blockIdx.x; t < ntiles; t += gridDim.x, ++tl) {
+                const int pr = t / tiles_per;
+                const uint32_t keep = p.prob[pr].a.desc[t - pr * tiles_per].keep >> (4 * p.prob[pr].a.z);
                 if (ct == 0) GTRACE_T(0, tl);
+                const int rs = tl & 1;
+                mbar_wait(&raw_full[rs], (tl >> 1) & 1);
+                r.load_smem(rb + rs * 4 * FRAME_BYTES, keep, ct);
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&raw_empty[rs]);
+                const int buf = tl % nbuf;
                 if (tl >= nbuf) mbar_wait(&a_empty[buf], ((tl / nbuf) - 1) & 1);
                 r.store(abase + buf * OA::BUF, OA::PLANE, ct);
                 fence_proxy_async_smem();
                 __syncwarp();
                 if (lane == 0) mbar_arrive(&a_full[buf]);
+                if (lane == 0) GTRACE_C(cw, tl);  // (every converter warp's hand-over)
                 if (ct == 0) GTRACE_T(1, tl);
-            };
-            const int G = gridDim.x;
-            fetch(blockIdx.x, r0);
-            for (int t = blockIdx.x, tl = 0; t < ntiles; t += 2 * G, tl += 2) {
-                fetch(t + G, r1);
-                put(tl, r0);
-                if (t + G >= ntiles) break;
-                fetch(t + 2 * G, r0);
-                put(tl + 1, r1);
             }
-        }
-    } else if constexpr (ep_row_pre<EP>::value && BN <= 64) {
-        static_assert(CFG::ES == 1, "row-input epilogues run one warp group");
-        // epilogue warps 2..5, per-row inputs (the ReLU masks of a data gradient): every M-block's
-        // inputs of the NEXT tile are requested before this tile's accumulator is read, so their
-        // latency hides under a whole tile (two register sets in turn)
-        const int quad = warp & 3;
-        using PT = EpPre<EP>;
-        using PreT = typename PT::type;
-        constexpr int NC = BN / 16;
-        PreT pa[MB][NC], pb[MB][NC];
-        const int G = gridDim.x;
-        auto fetch = [&](int t, PreT (&pp)[MB][NC]) {
-            if (t >= ntiles) return;
-            const int prob = t / tiles_per, tile = t - prob * tiles_per;
-            const ShiftProb<OA, OB, EP>& P = p.prob[prob];
-            const int m0 = P.a.mb0(tile);
-#pragma unroll
-            for (int mb = 0; mb < MB; ++mb) {
-                const int i = P.a.row(tile, m0 + mb, quad * 32 + lane);
-#pragma unroll
-                for (int c = 0; c < NC; ++c)
-                    if (i >= 0) pp[mb][c] = PT::load(P.ep, i, c * 16);
-            }
-        };
-        auto drain = [&](int t, int tl, const PreT (&pp)[MB][NC]) {
-            const int prob = t / tiles_per, tile = t - prob * tiles_per;
-            const ShiftProb<OA, OB, EP>& P = p.prob[prob];
-            const EP ep = P.ep;
-            const uint32_t abuf = tl & 1;
-            const int m0 = P.a.mb0(tile);
-            if (quad == 2 && lane == 0) GTRACE_T(5, tl);
-            mbar_wait(&acc_full[abuf], (tl >> 1) & 1);
-            if (quad == 2 && lane == 0) GTRACE_T(6, tl);
-            tc_fence_after();
-            const uint32_t acc = tmem + abuf * CFG::ACC + ((uint32_t)(quad * 32) << 16);
-#pragma unroll
-            for (int mb = 0; mb < MB; ++mb) {
-                const int i = P.a.row(tile, m0 + mb, quad * 32 + lane);
-#pragma unroll
-                for (int c2 = 0; c2 < NC; c2 += 2) {
-                    float v[32];
-                    if (c2 + 1 < NC) tmem_ld16x2(acc + (uint32_t)(mb * BN + c2 * 16), v);
-                    else tmem_ld16(acc + (uint32_t)(mb * BN + c2 * 16), v);
-#pragma unroll
-                    for (int h = 0; h < 2; ++h)
-                        if (c2 + h < NC && i >= 0 && (c2 + h) * 16 < p.N)
-                            PT::apply(ep, i, (c2 + h) * 16, v + 16 * h, pp[mb][c2 + h], 0);
-                }
-            }
-            tc_fence_before();
-            __syncwarp();
-            if (lane == 0) mbar_arrive(&acc_empty[abuf]);
-            if (quad == 2 && lane == 0) GTRACE_T(7, tl);
-        };
-        fetch(blockIdx.x, pa);
-        for (int t = blockIdx.x, tl = 0; t < ntiles; t += 2 * G, tl += 2) {
-            fetch(t + G, pb);
-            drain(t, tl, pa);
-            if (t + G >= ntiles) break;
-            fetch(t + 2 * G, pa);
-            drain(t + G, tl + 1, pb);
         }
     } else if constexpr (ep_col_pre<EP>::value && BN <= 64) {
         // epilogue warps 2..5, column-only inputs (the biases): loaded once per CTA (per problem);
