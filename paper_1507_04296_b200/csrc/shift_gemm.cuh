@@ -677,8 +677,11 @@ namespace c1wg {
 constexpr int KSTEPS = 27;                           // 432 virtual rows, 420 of them g1 rows (21 x 20)
 constexpr int PLANE = ShConv1FwdU8::PLANE;           // 544 rows of 32 B (rows <= 431 + 22 are read)
 constexpr int ABUF = 4 * PLANE, BBUF = KSTEPS * 16 * 64, STAGE = ABUF + BBUF;  // 69632 + 27648
-constexpr int NBUF = 2, CONV_WARPS = 8, THREADS = 64 + 32 * CONV_WARPS;     // warps 2.. convert
-constexpr int SMEM = 1024 + NBUF * STAGE + ONES_BYTES + 128;
+// converters: warps 2, 3, 4, 6, 7, 8, 10, 11 (off the MMA warp's sub-partition 1); epilogue 2..5
+constexpr int NBUF = 2, CONV_WARPS = 8, THREADS = 32 * 12;
+constexpr int RAW = 4 * FRAME_BYTES;  // the sample's four ring frames (cp.async.bulk)
+constexpr int SMEM = 1024 + NBUF * STAGE + ONES_BYTES + RAW + 128;
+GORILA_DEV int conv_index(int w) { return (w < 2 || w > 11 || (w & 3) == 1) ? -1 : w - 2 - (w > 5) - (w > 9); }
 constexpr uint32_t TCOLS = 128;  // 4 (dy, dx) accumulators in columns 0..63, the ones accumulator 64..95
 }  // namespace c1wg
 
@@ -687,12 +690,15 @@ __global__ void __launch_bounds__(c1wg::THREADS) k_conv1_wgrad_u8(const __grid_c
     extern __shared__ __align__(1024) uint8_t smem_raw[];
     uint8_t* smem = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
     uint8_t* ones = smem + NBUF * STAGE;
-    uint64_t* bars = reinterpret_cast<uint64_t*>(ones + ONES_BYTES);
+    uint8_t* raw = ones + ONES_BYTES;
+    uint64_t* bars = reinterpret_cast<uint64_t*>(raw + RAW);
     uint64_t* a_full = bars;               // [NBUF] converter warps
     uint64_t* b_full = a_full + NBUF;      // [NBUF] TMA of g1
     uint64_t* empty = b_full + NBUF;       // [NBUF] MMA commit
     uint64_t* done = empty + NBUF;
-    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+    uint64_t* raw_full = done + 1;         // the frames landed / read by the converters
+    uint64_t* raw_empty = raw_full + 1;
+    uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(raw_empty + 1);
     const int tid = threadIdx.x, warp = warp_uniform(), lane = tid & 31;
     const int nt = p.batch > (int)blockIdx.x ? (p.batch - 1 - (int)blockIdx.x) / (int)gridDim.x + 1 : 0;
     if (warp == 0) tmem_alloc(tmem_slot, TCOLS);
@@ -714,6 +720,8 @@ __global__ void __launch_bounds__(c1wg::THREADS) k_conv1_wgrad_u8(const __grid_c
             mbar_init(&empty[i], 1);
         }
         mbar_init(done, 1);
+        mbar_init(raw_full, 1);
+        mbar_init(raw_empty, CONV_WARPS);
         fence_mbar_init();
     }
     tc_fence_before();
@@ -724,9 +732,15 @@ __global__ void __launch_bounds__(c1wg::THREADS) k_conv1_wgrad_u8(const __grid_c
     const uint32_t tmem = *tmem_slot;
     const uint32_t sbase = smem_u32(smem);
     if (warp == 0) {
-        if (lane == 0) {  // g1 of each sample (420 rows of 64 B, x = 20 zero filled)
+        if (lane == 0) {  // per sample: its four frames (once the converters read the last ones), g1
+            const uint32_t rb = smem_u32(raw);
             for (int tl = 0; tl < nt; ++tl) {
                 const int b = blockIdx.x + tl * gridDim.x, s = tl % NBUF;
+                if (tl >= 1) mbar_wait(raw_empty, (tl - 1) & 1);
+                const SampleDesc* d = p.desc + b;
+#pragma unroll
+                for (int c = 0; c < 4; ++c) bulk_load(rb + c * FRAME_BYTES, d->frame[c], FRAME_BYTES, raw_full);
+                mbar_expect_tx(raw_full, 4 * FRAME_BYTES);
                 if (tl >= NBUF) mbar_wait(&empty[s], ((tl / NBUF) - 1) & 1);
                 tma_load(&p.g1_map, sbase + s * STAGE + ABUF, &b_full[s], 0, 0, 0, b);
                 mbar_expect_tx(&b_full[s], 420 * 64);
@@ -759,28 +773,23 @@ __global__ void __launch_bounds__(c1wg::THREADS) k_conv1_wgrad_u8(const __grid_c
             }
             umma_commit_w(done);
         }
-    } else {  // converter warps 2..9: the samples' u8 staging -> bf16 planes
+    } else {  // converter warps (conv_index >= 0): the samples' frames -> bf16 planes
         constexpr int NT = 32 * CONV_WARPS;
-        const int ct = tid - 64;
-        U8Planes<NT> r0, r1;  // two register sets in turn (see gemm_shift's converter)
-        auto fetch = [&](int tl, U8Planes<NT>& r) {
-            if (tl < nt) r.load(p.desc + (blockIdx.x + tl * gridDim.x), 0, ct);
-        };
-        auto put = [&](int tl, const U8Planes<NT>& r) {
+        const int cw = conv_index(warp), ct = cw * 32 + lane;
+        const uint32_t rb = smem_u32(raw);
+        U8Planes<NT> r;
+        for (int tl = 0; cw >= 0 && tl < nt; ++tl) {
+            const uint32_t keep = p.desc[blockIdx.x + tl * gridDim.x].keep;
+            mbar_wait(raw_full, tl & 1);
+            r.load_smem(rb, keep, ct);
+            __syncwarp();
+            if (lane == 0) mbar_arrive(raw_empty);
             const int s = tl % NBUF;
             if (tl >= NBUF) mbar_wait(&empty[s], ((tl / NBUF) - 1) & 1);
             r.store(sbase + s * STAGE, PLANE, ct);
             fence_proxy_async_smem();
             __syncwarp();
             if (lane == 0) mbar_arrive(&a_full[s]);
-        };
-        fetch(0, r0);
-        for (int tl = 0; tl < nt; tl += 2) {
-            fetch(tl + 1, r1);
-            put(tl, r0);
-            if (tl + 1 >= nt) break;
-            fetch(tl + 2, r0);
-            put(tl + 1, r1);
         }
         if (warp < 6) {  // epilogue (warps 2..5 = TMEM lane quarters 2, 3, 0, 1)
             const int quad = warp & 3;
