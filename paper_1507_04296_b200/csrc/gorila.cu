@@ -222,6 +222,7 @@ struct gorila_ctx {
     // conv2 / conv3 data gradients read (EpMaskBits) instead of the activations
     uint32_t* mbits1 = nullptr;  // [B * 400] one word (32 channels) per a1 row
     uint32_t* mbits2 = nullptr;  // [B * 81][2]
+    uint32_t* mbits3 = nullptr;  // [B * 49][2] = [B][98]: conv3 forward's decisions, read by fc4's data gradient
     float* part_bias[3] = {};    // u8 path: b1..b3 partials [split_w[l]][C] from the weight-gradient GEMMs
     SampleDesc* sdesc = nullptr; // u8 path: [B] the samples' ring frames (the sampler's output)
     // side stream for the weight-gradient GEMMs, which are off the dgrad critical path
@@ -979,6 +980,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                 pr[z].b = sh_wk<64, 128, 9, 0>(ctx, z ? (const void*)(tt + RT.w3) : (const void*)(rt + RL.w3), K3);
                 pr[z].ep = {z ? t3 : a3, C3_OUT, z ? tf + RT.b3 : rf + RL.b3, 1.f, M, C3_OUT, 1};
             }
+            if (ctx->u8) pr[0].ep.mask = ctx->mbits3;
             gemm_shift_launch<64, 1>(ctx, pr, 2, C3_OUT);
         } else {  // TMA: two samples (98 rows) per tile, one tap per K-chunk
             using OA = OpConvFwdS<Conv3, 1>; using OB = OpMatKS<64>; using EP = EpAct<T>;
@@ -1101,7 +1103,14 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         pr[0].ep = {g3, a3, FC4_IN, FC4_IN, B};                                                                \
         gemm_tma_launch<BN_, 1>(ctx, pr, 1, (FC4_IN + 127) / 128, (B + BN_ - 1) / BN_, FC4_OUT / 64, 1, 148, B); \
     }
-            if (B >= ctx->fc4_normal_min) {  // large batch: M = samples, N = 3136 (row-major masked stores)
+            if (B >= ctx->fc4_normal_min && ctx->u8 && (ctx->shift & 4)) {  // as below, decisions as bits
+                using OA = OpMatKS<128>; using OB = OpMatMNS<256>; using EP = EpMaskBits<T>;
+                TmaProb<OA, OB, EP> pr[1];
+                pr[0].a = op_matks<128>(ctx, g4, B, FC4_OUT, FC4_OUT);
+                pr[0].b = op_matmns<256>(ctx, rt + RL.w4, FC4_OUT, FC4_IN, FC4_IN);
+                pr[0].ep = {g3, ctx->mbits3, FC4_IN, B, FC4_IN, FC4_IN / 32};
+                gemm_tma_launch<256, 1>(ctx, pr, 1, (B + 127) / 128, (FC4_IN + 255) / 256, FC4_OUT / 64, 1, 0, FC4_IN);
+            } else if (B >= ctx->fc4_normal_min) {  // large batch: M = samples, N = 3136 (row-major masked stores)
                 using OA = OpMatKS<128>; using OB = OpMatMNS<256>; using EP = EpMask<T>;
                 TmaProb<OA, OB, EP> pr[1];
                 pr[0].a = op_matks<128>(ctx, g4, B, FC4_OUT, FC4_OUT);
@@ -1627,6 +1636,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
     void* g4 = c.take<uint8_t>(Bs * A4 * esz);
     uint32_t* mbits1 = c.take<uint32_t>(u8_staging(cfg) ? Bs * H1 * H1 : 0);
     uint32_t* mbits2 = c.take<uint32_t>(u8_staging(cfg) ? Bs * H2 * H2 * 2 : 0);
+    uint32_t* mbits3 = c.take<uint32_t>(u8_staging(cfg) ? Bs * H3 * H3 * 2 : 0);
     SampleDesc* sdesc = c.take<SampleDesc>(Bs);
     uint8_t* sa = c.take<uint8_t>(Bs);
     uint8_t* sd = c.take<uint8_t>(Bs);
@@ -1708,7 +1718,7 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
         ctx->s = s; ctx->s2 = s2; ctx->a1 = a1; ctx->a2 = a2; ctx->a3 = a3; ctx->a4 = a4;
         ctx->t1 = t1; ctx->t2 = t2; ctx->t3 = t3; ctx->t4 = t4;
         ctx->g1 = g1; ctx->g2 = g2; ctx->g3 = g3; ctx->g4 = g4;
-        ctx->mbits1 = mbits1; ctx->mbits2 = mbits2; ctx->sdesc = sdesc;
+        ctx->mbits1 = mbits1; ctx->mbits2 = mbits2; ctx->mbits3 = mbits3; ctx->sdesc = sdesc;
         ctx->sa = sa; ctx->sd = sd; ctx->sr = sr; ctx->sidx = sidx; ctx->dQ = dQ;
         ctx->sshard = sshard; ctx->shard_tab = shard_tab; ctx->rflags = rflags; ctx->replay_epoch = replay_epoch;
         ctx->n_snap = n_snap;

@@ -1,6 +1,6 @@
 """Per-kernel summary of an ncu --set full report (for profiles/): duration, SM / tensor-pipe
 activity, DRAM bytes, L2 throughput, achieved occupancy.
-usage: python tools/ncu_summary.py report.ncu-rep > profiles/<name>.txt"""
+usage: python tools/ncu_summary.py report.ncu-rep|raw.csv > profiles/<name>.txt"""
 import csv
 import io
 import subprocess
@@ -19,7 +19,10 @@ EXTRA = ",".join(TC + ["sm__pipe_tensor_subpipe_hmma_cycles_active.avg.pct_of_pe
 
 
 def main(rep):
-    out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
+    if rep.endswith(".csv"):  # an exported raw page (tools/ncu_deep.sh)
+        out = open(rep).read()
+    else:
+        out = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True, text=True).stdout
     rows = list(csv.reader(io.StringIO(out)))
     h, units = rows[0], rows[1]
     print(f"# {rep}: ncu --set full (--clock-control none), one line per profiled launch")
