@@ -283,7 +283,10 @@ template <class O, class = void>
 struct shift_convert : std::false_type {};
 template <class O>
 struct shift_convert<O, std::void_t<decltype(O::CONVERT)>> : std::integral_constant<bool, O::CONVERT> {};
-constexpr int SHIFT_CONV_WARPS = 8;  // converter warps of a CONVERT operand (warps 6 ..)
+#ifndef GORILA_CONV_WARPS
+#define GORILA_CONV_WARPS 8
+#endif
+constexpr int SHIFT_CONV_WARPS = GORILA_CONV_WARPS;  // converter warps of a CONVERT operand
 
 // ---------------------------------------------------------------- B operands (resident weights)
 // Interface: kMN, CHUNK (bytes per chunk, multiple of 1024), NCH (chunks incl. M-block variants),
@@ -366,14 +369,22 @@ struct ShiftCfg {
     static constexpr int EPI_END = 2 + 4 * ES;  // epilogue warps 2 .. EPI_END - 1, converters after
     // converter warps avoid the MMA warp's scheduler (warp w runs on sub-partition w % 4; warp 1
     // issues the MMAs): with ES = 2 they are warps 10, 11, 12, 14, 15, 16, 18, 19 (13, 17 idle)
-    static constexpr int CONV_SPAN = CONV ? (ES == 2 ? 10 : SHIFT_CONV_WARPS) : 0;
+    // (ES == 2: the converter warps skip sub-partition 1 -> SHIFT_CONV_WARPS / 3 * 4 warp slots)
+    static constexpr int conv_span() {
+        int w = EPI_END, k = 0;
+        while (k < SHIFT_CONV_WARPS) k += ((w++ & 3) != 1) ? 1 : 0;
+        return w - EPI_END;
+    }
+    static constexpr int CONV_SPAN = CONV ? (ES == 2 ? conv_span() : SHIFT_CONV_WARPS) : 0;
     static constexpr int THREADS = 32 * (EPI_END + CONV_SPAN);
-    static GORILA_DEV int conv_index(int w) {  // converter number 0..7 of warp w, or -1
+    static GORILA_DEV int conv_index(int w) {  // converter number 0..SHIFT_CONV_WARPS-1 of warp w, or -1
         const int o = w - EPI_END;
         if (o < 0 || o >= CONV_SPAN) return -1;
         if (ES != 2) return o;
         if ((w & 3) == 1) return -1;
-        return o - (o > 3) - (o > 7);
+        int k = 0;  // converters before warp w (warps on sub-partition 1 skipped)
+        for (int u = EPI_END; u < w; ++u) k += (u & 3) != 1;
+        return k < SHIFT_CONV_WARPS ? k : -1;
     }
     // CONVERT: the tile's four ring frames, bulk-copied (cp.async.bulk) by the load warp
     static constexpr int RAW = CONV ? 2 * 4 * FRAME_BYTES : 0;  // two tiles' frames
