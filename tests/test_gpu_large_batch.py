@@ -75,3 +75,26 @@ def test_large_batch_update_parity(B, math):
         floor = np.linalg.norm(ulp[sl]) / np.linalg.norm(d_ref[sl])
         assert e <= tol["dtheta"] + floor, ("dtheta", name, e, floor)
     g.close()
+
+
+@pytest.mark.parametrize("B", [130, 300])
+def test_ring_gather_descriptors_match_oracle_stacking(B):
+    """B >= 75 (bf16): no stacked s is written; conv1 gathers its input from the replay ring through the
+    sampler's per-sample descriptors (the five frame addresses and the episode / eviction keep bits,
+    P:121 O3, DESIGN R3). The stack those descriptors describe (gorila_get_activation("s") expands it
+    with the converters' gather) equals the oracle's O3 stacking bit for bit, on a wrapped ring with
+    dense episode ends."""
+    def dense_terms(j, d):
+        d = d.copy()
+        d[::5] = 1
+        return d
+
+    g, orc = make_pair(nA=6, B=B, C=500, n_insert=1337, math="bf16", terminals=dense_terms)
+    ring = orc.learners[0].ring
+    for k in (0, 3):
+        g.round(np.array([0], np.int32), k)
+        s_gpu = g.get_activation("s")  # [B][84][84][4], bf16 widened (integers: exact)
+        tau = O.sample_indices(ring.n, ring.size, B, 1507, 0, k)
+        s = ring.gather(tau)[0]  # [B][4][84][84] u8
+        assert np.array_equal(s_gpu.transpose(0, 3, 1, 2), s.astype(np.float32)), k
+    g.close()
