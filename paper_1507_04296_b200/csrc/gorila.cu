@@ -1688,8 +1688,12 @@ uint64_t layout_bytes(const gorila_config* cfg, gorila_ctx* ctx, uint8_t* base) 
             const int want = std::max(1, std::min(lim, (148 + ta - 1) / ta));
             const int cps = (nch + want - 1) / want;
             split_w[l] = (nch + cps - 1) / cps;
-            // k_conv1_wgrad_u8 / k_wgrad_shift: one partial per CTA
-            if (u8_staging(cfg)) split_w[l] = std::min(148, B);
+            // k_conv1_wgrad_u8 / k_wgrad_shift: one partial per CTA. conv2 / conv3 (144 / 128 KB of
+            // partials per CTA) balance the kernel (samples per CTA x ~0.6-0.9 us) against the
+            // reduction's partial traffic: about sqrt(25 B) CTAs below B = 876
+            if (u8_staging(cfg))
+                split_w[l] = l == 0 ? std::min(148, B)
+                                    : std::min(148, std::max(1, (int)std::lround(std::sqrt(25.0 * B))));
         }
         part_w[l] = c.take<float>((int64_t)split_w[l] * wcount[l]);
     }
