@@ -37,6 +37,14 @@ def test_sharded_ps_two_ranks_one_gpu(math, mode):
     print(_run(2, dict(MATH=math, ROUNDS="4", BOOTSTRAP="ipc", CUDA_VISIBLE_DEVICES=_first_gpu(), **MODES[mode])))
 
 
+def test_large_batch_global_replay_two_ranks_one_gpu():
+    """B = 80 (the large-batch path: conv1 bulk-copies its frames straight from the replay rings) with
+    global replay (f4): half of the draws' frames live in the other rank's ring, read through the peer
+    mapping by the same bulk copies."""
+    print(_run(2, dict(MATH="bf16", ROUNDS="3", BOOTSTRAP="ipc", BATCH="80", REPLAY="global",
+                       CUDA_VISIBLE_DEVICES=_first_gpu())))
+
+
 @pytest.mark.parametrize("n", [4, 8])
 def test_sharded_ps_many_ranks_one_gpu(n):
     """W = 4 and the exchange's maximum W = 8 (MAX_W): eight shards, eight owners."""

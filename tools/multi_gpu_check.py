@@ -63,7 +63,7 @@ def main():
     rounds = int(os.environ.get("ROUNDS", "4"))
     replay = os.environ.get("REPLAY", "local")
     Ll = int(os.environ.get("L_LOCAL", "1"))
-    nA, B, C = 6, 16, 1200
+    nA, B, C = 6, int(os.environ.get("BATCH", "16")), 1200  # BATCH >= 75: the large-batch (ring-gather) path
     G_ = world * Ll
     fill = (lambda j: [1500, 700, 1000, 400][j % 4]) if replay == "global" else (lambda j: C)
     tol = TOL[math]
