@@ -536,7 +536,7 @@ bool cluster_env_on() {
 // persistent launch: grid = min(tiles, SMs x resident CTAs per SM)
 template <int BN, int MB, class OA, class OB, class EP>
 void gemm_tma_p_launch(gorila_ctx* ctx, const TmaProb<OA, OB, EP>* probs, int nprob, int tilesA, int tilesB,
-                       int nchunks, int splits, int N) {
+                       int nchunks, int splits, int N, int max_grid = 0) {
     using CFG = TmaPCfg<BN, MB, OA, OB>;
     static int occ = 0;
     if (!occ) {
@@ -558,7 +558,7 @@ void gemm_tma_p_launch(gorila_ctx* ctx, const TmaProb<OA, OB, EP>* probs, int np
     gb.cluster = 1;
     const int tiles = tilesA * tilesB * nprob * gb.splits;
     cudaLaunchConfig_t cfg{};
-    cfg.gridDim = dim3(std::min(tiles, ctx->num_sms * occ));
+    cfg.gridDim = dim3(std::min(std::min(tiles, ctx->num_sms * occ), max_grid > 0 ? max_grid : 1 << 30));
     cfg.blockDim = dim3(CFG::THREADS);
     cfg.dynamicSmemBytes = CFG::SMEM;
     cfg.stream = ctx->stream;
@@ -1195,7 +1195,18 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             pr[0].a = op_matmns<128>(ctx, a3, B, FC4_IN, FC4_IN);
             pr[0].b = op_matmns<64>(ctx, g4, B, FC4_OUT, FC4_OUT);
             pr[0].ep = {Gd + OFF_W4, FC4_IN, FC4_IN, FC4_OUT, accumulate};
-            gemm_tma_launch<64, 1>(ctx, pr, 1, (FC4_IN + 127) / 128, FC4_OUT / 64, (B + 63) / 64, 1, 0, FC4_OUT);
+            // small batches: this GEMM runs on the side stream beside the dgrad chain, so fewer,
+            // longer CTAs leave that chain its SMs (B = 32: 200 tiles on 80 CTAs measured 70.2-70.5
+            // vs 71.5 us per step on 148 x 2; GORILA_FC4WG_GRID overrides, 0 = uncapped)
+            static const int fc4wg_env = [] {
+                const char* e = getenv("GORILA_FC4WG_GRID");
+                return e ? atoi(e) : -1;
+            }();
+            const int fc4wg_grid = fc4wg_env >= 0 ? fc4wg_env : (2 * B <= ctx->num_sms ? 80 : 0);
+            if (fc4wg_grid > 0)
+                gemm_tma_p_launch<64, 1>(ctx, pr, 1, (FC4_IN + 127) / 128, FC4_OUT / 64, (B + 63) / 64, 1, FC4_OUT, fc4wg_grid);
+            else
+                gemm_tma_launch<64, 1>(ctx, pr, 1, (FC4_IN + 127) / 128, FC4_OUT / 64, (B + 63) / 64, 1, 0, FC4_OUT);
         }
     }
     }
