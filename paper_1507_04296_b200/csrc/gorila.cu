@@ -1196,13 +1196,13 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             pr[0].b = op_matmns<64>(ctx, g4, B, FC4_OUT, FC4_OUT);
             pr[0].ep = {Gd + OFF_W4, FC4_IN, FC4_IN, FC4_OUT, accumulate};
             // small batches: this GEMM runs on the side stream beside the dgrad chain, so fewer,
-            // longer CTAs leave that chain its SMs (B = 32: 200 tiles on 80 CTAs measured 70.2-70.5
-            // vs 71.5 us per step on 148 x 2; GORILA_FC4WG_GRID overrides, 0 = uncapped)
+            // longer CTAs leave that chain its SMs (B = 32, 200 tiles: 60 CTAs 69.6-69.7 us per step,
+            // 80: 70.2-70.5, 148 x 2: 71.5; 20 / 50: 71.9 / 72.1; GORILA_FC4WG_GRID overrides, 0 = uncapped)
             static const int fc4wg_env = [] {
                 const char* e = getenv("GORILA_FC4WG_GRID");
                 return e ? atoi(e) : -1;
             }();
-            const int fc4wg_grid = fc4wg_env >= 0 ? fc4wg_env : (2 * B <= ctx->num_sms ? 80 : 0);
+            const int fc4wg_grid = fc4wg_env >= 0 ? fc4wg_env : (2 * B <= ctx->num_sms ? 60 : 0);
             if (fc4wg_grid > 0)
                 gemm_tma_p_launch<64, 1>(ctx, pr, 1, (FC4_IN + 127) / 128, FC4_OUT / 64, (B + 63) / 64, 1, FC4_OUT, fc4wg_grid);
             else
