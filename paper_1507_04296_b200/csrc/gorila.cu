@@ -16,6 +16,7 @@
 #include <string>
 #include <type_traits>
 #include <atomic>
+#include <memory>
 #include <vector>
 
 #include <cudaTypedefs.h>
@@ -229,6 +230,7 @@ struct gorila_ctx {
     // (a fork / join of the round; a graph captures it as parallel branches)
     cudaStream_t side = nullptr;
     cudaEvent_t ev_fork[4] = {}, ev_join = nullptr;
+    cudaEvent_t ev_join2 = nullptr;  // side2 -> main (small batches: conv3 / conv2 weight gradients on side2)
     bool fork = true;
     // parity diagnostics (gorila_capture_activations): every learner's a1..a4 copied after its
     // forward, so that tests can read the ReLU decisions of each learner of a multi-learner step
@@ -1180,6 +1182,15 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     // reduction right after conv2's weight gradient (neither waits for g1), so both run under the
     // main stream's conv2 data gradient / conv1 weight gradient
     const bool early_side = fk && ctx->u8 && split_red;
+    // small batches, one GPU: the conv3 / conv2 weight gradients run on side2 as soon as g3 / g2
+    // exist (instead of queueing behind fc4's weight gradient on side), the bias partials on side
+    // after fc4's; no side reduction: one K10 on the main stream after both joins
+    // (GORILA_SIDE2=0: everything on side)
+    static const bool side2_env = [] {
+        const char* e = getenv("GORILA_SIDE2");
+        return !(e && atoi(e) == 0);
+    }();
+    const bool on2 = fk && !ctx->u8 && ctx->W == 1 && side2_env && ctx->side2 != nullptr;
     PHASE(PH_FC4WG) {
     // fc4 wgrad (i = k, j = n, red = b): G[W4][n][k] += sum_b a3[b][k] g4[b][n]
     {
@@ -1223,6 +1234,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                (const T*)g3, (const T*)g4, B, ctx->part_b, ctx->bias_chunks, 3);
     }
     if (fk) fork_side(ctx, 1);  // g3 ready (fc4 dgrad is on the main stream before this point)
+    if (on2) cudaStreamWaitEvent(ctx->side2, ctx->ev_fork[1], 0);
     PHASE(PH_CONV3DG) {
     // conv3 dgrad: g2 = mask(conv3^T(g3))
     {
@@ -1265,7 +1277,8 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     PHASE(PH_CONV3WG) {
     // conv3 wgrad (i = r, j = o, red = m): partial[s][o][r]
     {
-        OnSide on_side(ctx, fk);
+        OnSide on_side(ctx, fk && !on2);
+        std::unique_ptr<OnSide2> on_side2(on2 ? new OnSide2(ctx) : nullptr);
         const int Mred = B * H3 * H3;
         if constexpr (fp32v) {
             using LA = LdConvInMN<T, Conv3>; using LB = LdRowsMN<T>; using EP = EpStoreT;
@@ -1300,6 +1313,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }
     mark(ctx, PH_CONV3WG);
     if (fk) fork_side(ctx, 2);  // g2 ready
+    if (on2) cudaStreamWaitEvent(ctx->side2, ctx->ev_fork[2], 0);
     PHASE(PH_CONV2DG) {
     // conv2 dgrad: g1 = mask(conv2^T(g2))
     {
@@ -1354,7 +1368,8 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     PHASE(PH_CONV2WG) {
     // conv2 wgrad
     {
-        OnSide on_side(ctx, fk);
+        OnSide on_side(ctx, fk && !on2);
+        std::unique_ptr<OnSide2> on_side2(on2 ? new OnSide2(ctx) : nullptr);
         const int Mred = B * H2 * H2;
         if constexpr (fp32v) {
             using LA = LdConvInMN<T, Conv2>; using LB = LdRowsMN<T>; using EP = EpStoreT;
@@ -1436,18 +1451,22 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
            (const T*)g3, (const T*)g4, B, ctx->part_b, ctx->bias_chunks, l0);
     // forked round: the side stream reduces what it produced (conv2 / conv3 weights, the biases)
     // while the main stream finishes conv1's weight gradient
-    if (split_red && fk && (phases & (1u << PH_WGRED))) {
+    if (split_red && fk && (phases & (1u << PH_WGRED)) && !on2) {
         const WgradReduceParams q = pick({1, 2, 3, 4, 5, 6});
         launch(ctx, k_wgrad_reduce, dim3(red_grid(q)), dim3(256), 0, q, Gd);
     }
     }
     mark(ctx, PH_BIASG);
+    if (on2) {
+        cudaEventRecord(ctx->ev_join2, ctx->side2);
+        cudaStreamWaitEvent(ctx->stream, ctx->ev_join2, 0);
+    }
     if (fk) join_side(ctx);
     PHASE(PH_WGRED) {
     // K10: fixed-order reduction of the conv wgrad partials into G (the rest of it when forked)
     {
         // (u8 path: b1 comes from conv1's weight gradient on the main stream, so the main reduce takes it)
-        const WgradReduceParams q = (fk && split_red) ? (ctx->u8 ? pick({0, 3, 7}) : pick({0, 7})) : all;
+        const WgradReduceParams q = (fk && split_red && !on2) ? (ctx->u8 ? pick({0, 3, 7}) : pick({0, 7})) : all;
         launch(ctx, k_wgrad_reduce, dim3(red_grid(q)), dim3(256), 0, q, Gd);
     }
     }
@@ -2009,6 +2028,7 @@ gorila_status gorila_init(const gorila_config* cfg, gorila_ctx** out) {
     CU(cudaEventCreateWithFlags(&ctx->ev_s2_join, cudaEventDisableTiming));
     for (auto& e : ctx->ev_fork) CU(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
     CU(cudaEventCreateWithFlags(&ctx->ev_join, cudaEventDisableTiming));
+    CU(cudaEventCreateWithFlags(&ctx->ev_join2, cudaEventDisableTiming));
     for (auto& l : ctx->learners) {
         CU(cudaMemsetAsync(l.n_dev, 0, sizeof(uint64_t), st));
         CU(cudaMemsetAsync(l.stats, 0, sizeof(LearnerStats), st));
@@ -2063,6 +2083,7 @@ void gorila_destroy(gorila_ctx* ctx) {
     for (auto e : ctx->ev_fork)
         if (e) cudaEventDestroy(e);
     if (ctx->ev_join) cudaEventDestroy(ctx->ev_join);
+    if (ctx->ev_join2) cudaEventDestroy(ctx->ev_join2);
     if (ctx->side2) {
         cudaStreamSynchronize(ctx->side2);
         cudaStreamDestroy(ctx->side2);
