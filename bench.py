@@ -85,6 +85,7 @@ class ClockSampler:
     def __init__(self, gpu_index):
         self.idx = gpu_index
         self.rows = []  # (sm_mhz, max_mhz, reasons)
+        self.failures = 0  # NVML queries that raised
         self.src = None
         self.proc = None
         self.stop = None
@@ -92,17 +93,27 @@ class ClockSampler:
 
     def _nvml_loop(self, h, nv):
         import time as _t
-        mx = nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM)
+        try:
+            mx = float(nv.nvmlDeviceGetMaxClockInfo(h, nv.NVML_CLOCK_SM))
+        except Exception:
+            mx = float("nan")
         while not self.stop.is_set():
             try:
                 sm = nv.nvmlDeviceGetClockInfo(h, nv.NVML_CLOCK_SM)
+            except Exception:
+                self.failures += 1
+                _t.sleep(0.02)
+                continue
+            reasons = set()
+            try:  # a failed reasons query still records the clock (and is counted)
                 try:
                     r = nv.nvmlDeviceGetCurrentClocksEventReasons(h)
                 except AttributeError:
                     r = nv.nvmlDeviceGetCurrentClocksThrottleReasons(h)
-                self.rows.append((float(sm), float(mx), {k for k, bit in self.BITS.items() if r & bit}))
+                reasons = {k for k, bit in self.BITS.items() if r & bit}
             except Exception:
-                pass
+                self.failures += 1
+            self.rows.append((float(sm), mx, reasons))
             _t.sleep(0.02)
 
     def __enter__(self):
@@ -134,6 +145,18 @@ class ClockSampler:
         if self.stop is not None:
             self.stop.set()
             self.th.join()
+            if not self.rows:  # every NVML query failed: one nvidia-smi sample right after the loop
+                try:
+                    out = subprocess.run(["nvidia-smi", "-i", str(self.idx), "--query-gpu=" + self.Q,
+                                          "--format=csv,noheader,nounits"], capture_output=True, text=True,
+                                         timeout=20).stdout
+                    names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+                    for r in [r.split(",") for r in out.strip().splitlines() if r.strip()]:
+                        self.rows.append((float(r[1]), float(r[2]),
+                                          {names[i] for i in range(4) if len(r) > 5 + i and r[5 + i].strip() == "Active"}))
+                    self.src = "nvidia-smi (after the loop: NVML failed)"
+                except Exception:
+                    pass
         if self.proc:
             self.proc.terminate()
             self.proc.wait()
@@ -150,11 +173,14 @@ class ClockSampler:
     def summary(self):
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no clock samples"], "samples": 0,
-                    "src": self.src}
+                    "src": self.src, "query_failures": self.failures}
         sm = [r[0] for r in self.rows]
-        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in self.rows),
-                "reasons": sorted(set().union(*[r[2] for r in self.rows])), "samples": len(self.rows),
-                "src": self.src}
+        out = {"sm_mhz": float(np.median(sm)), "sm_max_mhz": max(r[1] for r in self.rows),
+               "reasons": sorted(set().union(*[r[2] for r in self.rows])), "samples": len(self.rows),
+               "src": self.src}
+        if self.failures:
+            out["query_failures"] = self.failures
+        return out
 
 
 def dist_env():

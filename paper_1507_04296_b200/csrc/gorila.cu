@@ -1190,7 +1190,8 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         const char* e = getenv("GORILA_SIDE2");
         return !(e && atoi(e) == 0);
     }();
-    const bool on2 = fk && !ctx->u8 && ctx->W == 1 && side2_env && ctx->side2 != nullptr;
+    // (not in asynchronous mode: side2 then hosts the persistent shard server)
+    const bool on2 = fk && !ctx->u8 && ctx->W == 1 && !ctx->async_mode && side2_env && ctx->side2 != nullptr;
     PHASE(PH_FC4WG) {
     // fc4 wgrad (i = k, j = n, red = b): G[W4][n][k] += sum_b a3[b][k] g4[b][n]
     {
