@@ -1400,6 +1400,11 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }
     }
     mark(ctx, PH_CONV2WG);
+    if (on2 && split_red && (phases & (1u << PH_WGRED))) {  // conv2 / conv3 weights, on side2 behind them
+        OnSide2 on_side2(ctx);
+        const WgradReduceParams q = pick({1, 2});
+        launch(ctx, k_wgrad_reduce, dim3(red_grid(q)), dim3(256), 0, q, Gd);
+    }
     if (early_side) {
         OnSide on_side(ctx, true);
         const WgradReduceParams q = pick({1, 2, 4, 5, 6});
@@ -1452,25 +1457,29 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
            (const T*)g3, (const T*)g4, B, ctx->part_b, ctx->bias_chunks, l0);
     // forked round: the side stream reduces what it produced (conv2 / conv3 weights, the biases)
     // while the main stream finishes conv1's weight gradient
-    if (split_red && fk && (phases & (1u << PH_WGRED)) && !on2) {
-        const WgradReduceParams q = pick({1, 2, 3, 4, 5, 6});
+    if (split_red && fk && (phases & (1u << PH_WGRED))) {
+        // on2: the side stream reduces only the biases (side2 reduced conv2 / conv3's weights)
+        const WgradReduceParams q = on2 ? pick({3, 4, 5, 6}) : pick({1, 2, 3, 4, 5, 6});
         launch(ctx, k_wgrad_reduce, dim3(red_grid(q)), dim3(256), 0, q, Gd);
     }
     }
     mark(ctx, PH_BIASG);
+    // on2: the main reduction (conv1's weight, fc5) runs before the joins, beside the other two
+    auto main_reduce = [&]() {
+        PHASE(PH_WGRED) {
+        // K10: fixed-order reduction of the conv wgrad partials into G (the rest of it when forked)
+        // (u8 path: b1 comes from conv1's weight gradient on the main stream, so the main reduce takes it)
+        const WgradReduceParams q = (fk && split_red) ? (ctx->u8 ? pick({0, 3, 7}) : pick({0, 7})) : all;
+        launch(ctx, k_wgrad_reduce, dim3(red_grid(q)), dim3(256), 0, q, Gd);
+        }
+    };
+    if (on2 && split_red) main_reduce();
     if (on2) {
         cudaEventRecord(ctx->ev_join2, ctx->side2);
         cudaStreamWaitEvent(ctx->stream, ctx->ev_join2, 0);
     }
     if (fk) join_side(ctx);
-    PHASE(PH_WGRED) {
-    // K10: fixed-order reduction of the conv wgrad partials into G (the rest of it when forked)
-    {
-        // (u8 path: b1 comes from conv1's weight gradient on the main stream, so the main reduce takes it)
-        const WgradReduceParams q = (fk && split_red && !on2) ? (ctx->u8 ? pick({0, 3, 7}) : pick({0, 7})) : all;
-        launch(ctx, k_wgrad_reduce, dim3(red_grid(q)), dim3(256), 0, q, Gd);
-    }
-    }
+    if (!(on2 && split_red)) main_reduce();
     mark(ctx, PH_WGRED);
     CU(cudaGetLastError());
     return GORILA_OK;
