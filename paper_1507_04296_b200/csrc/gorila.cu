@@ -648,7 +648,7 @@ ShWeightK<CO, RB, NCH, KOFF> sh_wk(gorila_ctx* ctx, const void* w, int ktot) {
 // grid + launch of the TMA engine (cluster split-K when cluster_target > 0)
 template <int BN, int MB, class OA, class OB, class EP>
 void gemm_tma_launch(gorila_ctx* ctx, const TmaProb<OA, OB, EP>* probs, int nprob, int tilesA, int tilesB,
-                     int nchunks, int splits, int cluster_target, int N) {
+                     int nchunks, int splits, int cluster_target, int N, int cl_cap = 0) {
     using CFG = TmaCfg<BN, MB, OA, OB>;
     static bool attr_set = false;
     if (!attr_set) {
@@ -668,7 +668,7 @@ void gemm_tma_launch(gorila_ctx* ctx, const TmaProb<OA, OB, EP>* probs, int npro
             const char* e = getenv("GORILA_CLUSTER_MAX");  // in-cluster split-K size cap (default 8)
             return e ? std::max(1, std::min(16, atoi(e))) : 8;
         }();
-        while (cl * 2 <= std::min(cl_max, std::min(want, nchunks))) cl *= 2;
+        while (cl * 2 <= std::min(cl_cap > 0 ? cl_cap : cl_max, std::min(want, nchunks))) cl *= 2;
     }
     if (persist_env && cl == 1 &&
         (int64_t)tilesA * tilesB * nprob * std::max(1, std::min(splits, nchunks)) > ctx->num_sms) {
@@ -1192,6 +1192,16 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     }();
     // (not in asynchronous mode: side2 then hosts the persistent shard server)
     const bool on2 = fk && !ctx->u8 && ctx->W == 1 && !ctx->async_mode && side2_env && ctx->side2 != nullptr;
+    // on2, first learner: conv1's weight gradient reduced in-cluster straight into G and fc5's
+    // partials reduced by the side stream, so no reduction kernel is left on the main path
+    static const bool c1d_env = [] {  // B = 32: 65.0 vs 65.3 us per step (GORILA_C1_DIRECT=0: off)
+        const char* e = getenv("GORILA_C1_DIRECT");
+        return !(e && atoi(e) == 0);
+    }();
+    // (aggregate mode only: the in-cluster order of the sum differs from K10's, and the per-message
+    // mode must stay bitwise equal to the asynchronous one, which does not fork)
+    const bool c1_direct = on2 && split_red && accumulate == 0 && !fp32v && !ctx->per_msg && c1d_env &&
+                           cluster_env_on();
     PHASE(PH_FC4WG) {
     // fc4 wgrad (i = k, j = n, red = b): G[W4][n][k] += sum_b a3[b][k] g4[b][n]
     {
@@ -1438,6 +1448,13 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
                 attr = true;
             }
             launch(ctx, k_conv1_wgrad_u8, dim3(ctx->split_w[0]), dim3(c1wg::THREADS), c1wg::SMEM, wp);
+        } else if (c1_direct) {  // the splits of a tile reduced in the cluster (DSMEM), stored into G
+            using OA = OpWgradIn1S; using OB = OpWgradOutS<32, 80, true>; using EP = EpStoreT;
+            TmaProb<OA, OB, EP> pr[1];
+            pr[0].a.map = conv1_map_sw(ctx, s, B, 1, 4);
+            pr[0].b = op_wgout_s<32, 80, true>(ctx, g1, H1 * H1, B);
+            pr[0].ep = {Gd + OFF_W1, K1, 0, in_scale, K1, C1_OUT};
+            gemm_tma_launch<32, 1>(ctx, pr, 1, K1 / 128, 1, B * 5, 1, 148, C1_OUT, 16);
         } else {  // TMA: K-chunk = 4 output rows (80 pixels) of one sample
             using OA = OpWgradIn1S; using OB = OpWgradOutS<32, 80, true>; using EP = EpStoreT;
             TmaProb<OA, OB, EP> pr[1];
@@ -1459,7 +1476,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     // while the main stream finishes conv1's weight gradient
     if (split_red && fk && (phases & (1u << PH_WGRED))) {
         // on2: the side stream reduces only the biases (side2 reduced conv2 / conv3's weights)
-        const WgradReduceParams q = on2 ? pick({3, 4, 5, 6}) : pick({1, 2, 3, 4, 5, 6});
+        const WgradReduceParams q = c1_direct ? pick({3, 4, 5, 6, 7}) : on2 ? pick({3, 4, 5, 6}) : pick({1, 2, 3, 4, 5, 6});
         launch(ctx, k_wgrad_reduce, dim3(red_grid(q)), dim3(256), 0, q, Gd);
     }
     }
@@ -1473,7 +1490,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         launch(ctx, k_wgrad_reduce, dim3(red_grid(q)), dim3(256), 0, q, Gd);
         }
     };
-    if (on2 && split_red) main_reduce();
+    if (on2 && split_red && !c1_direct) main_reduce();
     if (on2) {
         cudaEventRecord(ctx->ev_join2, ctx->side2);
         cudaStreamWaitEvent(ctx->stream, ctx->ev_join2, 0);
