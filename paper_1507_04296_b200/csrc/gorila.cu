@@ -1191,7 +1191,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         return !(e && atoi(e) == 0);
     }();
     // (not in asynchronous mode: side2 then hosts the persistent shard server)
-    const bool on2 = fk && !ctx->u8 && ctx->W == 1 && !ctx->async_mode && side2_env && ctx->side2 != nullptr;
+    // (several ranks: only without the opt-in early exchange, which also uses side2)
+    const bool on2 = fk && !ctx->u8 && (ctx->W == 1 || ctx->early_learner < 0) && !ctx->async_mode && side2_env &&
+                     ctx->side2 != nullptr;
     // on2, first learner: conv1's weight gradient reduced in-cluster straight into G and fc5's
     // partials reduced by the side stream, so no reduction kernel is left on the main path
     static const bool c1d_env = [] {  // B = 32: 65.0 vs 65.3 us per step (GORILA_C1_DIRECT=0: off)
