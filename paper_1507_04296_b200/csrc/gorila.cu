@@ -1064,10 +1064,15 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             const size_t smem = (size_t)(2 * nA * FC4_OUT + 64) * sizeof(float);
             static bool attr = false;
             if (!attr) {
-                cudaFuncSetAttribute(k_fc5_td_wide, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * 32 * FC4_OUT + 64) * 4);
+                cudaFuncSetAttribute(k_fc5_td_wide<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * 32 * FC4_OUT + 64) * 4);
+                cudaFuncSetAttribute(k_fc5_td_wide<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * 32 * FC4_OUT + 64) * 4);
                 attr = true;
             }
-            launch(ctx, k_fc5_td_wide, dim3(std::min((B + 31) / 32, 148)), dim3(256), smem, p);
+            // one sample per warp until the grid would exceed two blocks per SM, then two
+            const int S = B > 2 * ctx->num_sms * FC5W_WARPS ? 2 : 1;
+            const dim3 grid(std::min((B + FC5W_WARPS * S - 1) / (FC5W_WARPS * S), 2 * ctx->num_sms));
+            if (S == 1) launch(ctx, k_fc5_td_wide<1>, grid, dim3(FC5W_WARPS * 32), smem, p);
+            else launch(ctx, k_fc5_td_wide<2>, grid, dim3(FC5W_WARPS * 32), smem, p);
         } else {
             launch(ctx, k_fc5_td, dim3(fc5_fused ? B : std::min(B, 2 * 148)), dim3(512), 0, p);
         }

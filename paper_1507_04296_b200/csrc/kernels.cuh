@@ -504,12 +504,15 @@ __global__ void __launch_bounds__(512) k_fc5_td(Fc5TdParams p) {
     }
 }
 
-// Large batches (B >= 256): the same fc5 forward + TD + decisions with one warp per sample (both
+// Large batches (B >= 256): the same fc5 forward + TD + decisions with one warp per S samples (both
 // nets) instead of all warps on one sample at a time. W5 / W5t sit in shared memory (loaded before
-// the PDL wait: written two or more kernels back); a warp takes four samples at a time, so each W5
-// element read from shared memory feeds four FMAs. The last block sums the per-sample terms in
-// sample order and decides (td_decide), as k_fc5_td.
-__global__ void __launch_bounds__(256) k_fc5_td_wide(Fc5TdParams p) {
+// the PDL wait: written two or more kernels back); each W5 element read from shared memory feeds S
+// FMAs, and three actions' warp sums are in flight together (the shuffles' latency, not the FMAs,
+// bounds this kernel: 16 warps per block, S chosen so the grid fills the SMs). The last block sums
+// the per-sample terms in sample order and decides (td_decide), as k_fc5_td.
+constexpr int FC5W_WARPS = 16;
+template <int S>
+__global__ void __launch_bounds__(FC5W_WARPS * 32) k_fc5_td_wide(Fc5TdParams p) {
     const TdParams& t = p.td;
     const int nA = t.nA;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -528,33 +531,44 @@ __global__ void __launch_bounds__(256) k_fc5_td_wide(Fc5TdParams p) {
     mbar_wait(&wbar, 0);
     pdl_wait();
     pdl_trigger();
-    // four samples per warp at a time: every W5 element read from shared memory feeds four FMAs
-    constexpr int S = 4;
-    __shared__ float qs[8][2][S][32];  // [warp][net][sample][action]
-    for (int b0 = (blockIdx.x * 8 + warp) * S; b0 < t.B; b0 += gridDim.x * 8 * S) {
+    __shared__ float qs[FC5W_WARPS][2][S][32];  // [warp][net][sample][action]
+    for (int b0 = (blockIdx.x * FC5W_WARPS + warp) * S; b0 < t.B; b0 += gridDim.x * FC5W_WARPS * S) {
+        float xv[2][S][FC4_OUT / 32];
 #pragma unroll
-        for (int z = 0; z < 2; ++z) {
-            float xv[S][FC4_OUT / 32];
+        for (int z = 0; z < 2; ++z)
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 const float* x = (z ? p.t4 : p.a4) + (int64_t)min(b0 + s, t.B - 1) * FC4_OUT;
 #pragma unroll
-                for (int k = 0; k < FC4_OUT / 32; ++k) xv[s][k] = x[lane + 32 * k];
+                for (int k = 0; k < FC4_OUT / 32; ++k) xv[z][s][k] = x[lane + 32 * k];
             }
+#pragma unroll
+        for (int z = 0; z < 2; ++z) {
             const float* w = sw + z * nA * FC4_OUT;
-            for (int a = 0; a < nA; ++a) {
-                float acc[S] = {};
+            for (int a0 = 0; a0 < nA; a0 += 3) {
+                float acc[3][S] = {};
 #pragma unroll
-                for (int k = 0; k < FC4_OUT / 32; ++k) {
-                    const float wk = w[a * FC4_OUT + lane + 32 * k];
+                for (int u = 0; u < 3; ++u) {
+                    const int a = min(a0 + u, nA - 1);
 #pragma unroll
-                    for (int s = 0; s < S; ++s) acc[s] = fmaf(xv[s][k], wk, acc[s]);
+                    for (int k = 0; k < FC4_OUT / 32; ++k) {
+                        const float wk = w[a * FC4_OUT + lane + 32 * k];
+#pragma unroll
+                        for (int s = 0; s < S; ++s) acc[u][s] = fmaf(xv[z][s][k], wk, acc[u][s]);
+                    }
                 }
 #pragma unroll
-                for (int s = 0; s < S; ++s) {
-                    const float v = warp_sum(acc[s]);
-                    if (lane == 0) qs[warp][z][s][a] = v;
-                }
+                for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+                    for (int u = 0; u < 3; ++u)
+#pragma unroll
+                        for (int s = 0; s < S; ++s) acc[u][s] += __shfl_xor_sync(0xffffffffu, acc[u][s], o);
+                if (lane == 0)
+#pragma unroll
+                    for (int u = 0; u < 3; ++u)
+                        if (a0 + u < nA)
+#pragma unroll
+                            for (int s = 0; s < S; ++s) qs[warp][z][s][a0 + u] = acc[u][s];
             }
         }
         __syncwarp();
@@ -576,10 +590,8 @@ __global__ void __launch_bounds__(256) k_fc5_td_wide(Fc5TdParams p) {
                 const float cl = fminf(fmaxf(delta, -1.f), 1.f);  // reading R3
                 t.dQ[b * nA + lane] = (lane == ab) ? -cl / (float)t.B : 0.f;
             }
-            if (lane == 0) {
-                p.per_sample[2 * b] = delta * delta;
-                p.per_sample[2 * b + 1] = fabsf(delta);
-            }
+            if (lane == 0)
+                reinterpret_cast<float2*>(p.per_sample)[b] = make_float2(delta * delta, fabsf(delta));
         }
         __syncwarp();
     }
@@ -590,12 +602,22 @@ __global__ void __launch_bounds__(256) k_fc5_td_wide(Fc5TdParams p) {
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    __shared__ float s_sq[8], s_ab[8];
+    __shared__ float s_sq[FC5W_WARPS], s_ab[FC5W_WARPS];
     __shared__ int s_keep;
     float sq = 0.f, sa = 0.f;
-    for (int i = threadIdx.x; i < t.B; i += blockDim.x) {
-        sq += __ldcg(&p.per_sample[2 * i]);
-        sa += __ldcg(&p.per_sample[2 * i + 1]);
+    // thread i sums samples i, i + 512, ... in order; eight loads in flight at a time
+    for (int i0 = threadIdx.x; i0 < t.B; i0 += 8 * FC5W_WARPS * 32) {
+        float2 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const int i = i0 + u * FC5W_WARPS * 32;
+            v[u] = i < t.B ? __ldcg(reinterpret_cast<const float2*>(p.per_sample) + i) : make_float2(0.f, 0.f);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            sq += v[u].x;
+            sa += v[u].y;
+        }
     }
     sq = warp_sum(sq);
     sa = warp_sum(sa);
@@ -605,7 +627,7 @@ __global__ void __launch_bounds__(256) k_fc5_td_wide(Fc5TdParams p) {
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        s_keep = td_decide(t, s_sq, s_ab, 8);
+        s_keep = td_decide(t, s_sq, s_ab, FC5W_WARPS);
         *p.counter = 0;
     }
     __syncthreads();
@@ -642,7 +664,7 @@ __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, c
     // a4 (fc4's output) and W5 (the replica) were written two or more kernels back: loaded before
     // the wait (PDL: complete once this grid runs); only dQ comes from the kernel just before
     if ((int)blockIdx.x < 2 * n_chunks) {  // (chunk, column half)
-        __shared__ float dq[FC5_ROWS_MAX * 32];
+        __shared__ __align__(16) float dq[FC5_ROWS_MAX * 32];  // [row][32]: actions padded with zeros
         const int rows = fc5_rows(B), c = blockIdx.x >> 1, b0 = c * rows, nb = min(rows, B - b0);
         const int n = threadIdx.x + 256 * (blockIdx.x & 1);
         float xpre[8];
@@ -650,7 +672,8 @@ __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, c
         for (int u = 0; u < 8; ++u) xpre[u] = u < nb ? a4[(int64_t)(b0 + u) * FC4_OUT + n] : 0.f;
         pdl_wait();
         pdl_trigger();
-        for (int i = threadIdx.x; i < nb * nA; i += 256) dq[i] = dQ[(int64_t)b0 * nA + i];
+        for (int i = threadIdx.x; i < nb * 32; i += 256)
+            dq[i] = (i & 31) < nA ? dQ[(int64_t)(b0 + (i >> 5)) * nA + (i & 31)] : 0.f;
         __syncthreads();
         float acc[32];
 #pragma unroll
@@ -664,10 +687,16 @@ __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, c
 #pragma unroll
             for (int u = 0; u < 16; ++u) {
                 if (bb + u >= nb) break;
-                const float* q = dq + (bb + u) * nA;
+                const float4* q = reinterpret_cast<const float4*>(dq + (bb + u) * 32);
 #pragma unroll
-                for (int a = 0; a < 32; ++a)
-                    if (a < nA) acc[a] = fmaf(q[a], x[u], acc[a]);
+                for (int a = 0; a < 32; a += 4)
+                    if (a < nA) {  // one 16-B shared load feeds four FMAs
+                        const float4 qq = q[a / 4];
+                        acc[a] = fmaf(qq.x, x[u], acc[a]);
+                        acc[a + 1] = fmaf(qq.y, x[u], acc[a + 1]);
+                        acc[a + 2] = fmaf(qq.z, x[u], acc[a + 2]);
+                        acc[a + 3] = fmaf(qq.w, x[u], acc[a + 3]);
+                    }
             }
         }
         float* out = part + (int64_t)c * nA * (FC4_OUT + 1);
@@ -676,7 +705,7 @@ __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, c
             if (a < nA) out[a * FC4_OUT + n] = acc[a];
         if ((blockIdx.x & 1) == 0 && (int)threadIdx.x < nA) {
             float t = 0.f;
-            for (int b = 0; b < nb; ++b) t += dq[b * nA + threadIdx.x];
+            for (int b = 0; b < nb; ++b) t += dq[b * 32 + threadIdx.x];
             out[nA * FC4_OUT + threadIdx.x] = t;
         }
         return;
@@ -696,8 +725,12 @@ __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, c
         const float v[4] = {x.x > 0.f ? dq * w.x : 0.f, x.y > 0.f ? dq * w.y : 0.f, x.z > 0.f ? dq * w.z : 0.f,
                             x.w > 0.f ? dq * w.w : 0.f};
         T* dst = g4 + (int64_t)b * FC4_OUT + n;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) dst[c] = fromf<T>(v[c]);
+        if constexpr (sizeof(T) == 2) {  // one 8-B store
+            __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]), h1 = __floats2bfloat162_rn(v[2], v[3]);
+            *reinterpret_cast<uint2*>(dst) = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+        } else {
+            *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+        }
     }
 }
 
