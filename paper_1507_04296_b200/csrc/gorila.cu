@@ -1066,13 +1066,23 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
             if (!attr) {
                 cudaFuncSetAttribute(k_fc5_td_wide<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * 32 * FC4_OUT + 64) * 4);
                 cudaFuncSetAttribute(k_fc5_td_wide<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * 32 * FC4_OUT + 64) * 4);
+                cudaFuncSetAttribute(k_fc5_td_wide<4>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(2 * 32 * FC4_OUT + 64) * 4);
                 attr = true;
             }
-            // one sample per warp until the grid would exceed two blocks per SM, then two
-            const int S = B > 2 * ctx->num_sms * FC5W_WARPS ? 2 : 1;
-            const dim3 grid(std::min((B + FC5W_WARPS * S - 1) / (FC5W_WARPS * S), 2 * ctx->num_sms));
-            if (S == 1) launch(ctx, k_fc5_td_wide<1>, grid, dim3(FC5W_WARPS * 32), smem, p);
-            else launch(ctx, k_fc5_td_wide<2>, grid, dim3(FC5W_WARPS * 32), smem, p);
+            // S samples per warp, nw warps per block: every W5 element read from shared memory feeds S
+            // FMAs (shared-memory bandwidth) while nw warps hide the warp sums' latency
+            static const int env_s = [] { const char* e = getenv("GORILA_FC5W_S"); return e ? atoi(e) : 0; }();
+            static const int env_w = [] { const char* e = getenv("GORILA_FC5W_WARPS"); return e ? atoi(e) : 0; }();
+            const int per_sm = (B + ctx->num_sms - 1) / ctx->num_sms;
+            // measured (tools/fc5w_sweep.sh, phase us at B = 256 / 1024 / 4096): S = 2 with 4 warps
+            // 9.7 / 9.9 / 21.7, with 8 warps 10.8 / 11.1 / 19.4; S = 1 x 16 warps 14.2 / 14.5 / 23.7;
+            // S = 4 x 4 / 8 warps 14.2-16.8 / 20.6-21.9
+            const int S = env_s == 1 || env_s == 2 || env_s == 4 ? env_s : 2;
+            const int nw = env_w > 0 ? std::min(env_w, FC5W_WARPS) : per_sm >= 16 ? 8 : 4;
+            const dim3 grid(std::min((B + nw * S - 1) / (nw * S), 2 * ctx->num_sms));
+            if (S == 1) launch(ctx, k_fc5_td_wide<1>, grid, dim3(nw * 32), smem, p);
+            else if (S == 2) launch(ctx, k_fc5_td_wide<2>, grid, dim3(nw * 32), smem, p);
+            else launch(ctx, k_fc5_td_wide<4>, grid, dim3(nw * 32), smem, p);
         } else {
             launch(ctx, k_fc5_td, dim3(fc5_fused ? B : std::min(B, 2 * 148)), dim3(512), 0, p);
         }

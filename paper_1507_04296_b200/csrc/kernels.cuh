@@ -532,18 +532,17 @@ __global__ void __launch_bounds__(FC5W_WARPS * 32) k_fc5_td_wide(Fc5TdParams p) 
     pdl_wait();
     pdl_trigger();
     __shared__ float qs[FC5W_WARPS][2][S][32];  // [warp][net][sample][action]
-    for (int b0 = (blockIdx.x * FC5W_WARPS + warp) * S; b0 < t.B; b0 += gridDim.x * FC5W_WARPS * S) {
-        float xv[2][S][FC4_OUT / 32];
+    const int nw = blockDim.x >> 5;  // <= FC5W_WARPS
+    for (int b0 = (blockIdx.x * nw + warp) * S; b0 < t.B; b0 += gridDim.x * nw * S) {
 #pragma unroll
-        for (int z = 0; z < 2; ++z)
+        for (int z = 0; z < 2; ++z) {
+            float xv[S][FC4_OUT / 32];
 #pragma unroll
             for (int s = 0; s < S; ++s) {
                 const float* x = (z ? p.t4 : p.a4) + (int64_t)min(b0 + s, t.B - 1) * FC4_OUT;
 #pragma unroll
-                for (int k = 0; k < FC4_OUT / 32; ++k) xv[z][s][k] = x[lane + 32 * k];
+                for (int k = 0; k < FC4_OUT / 32; ++k) xv[s][k] = x[lane + 32 * k];
             }
-#pragma unroll
-        for (int z = 0; z < 2; ++z) {
             const float* w = sw + z * nA * FC4_OUT;
             for (int a0 = 0; a0 < nA; a0 += 3) {
                 float acc[3][S] = {};
@@ -554,7 +553,7 @@ __global__ void __launch_bounds__(FC5W_WARPS * 32) k_fc5_td_wide(Fc5TdParams p) 
                     for (int k = 0; k < FC4_OUT / 32; ++k) {
                         const float wk = w[a * FC4_OUT + lane + 32 * k];
 #pragma unroll
-                        for (int s = 0; s < S; ++s) acc[u][s] = fmaf(xv[z][s][k], wk, acc[u][s]);
+                        for (int s = 0; s < S; ++s) acc[u][s] = fmaf(xv[s][k], wk, acc[u][s]);
                     }
                 }
 #pragma unroll
@@ -605,12 +604,12 @@ __global__ void __launch_bounds__(FC5W_WARPS * 32) k_fc5_td_wide(Fc5TdParams p) 
     __shared__ float s_sq[FC5W_WARPS], s_ab[FC5W_WARPS];
     __shared__ int s_keep;
     float sq = 0.f, sa = 0.f;
-    // thread i sums samples i, i + 512, ... in order; eight loads in flight at a time
-    for (int i0 = threadIdx.x; i0 < t.B; i0 += 8 * FC5W_WARPS * 32) {
+    // thread i sums samples i, i + blockDim, ... in order; eight loads in flight at a time
+    for (int i0 = threadIdx.x; i0 < t.B; i0 += 8 * blockDim.x) {
         float2 v[8];
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const int i = i0 + u * FC5W_WARPS * 32;
+            const int i = i0 + u * blockDim.x;
             v[u] = i < t.B ? __ldcg(reinterpret_cast<const float2*>(p.per_sample) + i) : make_float2(0.f, 0.f);
         }
 #pragma unroll
@@ -627,7 +626,7 @@ __global__ void __launch_bounds__(FC5W_WARPS * 32) k_fc5_td_wide(Fc5TdParams p) 
     }
     __syncthreads();
     if (threadIdx.x == 0) {
-        s_keep = td_decide(t, s_sq, s_ab, FC5W_WARPS);
+        s_keep = td_decide(t, s_sq, s_ab, nw);
         *p.counter = 0;
     }
     __syncthreads();
