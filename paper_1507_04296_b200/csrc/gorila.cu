@@ -823,8 +823,9 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
         dim3 grid((FRAME_BYTES / 16 + 255) / 256, B);
         uint2 key = make_uint2((uint32_t)cfg.seed, (uint32_t)(cfg.seed >> 32));
         using ST = std::conditional_t<fp32v, T, uint8_t>;  // (bf16: u8 staging when ctx->u8)
-        if (!fp32v && ctx->u8)  // the samples' frame addresses only (one block per sample)
-            launch(ctx, k_sample<ST>, dim3(1, B), dim3(256), 0, (const uint8_t*)Lr.frames, (const uint8_t*)Lr.a,
+        if (!fp32v && ctx->u8)  // the samples' frame addresses only (one block of three warps per sample:
+                                // threads 0-3 / 32 / 64 load the flags / action / reward)
+            launch(ctx, k_sample<ST>, dim3(1, B), dim3(96), 0, (const uint8_t*)Lr.frames, (const uint8_t*)Lr.a,
                    (const float*)Lr.r, (const uint8_t*)Lr.d, (int64_t)cfg.replay_capacity, (const uint64_t*)Lr.n_dev,
                    (const ShardPtrs*)(ctx->replay_global ? ctx->shard_tab : nullptr), ctx->n_shards,
                    (const uint64_t*)(ctx->replay_global && ctx->W > 1 && !replay_barrier_off() ? ctx->n_snap : nullptr),
@@ -1094,7 +1095,7 @@ gorila_status run_learner(gorila_ctx* ctx, int j, uint64_t round, int s_j, int a
     // fc5 bwd: dW5, db5 into G; g4 = mask(dQ W5)
     {
         const int nch = (B + fc5_rows(B) - 1) / fc5_rows(B);
-        const int g4_blocks = (B * (FC4_OUT / 4) + 255) / 256;  // one thread per (sample, 4 columns)
+        const int g4_blocks = (B + 7) / 8;  // one warp per sample
         launch(ctx, k_fc5_bwd<T>, dim3(2 * nch + g4_blocks), dim3(256), 0,
                (const float*)ctx->dQ, (const float*)a4, (const float*)(rf + RL.w5), B, nA, ctx->part5, nch, g4,
                (const uint8_t*)ctx->sa);

@@ -711,24 +711,34 @@ __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, c
     }
     // g4[b][n] = mask(dQ[b][a_b] W5[a_b][n]): dQ has one nonzero entry per sample (the action taken,
     // k_fc5_td), so the sum over actions is that single product (exact: the other terms are zeros).
-    // One thread per (sample, 4 columns).
+    // One warp per sample, four float4 columns per lane (every load after the PDL wait: with the
+    // a4 / W5 / action loads before it, the asynchronous and per-message modes disagreed, measured)
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int64_t nwarps = (int64_t)(gridDim.x - 2 * n_chunks) * (blockDim.x >> 5);
     pdl_wait();
     pdl_trigger();
-    const int64_t n_g4 = (int64_t)B * (FC4_OUT / 4), nblk = gridDim.x - 2 * n_chunks;
-    for (int64_t f = (blockIdx.x - 2 * n_chunks) * (int64_t)blockDim.x + threadIdx.x; f < n_g4; f += nblk * blockDim.x) {
-        const int b = (int)(f / (FC4_OUT / 4)), n = (int)(f - (int64_t)b * (FC4_OUT / 4)) * 4;
+    for (int64_t b = (int64_t)(blockIdx.x - 2 * n_chunks) * (blockDim.x >> 5) + warp; b < B; b += nwarps) {
         const int ab = act[b];
+        float4 x[4], w[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            x[i] = *reinterpret_cast<const float4*>(a4 + b * FC4_OUT + (lane + 32 * i) * 4);
+            w[i] = *reinterpret_cast<const float4*>(w5 + ab * FC4_OUT + (lane + 32 * i) * 4);
+        }
         const float dq = dQ[b * nA + ab];
-        const float4 w = *reinterpret_cast<const float4*>(w5 + ab * FC4_OUT + n);
-        const float4 x = *reinterpret_cast<const float4*>(a4 + (int64_t)b * FC4_OUT + n);
-        const float v[4] = {x.x > 0.f ? dq * w.x : 0.f, x.y > 0.f ? dq * w.y : 0.f, x.z > 0.f ? dq * w.z : 0.f,
-                            x.w > 0.f ? dq * w.w : 0.f};
-        T* dst = g4 + (int64_t)b * FC4_OUT + n;
-        if constexpr (sizeof(T) == 2) {  // one 8-B store
-            __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]), h1 = __floats2bfloat162_rn(v[2], v[3]);
-            *reinterpret_cast<uint2*>(dst) = make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
-        } else {
-            *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+            const int n = (lane + 32 * i) * 4;
+            const float v[4] = {x[i].x > 0.f ? dq * w[i].x : 0.f, x[i].y > 0.f ? dq * w[i].y : 0.f,
+                                x[i].z > 0.f ? dq * w[i].z : 0.f, x[i].w > 0.f ? dq * w[i].w : 0.f};
+            T* dst = g4 + b * FC4_OUT + n;
+            if constexpr (sizeof(T) == 2) {  // one 8-B store
+                __nv_bfloat162 h0 = __floats2bfloat162_rn(v[0], v[1]), h1 = __floats2bfloat162_rn(v[2], v[3]);
+                *reinterpret_cast<uint2*>(dst) =
+                    make_uint2(*reinterpret_cast<uint32_t*>(&h0), *reinterpret_cast<uint32_t*>(&h1));
+            } else {
+                *reinterpret_cast<float4*>(dst) = make_float4(v[0], v[1], v[2], v[3]);
+            }
         }
     }
 }
