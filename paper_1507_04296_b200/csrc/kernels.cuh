@@ -412,13 +412,15 @@ __global__ void __launch_bounds__(512) k_fc5_td(Fc5TdParams p) {
     for (int u = 0; u < 4; ++u) {
         const int a = wz + 8 * u;
 #pragma unroll
-        for (int k = 0; k < FC4_OUT / 32; ++k) wv[u][k] = a < nA ? w5[a * FC4_OUT + lane + 32 * k] : 0.f;
+        for (int k = 0; k < FC4_OUT / 32; ++k) wv[u][k] = a < nA ? __ldcg(w5 + a * FC4_OUT + lane + 32 * k) : 0.f;
     }
     // W5 / b5 (the replica and theta^-) were written two or more kernels back: loaded before the
-    // wait for fc4's output (PDL: the preceding kernel has passed its own wait when this one starts)
+    // wait for fc4's output (PDL: the preceding kernel has passed its own wait when this one starts).
+    // Loads issued before the wait go through L2 (ld.global.cg): an SM's L1 may still hold lines of
+    // an older value of these addresses, and only the wait orders this grid after the flush
     float bv[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) bv[u] = wz + 8 * u < nA ? b5[wz + 8 * u] : 0.f;
+    for (int u = 0; u < 4; ++u) bv[u] = wz + 8 * u < nA ? __ldcg(b5 + wz + 8 * u) : 0.f;
     pdl_wait();
     pdl_trigger();
     int it = 0;
@@ -526,7 +528,8 @@ __global__ void __launch_bounds__(FC5W_WARPS * 32) k_fc5_td_wide(Fc5TdParams p) 
         bulk_load(smem_u32(sw + nA * FC4_OUT), p.w5t, nA * FC4_OUT * 4u, &wbar);
     }
     float* sb = sw + 2 * nA * FC4_OUT;
-    if (threadIdx.x < 64) sb[threadIdx.x] = (threadIdx.x & 31) < nA ? (threadIdx.x < 32 ? p.b5 : p.b5t)[threadIdx.x & 31] : 0.f;
+    if (threadIdx.x < 64)  // before the wait: through L2 (see k_fc5_td)
+        sb[threadIdx.x] = (threadIdx.x & 31) < nA ? __ldcg((threadIdx.x < 32 ? p.b5 : p.b5t) + (threadIdx.x & 31)) : 0.f;
     __syncthreads();
     mbar_wait(&wbar, 0);
     pdl_wait();
@@ -668,7 +671,7 @@ __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, c
         const int n = threadIdx.x + 256 * (blockIdx.x & 1);
         float xpre[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) xpre[u] = u < nb ? a4[(int64_t)(b0 + u) * FC4_OUT + n] : 0.f;
+        for (int u = 0; u < 8; ++u) xpre[u] = u < nb ? __ldcg(a4 + (int64_t)(b0 + u) * FC4_OUT + n) : 0.f;  // L2: see k_fc5_td
         pdl_wait();
         pdl_trigger();
         for (int i = threadIdx.x; i < nb * 32; i += 256)
@@ -711,20 +714,26 @@ __global__ void __launch_bounds__(256) k_fc5_bwd(const float* __restrict__ dQ, c
     }
     // g4[b][n] = mask(dQ[b][a_b] W5[a_b][n]): dQ has one nonzero entry per sample (the action taken,
     // k_fc5_td), so the sum over actions is that single product (exact: the other terms are zeros).
-    // One warp per sample, four float4 columns per lane (every load after the PDL wait: with the
-    // a4 / W5 / action loads before it, the asynchronous and per-message modes disagreed, measured)
+    // One warp per sample, four float4 columns per lane: its first sample's a4 row is requested
+    // through L2 before the PDL wait (with plain, L1-cached loads there the asynchronous and
+    // per-message modes disagreed, measured), everything else after it
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int64_t nwarps = (int64_t)(gridDim.x - 2 * n_chunks) * (blockDim.x >> 5);
+    const int64_t b_first = (int64_t)(blockIdx.x - 2 * n_chunks) * (blockDim.x >> 5) + warp;
+    float4 x[4];
+    if (b_first < B)
+#pragma unroll
+        for (int i = 0; i < 4; ++i) x[i] = __ldcg(reinterpret_cast<const float4*>(a4 + b_first * FC4_OUT + (lane + 32 * i) * 4));
     pdl_wait();
     pdl_trigger();
-    for (int64_t b = (int64_t)(blockIdx.x - 2 * n_chunks) * (blockDim.x >> 5) + warp; b < B; b += nwarps) {
+    for (int64_t b = b_first; b < B; b += nwarps) {
         const int ab = act[b];
-        float4 x[4], w[4];
+        float4 w[4];
+        if (b != b_first)
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-            x[i] = *reinterpret_cast<const float4*>(a4 + b * FC4_OUT + (lane + 32 * i) * 4);
-            w[i] = *reinterpret_cast<const float4*>(w5 + ab * FC4_OUT + (lane + 32 * i) * 4);
-        }
+            for (int i = 0; i < 4; ++i) x[i] = *reinterpret_cast<const float4*>(a4 + b * FC4_OUT + (lane + 32 * i) * 4);
+#pragma unroll
+        for (int i = 0; i < 4; ++i) w[i] = *reinterpret_cast<const float4*>(w5 + ab * FC4_OUT + (lane + 32 * i) * 4);
         const float dq = dQ[b * nA + ab];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
